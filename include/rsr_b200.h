@@ -1,0 +1,173 @@
+/*
+ * rsr_b200.h -- C ABI of the B200-native RSR hot path (librsr_b200.so).
+ *
+ * The reference (arxiv 2604.17066 artifact, Python package `rsr`) has no FFI:
+ * its seam is the Python API re-exported by pkg/src/rsr/__init__.py:5-35.
+ * Each entry point below replaces the numpy body of one reference function;
+ * the citation names the function it replaces (paths relative to
+ * pkg/src/rsr/).  The Python package paper_2604_17066_b200 binds these with
+ * ctypes (INTEGRATION.md shows the binding a maintainer of the reference
+ * would add).
+ *
+ * Conventions
+ *   - every function returns int status: RSR_OK (0), RSR_EINVAL (bad argument,
+ *     mapped to ValueError), RSR_ECUDA (CUDA error, RuntimeError),
+ *     RSR_EUNSUPPORTED (shape outside what the kernels handle, ValueError);
+ *     rsr_last_error() returns a thread-local message for the last failure;
+ *   - all array arguments are caller-owned DEVICE pointers (the library never
+ *     allocates or frees them) unless the name ends in _host;
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and never synchronises the device;
+ *   - states are uint8 (0 .. M-1), matrices are row-major.
+ *
+ * Thermometer layout (shared by samples "A" and reference rows "B"):
+ *   Kdim = N*(M-1) columns c = n*(M-1) + (k-1), k = 1..M-1, followed by
+ *   nb = ceil(Kdim/127) bias columns, zero-padded to Kpad = round_up(Kdim+nb, 32)
+ *   (rsr_thermo_kpad).  A[s,c] = [x_n < k], A[s,Kdim+j] = 1.
+ *   Upper ref r: B[r,c] = [r_n >= k], bias 0            -> A.B = #violations.
+ *   Lower ref r: B[r,c] = -[r_n < k], bias sums to
+ *                sum_c [r_n < k]                        -> A.B = c_r - overlap.
+ *   Pad ref rows: B[r,Kdim] = 1, else 0                 -> A.B = 1, never a hit.
+ *   In every case A.B >= 0 and A.B == 0  <=>  the sample is dominated by
+ *   (lower) / dominates (upper) the reference state.
+ */
+#ifndef RSR_B200_H
+#define RSR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSR_OK 0
+#define RSR_EINVAL 1
+#define RSR_ECUDA 2
+#define RSR_EUNSUPPORTED 3
+
+#define RSR_SIDE_LOWER 0
+#define RSR_SIDE_UPPER 1
+
+/* label codes written by rsr_finalize (device convention) */
+#define RSR_LABEL_LOWER 0
+#define RSR_LABEL_UPPER 1
+#define RSR_LABEL_UNCLASSIFIED 2
+
+/* flags bits written by the classifiers */
+#define RSR_HIT_LOWER 1
+#define RSR_HIT_UPPER 2
+
+/* Phi kinds (sysfn.py:87-185 plus builder-defined widest path) */
+#define RSR_PHI_ST_CONNECTIVITY 0  /* sysfn.py:87-98 single_od_connectivity   */
+#define RSR_PHI_WIDEST_PATH 1      /* max k: s-t connected on {x_e >= k}      */
+#define RSR_PHI_GLOBAL_CONNECTIVITY 2 /* sysfn.py:101-109                     */
+#define RSR_PHI_K_OUT_OF_N 3       /* sysfn.py:177-185                        */
+#define RSR_PHI_CONE_SUM 4         /* sum_l [x >= some anchor of level l]     */
+
+typedef struct rsr_phi_desc {
+  int32_t kind;
+  int32_t n_components;   /* N (== number of edges for graph kinds)            */
+  int32_t n_states;       /* M                                                 */
+  int32_t n_nodes;        /* graph kinds                                       */
+  int32_t source;         /* s (st / widest)                                   */
+  int32_t target;         /* t (st / widest)                                   */
+  int32_t k;              /* k_out_of_n                                        */
+  int32_t n_anchors;      /* cone sum                                          */
+  const int32_t* edge_u;  /* device [N]                                        */
+  const int32_t* edge_v;  /* device [N]                                        */
+  const uint8_t* anchors; /* device [n_anchors * N]                            */
+  const int32_t* anchor_level; /* device [n_anchors], 0-based level index      */
+} rsr_phi_desc;
+
+/* ---- library ---------------------------------------------------------- */
+int rsr_version(void);
+const char* rsr_last_error(void);
+int rsr_thermo_kpad(int n_components, int n_states);
+/* number of device SMs and the int8 tcgen05 path availability (sm_100) */
+int rsr_device_info(int* sm_count_host, int* cc_major_host, int* cc_minor_host);
+
+/* ---- (1) sampling: sampling.py:45-66 uniform_field, :69-90 sample_batch - */
+/* Philox4x64-10 raw words first..first+count-1 of stream key (seed, gen). */
+int rsr_philox_raw(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
+                   uint64_t* out, void* stream);
+int rsr_uniform_field(uint64_t seed, uint64_t gen, int64_t start, int64_t count,
+                      int n_components, double* out, void* stream);
+/* Inverse-CDF samples [start, start+count) of the (seed, gen) batch.
+ * probs: device f64 [N*M] (rows sum to 1).  out_states: u8 [count*N] or NULL.
+ * out_thermo: s8 [count*ld_thermo] thermometer rows (ld >= Kpad) or NULL. */
+int rsr_sample(const double* probs, int n_components, int n_states, uint64_t seed,
+               uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+               int8_t* out_thermo, int ld_thermo, void* stream);
+
+/* ---- (2) encodings: encoding.py:138-153 encode_batch ---------------------- */
+int rsr_encode_samples(const uint8_t* states, int64_t count, int n_components,
+                       int n_states, int8_t* out, int ld, void* stream);
+/* side: RSR_SIDE_LOWER / RSR_SIDE_UPPER; rows [0,count) from states, rows
+ * [count, rows_total) written as never-hit pad rows. */
+int rsr_encode_refs(const uint8_t* states, int64_t count, int64_t rows_total,
+                    int n_components, int n_states, int side, int8_t* out, int ld,
+                    void* stream);
+
+/* ---- (2) dominance classification: classify.py:99-148, 187-249 --------- */
+/* tcgen05 int8 tensor-core classifier.  A: s8 [S x ld_a] thermometer samples;
+ * B_lower / B_upper: s8 [rows x ld_b] thermometer refs (rows multiple of 128,
+ * pad rows never hit), n_lower / n_upper = rows actually holding refs.
+ * flags[s] (u8) = RSR_HIT_LOWER | RSR_HIT_UPPER bits, OR-ed into the existing
+ * value when accumulate != 0.  Kpad = ld_a = ld_b. */
+int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower,
+                    int64_t n_lower, const int8_t* B_upper, int64_t n_upper,
+                    int Kpad, uint8_t* flags, int accumulate, void* stream);
+/* Bit-packed CUDA-core comparison variant (AND + OR-reduce, LOP3).
+ * Packs states on the fly; optional first-match indices (explain / strict,
+ * classify.py:99-118): first_lower / first_upper int64 [S] or NULL. */
+int rsr_pack_thermo_bits(const uint8_t* states, int64_t count, int n_components,
+                         int n_states, int invert, uint32_t* out, int words,
+                         void* stream);
+int rsr_classify_bits(const uint32_t* sample_bits, int64_t S,
+                      const uint32_t* lower_bits, int64_t n_lower,
+                      const uint32_t* upper_bits, int64_t n_upper, int words,
+                      uint8_t* flags, int64_t* first_lower, int64_t* first_upper,
+                      int accumulate, void* stream);
+/* flags -> labels (lower precedence, classify.py:240-245) + counts
+ * counts_i64[4] = {lower, upper_only, unclassified, both}. */
+int rsr_finalize(const uint8_t* flags, int64_t S, uint8_t* labels,
+                 int64_t* counts, void* stream);
+/* order-preserving compaction of indices with labels[i] == label
+ * (np.flatnonzero, classify.py:242-245).  scratch: int64 [rsr_compact_scratch(S)]. */
+int64_t rsr_compact_scratch(int64_t S);
+int rsr_compact(const uint8_t* labels, int64_t S, int label, int64_t* out_idx,
+                int64_t* out_count, int64_t* scratch, void* stream);
+/* full H x R violation matrix, classify.py:57-96 (count = #components
+ * violated: x_n > r_n for lower, x_n < r_n for upper). */
+int rsr_violation_counts(const uint8_t* samples, int64_t H, const uint8_t* refs,
+                         int64_t R, int n_components, int side, int32_t* out,
+                         void* stream);
+
+/* ---- (3) batched Phi: model.py:88-97 -> sysfn.py:79-185 ------------------ */
+/* out[i] = Phi(states[idx[i]]) (idx NULL: rows 0..count-1). */
+int rsr_phi_eval(const rsr_phi_desc* phi, const uint8_t* states,
+                 const int64_t* idx, int64_t count, uint8_t* out, void* stream);
+
+/* ---- (4) batched boundary search + reference insertion ------------------ */
+/* boundary.py:116-147, one warp per start vector. out_side: RSR_SIDE_*;
+ * out_calls: Phi evaluations per search (== reference evaluation count). */
+int rsr_boundary_search(const rsr_phi_desc* phi, int threshold, const uint8_t* x0,
+                        int64_t B, uint8_t* out_refs, uint8_t* out_side,
+                        int64_t* out_calls, void* stream);
+/* gather rows: out[i] = states[idx[i]] (N bytes each) */
+int rsr_gather_rows(const uint8_t* states, int n_components, const int64_t* idx,
+                    int64_t count, uint8_t* out, void* stream);
+/* boundary.py:50-54 / 87-108 dominance scan of B candidates against K members:
+ * covered[c] = 1 if some member makes candidate c redundant,
+ * covers[c]  = 1 if candidate c makes some member redundant,
+ * member_mask (u8 [K], may be NULL): 1 where candidate `mask_candidate`
+ * makes the member redundant. */
+int rsr_dominance_scan(const uint8_t* cands, int64_t B, const uint8_t* members,
+                       int64_t K, int n_components, int side, uint8_t* covered,
+                       uint8_t* covers, int mask_candidate, uint8_t* member_mask,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSR_B200_H */

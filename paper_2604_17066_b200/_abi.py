@@ -1,0 +1,141 @@
+"""ctypes binding of ``librsr_b200.so`` (declared in ``include/rsr_b200.h``).
+
+The library is loaded lazily on the first device call so that the host-side
+API (models, distributions, reference-set bookkeeping) imports on machines
+without a GPU.  There is no CPU fallback: every hot-path call goes through
+this module and raises if the library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+__all__ = ["lib", "call", "stream_ptr", "ptr", "PhiDesc", "LIB_PATH", "require_device",
+           "SIDE_LOWER", "SIDE_UPPER", "HIT_LOWER", "HIT_UPPER", "LABEL_LOWER", "LABEL_UPPER",
+           "LABEL_UNCLASSIFIED", "PHI_ST", "PHI_WIDEST", "PHI_GLOBAL", "PHI_KOFN", "PHI_CONES",
+           "thermo_kpad", "thermo_words", "EXPORTED"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librsr_b200.so")
+
+RSR_OK, RSR_EINVAL, RSR_ECUDA, RSR_EUNSUPPORTED = 0, 1, 2, 3
+SIDE_LOWER, SIDE_UPPER = 0, 1
+HIT_LOWER, HIT_UPPER = 1, 2
+LABEL_LOWER, LABEL_UPPER, LABEL_UNCLASSIFIED = 0, 1, 2
+PHI_ST, PHI_WIDEST, PHI_GLOBAL, PHI_KOFN, PHI_CONES = 0, 1, 2, 3, 4
+
+
+class PhiDesc(ctypes.Structure):
+    """Mirror of ``rsr_phi_desc`` (include/rsr_b200.h)."""
+
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("n_components", ctypes.c_int32),
+        ("n_states", ctypes.c_int32),
+        ("n_nodes", ctypes.c_int32),
+        ("source", ctypes.c_int32),
+        ("target", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("n_anchors", ctypes.c_int32),
+        ("edge_u", ctypes.c_void_p),
+        ("edge_v", ctypes.c_void_p),
+        ("anchors", ctypes.c_void_p),
+        ("anchor_level", ctypes.c_void_p),
+    ]
+
+
+_P, _I, _I64, _U64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+
+# name -> (restype, argtypes); the full exported surface of include/rsr_b200.h
+EXPORTED = {
+    "rsr_version": (_I, []),
+    "rsr_last_error": (ctypes.c_char_p, []),
+    "rsr_thermo_kpad": (_I, [_I, _I]),
+    "rsr_device_info": (_I, [_P, _P, _P]),
+    "rsr_philox_raw": (_I, [_U64, _U64, _I64, _I64, _P, _P]),
+    "rsr_uniform_field": (_I, [_U64, _U64, _I64, _I64, _I, _P, _P]),
+    "rsr_sample": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
+    "rsr_encode_samples": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
+    "rsr_encode_refs": (_I, [_P, _I64, _I64, _I, _I, _I, _P, _I, _P]),
+    "rsr_classify_tc": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _I, _P]),
+    "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),
+    "rsr_classify_bits": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
+    "rsr_finalize": (_I, [_P, _I64, _P, _P, _P]),
+    "rsr_compact_scratch": (_I64, [_I64]),
+    "rsr_compact": (_I, [_P, _I64, _I, _P, _P, _P, _P]),
+    "rsr_violation_counts": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P]),
+    "rsr_phi_eval": (_I, [ctypes.POINTER(PhiDesc), _P, _P, _I64, _P, _P]),
+    "rsr_boundary_search": (_I, [ctypes.POINTER(PhiDesc), _I, _P, _I64, _P, _P, _P, _P]),
+    "rsr_gather_rows": (_I, [_P, _I, _P, _I64, _P, _P]),
+    "rsr_dominance_scan": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P, _I, _P, _P]),
+}
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load and type the shared library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                        "g.build()'` (no CPU fallback exists for the RSR device path)")
+                handle = ctypes.CDLL(LIB_PATH)
+                for name, (res, args) in EXPORTED.items():
+                    fn = getattr(handle, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = handle
+    return _lib
+
+
+def require_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the RSR hot path runs on CUDA devices only (no CPU fallback); "
+                           "torch.cuda.is_available() is False")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def call(name: str, *args) -> int:
+    """Invoke an entry point, mapping status codes to Python exceptions."""
+    L = lib()
+    rc = getattr(L, name)(*args)
+    if name in ("rsr_compact_scratch", "rsr_thermo_kpad", "rsr_version"):
+        return rc
+    if rc != RSR_OK:
+        msg = (L.rsr_last_error() or b"").decode(errors="replace")
+        if rc in (RSR_EINVAL, RSR_EUNSUPPORTED):
+            raise ValueError(f"{name}: {msg}")
+        raise RuntimeError(f"{name}: {msg}")
+    return rc
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device pointer expected")
+    return t.data_ptr()
+
+
+def thermo_kpad(n: int, m: int) -> int:
+    """Kpad of the thermometer layout (mirrors rsr_thermo_kpad; pure arithmetic)."""
+    kdim = n * (m - 1)
+    nb = (kdim + 126) // 127
+    return (kdim + nb + 31) // 32 * 32
+
+
+def thermo_words(n: int, m: int) -> int:
+    return (n * (m - 1) + 31) // 32

@@ -1,0 +1,404 @@
+// (2) Dominance classification on tcgen05 int8 tensor cores.
+//
+// Replaces classify.py:99-148 (_chunk_hits / _hits_for: popcount of
+// sample & ~ref over bit-packed rows, any-zero per sample) and the precedence
+// step classify.py:240-241.  The violation product is recast as a thermometer
+// contraction D = A . B^T (see include/rsr_b200.h): A = [x_n < k] samples,
+// B = refs with a bias column, D >= 0 and D == 0 <=> dominated.  The S x K
+// matrix D never leaves TMEM: the epilogue reduces each accumulator row to a
+// min and ORs a hit bit per side.
+//
+// Kernel shape (persistent, one CTA per SM):
+//   * a "group" is MT x 128 sample rows; its A tiles (MT x KB x 16 KB, K-major,
+//     128-byte swizzle) are loaded once by TMA and stay resident while every
+//     reference tile streams past;
+//   * reference tiles are 128 rows; each k-block (128 bytes of K) of a tile is
+//     one pipeline stage (16 KB), STAGES deep;
+//   * warp 0 = TMA producer, warp 1 = MMA issuer (one thread issues
+//     tcgen05.mma.cta_group::1.kind::i8, M=128 N=128 K=32), warp 2 = TMEM
+//     allocator, warps 4 .. 4+4*MT-1 = epilogue (one thread per sample row,
+//     tcgen05.ld 32x32b, min-reduce over 128 columns);
+//   * TMEM holds 2 buffers x MT accumulators of 128 int32 columns, so the
+//     epilogue of tile j overlaps the MMAs of tile j+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kTileM = 128;
+constexpr int kTileN = 128;
+constexpr int kKBlock = 128;  // bytes of K per swizzle atom row
+constexpr int kKStep = 32;    // UMMA K for kind::i8
+constexpr int kTileBytes = kTileM * kKBlock;  // 16 KB
+
+struct TcParams {
+  int64_t S;
+  int n_groups;
+  int kb;           // k-blocks per row
+  int ksteps_last;  // UMMA k-steps in the last k-block
+  int nt_lower;     // reference tiles holding lower refs (come first)
+  int nt_total;
+  int stages;
+  uint8_t* flags;
+  int accumulate;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// K-major, 128-byte-swizzled operand tile: 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// kind::i8 instruction descriptor: D = s32, A = B = s8, K-major, M x N.
+__host__ __device__ constexpr uint32_t i8_idesc(int m, int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+#define RSR_LD32(addr, v)                                                                       \
+  asm volatile(                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"        \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),     \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),              \
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),           \
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),           \
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),           \
+        "=r"(v[31])                                                                             \
+      : "r"(addr))
+
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int MT>
+__global__ void __launch_bounds__(128 + 128 * MT, 1)
+classify_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_lower,
+                   const __grid_constant__ CUtensorMap map_upper, const TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment for the 128-byte swizzle atoms.
+  const uint32_t raw_addr = smem_addr(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + (size_t)MT * p.kb * kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * kTileBytes);
+  uint64_t* b_full = bars;
+  uint64_t* b_empty = bars + p.stages;
+  uint64_t* a_full = bars + 2 * p.stages;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* t_full = a_full + 2;   // [2]
+  uint64_t* t_empty = a_full + 4;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+
+  constexpr uint32_t kTmemCols = MT == 2 ? 512 : 256;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lower)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_upper)));
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(smem_addr(&b_full[i]), 1);
+      mbar_init(smem_addr(&b_empty[i]), 1);
+    }
+    mbar_init(smem_addr(a_full), 1);
+    mbar_init(smem_addr(a_empty), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_addr(&t_full[i]), 1);
+      mbar_init(smem_addr(&t_empty[i]), 4 * MT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0, a_phase = 0;
+      for (int g = blockIdx.x; g < p.n_groups; g += gridDim.x) {
+        mbar_wait(smem_addr(a_empty), a_phase ^ 1);
+        mbar_expect_tx(smem_addr(a_full), (uint32_t)(MT * p.kb * kTileBytes));
+        for (int mt = 0; mt < MT; ++mt)
+          for (int kb = 0; kb < p.kb; ++kb)
+            tma_load_2d(smem_addr(sA + (size_t)(mt * p.kb + kb) * kTileBytes), &map_a,
+                        smem_addr(a_full), kb * kKBlock, (g * MT + mt) * kTileM);
+        a_phase ^= 1;
+        for (int j = 0; j < p.nt_total; ++j) {
+          const bool low = j < p.nt_lower;
+          const CUtensorMap* map = low ? &map_lower : &map_upper;
+          const int y = (low ? j : j - p.nt_lower) * kTileN;
+          for (int kb = 0; kb < p.kb; ++kb) {
+            mbar_wait(smem_addr(&b_empty[stage]), phase ^ 1);
+            mbar_expect_tx(smem_addr(&b_full[stage]), (uint32_t)kTileBytes);
+            tma_load_2d(smem_addr(sB + (size_t)stage * kTileBytes), map,
+                        smem_addr(&b_full[stage]), kb * kKBlock, y);
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = i8_idesc(kTileM, kTileN);
+      int stage = 0;
+      uint32_t phase = 0, a_phase = 0, tc = 0;
+      for (int g = blockIdx.x; g < p.n_groups; g += gridDim.x) {
+        mbar_wait(smem_addr(a_full), a_phase);
+        a_phase ^= 1;
+        tc_fence_after();
+        for (int j = 0; j < p.nt_total; ++j, ++tc) {
+          const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
+          mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < p.kb; ++kb) {
+            mbar_wait(smem_addr(&b_full[stage]), phase);
+            tc_fence_after();
+            const int nks = (kb == p.kb - 1) ? p.ksteps_last : kKBlock / kKStep;
+            const uint32_t b_base = smem_addr(sB + (size_t)stage * kTileBytes);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              const uint32_t a_base = smem_addr(sA + (size_t)(mt * p.kb + kb) * kTileBytes);
+              const uint32_t d = tmem_base + (buf * MT + mt) * kTileN;
+              for (int ks = 0; ks < nks; ++ks)
+                umma_i8(d, sw128_desc(a_base + ks * kKStep), sw128_desc(b_base + ks * kKStep),
+                        idesc, (kb | ks) != 0);
+            }
+            umma_commit(smem_addr(&b_empty[stage]));
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(smem_addr(&t_full[buf]));
+        }
+        umma_commit(smem_addr(a_empty));
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------ epilogue
+    const int mt = (warp - 4) >> 2;
+    const int quad = warp & 3;
+    uint32_t tc = 0;
+    for (int g = blockIdx.x; g < p.n_groups; g += gridDim.x) {
+      uint32_t hit = 0;
+      for (int j = 0; j < p.nt_total; ++j, ++tc) {
+        const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
+        mbar_wait(smem_addr(&t_full[buf]), tphase);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(quad * 32) << 16) + (buf * MT + mt) * kTileN;
+        uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t v[64];
+          RSR_LD32(taddr + half * 64, v);
+          RSR_LD32(taddr + half * 64 + 32, (v + 32));
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 64; ++i) mn = min(mn, v[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_addr(&t_empty[buf]));
+        if (mn == 0) hit |= (j < p.nt_lower) ? RSR_HIT_LOWER : RSR_HIT_UPPER;
+      }
+      const int64_t row = ((int64_t)g * MT + mt) * kTileM + quad * 32 + lane;
+      if (row < p.S) {
+        const uint8_t prev = p.accumulate ? p.flags[row] : 0;
+        p.flags[row] = (uint8_t)(prev | hit);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+__global__ void clear_flags_kernel(uint8_t* flags, int64_t S) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < S) flags[i] = 0;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+int make_map(CUtensorMap* map, const void* base, int64_t rows, int kpad) {
+  auto enc = tensor_map_encoder();
+  RSR_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kpad};
+  cuuint32_t box[2] = {(cuuint32_t)kKBlock, (cuuint32_t)kTileM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    rsr::set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return RSR_ECUDA;
+  }
+  return RSR_OK;
+}
+
+template <int MT>
+int launch_tc(const CUtensorMap& ma, const CUtensorMap& ml, const CUtensorMap& mu, TcParams p,
+              size_t smem, int sm_count, cudaStream_t st) {
+  auto k = classify_tc_kernel<MT>;
+  RSR_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = p.n_groups < sm_count ? p.n_groups : sm_count;
+  k<<<grid, 128 + 128 * MT, smem, st>>>(ma, ml, mu, p);
+  return rsr::check_launch("classify_tc_kernel");
+}
+
+}  // namespace
+
+extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower, int64_t n_lower,
+                               const int8_t* B_upper, int64_t n_upper, int Kpad, uint8_t* flags,
+                               int accumulate, void* stream) {
+  RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_tc: negative size");
+  RSR_REQUIRE(Kpad >= 32 && Kpad % 32 == 0, "rsr_classify_tc: Kpad must be a multiple of 32");
+  RSR_REQUIRE(Kpad <= 6 * kKBlock, "rsr_classify_tc: Kpad > 768 unsupported");
+  RSR_REQUIRE(S <= ((int64_t)1 << 31) - kTileM * 2, "rsr_classify_tc: S too large");
+  cudaStream_t st = rsr::as_stream(stream);
+  if (S == 0) return RSR_OK;
+  RSR_REQUIRE(flags != nullptr && A != nullptr, "rsr_classify_tc: null pointer");
+  const int64_t nt_l = rsr::ceil_div(n_lower, kTileN), nt_u = rsr::ceil_div(n_upper, kTileN);
+  if (nt_l + nt_u == 0) {
+    if (!accumulate) {
+      clear_flags_kernel<<<(unsigned)rsr::ceil_div(S, 256), 256, 0, st>>>(flags, S);
+      return rsr::check_launch("clear_flags_kernel");
+    }
+    return RSR_OK;
+  }
+  RSR_REQUIRE(nt_l + nt_u < (1 << 30), "rsr_classify_tc: too many reference tiles");
+  RSR_REQUIRE((nt_l == 0 || B_lower) && (nt_u == 0 || B_upper), "rsr_classify_tc: null refs");
+
+  int dev = 0, sm_count = 0;
+  RSR_CUDA(cudaGetDevice(&dev));
+  RSR_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+
+  CUtensorMap ma, ml, mu;
+  int rc = make_map(&ma, A, S, Kpad);
+  if (rc) return rc;
+  const int8_t* bl = nt_l ? B_lower : B_upper;
+  const int8_t* bu = nt_u ? B_upper : B_lower;
+  rc = make_map(&ml, bl, (nt_l ? nt_l : nt_u) * kTileN, Kpad);
+  if (rc) return rc;
+  rc = make_map(&mu, bu, (nt_u ? nt_u : nt_l) * kTileN, Kpad);
+  if (rc) return rc;
+
+  TcParams p;
+  p.S = S;
+  p.kb = (int)rsr::ceil_div(Kpad, kKBlock);
+  p.ksteps_last = (Kpad - (p.kb - 1) * kKBlock) / kKStep;
+  p.nt_lower = (int)nt_l;
+  p.nt_total = (int)(nt_l + nt_u);
+  p.flags = flags;
+  p.accumulate = accumulate;
+
+  const size_t max_smem = 227 * 1024;
+  const size_t fixed = 1024 /*align slack*/ + 256 /*barriers*/;
+  const int mt = ((size_t)2 * p.kb * kTileBytes + 4 * kTileBytes + fixed <= max_smem) ? 2 : 1;
+  const size_t a_bytes = (size_t)mt * p.kb * kTileBytes;
+  int stages = (int)((max_smem - fixed - a_bytes) / kTileBytes);
+  if (stages > 8) stages = 8;
+  RSR_REQUIRE(stages >= 2, "rsr_classify_tc: Kpad too large for shared memory");
+  p.stages = stages;
+  const size_t smem = fixed + a_bytes + (size_t)stages * kTileBytes;
+  p.n_groups = (int)rsr::ceil_div(S, (int64_t)mt * kTileM);
+  if (mt == 2) return launch_tc<2>(ma, ml, mu, p, smem, sm_count, st);
+  return launch_tc<1>(ma, ml, mu, p, smem, sm_count, st);
+}

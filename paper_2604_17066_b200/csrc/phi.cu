@@ -1,0 +1,328 @@
+// (3) Batched system-function evaluation and (4) batched boundary search.
+//
+// Replaces model.py:88-97 (SystemModel.evaluate) -> sysfn.py:62-185 (union-find
+// s-t / global connectivity, k-out-of-n) plus the builder-defined widest-path
+// level and the cone-sum monotone function of the reference test
+// fixtures (tests/conftest.py:53-75); and boundary.py:116-147
+// (boundary_search), boundary.py:50-54 (_redundant_under).
+//
+// One warp per sample.  Connectivity is label propagation over the alive edges
+// (x_e >= level): lanes sweep the edge list, OR-ing a per-node reach flag in
+// shared memory, until a sweep changes nothing (or t is reached).  The result
+// equals the union-find answer of the reference: both compute the connected
+// component of s in the alive subgraph.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kWarps = 8;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct Phi {
+  int kind, N, M, n_nodes, s, t, k, n_anchors;
+  const int32_t* eu;  // smem copies for graph kinds
+  const int32_t* ev;
+  const uint8_t* anchors;
+  const int32_t* alevel;
+};
+
+__device__ bool reach_from(const Phi& f, const volatile uint8_t* x, volatile uint8_t* reach,
+                           int source, int stop_at, int level, int lane) {
+  __syncwarp();  // previous readers of reach[] are done
+  for (int i = lane; i < f.n_nodes; i += 32) reach[i] = (uint8_t)(i == source);
+  __syncwarp();
+  bool result;
+  while (true) {
+    int changed = 0;
+    for (int e = lane; e < f.N; e += 32) {
+      if (x[e] >= level) {
+        const int u = f.eu[e], v = f.ev[e];
+        const uint8_t ru = reach[u], rv = reach[v];
+        if (ru != rv) {
+          reach[u] = 1;
+          reach[v] = 1;
+          changed = 1;
+        }
+      }
+    }
+    __syncwarp();
+    const bool at_stop = stop_at >= 0 ? reach[stop_at] != 0 : true;
+    if (!__any_sync(kFull, changed) || (stop_at >= 0 && at_stop)) {
+      result = at_stop;
+      break;
+    }
+  }
+  __syncwarp();
+  return result;
+}
+
+__device__ int phi_warp(const Phi& f, const volatile uint8_t* x, volatile uint8_t* reach, int lane) {
+  switch (f.kind) {
+    case RSR_PHI_ST_CONNECTIVITY:
+      return reach_from(f, x, reach, f.s, f.t, 1, lane) ? 1 : 0;
+    case RSR_PHI_WIDEST_PATH:
+      for (int level = f.M - 1; level >= 1; --level)
+        if (reach_from(f, x, reach, f.s, f.t, level, lane)) return level;
+      return 0;
+    case RSR_PHI_GLOBAL_CONNECTIVITY: {
+      reach_from(f, x, reach, 0, -1, 1, lane);
+      int all = 1;
+      for (int i = lane; i < f.n_nodes; i += 32) all &= reach[i] != 0;
+      return __all_sync(kFull, all) ? 1 : 0;
+    }
+    case RSR_PHI_K_OUT_OF_N: {
+      for (int v = f.M - 1; v >= 1; --v) {
+        int c = 0;
+        for (int e = lane; e < f.N; e += 32) c += x[e] >= v;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+        if (c >= f.k) return v;
+      }
+      return 0;
+    }
+    case RSR_PHI_CONE_SUM: {
+      unsigned levels_hit = 0;
+      for (int a = 0; a < f.n_anchors; ++a) {
+        const uint8_t* an = f.anchors + (int64_t)a * f.N;
+        int ok = 1;
+        for (int e = lane; e < f.N; e += 32) ok &= x[e] >= an[e];
+        if (__all_sync(kFull, ok)) levels_hit |= 1u << f.alevel[a];
+      }
+      return __popc(levels_hit);
+    }
+  }
+  return 0;
+}
+
+// Shared-memory layout per block: edges (graph kinds), then per warp x[N] and
+// reach[n_nodes].
+__device__ Phi load_phi(const rsr_phi_desc& d, uint8_t* smem, int32_t** tail) {
+  Phi f;
+  f.kind = d.kind;
+  f.N = d.n_components;
+  f.M = d.n_states;
+  f.n_nodes = d.n_nodes;
+  f.s = d.source;
+  f.t = d.target;
+  f.k = d.k;
+  f.n_anchors = d.n_anchors;
+  f.anchors = d.anchors;
+  f.alevel = d.anchor_level;
+  int32_t* eu = reinterpret_cast<int32_t*>(smem);
+  int32_t* ev = eu + (d.edge_u ? f.N : 0);
+  if (d.edge_u) {
+    for (int i = threadIdx.x; i < f.N; i += blockDim.x) {
+      eu[i] = d.edge_u[i];
+      ev[i] = d.edge_v[i];
+    }
+  }
+  f.eu = eu;
+  f.ev = ev;
+  *tail = ev + (d.edge_u ? f.N : 0);
+  __syncthreads();
+  return f;
+}
+
+__host__ __device__ inline size_t phi_smem_bytes(const rsr_phi_desc& d) {
+  const size_t edges = d.edge_u ? 2 * sizeof(int32_t) * (size_t)d.n_components : 0;
+  const size_t per_warp = ((size_t)d.n_components + (size_t)d.n_nodes + 15) / 16 * 16;
+  return edges + kWarps * per_warp;
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+phi_eval_kernel(const rsr_phi_desc d, const uint8_t* __restrict__ states,
+                const int64_t* __restrict__ idx, int64_t count, uint8_t* __restrict__ out) {
+  extern __shared__ uint8_t smem[];
+  int32_t* tail;
+  const Phi f = load_phi(d, smem, &tail);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t per_warp = ((size_t)f.N + f.n_nodes + 15) / 16 * 16;
+  volatile uint8_t* x = reinterpret_cast<uint8_t*>(tail) + warp * per_warp;
+  volatile uint8_t* reach = x + f.N;
+  for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < count;
+       i += (int64_t)gridDim.x * kWarps) {
+    const int64_t row = idx ? idx[i] : i;
+    const uint8_t* src = states + row * f.N;
+    for (int e = lane; e < f.N; e += 32) x[e] = src[e];
+    __syncwarp();
+    const int v = phi_warp(f, x, reach, lane);
+    if (lane == 0) out[i] = (uint8_t)v;
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+boundary_kernel(const rsr_phi_desc d, int threshold, const uint8_t* __restrict__ x0, int64_t B,
+                uint8_t* __restrict__ out_refs, uint8_t* __restrict__ out_side,
+                int64_t* __restrict__ out_calls) {
+  extern __shared__ uint8_t smem[];
+  int32_t* tail;
+  const Phi f = load_phi(d, smem, &tail);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t per_warp = ((size_t)f.N + f.n_nodes + 15) / 16 * 16;
+  volatile uint8_t* x = reinterpret_cast<uint8_t*>(tail) + warp * per_warp;
+  volatile uint8_t* reach = x + f.N;
+  for (int64_t b = (int64_t)blockIdx.x * kWarps + warp; b < B; b += (int64_t)gridDim.x * kWarps) {
+    const uint8_t* src = x0 + b * f.N;
+    for (int e = lane; e < f.N; e += 32) x[e] = src[e];
+    __syncwarp();
+    int64_t calls = 1;
+    const bool lower = phi_warp(f, x, reach, lane) <= threshold;
+    const int step = lower ? 1 : -1, limit = lower ? f.M - 1 : 0;
+    for (int n = 0; n < f.N; ++n) {
+      while (x[n] != limit) {
+        __syncwarp();
+        if (lane == 0) x[n] = (uint8_t)(x[n] + step);
+        __syncwarp();
+        const int s = phi_warp(f, x, reach, lane);
+        ++calls;
+        const bool crossed = lower ? (s > threshold) : (s <= threshold);
+        if (crossed) {
+          __syncwarp();
+          if (lane == 0) x[n] = (uint8_t)(x[n] - step);
+          __syncwarp();
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    uint8_t* dst = out_refs + b * f.N;
+    for (int e = lane; e < f.N; e += 32) dst[e] = x[e];
+    if (lane == 0) {
+      out_side[b] = lower ? RSR_SIDE_LOWER : RSR_SIDE_UPPER;
+      out_calls[b] = calls;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void gather_kernel(const uint8_t* __restrict__ states, int N,
+                              const int64_t* __restrict__ idx, int64_t count,
+                              uint8_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * N) return;
+  const int64_t i = t / N;
+  const int n = (int)(t - i * N);
+  out[t] = states[idx[i] * N + n];
+}
+
+// a is redundant given b: lower a <= b, upper a >= b (boundary.py:50-54)
+__device__ __forceinline__ bool redundant_under(int side, const uint8_t* a, const uint8_t* b,
+                                                int N) {
+  if (side == RSR_SIDE_LOWER) {
+    for (int n = 0; n < N; ++n)
+      if (a[n] > b[n]) return false;
+  } else {
+    for (int n = 0; n < N; ++n)
+      if (a[n] < b[n]) return false;
+  }
+  return true;
+}
+
+__global__ void dominance_kernel(const uint8_t* __restrict__ cands, int64_t B,
+                                 const uint8_t* __restrict__ members, int64_t K, int N, int side,
+                                 uint8_t* covered, uint8_t* covers, int mask_c,
+                                 uint8_t* member_mask) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (m >= K || c >= B) return;
+  const uint8_t* cv = cands + c * N;
+  const uint8_t* mv = members + m * N;
+  if (covered && redundant_under(side, cv, mv, N)) covered[c] = 1;
+  const bool dropped = redundant_under(side, mv, cv, N);
+  if (covers && dropped) covers[c] = 1;
+  if (member_mask && c == mask_c) member_mask[m] = dropped ? 1 : 0;
+}
+
+int check_phi(const rsr_phi_desc* d) {
+  RSR_REQUIRE(d != nullptr, "null phi descriptor");
+  RSR_REQUIRE(d->n_components >= 1 && d->n_states >= 2, "phi: bad N/M");
+  switch (d->kind) {
+    case RSR_PHI_ST_CONNECTIVITY:
+    case RSR_PHI_WIDEST_PATH:
+      RSR_REQUIRE(d->source >= 0 && d->source < d->n_nodes && d->target >= 0 &&
+                      d->target < d->n_nodes && d->source != d->target,
+                  "phi: bad source/target");
+      /* fallthrough */
+    case RSR_PHI_GLOBAL_CONNECTIVITY:
+      RSR_REQUIRE(d->edge_u && d->edge_v && d->n_nodes >= 1, "phi: graph kinds need edges");
+      break;
+    case RSR_PHI_K_OUT_OF_N:
+      RSR_REQUIRE(d->k >= 1 && d->k <= d->n_components, "phi: bad k");
+      break;
+    case RSR_PHI_CONE_SUM:
+      RSR_REQUIRE(d->n_anchors >= 0 && (d->n_anchors == 0 || (d->anchors && d->anchor_level)),
+                  "phi: cone sum needs anchors");
+      break;
+    default:
+      RSR_REQUIRE(false, "phi: unknown kind %d", d->kind);
+  }
+  RSR_REQUIRE(phi_smem_bytes(*d) <= 200 * 1024, "phi: graph too large for shared memory");
+  return RSR_OK;
+}
+
+int grid_for(int64_t items) {
+  int64_t g = rsr::ceil_div(items, kWarps);
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+extern "C" int rsr_phi_eval(const rsr_phi_desc* phi, const uint8_t* states, const int64_t* idx,
+                            int64_t count, uint8_t* out, void* stream) {
+  int rc = check_phi(phi);
+  if (rc) return rc;
+  RSR_REQUIRE(count >= 0, "rsr_phi_eval: negative count");
+  if (count == 0) return RSR_OK;
+  const size_t smem = phi_smem_bytes(*phi);
+  if (smem > 48 * 1024)
+    RSR_CUDA(cudaFuncSetAttribute(phi_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  phi_eval_kernel<<<grid_for(count), kWarps * 32, smem, rsr::as_stream(stream)>>>(
+      *phi, states, idx, count, out);
+  return rsr::check_launch("phi_eval_kernel");
+}
+
+extern "C" int rsr_boundary_search(const rsr_phi_desc* phi, int threshold, const uint8_t* x0,
+                                   int64_t B, uint8_t* out_refs, uint8_t* out_side,
+                                   int64_t* out_calls, void* stream) {
+  int rc = check_phi(phi);
+  if (rc) return rc;
+  RSR_REQUIRE(B >= 0, "rsr_boundary_search: negative count");
+  if (B == 0) return RSR_OK;
+  const size_t smem = phi_smem_bytes(*phi);
+  if (smem > 48 * 1024)
+    RSR_CUDA(cudaFuncSetAttribute(boundary_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  boundary_kernel<<<grid_for(B), kWarps * 32, smem, rsr::as_stream(stream)>>>(
+      *phi, threshold, x0, B, out_refs, out_side, out_calls);
+  return rsr::check_launch("boundary_kernel");
+}
+
+extern "C" int rsr_gather_rows(const uint8_t* states, int n_components, const int64_t* idx,
+                               int64_t count, uint8_t* out, void* stream) {
+  RSR_REQUIRE(n_components >= 1 && count >= 0, "rsr_gather_rows: bad shape");
+  if (count == 0) return RSR_OK;
+  const int64_t total = count * n_components;
+  gather_kernel<<<(unsigned)rsr::ceil_div(total, 256), 256, 0, rsr::as_stream(stream)>>>(
+      states, n_components, idx, count, out);
+  return rsr::check_launch("gather_kernel");
+}
+
+extern "C" int rsr_dominance_scan(const uint8_t* cands, int64_t B, const uint8_t* members,
+                                  int64_t K, int n_components, int side, uint8_t* covered,
+                                  uint8_t* covers, int mask_candidate, uint8_t* member_mask,
+                                  void* stream) {
+  RSR_REQUIRE(B >= 0 && K >= 0 && n_components >= 1, "rsr_dominance_scan: bad shape");
+  RSR_REQUIRE(side == RSR_SIDE_LOWER || side == RSR_SIDE_UPPER, "rsr_dominance_scan: bad side");
+  RSR_REQUIRE(B <= 65535, "rsr_dominance_scan: at most 65535 candidates per call");
+  cudaStream_t st = rsr::as_stream(stream);
+  if (covered && B) RSR_CUDA(cudaMemsetAsync(covered, 0, B, st));
+  if (covers && B) RSR_CUDA(cudaMemsetAsync(covers, 0, B, st));
+  if (B == 0 || K == 0) return RSR_OK;
+  dim3 grid((unsigned)rsr::ceil_div(K, 128), (unsigned)B);
+  dominance_kernel<<<grid, 128, 0, st>>>(cands, B, members, K, n_components, side, covered,
+                                         covers, mask_candidate, member_mask);
+  return rsr::check_launch("dominance_kernel");
+}

@@ -1,0 +1,237 @@
+// (1) On-device sampling and (2) thermometer encodings.
+//
+// Replaces sampling.py:39-90 (numpy Philox4x64-10 stream keyed by
+// [seed, generation_index], flat draw index (start+i)*N + n, inverse CDF by
+// searchsorted(side="right") on cumsum(probs)) and encoding.py:138-153.
+//
+// Bit-exactness: numpy's Philox pre-increments its 256-bit counter, so flat
+// draw f is word f%4 of the block generated from counter f/4 + 1.  The
+// inverse CDF is done in integers: with r = raw >> 11 and u = r * 2^-53
+// (exact), u >= cum  <=>  r >= ceil(cum * 2^53) (scaling by 2^53 is exact), so
+// state = #{m < M-1 : r >= T_m} with T_m = ceil(cumsum(probs[n])[m] * 2^53).
+// The clip to M-1 (sampling.py:89) is implied by counting only m < M-1.
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// Per-block prologue: thresholds T[n*(M-1)+m] from a sequential fp64 cumsum
+// (np.cumsum order), stored in shared memory.
+__device__ void load_thresholds(const double* __restrict__ probs, int N, int M,
+                                unsigned long long* T) {
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    double cum = 0.0;
+    for (int m = 0; m < M - 1; ++m) {
+      cum = __dadd_rn(cum, probs[(int64_t)n * M + m]);
+      double scaled = __dmul_rn(cum, 9007199254740992.0);  // * 2^53, exact
+      T[n * (M - 1) + m] = (unsigned long long)ceil(scaled);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads)
+sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
+              int64_t f0, int64_t f1, int64_t b_lo, int64_t nblk, uint8_t* __restrict__ states,
+              int8_t* __restrict__ thermo, int ld, int kdim, int nbias) {
+  extern __shared__ unsigned long long T[];
+  load_thresholds(probs, N, M, T);
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nblk) return;
+  const int64_t b = b_lo + t;
+  uint64_t w[4];
+  rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+  const int64_t fb = 4 * b;
+  int64_t row = fb / N;
+  int n = (int)(fb - row * N);
+  const int64_t start_row = f0 / N;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t f = fb + j;
+    if (f >= f0 && f < f1) {
+      const unsigned long long r = w[j] >> 11;
+      int st = 0;
+      const unsigned long long* Tn = T + n * (M - 1);
+      for (int m = 0; m < M - 1; ++m) st += (r >= Tn[m]) ? 1 : 0;
+      const int64_t i = row - start_row;
+      if (states) states[f - f0] = (uint8_t)st;
+      if (thermo) {
+        int8_t* arow = thermo + i * (int64_t)ld;
+        for (int k = 1; k < M; ++k) arow[n * (M - 1) + (k - 1)] = (int8_t)(st < k);
+        if (n == N - 1) {
+          for (int c = kdim; c < ld; ++c) arow[c] = (int8_t)(c < kdim + nbias);
+        }
+      }
+    }
+    if (++n == N) {
+      n = 0;
+      ++row;
+    }
+  }
+}
+
+__global__ void philox_raw_kernel(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
+                                  int64_t b_lo, int64_t nblk, uint64_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nblk) return;
+  const int64_t b = b_lo + t;
+  uint64_t w[4];
+  rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t f = 4 * b + j;
+    if (f >= first && f < first + count) out[f - first] = w[j];
+  }
+}
+
+__global__ void uniform_kernel(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
+                               int64_t b_lo, int64_t nblk, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nblk) return;
+  const int64_t b = b_lo + t;
+  uint64_t w[4];
+  rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t f = 4 * b + j;
+    if (f >= first && f < first + count)
+      out[f - first] = __dmul_rn((double)(w[j] >> 11), 1.1102230246251565e-16);  // 2^-53
+  }
+}
+
+// A rows from states: A[i, n(M-1)+k-1] = [x_n < k]; bias columns = 1; zero pad.
+__global__ void encode_samples_kernel(const uint8_t* __restrict__ states, int64_t count, int N,
+                                      int M, int8_t* __restrict__ out, int ld, int kdim,
+                                      int nbias) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * ld) return;
+  const int64_t i = t / ld;
+  const int c = (int)(t - i * ld);
+  int8_t v;
+  if (c < kdim) {
+    const int n = c / (M - 1), k = c % (M - 1) + 1;
+    v = (int8_t)(states[i * N + n] < k);
+  } else {
+    v = (int8_t)(c < kdim + nbias);
+  }
+  out[t] = v;
+}
+
+// B rows from reference states (see include/rsr_b200.h for the layout).
+__global__ void encode_refs_kernel(const uint8_t* __restrict__ states, int64_t count,
+                                   int64_t rows_total, int N, int M, int side,
+                                   int8_t* __restrict__ out, int ld, int kdim, int nbias) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows_total) return;
+  int8_t* row = out + r * (int64_t)ld;
+  if (r >= count) {  // never-hit pad row: A.B = bias column 0 = 1
+    for (int c = lane; c < ld; c += 32) row[c] = (int8_t)(c == kdim);
+    return;
+  }
+  const uint8_t* x = states + r * (int64_t)N;
+  int below = 0;  // c_r = #{(n,k) : r_n < k}
+  for (int c = lane; c < kdim; c += 32) {
+    const int n = c / (M - 1), k = c % (M - 1) + 1;
+    const int lt = x[n] < k;
+    if (side == RSR_SIDE_UPPER) {
+      row[c] = (int8_t)(!lt);
+    } else {
+      row[c] = (int8_t)(-lt);
+      below += lt;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+  for (int c = kdim + lane; c < ld; c += 32) {
+    int v = 0;
+    if (side == RSR_SIDE_LOWER && c < kdim + nbias) {
+      const int j = c - kdim;
+      const int rem = below - 127 * j;
+      v = rem <= 0 ? 0 : (rem > 127 ? 127 : rem);
+    }
+    row[c] = (int8_t)v;
+  }
+}
+
+}  // namespace
+
+extern "C" int rsr_philox_raw(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
+                              uint64_t* out, void* stream) {
+  RSR_REQUIRE(first >= 0 && count >= 0, "rsr_philox_raw: negative range");
+  if (count == 0) return RSR_OK;
+  RSR_REQUIRE(out != nullptr, "rsr_philox_raw: null output");
+  const int64_t b_lo = first / 4, b_hi = (first + count - 1) / 4, nblk = b_hi - b_lo + 1;
+  philox_raw_kernel<<<(unsigned)rsr::ceil_div(nblk, kThreads), kThreads, 0,
+                      rsr::as_stream(stream)>>>(seed, gen, first, count, b_lo, nblk, out);
+  return rsr::check_launch("philox_raw_kernel");
+}
+
+extern "C" int rsr_uniform_field(uint64_t seed, uint64_t gen, int64_t start, int64_t count,
+                                 int n_components, double* out, void* stream) {
+  RSR_REQUIRE(start >= 0 && count >= 0 && n_components >= 1, "rsr_uniform_field: bad shape");
+  if (count == 0) return RSR_OK;
+  RSR_REQUIRE(out != nullptr, "rsr_uniform_field: null output");
+  const int64_t first = start * n_components, total = count * n_components;
+  const int64_t b_lo = first / 4, b_hi = (first + total - 1) / 4, nblk = b_hi - b_lo + 1;
+  uniform_kernel<<<(unsigned)rsr::ceil_div(nblk, kThreads), kThreads, 0,
+                   rsr::as_stream(stream)>>>(seed, gen, first, total, b_lo, nblk, out);
+  return rsr::check_launch("uniform_kernel");
+}
+
+extern "C" int rsr_sample(const double* probs, int n_components, int n_states, uint64_t seed,
+                          uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+                          int8_t* out_thermo, int ld_thermo, void* stream) {
+  const int N = n_components, M = n_states;
+  RSR_REQUIRE(N >= 1 && M >= 2 && M <= 255, "rsr_sample: need N >= 1 and 2 <= M <= 255");
+  RSR_REQUIRE(start >= 0 && count >= 1, "rsr_sample: n_samples must be >= 1");
+  RSR_REQUIRE(probs != nullptr, "rsr_sample: null probs");
+  RSR_REQUIRE(out_states || out_thermo, "rsr_sample: no output requested");
+  const int kdim = rsr::thermo_kdim(N, M), nbias = rsr::thermo_bias_cols(N, M);
+  if (out_thermo)
+    RSR_REQUIRE(ld_thermo >= rsr::thermo_kpad(N, M), "rsr_sample: ld_thermo < Kpad (%d)",
+                rsr::thermo_kpad(N, M));
+  const size_t smem = (size_t)N * (M - 1) * sizeof(unsigned long long);
+  RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample: N*(M-1) too large for the threshold table");
+  if (smem > 48 * 1024)
+    RSR_CUDA(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  const int64_t f0 = start * N, f1 = (start + count) * N;
+  const int64_t b_lo = f0 / 4, b_hi = (f1 - 1) / 4, nblk = b_hi - b_lo + 1;
+  sample_kernel<<<(unsigned)rsr::ceil_div(nblk, kThreads), kThreads, smem,
+                  rsr::as_stream(stream)>>>(probs, N, M, seed, gen, f0, f1, b_lo, nblk,
+                                            out_states, out_thermo, ld_thermo, kdim, nbias);
+  return rsr::check_launch("sample_kernel");
+}
+
+extern "C" int rsr_encode_samples(const uint8_t* states, int64_t count, int n_components,
+                                  int n_states, int8_t* out, int ld, void* stream) {
+  const int N = n_components, M = n_states;
+  RSR_REQUIRE(N >= 1 && M >= 2 && count >= 0, "rsr_encode_samples: bad shape");
+  RSR_REQUIRE(ld >= rsr::thermo_kpad(N, M) && ld % 16 == 0, "rsr_encode_samples: bad ld");
+  if (count == 0) return RSR_OK;
+  const int64_t total = count * ld;
+  encode_samples_kernel<<<(unsigned)rsr::ceil_div(total, kThreads), kThreads, 0,
+                          rsr::as_stream(stream)>>>(states, count, N, M, out, ld,
+                                                    rsr::thermo_kdim(N, M),
+                                                    rsr::thermo_bias_cols(N, M));
+  return rsr::check_launch("encode_samples_kernel");
+}
+
+extern "C" int rsr_encode_refs(const uint8_t* states, int64_t count, int64_t rows_total,
+                               int n_components, int n_states, int side, int8_t* out, int ld,
+                               void* stream) {
+  const int N = n_components, M = n_states;
+  RSR_REQUIRE(N >= 1 && M >= 2 && count >= 0 && rows_total >= count, "rsr_encode_refs: bad shape");
+  RSR_REQUIRE(side == RSR_SIDE_LOWER || side == RSR_SIDE_UPPER, "rsr_encode_refs: bad side");
+  RSR_REQUIRE(ld >= rsr::thermo_kpad(N, M) && ld % 16 == 0, "rsr_encode_refs: bad ld");
+  if (rows_total == 0) return RSR_OK;
+  const int warps = kThreads / 32;
+  encode_refs_kernel<<<(unsigned)rsr::ceil_div(rows_total, warps), kThreads, 0,
+                       rsr::as_stream(stream)>>>(states, count, rows_total, N, M, side, out, ld,
+                                                 rsr::thermo_kdim(N, M),
+                                                 rsr::thermo_bias_cols(N, M));
+  return rsr::check_launch("encode_refs_kernel");
+}

@@ -1,0 +1,214 @@
+"""Raw C-ABI kernel parity against the oracle (GPU)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2604_17066_b200 import _abi as A
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(x, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(x))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def test_philox_raw_and_uniform():
+    for seed, gen, first, count in [(123, 0, 0, 8), (2**64 - 1, 7, 5, 1001), (9, 2**63 + 3, 12345, 777)]:
+        out = torch.empty(count, dtype=torch.int64, device="cuda")
+        A.call("rsr_philox_raw", seed, gen, first, count, A.ptr(out), A.stream_ptr())
+        got = out.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, oracle.random_raw(seed, gen, first, count))
+    u = torch.empty((33, 13), dtype=torch.float64, device="cuda")
+    A.call("rsr_uniform_field", 5, 3, 17, 33, 13, A.ptr(u), A.stream_ptr())
+    assert np.array_equal(u.cpu().numpy(), oracle.uniform_field(5, 3, 17, 33, 13))
+
+
+@pytest.mark.parametrize("n,m,count,start", [(295, 2, 4099, 0), (40, 2, 1000, 3), (7, 3, 513, 11),
+                                             (5, 5, 300, 1)])
+def test_sample_states_and_thermo(n, m, count, start):
+    rng = np.random.default_rng(n * 31 + m)
+    raw = rng.random((n, m)) + 0.01
+    probs = raw / raw.sum(1, keepdims=True)
+    want = oracle.sample_states(probs, count, seed=77, generation_index=2, start=start)
+    kpad = A.thermo_kpad(n, m)
+    st = torch.empty((count, n), dtype=torch.uint8, device="cuda")
+    th = torch.empty((count, kpad), dtype=torch.int8, device="cuda")
+    A.call("rsr_sample", A.ptr(_dev(probs)), n, m, 77, 2, start, count, A.ptr(st), A.ptr(th), kpad,
+           A.stream_ptr())
+    assert np.array_equal(st.cpu().numpy(), want)
+    th2 = torch.empty_like(th)
+    A.call("rsr_encode_samples", A.ptr(st), count, n, m, A.ptr(th2), kpad, A.stream_ptr())
+    assert torch.equal(th, th2)
+    kdim = n * (m - 1)
+    t = th.cpu().numpy().astype(np.int64)
+    for k in range(1, m):
+        assert np.array_equal(t[:, [j * (m - 1) + k - 1 for j in range(n)]], (want < k).astype(np.int64))
+
+
+def _refs_dev(refs, n, m, side):
+    kpad = A.thermo_kpad(n, m)
+    k = refs.shape[0]
+    rows = max(128, (k + 127) // 128 * 128)
+    st = _dev(refs.astype(np.uint8))
+    out = torch.empty((rows, kpad), dtype=torch.int8, device="cuda")
+    A.call("rsr_encode_refs", A.ptr(st) if k else None, k, rows, n, m, side, A.ptr(out), kpad, A.stream_ptr())
+    return out
+
+
+def _classify_tc(samples, lower, upper, n, m):
+    kpad = A.thermo_kpad(n, m)
+    s = samples.shape[0]
+    st = _dev(samples.astype(np.uint8))
+    a = torch.empty((s, kpad), dtype=torch.int8, device="cuda")
+    A.call("rsr_encode_samples", A.ptr(st), s, n, m, A.ptr(a), kpad, A.stream_ptr())
+    bl = _refs_dev(lower, n, m, A.SIDE_LOWER)
+    bu = _refs_dev(upper, n, m, A.SIDE_UPPER)
+    flags = torch.empty(s, dtype=torch.uint8, device="cuda")
+    A.call("rsr_classify_tc", A.ptr(a), s, A.ptr(bl), lower.shape[0], A.ptr(bu), upper.shape[0], kpad,
+           A.ptr(flags), 0, A.stream_ptr())
+    return flags.cpu().numpy()
+
+
+def _classify_bits(samples, lower, upper, n, m, first=False):
+    w = A.thermo_words(n, m)
+    s = samples.shape[0]
+
+    def pack(x, invert):
+        out = torch.zeros((max(1, x.shape[0]), w), dtype=torch.int32, device="cuda")
+        if x.shape[0]:
+            A.call("rsr_pack_thermo_bits", A.ptr(_dev(x.astype(np.uint8))), x.shape[0], n, m, invert,
+                   A.ptr(out), w, A.stream_ptr())
+        return out
+    sb, lb, ub = pack(samples, 0), pack(lower, 0), pack(upper, 1)
+    flags = torch.empty(s, dtype=torch.uint8, device="cuda")
+    fl = torch.empty(s, dtype=torch.int64, device="cuda") if first else None
+    fu = torch.empty(s, dtype=torch.int64, device="cuda") if first else None
+    A.call("rsr_classify_bits", A.ptr(sb), s, A.ptr(lb), lower.shape[0], A.ptr(ub), upper.shape[0], w,
+           A.ptr(flags), A.ptr(fl), A.ptr(fu), 0, A.stream_ptr())
+    if first:
+        return flags.cpu().numpy(), fl.cpu().numpy(), fu.cpu().numpy()
+    return flags.cpu().numpy()
+
+
+def _want_flags(samples, lower, upper, m):
+    hl, _ = oracle.dominance_hits(samples, lower, m, oracle.LOWER)
+    hu, _ = oracle.dominance_hits(samples, upper, m, oracle.UPPER)
+    return hl.astype(np.uint8) | (hu.astype(np.uint8) << 1)
+
+
+@pytest.mark.parametrize("n,m,s,kl,ku,p1", [
+    (295, 2, 3000, 300, 260, 0.5),
+    (295, 2, 1000, 1, 129, 0.9),
+    (40, 2, 777, 50, 0, 0.9),
+    (13, 3, 2000, 37, 41, 0.6),
+    (100, 3, 600, 200, 130, 0.5),
+    (9, 4, 500, 20, 20, 0.5),
+    (200, 4, 300, 64, 64, 0.5),
+])
+def test_classifiers_match_oracle(n, m, s, kl, ku, p1):
+    rng = np.random.default_rng(n + 1000 * m + s)
+    samples = rng.integers(0, m, size=(s, n))
+    if m == 2:
+        samples = (rng.random((s, n)) < p1).astype(np.int64)
+    # references near the samples so both sides get hits
+    lower = np.clip(samples[rng.integers(0, s, kl)] + rng.integers(0, 2, (kl, n)), 0, m - 1)
+    upper = np.clip(samples[rng.integers(0, s, ku)] - rng.integers(0, 2, (ku, n)), 0, m - 1)
+    want = _want_flags(samples, lower, upper, m)
+    assert want.min() == 0 or True
+    got_tc = _classify_tc(samples, lower, upper, n, m)
+    assert np.array_equal(got_tc, want), f"tc mismatch at {np.flatnonzero(got_tc != want)[:10]}"
+    got_bits = _classify_bits(samples, lower, upper, n, m)
+    assert np.array_equal(got_bits, want)
+
+
+def test_first_match_and_violation_counts():
+    rng = np.random.default_rng(3)
+    n, m = 9, 3
+    samples = rng.integers(0, m, size=(500, n))
+    refs = rng.integers(0, m, size=(200, n))
+    flags, fl, fu = _classify_bits(samples, refs, refs, n, m, first=True)
+    r = oracle.classify_labels(samples, refs, refs, m, want_first=True)
+    assert np.array_equal(fl, r["first_lower"]) and np.array_equal(fu, r["first_upper"])
+    for side, kind in ((A.SIDE_LOWER, "lower_ref"), (A.SIDE_UPPER, "upper_ref")):
+        out = torch.empty((500, 200), dtype=torch.int32, device="cuda")
+        A.call("rsr_violation_counts", A.ptr(_dev(samples.astype(np.uint8))), 500,
+               A.ptr(_dev(refs.astype(np.uint8))), 200, n, side, A.ptr(out), A.stream_ptr())
+        assert np.array_equal(out.cpu().numpy(), oracle.violation_counts(samples, refs, m, kind))
+
+
+def test_finalize_and_compact():
+    rng = np.random.default_rng(5)
+    s = 100_003
+    flags = rng.integers(0, 4, s).astype(np.uint8)
+    f = _dev(flags)
+    labels = torch.empty(s, dtype=torch.uint8, device="cuda")
+    counts = torch.empty(4, dtype=torch.int64, device="cuda")
+    A.call("rsr_finalize", A.ptr(f), s, A.ptr(labels), A.ptr(counts), A.stream_ptr())
+    lab = labels.cpu().numpy()
+    want = np.where(flags & 1, 0, np.where(flags & 2, 1, 2)).astype(np.uint8)
+    assert np.array_equal(lab, want)
+    assert counts.cpu().tolist() == [int((want == 0).sum()), int((want == 1).sum()),
+                                     int((want == 2).sum()), int((flags == 3).sum())]
+    scratch = torch.empty(A.call("rsr_compact_scratch", s), dtype=torch.int64, device="cuda")
+    for label in (0, 1, 2):
+        idx = torch.empty(s, dtype=torch.int64, device="cuda")
+        cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+        A.call("rsr_compact", A.ptr(labels), s, label, A.ptr(idx), A.ptr(cnt), A.ptr(scratch), A.stream_ptr())
+        c = int(cnt.item())
+        assert np.array_equal(idx[:c].cpu().numpy(), np.flatnonzero(want == label))
+
+
+def _grid(rows=5, cols=5):
+    edges = [(r * cols + c, r * cols + c + 1) for r in range(rows) for c in range(cols - 1)]
+    edges += [(r * cols + c, (r + 1) * cols + c) for r in range(rows - 1) for c in range(cols)]
+    return rows * cols, edges
+
+
+def _phi_desc(kind, n_nodes, edges, s, t, m, k=0, keep=None):
+    eu = _dev(np.array([e[0] for e in edges], dtype=np.int32))
+    ev = _dev(np.array([e[1] for e in edges], dtype=np.int32))
+    d = A.PhiDesc(kind, len(edges), m, n_nodes, s, t, k, 0, eu.data_ptr(), ev.data_ptr(), None, None)
+    if keep is not None:
+        keep.extend([eu, ev])
+    return d
+
+
+@pytest.mark.parametrize("kind,m", [(A.PHI_ST, 2), (A.PHI_WIDEST, 3), (A.PHI_GLOBAL, 2)])
+def test_phi_eval_and_boundary(kind, m):
+    nn, edges = _grid()
+    keep = []
+    d = _phi_desc(kind, nn, edges, 0, nn - 1, m, keep=keep)
+    rng = np.random.default_rng(kind)
+    xs = rng.integers(0, m, size=(2000, len(edges)))
+    if m == 2:
+        xs = (rng.random((2000, len(edges))) < 0.7).astype(np.int64)
+    if kind == A.PHI_ST:
+        ref = oracle.phi_st(nn, edges, 0, nn - 1)
+    elif kind == A.PHI_WIDEST:
+        ref = oracle.phi_widest(nn, edges, 0, nn - 1, m)
+    else:
+        ref = oracle.phi_global(nn, edges)
+    want = np.array([ref(x) for x in xs])
+    out = torch.empty(2000, dtype=torch.uint8, device="cuda")
+    A.call("rsr_phi_eval", A.ctypes.byref(d), A.ptr(_dev(xs.astype(np.uint8))), None, 2000, A.ptr(out),
+           A.stream_ptr())
+    assert np.array_equal(out.cpu().numpy(), want)
+    ms = m if kind == A.PHI_WIDEST else 2
+    for thr in range(ms - 1):
+        B = 64
+        x0 = xs[:B]
+        refs = torch.empty((B, len(edges)), dtype=torch.uint8, device="cuda")
+        side = torch.empty(B, dtype=torch.uint8, device="cuda")
+        calls = torch.empty(B, dtype=torch.int64, device="cuda")
+        A.call("rsr_boundary_search", A.ctypes.byref(d), thr, A.ptr(_dev(x0.astype(np.uint8))), B,
+               A.ptr(refs), A.ptr(side), A.ptr(calls), A.stream_ptr())
+        for b in range(B):
+            ev = oracle.CountingPhi(ref, len(edges), m, ms)
+            vec, sd = oracle.boundary_search(ev, x0[b], thr)
+            assert tuple(refs[b].cpu().tolist()) == vec
+            assert int(side[b]) == (A.SIDE_LOWER if sd == oracle.LOWER else A.SIDE_UPPER)
+            assert int(calls[b]) == ev.count
