@@ -108,6 +108,15 @@ int rsr_encode_refs(const uint8_t* states, int64_t count, int64_t rows_total,
                     int n_components, int n_states, int side, int8_t* out, int ld,
                     void* stream);
 
+/* Reference-layout rows (encoding.py:42-57, 138-153): kind 0 = sample
+ * (one-hot), 1 = lower_ref (prefix), 2 = upper_ref (suffix); out u8 [K x N*M]. */
+int rsr_encode_rows(const uint8_t* states, int64_t count, int n_components, int n_states,
+                    int kind, uint8_t* out, void* stream);
+/* np.packbits(rows, axis=1) (MSB first, zero padded), complement != 0 packs
+ * 1 - rows with pad bits zero (encoding.py:82-98); out u8 [K x ceil(L/8)]. */
+int rsr_packbits_rows(const uint8_t* rows, int64_t count, int row_len, int complement,
+                      uint8_t* out, void* stream);
+
 /* ---- (2) dominance classification: classify.py:99-148, 187-249 --------- */
 /* tcgen05 int8 tensor-core classifier.  A: s8 [S x ld_a] thermometer samples;
  * B_lower / B_upper: s8 [rows x ld_b] thermometer refs (rows multiple of 128,
@@ -142,11 +151,19 @@ int rsr_compact(const uint8_t* labels, int64_t S, int label, int64_t* out_idx,
 int rsr_violation_counts(const uint8_t* samples, int64_t H, const uint8_t* refs,
                          int64_t R, int n_components, int side, int32_t* out,
                          void* stream);
+/* same on flattened binary rows for any EncodedBatch content:
+ * out[h,r] = sum_j s[h,j] & (1 - r[r,j])  (classify.py:42-49). */
+int rsr_violation_counts_rows(const uint8_t* sample_rows, int64_t H,
+                              const uint8_t* ref_rows, int64_t R, int row_len,
+                              int32_t* out, void* stream);
 
 /* ---- (3) batched Phi: model.py:88-97 -> sysfn.py:79-185 ------------------ */
-/* out[i] = Phi(states[idx[i]]) (idx NULL: rows 0..count-1). */
+/* out[i] = Phi(states[idx[i]]) (idx NULL: rows 0..count-1; out may be NULL).
+ * count_leq (int64 [1] or NULL) += #{i : Phi <= threshold} -- the Stage-2
+ * resolution count of workflow.py:229-233. */
 int rsr_phi_eval(const rsr_phi_desc* phi, const uint8_t* states,
-                 const int64_t* idx, int64_t count, uint8_t* out, void* stream);
+                 const int64_t* idx, int64_t count, uint8_t* out, int threshold,
+                 int64_t* count_leq, void* stream);
 
 /* ---- (4) batched boundary search + reference insertion ------------------ */
 /* boundary.py:116-147, one warp per start vector. out_side: RSR_SIDE_*;
@@ -160,8 +177,10 @@ int rsr_gather_rows(const uint8_t* states, int n_components, const int64_t* idx,
 /* boundary.py:50-54 / 87-108 dominance scan of B candidates against K members:
  * covered[c] = 1 if some member makes candidate c redundant,
  * covers[c]  = 1 if candidate c makes some member redundant,
- * member_mask (u8 [K], may be NULL): 1 where candidate `mask_candidate`
- * makes the member redundant. */
+ * member_mask (may be NULL): with mask_candidate >= 0, u8 [K] = 1 where that
+ * candidate makes the member redundant; with mask_candidate < 0, the full
+ * relation u8 [B x K]: bit0 = member redundant under candidate, bit1 =
+ * candidate redundant under member. */
 int rsr_dominance_scan(const uint8_t* cands, int64_t B, const uint8_t* members,
                        int64_t K, int n_components, int side, uint8_t* covered,
                        uint8_t* covers, int mask_candidate, uint8_t* member_mask,

@@ -60,6 +60,8 @@ EXPORTED = {
     "rsr_sample": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
     "rsr_encode_samples": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "rsr_encode_refs": (_I, [_P, _I64, _I64, _I, _I, _I, _P, _I, _P]),
+    "rsr_encode_rows": (_I, [_P, _I64, _I, _I, _I, _P, _P]),
+    "rsr_packbits_rows": (_I, [_P, _I64, _I, _I, _P, _P]),
     "rsr_classify_tc": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _I, _P]),
     "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_classify_bits": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
@@ -67,7 +69,8 @@ EXPORTED = {
     "rsr_compact_scratch": (_I64, [_I64]),
     "rsr_compact": (_I, [_P, _I64, _I, _P, _P, _P, _P]),
     "rsr_violation_counts": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P]),
-    "rsr_phi_eval": (_I, [ctypes.POINTER(PhiDesc), _P, _P, _I64, _P, _P]),
+    "rsr_violation_counts_rows": (_I, [_P, _I64, _P, _I64, _I, _P, _P]),
+    "rsr_phi_eval": (_I, [ctypes.POINTER(PhiDesc), _P, _P, _I64, _P, _I, _P, _P]),
     "rsr_boundary_search": (_I, [ctypes.POINTER(PhiDesc), _I, _P, _I64, _P, _P, _P, _P]),
     "rsr_gather_rows": (_I, [_P, _I, _P, _I64, _P, _P]),
     "rsr_dominance_scan": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P, _I, _P, _P]),

@@ -1,0 +1,265 @@
+"""(2)+(5) Dominance classification and estimates (mirror of reference ``classify.py``).
+
+``classify`` keeps the reference signature and semantics (classify.py:187-249):
+lower takes precedence over upper, ``strict`` raises on overlap,
+``explain`` records the first matching reference per sample.  The work is
+done on the device:
+
+* default (``method="tc"``): ``rsr_classify_tc`` -- thermometer-encoded int8
+  contraction on tcgen05 tensor cores with the any-zero epilogue fused, the
+  S x K violation matrix never materialised;
+* ``method="bits"`` (and whenever first-match indices are needed):
+  ``rsr_classify_bits`` -- bit-packed AND/OR-reduce on CUDA cores;
+* then ``rsr_finalize`` (labels + counts) and, lazily, ``rsr_compact``
+  (order-preserving index arrays, np.flatnonzero semantics).
+
+``chunk_size`` and ``n_workers`` are accepted for API compatibility; the
+results are invariant to them as in the reference (the device kernels tile
+internally).
+"""
+
+from __future__ import annotations
+
+import math
+from typing import TYPE_CHECKING
+
+import numpy as np
+import torch
+
+from . import _abi, _device
+from .boundary import ReferenceSet, Side
+from .encoding import EncodedBatch
+from .sampling import SampleBatch
+
+if TYPE_CHECKING:  # pragma: no cover
+    pass
+
+__all__ = ["ClassificationResult", "InconsistentReferenceSets", "violation_counts", "classify",
+           "cov", "DEFAULT_CHUNK_SIZE", "classify_flags"]
+
+DEFAULT_CHUNK_SIZE = 65536
+
+
+class InconsistentReferenceSets(ValueError):
+    """A sample matched both a lower and an upper reference in strict mode."""
+
+
+def violation_counts(samples: EncodedBatch, refs: EncodedBatch, chunk_size: int = DEFAULT_CHUNK_SIZE,
+                     method: str = "packed") -> np.ndarray:
+    """Full H x R violation matrix (classify.py:57-96), ``rsr_violation_counts_rows``."""
+    if samples.kind != "sample":
+        raise ValueError("samples batch must have kind='sample'")
+    if refs.kind not in ("lower_ref", "upper_ref"):
+        raise ValueError("refs batch must have kind 'lower_ref' or 'upper_ref'")
+    if (samples.n_components, samples.n_states) != (refs.n_components, refs.n_states):
+        raise ValueError("samples and refs must share N and M")
+    if len(refs) == 0:
+        raise ValueError("refs batch is empty")
+    if chunk_size < 1:
+        raise ValueError("chunk_size must be >= 1")
+    if method not in ("packed", "unpacked"):
+        raise ValueError("method must be 'packed' or 'unpacked'")
+    h, r = len(samples), len(refs)
+    out = torch.empty((max(h, 1), r), dtype=torch.int32, device=_device.device())
+    if h:
+        _abi.call("rsr_violation_counts_rows", _abi.ptr(samples.device_rows()), h,
+                  _abi.ptr(refs.device_rows()), r, samples.data.shape[1], _abi.ptr(out),
+                  _device.stream())
+    return out[:h].cpu().numpy()
+
+
+class ClassificationResult:
+    """Partition of sample indices plus probability estimates (classify.py:151-184).
+
+    Counts are host integers; the index arrays are compacted on the device
+    and copied to the host on first access.
+    """
+
+    def __init__(self, lower_indices=None, upper_indices=None, unclassified_indices=None,
+                 n_samples: int = 0, first_match_lower=None, first_match_upper=None, *,
+                 counts: tuple[int, int, int] | None = None, labels: torch.Tensor | None = None):
+        self.n_samples = int(n_samples)
+        self.first_match_lower = first_match_lower
+        self.first_match_upper = first_match_upper
+        self._labels = labels
+        self._idx = {0: lower_indices, 1: upper_indices, 2: unclassified_indices}
+        if counts is None:
+            counts = tuple(int(np.asarray(self._idx[k]).size) for k in range(3))
+        self.counts = tuple(int(c) for c in counts)
+        self._dev_idx: dict[int, torch.Tensor] = {}
+
+    @property
+    def labels_device(self) -> torch.Tensor | None:
+        """uint8 labels on the device: 0 lower, 1 upper, 2 unclassified."""
+        return self._labels
+
+    def indices_device(self, label: int) -> torch.Tensor:
+        """Sorted int64 indices with the given label, compacted on the device."""
+        t = self._dev_idx.get(label)
+        if t is None:
+            if self._labels is None:
+                t = _device.to_device(np.asarray(self._idx[label], dtype=np.int64))
+            else:
+                n = self.counts[label]
+                S = self.n_samples
+                t = torch.empty(max(n, 1), dtype=torch.int64, device=self._labels.device)
+                cnt = torch.empty(1, dtype=torch.int64, device=self._labels.device)
+                scratch = torch.empty(_abi.call("rsr_compact_scratch", S), dtype=torch.int64,
+                                      device=self._labels.device)
+                _abi.call("rsr_compact", _abi.ptr(self._labels), S, label, _abi.ptr(t), _abi.ptr(cnt),
+                          _abi.ptr(scratch), _device.stream())
+                t = t[:n]
+            self._dev_idx[label] = t
+        return t
+
+    def _host(self, label: int) -> np.ndarray:
+        v = self._idx[label]
+        if v is None:
+            v = self.indices_device(label).cpu().numpy()
+            self._idx[label] = v
+        return np.asarray(v)
+
+    @property
+    def lower_indices(self) -> np.ndarray:
+        return self._host(0)
+
+    @property
+    def upper_indices(self) -> np.ndarray:
+        return self._host(1)
+
+    @property
+    def unclassified_indices(self) -> np.ndarray:
+        return self._host(2)
+
+    @property
+    def p_lower(self) -> float:
+        return self.counts[0] / self.n_samples
+
+    @property
+    def p_upper(self) -> float:
+        return self.counts[1] / self.n_samples
+
+    @property
+    def p_unclassified(self) -> float:
+        return self.counts[2] / self.n_samples
+
+    @property
+    def cov_lower(self) -> float | None:
+        return cov(self.p_lower, self.n_samples)
+
+    @property
+    def cov_upper(self) -> float | None:
+        return cov(self.p_upper, self.n_samples)
+
+
+def _infer_n_states(batch: SampleBatch, lower_set, upper_set) -> int:
+    """Largest state in samples or refs + 1 (classify.py:252-262)."""
+    if batch._host is not None:
+        top = int(batch._host.max(initial=0))
+    else:
+        top = int(batch.device_states().max().item()) if batch.n_samples else 0
+    for s in (lower_set, upper_set):
+        if s is not None and len(s):
+            top = max(top, s.max_state)
+    return top + 1
+
+
+def _check_range(batch: SampleBatch, sets, n_states: int) -> None:
+    """encode_batch's range check (encoding.py:35-39) without a host copy when avoidable."""
+    if batch.state_bound > n_states:
+        top = (int(batch._host.max(initial=0)) if batch._host is not None
+               else int(batch.device_states().max().item()))
+        if top >= n_states:
+            raise ValueError(f"states must lie in [0, {n_states - 1}]")
+    for s in sets:
+        if s is not None and len(s) and s.max_state >= n_states:
+            raise ValueError(f"states must lie in [0, {n_states - 1}]")
+
+
+def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
+                   upper_set: ReferenceSet | None, n_states: int, method: str = "tc",
+                   flags: torch.Tensor | None = None, want_first: bool = False):
+    """Run one classifier; returns (flags[u8 H], first_lower, first_upper) on device."""
+    H = batch.n_samples
+    dev = _device.device()
+    if flags is None:
+        flags = torch.empty(H, dtype=torch.uint8, device=dev)
+    m_eff = max(2, n_states, batch.state_bound)
+    fl = fu = None
+    st = _device.stream()
+    if method == "tc" and not want_first:
+        a = batch.thermo(m_eff)
+        bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
+        bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
+        _abi.call("rsr_classify_tc", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu), nu,
+                  a.shape[1], _abi.ptr(flags), 0, st)
+    elif method in ("bits", "tc"):
+        sb = batch.thermo_bits(m_eff)
+        lb, nl = lower_set.device_bits(m_eff) if lower_set is not None else (None, 0)
+        ub, nu = upper_set.device_bits(m_eff) if upper_set is not None else (None, 0)
+        if want_first:
+            fl = torch.empty(H, dtype=torch.int64, device=dev)
+            fu = torch.empty(H, dtype=torch.int64, device=dev)
+        _abi.call("rsr_classify_bits", _abi.ptr(sb), H, _abi.ptr(lb), nl, _abi.ptr(ub), nu,
+                  sb.shape[1], _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
+    else:
+        raise ValueError("method must be 'tc' or 'bits'")
+    return flags, fl, fu
+
+
+def classify(batch: SampleBatch, lower_set: ReferenceSet | None, upper_set: ReferenceSet | None,
+             chunk_size: int = DEFAULT_CHUNK_SIZE, n_workers: int = 1, strict: bool = False,
+             explain: bool = False, n_states: int | None = None, *,
+             method: str = "tc") -> ClassificationResult:
+    """Partition a sample batch against lower and upper reference sets (classify.py:187-249)."""
+    if lower_set is not None and upper_set is not None:
+        if lower_set.threshold != upper_set.threshold:
+            raise ValueError(f"threshold mismatch: lower m'={lower_set.threshold}, "
+                             f"upper m'={upper_set.threshold}")
+    if lower_set is not None and lower_set.side != Side.LOWER:
+        raise ValueError("lower_set must have side 'lower'")
+    if upper_set is not None and upper_set.side != Side.UPPER:
+        raise ValueError("upper_set must have side 'upper'")
+    if not isinstance(batch, SampleBatch):
+        raise TypeError("batch must be a SampleBatch")
+    for s in (lower_set, upper_set):
+        if s is not None and len(s) and s._width != batch.n_components:
+            raise ValueError("reference vectors and samples must share N")
+    H = batch.n_samples
+    if n_states is None:
+        n_states = _infer_n_states(batch, lower_set, upper_set)
+    else:
+        _check_range(batch, (lower_set, upper_set), n_states)
+    want_first = bool(explain or strict)
+    flags, fl, fu = classify_flags(batch, lower_set, upper_set, n_states, method,
+                                   want_first=want_first)
+    dev = flags.device
+    labels = torch.empty(H, dtype=torch.uint8, device=dev)
+    counts_d = torch.empty(4, dtype=torch.int64, device=dev)
+    _abi.call("rsr_finalize", _abi.ptr(flags), H, _abi.ptr(labels), _abi.ptr(counts_d),
+              _device.stream())
+    counts = counts_d.cpu().tolist()
+    if strict and counts[3] > 0:
+        idx = torch.empty(counts[3], dtype=torch.int64, device=dev)
+        cnt = torch.empty(1, dtype=torch.int64, device=dev)
+        scratch = torch.empty(_abi.call("rsr_compact_scratch", H), dtype=torch.int64, device=dev)
+        _abi.call("rsr_compact", _abi.ptr(flags), H, _abi.HIT_LOWER | _abi.HIT_UPPER, _abi.ptr(idx),
+                  _abi.ptr(cnt), _abi.ptr(scratch), _device.stream())
+        first = int(idx[0].item())
+        raise InconsistentReferenceSets(
+            f"sample {first} matches both a lower and an upper reference")
+    return ClassificationResult(
+        n_samples=H, counts=(counts[0], counts[1], counts[2]), labels=labels,
+        first_match_lower=fl.cpu().numpy() if (explain and fl is not None) else None,
+        first_match_upper=fu.cpu().numpy() if (explain and fu is not None) else None)
+
+
+def cov(p_hat: float, n_samples: int) -> float | None:
+    """sqrt((1 - p) / (H p)); None at p = 0 (classify.py:265-277)."""
+    if n_samples < 1:
+        raise ValueError("n_samples must be >= 1")
+    if not 0.0 <= p_hat <= 1.0:
+        raise ValueError("p_hat must lie in [0, 1]")
+    if p_hat == 0.0:
+        return None
+    return math.sqrt((1.0 - p_hat) / (n_samples * p_hat))

@@ -226,6 +226,19 @@ __global__ void violation_kernel(const uint8_t* __restrict__ xs, int64_t H,
   out[h * R + r] = v;
 }
 
+__global__ void violation_rows_kernel(const uint8_t* __restrict__ xs, int64_t H,
+                                      const uint8_t* __restrict__ rs, int64_t R, int L,
+                                      int32_t* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t h = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  if (r >= R || h >= H) return;
+  const uint8_t* x = xs + h * L;
+  const uint8_t* ref = rs + r * L;
+  int v = 0;
+  for (int j = 0; j < L; ++j) v += (x[j] != 0) & (ref[j] == 0);
+  out[h * R + r] = v;
+}
+
 template <int W>
 int launch_bits(const uint32_t* sb, int64_t S, const uint32_t* lb, int64_t nl, const uint32_t* ub,
                 int64_t nu, uint8_t* flags, int64_t* fl, int64_t* fu, int acc, cudaStream_t st) {
@@ -324,4 +337,16 @@ extern "C" int rsr_violation_counts(const uint8_t* samples, int64_t H, const uin
   violation_kernel<<<grid, 128, 0, rsr::as_stream(stream)>>>(samples, H, refs, R, n_components,
                                                              side, out);
   return rsr::check_launch("violation_kernel");
+}
+
+extern "C" int rsr_violation_counts_rows(const uint8_t* sample_rows, int64_t H,
+                                         const uint8_t* ref_rows, int64_t R, int row_len,
+                                         int32_t* out, void* stream) {
+  RSR_REQUIRE(H >= 0 && R >= 0 && row_len >= 0, "rsr_violation_counts_rows: bad shape");
+  if (H == 0 || R == 0) return RSR_OK;
+  dim3 grid((unsigned)rsr::ceil_div(R, 128), (unsigned)(H < 65535 ? H : 65535),
+            (unsigned)rsr::ceil_div(H, 65535));
+  violation_rows_kernel<<<grid, 128, 0, rsr::as_stream(stream)>>>(sample_rows, H, ref_rows, R,
+                                                                  row_len, out);
+  return rsr::check_launch("violation_rows_kernel");
 }

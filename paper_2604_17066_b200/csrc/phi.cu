@@ -131,7 +131,8 @@ __host__ __device__ inline size_t phi_smem_bytes(const rsr_phi_desc& d) {
 
 __global__ void __launch_bounds__(kWarps * 32)
 phi_eval_kernel(const rsr_phi_desc d, const uint8_t* __restrict__ states,
-                const int64_t* __restrict__ idx, int64_t count, uint8_t* __restrict__ out) {
+                const int64_t* __restrict__ idx, int64_t count, uint8_t* __restrict__ out,
+                int threshold, unsigned long long* count_leq) {
   extern __shared__ uint8_t smem[];
   int32_t* tail;
   const Phi f = load_phi(d, smem, &tail);
@@ -139,6 +140,7 @@ phi_eval_kernel(const rsr_phi_desc d, const uint8_t* __restrict__ states,
   const size_t per_warp = ((size_t)f.N + f.n_nodes + 15) / 16 * 16;
   volatile uint8_t* x = reinterpret_cast<uint8_t*>(tail) + warp * per_warp;
   volatile uint8_t* reach = x + f.N;
+  unsigned long long leq = 0;
   for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < count;
        i += (int64_t)gridDim.x * kWarps) {
     const int64_t row = idx ? idx[i] : i;
@@ -146,9 +148,11 @@ phi_eval_kernel(const rsr_phi_desc d, const uint8_t* __restrict__ states,
     for (int e = lane; e < f.N; e += 32) x[e] = src[e];
     __syncwarp();
     const int v = phi_warp(f, x, reach, lane);
-    if (lane == 0) out[i] = (uint8_t)v;
+    if (lane == 0 && out) out[i] = (uint8_t)v;
+    leq += (v <= threshold);
     __syncwarp();
   }
+  if (count_leq && lane == 0 && leq) atomicAdd(count_leq, leq);
 }
 
 __global__ void __launch_bounds__(kWarps * 32)
@@ -228,10 +232,16 @@ __global__ void dominance_kernel(const uint8_t* __restrict__ cands, int64_t B,
   if (m >= K || c >= B) return;
   const uint8_t* cv = cands + c * N;
   const uint8_t* mv = members + m * N;
-  if (covered && redundant_under(side, cv, mv, N)) covered[c] = 1;
+  const bool red = redundant_under(side, cv, mv, N);
+  if (covered && red) covered[c] = 1;
   const bool dropped = redundant_under(side, mv, cv, N);
   if (covers && dropped) covers[c] = 1;
-  if (member_mask && c == mask_c) member_mask[m] = dropped ? 1 : 0;
+  if (member_mask) {
+    if (mask_c < 0)  // full relation matrix [B x K]
+      member_mask[c * K + m] = (uint8_t)((dropped ? 1 : 0) | (red ? 2 : 0));
+    else if (c == mask_c)
+      member_mask[m] = dropped ? 1 : 0;
+  }
 }
 
 int check_phi(const rsr_phi_desc* d) {
@@ -270,7 +280,8 @@ int grid_for(int64_t items) {
 }  // namespace
 
 extern "C" int rsr_phi_eval(const rsr_phi_desc* phi, const uint8_t* states, const int64_t* idx,
-                            int64_t count, uint8_t* out, void* stream) {
+                            int64_t count, uint8_t* out, int threshold, int64_t* count_leq,
+                            void* stream) {
   int rc = check_phi(phi);
   if (rc) return rc;
   RSR_REQUIRE(count >= 0, "rsr_phi_eval: negative count");
@@ -280,7 +291,8 @@ extern "C" int rsr_phi_eval(const rsr_phi_desc* phi, const uint8_t* states, cons
     RSR_CUDA(cudaFuncSetAttribute(phi_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   phi_eval_kernel<<<grid_for(count), kWarps * 32, smem, rsr::as_stream(stream)>>>(
-      *phi, states, idx, count, out);
+      *phi, states, idx, count, out, threshold,
+      reinterpret_cast<unsigned long long*>(count_leq));
   return rsr::check_launch("phi_eval_kernel");
 }
 

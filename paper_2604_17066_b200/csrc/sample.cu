@@ -156,7 +156,60 @@ __global__ void encode_refs_kernel(const uint8_t* __restrict__ states, int64_t c
   }
 }
 
+// encoding.py:138-153 row layout: row-major N x M per item.
+__global__ void encode_rows_kernel(const uint8_t* __restrict__ states, int64_t count, int N, int M,
+                                   int kind, uint8_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t L = (int64_t)N * M;
+  if (t >= count * L) return;
+  const int64_t i = t / L;
+  const int j = (int)(t - i * L);
+  const int n = j / M, m = j - n * M;
+  const int x = states[i * N + n];
+  out[t] = (uint8_t)(kind == 0 ? (m == x) : kind == 1 ? (m <= x) : (m >= x));
+}
+
+// np.packbits(axis=1): byte b holds bits 8b..8b+7, MSB first, zero padded.
+__global__ void packbits_kernel(const uint8_t* __restrict__ rows, int64_t count, int L, int comp,
+                                uint8_t* __restrict__ out) {
+  const int nbytes = (L + 7) / 8;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * nbytes) return;
+  const int64_t i = t / nbytes;
+  const int b = (int)(t - i * nbytes);
+  const uint8_t* r = rows + i * L;
+  unsigned v = 0;
+  for (int q = 0; q < 8; ++q) {
+    const int j = 8 * b + q;
+    unsigned bit = 0;
+    if (j < L) bit = comp ? (r[j] == 0) : (r[j] != 0);
+    v |= bit << (7 - q);
+  }
+  out[t] = (uint8_t)v;
+}
+
 }  // namespace
+
+extern "C" int rsr_encode_rows(const uint8_t* states, int64_t count, int n_components,
+                               int n_states, int kind, uint8_t* out, void* stream) {
+  RSR_REQUIRE(n_components >= 1 && n_states >= 1 && count >= 0, "rsr_encode_rows: bad shape");
+  RSR_REQUIRE(kind >= 0 && kind <= 2, "rsr_encode_rows: kind must be 0, 1 or 2");
+  const int64_t total = count * n_components * n_states;
+  if (total == 0) return RSR_OK;
+  encode_rows_kernel<<<(unsigned)rsr::ceil_div(total, kThreads), kThreads, 0,
+                       rsr::as_stream(stream)>>>(states, count, n_components, n_states, kind, out);
+  return rsr::check_launch("encode_rows_kernel");
+}
+
+extern "C" int rsr_packbits_rows(const uint8_t* rows, int64_t count, int row_len, int complement,
+                                 uint8_t* out, void* stream) {
+  RSR_REQUIRE(row_len >= 0 && count >= 0, "rsr_packbits_rows: bad shape");
+  const int64_t total = count * ((row_len + 7) / 8);
+  if (total == 0) return RSR_OK;
+  packbits_kernel<<<(unsigned)rsr::ceil_div(total, kThreads), kThreads, 0,
+                    rsr::as_stream(stream)>>>(rows, count, row_len, complement, out);
+  return rsr::check_launch("packbits_kernel");
+}
 
 extern "C" int rsr_philox_raw(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
                               uint64_t* out, void* stream) {

@@ -1,0 +1,152 @@
+"""(1) Device-resident Monte Carlo batches (mirror of reference ``sampling.py``).
+
+``sample_batch`` runs ``rsr_sample``: numpy-compatible Philox4x64-10 keyed by
+(seed, generation_index), flat draw index (start+i)*N + n, inverse CDF on the
+cumulative probabilities (sampling.py:39-90), bit-exact with the reference.
+The kernel writes the uint8 state matrix and, fused, the int8 thermometer
+rows that feed the tensor-core classifier.  The batch stays in HBM; the
+host ``states`` array (int64, as in the reference) is materialised lazily.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _abi, _device
+from .model import ComponentDistribution
+
+__all__ = ["SampleBatch", "sample_batch", "uniform_field"]
+
+
+class SampleBatch:
+    """H component-state vectors plus the keys that regenerate them (sampling.py:22-36).
+
+    ``states`` may be a host array (any integer dtype) or a CUDA uint8 tensor.
+    """
+
+    def __init__(self, states, seed: int, generation_index: int, *, state_bound: int | None = None):
+        self.seed = int(seed)
+        self.generation_index = int(generation_index)
+        self._host: np.ndarray | None = None
+        self._dev: torch.Tensor | None = None
+        self._thermo: dict[int, torch.Tensor] = {}
+        self._bits: dict[int, torch.Tensor] = {}
+        if isinstance(states, torch.Tensor):
+            if states.dim() != 2:
+                raise ValueError("states must be an H x N matrix")
+            self._dev = states
+            self._shape = tuple(states.shape)
+            self._bound = state_bound
+        else:
+            arr = np.asarray(states)
+            if arr.ndim != 2:
+                raise ValueError("states must be an H x N matrix")
+            self._host = arr
+            self._shape = arr.shape
+            self._bound = state_bound
+            if self._bound is None and arr.size:
+                if arr.min() < 0:
+                    raise ValueError("states must be non-negative")
+                self._bound = int(arr.max()) + 1
+
+    # -- reference API -----------------------------------------------------
+    @property
+    def states(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._dev.cpu().numpy().astype(np.int64)
+        return self._host
+
+    @property
+    def n_samples(self) -> int:
+        return self._shape[0]
+
+    @property
+    def n_components(self) -> int:
+        return self._shape[1]
+
+    # -- device views ------------------------------------------------------
+    @property
+    def state_bound(self) -> int:
+        """Exclusive upper bound of the states (M of the sampler, or max+1)."""
+        if self._bound is None:
+            self._bound = int(self.device_states().max().item()) + 1 if self.n_samples else 1
+        return self._bound
+
+    def device_states(self) -> torch.Tensor:
+        if self._dev is None:
+            arr = self._host
+            if arr.size and (arr.min() < 0 or arr.max() > 255):
+                raise ValueError("device states must lie in [0, 255]")
+            self._dev = _device.to_device(arr.astype(np.uint8, copy=False))
+        return self._dev
+
+    def thermo(self, n_states: int) -> torch.Tensor:
+        """int8 thermometer rows [H, Kpad] (A operand of the classifier), cached per M."""
+        t = self._thermo.get(n_states)
+        if t is None:
+            n = self.n_components
+            kpad = _abi.thermo_kpad(n, n_states)
+            st = self.device_states()
+            t = torch.empty((self.n_samples, kpad), dtype=torch.int8, device=st.device)
+            _abi.call("rsr_encode_samples", _abi.ptr(st), self.n_samples, n, n_states,
+                      _abi.ptr(t), kpad, _device.stream())
+            self._thermo[n_states] = t
+        return t
+
+    def thermo_bits(self, n_states: int) -> torch.Tensor:
+        """Packed thermometer bits [H, words] (bit-packed classifier operand)."""
+        t = self._bits.get(n_states)
+        if t is None:
+            n = self.n_components
+            w = _abi.thermo_words(n, n_states)
+            st = self.device_states()
+            t = torch.empty((max(1, self.n_samples), w), dtype=torch.int32, device=st.device)
+            _abi.call("rsr_pack_thermo_bits", _abi.ptr(st), self.n_samples, n, n_states, 0,
+                      _abi.ptr(t), w, _device.stream())
+            self._bits[n_states] = t
+        return t
+
+    def release_thermo(self) -> None:
+        self._thermo.clear()
+        self._bits.clear()
+
+
+def uniform_field(seed: int, generation_index: int, start: int, count: int,
+                  n_components: int) -> np.ndarray:
+    """Uniform(0,1) field of samples [start, start+count) (sampling.py:45-66), on device."""
+    out = torch.empty((count, n_components), dtype=torch.float64, device=_device.device())
+    mask = (1 << 64) - 1
+    _abi.call("rsr_uniform_field", seed & mask, generation_index & mask, start, count,
+              n_components, _abi.ptr(out), _device.stream())
+    return out.cpu().numpy()
+
+
+def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
+                 generation_index: int = 0, start: int = 0, *, encode: bool = True,
+                 out_states: torch.Tensor | None = None,
+                 out_thermo: torch.Tensor | None = None) -> SampleBatch:
+    """Inverse-CDF draw on the counter-based stream (sampling.py:69-90), on device.
+
+    ``encode`` also writes the thermometer rows for M = dist.n_states in the
+    same kernel.  ``out_*`` let callers reuse preallocated buffers.
+    """
+    if n_samples < 1:
+        raise ValueError("n_samples must be >= 1")
+    n, m = dist.n_components, dist.n_states
+    dev = _device.device()
+    states = out_states if out_states is not None else torch.empty(
+        (n_samples, n), dtype=torch.uint8, device=dev)
+    thermo = None
+    kpad = _abi.thermo_kpad(n, m)
+    if encode:
+        thermo = out_thermo if out_thermo is not None else torch.empty(
+            (n_samples, kpad), dtype=torch.int8, device=dev)
+    mask = (1 << 64) - 1
+    _abi.call("rsr_sample", _abi.ptr(dist.device_probs()), n, m, seed & mask,
+              generation_index & mask, start, n_samples, _abi.ptr(states), _abi.ptr(thermo),
+              kpad, _device.stream())
+    batch = SampleBatch(states, seed, generation_index, state_bound=m)
+    if thermo is not None:
+        batch._thermo[m] = thermo
+    return batch

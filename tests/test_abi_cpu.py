@@ -1,0 +1,59 @@
+"""The C-ABI library loads without a GPU and exports every declared entry point."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2604_17066_b200 import _abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rsr_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(rsr_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_expected_surface():
+    names = _declared()
+    assert "rsr_classify_tc" in names and "rsr_sample" in names and "rsr_boundary_search" in names
+    assert set(names) == set(_abi.EXPORTED), set(names) ^ set(_abi.EXPORTED)
+
+
+def test_library_loads_and_exports_every_symbol():
+    if not os.path.exists(_abi.LIB_PATH):
+        pytest.fail("librsr_b200.so not built; run __graft_entry__.build()")
+    lib = _abi.lib()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert lib.rsr_version() == 1
+    assert lib.rsr_thermo_kpad(295, 2) == _abi.thermo_kpad(295, 2) == 320
+    assert lib.rsr_thermo_kpad(295, 3) == _abi.thermo_kpad(295, 3) == 608
+    assert lib.rsr_thermo_kpad(40, 2) == 64
+
+
+def test_bad_arguments_fail_before_any_device_work():
+    lib = _abi.lib()
+    # argument validation happens on the host side of the ABI: no GPU needed
+    with pytest.raises(ValueError, match="n_samples"):
+        _abi.call("rsr_sample", None, 4, 2, 0, 0, 0, 0, None, None, 0, None)
+    with pytest.raises(ValueError, match="Kpad"):
+        _abi.call("rsr_classify_tc", None, 10, None, 0, None, 0, 48, None, 0, None)
+    with pytest.raises(ValueError):
+        _abi.call("rsr_encode_rows", None, 1, 3, 2, 7, None, None)
+    assert lib.rsr_last_error()
+
+
+def test_shared_object_is_sm100a_only():
+    # the fatbin must carry sm_100a SASS (cuobjdump lists the ELF arch)
+    import shutil
+    import subprocess
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run(["cuobjdump", "--list-elf", _abi.LIB_PATH], capture_output=True, text=True)
+    archs = set(re.findall(r"sm_\d+a?", out.stdout))
+    assert archs == {"sm_100a"}, archs

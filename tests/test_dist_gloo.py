@@ -1,0 +1,70 @@
+"""World-size-2 gloo run of the sharding/exchange logic (CPU)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2604_17066_b200.dist import Comm, global_pick_owners, shard_range
+    import oracle
+    comm = Comm.from_env(backend="gloo")
+    H, N = 1001, 7
+    probs = np.tile([0.3, 0.7], (N, 1))
+    start, count = shard_range(H, world, rank)
+    # each rank draws its shard of the same stream with the oracle sampler
+    xs = oracle.sample_states(probs, count, seed=5, generation_index=2, start=start)
+    unc = np.flatnonzero(xs.sum(1) <= 3)  # stand-in "unclassified" predicate
+    counts = comm.allreduce_sum_i64([len(unc), count])
+    per = comm.allgather_i64(len(unc))
+    total = int(per.sum())
+    pos = np.random.default_rng([5, 2]).choice(total, size=min(6, total), replace=False)
+    owner, local = global_pick_owners(per, pos)
+    mine = np.flatnonzero(owner == comm.rank)
+    rows = torch.as_tensor(xs[unc[local[mine]]].astype(np.uint8))
+    gathered = comm.allgather_rows(rows, np.bincount(owner, minlength=world))
+    order = np.argsort(owner, kind="stable")
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order))
+    picked = gathered[torch.as_tensor(inv)].numpy()
+    flags = torch.tensor([rank % 2, 1 - rank % 2], dtype=torch.uint8)
+    orf = comm.allreduce_max_u8(flags).tolist()
+    q.put((rank, counts.tolist(), picked.tolist(), orf))
+    import torch.distributed as dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_two_rank_sharding_matches_single_process():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=100) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=30)
+    import oracle
+    xs = oracle.sample_states(np.tile([0.3, 0.7], (7, 1)), 1001, seed=5, generation_index=2)
+    unc = np.flatnonzero(xs.sum(1) <= 3)
+    pos = np.random.default_rng([5, 2]).choice(len(unc), size=min(6, len(unc)), replace=False)
+    want = xs[unc[pos]].tolist()
+    for rank, counts, picked, orf in out:
+        assert counts == [len(unc), 1001]
+        assert picked == want  # every rank sees the picks in single-process order
+        assert orf == [1, 1]

@@ -133,10 +133,11 @@ def test_first_match_and_violation_counts():
     flags, fl, fu = _classify_bits(samples, refs, refs, n, m, first=True)
     r = oracle.classify_labels(samples, refs, refs, m, want_first=True)
     assert np.array_equal(fl, r["first_lower"]) and np.array_equal(fu, r["first_upper"])
+    sd, rd = _dev(samples.astype(np.uint8)), _dev(refs.astype(np.uint8))  # keep both alive
     for side, kind in ((A.SIDE_LOWER, "lower_ref"), (A.SIDE_UPPER, "upper_ref")):
         out = torch.empty((500, 200), dtype=torch.int32, device="cuda")
-        A.call("rsr_violation_counts", A.ptr(_dev(samples.astype(np.uint8))), 500,
-               A.ptr(_dev(refs.astype(np.uint8))), 200, n, side, A.ptr(out), A.stream_ptr())
+        A.call("rsr_violation_counts", A.ptr(sd), 500, A.ptr(rd), 200, n, side, A.ptr(out),
+               A.stream_ptr())
         assert np.array_equal(out.cpu().numpy(), oracle.violation_counts(samples, refs, m, kind))
 
 
@@ -194,7 +195,8 @@ def test_phi_eval_and_boundary(kind, m):
         ref = oracle.phi_global(nn, edges)
     want = np.array([ref(x) for x in xs])
     out = torch.empty(2000, dtype=torch.uint8, device="cuda")
-    A.call("rsr_phi_eval", A.ctypes.byref(d), A.ptr(_dev(xs.astype(np.uint8))), None, 2000, A.ptr(out),
+    xd = _dev(xs.astype(np.uint8))
+    A.call("rsr_phi_eval", A.ctypes.byref(d), A.ptr(xd), None, 2000, A.ptr(out), 0, None,
            A.stream_ptr())
     assert np.array_equal(out.cpu().numpy(), want)
     ms = m if kind == A.PHI_WIDEST else 2
