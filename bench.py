@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the RSR dominance-classification hot path on B200.
+
+Default workload (BASELINE.json configs[1], "cfg2"): S = 2^20 samples x
+N = 295 binary components (Bernoulli(0.9) via the device Philox sampler),
+K = 10^4 upper refs (15 ones) + 10^4 lower refs (10 zeros).  A step is one
+classification of the resident batch against all K refs: rsr_classify_tc
+(tcgen05 int8 thermometer contraction with fused any-zero epilogue) +
+rsr_finalize (labels + counts), plus an NCCL all-reduce of the counts when
+N > 1.  Metric: classified samples x reference states per second (pairs/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        bench.py --gpus N ...
+
+Other workloads for the profiles/ notes: --config cfg4 --k 500000 (path refs
+sweep), --config cfg1 / cfg3 (full RSR loop wall time).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "classified samples·ref-states/sec"
+UNIT = "pairs/s"
+N_COMP = 295
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="cfg2", choices=["cfg2", "cfg2_mixed", "cfg4"])
+    p.add_argument("--k", type=int, default=10_000, help="refs per side (cfg2) / path refs (cfg4)")
+    p.add_argument("--samples", type=int, default=None, help="samples per GPU")
+    p.add_argument("--method", choices=["tc", "bits"], default="tc")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------- workloads
+
+def workload(args):
+    """(p_survive, lower rows, upper rows, S, description) -- numpy only."""
+    from paper_2604_17066_b200 import workloads as W
+    if args.config == "cfg2":
+        lower, upper = W.cfg2_refs(0, N_COMP, args.k, args.k)
+        S = args.samples or (1 << 20)
+        desc = (f"cfg2: S=2^{int(np.log2(S))} x N=295 Bernoulli(0.9), K={len(upper)} upper "
+                f"(15 ones) + {len(lower)} lower (10 zeros)")
+        return 0.9, lower, upper, S, desc
+    if args.config == "cfg2_mixed":
+        lower, upper = W.cfg2_mixed_refs(0, N_COMP, args.k, args.k)
+        S = args.samples or (1 << 20)
+        return 0.5, lower, upper, S, f"cfg2-mixed: S={S}, p=0.5, 15-one upper / 14-zero lower"
+    g = W.cfg3(0)
+    upper = W.random_st_paths(g, args.k, seed=0)
+    lower = np.zeros((0, N_COMP), dtype=np.uint8)
+    S = args.samples or (1 << 22)
+    return 0.9, lower, upper, S, (f"cfg4: S={S} Bernoulli(0.9), K={len(upper)} s-t path refs "
+                                  f"(mean {upper.sum(1).mean():.1f} edges)")
+
+
+def cpu_classify_rate(p1, lower, upper, rows, seed=0):
+    """Reference algorithm (oracle port of classify.py:99-148) on host cores."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    probs = np.tile([1 - p1, p1], (N_COMP, 1))
+    xs = oracle.sample_states(probs, rows, seed, 0, 0)
+    chunk = max(256, rows // (4 * cores)) if cores > 1 else 65536
+    t0 = time.perf_counter()
+    oracle.classify_labels(xs, lower, upper, 2, chunk_size=chunk, n_workers=cores)
+    dt = time.perf_counter() - t0
+    return rows * (len(lower) + len(upper)) / dt, dt, cores, chunk
+
+
+def calibrated_cpu_rows(p1, lower, upper, target_s):
+    rate, _, _, _ = cpu_classify_rate(p1, lower, upper, 512)
+    pairs = rate * target_s
+    return int(max(512, min(1 << 18, pairs / max(1, len(lower) + len(upper)))))
+
+
+# ------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# -------------------------------------------------------------------- peaks
+
+def int8_peak_tops():
+    """Measured dense int8 GEMM throughput (cuBLASLt via torch._int_mm), best of 10.
+
+    MEASURED_PEAKS.json carries only the bf16 cuBLAS peak; this is the int8
+    counterpart measured the same way on the same box.  Falls back to
+    2 x bf16_tflops (int8 dense rate = 2 x bf16 on B200) if _int_mm fails.
+    """
+    import torch
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    try:
+        n = 8192
+        a = torch.randint(-8, 8, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-8, 8, (n, n), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = 0.0
+        for _ in range(10):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            torch._int_mm(a, b)
+            e.record()
+            e.synchronize()
+            best = max(best, 2 * n ** 3 / (s.elapsed_time(e) * 1e-3) / 1e12)
+        del a, b
+        return best, "measured: cuBLASLt int8 GEMM 8192^3 via torch._int_mm, best of 10 (burst)"
+    except Exception as exc:  # pragma: no cover
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        return 2 * bf16, f"2 x bf16_tflops of MEASURED_PEAKS.json ({exc.__class__.__name__})"
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu capture, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    p1, lower, upper, S, desc = workload(args)
+    rows = calibrated_cpu_rows(p1, lower, upper, 4.0)
+    for _ in range(args.warmup):
+        cpu_classify_rate(p1, lower, upper, rows, seed=1)
+    rates, times = [], []
+    cores = chunk = None
+    for k in range(args.steps):
+        r, dt, cores, chunk = cpu_classify_rate(p1, lower, upper, rows, seed=2 + k)
+        rates.append(r)
+        times.append(dt)
+    value = rows * (len(lower) + len(upper)) * args.steps / sum(times)
+    sample = (f"{rows} samples/step x {len(lower) + len(upper)} refs of {desc}; reference "
+              f"algorithm (oracle/core.py port of classify.py:99-148, packbits + bitwise_count, "
+              f"ThreadPool n_workers={cores}, chunk={chunk})")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": desc, "samples_per_step": rows,
+                       "ref_states": int(len(lower) + len(upper)), "n_components": N_COMP},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- ours
+
+def run_ours(args):
+    import torch
+
+    import paper_2604_17066_b200 as P
+    from paper_2604_17066_b200 import _abi
+    from paper_2604_17066_b200.dist import Comm
+
+    comm = Comm.from_env("nccl")
+    rank, world = comm.rank, comm.world
+    if world == 1:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p1, lower_rows, upper_rows, S, desc = workload(args)
+    lower = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower_rows, trusted=True)
+    upper = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper_rows, trusted=True)
+    K = len(lower) + len(upper)
+    dist = P.ComponentDistribution.iid(N_COMP, [1 - p1, p1])
+    batch = P.sample_batch(dist, S, seed=0, generation_index=0, start=rank * S)
+    A = batch.thermo(2)
+    bl, nl = lower.device_thermo(2)
+    bu, nu = upper.device_thermo(2)
+    sb = batch.thermo_bits(2) if args.method == "bits" else None
+    lb, _ = lower.device_bits(2) if args.method == "bits" else (None, 0)
+    ub, _ = upper.device_bits(2) if args.method == "bits" else (None, 0)
+    kpad = A.shape[1]
+    flags = torch.empty(S, dtype=torch.uint8, device=dev)
+    labels = torch.empty(S, dtype=torch.uint8, device=dev)
+    counts = torch.empty(4, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = _abi.stream_ptr()
+    launches = 0
+    import torch.distributed as tdist
+
+    def classify_kernel():
+        if args.method == "tc":
+            _abi.call("rsr_classify_tc", _abi.ptr(A), S, _abi.ptr(bl), nl, _abi.ptr(bu), nu, kpad,
+                      _abi.ptr(flags), 0, stream)
+        else:
+            _abi.call("rsr_classify_bits", _abi.ptr(sb), S, _abi.ptr(lb), nl, _abi.ptr(ub), nu,
+                      sb.shape[1], _abi.ptr(flags), None, None, 0, stream)
+
+    def step(kev=None):
+        nonlocal launches
+        if kev:
+            kev[0].record()
+        classify_kernel()
+        if kev:
+            kev[1].record()
+        _abi.call("rsr_finalize", _abi.ptr(flags), S, _abi.ptr(labels), _abi.ptr(counts), stream)
+        launches += 2
+        if world > 1:
+            tdist.all_reduce(counts)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    comm.barrier()
+    launches = 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    nv_index = int(vis.split(",")[local_rank]) if vis and vis.split(",")[0].isdigit() else local_rank
+    with ClockSampler(nv_index) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the step events)
+            ev[k][0].record()
+            step(kev[k])
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    comm.barrier()
+    step_ms = sum(s.elapsed_time(e) for s, e in ev)
+    kern_ms = [s.elapsed_time(e) for s, e in kev]
+    if world > 1:
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        step_ms = float(t.item())
+    ms_per_step = step_ms / args.steps
+    value = world * S * K / (ms_per_step * 1e-3)
+    final_counts = counts.cpu().tolist()
+
+    # ---- roofline of the dominant kernel (algorithmic ops, unpadded K)
+    ops_per_pair = 2 * N_COMP * (2 - 1)
+    kern_avg = sum(kern_ms) / len(kern_ms)
+    achieved = S * K * ops_per_pair / (kern_avg * 1e-3) / 1e12
+    peak, peak_src = int8_peak_tops()
+    kname = "classify_tc_kernel" if args.method == "tc" else "classify_bits_kernel"
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
+                "frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname,
+                "kernel_ms": kern_avg, "ops_per_pair": ops_per_pair,
+                "peak_source": peak_src, "spec_peak_tops": 4500.0,
+                "frac_of_spec": achieved / 4500.0}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((S, N_COMP), dtype=torch.uint8, pin_memory=True)
+        host.copy_(batch.device_states())
+        out = torch.empty(S, dtype=torch.uint8, pin_memory=True)
+        for _ in range(2):
+            P.classify.__module__  # noqa: B018
+            from paper_2604_17066_b200.classify import classify_host
+            classify_host(host, lower, upper, 2, labels_out=out)
+        torch.cuda.synchronize()
+        comm.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            _, c = classify_host(host, lower, upper, 2, labels_out=out)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            dt = float(t.item())
+        assert list(c) == final_counts[:3] or world > 1
+        e2e = {"value": world * S * K * args.steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": S * N_COMP, "d2h_bytes_per_step": S + 32,
+               "ms_per_step": 1e3 * dt / args.steps,
+               "api": "paper_2604_17066_b200.classify.classify_host (pinned host uint8 states -> "
+                      "labels), chunked H2D overlapped with rsr_encode_samples + rsr_classify_tc"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = calibrated_cpu_rows(p1, lower_rows, upper_rows, args.cpu_seconds)
+        rate, dt, cores, chunk = cpu_classify_rate(p1, lower_rows, upper_rows, rows)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{rows} samples x {K} refs of the same workload ({dt:.1f} s); oracle port "
+                         f"of the reference classify (packbits + bitwise_count, ThreadPool "
+                         f"n_workers={cores}, chunk={chunk})"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "int8", "data": "synthetic",
+                "config": {"workload": desc, "samples_per_gpu": S, "ref_states": K,
+                           "n_components": N_COMP, "method": args.method,
+                           "parallelism": f"dp{world} (samples sharded by stream offset, refs "
+                                          f"replicated, counts all-reduced)",
+                           "l2": "A operand 2^20x320 B = 335 MB > L2 and 256 MB L2 flush between "
+                                 "steps (outside the step events)",
+                           "labels": {"lower": final_counts[0], "upper": final_counts[1],
+                                      "unclassified": final_counts[2]}},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -179,7 +179,8 @@ class ReferenceSet:
             outcome.append("inserted")
         keep_new = [j for j, a in zip(inserted, alive) if a]
         if drop_members.any() or len(keep_new) != len(inserted):
-            rows = np.concatenate([self._rows[: self._n][~drop_members],
+            old = self._rows[: self._n] if self._n else np.zeros((0, N), dtype=np.uint8)
+            rows = np.concatenate([old[~drop_members],
                                    cands_host[keep_new].astype(np.uint8)], axis=0)
             self._set_rows(rows)
         elif keep_new:

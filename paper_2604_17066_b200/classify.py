@@ -254,6 +254,62 @@ def classify(batch: SampleBatch, lower_set: ReferenceSet | None, upper_set: Refe
         first_match_upper=fu.cpu().numpy() if (explain and fu is not None) else None)
 
 
+def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSet | None,
+                  n_states: int, *, chunk_rows: int = 1 << 17,
+                  labels_out: torch.Tensor | None = None) -> tuple[torch.Tensor, tuple[int, int, int]]:
+    """Classify host-resident uint8 samples, streaming them through the GPU.
+
+    ``states`` is a (preferably pinned) host uint8 tensor/array [S, N].  Chunks
+    are copied on a side stream while the previous chunk is encoded and
+    classified (rsr_encode_samples + rsr_classify_tc), then rsr_finalize runs
+    once and the uint8 labels (0 lower / 1 upper / 2 unclassified) come back
+    into ``labels_out`` (host).  Returns (labels_out, counts).
+    """
+    host = states if isinstance(states, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(states))
+    if host.dtype != torch.uint8 or host.dim() != 2:
+        raise ValueError("states must be a uint8 S x N host matrix")
+    S, N = host.shape
+    dev = _device.device()
+    m_eff = max(2, n_states)
+    for s in (lower_set, upper_set):
+        if s is not None and len(s) and s.max_state >= m_eff:
+            raise ValueError(f"states must lie in [0, {n_states - 1}]")
+    kpad = _abi.thermo_kpad(N, m_eff)
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    chunk = max(1, min(chunk_rows, S))
+    bufs = [torch.empty((chunk, N), dtype=torch.uint8, device=dev) for _ in range(2)]
+    therm = [torch.empty((chunk, kpad), dtype=torch.int8, device=dev) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    flags = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
+    bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
+    bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
+    st = _device.stream()
+    for i, lo in enumerate(range(0, S, chunk)):
+        hi = min(S, lo + chunk)
+        slot = i & 1
+        with torch.cuda.stream(copy):
+            if i >= 2:
+                copy.wait_event(free[slot])
+            bufs[slot][: hi - lo].copy_(host[lo:hi], non_blocking=True)
+            ready[slot].record(copy)
+        comp.wait_event(ready[slot])
+        _abi.call("rsr_encode_samples", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
+                  _abi.ptr(therm[slot]), kpad, st)
+        _abi.call("rsr_classify_tc", _abi.ptr(therm[slot]), hi - lo, _abi.ptr(bl), nl, _abi.ptr(bu),
+                  nu, kpad, _abi.ptr(flags[lo:hi]), 0, st)
+        free[slot].record(comp)
+    labels = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
+    counts_d = torch.empty(4, dtype=torch.int64, device=dev)
+    _abi.call("rsr_finalize", _abi.ptr(flags), S, _abi.ptr(labels), _abi.ptr(counts_d), st)
+    if labels_out is None:
+        labels_out = torch.empty(S, dtype=torch.uint8, pin_memory=True)
+    labels_out[:S].copy_(labels[:S], non_blocking=True)
+    counts = counts_d.cpu().tolist()  # synchronises the stream
+    return labels_out, (counts[0], counts[1], counts[2])
+
+
 def cov(p_hat: float, n_samples: int) -> float | None:
     """sqrt((1 - p) / (H p)); None at p = 0 (classify.py:265-277)."""
     if n_samples < 1:
