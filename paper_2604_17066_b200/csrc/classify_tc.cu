@@ -23,6 +23,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace {
@@ -43,7 +45,16 @@ struct TcParams {
   int stages;
   uint8_t* flags;
   int accumulate;
+  int debug;  // RSR_TC_DEBUG: bit0 = no B reloads after the first ring, bit1 = no TMEM loads
 };
+
+// Reference tiles are visited in a per-CTA rotated order so that the 148 SMs
+// do not all stream the same tile out of the same L2 slices at once; the
+// OR-reduction of hits is order independent.
+__device__ __forceinline__ int tile_at(int j, int rot, int nt) {
+  const int t = j + rot;
+  return t >= nt ? t - nt : t;
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -110,6 +121,32 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// Low word of the SW128 K-major descriptor (start address >> 4, LBO = 16 B);
+// the high word is the constant kDescHi (SBO = 1024 B, version 1, 128B swizzle).
+__device__ __forceinline__ uint32_t desc_lo(uint32_t saddr) {
+  return ((saddr >> 4) & 0x3FFFu) | (1u << 16);
+}
+constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+
+__device__ __forceinline__ void umma_i8_lo(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 da, {%1, %5};\n\t"
+      "mov.b64 db, {%2, %5};\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "r"(kDescHi));
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(e));
+  return e != 0;
 }
 
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
@@ -184,74 +221,106 @@ classify_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const int rot = (int)(((int64_t)blockIdx.x * p.nt_total) / gridDim.x);
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0, a_phase = 0;
-      for (int g = blockIdx.x; g < p.n_groups; g += gridDim.x) {
-        mbar_wait(smem_addr(a_empty), a_phase ^ 1);
+    // The whole warp runs the (warp-uniform) loop so addresses and coordinates
+    // stay in uniform registers; one elected lane issues each TMA.
+    int stage = 0, loads = 0;
+    uint32_t phase = 0, a_phase = 0;
+    const uint32_t sA0 = smem_addr(sA), sB0 = smem_addr(sB);
+    const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
+    for (int g = blockIdx.x; g < p.n_groups; g += gridDim.x) {
+      mbar_wait(smem_addr(a_empty), a_phase ^ 1);
+      if (elect_one()) {
         mbar_expect_tx(smem_addr(a_full), (uint32_t)(MT * p.kb * kTileBytes));
         for (int mt = 0; mt < MT; ++mt)
           for (int kb = 0; kb < p.kb; ++kb)
-            tma_load_2d(smem_addr(sA + (size_t)(mt * p.kb + kb) * kTileBytes), &map_a,
-                        smem_addr(a_full), kb * kKBlock, (g * MT + mt) * kTileM);
-        a_phase ^= 1;
-        for (int j = 0; j < p.nt_total; ++j) {
-          const bool low = j < p.nt_lower;
-          const CUtensorMap* map = low ? &map_lower : &map_upper;
-          const int y = (low ? j : j - p.nt_lower) * kTileN;
-          for (int kb = 0; kb < p.kb; ++kb) {
-            mbar_wait(smem_addr(&b_empty[stage]), phase ^ 1);
-            mbar_expect_tx(smem_addr(&b_full[stage]), (uint32_t)kTileBytes);
-            tma_load_2d(smem_addr(sB + (size_t)stage * kTileBytes), map,
-                        smem_addr(&b_full[stage]), kb * kKBlock, y);
-            if (++stage == p.stages) {
-              stage = 0;
-              phase ^= 1;
+            tma_load_2d(sA0 + (uint32_t)(mt * p.kb + kb) * kTileBytes, &map_a, smem_addr(a_full),
+                        kb * kKBlock, (g * MT + mt) * kTileM);
+      }
+      __syncwarp();
+      a_phase ^= 1;
+      for (int jj = 0; jj < p.nt_total; ++jj) {
+        const int j = tile_at(jj, rot, p.nt_total);
+        const bool low = j < p.nt_lower;
+        const CUtensorMap* map = low ? &map_lower : &map_upper;
+        const int y = (low ? j : j - p.nt_lower) * kTileN;
+        for (int kb = 0; kb < p.kb; ++kb) {
+          mbar_wait(bar_b_empty + 8 * stage, phase ^ 1);
+          if (elect_one()) {
+            if ((p.debug & 1) && loads >= p.stages) {
+              mbar_arrive(bar_b_full + 8 * stage);
+            } else {
+              mbar_expect_tx(bar_b_full + 8 * stage, (uint32_t)kTileBytes);
+              tma_load_2d(sB0 + (uint32_t)stage * kTileBytes, map, bar_b_full + 8 * stage,
+                          kb * kKBlock, y);
             }
+          }
+          __syncwarp();
+          ++loads;
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = i8_idesc(kTileM, kTileN);
-      int stage = 0;
-      uint32_t phase = 0, a_phase = 0, tc = 0;
-      for (int g = blockIdx.x; g < p.n_groups; g += gridDim.x) {
-        mbar_wait(smem_addr(a_full), a_phase);
-        a_phase ^= 1;
+    // Warp-uniform loop; descriptors are precomputed 32-bit words so each MMA
+    // costs two uniform adds (a single-lane loop would force an R2UR
+    // waterfall per MMA and cap the issue rate well below the tensor pipe).
+    constexpr uint32_t idesc = i8_idesc(kTileM, kTileN);
+    const uint32_t tm0 = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t a_lo0 = desc_lo(smem_addr(sA)), b_lo0 = desc_lo(smem_addr(sB));
+    const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
+    const int kb_full = (p.ksteps_last == kKBlock / kKStep) ? p.kb : p.kb - 1;
+    int stage = 0;
+    uint32_t phase = 0, a_phase = 0, tc = 0;
+    for (int g = blockIdx.x; g < p.n_groups; g += gridDim.x) {
+      mbar_wait(smem_addr(a_full), a_phase);
+      a_phase ^= 1;
+      tc_fence_after();
+      for (int j = 0; j < p.nt_total; ++j, ++tc) {
+        const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
+        mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
         tc_fence_after();
-        for (int j = 0; j < p.nt_total; ++j, ++tc) {
-          const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
-          mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
+        const uint32_t d0 = tm0 + buf * MT * kTileN;
+        for (int kb = 0; kb < p.kb; ++kb) {
+          mbar_wait(bar_b_full + 8 * stage, phase);
           tc_fence_after();
-          for (int kb = 0; kb < p.kb; ++kb) {
-            mbar_wait(smem_addr(&b_full[stage]), phase);
-            tc_fence_after();
-            const int nks = (kb == p.kb - 1) ? p.ksteps_last : kKBlock / kKStep;
-            const uint32_t b_base = smem_addr(sB + (size_t)stage * kTileBytes);
+          const uint32_t bl = b_lo0 + (uint32_t)stage * (kTileBytes >> 4);
+          if (elect_one()) {
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-              const uint32_t a_base = smem_addr(sA + (size_t)(mt * p.kb + kb) * kTileBytes);
-              const uint32_t d = tmem_base + (buf * MT + mt) * kTileN;
-              for (int ks = 0; ks < nks; ++ks)
-                umma_i8(d, sw128_desc(a_base + ks * kKStep), sw128_desc(b_base + ks * kKStep),
-                        idesc, (kb | ks) != 0);
+              const uint32_t al = a_lo0 + (uint32_t)(mt * p.kb + kb) * (kTileBytes >> 4);
+              const uint32_t d = d0 + mt * kTileN;
+              if (kb < kb_full) {
+#pragma unroll
+                for (int ks = 0; ks < kKBlock / kKStep; ++ks)
+                  umma_i8_lo(d, al + ks * (kKStep >> 4), bl + ks * (kKStep >> 4), idesc,
+                             (kb | ks) != 0);
+              } else {
+                for (int ks = 0; ks < p.ksteps_last; ++ks)
+                  umma_i8_lo(d, al + ks * (kKStep >> 4), bl + ks * (kKStep >> 4), idesc,
+                             (kb | ks) != 0);
+              }
             }
-            umma_commit(smem_addr(&b_empty[stage]));
-            if (++stage == p.stages) {
-              stage = 0;
-              phase ^= 1;
-            }
+            umma_commit(bar_b_empty + 8 * stage);
           }
-          umma_commit(smem_addr(&t_full[buf]));
+          __syncwarp();
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        umma_commit(smem_addr(a_empty));
+        if (elect_one()) umma_commit(smem_addr(&t_full[buf]));
+        __syncwarp();
       }
+      if (elect_one()) umma_commit(smem_addr(a_empty));
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------ epilogue
@@ -260,7 +329,8 @@ classify_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     uint32_t tc = 0;
     for (int g = blockIdx.x; g < p.n_groups; g += gridDim.x) {
       uint32_t hit = 0;
-      for (int j = 0; j < p.nt_total; ++j, ++tc) {
+      for (int jj = 0; jj < p.nt_total; ++jj, ++tc) {
+        const int j = tile_at(jj, rot, p.nt_total);
         const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
         mbar_wait(smem_addr(&t_full[buf]), tphase);
         tc_fence_after();
@@ -269,6 +339,10 @@ classify_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         uint32_t mn = 0xFFFFFFFFu;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
+          if (p.debug & 2) {
+            mn = 1;
+            break;
+          }
           uint32_t v[64];
           RSR_LD32(taddr + half * 64, v);
           RSR_LD32(taddr + half * 64 + 32, (v + 32));
@@ -388,6 +462,8 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
   p.nt_total = (int)(nt_l + nt_u);
   p.flags = flags;
   p.accumulate = accumulate;
+  const char* dbg = getenv("RSR_TC_DEBUG");
+  p.debug = dbg ? atoi(dbg) : 0;
 
   const size_t max_smem = 227 * 1024;
   const size_t fixed = 1024 /*align slack*/ + 256 /*barriers*/;
