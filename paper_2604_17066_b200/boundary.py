@@ -62,7 +62,7 @@ class ReferenceState:
         return cls(tuple(vector), side, threshold)
 
 
-_TILE = 128
+_TILE = 256  # reference rows per classifier tile (CTA-pair kernel: 2 x 128)
 
 
 class ReferenceSet:

@@ -73,8 +73,13 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Wait for the phase of parity `parity` to complete.  A wait that exceeds
+// ~2^34 cycles (several seconds) can only be a protocol bug: trap so the
+// launch fails loudly instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
+  long long t0 = 0;
+  int spins = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -83,7 +88,25 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
+    if (!done && ++spins == 64) t0 = clock64();
+    if (!done && spins > 64 && (spins & 1023) == 0 && clock64() - t0 > (1ll << 34)) __trap();
   } while (!done);
+}
+
+// Remote (or local) arrive on the pair leader's copy of a barrier: clearing
+// bit 24 of a shared::cluster address selects CTA rank 0 of the CTA pair.
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar & kPeerMask) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map,
+                                                 uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & kPeerMask), "r"(x), "r"(y)
+      : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
@@ -372,6 +395,260 @@ classify_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (default): cta_group::2, one MMA = 256 samples x 256 refs
+// x 32 K.  A cluster of two CTAs on one TPC owns a group of 256 sample rows
+// (128 per CTA, resident in shared memory); every reference tile of 256 rows
+// is split 128/128 between the two CTAs' shared memory.  The leader CTA
+// (rank 0) issues the MMAs; each CTA's TMEM holds the 128 x 256 int32
+// accumulator of its own rows (2 buffers = 512 columns).  Per unit of work
+// this halves the MMA instruction count and each SM's operand reads compared
+// with the 1-SM M=128/N=128 kernel above, at the same L2 traffic.
+//   barriers (leader copy used unless noted):
+//     b_full[s]  count 2 (leader arrive.expect_tx + peer arrive) + TMA bytes of both CTAs
+//     b_empty[s] per CTA, count 1 (multicast tcgen05.commit)
+//     a_full     count 2, like b_full;  a_empty per CTA (multicast commit)
+//     t_full[b]  per CTA, count 1 (multicast commit)
+//     t_empty[b] count 16 (8 epilogue warps x 2 CTAs, remote arrives)
+constexpr int kPairN = 256;
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void umma_i8_pair(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 da, {%1, %5};\n\t"
+      "mov.b64 db, {%2, %5};\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "r"(kDescHi));
+}
+
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n\t}" ::"r"(bar)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_lower,
+                        const __grid_constant__ CUtensorMap map_upper, const TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_addr(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+  uint8_t* sA = smem;                                      // kb x 16 KB (this CTA's 128 rows)
+  uint8_t* sB = sA + (size_t)p.kb * kTileBytes;            // stages x 16 KB (128 ref rows)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * kTileBytes);
+  uint64_t* b_full = bars;
+  uint64_t* b_empty = bars + p.stages;
+  uint64_t* a_full = bars + 2 * p.stages;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* t_full = a_full + 2;   // [2]
+  uint64_t* t_empty = a_full + 4;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lower)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_upper)));
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(smem_addr(&b_full[i]), 2);
+      mbar_init(smem_addr(&b_empty[i]), 1);
+    }
+    mbar_init(smem_addr(a_full), 2);
+    mbar_init(smem_addr(a_empty), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_addr(&t_full[i]), 1);
+      mbar_init(smem_addr(&t_empty[i]), 16);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_addr(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int rot = (int)(((int64_t)cluster * p.nt_total) / n_clusters);
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer (both CTAs)
+    int stage = 0;
+    uint32_t phase = 0, a_phase = 0;
+    const uint32_t sA0 = smem_addr(sA), sB0 = smem_addr(sB);
+    const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
+    const uint32_t a_bytes = (uint32_t)(2 * p.kb * kTileBytes);
+    for (int g = cluster; g < p.n_groups; g += n_clusters) {
+      mbar_wait(smem_addr(a_empty), a_phase ^ 1);
+      if (elect_one()) {
+        if (leader)
+          mbar_expect_tx(smem_addr(a_full), a_bytes);
+        else
+          mbar_arrive_leader(smem_addr(a_full));
+        for (int kb = 0; kb < p.kb; ++kb)
+          tma_load_2d_pair(sA0 + (uint32_t)kb * kTileBytes, &map_a, smem_addr(a_full),
+                           kb * kKBlock, g * 2 * kTileM + (int)rank * kTileM);
+      }
+      __syncwarp();
+      a_phase ^= 1;
+      for (int jj = 0; jj < p.nt_total; ++jj) {
+        const int j = tile_at(jj, rot, p.nt_total);
+        const bool low = j < p.nt_lower;
+        const CUtensorMap* map = low ? &map_lower : &map_upper;
+        const int y = (low ? j : j - p.nt_lower) * kPairN + (int)rank * kTileN;
+        for (int kb = 0; kb < p.kb; ++kb) {
+          mbar_wait(bar_b_empty + 8 * stage, phase ^ 1);
+          if (elect_one()) {
+            if (leader)
+              mbar_expect_tx(bar_b_full + 8 * stage, (uint32_t)(2 * kTileBytes));
+            else
+              mbar_arrive_leader(bar_b_full + 8 * stage);
+            tma_load_2d_pair(sB0 + (uint32_t)stage * kTileBytes, map, bar_b_full + 8 * stage,
+                             kb * kKBlock, y);
+          }
+          __syncwarp();
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      constexpr uint32_t idesc = i8_idesc(2 * kTileM, kPairN);
+      const uint32_t tm0 = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t a_lo0 = desc_lo(smem_addr(sA)), b_lo0 = desc_lo(smem_addr(sB));
+      const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
+      const int kb_full = (p.ksteps_last == kKBlock / kKStep) ? p.kb : p.kb - 1;
+      int stage = 0;
+      uint32_t phase = 0, a_phase = 0, tc = 0;
+      for (int g = cluster; g < p.n_groups; g += n_clusters) {
+        mbar_wait(smem_addr(a_full), a_phase);
+        a_phase ^= 1;
+        tc_fence_after();
+        for (int j = 0; j < p.nt_total; ++j, ++tc) {
+          const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
+          mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
+          tc_fence_after();
+          const uint32_t d = tm0 + buf * kPairN;
+          for (int kb = 0; kb < p.kb; ++kb) {
+            mbar_wait(bar_b_full + 8 * stage, phase);
+            tc_fence_after();
+            const uint32_t bl = b_lo0 + (uint32_t)stage * (kTileBytes >> 4);
+            const uint32_t al = a_lo0 + (uint32_t)kb * (kTileBytes >> 4);
+            if (elect_one()) {
+              if (kb < kb_full) {
+#pragma unroll
+                for (int ks = 0; ks < kKBlock / kKStep; ++ks)
+                  umma_i8_pair(d, al + ks * (kKStep >> 4), bl + ks * (kKStep >> 4), idesc,
+                               (kb | ks) != 0);
+              } else {
+                for (int ks = 0; ks < p.ksteps_last; ++ks)
+                  umma_i8_pair(d, al + ks * (kKStep >> 4), bl + ks * (kKStep >> 4), idesc,
+                               (kb | ks) != 0);
+              }
+              umma_commit_pair(bar_b_empty + 8 * stage);
+            }
+            __syncwarp();
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          if (elect_one()) umma_commit_pair(smem_addr(&t_full[buf]));
+          __syncwarp();
+        }
+        if (elect_one()) umma_commit_pair(smem_addr(a_empty));
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------ epilogue (both CTAs)
+    const int quad = warp & 3;
+    const int colhalf = (warp - 4) >> 2;
+    uint32_t tc = 0;
+    for (int g = cluster; g < p.n_groups; g += n_clusters) {
+      uint32_t hit = 0;
+      for (int jj = 0; jj < p.nt_total; ++jj, ++tc) {
+        const int j = tile_at(jj, rot, p.nt_total);
+        const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
+        mbar_wait(smem_addr(&t_full[buf]), tphase);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kPairN + colhalf * kTileN;
+        uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (p.debug & 2) {
+            mn = 1;
+            break;
+          }
+          uint32_t v[64];
+          RSR_LD32(taddr + half * 64, v);
+          RSR_LD32(taddr + half * 64 + 32, (v + 32));
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 64; ++i) mn = min(mn, v[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(smem_addr(&t_empty[buf]));
+        if (mn == 0) hit |= (j < p.nt_lower) ? RSR_HIT_LOWER : RSR_HIT_UPPER;
+      }
+      // the two column halves of a row live in two warps: combine through smem-free
+      // atomics on the flags byte would race, so OR via a warp-pair exchange instead
+      const int64_t row = (int64_t)g * 2 * kTileM + rank * kTileM + quad * 32 + lane;
+      uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 8);  // [128] scratch
+      named_bar_sync(1, 256);
+      if (colhalf == 1) xchg[quad * 32 + lane] = hit;
+      named_bar_sync(1, 256);
+      if (colhalf == 0) {
+        hit |= xchg[quad * 32 + lane];
+        if (row < p.S) {
+          const uint8_t prev = p.accumulate ? p.flags[row] : 0;
+          p.flags[row] = (uint8_t)(prev | hit);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
 __global__ void clear_flags_kernel(uint8_t* flags, int64_t S) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < S) flags[i] = 0;
@@ -429,7 +706,11 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
   cudaStream_t st = rsr::as_stream(stream);
   if (S == 0) return RSR_OK;
   RSR_REQUIRE(flags != nullptr && A != nullptr, "rsr_classify_tc: null pointer");
-  const int64_t nt_l = rsr::ceil_div(n_lower, kTileN), nt_u = rsr::ceil_div(n_upper, kTileN);
+  // Reference rows are tiled by 256 (pair kernel) -- callers pad B to a
+  // multiple of 256 rows with never-hit rows (rsr_encode_refs rows_total).
+  const int impl = getenv("RSR_TC_IMPL") ? atoi(getenv("RSR_TC_IMPL")) : 2;
+  const int tile_n = impl == 1 ? kTileN : kPairN;
+  const int64_t nt_l = rsr::ceil_div(n_lower, tile_n), nt_u = rsr::ceil_div(n_upper, tile_n);
   if (nt_l + nt_u == 0) {
     if (!accumulate) {
       clear_flags_kernel<<<(unsigned)rsr::ceil_div(S, 256), 256, 0, st>>>(flags, S);
@@ -449,9 +730,9 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
   if (rc) return rc;
   const int8_t* bl = nt_l ? B_lower : B_upper;
   const int8_t* bu = nt_u ? B_upper : B_lower;
-  rc = make_map(&ml, bl, (nt_l ? nt_l : nt_u) * kTileN, Kpad);
+  rc = make_map(&ml, bl, (nt_l ? nt_l : nt_u) * tile_n, Kpad);
   if (rc) return rc;
-  rc = make_map(&mu, bu, (nt_u ? nt_u : nt_l) * kTileN, Kpad);
+  rc = make_map(&mu, bu, (nt_u ? nt_u : nt_l) * tile_n, Kpad);
   if (rc) return rc;
 
   TcParams p;
@@ -464,8 +745,25 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
   p.accumulate = accumulate;
   const char* dbg = getenv("RSR_TC_DEBUG");
   p.debug = dbg ? atoi(dbg) : 0;
-
   const size_t max_smem = 227 * 1024;
+
+  if (impl != 1) {
+    const size_t fixed = 1024 /*align slack*/ + 1024 /*barriers + exchange*/;
+    const size_t a_bytes = (size_t)p.kb * kTileBytes;
+    int stages = (int)((max_smem - fixed - a_bytes) / kTileBytes);
+    if (stages > 12) stages = 12;
+    RSR_REQUIRE(stages >= 2, "rsr_classify_tc: Kpad too large for shared memory");
+    p.stages = stages;
+    const size_t smem = fixed + a_bytes + (size_t)stages * kTileBytes;
+    p.n_groups = (int)rsr::ceil_div(S, (int64_t)2 * kTileM);
+    RSR_CUDA(cudaFuncSetAttribute(classify_tc_pair_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int clusters = sm_count / 2;
+    if (p.n_groups < clusters) clusters = p.n_groups;
+    classify_tc_pair_kernel<<<2 * clusters, 384, smem, st>>>(ma, ml, mu, p);
+    return rsr::check_launch("classify_tc_pair_kernel");
+  }
+
   const size_t fixed = 1024 /*align slack*/ + 256 /*barriers*/;
   const int mt = ((size_t)2 * p.kb * kTileBytes + 4 * kTileBytes + fixed <= max_smem) ? 2 : 1;
   const size_t a_bytes = (size_t)mt * p.kb * kTileBytes;

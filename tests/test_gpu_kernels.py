@@ -52,7 +52,7 @@ def test_sample_states_and_thermo(n, m, count, start):
 def _refs_dev(refs, n, m, side):
     kpad = A.thermo_kpad(n, m)
     k = refs.shape[0]
-    rows = max(128, (k + 127) // 128 * 128)
+    rows = max(256, (k + 255) // 256 * 256)
     st = _dev(refs.astype(np.uint8))
     out = torch.empty((rows, kpad), dtype=torch.int8, device="cuda")
     A.call("rsr_encode_refs", A.ptr(st) if k else None, k, rows, n, m, side, A.ptr(out), kpad, A.stream_ptr())
