@@ -315,7 +315,7 @@ def run_ours(args):
     kern_avg = sum(kern_ms) / len(kern_ms)
     achieved = S * K * ops_per_pair / (kern_avg * 1e-3) / 1e12
     cublas_peak, cublas_src = int8_peak_tops()
-    kname = "classify_tc_kernel" if args.method == "tc" else "classify_bits_kernel"
+    kname = "classify_tc_pair_kernel" if args.method == "tc" else "classify_bits_kernel"
     # Denominator: dense int8 tensor peak 4.5 POPS (B200 spec), which our own
     # tcgen05 kind::i8 issue-rate microbenchmark (tools/mma_rate.cu) reaches
     # on this pool (4409-4544 TOPS at 1965 MHz); cuBLASLt int8 only reaches the

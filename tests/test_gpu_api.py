@@ -246,9 +246,13 @@ def test_phi_kinds_vs_oracle():
 
 # ----------------------------------------------------------------- workflow
 
-@pytest.mark.parametrize("case", [c["spec"]["name"] for c in load_json("workflow.json")])
-def test_workflow_golden(case):
-    rec = next(c for c in load_json("workflow.json") if c["spec"]["name"] == case)
+_WORKFLOW_CASES = [("workflow.json", c["spec"]["name"]) for c in load_json("workflow.json")] + [
+    ("cfg1_full.json", "cfg1_full")]  # BASELINE config 1 end to end (10^5 samples, 468 iterations)
+
+
+@pytest.mark.parametrize("fname,case", _WORKFLOW_CASES)
+def test_workflow_golden(fname, case):
+    rec = next(c for c in load_json(fname) if c["spec"]["name"] == case)
     spec = rec["spec"]
     model = device_model(spec["model"])
     dist = P.ComponentDistribution(np.array(spec["probs"]))
