@@ -43,7 +43,11 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", default="cfg2", choices=["cfg2", "cfg2_mixed", "cfg4"])
+    p.add_argument("--config", default="cfg2",
+                   choices=["cfg2", "cfg2_mixed", "cfg4", "cfg1", "cfg3", "cfg5"])
+    p.add_argument("--parallel-searches", type=int, default=64)
+    p.add_argument("--shard-refs", action="store_true",
+                   help="N>1: shard reference states across ranks, OR-reduce hit flags")
     p.add_argument("--k", type=int, default=10_000, help="refs per side (cfg2) / path refs (cfg4)")
     p.add_argument("--samples", type=int, default=None, help="samples per GPU")
     p.add_argument("--method", choices=["tc", "bits"], default="tc")
@@ -240,11 +244,21 @@ def run_ours(args):
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
     p1, lower_rows, upper_rows, S, desc = workload(args)
+    K_job = len(lower_rows) + len(upper_rows)
+    shard_refs = args.shard_refs and world > 1
+    if shard_refs:
+        # ref-sharded mode: every rank classifies the same S samples against its
+        # 1/world slice of each side; hit flags are OR-reduced (NCCL MAX on 0/1 bits)
+        from paper_2604_17066_b200.dist import shard_range
+        l0, lc = shard_range(len(lower_rows), world, rank)
+        u0, uc = shard_range(len(upper_rows), world, rank)
+        lower_rows, upper_rows = lower_rows[l0:l0 + lc], upper_rows[u0:u0 + uc]
     lower = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower_rows, trusted=True)
     upper = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper_rows, trusted=True)
     K = len(lower) + len(upper)
     dist = P.ComponentDistribution.iid(N_COMP, [1 - p1, p1])
-    batch = P.sample_batch(dist, S, seed=0, generation_index=0, start=rank * S)
+    batch = P.sample_batch(dist, S, seed=0, generation_index=0,
+                           start=0 if shard_refs else rank * S)
     A = batch.thermo(2)
     bl, nl = lower.device_thermo(2)
     bu, nu = upper.device_thermo(2)
@@ -275,9 +289,11 @@ def run_ours(args):
         classify_kernel()
         if kev:
             kev[1].record()
+        if shard_refs:
+            comm.allreduce_max_u8(flags)  # OR of hit bits across the ref shards
         _abi.call("rsr_finalize", _abi.ptr(flags), S, _abi.ptr(labels), _abi.ptr(counts), stream)
         launches += 2
-        if world > 1:
+        if world > 1 and not shard_refs:
             tdist.all_reduce(counts)
 
     for _ in range(args.warmup):
@@ -307,7 +323,9 @@ def run_ours(args):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         step_ms = float(t.item())
     ms_per_step = step_ms / args.steps
-    value = world * S * K / (ms_per_step * 1e-3)
+    # whole-job pairs per step: replicated refs -> world x S x K; sharded refs -> S x K_job
+    job_pairs = S * K_job if shard_refs else world * S * K
+    value = job_pairs / (ms_per_step * 1e-3)
     final_counts = counts.cpu().tolist()
 
     # ---- roofline of the dominant kernel (algorithmic ops, unpadded K)
@@ -370,14 +388,16 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "int8", "data": "synthetic",
-                "config": {"workload": desc, "samples_per_gpu": S, "ref_states": K,
-                           "n_components": N_COMP, "method": args.method,
-                           "parallelism": f"dp{world} (samples sharded by stream offset, refs "
-                                          f"replicated, counts all-reduced)",
-                           "l2": "A operand 2^20x320 B = 335 MB > L2 and 256 MB L2 flush between "
-                                 "steps (outside the step events)",
+                "higher_is_better": True, "scaling": "strong" if shard_refs else "weak",
+                "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+                "config": {"workload": desc, "samples_per_gpu": S, "ref_states": K_job,
+                           "ref_states_per_gpu": K, "n_components": N_COMP, "method": args.method,
+                           "parallelism": (f"ref-sharded x{world} (same samples on every rank, "
+                                           f"hit flags OR-reduced with NCCL MAX)" if shard_refs else
+                                           f"dp{world} (samples sharded by stream offset, refs "
+                                           f"replicated, counts all-reduced)"),
+                           "l2": f"A operand {S}x{kpad} B = {S * kpad / 1e6:.0f} MB > L2 and 256 MB "
+                                 f"L2 flush between steps (outside the step events)",
                            "labels": {"lower": final_counts[0], "upper": final_counts[1],
                                       "unclassified": final_counts[2]}},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
@@ -387,9 +407,80 @@ def run_ours(args):
         tdist.destroy_process_group()
 
 
+# --------------------------------------------------------------- full loops
+
+def loop_problem(cfg: str, parallel_searches: int):
+    """(model_spec, probs, RunConfig kwargs, thresholds, target) of cfg1/cfg3/cfg5."""
+    from paper_2604_17066_b200 import workloads as W
+    if cfg == "cfg1":
+        g = W.cfg1(0)
+        spec = {"kind": "st", "n_nodes": g["n_nodes"], "edges": g["edges"], "s": 0, "t": 24,
+                "m": 2, "ms": 2}
+        return spec, g["probs"], dict(n_samples=100_000, seed=0), [0], \
+            "cfg1: 5x5 grid s-t, 10^5 samples, reference defaults (eps_u 1e-5, r_max 1e4, 1 search/it)"
+    g = W.cfg3(0) if cfg == "cfg3" else W.cfg5(0)
+    m = 2 if cfg == "cfg3" else 3
+    spec = {"kind": "st" if cfg == "cfg3" else "widest", "n_nodes": g["n_nodes"],
+            "edges": g["edges"], "s": g["source"], "t": g["target"], "m": m, "ms": m}
+    kw = dict(n_samples=1 << 20, seed=0, eps_u=1e-5, r_max=10_000,
+              parallel_searches=parallel_searches)
+    thr = [0] if cfg == "cfg3" else [0, 1]
+    desc = (f"{cfg}: 119-node/295-edge shortest-pairs graph, {'binary s-t' if m == 2 else 'M=3 widest path'}, "
+            f"batches 2^20, eps_u 1e-5, r_max 1e4, {parallel_searches} searches/it, "
+            f"Stage 2 to c.o.v. 0.05 on P(S<=m')")
+    return spec, g["probs"], kw, thr, desc
+
+
+def run_loop(args):
+    """Wall time of the full RSR loop (Stage 1 + Stage 2 to c.o.v. 0.05) on one GPU."""
+    import torch
+
+    import paper_2604_17066_b200 as P
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _specs import device_model
+    spec, probs, kw, thresholds, desc = loop_problem(args.config, args.parallel_searches)
+    dist = P.ComponentDistribution(probs)
+    torch.cuda.set_device(0)
+    out = {"metric": "wall-time to c.o.v.=0.05", "unit": "s", "higher_is_better": False,
+           "n_gpus": 1, "dtype": "int8", "data": "synthetic", "config": {"workload": desc}}
+    # warm-up: build the library state / CUDA context on a tiny run
+    wm = device_model(spec)
+    P.stage1_find_references(wm, dist, P.RunConfig(n_samples=1000, seed=1, r_max=5,
+                                                    eps_u=0.5), thresholds[0])
+    torch.cuda.synchronize()
+    model = device_model(spec)
+    cfg = P.RunConfig(**kw)
+    t0 = time.perf_counter()
+    stages = []
+    with ClockSampler(0) as clk:
+        for thr in thresholds:
+            ts = time.perf_counter()
+            s1 = P.stage1_find_references(model, dist, cfg, thr)
+            t1 = time.perf_counter()
+            if args.config == "cfg1":
+                rep = P.stage2_evaluate(model, dist, s1.lower, s1.upper, cfg, thr)
+            else:
+                rep = P.stage2_until_cov(model, dist, s1.lower, s1.upper, cfg, thr, 0.05,
+                                         side="lower")
+            t2 = time.perf_counter()
+            stages.append({"threshold": thr, "stage1_s": t1 - ts, "stage2_s": t2 - t1,
+                           "refs": [len(s1.lower), len(s1.upper)], "iterations": s1.iterations,
+                           "terminated_by": s1.terminated_by,
+                           "p_unclassified_last": s1.trace[-1].p_unclassified,
+                           "p_lower": rep.p_lower, "cov_lower": rep.cov_lower,
+                           "stage2_samples": rep.n_samples})
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    out.update({"value": wall, "stages": stages, "phi_evaluations": model.evaluation_count,
+                "clocks": clk.summary()})
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.config in ("cfg1", "cfg3", "cfg5"):
+        run_loop(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

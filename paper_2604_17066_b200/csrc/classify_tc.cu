@@ -760,8 +760,34 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int clusters = sm_count / 2;
     if (p.n_groups < clusters) clusters = p.n_groups;
-    classify_tc_pair_kernel<<<2 * clusters, 384, smem, st>>>(ma, ml, mu, p);
-    return rsr::check_launch("classify_tc_pair_kernel");
+    // Reference chunks: every group streams all tiles of a launch, so a launch's
+    // B slice must stay L2-resident (126 MB L2); 256 tiles = 64K refs x Kpad
+    // bytes (20 MB at Kpad = 320).  Flags accumulate across launches.
+    const char* ct = getenv("RSR_TC_CHUNK_TILES");
+    const int64_t chunk = ct ? atoll(ct) : 256;
+    const int64_t total = nt_l + nt_u;
+    for (int64_t c0 = 0; c0 < total; c0 += chunk) {
+      const int64_t c1 = c0 + chunk < total ? c0 + chunk : total;
+      const int64_t l0 = c0 < nt_l ? c0 : nt_l, l1 = c1 < nt_l ? c1 : nt_l;
+      const int64_t u0 = (c0 > nt_l ? c0 : nt_l) - nt_l, u1 = (c1 > nt_l ? c1 : nt_l) - nt_l;
+      TcParams q = p;
+      q.nt_lower = (int)(l1 - l0);
+      q.nt_total = (int)((l1 - l0) + (u1 - u0));
+      q.accumulate = c0 == 0 ? accumulate : 1;
+      CUtensorMap cl = ml, cu = mu;
+      if (total > chunk) {
+        const int8_t* lb = l1 > l0 ? B_lower + l0 * kPairN * (int64_t)Kpad : nullptr;
+        const int8_t* ub = u1 > u0 ? B_upper + u0 * kPairN * (int64_t)Kpad : nullptr;
+        rc = make_map(&cl, lb ? lb : ub, ((lb ? l1 - l0 : u1 - u0)) * kPairN, Kpad);
+        if (rc) return rc;
+        rc = make_map(&cu, ub ? ub : lb, ((ub ? u1 - u0 : l1 - l0)) * kPairN, Kpad);
+        if (rc) return rc;
+      }
+      classify_tc_pair_kernel<<<2 * clusters, 384, smem, st>>>(ma, cl, cu, q);
+      rc = rsr::check_launch("classify_tc_pair_kernel");
+      if (rc) return rc;
+    }
+    return RSR_OK;
   }
 
   const size_t fixed = 1024 /*align slack*/ + 256 /*barriers*/;

@@ -121,50 +121,119 @@ def random_st_paths(graph: dict, k: int, seed: int = 0, sigma: float = 1.5,
     vectorised Bellman-Ford over a batch of weight draws.  Distinct simple
     s-t paths are mutually non-dominated as upper reference states.
     """
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return _random_st_paths_torch(graph, k, seed, sigma)
+    except ImportError:  # pragma: no cover
+        pass
     n_nodes, edges = graph["n_nodes"], graph["edges"]
     s, t = graph["source"], graph["target"]
     eu = np.array([e[0] for e in edges])
     ev = np.array([e[1] for e in edges])
     E = len(edges)
+    # directed arcs (both orientations) grouped by head node for reduceat
+    tail = np.concatenate([eu, ev])
+    head = np.concatenate([ev, eu])
+    arc_edge = np.concatenate([np.arange(E), np.arange(E)])
+    order = np.argsort(head, kind="stable")
+    tail, head, arc_edge = tail[order], head[order], arc_edge[order]
+    starts = np.flatnonzero(np.r_[True, head[1:] != head[:-1]])
+    heads = head[starts]
     rng = np.random.default_rng([seed, 4])
     found: dict[bytes, None] = {}
     rounds = 0
     while len(found) < k and rounds < 10_000:
         rounds += 1
-        w = np.exp(sigma * rng.standard_normal((batch, E)))
+        w = np.exp(sigma * rng.standard_normal((batch, E)))[:, arc_edge]
         dist = np.full((batch, n_nodes), np.inf)
         dist[:, s] = 0.0
-        pred = np.full((batch, n_nodes), -1, dtype=np.int64)
-        rows = np.arange(batch)
         for _ in range(n_nodes):
-            changed = False
-            for a, b in ((eu, ev), (ev, eu)):
-                cand = dist[:, a] + w
-                better = cand < dist[:, b]
-                if better.any():
-                    changed = True
-                    # resolve several edges into the same node: keep the best
-                    cand_m = np.where(better, cand, np.inf)
-                    for j in np.flatnonzero(better.any(axis=0)):
-                        pass
-                    order = np.argsort(cand_m, axis=1)[:, ::-1]
-                    for col in order.T:
-                        sel = better[rows, col] & (cand_m[rows, col] < dist[rows, b[col]])
-                        if sel.any():
-                            dist[rows[sel], b[col][sel]] = cand_m[rows[sel], col[sel]]
-                            pred[rows[sel], b[col][sel]] = col[sel]
-            if not changed:
+            cand = dist[:, tail] + w
+            best = np.minimum.reduceat(cand, starts, axis=1)
+            new = dist.copy()
+            new[:, heads] = np.minimum(dist[:, heads], best)
+            new[:, s] = 0.0
+            if np.array_equal(new, dist):
                 break
-        for i in range(batch):
-            row = np.zeros(E, dtype=np.uint8)
-            node, hops = t, 0
-            while node != s and hops <= n_nodes:
-                e = pred[i, node]
-                row[e] = 1
-                node = eu[e] if ev[e] == node else ev[e]
-                hops += 1
-            found.setdefault(row.tobytes(), None)
+            dist = new
+        # predecessor arc of every node: an incoming arc achieving dist[head]
+        tight = np.isclose(dist[:, tail] + w, dist[:, head], rtol=0, atol=1e-12) & \
+            np.isfinite(dist[:, tail])
+        pred = np.full((batch, n_nodes), -1, dtype=np.int64)
+        arc_ids = np.where(tight, np.arange(tail.size)[None, :], -1)
+        pred[:, heads] = np.maximum.reduceat(arc_ids, starts, axis=1)  # any tight arc
+        rows = np.zeros((batch, E), dtype=np.uint8)
+        node = np.full(batch, t)
+        ok = np.isfinite(dist[:, t])
+        for _ in range(n_nodes):
+            active = ok & (node != s)
+            if not active.any():
+                break
+            a = pred[np.arange(batch), node]
+            bad = active & (a < 0)
+            ok &= ~bad
+            active &= ~bad
+            rows[active, arc_edge[a[active]]] = 1
+            node = np.where(active, tail[a], node)
+        for r in rows[ok & (node == s)]:
+            found.setdefault(r.tobytes(), None)
             if len(found) >= k:
                 break
     out = np.frombuffer(b"".join(found.keys()), dtype=np.uint8).reshape(-1, E)
     return out[:k].copy()
+
+
+def _random_st_paths_torch(graph: dict, k: int, seed: int, sigma: float,
+                           batch: int = 1 << 16) -> np.ndarray:
+    """Same construction as ``random_st_paths`` with the batched Bellman-Ford on
+    the GPU (setup data only: cfg4 needs up to 5 x 10^5 distinct paths)."""
+    import torch
+    dev = torch.device("cuda")
+    n_nodes, edges = graph["n_nodes"], graph["edges"]
+    s, t = graph["source"], graph["target"]
+    E = len(edges)
+    eu = torch.tensor([e[0] for e in edges], device=dev)
+    ev = torch.tensor([e[1] for e in edges], device=dev)
+    tail = torch.cat([eu, ev])
+    head = torch.cat([ev, eu])
+    arc_edge = torch.cat([torch.arange(E, device=dev)] * 2)
+    A = tail.numel()
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(int(seed) * 1_000_003 + 4)
+    found = None
+    rounds = 0
+    while (found is None or found.shape[0] < k) and rounds < 1000:
+        rounds += 1
+        w = torch.exp(sigma * torch.randn((batch, E), generator=gen, device=dev,
+                                          dtype=torch.float64))[:, arc_edge]
+        dist = torch.full((batch, n_nodes), float("inf"), device=dev, dtype=torch.float64)
+        dist[:, s] = 0.0
+        hidx = head.unsqueeze(0).expand(batch, A)
+        for _ in range(n_nodes):
+            cand = dist[:, tail] + w
+            new = dist.scatter_reduce(1, hidx, cand, reduce="amin", include_self=True)
+            if torch.equal(new, dist):
+                break
+            dist = new
+        tight = (dist[:, tail] + w == dist[:, head]) & torch.isfinite(dist[:, tail])
+        arc_ids = torch.where(tight, torch.arange(A, device=dev).unsqueeze(0), -1)
+        pred = torch.full((batch, n_nodes), -1, dtype=torch.int64, device=dev)
+        pred = pred.scatter_reduce(1, hidx, arc_ids, reduce="amax", include_self=True)
+        rows = torch.zeros((batch, E), dtype=torch.uint8, device=dev)
+        node = torch.full((batch,), t, dtype=torch.int64, device=dev)
+        ok = torch.isfinite(dist[:, t])
+        ar = torch.arange(batch, device=dev)
+        for _ in range(n_nodes):
+            active = ok & (node != s)
+            if not bool(active.any()):
+                break
+            a = pred[ar, node]
+            ok &= ~(active & (a < 0))
+            active &= a >= 0
+            rows[ar[active], arc_edge[a[active]]] = 1
+            node = torch.where(active, tail[a.clamp(min=0)], node)
+        rows = rows[ok & (node == s)]
+        found = rows if found is None else torch.cat([found, rows])
+        found = torch.unique(found, dim=0)
+    return found[:k].cpu().numpy()

@@ -125,6 +125,19 @@ def test_classifiers_match_oracle(n, m, s, kl, ku, p1):
     assert np.array_equal(got_bits, want)
 
 
+@pytest.mark.parametrize("chunk_tiles", ["1", "2", "3"])
+def test_reference_chunked_launches(chunk_tiles, monkeypatch):
+    # B split across several launches (lower tail + upper head in one chunk, etc.)
+    monkeypatch.setenv("RSR_TC_CHUNK_TILES", chunk_tiles)
+    n, m, s = 120, 2, 2500
+    rng = np.random.default_rng(17)
+    samples = (rng.random((s, n)) < 0.5).astype(np.int64)
+    lower = np.clip(samples[rng.integers(0, s, 700)] + rng.integers(0, 2, (700, n)), 0, 1)
+    upper = np.clip(samples[rng.integers(0, s, 600)] - rng.integers(0, 2, (600, n)), 0, 1)
+    got = _classify_tc(samples, lower, upper, n, m)
+    assert np.array_equal(got, _want_flags(samples, lower, upper, m))
+
+
 def test_first_match_and_violation_counts():
     rng = np.random.default_rng(3)
     n, m = 9, 3
