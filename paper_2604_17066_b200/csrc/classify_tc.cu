@@ -46,6 +46,7 @@ struct TcParams {
   uint8_t* flags;
   int accumulate;
   int debug;  // RSR_TC_DEBUG: bit0 = no B reloads after the first ring, bit1 = no TMEM loads
+  int a_bufs;  // pair kernel: 1 or 2 sample-tile buffers
 };
 
 // Reference tiles are visited in a per-CTA rotated order so that the 148 SMs
@@ -453,16 +454,18 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_addr(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
-  uint8_t* sA = smem;                                      // kb x 16 KB (this CTA's 128 rows)
-  uint8_t* sB = sA + (size_t)p.kb * kTileBytes;            // stages x 16 KB (128 ref rows)
+  // a_bufs x kb x 16 KB of A (this CTA's 128 rows; double-buffered so the next
+  // group's samples load while the current group's MMAs run), then the B ring.
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + (size_t)p.a_bufs * p.kb * kTileBytes;  // stages x 16 KB (128 ref rows)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * kTileBytes);
   uint64_t* b_full = bars;
   uint64_t* b_empty = bars + p.stages;
-  uint64_t* a_full = bars + 2 * p.stages;
-  uint64_t* a_empty = a_full + 1;
-  uint64_t* t_full = a_full + 2;   // [2]
-  uint64_t* t_empty = a_full + 4;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+  uint64_t* a_full = bars + 2 * p.stages;  // [2]
+  uint64_t* a_empty = a_full + 2;          // [2]
+  uint64_t* t_full = a_full + 4;           // [2]
+  uint64_t* t_empty = a_full + 6;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -479,9 +482,9 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_init(smem_addr(&b_full[i]), 2);
       mbar_init(smem_addr(&b_empty[i]), 1);
     }
-    mbar_init(smem_addr(a_full), 2);
-    mbar_init(smem_addr(a_empty), 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_addr(&a_full[i]), 2);
+      mbar_init(smem_addr(&a_empty[i]), 1);
       mbar_init(smem_addr(&t_full[i]), 1);
       mbar_init(smem_addr(&t_empty[i]), 16);
     }
@@ -500,24 +503,26 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer (both CTAs)
-    int stage = 0;
-    uint32_t phase = 0, a_phase = 0;
+    int stage = 0, gi = 0;
+    uint32_t phase = 0;
     const uint32_t sA0 = smem_addr(sA), sB0 = smem_addr(sB);
     const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
     const uint32_t a_bytes = (uint32_t)(2 * p.kb * kTileBytes);
-    for (int g = cluster; g < p.n_groups; g += n_clusters) {
-      mbar_wait(smem_addr(a_empty), a_phase ^ 1);
+    for (int g = cluster; g < p.n_groups; g += n_clusters, ++gi) {
+      const int ab = gi % p.a_bufs;
+      const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
+      const uint32_t bar_af = smem_addr(&a_full[ab]);
+      mbar_wait(smem_addr(&a_empty[ab]), a_par ^ 1);
       if (elect_one()) {
         if (leader)
-          mbar_expect_tx(smem_addr(a_full), a_bytes);
+          mbar_expect_tx(bar_af, a_bytes);
         else
-          mbar_arrive_leader(smem_addr(a_full));
+          mbar_arrive_leader(bar_af);
         for (int kb = 0; kb < p.kb; ++kb)
-          tma_load_2d_pair(sA0 + (uint32_t)kb * kTileBytes, &map_a, smem_addr(a_full),
+          tma_load_2d_pair(sA0 + (uint32_t)(ab * p.kb + kb) * kTileBytes, &map_a, bar_af,
                            kb * kKBlock, g * 2 * kTileM + (int)rank * kTileM);
       }
       __syncwarp();
-      a_phase ^= 1;
       for (int jj = 0; jj < p.nt_total; ++jj) {
         const int j = tile_at(jj, rot, p.nt_total);
         const bool low = j < p.nt_lower;
@@ -549,12 +554,13 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       const uint32_t a_lo0 = desc_lo(smem_addr(sA)), b_lo0 = desc_lo(smem_addr(sB));
       const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
       const int kb_full = (p.ksteps_last == kKBlock / kKStep) ? p.kb : p.kb - 1;
-      int stage = 0;
-      uint32_t phase = 0, a_phase = 0, tc = 0;
-      for (int g = cluster; g < p.n_groups; g += n_clusters) {
-        mbar_wait(smem_addr(a_full), a_phase);
-        a_phase ^= 1;
+      int stage = 0, gi = 0;
+      uint32_t phase = 0, tc = 0;
+      for (int g = cluster; g < p.n_groups; g += n_clusters, ++gi) {
+        const int ab = gi % p.a_bufs;
+        mbar_wait(smem_addr(&a_full[ab]), (uint32_t)(gi / p.a_bufs) & 1);
         tc_fence_after();
+        const uint32_t a_lo_g = a_lo0 + (uint32_t)(ab * p.kb) * (kTileBytes >> 4);
         for (int j = 0; j < p.nt_total; ++j, ++tc) {
           const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
           mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
@@ -564,7 +570,7 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             mbar_wait(bar_b_full + 8 * stage, phase);
             tc_fence_after();
             const uint32_t bl = b_lo0 + (uint32_t)stage * (kTileBytes >> 4);
-            const uint32_t al = a_lo0 + (uint32_t)kb * (kTileBytes >> 4);
+            const uint32_t al = a_lo_g + (uint32_t)kb * (kTileBytes >> 4);
             if (elect_one()) {
               if (kb < kb_full) {
 #pragma unroll
@@ -587,7 +593,7 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
           if (elect_one()) umma_commit_pair(smem_addr(&t_full[buf]));
           __syncwarp();
         }
-        if (elect_one()) umma_commit_pair(smem_addr(a_empty));
+        if (elect_one()) umma_commit_pair(smem_addr(&a_empty[ab]));
         __syncwarp();
       }
     }
@@ -627,7 +633,7 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       // the two column halves of a row live in two warps: combine through smem-free
       // atomics on the flags byte would race, so OR via a warp-pair exchange instead
       const int64_t row = (int64_t)g * 2 * kTileM + rank * kTileM + quad * 32 + lane;
-      uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 8);  // [128] scratch
+      uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 10);  // [128] scratch
       named_bar_sync(1, 256);
       if (colhalf == 1) xchg[quad * 32 + lane] = hit;
       named_bar_sync(1, 256);
@@ -749,7 +755,13 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
 
   if (impl != 1) {
     const size_t fixed = 1024 /*align slack*/ + 1024 /*barriers + exchange*/;
-    const size_t a_bytes = (size_t)p.kb * kTileBytes;
+    // double-buffer the sample tile when at least 4 B stages still fit
+    const char* ab_env = getenv("RSR_TC_ABUFS");
+    p.a_bufs = 2;
+    if ((ab_env && atoi(ab_env) == 1) ||
+        (size_t)2 * p.kb * kTileBytes + 4 * kTileBytes + fixed > max_smem)
+      p.a_bufs = 1;
+    const size_t a_bytes = (size_t)p.a_bufs * p.kb * kTileBytes;
     int stages = (int)((max_smem - fixed - a_bytes) / kTileBytes);
     if (stages > 12) stages = 12;
     RSR_REQUIRE(stages >= 2, "rsr_classify_tc: Kpad too large for shared memory");
