@@ -77,7 +77,11 @@ typedef struct rsr_phi_desc {
   const int32_t* edge_v;  /* device [N]                                        */
   const uint8_t* anchors; /* device [n_anchors * N]                            */
   const int32_t* anchor_level; /* device [n_anchors], 0-based level index      */
+  int32_t flags;          /* RSR_PHI_FLAG_* hints                              */
 } rsr_phi_desc;
+
+/* no two edges share their endpoints: enables the bitset-BFS kernels */
+#define RSR_PHI_FLAG_SIMPLE 1
 
 /* ---- library ---------------------------------------------------------- */
 int rsr_version(void);

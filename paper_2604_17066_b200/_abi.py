@@ -44,7 +44,11 @@ class PhiDesc(ctypes.Structure):
         ("edge_v", ctypes.c_void_p),
         ("anchors", ctypes.c_void_p),
         ("anchor_level", ctypes.c_void_p),
+        ("flags", ctypes.c_int32),
     ]
+
+
+PHI_FLAG_SIMPLE = 1
 
 
 _P, _I, _I64, _U64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double

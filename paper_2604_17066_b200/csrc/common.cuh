@@ -19,6 +19,12 @@ int check_launch(const char* what);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// csrc/phi_bits.cu: bitset-BFS Phi / boundary search for simple graphs
+// (returns -1 when not applicable).
+int phi_bits_dispatch(const rsr_phi_desc& d, bool boundary, int threshold, const uint8_t* states,
+                      const int64_t* idx, int64_t count, uint8_t* out, int64_t* count_leq,
+                      uint8_t* out_side, int64_t* out_calls, cudaStream_t st);
+
 // Thermometer geometry (see include/rsr_b200.h).
 inline int thermo_kdim(int n, int m) { return n * (m - 1); }
 inline int thermo_bias_cols(int n, int m) { return (thermo_kdim(n, m) + 126) / 127; }

@@ -11,6 +11,8 @@
 // shared memory, until a sweep changes nothing (or t is reached).  The result
 // equals the union-find answer of the reference: both compute the connected
 // component of s in the alive subgraph.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace {
@@ -286,6 +288,12 @@ extern "C" int rsr_phi_eval(const rsr_phi_desc* phi, const uint8_t* states, cons
   if (rc) return rc;
   RSR_REQUIRE(count >= 0, "rsr_phi_eval: negative count");
   if (count == 0) return RSR_OK;
+  const char* bits_env = getenv("RSR_PHI_BITS");
+  if (!(bits_env && atoi(bits_env) == 0)) {
+    const int r = rsr::phi_bits_dispatch(*phi, false, threshold, states, idx, count, out,
+                                         count_leq, nullptr, nullptr, rsr::as_stream(stream));
+    if (r != -1) return r;
+  }
   const size_t smem = phi_smem_bytes(*phi);
   if (smem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(phi_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -303,6 +311,12 @@ extern "C" int rsr_boundary_search(const rsr_phi_desc* phi, int threshold, const
   if (rc) return rc;
   RSR_REQUIRE(B >= 0, "rsr_boundary_search: negative count");
   if (B == 0) return RSR_OK;
+  const char* bits_env = getenv("RSR_PHI_BITS");
+  if (!(bits_env && atoi(bits_env) == 0)) {
+    const int r = rsr::phi_bits_dispatch(*phi, true, threshold, x0, nullptr, B, out_refs, nullptr,
+                                         out_side, out_calls, rsr::as_stream(stream));
+    if (r != -1) return r;
+  }
   const size_t smem = phi_smem_bytes(*phi);
   if (smem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(boundary_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

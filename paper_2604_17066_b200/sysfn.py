@@ -114,9 +114,14 @@ class DevicePerformance:
             al = _device.to_device(np.asarray(self.anchor_level, dtype=np.int32))
             n_anchors = an.shape[0]
             keep += [an, al]
+        flags = 0
+        if self.graph is not None:
+            pairs = {(min(u, v), max(u, v)) for u, v in self.graph.edges}
+            if len(pairs) == len(self.graph.edges):
+                flags |= _abi.PHI_FLAG_SIMPLE  # bitset-BFS kernels (csrc/phi_bits.cu)
         d = _abi.PhiDesc(self.kind, self.n_components, int(n_states), n_nodes, self.source,
                          self.target, self.k, n_anchors, _abi.ptr(eu), _abi.ptr(ev),
-                         _abi.ptr(an), _abi.ptr(al))
+                         _abi.ptr(an), _abi.ptr(al), flags)
         self._cache[key] = (d, keep)
         return d
 

@@ -182,28 +182,43 @@ def _grid(rows=5, cols=5):
     return rows * cols, edges
 
 
-def _phi_desc(kind, n_nodes, edges, s, t, m, k=0, keep=None):
+def _phi_desc(kind, n_nodes, edges, s, t, m, k=0, keep=None, flags=0):
     eu = _dev(np.array([e[0] for e in edges], dtype=np.int32))
     ev = _dev(np.array([e[1] for e in edges], dtype=np.int32))
-    d = A.PhiDesc(kind, len(edges), m, n_nodes, s, t, k, 0, eu.data_ptr(), ev.data_ptr(), None, None)
+    d = A.PhiDesc(kind, len(edges), m, n_nodes, s, t, k, 0, eu.data_ptr(), ev.data_ptr(), None, None,
+                  flags)
     if keep is not None:
         keep.extend([eu, ev])
     return d
 
 
-@pytest.mark.parametrize("kind,m", [(A.PHI_ST, 2), (A.PHI_WIDEST, 3), (A.PHI_GLOBAL, 2)])
-def test_phi_eval_and_boundary(kind, m):
-    nn, edges = _grid()
+def _nn_graph():
+    from paper_2604_17066_b200 import workloads as W
+    g = W.cfg3(0)
+    return g["n_nodes"], g["edges"], g["source"], g["target"]
+
+
+# flags 0: edge-sweep label propagation (csrc/phi.cu); flags 1: bitset BFS (csrc/phi_bits.cu)
+@pytest.mark.parametrize("flags", [0, A.PHI_FLAG_SIMPLE])
+@pytest.mark.parametrize("graph", ["grid", "nn119"])
+@pytest.mark.parametrize("kind,m", [(A.PHI_ST, 2), (A.PHI_WIDEST, 3), (A.PHI_GLOBAL, 2),
+                                    (A.PHI_ST, 3)])
+def test_phi_eval_and_boundary(kind, m, graph, flags):
+    if graph == "grid":
+        nn, edges = _grid()
+        s_node, t_node = 0, nn - 1
+    else:
+        nn, edges, s_node, t_node = _nn_graph()
     keep = []
-    d = _phi_desc(kind, nn, edges, 0, nn - 1, m, keep=keep)
+    d = _phi_desc(kind, nn, edges, s_node, t_node, m, keep=keep, flags=flags)
     rng = np.random.default_rng(kind)
     xs = rng.integers(0, m, size=(2000, len(edges)))
     if m == 2:
         xs = (rng.random((2000, len(edges))) < 0.7).astype(np.int64)
     if kind == A.PHI_ST:
-        ref = oracle.phi_st(nn, edges, 0, nn - 1)
+        ref = oracle.phi_st(nn, edges, s_node, t_node)
     elif kind == A.PHI_WIDEST:
-        ref = oracle.phi_widest(nn, edges, 0, nn - 1, m)
+        ref = oracle.phi_widest(nn, edges, s_node, t_node, m)
     else:
         ref = oracle.phi_global(nn, edges)
     want = np.array([ref(x) for x in xs])
@@ -219,9 +234,10 @@ def test_phi_eval_and_boundary(kind, m):
         refs = torch.empty((B, len(edges)), dtype=torch.uint8, device="cuda")
         side = torch.empty(B, dtype=torch.uint8, device="cuda")
         calls = torch.empty(B, dtype=torch.int64, device="cuda")
-        A.call("rsr_boundary_search", A.ctypes.byref(d), thr, A.ptr(_dev(x0.astype(np.uint8))), B,
+        x0d = _dev(x0.astype(np.uint8))
+        A.call("rsr_boundary_search", A.ctypes.byref(d), thr, A.ptr(x0d), B,
                A.ptr(refs), A.ptr(side), A.ptr(calls), A.stream_ptr())
-        for b in range(B):
+        for b in range(0, B, 1 if graph == "grid" else 8):
             ev = oracle.CountingPhi(ref, len(edges), m, ms)
             vec, sd = oracle.boundary_search(ev, x0[b], thr)
             assert tuple(refs[b].cpu().tolist()) == vec
