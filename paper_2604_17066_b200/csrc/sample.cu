@@ -32,10 +32,21 @@ __device__ void load_thresholds(const double* __restrict__ probs, int N, int M,
   __syncthreads();
 }
 
+// Row-end padding of one thermometer row: nbias ones then zeros up to ld.
+__device__ __forceinline__ void thermo_tail(int8_t* arow, int kdim, int nbias, int ld) {
+  for (int c = kdim; c < ld; ++c) arow[c] = (int8_t)(c < kdim + nbias);
+}
+
+// One Philox block (4 consecutive flat draws) per thread.  M2 specialises the
+// binary case (state = [r >= T_n], thermometer byte = 1 - state).  The row of
+// flat index fb is fb / N computed as a multiply-high by magic = floor(2^64/N)
+// plus one correction step.
+template <bool M2>
 __global__ void __launch_bounds__(kThreads)
 sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
               int64_t f0, int64_t f1, int64_t b_lo, int64_t nblk, uint8_t* __restrict__ states,
-              int8_t* __restrict__ thermo, int ld, int kdim, int nbias) {
+              int8_t* __restrict__ thermo, int ld, int kdim, int nbias, uint64_t magic,
+              int64_t start_row) {
   extern __shared__ unsigned long long T[];
   load_thresholds(probs, N, M, T);
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -43,31 +54,62 @@ sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uin
   const int64_t b = b_lo + t;
   uint64_t w[4];
   rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
-  const int64_t fb = 4 * b;
-  int64_t row = fb / N;
-  int n = (int)(fb - row * N);
-  const int64_t start_row = f0 / N;
+  const uint64_t fb = 4ull * (uint64_t)b;
+  uint64_t row = __umul64hi(fb, magic);
+  int n = (int)(fb - row * (uint64_t)N);
+  if (n >= N) {
+    n -= N;
+    ++row;
+  }
+  uint8_t st[4];
+  int ns[4];
+  int64_t rows[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int64_t f = fb + j;
-    if (f >= f0 && f < f1) {
-      const unsigned long long r = w[j] >> 11;
-      int st = 0;
+    const unsigned long long r = w[j] >> 11;
+    int s;
+    if (M2) {
+      s = r >= T[n] ? 1 : 0;
+    } else {
+      s = 0;
       const unsigned long long* Tn = T + n * (M - 1);
-      for (int m = 0; m < M - 1; ++m) st += (r >= Tn[m]) ? 1 : 0;
-      const int64_t i = row - start_row;
-      if (states) states[f - f0] = (uint8_t)st;
-      if (thermo) {
-        int8_t* arow = thermo + i * (int64_t)ld;
-        for (int k = 1; k < M; ++k) arow[n * (M - 1) + (k - 1)] = (int8_t)(st < k);
-        if (n == N - 1) {
-          for (int c = kdim; c < ld; ++c) arow[c] = (int8_t)(c < kdim + nbias);
-        }
-      }
+      for (int m = 0; m < M - 1; ++m) s += (r >= Tn[m]) ? 1 : 0;
     }
+    st[j] = (uint8_t)s;
+    ns[j] = n;
+    rows[j] = (int64_t)row - start_row;
     if (++n == N) {
       n = 0;
       ++row;
+    }
+  }
+  const bool full = (int64_t)fb >= f0 && (int64_t)fb + 3 < f1;
+  if (states) {
+    if (full && ((f0 & 3) == 0)) {
+      const uint32_t packed = (uint32_t)st[0] | ((uint32_t)st[1] << 8) | ((uint32_t)st[2] << 16) |
+                              ((uint32_t)st[3] << 24);
+      *reinterpret_cast<uint32_t*>(states + ((int64_t)fb - f0)) = packed;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t f = (int64_t)fb + j;
+        if (f >= f0 && f < f1) states[f - f0] = st[j];
+      }
+    }
+  }
+  if (thermo) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t f = (int64_t)fb + j;
+      if (full || (f >= f0 && f < f1)) {
+        int8_t* arow = thermo + rows[j] * (int64_t)ld;
+        if (M2) {
+          arow[ns[j]] = (int8_t)(1 - st[j]);
+        } else {
+          for (int k = 1; k < M; ++k) arow[ns[j] * (M - 1) + (k - 1)] = (int8_t)(st[j] < k);
+        }
+        if (ns[j] == N - 1) thermo_tail(arow, kdim, nbias, ld);
+      }
     }
   }
 }
@@ -248,14 +290,15 @@ extern "C" int rsr_sample(const double* probs, int n_components, int n_states, u
                 rsr::thermo_kpad(N, M));
   const size_t smem = (size_t)N * (M - 1) * sizeof(unsigned long long);
   RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample: N*(M-1) too large for the threshold table");
+  auto kern = M == 2 ? sample_kernel<true> : sample_kernel<false>;
   if (smem > 48 * 1024)
-    RSR_CUDA(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+    RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t f0 = start * N, f1 = (start + count) * N;
   const int64_t b_lo = f0 / 4, b_hi = (f1 - 1) / 4, nblk = b_hi - b_lo + 1;
-  sample_kernel<<<(unsigned)rsr::ceil_div(nblk, kThreads), kThreads, smem,
-                  rsr::as_stream(stream)>>>(probs, N, M, seed, gen, f0, f1, b_lo, nblk,
-                                            out_states, out_thermo, ld_thermo, kdim, nbias);
+  const uint64_t magic = ~0ull / (uint64_t)N;  // floor((2^64 - 1) / N)
+  kern<<<(unsigned)rsr::ceil_div(nblk, kThreads), kThreads, smem, rsr::as_stream(stream)>>>(
+      probs, N, M, seed, gen, f0, f1, b_lo, nblk, out_states, out_thermo, ld_thermo, kdim, nbias,
+      magic, start);
   return rsr::check_launch("sample_kernel");
 }
 

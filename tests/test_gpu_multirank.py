@@ -1,0 +1,85 @@
+"""Sharded Stage 1 / Stage 2 over 2 ranks reproduces the single-device results.
+
+Both ranks run on the one visible GPU with gloo collectives (host-side); no
+kernel waits on another rank, so sharing the device is safe.  On an 8-GPU node
+the same code runs with NCCL, one GPU per rank.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from _specs import load_json
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["grid_st_b8", "grid_widest_m3", "cones6"]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    sys.path.insert(0, here)
+    import torch
+    torch.cuda.set_device(0)
+    import paper_2604_17066_b200 as P
+    from paper_2604_17066_b200.dist import Comm
+    from _specs import device_model, load_json as lj
+    rec = next(c for c in lj("workflow.json") if c["spec"]["name"] == case)
+    spec = rec["spec"]
+    comm = Comm.from_env(backend="gloo")
+    model = device_model(spec["model"])
+    dist = P.ComponentDistribution(np.array(spec["probs"]))
+    cfg = P.RunConfig(**spec["config"])
+    out = []
+    for st in rec["stages"]:
+        s1 = P.stage1_find_references(model, dist, cfg, st["threshold"], comm)
+        rep = P.stage2_evaluate(model, dist, s1.lower, s1.upper, cfg, st["threshold"], comm)
+        out.append({
+            "lower": [list(v) for v in s1.lower.members],
+            "upper": [list(v) for v in s1.upper.members],
+            "trace": [[t.reference_count, t.phi_evaluations, t.p_lower, t.p_upper,
+                       t.p_unclassified] for t in s1.trace],
+            "iterations": s1.iterations, "redundant": s1.redundant_searches,
+            "p_lower": rep.p_lower, "unclassified_resolved": rep.unclassified_resolved,
+            "phi_total": model.evaluation_count})
+    q.put((rank, out))
+    import torch.distributed as dist_
+    dist_.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case", CASES)
+def test_two_rank_workflow_matches_single_device(case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=280) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    rec = next(c for c in load_json("workflow.json") if c["spec"]["name"] == case)
+    for rank in (0, 1):
+        for got, st in zip(res[rank], rec["stages"]):
+            want = st["stage1"]
+            assert got["lower"] == want["lower"] and got["upper"] == want["upper"]
+            assert got["trace"] == want["trace"]
+            assert got["iterations"] == want["iterations"]
+            assert got["redundant"] == want["redundant_searches"]
+            assert got["p_lower"] == st["stage2"]["p_lower"]
+            assert got["unclassified_resolved"] == st["stage2"]["unclassified_resolved"]
+            assert got["phi_total"] == st["stage2"]["phi_total"]

@@ -1,0 +1,52 @@
+"""CUDA-event timings of the non-classifier kernels on their config shapes."""
+
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_17066_b200 as P  # noqa: E402
+from paper_2604_17066_b200 import workloads as W  # noqa: E402
+
+
+def timed(fn, reps=10):
+    fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def main():
+    torch.cuda.set_device(0)
+    for m, probs in ((2, [0.1, 0.9]), (3, [0.05, 0.15, 0.8])):
+        d = P.ComponentDistribution.iid(295, probs)
+        S = 1 << 20
+        st = torch.empty((S, 295), dtype=torch.uint8, device="cuda")
+        th = torch.empty((S, P._abi.thermo_kpad(295, m)), dtype=torch.int8, device="cuda")
+        ms = timed(lambda: P.sample_batch(d, S, 0, 1, out_states=st, out_thermo=th))
+        print(f"sample_batch M={m} S=2^20 N=295: {ms:.3f} ms = {S * 295 / ms / 1e6:.1f} G draws/s")
+    g = W.cfg3(0)
+    graph = P.Graph(g["n_nodes"], tuple(g["edges"]))
+    for name, phi, m in (("st", P.single_od_connectivity(graph, g["source"], g["target"]), 2),
+                         ("widest", P.widest_path_level(graph, g["source"], g["target"]), 3)):
+        model = P.SystemModel(graph.n_edges, m, m, phi)
+        rng = np.random.default_rng(0)
+        x = torch.as_tensor(rng.integers(0, m, size=(4096, graph.n_edges)).astype(np.uint8)).cuda()
+        out = torch.empty(4096, dtype=torch.uint8, device="cuda")
+        ms = timed(lambda: phi.eval_into(x, None, 4096, m, out))
+        print(f"phi {name} 4096 vectors: {ms:.3f} ms = {ms * 1e3 / 4096:.2f} us/vector")
+        x0 = x[:64].contiguous()
+        ms = timed(lambda: P.boundary_search_batch(model, x0, 0), reps=3)
+        print(f"boundary_search {name} 64 searches: {ms:.3f} ms")
+
+
+if __name__ == "__main__":
+    main()
