@@ -452,11 +452,13 @@ def run_loop(args):
     cfg = P.RunConfig(**kw)
     t0 = time.perf_counter()
     stages = []
+    s1_first = None
     with ClockSampler(0) as clk:
         for thr in thresholds:
             ts = time.perf_counter()
             s1 = P.stage1_find_references(model, dist, cfg, thr)
             t1 = time.perf_counter()
+            s1_first = s1_first or s1
             if args.config == "cfg1":
                 rep = P.stage2_evaluate(model, dist, s1.lower, s1.upper, cfg, thr)
             else:
@@ -473,7 +475,39 @@ def run_loop(args):
     wall = time.perf_counter() - t0
     out.update({"value": wall, "stages": stages, "phi_evaluations": model.evaluation_count,
                 "clocks": clk.summary()})
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = loop_cpu_baseline(spec, probs, kw, thresholds[0], args.cpu_seconds,
+                                                gpu_trace=s1_first.trace if s1_first else None)
     print(json.dumps(out), flush=True)
+
+
+def loop_cpu_baseline(spec, probs, kw, threshold, budget, gpu_trace):
+    """Reference Stage-1 loop (oracle port, numpy Philox as in sampling.py, thread-pool
+    classify over all host cores, scalar union-find Phi) for `budget` seconds; compared
+    with the GPU's cumulative Stage-1 time at the same iteration count."""
+    import oracle
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _specs import oracle_phi
+    phi, n = oracle_phi(spec)
+    ev = oracle.CountingPhi(phi, n, spec["m"], spec["ms"])
+    cores = len(os.sched_getaffinity(0))
+    kw2 = dict(kw)
+    H = kw2.pop("n_samples")
+    res = oracle.stage1(ev, probs, threshold, H, n_workers=cores,
+                        chunk_size=max(256, H // (4 * cores)), time_budget=budget, fast=True,
+                        **kw2)
+    done = [t for t in res["trace"] if "elapsed" in t]
+    if not done:
+        return None
+    k = len(done)
+    cpu_s = done[-1]["elapsed"]
+    gpu_s = gpu_trace[k].elapsed_seconds if gpu_trace is not None and len(gpu_trace) > k else None
+    return {"value": cpu_s, "unit": "s", "cores": cores, "kind": "port",
+            "sample": f"first {k} Stage-1 iterations (threshold {threshold}) of the same run: "
+                      f"oracle port of workflow.py:122-195 with numpy Philox, ThreadPool classify "
+                      f"(n_workers={cores}), scalar union-find Phi",
+            "iterations": k, "gpu_seconds_same_iterations": gpu_s,
+            "speedup_same_iterations": (cpu_s / gpu_s) if gpu_s else None}
 
 
 def main():

@@ -31,17 +31,18 @@ UPPER = "upper"
 
 
 def sample_states(probs: np.ndarray, n_samples: int, seed: int, generation_index: int = 0,
-                  start: int = 0) -> np.ndarray:
+                  start: int = 0, fast: bool = False) -> np.ndarray:
     """Inverse-CDF draw on the Philox field (``sampling.py:69-90``).
 
     state[i, n] = #{m : cumsum(probs[n])[m] <= u[i, n]} clipped to M-1, which is
     ``np.searchsorted(cum[n], u, side="right")`` for the non-decreasing cum.
+    ``fast`` uses numpy's own Philox as the reference does (timing runs).
     """
     if n_samples < 1:
         raise ValueError("n_samples must be >= 1")
     probs = np.asarray(probs, dtype=np.float64)
     n, m = probs.shape
-    u = uniform_field(seed, generation_index, start, n_samples, n)
+    u = uniform_field(seed, generation_index, start, n_samples, n, fast=fast)
     cum = np.cumsum(probs, axis=1)
     out = np.empty((n_samples, n), dtype=np.int64)
     for comp in range(n):
@@ -321,19 +322,27 @@ class RefSet:
 def stage1(ev: CountingPhi, probs: np.ndarray, threshold: int, n_samples: int,
            eps_u: float = 1e-5, r_max: int = 10_000, seed: int = 0,
            parallel_searches: int = 1, boundary_search_enabled: bool = True,
-           chunk_size: int = 65536, n_workers: int = 1) -> dict:
+           chunk_size: int = 65536, n_workers: int = 1, time_budget: float | None = None,
+           fast: bool = False) -> dict:
     """Reference discovery loop (``workflow.py:122-195``).
 
     Trace records omit elapsed time and RSS (host-dependent); everything else
-    is restated field for field.
+    is restated field for field.  ``time_budget`` (seconds) stops the loop
+    early for CPU-baseline timing (terminated_by = "budget"); each trace
+    record then also carries the cumulative ``elapsed`` seconds.
     """
+    import time
     if not 0 <= threshold <= ev.ms - 2:
         raise ValueError("threshold out of range")
     lower, upper = RefSet(LOWER, threshold), RefSet(UPPER, threshold)
     trace, redundant, phi0, it = [], 0, ev.count, 0
     terminated_by = "r_max"
+    t0 = time.perf_counter()
     while True:
-        xs = sample_states(probs, n_samples, seed, it)
+        if time_budget is not None and trace and time.perf_counter() - t0 > time_budget:
+            terminated_by = "budget"
+            break
+        xs = sample_states(probs, n_samples, seed, it, fast=fast)
         res = classify_labels(xs, lower.array(ev.n), upper.array(ev.n), ev.m,
                               chunk_size, n_workers)
         n_l, n_u = res["lower_indices"].size, res["upper_indices"].size
@@ -363,6 +372,8 @@ def stage1(ev: CountingPhi, probs: np.ndarray, threshold: int, n_samples: int,
             tgt = lower if side == LOWER else upper
             if tgt.insert(vec) == "redundant":
                 redundant += 1
+        if time_budget is not None:
+            trace[-1]["elapsed"] = time.perf_counter() - t0
         it += 1
     return {"lower": list(lower.members), "upper": list(upper.members), "trace": trace,
             "iterations": it + 1, "redundant_searches": redundant,

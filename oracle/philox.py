@@ -79,8 +79,21 @@ def random_raw(seed: int, generation_index: int, first: int, count: int) -> np.n
 
 
 def uniform_field(seed: int, generation_index: int, start: int, count: int,
-                  n_components: int) -> np.ndarray:
-    """u[i, n] = (raw >> 11) * 2**-53 at flat index (start+i)*N + n (``sampling.py:45-66``)."""
-    raw = random_raw(seed, generation_index, start * n_components, count * n_components)
+                  n_components: int, fast: bool = False) -> np.ndarray:
+    """u[i, n] = (raw >> 11) * 2**-53 at flat index (start+i)*N + n (``sampling.py:45-66``).
+
+    ``fast`` draws the raws from ``numpy.random.Philox`` itself, exactly as the
+    reference does (used when *timing* the reference path; the restatement
+    above is what pins correctness, and tests check the two agree).
+    """
+    if fast:
+        mask = (1 << 64) - 1
+        bg = np.random.Philox(key=np.array([seed & mask, generation_index & mask],
+                                           dtype=np.uint64))
+        first = start * n_components
+        bg.advance(first // 4)
+        raw = bg.random_raw(first % 4 + count * n_components)[first % 4:]
+    else:
+        raw = random_raw(seed, generation_index, start * n_components, count * n_components)
     u = (raw >> np.uint64(11)).astype(np.float64) * float(2.0 ** -53)
     return u.reshape(count, n_components)

@@ -122,3 +122,19 @@ def test_assemble_pmf_and_cov_known_answers():
         oracle.cov(1.5, 100)
     with pytest.raises(ValueError):
         oracle.cov(0.5, 0)
+
+
+def test_fast_sampler_equals_restatement():
+    # the timing path draws with numpy's own Philox (as the reference does)
+    probs = np.tile([0.2, 0.5, 0.3], (11, 1))
+    for seed, gen, start in [(0, 0, 0), (5, 3, 17), (2**64 - 1, 2**40, 1001)]:
+        a = oracle.sample_states(probs, 77, seed, gen, start)
+        b = oracle.sample_states(probs, 77, seed, gen, start, fast=True)
+        assert np.array_equal(a, b)
+
+
+def test_stage1_time_budget_records_elapsed():
+    ev = oracle.CountingPhi(oracle.phi_kofn(3, 3), 3, 2, 2)
+    r = oracle.stage1(ev, np.tile([0.1, 0.9], (3, 1)), 0, 2000, eps_u=1e-3, r_max=50, seed=7,
+                      time_budget=1e-9)
+    assert r["terminated_by"] == "budget" and "elapsed" in r["trace"][0]
