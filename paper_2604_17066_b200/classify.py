@@ -38,6 +38,9 @@ __all__ = ["ClassificationResult", "InconsistentReferenceSets", "violation_count
            "cov", "DEFAULT_CHUNK_SIZE", "classify_flags"]
 
 DEFAULT_CHUNK_SIZE = 65536
+# widest thermometer row the tensor-core kernel keeps resident (6 x 128 bytes);
+# wider rows (N(M-1) > ~760) go to the bit-packed kernel
+TC_MAX_KPAD = 768
 
 
 class InconsistentReferenceSets(ValueError):
@@ -187,7 +190,8 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
     m_eff = max(2, n_states, batch.state_bound)
     fl = fu = None
     st = _device.stream()
-    if method == "tc" and not want_first:
+    tc_ok = _abi.thermo_kpad(batch.n_components, m_eff) <= TC_MAX_KPAD
+    if method == "tc" and not want_first and tc_ok:
         a = batch.thermo(m_eff)
         bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
         bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)

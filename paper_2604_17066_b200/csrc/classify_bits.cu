@@ -95,6 +95,38 @@ classify_bits_kernel(const uint32_t* __restrict__ sbits, int64_t S,
   }
 }
 
+// Any row width: one thread per sample, words streamed from global memory (L1
+// caches the sample row; reference rows are read by every thread of the warp
+// at the same address, i.e. broadcast).
+__global__ void classify_bits_wide_kernel(const uint32_t* __restrict__ sbits, int64_t S,
+                                          const uint32_t* __restrict__ lbits, int64_t nl,
+                                          const uint32_t* __restrict__ ubits, int64_t nu,
+                                          int W, uint8_t* __restrict__ flags,
+                                          int64_t* __restrict__ first_l,
+                                          int64_t* __restrict__ first_u, int acc) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const uint32_t* a = sbits + s * W;
+  uint32_t hit = 0;
+  int64_t fst[2] = {-1, -1};
+  for (int side = 0; side < 2; ++side) {
+    const uint32_t* refs = side ? ubits : lbits;
+    const int64_t n = side ? nu : nl;
+    for (int64_t r = 0; r < n; ++r) {
+      const uint32_t* b = refs + r * W;
+      uint32_t v = 0;
+      for (int w = 0; w < W && !v; ++w) v |= (side ? a[w] : ~a[w]) & b[w];
+      if (v == 0) {
+        hit |= side ? RSR_HIT_UPPER : RSR_HIT_LOWER;
+        if (fst[side] < 0) fst[side] = r;
+      }
+    }
+  }
+  flags[s] = (uint8_t)((acc ? flags[s] : 0) | hit);
+  if (first_l) first_l[s] = fst[0];
+  if (first_u) first_u[s] = fst[1];
+}
+
 __global__ void finalize_kernel(const uint8_t* __restrict__ flags, int64_t S,
                                 uint8_t* __restrict__ labels, unsigned long long* counts) {
   __shared__ unsigned long long bc[4];
@@ -274,9 +306,16 @@ extern "C" int rsr_classify_bits(const uint32_t* sample_bits, int64_t S,
                                  uint8_t* flags, int64_t* first_lower, int64_t* first_upper,
                                  int accumulate, void* stream) {
   RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_bits: negative size");
-  RSR_REQUIRE(words >= 1 && words <= 32, "rsr_classify_bits: 1 <= words <= 32 (Kdim <= 1024)");
+  RSR_REQUIRE(words >= 1, "rsr_classify_bits: words >= 1");
   if (S == 0) return RSR_OK;
   cudaStream_t st = rsr::as_stream(stream);
+  if (words > 32) {  // wide rows (N(M-1) > 1024): generic-width kernel
+    const unsigned grid = (unsigned)rsr::ceil_div(S, 128);
+    classify_bits_wide_kernel<<<grid, 128, 0, st>>>(sample_bits, S, lower_bits, n_lower, upper_bits,
+                                                    n_upper, words, flags, first_lower,
+                                                    first_upper, accumulate);
+    return rsr::check_launch("classify_bits_wide_kernel");
+  }
   switch (words) {
 #define RSR_W(w) \
   case w:        \

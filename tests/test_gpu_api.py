@@ -158,6 +158,23 @@ def test_classify_random_vs_oracle(seed):
         assert np.array_equal(r.labels_device.cpu().numpy(), want["labels"])
 
 
+@pytest.mark.parametrize("n,m", [(300, 4), (400, 4), (700, 3)])
+def test_classify_wide_rows_vs_oracle(n, m):
+    # N(M-1) beyond the tensor-core row limit (and beyond 32 bit-words): bit-packed path
+    rng = np.random.default_rng(n * m)
+    h = 700
+    samples = rng.integers(0, m, size=(h, n))
+    lower = np.clip(samples[rng.integers(0, h, 25)] + rng.integers(0, 2, (25, n)), 0, m - 1)
+    upper = np.clip(samples[rng.integers(0, h, 25)] - rng.integers(0, 2, (25, n)), 0, m - 1)
+    want = oracle.classify_labels(samples, lower, upper, m, want_first=True)
+    lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
+    r = P.classify(P.SampleBatch(samples, 0, 0), lo, up, n_states=m, explain=True)
+    assert np.array_equal(r.labels_device.cpu().numpy(), want["labels"])
+    assert np.array_equal(r.first_match_lower, want["first_lower"])
+    assert np.array_equal(r.first_match_upper, want["first_upper"])
+
+
 def _cfg2_sets(mixed, k=10_000, seed=0):
     from paper_2604_17066_b200 import workloads as W
     lower, upper = (W.cfg2_mixed_refs if mixed else W.cfg2_refs)(seed, 295, k, k)
