@@ -1,0 +1,88 @@
+"""Randomised parity sweeps: device path vs the CPU oracle, bit-exact.
+
+The oracle is pinned to the reference by tests/test_oracle_golden.py; here
+random coherent systems (the reference suite's cone-sum construction,
+tests/conftest.py:53-75), random distributions and random classifier shapes
+exercise the device path far beyond the fixed golden cases.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2604_17066_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_system(rng):
+    n, m, ms = int(rng.integers(2, 9)), int(rng.integers(2, 5)), int(rng.integers(2, 4))
+    levels = [[[int(v) for v in rng.integers(0, m, size=n)] for _ in range(int(rng.integers(1, 4)))]
+              for _ in range(ms - 1)]
+    raw = rng.random((n, m)) + 0.05
+    probs = raw / raw.sum(1, keepdims=True)
+    return n, m, ms, levels, probs
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_cone_systems_workflow(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n, m, ms, levels, probs = _random_system(rng)
+    cfg = dict(n_samples=int(rng.integers(500, 4000)), eps_u=float(rng.choice([1e-2, 1e-3])),
+               r_max=int(rng.integers(5, 200)), seed=int(rng.integers(0, 2**31)),
+               parallel_searches=int(rng.integers(1, 9)),
+               boundary_search_enabled=bool(rng.random() < 0.85))
+    model = P.SystemModel(n, m, ms, P.cone_sum(levels, n))
+    dist = P.ComponentDistribution(probs)
+    ev = oracle.CountingPhi(oracle.phi_cones(levels), n, m, ms)
+    for thr in range(ms - 1):
+        s1 = P.stage1_find_references(model, dist, P.RunConfig(**cfg), thr)
+        o1 = oracle.stage1(ev, probs, thr, **cfg)
+        assert s1.lower.members == o1["lower"] and s1.upper.members == o1["upper"]
+        assert [[t.reference_count, t.phi_evaluations, t.p_lower, t.p_upper, t.p_unclassified]
+                for t in s1.trace] == [[t["reference_count"], t["phi_evaluations"], t["p_lower"],
+                                        t["p_upper"], t["p_unclassified"]] for t in o1["trace"]]
+        assert (s1.iterations, s1.redundant_searches, s1.terminated_by) == (
+            o1["iterations"], o1["redundant_searches"], o1["terminated_by"])
+        rep = P.stage2_evaluate(model, dist, s1.lower, s1.upper, P.RunConfig(**cfg), thr)
+        o2 = oracle.stage2(ev, probs, o1["lower"], o1["upper"], thr, cfg["n_samples"], cfg["seed"])
+        assert (rep.p_lower, rep.p_upper, rep.unclassified_resolved) == (
+            o2["p_lower"], o2["p_upper"], o2["unclassified_resolved"])
+        assert model.evaluation_count == ev.count
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_classifier_shapes(seed):
+    rng = np.random.default_rng(2000 + seed)
+    n = int(rng.choice([1, 2, 7, 31, 33, 64, 100, 127, 128, 129, 295, 380]))
+    m = int(rng.integers(2, 4)) if n > 200 else int(rng.integers(2, 6))
+    h = int(rng.choice([1, 2, 255, 256, 257, 511, 1000, 3333]))
+    kl, ku = int(rng.choice([0, 1, 255, 256, 257, 600])), int(rng.choice([0, 1, 255, 256, 257, 600]))
+    samples = rng.integers(0, m, size=(h, n))
+    base_l = samples[rng.integers(0, h, kl)] if kl else np.zeros((0, n), dtype=np.int64)
+    base_u = samples[rng.integers(0, h, ku)] if ku else np.zeros((0, n), dtype=np.int64)
+    lower = np.clip(base_l + rng.integers(0, 2, base_l.shape), 0, m - 1)
+    upper = np.clip(base_u - rng.integers(0, 2, base_u.shape), 0, m - 1)
+    want = oracle.classify_labels(samples, lower, upper, m)["labels"]
+    lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
+    batch = P.SampleBatch(samples, 0, 0)
+    for method in ("tc", "bits"):
+        r = P.classify(batch, lo, up, n_states=m, method=method)
+        assert np.array_equal(r.labels_device.cpu().numpy(), want), (method, n, m, h, kl, ku)
+        assert r.counts == (int((want == 0).sum()), int((want == 1).sum()), int((want == 2).sum()))
+        assert np.array_equal(r.unclassified_indices, np.flatnonzero(want == 2))
+
+
+def test_sampling_random_tables_and_offsets():
+    rng = np.random.default_rng(7)
+    for _ in range(8):
+        n, m = int(rng.integers(1, 60)), int(rng.integers(2, 7))
+        raw = rng.random((n, m)) ** 3
+        raw[rng.random((n, m)) < 0.2] = 0.0
+        raw[:, 0] += 1e-3
+        probs = raw / raw.sum(1, keepdims=True)
+        count, start = int(rng.integers(1, 3000)), int(rng.integers(0, 10**6))
+        seed, gen = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**40))
+        b = P.sample_batch(P.ComponentDistribution(probs), count, seed, gen, start)
+        assert np.array_equal(b.states, oracle.sample_states(probs, count, seed, gen, start))
