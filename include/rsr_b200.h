@@ -130,6 +130,12 @@ int rsr_packbits_rows(const uint8_t* rows, int64_t count, int row_len, int compl
 int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower,
                     int64_t n_lower, const int8_t* B_upper, int64_t n_upper,
                     int Kpad, uint8_t* flags, int accumulate, void* stream);
+/* Same, also recording per sample the smallest matching reference index of each
+ * side (int64, -1 when none; explain / strict, classify.py:99-118, 226-238). */
+int rsr_classify_tc_explain(const int8_t* A, int64_t S, const int8_t* B_lower,
+                            int64_t n_lower, const int8_t* B_upper, int64_t n_upper,
+                            int Kpad, uint8_t* flags, int64_t* first_lower,
+                            int64_t* first_upper, int accumulate, void* stream);
 /* Bit-packed CUDA-core comparison variant (AND + OR-reduce, LOP3).
  * Packs states on the fly; optional first-match indices (explain / strict,
  * classify.py:99-118): first_lower / first_upper int64 [S] or NULL. */

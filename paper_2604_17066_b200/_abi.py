@@ -67,6 +67,7 @@ EXPORTED = {
     "rsr_encode_rows": (_I, [_P, _I64, _I, _I, _I, _P, _P]),
     "rsr_packbits_rows": (_I, [_P, _I64, _I, _I, _P, _P]),
     "rsr_classify_tc": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _I, _P]),
+    "rsr_classify_tc_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_classify_bits": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_finalize": (_I, [_P, _I64, _P, _P, _P]),

@@ -191,12 +191,18 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
     fl = fu = None
     st = _device.stream()
     tc_ok = _abi.thermo_kpad(batch.n_components, m_eff) <= TC_MAX_KPAD
-    if method == "tc" and not want_first and tc_ok:
+    if method == "tc" and tc_ok:
         a = batch.thermo(m_eff)
         bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
         bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
-        _abi.call("rsr_classify_tc", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu), nu,
-                  a.shape[1], _abi.ptr(flags), 0, st)
+        if want_first:  # first-match indices from the tensor-core epilogue
+            fl = torch.empty(H, dtype=torch.int64, device=dev)
+            fu = torch.empty(H, dtype=torch.int64, device=dev)
+            _abi.call("rsr_classify_tc_explain", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu),
+                      nu, a.shape[1], _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
+        else:
+            _abi.call("rsr_classify_tc", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu), nu,
+                      a.shape[1], _abi.ptr(flags), 0, st)
     elif method in ("bits", "tc"):
         sb = batch.thermo_bits(m_eff)
         lb, nl = lower_set.device_bits(m_eff) if lower_set is not None else (None, 0)

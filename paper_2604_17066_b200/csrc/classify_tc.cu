@@ -47,6 +47,10 @@ struct TcParams {
   int accumulate;
   int debug;  // RSR_TC_DEBUG: bit0 = no B reloads after the first ring, bit1 = no TMEM loads
   int a_bufs;  // pair kernel: 1 or 2 sample-tile buffers
+  int64_t* first_lower;  // pair kernel FIRST variant: smallest matching ref index, -1 if none
+  int64_t* first_upper;
+  int64_t first_base_lower;  // reference index of this launch's first lower / upper row
+  int64_t first_base_upper;
 };
 
 // Reference tiles are visited in a per-CTA rotated order so that the 148 SMs
@@ -447,6 +451,7 @@ __device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+template <bool FIRST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_lower,
@@ -604,6 +609,10 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     uint32_t tc = 0;
     for (int g = cluster; g < p.n_groups; g += n_clusters) {
       uint32_t hit = 0;
+      // FIRST: smallest matching reference index per side (accumulator column n
+      // of pair tile j is reference j*256 + n: columns 0-127 come from CTA 0's
+      // B half, 128-255 from CTA 1's)
+      int64_t first[2] = {INT64_MAX, INT64_MAX};
       for (int jj = 0; jj < p.nt_total; ++jj, ++tc) {
         const int j = tile_at(jj, rot, p.nt_total);
         const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
@@ -612,6 +621,7 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         const uint32_t taddr =
             tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kPairN + colhalf * kTileN;
         uint32_t mn = 0xFFFFFFFFu;
+        int zero_col = -1;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           if (p.debug & 2) {
@@ -622,26 +632,63 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
           RSR_LD32(taddr + half * 64, v);
           RSR_LD32(taddr + half * 64 + 32, (v + 32));
           tmem_ld_wait();
+          uint32_t mh = 0xFFFFFFFFu;
 #pragma unroll
-          for (int i = 0; i < 64; ++i) mn = min(mn, v[i]);
+          for (int i = 0; i < 64; ++i) mh = min(mh, v[i]);
+          if (FIRST && mh == 0 && zero_col < 0) {
+            for (int i = 0; i < 64; ++i)
+              if (v[i] == 0) {
+                zero_col = half * 64 + i;
+                break;
+              }
+          }
+          mn = min(mn, mh);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_leader(smem_addr(&t_empty[buf]));
-        if (mn == 0) hit |= (j < p.nt_lower) ? RSR_HIT_LOWER : RSR_HIT_UPPER;
+        if (mn == 0) {
+          const bool low = j < p.nt_lower;
+          hit |= low ? RSR_HIT_LOWER : RSR_HIT_UPPER;
+          if (FIRST) {
+            const int64_t ref = (low ? p.first_base_lower + (int64_t)j * kPairN
+                                     : p.first_base_upper + (int64_t)(j - p.nt_lower) * kPairN) +
+                                colhalf * kTileN + zero_col;
+            first[low ? 0 : 1] = min(first[low ? 0 : 1], ref);
+          }
+        }
       }
       // the two column halves of a row live in two warps: combine through smem-free
       // atomics on the flags byte would race, so OR via a warp-pair exchange instead
       const int64_t row = (int64_t)g * 2 * kTileM + rank * kTileM + quad * 32 + lane;
       uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 10);  // [128] scratch
+      int64_t* xfirst = reinterpret_cast<int64_t*>(xchg + 128);   // [2][128] (FIRST)
       named_bar_sync(1, 256);
-      if (colhalf == 1) xchg[quad * 32 + lane] = hit;
+      if (colhalf == 1) {
+        xchg[quad * 32 + lane] = hit;
+        if (FIRST) {
+          xfirst[quad * 32 + lane] = first[0];
+          xfirst[128 + quad * 32 + lane] = first[1];
+        }
+      }
       named_bar_sync(1, 256);
       if (colhalf == 0) {
         hit |= xchg[quad * 32 + lane];
         if (row < p.S) {
           const uint8_t prev = p.accumulate ? p.flags[row] : 0;
           p.flags[row] = (uint8_t)(prev | hit);
+          if (FIRST) {
+#pragma unroll
+            for (int sd = 0; sd < 2; ++sd) {
+              int64_t* out = sd ? p.first_upper : p.first_lower;
+              if (!out) continue;
+              const int64_t f = min(first[sd], xfirst[sd * 128 + quad * 32 + lane]);
+              const int64_t mine = f == INT64_MAX ? -1 : f;
+              // chunks run in increasing reference order: an earlier chunk's hit wins
+              const int64_t old = p.accumulate ? out[row] : -1;
+              out[row] = old >= 0 ? old : mine;
+            }
+          }
         }
       }
     }
@@ -702,9 +749,12 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& ml, const CUtensorMap& m
 
 }  // namespace
 
-extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower, int64_t n_lower,
-                               const int8_t* B_upper, int64_t n_upper, int Kpad, uint8_t* flags,
-                               int accumulate, void* stream) {
+namespace {
+
+int classify_tc_impl(const int8_t* A, int64_t S, const int8_t* B_lower, int64_t n_lower,
+                     const int8_t* B_upper, int64_t n_upper, int Kpad, uint8_t* flags,
+                     int accumulate, int64_t* first_lower, int64_t* first_upper, void* stream) {
+  const bool want_first = first_lower != nullptr || first_upper != nullptr;
   RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_tc: negative size");
   RSR_REQUIRE(Kpad >= 32 && Kpad % 32 == 0, "rsr_classify_tc: Kpad must be a multiple of 32");
   RSR_REQUIRE(Kpad <= 6 * kKBlock, "rsr_classify_tc: Kpad > 768 unsupported");
@@ -720,7 +770,10 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
   if (nt_l + nt_u == 0) {
     if (!accumulate) {
       clear_flags_kernel<<<(unsigned)rsr::ceil_div(S, 256), 256, 0, st>>>(flags, S);
-      return rsr::check_launch("clear_flags_kernel");
+      int rc0 = rsr::check_launch("clear_flags_kernel");
+      if (rc0) return rc0;
+      for (int64_t* f : {first_lower, first_upper})
+        if (f) RSR_CUDA(cudaMemsetAsync(f, 0xFF, S * sizeof(int64_t), st));  // -1
     }
     return RSR_OK;
   }
@@ -749,12 +802,16 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
   p.nt_total = (int)(nt_l + nt_u);
   p.flags = flags;
   p.accumulate = accumulate;
+  p.first_lower = first_lower;
+  p.first_upper = first_upper;
+  p.first_base_lower = p.first_base_upper = 0;
   const char* dbg = getenv("RSR_TC_DEBUG");
   p.debug = dbg ? atoi(dbg) : 0;
   const size_t max_smem = 227 * 1024;
 
   if (impl != 1) {
-    const size_t fixed = 1024 /*align slack*/ + 1024 /*barriers + exchange*/;
+    // align slack + barriers + hit exchange (+ first-match exchange, 2 x 128 int64)
+    const size_t fixed = 1024 + 1024 + (want_first ? 2048 : 0);
     // double-buffer the sample tile when at least 4 B stages still fit
     const char* ab_env = getenv("RSR_TC_ABUFS");
     p.a_bufs = 2;
@@ -768,8 +825,8 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
     p.stages = stages;
     const size_t smem = fixed + a_bytes + (size_t)stages * kTileBytes;
     p.n_groups = (int)rsr::ceil_div(S, (int64_t)2 * kTileM);
-    RSR_CUDA(cudaFuncSetAttribute(classify_tc_pair_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = want_first ? classify_tc_pair_kernel<true> : classify_tc_pair_kernel<false>;
+    RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int clusters = sm_count / 2;
     if (p.n_groups < clusters) clusters = p.n_groups;
     // Reference chunks: every group streams all tiles of a launch, so a launch's
@@ -786,6 +843,8 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
       q.nt_lower = (int)(l1 - l0);
       q.nt_total = (int)((l1 - l0) + (u1 - u0));
       q.accumulate = c0 == 0 ? accumulate : 1;
+      q.first_base_lower = l0 * kPairN;
+      q.first_base_upper = u0 * kPairN;
       CUtensorMap cl = ml, cu = mu;
       if (total > chunk) {
         const int8_t* lb = l1 > l0 ? B_lower + l0 * kPairN * (int64_t)Kpad : nullptr;
@@ -795,13 +854,14 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
         rc = make_map(&cu, ub ? ub : lb, ((ub ? u1 - u0 : l1 - l0)) * kPairN, Kpad);
         if (rc) return rc;
       }
-      classify_tc_pair_kernel<<<2 * clusters, 384, smem, st>>>(ma, cl, cu, q);
+      kern<<<2 * clusters, 384, smem, st>>>(ma, cl, cu, q);
       rc = rsr::check_launch("classify_tc_pair_kernel");
       if (rc) return rc;
     }
     return RSR_OK;
   }
 
+  RSR_REQUIRE(!want_first, "rsr_classify_tc: first-match needs the CTA-pair kernel");
   const size_t fixed = 1024 /*align slack*/ + 256 /*barriers*/;
   const int mt = ((size_t)2 * p.kb * kTileBytes + 4 * kTileBytes + fixed <= max_smem) ? 2 : 1;
   const size_t a_bytes = (size_t)mt * p.kb * kTileBytes;
@@ -813,4 +873,21 @@ extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower
   p.n_groups = (int)rsr::ceil_div(S, (int64_t)mt * kTileM);
   if (mt == 2) return launch_tc<2>(ma, ml, mu, p, smem, sm_count, st);
   return launch_tc<1>(ma, ml, mu, p, smem, sm_count, st);
+}
+
+}  // namespace
+
+extern "C" int rsr_classify_tc(const int8_t* A, int64_t S, const int8_t* B_lower, int64_t n_lower,
+                               const int8_t* B_upper, int64_t n_upper, int Kpad, uint8_t* flags,
+                               int accumulate, void* stream) {
+  return classify_tc_impl(A, S, B_lower, n_lower, B_upper, n_upper, Kpad, flags, accumulate,
+                          nullptr, nullptr, stream);
+}
+
+extern "C" int rsr_classify_tc_explain(const int8_t* A, int64_t S, const int8_t* B_lower,
+                                       int64_t n_lower, const int8_t* B_upper, int64_t n_upper,
+                                       int Kpad, uint8_t* flags, int64_t* first_lower,
+                                       int64_t* first_upper, int accumulate, void* stream) {
+  return classify_tc_impl(A, S, B_lower, n_lower, B_upper, n_upper, Kpad, flags, accumulate,
+                          first_lower, first_upper, stream);
 }

@@ -99,7 +99,7 @@ def test_classify_golden(method):
         assert np.array_equal(r.lower_indices, g[f"lo_idx{i}"])
         assert np.array_equal(r.upper_indices, g[f"up_idx{i}"])
         assert np.array_equal(r.unclassified_indices, g[f"un_idx{i}"])
-        e = P.classify(batch, lo, up, n_states=m, explain=True)
+        e = P.classify(batch, lo, up, n_states=m, explain=True, method=method)
         assert np.array_equal(e.first_match_lower, g[f"first_lo{i}"])
         assert np.array_equal(e.first_match_upper, g[f"first_up{i}"])
 
@@ -156,6 +156,24 @@ def test_classify_random_vs_oracle(seed):
     for method in ("tc", "bits"):
         r = P.classify(P.SampleBatch(samples, 0, 0), lo, up, n_states=m, method=method)
         assert np.array_equal(r.labels_device.cpu().numpy(), want["labels"])
+
+
+@pytest.mark.parametrize("chunk_tiles", ["1", "256"])
+def test_explain_first_match_tensor_core_chunked(chunk_tiles, monkeypatch):
+    # first-match indices from the tensor-core epilogue, also across chunked launches
+    monkeypatch.setenv("RSR_TC_CHUNK_TILES", chunk_tiles)
+    rng = np.random.default_rng(9)
+    n, m, h = 60, 3, 3000
+    samples = rng.integers(0, m, size=(h, n))
+    lower = np.clip(samples[rng.integers(0, h, 700)] + rng.integers(0, 2, (700, n)), 0, m - 1)
+    upper = np.clip(samples[rng.integers(0, h, 900)] - rng.integers(0, 2, (900, n)), 0, m - 1)
+    want = oracle.classify_labels(samples, lower, upper, m, want_first=True)
+    lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
+    r = P.classify(P.SampleBatch(samples, 0, 0), lo, up, n_states=m, explain=True, method="tc")
+    assert np.array_equal(r.labels_device.cpu().numpy(), want["labels"])
+    assert np.array_equal(r.first_match_lower, want["first_lower"])
+    assert np.array_equal(r.first_match_upper, want["first_upper"])
 
 
 @pytest.mark.parametrize("n,m", [(300, 4), (400, 4), (700, 3)])
