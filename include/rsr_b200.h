@@ -63,6 +63,7 @@ extern "C" {
 #define RSR_PHI_GLOBAL_CONNECTIVITY 2 /* sysfn.py:101-109                     */
 #define RSR_PHI_K_OUT_OF_N 3       /* sysfn.py:177-185                        */
 #define RSR_PHI_CONE_SUM 4         /* sum_l [x >= some anchor of level l]     */
+#define RSR_PHI_EDGE_DISJOINT 5    /* sysfn.py:140-174 min_t maxflow(0,t) capped at k */
 
 typedef struct rsr_phi_desc {
   int32_t kind;

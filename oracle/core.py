@@ -20,6 +20,7 @@ from .philox import uniform_field
 __all__ = [
     "sample_states", "encode", "dominance_hits", "classify_labels", "violation_counts",
     "cov", "UnionFind", "phi_st", "phi_global", "phi_kofn", "phi_widest", "phi_cones",
+    "phi_edge_disjoint",
     "CountingPhi", "boundary_search", "RefSet", "stage1", "stage2", "assemble_pmf",
     "multistate_pmf", "LOWER", "UPPER",
 ]
@@ -211,6 +212,56 @@ def phi_global(n_nodes: int, edges):
         uf = _alive_uf(n_nodes, edges, x)
         r = uf.find(0)
         return int(all(uf.find(v) == r for v in range(1, n_nodes)))
+    return phi
+
+
+def _unit_max_flow(n_nodes: int, arcs, s: int, t: int, cap_limit: int) -> int:
+    """Edge-disjoint s-t path count by BFS augmentation, stopped at cap_limit (``sysfn.py:112-137``).
+
+    ``arcs`` is a list of (tail, head); arc 2e and 2e+1 are the two directions of
+    edge e (unit capacity each); augmenting along arc a moves one unit to a ^ 1.
+    """
+    res = [1] * len(arcs)
+    flow = 0
+    while flow < cap_limit:
+        parent = [-1] * n_nodes
+        parent[s] = -2
+        frontier = [s]
+        while frontier and parent[t] == -1:
+            nxt = []
+            for a, (u, v) in enumerate(arcs):
+                if res[a] > 0 and parent[v] == -1 and parent[u] != -1 and u in frontier:
+                    parent[v] = a
+                    nxt.append(v)
+            frontier = nxt
+        if parent[t] == -1:
+            break
+        v = t
+        while v != s:
+            a = parent[v]
+            res[a] -= 1
+            res[a ^ 1] += 1
+            v = arcs[a][0]
+        flow += 1
+    return flow
+
+
+def phi_edge_disjoint(n_nodes: int, edges, max_level: int):
+    """Min over targets of capped unit max-flows from node 0 (``sysfn.py:140-174``)."""
+    if max_level < 1 or n_nodes < 2:
+        raise ValueError("bad edge_disjoint_level parameters")
+
+    def phi(x):
+        arcs = []
+        for e, (u, v) in enumerate(edges):
+            if x[e] >= 1:
+                arcs += [(u, v), (v, u)]
+        level = max_level
+        for t in range(1, n_nodes):
+            level = min(level, _unit_max_flow(n_nodes, arcs, 0, t, level))
+            if level == 0:
+                return 0
+        return level
     return phi
 
 

@@ -25,7 +25,7 @@ RSR_OK, RSR_EINVAL, RSR_ECUDA, RSR_EUNSUPPORTED = 0, 1, 2, 3
 SIDE_LOWER, SIDE_UPPER = 0, 1
 HIT_LOWER, HIT_UPPER = 1, 2
 LABEL_LOWER, LABEL_UPPER, LABEL_UNCLASSIFIED = 0, 1, 2
-PHI_ST, PHI_WIDEST, PHI_GLOBAL, PHI_KOFN, PHI_CONES = 0, 1, 2, 3, 4
+PHI_ST, PHI_WIDEST, PHI_GLOBAL, PHI_KOFN, PHI_CONES, PHI_EDGE_DISJOINT = 0, 1, 2, 3, 4, 5
 
 
 class PhiDesc(ctypes.Structure):

@@ -58,8 +58,65 @@ __device__ bool reach_from(const Phi& f, const volatile uint8_t* x, volatile uin
   return result;
 }
 
-__device__ int phi_warp(const Phi& f, const volatile uint8_t* x, volatile uint8_t* reach, int lane) {
+// Unit-capacity max-flow from node 0 to every t, capped at the running minimum
+// (sysfn.py:112-174).  Arc 2e / 2e+1 are the two directions of edge e, each of
+// capacity 1 when x_e >= 1; augmenting along arc a moves a unit to a ^ 1.  BFS
+// parents are claimed with atomicCAS so the BFS tree stays acyclic; the flow
+// value (hence Phi) does not depend on which augmenting paths are found.
+__device__ int edge_disjoint_warp(const Phi& f, const volatile uint8_t* x, volatile uint8_t* res,
+                                  volatile int* parent, int lane) {
+  int level = f.k;
+  for (int t = 1; t < f.n_nodes && level > 0; ++t) {
+    __syncwarp();
+    for (int a = lane; a < 2 * f.N; a += 32) res[a] = x[a >> 1] >= 1 ? 1 : 0;
+    __syncwarp();
+    int flow = 0;
+    while (flow < level) {
+      for (int v = lane; v < f.n_nodes; v += 32) parent[v] = v == 0 ? -2 : -1;
+      __syncwarp();
+      int reached = 0;
+      while (true) {
+        int changed = 0;
+        for (int a = lane; a < 2 * f.N; a += 32) {
+          if (res[a]) {
+            const int e = a >> 1;
+            const int u = (a & 1) ? f.ev[e] : f.eu[e];
+            const int v = (a & 1) ? f.eu[e] : f.ev[e];
+            if (parent[u] != -1 && parent[v] == -1 &&
+                atomicCAS(const_cast<int*>(&parent[v]), -1, a) == -1)
+              changed = 1;
+          }
+        }
+        __syncwarp();
+        reached = __shfl_sync(kFull, lane == 0 ? (parent[t] != -1) : 0, 0);
+        if (reached || !__any_sync(kFull, changed)) break;
+      }
+      if (!reached) break;
+      if (lane == 0) {
+        int v = t;
+        while (v != 0) {
+          const int a = parent[v];
+          res[a] = (uint8_t)(res[a] - 1);
+          res[a ^ 1] = (uint8_t)(res[a ^ 1] + 1);
+          const int e = a >> 1;
+          v = (a & 1) ? f.ev[e] : f.eu[e];  // tail of arc a
+        }
+      }
+      __syncwarp();
+      ++flow;
+    }
+    if (flow < level) level = flow;
+  }
+  return level;
+}
+
+__device__ int phi_warp(const Phi& f, const volatile uint8_t* x, volatile uint8_t* reach, int lane,
+                        volatile uint8_t* xtra) {
   switch (f.kind) {
+    case RSR_PHI_EDGE_DISJOINT:
+      return edge_disjoint_warp(
+          f, x, xtra, reinterpret_cast<volatile int*>(xtra + ((2 * (size_t)f.N + 15) / 16 * 16)),
+          lane);
     case RSR_PHI_ST_CONNECTIVITY:
       return reach_from(f, x, reach, f.s, f.t, 1, lane) ? 1 : 0;
     case RSR_PHI_WIDEST_PATH:
@@ -125,10 +182,19 @@ __device__ Phi load_phi(const rsr_phi_desc& d, uint8_t* smem, int32_t** tail) {
   return f;
 }
 
+// per warp: x[N] + reach[n] (+ edge-disjoint: res[2N] + parent[n] int32)
+__host__ __device__ inline size_t base_warp_bytes(int N, int n) {
+  return ((size_t)N + (size_t)n + 15) / 16 * 16;
+}
+__host__ __device__ inline size_t warp_bytes(int kind, int N, int n) {
+  size_t b = base_warp_bytes(N, n);
+  if (kind == RSR_PHI_EDGE_DISJOINT) b += (2 * (size_t)N + 15) / 16 * 16 + 4 * (size_t)n;
+  return (b + 15) / 16 * 16;
+}
+
 __host__ __device__ inline size_t phi_smem_bytes(const rsr_phi_desc& d) {
   const size_t edges = d.edge_u ? 2 * sizeof(int32_t) * (size_t)d.n_components : 0;
-  const size_t per_warp = ((size_t)d.n_components + (size_t)d.n_nodes + 15) / 16 * 16;
-  return edges + kWarps * per_warp;
+  return edges + kWarps * warp_bytes(d.kind, d.n_components, d.n_nodes);
 }
 
 __global__ void __launch_bounds__(kWarps * 32)
@@ -139,9 +205,10 @@ phi_eval_kernel(const rsr_phi_desc d, const uint8_t* __restrict__ states,
   int32_t* tail;
   const Phi f = load_phi(d, smem, &tail);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t per_warp = ((size_t)f.N + f.n_nodes + 15) / 16 * 16;
+  const size_t per_warp = warp_bytes(f.kind, f.N, f.n_nodes);
   volatile uint8_t* x = reinterpret_cast<uint8_t*>(tail) + warp * per_warp;
   volatile uint8_t* reach = x + f.N;
+  volatile uint8_t* xtra = x + base_warp_bytes(f.N, f.n_nodes);
   unsigned long long leq = 0;
   for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < count;
        i += (int64_t)gridDim.x * kWarps) {
@@ -149,7 +216,7 @@ phi_eval_kernel(const rsr_phi_desc d, const uint8_t* __restrict__ states,
     const uint8_t* src = states + row * f.N;
     for (int e = lane; e < f.N; e += 32) x[e] = src[e];
     __syncwarp();
-    const int v = phi_warp(f, x, reach, lane);
+    const int v = phi_warp(f, x, reach, lane, xtra);
     if (lane == 0 && out) out[i] = (uint8_t)v;
     leq += (v <= threshold);
     __syncwarp();
@@ -165,22 +232,23 @@ boundary_kernel(const rsr_phi_desc d, int threshold, const uint8_t* __restrict__
   int32_t* tail;
   const Phi f = load_phi(d, smem, &tail);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t per_warp = ((size_t)f.N + f.n_nodes + 15) / 16 * 16;
+  const size_t per_warp = warp_bytes(f.kind, f.N, f.n_nodes);
   volatile uint8_t* x = reinterpret_cast<uint8_t*>(tail) + warp * per_warp;
   volatile uint8_t* reach = x + f.N;
+  volatile uint8_t* xtra = x + base_warp_bytes(f.N, f.n_nodes);
   for (int64_t b = (int64_t)blockIdx.x * kWarps + warp; b < B; b += (int64_t)gridDim.x * kWarps) {
     const uint8_t* src = x0 + b * f.N;
     for (int e = lane; e < f.N; e += 32) x[e] = src[e];
     __syncwarp();
     int64_t calls = 1;
-    const bool lower = phi_warp(f, x, reach, lane) <= threshold;
+    const bool lower = phi_warp(f, x, reach, lane, xtra) <= threshold;
     const int step = lower ? 1 : -1, limit = lower ? f.M - 1 : 0;
     for (int n = 0; n < f.N; ++n) {
       while (x[n] != limit) {
         __syncwarp();
         if (lane == 0) x[n] = (uint8_t)(x[n] + step);
         __syncwarp();
-        const int s = phi_warp(f, x, reach, lane);
+        const int s = phi_warp(f, x, reach, lane, xtra);
         ++calls;
         const bool crossed = lower ? (s > threshold) : (s <= threshold);
         if (crossed) {
@@ -261,6 +329,10 @@ int check_phi(const rsr_phi_desc* d) {
       break;
     case RSR_PHI_K_OUT_OF_N:
       RSR_REQUIRE(d->k >= 1 && d->k <= d->n_components, "phi: bad k");
+      break;
+    case RSR_PHI_EDGE_DISJOINT:
+      RSR_REQUIRE(d->edge_u && d->edge_v && d->n_nodes >= 2 && d->k >= 1,
+                  "phi: edge_disjoint_level needs edges, >= 2 nodes and max_level >= 1");
       break;
     case RSR_PHI_CONE_SUM:
       RSR_REQUIRE(d->n_anchors >= 0 && (d->n_anchors == 0 || (d->anchors && d->anchor_level)),

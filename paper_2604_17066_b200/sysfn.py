@@ -13,14 +13,14 @@ Kinds (``include/rsr_b200.h``):
     (BASELINE cfg5; not in the reference, SURVEY a15);
   * ``global_connectivity`` (sysfn.py:101-109);
   * ``k_out_of_n`` -- k-th largest state (sysfn.py:177-185);
+  * ``edge_disjoint_level`` -- capped edge connectivity (sysfn.py:112-174);
   * ``cone_sum`` -- number of levels whose anchor set has a member dominated
     by x: the coherent-by-construction test system of the reference suite
     (tests/conftest.py:53-75).
 
 ``Graph``, ``random_geometric_graph`` and ``pick_od_pair`` are host-side
 graph construction utilities with the reference semantics
-(sysfn.py:32-59, 188-269); ``edge_disjoint_level`` is outside this build's
-hot-path scope and raises.
+(sysfn.py:32-59, 188-269).
 """
 
 from __future__ import annotations
@@ -191,11 +191,18 @@ def cone_sum(levels: Sequence[Sequence[Sequence[int]]], n_components: int) -> De
                              anchor_level=np.array(lev, dtype=np.int32), name="cone_sum")
 
 
-def edge_disjoint_level(graph: Graph, max_level: int) -> Callable:
-    """Out of this build's hot-path scope."""
-    raise NotImplementedError(
-        "edge_disjoint_level (unit-capacity max-flow Phi, reference sysfn.py:112-174) is not "
-        "implemented on the device path in this build")
+def edge_disjoint_level(graph: Graph, max_level: int) -> DevicePerformance:
+    """Min over node pairs of edge-disjoint path counts, capped (sysfn.py:140-174), M_S = max_level + 1.
+
+    Device: unit-capacity max-flow from node 0 to every other node by BFS
+    augmentation, one warp per vector (csrc/phi.cu).
+    """
+    if max_level < 1:
+        raise ValueError("max_level must be >= 1")
+    if graph.n_nodes < 2:
+        raise ValueError("need at least two nodes")
+    return DevicePerformance(_abi.PHI_EDGE_DISJOINT, graph.n_edges, graph=graph, k=max_level,
+                             name=f"edge_disjoint_level({max_level})")
 
 
 class _UnionFind:

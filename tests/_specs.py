@@ -34,6 +34,9 @@ def oracle_phi(spec_model: dict):
         return oracle.phi_widest(m["n_nodes"], edges, m["s"], m["t"], m["m"]), len(edges)
     if m["kind"] == "cones":
         return oracle.phi_cones(m["levels"]), m["n"]
+    if m["kind"] == "edk":
+        edges = [tuple(e) for e in m["edges"]]
+        return oracle.phi_edge_disjoint(m["n_nodes"], edges, m["max_level"]), len(edges)
     raise ValueError(m["kind"])
 
 
@@ -49,4 +52,7 @@ def device_model(spec_model: dict):
         return P.SystemModel(len(m["edges"]), m["m"], m["ms"], f(g, m["s"], m["t"]))
     if m["kind"] == "cones":
         return P.SystemModel(m["n"], m["m"], m["ms"], P.cone_sum(m["levels"], m["n"]))
+    if m["kind"] == "edk":
+        g = P.Graph(m["n_nodes"], tuple(tuple(e) for e in m["edges"]))
+        return P.SystemModel(len(m["edges"]), m["m"], m["ms"], P.edge_disjoint_level(g, m["max_level"]))
     raise ValueError(m["kind"])

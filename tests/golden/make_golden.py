@@ -28,7 +28,8 @@ from rsr.classify import classify, violation_counts  # noqa: E402
 from rsr.encoding import encode_batch  # noqa: E402
 from rsr.model import ComponentDistribution, SystemModel  # noqa: E402
 from rsr.sampling import SampleBatch, sample_batch  # noqa: E402
-from rsr.sysfn import Graph, k_out_of_n, single_od_connectivity  # noqa: E402
+from rsr.sysfn import (Graph, edge_disjoint_level, k_out_of_n, random_geometric_graph,  # noqa: E402
+                       single_od_connectivity)
 from rsr.workflow import RunConfig, multistate_pmf, stage1_find_references, stage2_evaluate  # noqa: E402
 
 from paper_2604_17066_b200 import workloads  # noqa: E402  (host-side generators only)
@@ -191,6 +192,7 @@ def workflow_cases():
     rng = np.random.default_rng(5)
     probs3 = rng.dirichlet([1.0, 3.0, 16.0], size=len(grid_m3["edges"]))
     cone_levels = [[[1, 0, 2, 1, 0, 1], [0, 2, 1, 1, 1, 0]], [[2, 1, 2, 2, 1, 1]]]
+    rgg = random_geometric_graph(10, 0.55, seed=3)
     return [
         {"name": "series3", "model": {"kind": "kofn", "k": 3, "n": 3, "m": 2, "ms": 2},
          "probs": np.tile([0.1, 0.9], (3, 1)).tolist(),
@@ -220,6 +222,12 @@ def workflow_cases():
          "probs": probs3.tolist(),
          "config": dict(n_samples=10_000, eps_u=1e-3, r_max=10_000, seed=1, parallel_searches=4),
          "thresholds": [0, 1]},
+        {"name": "rgg_edge_disjoint", "model": {"kind": "edk", "n_nodes": rgg.n_nodes,
+                                                "edges": [list(e) for e in rgg.edges], "max_level": 2,
+                                                "m": 2, "ms": 3},
+         "probs": np.tile([0.15, 0.85], (rgg.n_edges, 1)).tolist(),
+         "config": dict(n_samples=3000, eps_u=1e-3, r_max=300, seed=5, parallel_searches=4),
+         "thresholds": [0, 1]},
         {"name": "cones6", "model": {"kind": "cones", "levels": cone_levels, "n": 6, "m": 3, "ms": 3},
          "probs": np.tile([0.2, 0.3, 0.5], (6, 1)).tolist(),
          "config": dict(n_samples=5000, eps_u=1e-3, r_max=200, seed=11, parallel_searches=3),
@@ -238,6 +246,9 @@ def build_reference_model(spec):
         return SystemModel(len(m["edges"]), m["m"], m["ms"], phi)
     if m["kind"] == "cones":
         return SystemModel(m["n"], m["m"], m["ms"], _cone_phi(m["levels"]))
+    if m["kind"] == "edk":
+        g = Graph(m["n_nodes"], tuple(tuple(e) for e in m["edges"]))
+        return SystemModel(len(m["edges"]), m["m"], m["ms"], edge_disjoint_level(g, m["max_level"]))
     raise ValueError(m["kind"])
 
 

@@ -74,6 +74,30 @@ def test_random_classifier_shapes(seed):
         assert np.array_equal(r.unclassified_indices, np.flatnonzero(want == 2))
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_edge_disjoint_level_vs_oracle(seed):
+    rng = np.random.default_rng(300 + seed)
+    if seed == 0:  # multigraph (parallel edges add capacity)
+        graph = P.Graph(5, ((0, 1), (0, 1), (1, 2), (2, 3), (3, 4), (4, 0), (1, 3), (2, 4)))
+    else:
+        graph = P.random_geometric_graph(int(rng.integers(8, 16)), 0.5, seed=seed)
+    for max_level in (1, 2, 3):
+        phi = P.edge_disjoint_level(graph, max_level)
+        ref = oracle.phi_edge_disjoint(graph.n_nodes, graph.edges, max_level)
+        xs = (rng.random((300, graph.n_edges)) < 0.85).astype(np.int64)
+        got = phi.evaluate_device(xs, 2)
+        assert np.array_equal(got, np.array([ref(x) for x in xs]))
+        model = P.SystemModel(graph.n_edges, 2, max_level + 1, phi)
+        for thr in range(max_level):
+            for x0 in xs[:4]:
+                ev = oracle.CountingPhi(ref, graph.n_edges, 2, max_level + 1)
+                vec, side = oracle.boundary_search(ev, x0, thr)
+                model.reset_evaluation_count()
+                r = P.boundary_search(model, x0, thr)
+                assert r.vector == vec and r.side == side
+                assert model.evaluation_count == ev.count
+
+
 def test_sampling_random_tables_and_offsets():
     rng = np.random.default_rng(7)
     for _ in range(8):

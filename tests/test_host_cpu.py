@@ -78,8 +78,9 @@ def test_graph_utilities_match_reference_semantics():
     g = P.random_geometric_graph(30, 0.35, seed=0)
     o, d = P.pick_od_pair(g)
     assert 0 <= o < g.n_nodes and 0 <= d < g.n_nodes and o != d
-    with pytest.raises(NotImplementedError):
-        P.edge_disjoint_level(g, 2)
+    with pytest.raises(ValueError):
+        P.edge_disjoint_level(g, 0)
+    assert P.edge_disjoint_level(g, 2).k == 2
 
 
 def test_graph_utilities_vs_reference(reference_rsr):
