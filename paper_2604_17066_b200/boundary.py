@@ -158,6 +158,14 @@ class ReferenceSet:
         covered_h = covered.cpu().numpy().astype(bool)
         covers_h = covers.cpu().numpy().astype(bool)
         rel_h = rel.cpu().numpy()
+        if not covers_h.any() and not np.tril(rel_h, -1).any():
+            # common case (e.g. bulk loads of non-dominated sets): no candidate relates
+            # to an earlier one and none drops a member -> inserted iff not covered
+            keep = np.flatnonzero(~covered_h)
+            if keep.size:
+                idx = torch.as_tensor(keep, dtype=torch.int64, device=dev)
+                self._append_device(cands_dev.index_select(0, idx), cands_host[keep])
+            return ["redundant" if c else "inserted" for c in covered_h]
         outcome: list[str] = []
         inserted: list[int] = []
         alive: list[bool] = []

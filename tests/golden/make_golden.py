@@ -270,6 +270,44 @@ def gen_workflow(specs, fname):
         json.dump(out, f)
 
 
+def gen_refsets():
+    """Reference-written rsr/1 set files and the member lists the reference loads."""
+    from rsr.files import load_reference_sets, save_reference_sets
+    import tempfile
+    out = []
+    rng = np.random.default_rng(77)
+    docs = []
+    # clean: a Stage-1 result of the 5x5 grid
+    spec = next(c for c in workflow_cases() if c["name"] == "grid_st_small")
+    model = build_reference_model(spec)
+    s1 = stage1_find_references(model, ComponentDistribution(np.array(spec["probs"])),
+                                RunConfig(**spec["config"]), 0)
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "r.json")
+        save_reference_sets(p, s1.lower, s1.upper, "grid-hash", seed=0)
+        docs.append(json.loads(open(p).read()))
+    # messy: duplicates and mutually dominated vectors, written raw
+    vec = lambda k: [[int(v) for v in r] for r in rng.integers(0, 3, size=(k, 6))]  # noqa: E731
+    lo, up = vec(80), vec(80)
+    lo += lo[:5]
+    up += up[3:9]
+    docs.append({"format": "rsr/1", "threshold": 0, "model_hash": "messy",
+                 "lower": {"format": "rsr/1", "side": "lower", "threshold": 0, "vectors": lo,
+                           "model_hash": "messy"},
+                 "upper": {"format": "rsr/1", "side": "upper", "threshold": 0, "vectors": up,
+                           "model_hash": "messy"}})
+    for doc in docs:
+        with tempfile.TemporaryDirectory() as d:
+            p = os.path.join(d, "r.json")
+            with open(p, "w") as f:
+                json.dump(doc, f)
+            lower, upper = load_reference_sets(p, doc["model_hash"])
+        out.append({"file": doc, "lower": [list(v) for v in lower.members],
+                    "upper": [list(v) for v in upper.members]})
+    with open(os.path.join(HERE, "refsets.json"), "w") as f:
+        json.dump(out, f)
+
+
 def gen_pmf():
     model = SystemModel(3, 3, 3, k_out_of_n(2, 3))
     dist = ComponentDistribution.iid(3, [0.2, 0.3, 0.5])
@@ -297,5 +335,6 @@ if __name__ == "__main__":
     gen_classify()
     gen_boundary()
     gen_pmf()
+    gen_refsets()
     gen_workflow(workflow_cases(), "workflow.json")
     print("rsr", rsr.__version__, "numpy", np.__version__)
