@@ -182,6 +182,16 @@ int rsr_phi_eval(const rsr_phi_desc* phi, const uint8_t* states,
 int rsr_boundary_search(const rsr_phi_desc* phi, int threshold, const uint8_t* x0,
                         int64_t B, uint8_t* out_refs, uint8_t* out_side,
                         int64_t* out_calls, void* stream);
+/* Exact enumeration for small models (oracle.py:49-63): vectors first ..
+ * first+count-1 of itertools.product(range(M), repeat=N) and their probabilities
+ * prod_n probs[n, x_n] (f64). */
+int rsr_enumerate_states(const double* probs, int n_components, int n_states,
+                         int64_t first, int64_t count, uint8_t* out_states,
+                         double* out_prob, void* stream);
+/* mass[s] += prob[i], counts[s] += 1 for s = phi[i], sequentially in i order
+ * (bit-exact with the reference's float64 accumulation). */
+int rsr_state_mass(const uint8_t* phi_values, const double* probs, int64_t count,
+                   int n_system_states, double* mass, int64_t* counts, void* stream);
 /* gather rows: out[i] = states[idx[i]] (N bytes each) */
 int rsr_gather_rows(const uint8_t* states, int n_components, const int64_t* idx,
                     int64_t count, uint8_t* out, void* stream);

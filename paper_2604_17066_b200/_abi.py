@@ -78,6 +78,8 @@ EXPORTED = {
     "rsr_phi_eval": (_I, [ctypes.POINTER(PhiDesc), _P, _P, _I64, _P, _I, _P, _P]),
     "rsr_boundary_search": (_I, [ctypes.POINTER(PhiDesc), _I, _P, _I64, _P, _P, _P, _P]),
     "rsr_gather_rows": (_I, [_P, _I, _P, _I64, _P, _P]),
+    "rsr_enumerate_states": (_I, [_P, _I, _I, _I64, _I64, _P, _P, _P]),
+    "rsr_state_mass": (_I, [_P, _P, _I64, _I, _P, _P, _P]),
     "rsr_dominance_scan": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P, _I, _P, _P]),
 }
 

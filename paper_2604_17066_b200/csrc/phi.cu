@@ -398,6 +398,63 @@ extern "C" int rsr_boundary_search(const rsr_phi_desc* phi, int threshold, const
   return rsr::check_launch("boundary_kernel");
 }
 
+// Exact enumeration (oracle.py:49-63, CLI `oracle --mode exact`): vector number
+// `first + i` in itertools.product order (last component fastest) and its
+// probability prod_n probs[n, x_n], multiplied in component order like the
+// reference's scalar loop.
+namespace {
+__global__ void enumerate_kernel(const double* __restrict__ probs, int N, int M, int64_t first,
+                                 int64_t count, uint8_t* __restrict__ out,
+                                 double* __restrict__ prob) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  int64_t code = first + i;
+  uint8_t* row = out + i * N;
+  for (int n = N - 1; n >= 0; --n) {
+    row[n] = (uint8_t)(code % M);
+    code /= M;
+  }
+  double p = 1.0;
+  for (int n = 0; n < N; ++n) p = __dmul_rn(p, probs[(int64_t)n * M + row[n]]);
+  prob[i] = p;
+}
+
+// mass[s] += p and count[s] += 1 in enumeration order (single thread: the
+// reference's sequential float64 sum, oracle.py:56-61).
+__global__ void state_mass_kernel(const uint8_t* __restrict__ phi, const double* __restrict__ prob,
+                                  int64_t count, int n_sys, double* mass, int64_t* counts) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int64_t i = 0; i < count; ++i) {
+    const int s = phi[i];
+    if (s < n_sys) {
+      mass[s] = __dadd_rn(mass[s], prob[i]);
+      counts[s] += 1;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int rsr_state_mass(const uint8_t* phi_values, const double* probs, int64_t count,
+                              int n_system_states, double* mass, int64_t* counts, void* stream) {
+  RSR_REQUIRE(count >= 0 && n_system_states >= 1, "rsr_state_mass: bad arguments");
+  if (count == 0) return RSR_OK;
+  state_mass_kernel<<<1, 1, 0, rsr::as_stream(stream)>>>(phi_values, probs, count, n_system_states,
+                                                         mass, counts);
+  return rsr::check_launch("state_mass_kernel");
+}
+
+extern "C" int rsr_enumerate_states(const double* probs, int n_components, int n_states,
+                                    int64_t first, int64_t count, uint8_t* out_states,
+                                    double* out_prob, void* stream) {
+  RSR_REQUIRE(n_components >= 1 && n_states >= 2 && first >= 0 && count >= 0,
+              "rsr_enumerate_states: bad arguments");
+  if (count == 0) return RSR_OK;
+  enumerate_kernel<<<(unsigned)rsr::ceil_div(count, 256), 256, 0, rsr::as_stream(stream)>>>(
+      probs, n_components, n_states, first, count, out_states, out_prob);
+  return rsr::check_launch("enumerate_kernel");
+}
+
 extern "C" int rsr_gather_rows(const uint8_t* states, int n_components, const int64_t* idx,
                                int64_t count, uint8_t* out, void* stream) {
   RSR_REQUIRE(n_components >= 1 && count >= 0, "rsr_gather_rows: bad shape");

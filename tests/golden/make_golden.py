@@ -19,6 +19,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import rsr  # noqa: E402
@@ -308,6 +309,18 @@ def gen_refsets():
         json.dump(out, f)
 
 
+from _cli_cases import run_cli  # noqa: E402  (shared with tests/test_cli.py)
+
+
+def gen_cli():
+    import tempfile
+    from rsr.cli import main
+    with tempfile.TemporaryDirectory() as d:
+        outs = run_cli(main, d)
+    with open(os.path.join(HERE, "cli.json"), "w") as f:
+        json.dump(outs, f)
+
+
 def gen_pmf():
     model = SystemModel(3, 3, 3, k_out_of_n(2, 3))
     dist = ComponentDistribution.iid(3, [0.2, 0.3, 0.5])
@@ -336,5 +349,6 @@ if __name__ == "__main__":
     gen_boundary()
     gen_pmf()
     gen_refsets()
+    gen_cli()
     gen_workflow(workflow_cases(), "workflow.json")
     print("rsr", rsr.__version__, "numpy", np.__version__)
