@@ -50,7 +50,8 @@ def parse():
                    help="N>1: shard reference states across ranks, OR-reduce hit flags")
     p.add_argument("--k", type=int, default=10_000, help="refs per side (cfg2) / path refs (cfg4)")
     p.add_argument("--samples", type=int, default=None, help="samples per GPU")
-    p.add_argument("--method", choices=["tc", "bits"], default="tc")
+    p.add_argument("--method", choices=["tc", "tc8", "bits"], default="tc",
+                   help="tc: FP4 (kind::mxf4) tensor cores; tc8: int8 tensor cores; bits: CUDA cores")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -259,24 +260,38 @@ def run_ours(args):
     dist = P.ComponentDistribution.iid(N_COMP, [1 - p1, p1])
     batch = P.sample_batch(dist, S, seed=0, generation_index=0,
                            start=0 if shard_refs else rank * S)
-    A = batch.thermo(2)
-    bl, nl = lower.device_thermo(2)
-    bu, nu = upper.device_thermo(2)
+    if args.method == "tc":
+        A = batch.fp4(2)
+        bl, nl = lower.device_fp4(2)
+        bu, nu = upper.device_fp4(2)
+        width = A.shape[1] // 2  # bytes per operand row
+    else:
+        A = batch.thermo(2)
+        bl, nl = lower.device_thermo(2)
+        bu, nu = upper.device_thermo(2)
+        width = A.shape[1]
     sb = batch.thermo_bits(2) if args.method == "bits" else None
     lb, _ = lower.device_bits(2) if args.method == "bits" else (None, 0)
     ub, _ = upper.device_bits(2) if args.method == "bits" else (None, 0)
-    kpad = A.shape[1]
+    a_bytes = A.shape[0] * A.shape[1]
     flags = torch.empty(S, dtype=torch.uint8, device=dev)
     labels = torch.empty(S, dtype=torch.uint8, device=dev)
     counts = torch.empty(4, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = _abi.stream_ptr()
     launches = 0
+    # reference-chunked launches of the classifier (L2-resident B slices)
+    tiles = {"tc": lambda n: -(-n // 240), "tc8": lambda n: -(-n // 256), "bits": lambda n: 0}[args.method]
+    per_launch = {"tc": 512, "tc8": 256, "bits": 1}[args.method]
+    classify_launches = max(1, -(-(tiles(nl) + tiles(nu)) // per_launch))
     import torch.distributed as tdist
 
     def classify_kernel():
         if args.method == "tc":
-            _abi.call("rsr_classify_tc", _abi.ptr(A), S, _abi.ptr(bl), nl, _abi.ptr(bu), nu, kpad,
+            _abi.call("rsr_classify_fp4", _abi.ptr(A), S, _abi.ptr(bl), nl, _abi.ptr(bu), nu, width,
+                      _abi.ptr(flags), 0, stream)
+        elif args.method == "tc8":
+            _abi.call("rsr_classify_tc", _abi.ptr(A), S, _abi.ptr(bl), nl, _abi.ptr(bu), nu, width,
                       _abi.ptr(flags), 0, stream)
         else:
             _abi.call("rsr_classify_bits", _abi.ptr(sb), S, _abi.ptr(lb), nl, _abi.ptr(ub), nu,
@@ -292,7 +307,7 @@ def run_ours(args):
         if shard_refs:
             comm.allreduce_max_u8(flags)  # OR of hit bits across the ref shards
         _abi.call("rsr_finalize", _abi.ptr(flags), S, _abi.ptr(labels), _abi.ptr(counts), stream)
-        launches += 2
+        launches += classify_launches + 1
         if world > 1 and not shard_refs:
             tdist.all_reduce(counts)
 
@@ -333,23 +348,31 @@ def run_ours(args):
     kern_avg = sum(kern_ms) / len(kern_ms)
     achieved = S * K * ops_per_pair / (kern_avg * 1e-3) / 1e12
     cublas_peak, cublas_src = int8_peak_tops()
-    kname = "classify_tc_pair_kernel" if args.method == "tc" else "classify_bits_kernel"
-    # Denominator: dense int8 tensor peak 4.5 POPS (B200 spec), which our own
-    # tcgen05 kind::i8 issue-rate microbenchmark (tools/mma_rate.cu) reaches
-    # on this pool (4409-4544 TOPS at 1965 MHz); cuBLASLt int8 only reaches the
-    # lower `cublas_int8_tops`, reported alongside.
-    peak = 4500.0
+    kname = {"tc": "classify_fp4_pair_kernel", "tc8": "classify_tc_pair_kernel",
+             "bits": "classify_bits_kernel"}[args.method]
+    # Denominators: dense tensor peaks of the pipe the kernel runs on -- FP4
+    # (kind::mxf4) 9 POPS and int8 4.5 POPS (B200 spec), which our own tcgen05
+    # issue-rate microbenchmarks reach on this pool (tools/mxf4_check.cu:
+    # 8781-8931 TOPS, tools/mma_rate.cu: 4409-4544 TOPS at 1965 MHz);
+    # MEASURED_PEAKS.json has neither figure.  cuBLASLt int8 (the best library
+    # GEMM for this contraction) is reported alongside.
+    int8_peak = 4500.0
+    peak = 9000.0 if args.method == "tc" else int8_peak
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
                 "frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname,
                 "kernel_ms": kern_avg, "ops_per_pair": ops_per_pair,
-                "peak_source": "B200 dense int8 spec = measured tcgen05 kind::i8 rate "
-                               "(tools/mma_rate.cu: 4409-4544 TOPS); MEASURED_PEAKS.json has "
-                               "no int8 figure",
+                "peak_source": ("B200 dense FP4 spec = measured tcgen05 kind::mxf4 rate "
+                                "(tools/mxf4_check.cu: 8781-8931 TOPS)" if args.method == "tc" else
+                                "B200 dense int8 spec = measured tcgen05 kind::i8 rate "
+                                "(tools/mma_rate.cu: 4409-4544 TOPS)") +
+                               "; MEASURED_PEAKS.json has no int8/fp4 figure",
+                "frac_of_int8_peak": achieved / int8_peak,
                 "cublas_int8_tops": cublas_peak, "cublas_int8_source": cublas_src,
                 "frac_of_cublas_int8": achieved / cublas_peak}
 
     # ---- end to end through the public API with host buffers
     e2e = None
+    e2e_method = "tc8" if args.method == "tc8" else "tc"
     if not args.no_e2e:
         host = torch.empty((S, N_COMP), dtype=torch.uint8, pin_memory=True)
         host.copy_(batch.device_states())
@@ -357,12 +380,12 @@ def run_ours(args):
         for _ in range(2):
             P.classify.__module__  # noqa: B018
             from paper_2604_17066_b200.classify import classify_host
-            classify_host(host, lower, upper, 2, labels_out=out)
+            classify_host(host, lower, upper, 2, labels_out=out, method=e2e_method)
         torch.cuda.synchronize()
         comm.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            _, c = classify_host(host, lower, upper, 2, labels_out=out)
+            _, c = classify_host(host, lower, upper, 2, labels_out=out, method=e2e_method)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
@@ -374,7 +397,9 @@ def run_ours(args):
                "h2d_bytes_per_step": S * N_COMP, "d2h_bytes_per_step": S + 32,
                "ms_per_step": 1e3 * dt / args.steps,
                "api": "paper_2604_17066_b200.classify.classify_host (pinned host uint8 states -> "
-                      "labels), chunked H2D overlapped with rsr_encode_samples + rsr_classify_tc"}
+                      "labels), chunked H2D overlapped with " +
+                      ("rsr_encode_samples + rsr_classify_tc" if e2e_method == "tc8" else
+                       "rsr_encode_samples_fp4 + rsr_classify_fp4")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -389,14 +414,17 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "strong" if shard_refs else "weak",
-                "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+                "vs_baseline": None,
+                "dtype": {"tc": "e2m1 (0/1, exact fp32 accumulate)", "tc8": "int8",
+                          "bits": "u32 bitwise"}[args.method],
+                "data": "synthetic",
                 "config": {"workload": desc, "samples_per_gpu": S, "ref_states": K_job,
                            "ref_states_per_gpu": K, "n_components": N_COMP, "method": args.method,
                            "parallelism": (f"ref-sharded x{world} (same samples on every rank, "
                                            f"hit flags OR-reduced with NCCL MAX)" if shard_refs else
                                            f"dp{world} (samples sharded by stream offset, refs "
                                            f"replicated, counts all-reduced)"),
-                           "l2": f"A operand {S}x{kpad} B = {S * kpad / 1e6:.0f} MB > L2 and 256 MB "
+                           "l2": f"A operand {a_bytes / 1e6:.0f} MB > L2 and 256 MB "
                                  f"L2 flush between steps (outside the step events)",
                            "labels": {"lower": final_counts[0], "upper": final_counts[1],
                                       "unclassified": final_counts[2]}},

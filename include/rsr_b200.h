@@ -137,6 +137,33 @@ int rsr_classify_tc_explain(const int8_t* A, int64_t S, const int8_t* B_lower,
                             int64_t n_lower, const int8_t* B_upper, int64_t n_upper,
                             int Kpad, uint8_t* flags, int64_t* first_lower,
                             int64_t* first_upper, int accumulate, void* stream);
+/* Block-scaled FP4 tensor-core classifier (default path; 2x the int8 MMA
+ * rate): tcgen05.mma.cta_group::2.kind::mxf4, e2m1 operands, unit scales.
+ * FP4 layout (row_bytes = rsr_fp4_row_bytes(N, M) = round_up(Kdim+1, 64)/2,
+ * element c of a row in byte c/2, low nibble first, 0x2 = 1.0, 0x0 = 0):
+ *   sample row s: [A_up | A_lo], 2*row_bytes bytes, A_up[c] = [x_n < k],
+ *     A_lo[c] = [x_n >= k] (c < Kdim), both 1 at the bias column c = Kdim;
+ *   upper ref row: [r_n >= k], lower ref row: [r_n < k], bias column 0;
+ *   pad ref rows: only the bias column set (never hit).
+ * Reference buffers hold ceil(n/240)*240 rows (tiles of 240).  D = A_up.B_up
+ * (upper) or A_lo.B_lo (lower) counts violated thermometer columns exactly
+ * (fp32 accumulation of 0/1 products); D == 0 <=> dominance.  flags and
+ * accumulate as rsr_classify_tc.  row_bytes <= RSR_FP4_MAX_ROW_BYTES. */
+#define RSR_FP4_MAX_ROW_BYTES 448
+#define RSR_FP4_TILE_ROWS 240
+int rsr_fp4_row_bytes(int n_components, int n_states);
+int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int n_components,
+                           int n_states, uint8_t* out, int row_bytes, void* stream);
+int rsr_encode_refs_fp4(const uint8_t* states, int64_t count, int64_t rows_total,
+                        int n_components, int n_states, int side, uint8_t* out,
+                        int row_bytes, void* stream);
+int rsr_classify_fp4(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64_t n_lower,
+                     const uint8_t* B_upper, int64_t n_upper, int row_bytes,
+                     uint8_t* flags, int accumulate, void* stream);
+int rsr_classify_fp4_explain(const uint8_t* A, int64_t S, const uint8_t* B_lower,
+                             int64_t n_lower, const uint8_t* B_upper, int64_t n_upper,
+                             int row_bytes, uint8_t* flags, int64_t* first_lower,
+                             int64_t* first_upper, int accumulate, void* stream);
 /* Bit-packed CUDA-core comparison variant (AND + OR-reduce, LOP3).
  * Packs states on the fly; optional first-match indices (explain / strict,
  * classify.py:99-118): first_lower / first_upper int64 [S] or NULL. */

@@ -17,7 +17,8 @@ import torch
 __all__ = ["lib", "call", "stream_ptr", "ptr", "PhiDesc", "LIB_PATH", "require_device",
            "SIDE_LOWER", "SIDE_UPPER", "HIT_LOWER", "HIT_UPPER", "LABEL_LOWER", "LABEL_UPPER",
            "LABEL_UNCLASSIFIED", "PHI_ST", "PHI_WIDEST", "PHI_GLOBAL", "PHI_KOFN", "PHI_CONES",
-           "thermo_kpad", "thermo_words", "EXPORTED"]
+           "thermo_kpad", "thermo_words", "fp4_row_bytes", "FP4_TILE_ROWS",
+           "FP4_MAX_ROW_BYTES", "EXPORTED"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librsr_b200.so")
 
@@ -68,6 +69,11 @@ EXPORTED = {
     "rsr_packbits_rows": (_I, [_P, _I64, _I, _I, _P, _P]),
     "rsr_classify_tc": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _I, _P]),
     "rsr_classify_tc_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
+    "rsr_fp4_row_bytes": (_I, [_I, _I]),
+    "rsr_encode_samples_fp4": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
+    "rsr_encode_refs_fp4": (_I, [_P, _I64, _I64, _I, _I, _I, _P, _I, _P]),
+    "rsr_classify_fp4": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _I, _P]),
+    "rsr_classify_fp4_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_classify_bits": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_finalize": (_I, [_P, _I64, _P, _P, _P]),
@@ -117,7 +123,7 @@ def call(name: str, *args) -> int:
     """Invoke an entry point, mapping status codes to Python exceptions."""
     L = lib()
     rc = getattr(L, name)(*args)
-    if name in ("rsr_compact_scratch", "rsr_thermo_kpad", "rsr_version"):
+    if name in ("rsr_compact_scratch", "rsr_thermo_kpad", "rsr_version", "rsr_fp4_row_bytes"):
         return rc
     if rc != RSR_OK:
         msg = (L.rsr_last_error() or b"").decode(errors="replace")
@@ -145,6 +151,15 @@ def thermo_kpad(n: int, m: int) -> int:
     kdim = n * (m - 1)
     nb = (kdim + 126) // 127
     return (kdim + nb + 31) // 32 * 32
+
+
+FP4_TILE_ROWS = 240
+FP4_MAX_ROW_BYTES = 448
+
+
+def fp4_row_bytes(n: int, m: int) -> int:
+    """Bytes per operand row of the FP4 layout (mirrors rsr_fp4_row_bytes)."""
+    return (n * (m - 1) + 1 + 63) // 64 * 32
 
 
 def thermo_words(n: int, m: int) -> int:

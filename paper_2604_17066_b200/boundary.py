@@ -2,9 +2,11 @@
 
 ``ReferenceSet`` keeps the reference's ordered member list semantics
 (boundary.py:57-113) and mirrors it on the device: a uint8 state matrix plus,
-per component-state count M, the int8 thermometer rows the tensor-core
-classifier streams (``rsr_encode_refs``; rows padded to 128 with never-hit
-rows) and the packed bits of the CUDA-core variant.  Appends encode only the
+per component-state count M, the packed e2m1 rows the FP4 tensor-core
+classifier streams (``rsr_encode_refs_fp4``; rows padded to 240-row tiles with
+never-hit rows), the int8 thermometer rows of the int8 variant
+(``rsr_encode_refs``, 256-row tiles) and the packed bits of the CUDA-core
+variant.  Appends encode only the
 new rows; a drop (a new member dominating old ones) rebuilds the mirror.
 
 Redundancy checks run on the device (``rsr_dominance_scan``), for a single
@@ -63,6 +65,7 @@ class ReferenceState:
 
 
 _TILE = 256  # reference rows per classifier tile (CTA-pair kernel: 2 x 128)
+_TILE4 = _abi.FP4_TILE_ROWS  # reference rows per FP4 classifier tile (2 x 120)
 
 
 class ReferenceSet:
@@ -81,6 +84,7 @@ class ReferenceSet:
         self._dev_n = 0
         self._thermo: dict[int, list] = {}  # M -> [tensor, encoded_rows]
         self._bits: dict[int, list] = {}
+        self._fp4: dict[int, list] = {}  # M -> [tensor, encoded_rows]
         for m in members:
             self.insert(ReferenceState(tuple(m), side, threshold))
 
@@ -237,6 +241,7 @@ class ReferenceSet:
         self._dev_n = 0
         self._thermo.clear()
         self._bits.clear()
+        self._fp4.clear()
 
     def _ensure_dev_capacity(self, n: int) -> None:
         cap = 0 if self._dev_rows is None else self._dev_rows.shape[0]
@@ -283,6 +288,31 @@ class ReferenceSet:
         if done < self._n:
             _abi.call("rsr_encode_refs", _abi.ptr(rows_dev[done:]), self._n - done, need - done, N,
                       n_states, _side_code(self.side), _abi.ptr(t[done:]), kpad, _device.stream())
+            ent[1] = self._n
+        return t, self._n
+
+    def device_fp4(self, n_states: int) -> tuple[torch.Tensor | None, int]:
+        """FP4 B rows ([r < k] lower / [r >= k] upper as packed e2m1, padded to
+        240-row tiles with never-hit rows) and the member count."""
+        if self._n == 0:
+            return None, 0
+        rows_dev = self.device_rows()
+        N = self._width
+        rb = _abi.fp4_row_bytes(N, n_states)
+        need = (self._n + _TILE4 - 1) // _TILE4 * _TILE4
+        ent = self._fp4.get(n_states)
+        if ent is None or ent[0].shape[0] < need:
+            cap = max(need, 2 * (ent[0].shape[0] if ent else 0), _TILE4)
+            cap = (cap + _TILE4 - 1) // _TILE4 * _TILE4
+            t = torch.empty((cap, rb), dtype=torch.uint8, device=rows_dev.device)
+            if ent is not None and ent[1]:
+                t[: ent[1]].copy_(ent[0][: ent[1]])
+            ent = [t, ent[1] if ent else 0]
+            self._fp4[n_states] = ent
+        t, done = ent
+        if done < self._n:
+            _abi.call("rsr_encode_refs_fp4", _abi.ptr(rows_dev[done:]), self._n - done, need - done,
+                      N, n_states, _side_code(self.side), _abi.ptr(t[done:]), rb, _device.stream())
             ent[1] = self._n
         return t, self._n
 

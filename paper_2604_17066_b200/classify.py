@@ -5,11 +5,17 @@ lower takes precedence over upper, ``strict`` raises on overlap,
 ``explain`` records the first matching reference per sample.  The work is
 done on the device:
 
-* default (``method="tc"``): ``rsr_classify_tc`` -- thermometer-encoded int8
-  contraction on tcgen05 tensor cores with the any-zero epilogue fused, the
-  S x K violation matrix never materialised;
-* ``method="bits"`` (and whenever first-match indices are needed):
-  ``rsr_classify_bits`` -- bit-packed AND/OR-reduce on CUDA cores;
+* default (``method="tc"``): ``rsr_classify_fp4`` -- thermometer contraction
+  on block-scaled FP4 tcgen05 tensor cores (kind::mxf4, exact for 0/1
+  operands, twice the int8 rate) with the any-zero epilogue fused, the S x K
+  violation matrix never materialised; rows wider than the FP4 kernel keeps
+  resident use the int8 kernel, wider still the bit-packed one;
+* ``method="tc8"``: ``rsr_classify_tc`` -- the same contraction on int8
+  tcgen05 tensor cores (comparison variant);
+* ``method="bits"``: ``rsr_classify_bits`` -- bit-packed AND/OR-reduce on CUDA
+  cores (comparison variant);
+* first-match indices (``explain`` / ``strict``) come from the same kernels'
+  epilogues (``*_explain`` entry points);
 * then ``rsr_finalize`` (labels + counts) and, lazily, ``rsr_compact``
   (order-preserving index arrays, np.flatnonzero semantics).
 
@@ -190,8 +196,24 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
     m_eff = max(2, n_states, batch.state_bound)
     fl = fu = None
     st = _device.stream()
+    if method not in ("tc", "tc8", "fp4", "bits"):
+        raise ValueError("method must be 'tc', 'tc8', 'fp4' or 'bits'")
+    fp4_ok = _abi.fp4_row_bytes(batch.n_components, m_eff) <= _abi.FP4_MAX_ROW_BYTES
     tc_ok = _abi.thermo_kpad(batch.n_components, m_eff) <= TC_MAX_KPAD
-    if method == "tc" and tc_ok:
+    if method in ("tc", "fp4") and fp4_ok:
+        a = batch.fp4(m_eff)
+        rb = a.shape[1] // 2
+        bl, nl = lower_set.device_fp4(m_eff) if lower_set is not None else (None, 0)
+        bu, nu = upper_set.device_fp4(m_eff) if upper_set is not None else (None, 0)
+        if want_first:
+            fl = torch.empty(H, dtype=torch.int64, device=dev)
+            fu = torch.empty(H, dtype=torch.int64, device=dev)
+            _abi.call("rsr_classify_fp4_explain", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu),
+                      nu, rb, _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
+        else:
+            _abi.call("rsr_classify_fp4", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu), nu, rb,
+                      _abi.ptr(flags), 0, st)
+    elif method in ("tc", "tc8", "fp4") and tc_ok:
         a = batch.thermo(m_eff)
         bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
         bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
@@ -203,7 +225,7 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
         else:
             _abi.call("rsr_classify_tc", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu), nu,
                       a.shape[1], _abi.ptr(flags), 0, st)
-    elif method in ("bits", "tc"):
+    else:
         sb = batch.thermo_bits(m_eff)
         lb, nl = lower_set.device_bits(m_eff) if lower_set is not None else (None, 0)
         ub, nu = upper_set.device_bits(m_eff) if upper_set is not None else (None, 0)
@@ -212,8 +234,6 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
             fu = torch.empty(H, dtype=torch.int64, device=dev)
         _abi.call("rsr_classify_bits", _abi.ptr(sb), H, _abi.ptr(lb), nl, _abi.ptr(ub), nu,
                   sb.shape[1], _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
-    else:
-        raise ValueError("method must be 'tc' or 'bits'")
     return flags, fl, fu
 
 
@@ -266,35 +286,49 @@ def classify(batch: SampleBatch, lower_set: ReferenceSet | None, upper_set: Refe
 
 def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSet | None,
                   n_states: int, *, chunk_rows: int = 1 << 17,
-                  labels_out: torch.Tensor | None = None) -> tuple[torch.Tensor, tuple[int, int, int]]:
+                  labels_out: torch.Tensor | None = None,
+                  method: str = "tc") -> tuple[torch.Tensor, tuple[int, int, int]]:
     """Classify host-resident uint8 samples, streaming them through the GPU.
 
     ``states`` is a (preferably pinned) host uint8 tensor/array [S, N].  Chunks
     are copied on a side stream while the previous chunk is encoded and
-    classified (rsr_encode_samples + rsr_classify_tc), then rsr_finalize runs
-    once and the uint8 labels (0 lower / 1 upper / 2 unclassified) come back
-    into ``labels_out`` (host).  Returns (labels_out, counts).
+    classified (rsr_encode_samples_fp4 + rsr_classify_fp4; ``method="tc8"``:
+    rsr_encode_samples + rsr_classify_tc), then rsr_finalize runs once and the
+    uint8 labels (0 lower / 1 upper / 2 unclassified) come back into
+    ``labels_out`` (host).  Returns (labels_out, counts).
     """
     host = states if isinstance(states, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(states))
     if host.dtype != torch.uint8 or host.dim() != 2:
         raise ValueError("states must be a uint8 S x N host matrix")
+    if method not in ("tc", "tc8"):
+        raise ValueError("method must be 'tc' or 'tc8'")
     S, N = host.shape
     dev = _device.device()
     m_eff = max(2, n_states)
     for s in (lower_set, upper_set):
         if s is not None and len(s) and s.max_state >= m_eff:
             raise ValueError(f"states must lie in [0, {n_states - 1}]")
-    kpad = _abi.thermo_kpad(N, m_eff)
+    fp4 = method == "tc" and _abi.fp4_row_bytes(N, m_eff) <= _abi.FP4_MAX_ROW_BYTES
+    if fp4:
+        width = _abi.fp4_row_bytes(N, m_eff)
+        opnd_shape, opnd_dtype = (2 * width,), torch.uint8
+        bl, nl = lower_set.device_fp4(m_eff) if lower_set is not None else (None, 0)
+        bu, nu = upper_set.device_fp4(m_eff) if upper_set is not None else (None, 0)
+    else:
+        width = _abi.thermo_kpad(N, m_eff)
+        if width > TC_MAX_KPAD:
+            raise ValueError("rows too wide for the tensor-core classifiers")
+        opnd_shape, opnd_dtype = (width,), torch.int8
+        bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
+        bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
     comp = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
     chunk = max(1, min(chunk_rows, S))
     bufs = [torch.empty((chunk, N), dtype=torch.uint8, device=dev) for _ in range(2)]
-    therm = [torch.empty((chunk, kpad), dtype=torch.int8, device=dev) for _ in range(2)]
+    opnd = [torch.empty((chunk,) + opnd_shape, dtype=opnd_dtype, device=dev) for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
     free = [torch.cuda.Event() for _ in range(2)]
     flags = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
-    bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
-    bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
     st = _device.stream()
     for i, lo in enumerate(range(0, S, chunk)):
         hi = min(S, lo + chunk)
@@ -305,10 +339,16 @@ def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSe
             bufs[slot][: hi - lo].copy_(host[lo:hi], non_blocking=True)
             ready[slot].record(copy)
         comp.wait_event(ready[slot])
-        _abi.call("rsr_encode_samples", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
-                  _abi.ptr(therm[slot]), kpad, st)
-        _abi.call("rsr_classify_tc", _abi.ptr(therm[slot]), hi - lo, _abi.ptr(bl), nl, _abi.ptr(bu),
-                  nu, kpad, _abi.ptr(flags[lo:hi]), 0, st)
+        if fp4:
+            _abi.call("rsr_encode_samples_fp4", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
+                      _abi.ptr(opnd[slot]), width, st)
+            _abi.call("rsr_classify_fp4", _abi.ptr(opnd[slot]), hi - lo, _abi.ptr(bl), nl,
+                      _abi.ptr(bu), nu, width, _abi.ptr(flags[lo:hi]), 0, st)
+        else:
+            _abi.call("rsr_encode_samples", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
+                      _abi.ptr(opnd[slot]), width, st)
+            _abi.call("rsr_classify_tc", _abi.ptr(opnd[slot]), hi - lo, _abi.ptr(bl), nl,
+                      _abi.ptr(bu), nu, width, _abi.ptr(flags[lo:hi]), 0, st)
         free[slot].record(comp)
     labels = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
     counts_d = torch.empty(4, dtype=torch.int64, device=dev)

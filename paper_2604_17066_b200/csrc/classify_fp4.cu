@@ -1,0 +1,588 @@
+// (2) Dominance classification on block-scaled FP4 tensor cores
+// (tcgen05.mma.cta_group::2.kind::mxf4, e2m1 operands, unit ue8m0 scales).
+//
+// Replaces the same reference code as classify_tc.cu -- classify.py:99-148
+// (_chunk_hits / _hits_for: any reference with popcount(sample & ~ref) == 0)
+// and the precedence step classify.py:240-241 -- at twice the int8 MMA rate.
+// 0/1 operands and dot products <= N(M-1) are exact in e2m1 x e2m1 -> fp32, so
+// the result is the same integer violation count, but there are no negative
+// operands, so each side gets its own sample operand:
+//   upper ref r:  D = sum_c [x_n <  k] [r_n >= k]   (A_up = thermometer "below")
+//   lower ref r:  D = sum_c [x_n >= k] [r_n <  k]   (A_lo = its complement)
+// and D == 0 <=> x dominates r (upper) / is dominated by r (lower).  Column
+// Kdim = N(M-1) is a bias column: 1 in both sample operands, 0 in real
+// reference rows, 1 in never-hit pad rows (D >= 1).  See include/rsr_b200.h
+// ("FP4 layout").
+//
+// Kernel shape (persistent, one CTA pair per TPC, 384 threads per CTA):
+//   * operands are stored in HBM as rows of 32-byte chunks and land in shared
+//     memory chunk-major ([chunk][row][32 B], 32-byte swizzle) from ONE 3-D TMA
+//     box per operand tile, so a chunk is exactly one MMA K-step (64 e2m1) and
+//     no shared memory is spent on K padding;
+//   * a group of 256 samples (128 per CTA) holds both A_up and A_lo
+//     (2 x cq chunks), double-buffered so the next group loads during compute;
+//   * reference tiles of 240 rows (120 per CTA) stream through a ring of
+//     whole-tile stages; the leader issues cq MMAs M=256 N=240 K=64 per tile;
+//   * TMEM: accumulators at columns 0 and 240 (two buffers, the epilogue of
+//     tile j overlaps the MMAs of tile j+1), unit scale factors at 480..511;
+//   * 8 epilogue warps per CTA read the 128 x 240 fp32 accumulator
+//     (tcgen05.ld 32x32b), min-reduce the raw bits (all values are >= +0.0, so
+//     unsigned order = float order and 0 <=> hit), OR a hit bit per side, and
+//     optionally keep the first matching reference index (explain/strict).
+#include <stdlib.h>
+
+#include "tc_common.cuh"
+
+namespace {
+
+constexpr int kRowsA = 128;      // sample rows per CTA
+constexpr int kHalfN = 120;      // reference rows per CTA per tile
+constexpr int kTileN4 = 240;     // reference rows per pair tile (MMA N)
+constexpr int kChunk = 32;       // bytes per chunk = 64 e2m1 = one MMA K-step
+constexpr int kChunkA = kRowsA * kChunk;  // 4096 B
+constexpr int kChunkB = kHalfN * kChunk;  // 3840 B
+constexpr uint32_t kSfaCol = 480, kSfbCol = 496;
+
+struct Fp4Params {
+  int64_t S;
+  int n_groups;
+  int cq;           // chunks per operand row (row bytes / 32)
+  int nt_lower;     // tiles of lower refs (come first)
+  int nt_total;
+  int stages;
+  int a_bufs;
+  uint8_t* flags;
+  int accumulate;
+  int64_t* first_lower;
+  int64_t* first_upper;
+  int64_t first_base_lower;
+  int64_t first_base_upper;
+};
+
+__device__ __forceinline__ int tile_rot(int j, int rot, int nt) {
+  const int t = j + rot;
+  return t >= nt ? t - nt : t;
+}
+
+// SW32 K-major descriptor: 8-row core groups 256 B apart, version 1, layout 6.
+__device__ __forceinline__ uint32_t desc32_lo(uint32_t saddr) {
+  return ((saddr >> 4) & 0x3FFFu) | (1u << 16);
+}
+constexpr uint32_t kDesc32Hi = (256u >> 4) | (1u << 14) | (6u << 29);
+
+// kind::mxf4 instruction descriptor: A = B = e2m1 (1), D = f32, scales ue8m0,
+// K-major, K = 64, scale factor ids 0.
+__host__ __device__ constexpr uint32_t mxf4_idesc(int m, int n) {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (1u << 23) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_mxf4_pair(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo,
+                                               uint32_t idesc, uint32_t sfa, uint32_t sfb,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 da, {%1, %5};\n\t"
+      "mov.b64 db, {%2, %5};\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], da, db, %3, [%6], [%7], "
+      "p;\n\t}" ::"r"(d_tmem),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "r"(kDesc32Hi), "r"(sfa), "r"(sfb));
+}
+
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & kPeerMask), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+#define RSR_LD16(addr, v)                                                                      \
+  asm volatile(                                                                                \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15}, [%16];"                                                                       \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),    \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),             \
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])                                                  \
+      : "r"(addr))
+#define RSR_LD8(addr, v)                                                                        \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"        \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),        \
+                 "=r"(v[6]), "=r"(v[7])                                                         \
+               : "r"(addr))
+
+template <bool FIRST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                         const __grid_constant__ CUtensorMap map_lower,
+                         const __grid_constant__ CUtensorMap map_upper, const Fp4Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_addr(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+  const uint32_t a_buf_bytes = (uint32_t)(2 * p.cq * kChunkA);
+  const uint32_t b_stage_bytes = (uint32_t)(p.cq * kChunkB);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + (size_t)p.a_bufs * a_buf_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * b_stage_bytes);
+  uint64_t* b_full = bars;
+  uint64_t* b_empty = bars + p.stages;
+  uint64_t* a_full = bars + 2 * p.stages;  // [2]
+  uint64_t* a_empty = a_full + 2;          // [2]
+  uint64_t* t_full = a_full + 4;           // [2]
+  uint64_t* t_empty = a_full + 6;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 8);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lower)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_upper)));
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(smem_addr(&b_full[i]), 2);
+      mbar_init(smem_addr(&b_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_addr(&a_full[i]), 2);
+      mbar_init(smem_addr(&a_empty[i]), 1);
+      mbar_init(smem_addr(&t_full[i]), 1);
+      mbar_init(smem_addr(&t_empty[i]), 16);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_addr(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (warp >= 4 && warp < 8) {
+    // unit ue8m0 scale factors (0x7F = 2^0) for A and B in this CTA's TMEM
+    const uint32_t addr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + kSfaCol;
+    const uint32_t v = 0x7F7F7F7Fu;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
+        "r"(v));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const int rot = (int)(((int64_t)cluster * p.nt_total) / n_clusters);
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer (both CTAs)
+    int stage = 0, gi = 0;
+    uint32_t phase = 0;
+    const uint32_t sA0 = smem_addr(sA), sB0 = smem_addr(sB);
+    const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
+    for (int g = cluster; g < p.n_groups; g += n_clusters, ++gi) {
+      const int ab = gi % p.a_bufs;
+      const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
+      const uint32_t bar_af = smem_addr(&a_full[ab]);
+      mbar_wait(smem_addr(&a_empty[ab]), a_par ^ 1);
+      if (elect_one()) {
+        if (leader)
+          mbar_expect_tx(bar_af, 2 * a_buf_bytes);
+        else
+          mbar_arrive_leader(bar_af);
+        tma_load_3d_pair(sA0 + (uint32_t)ab * a_buf_bytes, &map_a, bar_af, 0,
+                         g * 2 * kRowsA + (int)rank * kRowsA, 0);
+      }
+      __syncwarp();
+      for (int jj = 0; jj < p.nt_total; ++jj) {
+        const int j = tile_rot(jj, rot, p.nt_total);
+        const bool low = j < p.nt_lower;
+        const CUtensorMap* map = low ? &map_lower : &map_upper;
+        const int y = (low ? j : j - p.nt_lower) * kTileN4 + (int)rank * kHalfN;
+        mbar_wait(bar_b_empty + 8 * stage, phase ^ 1);
+        if (elect_one()) {
+          if (leader)
+            mbar_expect_tx(bar_b_full + 8 * stage, 2 * b_stage_bytes);
+          else
+            mbar_arrive_leader(bar_b_full + 8 * stage);
+          tma_load_3d_pair(sB0 + (uint32_t)stage * b_stage_bytes, map, bar_b_full + 8 * stage, 0,
+                           y, 0);
+        }
+        __syncwarp();
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      constexpr uint32_t idesc = mxf4_idesc(2 * kRowsA, kTileN4);
+      const uint32_t tm0 = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t sfa = tm0 + kSfaCol, sfb = tm0 + kSfbCol;
+      const uint32_t a_lo0 = desc32_lo(smem_addr(sA)), b_lo0 = desc32_lo(smem_addr(sB));
+      const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
+      const int cq = p.cq;
+      int stage = 0, gi = 0;
+      uint32_t phase = 0, tc = 0;
+      for (int g = cluster; g < p.n_groups; g += n_clusters, ++gi) {
+        const int ab = gi % p.a_bufs;
+        mbar_wait(smem_addr(&a_full[ab]), (uint32_t)(gi / p.a_bufs) & 1);
+        tc_fence_after();
+        const uint32_t a_up = a_lo0 + (uint32_t)ab * (a_buf_bytes >> 4);
+        const uint32_t a_dn = a_up + (uint32_t)cq * (kChunkA >> 4);
+        for (int jj = 0; jj < p.nt_total; ++jj, ++tc) {
+          const int j = tile_rot(jj, rot, p.nt_total);
+          const uint32_t al = j < p.nt_lower ? a_dn : a_up;
+          const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
+          mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
+          tc_fence_after();
+          const uint32_t d = tm0 + buf * kTileN4;
+          mbar_wait(bar_b_full + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t bl = b_lo0 + (uint32_t)stage * (b_stage_bytes >> 4);
+          if (elect_one()) {
+            for (int ks = 0; ks < cq; ++ks)
+              umma_mxf4_pair(d, al + ks * (kChunkA >> 4), bl + ks * (kChunkB >> 4), idesc, sfa,
+                             sfb, ks != 0);
+            umma_commit_pair(bar_b_empty + 8 * stage);
+            umma_commit_pair(smem_addr(&t_full[buf]));
+          }
+          __syncwarp();
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit_pair(smem_addr(&a_empty[ab]));
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------ epilogue (both CTAs)
+    const int quad = warp & 3;
+    const int colhalf = (warp - 4) >> 2;
+    uint32_t tc = 0;
+    for (int g = cluster; g < p.n_groups; g += n_clusters) {
+      uint32_t hit = 0;
+      int64_t first[2] = {INT64_MAX, INT64_MAX};
+      for (int jj = 0; jj < p.nt_total; ++jj, ++tc) {
+        const int j = tile_rot(jj, rot, p.nt_total);
+        const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
+        mbar_wait(smem_addr(&t_full[buf]), tphase);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN4 + colhalf * kHalfN;
+        uint32_t v[kHalfN];
+        RSR_LD32(taddr, v);
+        RSR_LD32(taddr + 32, (v + 32));
+        RSR_LD32(taddr + 64, (v + 64));
+        RSR_LD16(taddr + 96, (v + 96));
+        RSR_LD8(taddr + 112, (v + 112));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(smem_addr(&t_empty[buf]));
+        uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 0; i < kHalfN; ++i) mn = min(mn, v[i]);
+        if (mn == 0) {
+          const bool low = j < p.nt_lower;
+          hit |= low ? RSR_HIT_LOWER : RSR_HIT_UPPER;
+          if (FIRST) {
+            int zc = 0;
+#pragma unroll
+            for (int i = kHalfN - 1; i >= 0; --i)
+              if (v[i] == 0) zc = i;
+            const int64_t ref = (low ? p.first_base_lower + (int64_t)j * kTileN4
+                                     : p.first_base_upper + (int64_t)(j - p.nt_lower) * kTileN4) +
+                                colhalf * kHalfN + zc;
+            first[low ? 0 : 1] = min(first[low ? 0 : 1], ref);
+          }
+        }
+      }
+      // the two column halves of a row live in two warps: combine through shared memory
+      const int64_t row = (int64_t)g * 2 * kRowsA + rank * kRowsA + quad * 32 + lane;
+      uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 10);  // [128]
+      int64_t* xfirst = reinterpret_cast<int64_t*>(xchg + 128);   // [2][128] (FIRST)
+      named_bar_sync(1, 256);
+      if (colhalf == 1) {
+        xchg[quad * 32 + lane] = hit;
+        if (FIRST) {
+          xfirst[quad * 32 + lane] = first[0];
+          xfirst[128 + quad * 32 + lane] = first[1];
+        }
+      }
+      named_bar_sync(1, 256);
+      if (colhalf == 0) {
+        hit |= xchg[quad * 32 + lane];
+        if (row < p.S) {
+          const uint8_t prev = p.accumulate ? p.flags[row] : 0;
+          p.flags[row] = (uint8_t)(prev | hit);
+          if (FIRST) {
+#pragma unroll
+            for (int sd = 0; sd < 2; ++sd) {
+              int64_t* out = sd ? p.first_upper : p.first_lower;
+              if (!out) continue;
+              const int64_t f = min(first[sd], xfirst[sd * 128 + quad * 32 + lane]);
+              const int64_t mine = f == INT64_MAX ? -1 : f;
+              const int64_t old = p.accumulate ? out[row] : -1;  // earlier chunks win
+              out[row] = old >= 0 ? old : mine;
+            }
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+__global__ void clear_flags4_kernel(uint8_t* flags, int64_t S) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < S) flags[i] = 0;
+}
+
+// rows of `row_bytes` viewed as {32 B, rows, chunks} (strides {row_bytes, 32});
+// one box = `box_rows` rows x `chunks` chunks, landing chunk-major, 32 B swizzle.
+int make_map3(CUtensorMap* map, const void* base, int64_t rows, int row_bytes, int chunks,
+              int box_rows) {
+  auto enc = tensor_map_encoder();
+  RSR_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)kChunk, (cuuint64_t)rows, (cuuint64_t)chunks};
+  cuuint64_t strides[2] = {(cuuint64_t)row_bytes, (cuuint64_t)kChunk};
+  cuuint32_t box[3] = {(cuuint32_t)kChunk, (cuuint32_t)box_rows, (cuuint32_t)chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    rsr::set_error("cuTensorMapEncodeTiled (fp4) failed (%d)", (int)r);
+    return RSR_ECUDA;
+  }
+  return RSR_OK;
+}
+
+int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64_t n_lower,
+                      const uint8_t* B_upper, int64_t n_upper, int row_bytes, uint8_t* flags,
+                      int64_t* first_lower, int64_t* first_upper, int accumulate, void* stream) {
+  const bool want_first = first_lower != nullptr || first_upper != nullptr;
+  RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4: negative size");
+  RSR_REQUIRE(row_bytes >= kChunk && row_bytes % kChunk == 0,
+              "rsr_classify_fp4: row_bytes must be a positive multiple of 32");
+  RSR_REQUIRE(row_bytes <= RSR_FP4_MAX_ROW_BYTES, "rsr_classify_fp4: row_bytes > %d unsupported",
+              RSR_FP4_MAX_ROW_BYTES);
+  RSR_REQUIRE(S <= ((int64_t)1 << 31) - 2 * kRowsA, "rsr_classify_fp4: S too large");
+  cudaStream_t st = rsr::as_stream(stream);
+  if (S == 0) return RSR_OK;
+  RSR_REQUIRE(flags != nullptr && A != nullptr, "rsr_classify_fp4: null pointer");
+  const int64_t nt_l = rsr::ceil_div(n_lower, kTileN4), nt_u = rsr::ceil_div(n_upper, kTileN4);
+  if (nt_l + nt_u == 0) {
+    if (!accumulate) {
+      clear_flags4_kernel<<<(unsigned)rsr::ceil_div(S, 256), 256, 0, st>>>(flags, S);
+      int rc0 = rsr::check_launch("clear_flags4_kernel");
+      if (rc0) return rc0;
+      for (int64_t* f : {first_lower, first_upper})
+        if (f) RSR_CUDA(cudaMemsetAsync(f, 0xFF, S * sizeof(int64_t), st));  // -1
+    }
+    return RSR_OK;
+  }
+  RSR_REQUIRE(nt_l + nt_u < (1 << 30), "rsr_classify_fp4: too many reference tiles");
+  RSR_REQUIRE((nt_l == 0 || B_lower) && (nt_u == 0 || B_upper), "rsr_classify_fp4: null refs");
+
+  int dev = 0, sm_count = 0;
+  RSR_CUDA(cudaGetDevice(&dev));
+  RSR_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+
+  const int cq = row_bytes / kChunk;
+  CUtensorMap ma;
+  int rc = make_map3(&ma, A, S, 2 * row_bytes, 2 * cq, kRowsA);
+  if (rc) return rc;
+
+  Fp4Params p;
+  p.S = S;
+  p.cq = cq;
+  p.flags = flags;
+  p.first_lower = first_lower;
+  p.first_upper = first_upper;
+  const size_t max_smem = 227 * 1024;
+  const size_t fixed = 1024 + 1024 + (want_first ? 2048 : 0);  // align slack, barriers, exchange
+  const size_t a_buf = (size_t)2 * cq * kChunkA, b_stage = (size_t)cq * kChunkB;
+  p.a_bufs = 2;
+  const char* ab_env = getenv("RSR_TC_ABUFS");
+  if ((ab_env && atoi(ab_env) == 1) || fixed + 2 * a_buf + 4 * b_stage > max_smem) p.a_bufs = 1;
+  int stages = (int)((max_smem - fixed - p.a_bufs * a_buf) / b_stage);
+  if (stages > 12) stages = 12;
+  RSR_REQUIRE(stages >= 2, "rsr_classify_fp4: row_bytes too large for shared memory");
+  p.stages = stages;
+  const size_t smem = fixed + p.a_bufs * a_buf + (size_t)stages * b_stage;
+  p.n_groups = (int)rsr::ceil_div(S, (int64_t)2 * kRowsA);
+  auto kern = want_first ? classify_fp4_pair_kernel<true> : classify_fp4_pair_kernel<false>;
+  RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int clusters = sm_count / 2;
+  if (p.n_groups < clusters) clusters = p.n_groups;
+
+  // Reference chunks: a launch's B slice must stay L2-resident while every
+  // group streams it (512 tiles = 122,880 refs x row_bytes: 20 MB at 160 B).
+  const char* ct = getenv("RSR_TC_CHUNK_TILES");
+  const int64_t chunk = ct ? atoll(ct) : 512;
+  const int64_t total = nt_l + nt_u;
+  for (int64_t c0 = 0; c0 < total; c0 += chunk) {
+    const int64_t c1 = c0 + chunk < total ? c0 + chunk : total;
+    const int64_t l0 = c0 < nt_l ? c0 : nt_l, l1 = c1 < nt_l ? c1 : nt_l;
+    const int64_t u0 = (c0 > nt_l ? c0 : nt_l) - nt_l, u1 = (c1 > nt_l ? c1 : nt_l) - nt_l;
+    Fp4Params q = p;
+    q.nt_lower = (int)(l1 - l0);
+    q.nt_total = (int)((l1 - l0) + (u1 - u0));
+    q.accumulate = c0 == 0 ? accumulate : 1;
+    q.first_base_lower = l0 * kTileN4;
+    q.first_base_upper = u0 * kTileN4;
+    const uint8_t* lb = l1 > l0 ? B_lower + l0 * kTileN4 * (int64_t)row_bytes : nullptr;
+    const uint8_t* ub = u1 > u0 ? B_upper + u0 * kTileN4 * (int64_t)row_bytes : nullptr;
+    CUtensorMap cl, cu;
+    rc = make_map3(&cl, lb ? lb : ub, (lb ? l1 - l0 : u1 - u0) * kTileN4, row_bytes, cq, kHalfN);
+    if (rc) return rc;
+    rc = make_map3(&cu, ub ? ub : lb, (ub ? u1 - u0 : l1 - l0) * kTileN4, row_bytes, cq, kHalfN);
+    if (rc) return rc;
+    kern<<<2 * clusters, 384, smem, st>>>(ma, cl, cu, q);
+    rc = rsr::check_launch("classify_fp4_pair_kernel");
+    if (rc) return rc;
+  }
+  return RSR_OK;
+}
+
+// ---------------------------------------------------------------- encoders
+// Sample operand row i: [A_up (row_bytes) | A_lo (row_bytes)], element c in
+// byte c/2, low nibble for even c; e2m1 1.0 = 0x2.
+__global__ void encode_samples_fp4_kernel(const uint8_t* __restrict__ states, int64_t count,
+                                          int N, int M, uint8_t* __restrict__ out,
+                                          int row_bytes, int kdim) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * row_bytes) return;
+  const int64_t i = t / row_bytes;
+  const int b = (int)(t - i * row_bytes);
+  const uint8_t* x = states + i * N;
+  uint32_t up = 0, lo = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = 2 * b + h;
+    uint32_t u, l;
+    if (c < kdim) {
+      int n, k;
+      if (M == 2) {
+        n = c;
+        k = 1;
+      } else {
+        n = c / (M - 1);
+        k = c - n * (M - 1) + 1;
+      }
+      u = x[n] < k;
+      l = 1 - u;
+    } else {
+      u = l = (c == kdim);
+    }
+    up |= (u ? 0x2u : 0u) << (4 * h);
+    lo |= (l ? 0x2u : 0u) << (4 * h);
+  }
+  uint8_t* row = out + i * (int64_t)(2 * row_bytes);
+  row[b] = (uint8_t)up;
+  row[row_bytes + b] = (uint8_t)lo;
+}
+
+// Reference operand rows: upper [r_n >= k], lower [r_n < k], bias column 0;
+// rows [count, rows_total) are never-hit pad rows (bias column 1).
+__global__ void encode_refs_fp4_kernel(const uint8_t* __restrict__ states, int64_t count,
+                                       int64_t rows_total, int N, int M, int side,
+                                       uint8_t* __restrict__ out, int row_bytes, int kdim) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows_total * row_bytes) return;
+  const int64_t r = t / row_bytes;
+  const int b = (int)(t - r * row_bytes);
+  uint32_t v = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = 2 * b + h;
+    uint32_t e;
+    if (r >= count) {
+      e = c == kdim;
+    } else if (c < kdim) {
+      const int n = c / (M - 1), k = c - n * (M - 1) + 1;
+      const uint32_t lt = states[r * N + n] < k;
+      e = side == RSR_SIDE_UPPER ? 1 - lt : lt;
+    } else {
+      e = 0;
+    }
+    v |= (e ? 0x2u : 0u) << (4 * h);
+  }
+  out[t] = (uint8_t)v;
+}
+
+}  // namespace
+
+extern "C" int rsr_fp4_row_bytes(int n_components, int n_states) {
+  if (n_components < 1 || n_states < 2) return 0;
+  const int kdim = n_components * (n_states - 1);
+  return (kdim + 1 + 63) / 64 * 32;
+}
+
+extern "C" int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int n_components,
+                                      int n_states, uint8_t* out, int row_bytes, void* stream) {
+  const int N = n_components, M = n_states;
+  RSR_REQUIRE(N >= 1 && M >= 2 && count >= 0, "rsr_encode_samples_fp4: bad shape");
+  RSR_REQUIRE(row_bytes == rsr_fp4_row_bytes(N, M), "rsr_encode_samples_fp4: row_bytes must be %d",
+              rsr_fp4_row_bytes(N, M));
+  if (count == 0) return RSR_OK;
+  RSR_REQUIRE(states != nullptr && out != nullptr, "rsr_encode_samples_fp4: null pointer");
+  const int64_t total = count * row_bytes;
+  encode_samples_fp4_kernel<<<(unsigned)rsr::ceil_div(total, 256), 256, 0,
+                              rsr::as_stream(stream)>>>(states, count, N, M, out, row_bytes,
+                                                        N * (M - 1));
+  return rsr::check_launch("encode_samples_fp4_kernel");
+}
+
+extern "C" int rsr_encode_refs_fp4(const uint8_t* states, int64_t count, int64_t rows_total,
+                                   int n_components, int n_states, int side, uint8_t* out,
+                                   int row_bytes, void* stream) {
+  const int N = n_components, M = n_states;
+  RSR_REQUIRE(N >= 1 && M >= 2 && count >= 0 && rows_total >= count,
+              "rsr_encode_refs_fp4: bad shape");
+  RSR_REQUIRE(side == RSR_SIDE_LOWER || side == RSR_SIDE_UPPER, "rsr_encode_refs_fp4: bad side");
+  RSR_REQUIRE(row_bytes == rsr_fp4_row_bytes(N, M), "rsr_encode_refs_fp4: row_bytes must be %d",
+              rsr_fp4_row_bytes(N, M));
+  if (rows_total == 0) return RSR_OK;
+  RSR_REQUIRE(out != nullptr && (count == 0 || states != nullptr),
+              "rsr_encode_refs_fp4: null pointer");
+  const int64_t total = rows_total * row_bytes;
+  encode_refs_fp4_kernel<<<(unsigned)rsr::ceil_div(total, 256), 256, 0,
+                           rsr::as_stream(stream)>>>(states, count, rows_total, N, M, side, out,
+                                                     row_bytes, N * (M - 1));
+  return rsr::check_launch("encode_refs_fp4_kernel");
+}
+
+extern "C" int rsr_classify_fp4(const uint8_t* A, int64_t S, const uint8_t* B_lower,
+                                int64_t n_lower, const uint8_t* B_upper, int64_t n_upper,
+                                int row_bytes, uint8_t* flags, int accumulate, void* stream) {
+  return classify_fp4_impl(A, S, B_lower, n_lower, B_upper, n_upper, row_bytes, flags, nullptr,
+                           nullptr, accumulate, stream);
+}
+
+extern "C" int rsr_classify_fp4_explain(const uint8_t* A, int64_t S, const uint8_t* B_lower,
+                                        int64_t n_lower, const uint8_t* B_upper, int64_t n_upper,
+                                        int row_bytes, uint8_t* flags, int64_t* first_lower,
+                                        int64_t* first_upper, int accumulate, void* stream) {
+  return classify_fp4_impl(A, S, B_lower, n_lower, B_upper, n_upper, row_bytes, flags,
+                           first_lower, first_upper, accumulate, stream);
+}

@@ -32,6 +32,7 @@ class SampleBatch:
         self._dev: torch.Tensor | None = None
         self._thermo: dict[int, torch.Tensor] = {}
         self._bits: dict[int, torch.Tensor] = {}
+        self._fp4: dict[int, torch.Tensor] = {}
         if isinstance(states, torch.Tensor):
             if states.dim() != 2:
                 raise ValueError("states must be an H x N matrix")
@@ -94,6 +95,25 @@ class SampleBatch:
             self._thermo[n_states] = t
         return t
 
+    def fp4(self, n_states: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """FP4 sample operand [H, 2 * row_bytes] = [A_up | A_lo] packed e2m1 rows
+        (A operand of the FP4 classifier, include/rsr_b200.h), cached per M."""
+        t = self._fp4.get(n_states)
+        if t is None:
+            n = self.n_components
+            rb = _abi.fp4_row_bytes(n, n_states)
+            st = self.device_states()
+            if out is not None:
+                if out.dtype != torch.uint8 or out.shape[0] < self.n_samples or out.shape[1] != 2 * rb:
+                    raise ValueError("fp4 buffer must be uint8 [>= H, 2 * row_bytes]")
+                t = out[: self.n_samples]
+            else:
+                t = torch.empty((self.n_samples, 2 * rb), dtype=torch.uint8, device=st.device)
+            _abi.call("rsr_encode_samples_fp4", _abi.ptr(st), self.n_samples, n, n_states,
+                      _abi.ptr(t), rb, _device.stream())
+            self._fp4[n_states] = t
+        return t
+
     def thermo_bits(self, n_states: int) -> torch.Tensor:
         """Packed thermometer bits [H, words] (bit-packed classifier operand)."""
         t = self._bits.get(n_states)
@@ -110,6 +130,7 @@ class SampleBatch:
     def release_thermo(self) -> None:
         self._thermo.clear()
         self._bits.clear()
+        self._fp4.clear()
 
 
 def uniform_field(seed: int, generation_index: int, start: int, count: int,
@@ -123,13 +144,16 @@ def uniform_field(seed: int, generation_index: int, start: int, count: int,
 
 
 def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
-                 generation_index: int = 0, start: int = 0, *, encode: bool = True,
+                 generation_index: int = 0, start: int = 0, *, encode: bool = False,
                  out_states: torch.Tensor | None = None,
-                 out_thermo: torch.Tensor | None = None) -> SampleBatch:
+                 out_thermo: torch.Tensor | None = None,
+                 out_fp4: torch.Tensor | None = None) -> SampleBatch:
     """Inverse-CDF draw on the counter-based stream (sampling.py:69-90), on device.
 
-    ``encode`` also writes the thermometer rows for M = dist.n_states in the
-    same kernel.  ``out_*`` let callers reuse preallocated buffers.
+    ``encode`` (or ``out_thermo``) also writes the int8 thermometer rows for
+    M = dist.n_states in the same kernel; ``out_fp4`` encodes the FP4 operand
+    of the default classifier into that buffer right after sampling.
+    ``out_*`` let callers reuse preallocated buffers.
     """
     if n_samples < 1:
         raise ValueError("n_samples must be >= 1")
@@ -139,7 +163,7 @@ def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
         (n_samples, n), dtype=torch.uint8, device=dev)
     thermo = None
     kpad = _abi.thermo_kpad(n, m)
-    if encode:
+    if encode or out_thermo is not None:
         thermo = out_thermo if out_thermo is not None else torch.empty(
             (n_samples, kpad), dtype=torch.int8, device=dev)
     mask = (1 << 64) - 1
@@ -149,4 +173,6 @@ def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
     batch = SampleBatch(states, seed, generation_index, state_bound=m)
     if thermo is not None:
         batch._thermo[m] = thermo
+    if out_fp4 is not None:
+        batch.fp4(m, out=out_fp4)
     return batch

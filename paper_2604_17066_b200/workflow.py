@@ -1,7 +1,7 @@
 """Two-stage RSR workflow on the device (mirror of reference ``workflow.py``).
 
 Stage 1 (workflow.py:122-195), per iteration ``i``:
-  rsr_sample (gen = i) -> rsr_classify_tc -> rsr_finalize (counts to host)
+  rsr_sample (gen = i) -> rsr_encode_samples_fp4 -> rsr_classify_fp4 -> rsr_finalize
   -> trace record -> termination test -> picks from
   ``default_rng([seed, i]).choice(U, size, replace=False)`` (the reference's
   own RNG call; positions into the sorted unclassified list, which
@@ -127,12 +127,14 @@ class _BatchBuffers:
     def __init__(self, count: int, n: int, m: int):
         dev = _device.device()
         self.states = torch.empty((count, n), dtype=torch.uint8, device=dev)
-        self.thermo = torch.empty((count, _abi.thermo_kpad(n, m)), dtype=torch.int8, device=dev)
+        self.fp4_ok = _abi.fp4_row_bytes(n, m) <= _abi.FP4_MAX_ROW_BYTES
+        self.fp4 = (torch.empty((count, 2 * _abi.fp4_row_bytes(n, m)), dtype=torch.uint8, device=dev)
+                    if self.fp4_ok else None)
 
 
 def _classify_shard(model, dist_, seed, gen, lower, upper, comm, bufs, start, count):
     batch = sample_batch(dist_, count, seed, gen, start, out_states=bufs.states,
-                         out_thermo=bufs.thermo)
+                         out_fp4=bufs.fp4 if bufs.fp4_ok else None)
     res = classify(batch, lower, upper, n_states=model.n_component_states)
     counts = comm.allreduce_sum_i64(list(res.counts)) if comm.distributed else np.array(res.counts)
     return batch, res, counts

@@ -87,7 +87,7 @@ def test_encoding_worked_examples():
 
 # ----------------------------------------------------------- classification
 
-@pytest.mark.parametrize("method", ["tc", "bits"])
+@pytest.mark.parametrize("method", ["tc", "tc8", "bits"])
 def test_classify_golden(method):
     g = load_npz("classify.npz")
     for i, m in enumerate(g["n_states"]):
@@ -153,13 +153,14 @@ def test_classify_random_vs_oracle(seed):
     want = oracle.classify_labels(samples, lower, upper, m)
     lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
     up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
-    for method in ("tc", "bits"):
+    for method in ("tc", "tc8", "bits"):
         r = P.classify(P.SampleBatch(samples, 0, 0), lo, up, n_states=m, method=method)
         assert np.array_equal(r.labels_device.cpu().numpy(), want["labels"])
 
 
+@pytest.mark.parametrize("method", ["tc", "tc8"])
 @pytest.mark.parametrize("chunk_tiles", ["1", "256"])
-def test_explain_first_match_tensor_core_chunked(chunk_tiles, monkeypatch):
+def test_explain_first_match_tensor_core_chunked(chunk_tiles, method, monkeypatch):
     # first-match indices from the tensor-core epilogue, also across chunked launches
     monkeypatch.setenv("RSR_TC_CHUNK_TILES", chunk_tiles)
     rng = np.random.default_rng(9)
@@ -170,7 +171,7 @@ def test_explain_first_match_tensor_core_chunked(chunk_tiles, monkeypatch):
     want = oracle.classify_labels(samples, lower, upper, m, want_first=True)
     lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
     up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
-    r = P.classify(P.SampleBatch(samples, 0, 0), lo, up, n_states=m, explain=True, method="tc")
+    r = P.classify(P.SampleBatch(samples, 0, 0), lo, up, n_states=m, explain=True, method=method)
     assert np.array_equal(r.labels_device.cpu().numpy(), want["labels"])
     assert np.array_equal(r.first_match_lower, want["first_lower"])
     assert np.array_equal(r.first_match_upper, want["first_upper"])
@@ -207,8 +208,10 @@ def test_cfg2_full_size_tc_equals_bits_and_slice_equals_oracle(mixed):
     lo, up, lower, upper = _cfg2_sets(mixed)
     b = P.sample_batch(d, 1 << 20, seed=0)
     tc = P.classify(b, lo, up, n_states=2, method="tc")
+    tc8 = P.classify(b, lo, up, n_states=2, method="tc8")
     bits = P.classify(b, lo, up, n_states=2, method="bits")
     assert torch.equal(tc.labels_device, bits.labels_device)
+    assert torch.equal(tc8.labels_device, bits.labels_device)
     assert tc.counts == bits.counts and sum(tc.counts) == 1 << 20
     if mixed:
         assert min(tc.counts) > 10_000  # all three labels are exercised

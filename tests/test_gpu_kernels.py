@@ -73,6 +73,80 @@ def _classify_tc(samples, lower, upper, n, m):
     return flags.cpu().numpy()
 
 
+def _fp4_rows(bits):
+    """Pack 0/1 element rows as e2m1 (1.0 = 0x2), element c in byte c // 2, low nibble first."""
+    b = np.asarray(bits, dtype=np.uint8)
+    return (b[:, 0::2] * 0x2) | (b[:, 1::2] * 0x20)
+
+
+def _fp4_want(samples, refs, n, m, side, rows_total=None):
+    """numpy restatement of the FP4 operand layout (include/rsr_b200.h)."""
+    kdim = n * (m - 1)
+    width = 2 * A.fp4_row_bytes(n, m)  # elements per row
+    cols = [(j // (m - 1), j % (m - 1) + 1) for j in range(kdim)]
+    if samples is not None:
+        up = np.zeros((samples.shape[0], width), dtype=np.uint8)
+        for c, (j, k) in enumerate(cols):
+            up[:, c] = samples[:, j] < k
+        lo = np.zeros_like(up)
+        lo[:, :kdim] = 1 - up[:, :kdim]
+        up[:, kdim] = lo[:, kdim] = 1
+        return np.concatenate([_fp4_rows(up), _fp4_rows(lo)], axis=1)
+    rows = np.zeros((rows_total, width), dtype=np.uint8)
+    for c, (j, k) in enumerate(cols):
+        lt = refs[:, j] < k
+        rows[: refs.shape[0], c] = (~lt) if side == A.SIDE_UPPER else lt
+    rows[refs.shape[0]:, kdim] = 1
+    return _fp4_rows(rows)
+
+
+def _fp4_refs_dev(refs, n, m, side):
+    rb = A.fp4_row_bytes(n, m)
+    k = refs.shape[0]
+    rows = max(240, (k + 239) // 240 * 240)
+    out = torch.empty((rows, rb), dtype=torch.uint8, device="cuda")
+    A.call("rsr_encode_refs_fp4", A.ptr(_dev(refs.astype(np.uint8))) if k else None, k, rows, n, m,
+           side, A.ptr(out), rb, A.stream_ptr())
+    return out
+
+
+def _classify_fp4(samples, lower, upper, n, m, first=False):
+    rb = A.fp4_row_bytes(n, m)
+    s = samples.shape[0]
+    a = torch.empty((s, 2 * rb), dtype=torch.uint8, device="cuda")
+    A.call("rsr_encode_samples_fp4", A.ptr(_dev(samples.astype(np.uint8))), s, n, m, A.ptr(a), rb,
+           A.stream_ptr())
+    bl = _fp4_refs_dev(lower, n, m, A.SIDE_LOWER)
+    bu = _fp4_refs_dev(upper, n, m, A.SIDE_UPPER)
+    flags = torch.empty(s, dtype=torch.uint8, device="cuda")
+    if first:
+        fl = torch.empty(s, dtype=torch.int64, device="cuda")
+        fu = torch.empty(s, dtype=torch.int64, device="cuda")
+        A.call("rsr_classify_fp4_explain", A.ptr(a), s, A.ptr(bl), lower.shape[0], A.ptr(bu),
+               upper.shape[0], rb, A.ptr(flags), A.ptr(fl), A.ptr(fu), 0, A.stream_ptr())
+        return flags.cpu().numpy(), fl.cpu().numpy(), fu.cpu().numpy()
+    A.call("rsr_classify_fp4", A.ptr(a), s, A.ptr(bl), lower.shape[0], A.ptr(bu), upper.shape[0], rb,
+           A.ptr(flags), 0, A.stream_ptr())
+    return flags.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,m,s,k", [(295, 2, 300, 250), (7, 3, 33, 5), (64, 2, 10, 0), (63, 2, 5, 3),
+                                     (100, 4, 17, 241)])
+def test_fp4_encoders_layout(n, m, s, k):
+    rng = np.random.default_rng(n + m)
+    samples = rng.integers(0, m, size=(s, n))
+    refs = rng.integers(0, m, size=(k, n))
+    rb = A.fp4_row_bytes(n, m)
+    assert rb == A.call("rsr_fp4_row_bytes", n, m) and rb % 32 == 0 and 2 * rb > n * (m - 1)
+    a = torch.empty((s, 2 * rb), dtype=torch.uint8, device="cuda")
+    A.call("rsr_encode_samples_fp4", A.ptr(_dev(samples.astype(np.uint8))), s, n, m, A.ptr(a), rb,
+           A.stream_ptr())
+    assert np.array_equal(a.cpu().numpy(), _fp4_want(samples, None, n, m, None))
+    for side in (A.SIDE_LOWER, A.SIDE_UPPER):
+        got = _fp4_refs_dev(refs, n, m, side).cpu().numpy()
+        assert np.array_equal(got, _fp4_want(None, refs, n, m, side, got.shape[0]))
+
+
 def _classify_bits(samples, lower, upper, n, m, first=False):
     w = A.thermo_words(n, m)
     s = samples.shape[0]
@@ -121,6 +195,8 @@ def test_classifiers_match_oracle(n, m, s, kl, ku, p1):
     assert want.min() == 0 or True
     got_tc = _classify_tc(samples, lower, upper, n, m)
     assert np.array_equal(got_tc, want), f"tc mismatch at {np.flatnonzero(got_tc != want)[:10]}"
+    got_fp4 = _classify_fp4(samples, lower, upper, n, m)
+    assert np.array_equal(got_fp4, want), f"fp4 mismatch at {np.flatnonzero(got_fp4 != want)[:10]}"
     got_bits = _classify_bits(samples, lower, upper, n, m)
     assert np.array_equal(got_bits, want)
 
@@ -136,6 +212,24 @@ def test_reference_chunked_launches(chunk_tiles, monkeypatch):
     upper = np.clip(samples[rng.integers(0, s, 600)] - rng.integers(0, 2, (600, n)), 0, 1)
     got = _classify_tc(samples, lower, upper, n, m)
     assert np.array_equal(got, _want_flags(samples, lower, upper, m))
+    assert np.array_equal(_classify_fp4(samples, lower, upper, n, m), _want_flags(samples, lower, upper, m))
+
+
+@pytest.mark.parametrize("n,m", [(295, 2), (295, 3), (440, 2), (120, 4), (895, 2)])
+def test_fp4_first_match_and_widths(n, m):
+    # every supported row width class (cq = 1 .. 14 chunks), first-match indices vs oracle
+    rng = np.random.default_rng(n * 7 + m)
+    s, kl, ku = 1100, 500, 700
+    samples = rng.integers(0, m, size=(s, n))
+    lower = np.clip(samples[rng.integers(0, s, kl)] + rng.integers(0, 2, (kl, n)), 0, m - 1)
+    upper = np.clip(samples[rng.integers(0, s, ku)] - rng.integers(0, 2, (ku, n)), 0, m - 1)
+    want = oracle.classify_labels(samples, lower, upper, m, want_first=True)
+    flags, fl, fu = _classify_fp4(samples, lower, upper, n, m, first=True)
+    assert np.array_equal(flags, _want_flags(samples, lower, upper, m))
+    hl, fl_want = oracle.dominance_hits(samples, lower, m, oracle.LOWER, want_first=True)
+    hu, fu_want = oracle.dominance_hits(samples, upper, m, oracle.UPPER, want_first=True)
+    assert np.array_equal(fl, fl_want) and np.array_equal(fu, fu_want)
+    assert want["labels"].shape == (s,)
 
 
 def test_first_match_and_violation_counts():

@@ -67,7 +67,7 @@ def test_random_classifier_shapes(seed):
     lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
     up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
     batch = P.SampleBatch(samples, 0, 0)
-    for method in ("tc", "bits"):
+    for method in ("tc", "tc8", "bits"):
         r = P.classify(batch, lo, up, n_states=m, method=method)
         assert np.array_equal(r.labels_device.cpu().numpy(), want), (method, n, m, h, kl, ku)
         assert r.counts == (int((want == 0).sum()), int((want == 1).sum()), int((want == 2).sum()))
