@@ -145,11 +145,12 @@ int rsr_classify_tc_explain(const int8_t* A, int64_t S, const int8_t* B_lower,
  *     A_lo[c] = [x_n >= k] (c < Kdim), both 1 at the bias column c = Kdim;
  *   upper ref row: [r_n >= k], lower ref row: [r_n < k], bias column 0;
  *   pad ref rows: only the bias column set (never hit).
- * Reference buffers hold ceil(n/240)*240 rows (tiles of 240).  D = A_up.B_up
+ * Reference buffers need n rows (the kernel masks columns past the last row of
+ * a side; pad rows written by rsr_encode_refs_fp4 are harmless).  D = A_up.B_up
  * (upper) or A_lo.B_lo (lower) counts violated thermometer columns exactly
  * (fp32 accumulation of 0/1 products); D == 0 <=> dominance.  flags and
  * accumulate as rsr_classify_tc.  row_bytes <= RSR_FP4_MAX_ROW_BYTES. */
-#define RSR_FP4_MAX_ROW_BYTES 448
+#define RSR_FP4_MAX_ROW_BYTES 416
 #define RSR_FP4_TILE_ROWS 240
 int rsr_fp4_row_bytes(int n_components, int n_states);
 int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int n_components,

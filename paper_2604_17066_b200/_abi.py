@@ -21,6 +21,8 @@ __all__ = ["lib", "call", "stream_ptr", "ptr", "PhiDesc", "LIB_PATH", "require_d
            "FP4_MAX_ROW_BYTES", "EXPORTED"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librsr_b200.so")
+# timing experiments (tools/fp4_prof.py) may load an instrumented build instead
+LIB_PATH = os.environ.get("RSR_LIB_OVERRIDE", LIB_PATH)
 
 RSR_OK, RSR_EINVAL, RSR_ECUDA, RSR_EUNSUPPORTED = 0, 1, 2, 3
 SIDE_LOWER, SIDE_UPPER = 0, 1
@@ -154,7 +156,7 @@ def thermo_kpad(n: int, m: int) -> int:
 
 
 FP4_TILE_ROWS = 240
-FP4_MAX_ROW_BYTES = 448
+FP4_MAX_ROW_BYTES = 416
 
 
 def fp4_row_bytes(n: int, m: int) -> int:

@@ -36,12 +36,54 @@
 namespace {
 
 constexpr int kRowsA = 128;      // sample rows per CTA
-constexpr int kHalfN = 120;      // reference rows per CTA per tile
-constexpr int kTileN4 = 240;     // reference rows per pair tile (MMA N)
 constexpr int kChunk = 32;       // bytes per chunk = 64 e2m1 = one MMA K-step
 constexpr int kChunkA = kRowsA * kChunk;  // 4096 B
-constexpr int kChunkB = kHalfN * kChunk;  // 3840 B
 constexpr uint32_t kSfaCol = 480, kSfbCol = 496;
+
+// Reference tiles are 240 rows (120 per CTA).  TMEM holds two accumulator
+// buffers of 240 columns (0..479; 480..511 hold the scale factors), so the
+// epilogue of tile j overlaps the MMAs of tile j+1.  Reading a 128 x 240 fp32
+// accumulator out of TMEM is the epilogue's cost and it is latency bound per
+// warp (tools/tmem_bw.cu: 175 / 324 / 459 B/clk per SM with 4 / 8 / 16 reading
+// warps), so kEpiWarps warps (4 per TMEM lane quarter) each own 240 / (kEpiWarps
+// / 4) columns.
+#ifndef RSR_FP4_EPI_WARPS
+#define RSR_FP4_EPI_WARPS 16
+#endif
+#ifndef RSR_FP4_TILE_N
+#define RSR_FP4_TILE_N 240
+#endif
+constexpr int kEpiWarps = RSR_FP4_EPI_WARPS;
+constexpr int kColGroups = kEpiWarps / 4;
+constexpr int kTileN = RSR_FP4_TILE_N;        // MMA N: 240 (2 buffers) or 160 (3 buffers)
+constexpr int kBufs = 480 / kTileN;           // accumulator buffers in TMEM columns 0..479
+constexpr int kHalfRows = kTileN / 2;         // reference rows per CTA per tile
+constexpr int kChunkB = kHalfRows * kChunk;   // 3840 B
+constexpr int kCols = kTileN / kColGroups;    // accumulator columns per epilogue warp
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+static_assert(kTileN % kColGroups == 0 && kCols % 4 == 0, "bad epilogue split");
+
+// RSR_FP4_PROF builds (tools/ only, never the product library) accumulate
+// per-role cycle counters into g_prof: 0 MMA wait b_full, 1 MMA wait t_empty,
+// 2 MMA loop total, 3 epilogue wait t_full, 4 epilogue load+release,
+// 5 epilogue compute, 6 producer wait b_empty, 7 tiles (MMA warp);
+// 4 covers load + release + compute of the tile, 5 the bookkeeping after it.
+// Counters live in registers (prof[8] per thread) and are flushed once per
+// warp at the end, so the instrumentation barely perturbs the timing.
+#ifdef RSR_FP4_PROF
+__device__ unsigned long long g_prof[8];
+#define PROF_DECL unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define PROF_T(x) const long long x = clock64()
+#define PROF_ADD(i, v) (prof[i] += (unsigned long long)(v))
+#define PROF_FLUSH                                                   \
+  if ((threadIdx.x & 31) == 0)                                       \
+    for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_prof[i_], prof[i_])
+#else
+#define PROF_DECL
+#define PROF_T(x)
+#define PROF_ADD(i, v)
+#define PROF_FLUSH
+#endif
 
 struct Fp4Params {
   int64_t S;
@@ -57,12 +99,9 @@ struct Fp4Params {
   int64_t* first_upper;
   int64_t first_base_lower;
   int64_t first_base_upper;
+  int64_t n_lower;  // reference rows of this launch per side (columns beyond are masked)
+  int64_t n_upper;
 };
-
-__device__ __forceinline__ int tile_rot(int j, int rot, int nt) {
-  const int t = j + rot;
-  return t >= nt ? t - nt : t;
-}
 
 // SW32 K-major descriptor: 8-row core groups 256 B apart, version 1, layout 6.
 __device__ __forceinline__ uint32_t desc32_lo(uint32_t saddr) {
@@ -113,8 +152,71 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
                  "=r"(v[6]), "=r"(v[7])                                                         \
                : "r"(addr))
 
+#define RSR_LD4(addr, v)                                                                    \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"                 \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])                             \
+               : "r"(addr))
+
+// Load HN consecutive accumulator columns of this warp's 32 lanes.
+template <int HN>
+__device__ __forceinline__ void ld_cols(uint32_t taddr, uint32_t* v) {
+  constexpr int n32 = HN / 32, r16 = (HN % 32) / 16, r8 = (HN % 16) / 8, r4 = (HN % 8) / 4;
+  constexpr int o16 = 32 * n32, o8 = o16 + 16 * r16, o4 = o8 + 8 * r8;
+#pragma unroll
+  for (int i = 0; i < n32; ++i) RSR_LD32(taddr + 32 * i, (v + 32 * i));
+  if constexpr (r16 != 0) RSR_LD16(taddr + o16, (v + o16));
+  if constexpr (r8 != 0) RSR_LD8(taddr + o8, (v + o8));
+  if constexpr (r4 != 0) RSR_LD4(taddr + o4, (v + o4));
+  static_assert(HN % 4 == 0, "HN must be a multiple of 4");
+}
+
+// Epilogue of one tile for one warp: load its kCols accumulator columns
+// (column c of the MMA is reference c of the tile: CTA c / kHalfRows's B row
+// c % kHalfRows), release the buffer (as early as possible: the MMA warp waits on
+// it), then min-reduce, mask columns past the side's last reference and find
+// the first zero column.  c0 = this warp's first column.
 template <bool FIRST>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+__device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_bar, int lane,
+                                              int c0, int64_t valid, bool& any, int& zref,
+                                              long long& t_loaded) {
+  uint32_t v[kCols];
+  ld_cols<kCols>(taddr, v);
+  tmem_ld_wait();
+#ifdef RSR_FP4_PROF
+  t_loaded = clock64();
+#endif
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive_leader(release_bar);
+  if (valid < c0 + kCols) {
+#pragma unroll
+    for (int c = 0; c < kCols; ++c)
+      if (c0 + c >= valid) v[c] = 0xFFFFFFFFu;
+  }
+  // independent 3-input min chains (one chain is latency bound), then a tree
+  constexpr int W = 4;
+  uint32_t m[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) m[q] = v[q];
+#pragma unroll
+  for (int c = W; c + 2 * W <= kCols; c += 2 * W)
+#pragma unroll
+    for (int q = 0; q < W; ++q) m[q] = min(m[q], min(v[c + q], v[c + W + q]));
+#pragma unroll
+  for (int c = W + (kCols - W) / (2 * W) * (2 * W); c < kCols; ++c) m[c % W] = min(m[c % W], v[c]);
+  const uint32_t mn = min(min(m[0], m[1]), min(m[2], m[3]));
+  any = mn == 0;
+  if (FIRST && any) {
+    int zc = kCols - 1;
+#pragma unroll
+    for (int c = kCols - 1; c >= 0; --c)
+      if (v[c] == 0) zc = c;
+    zref = c0 + zc;
+  }
+}
+
+template <bool FIRST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_lower,
                          const __grid_constant__ CUtensorMap map_upper, const Fp4Params p) {
@@ -130,9 +232,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   uint64_t* b_empty = bars + p.stages;
   uint64_t* a_full = bars + 2 * p.stages;  // [2]
   uint64_t* a_empty = a_full + 2;          // [2]
-  uint64_t* t_full = a_full + 4;           // [2]
-  uint64_t* t_empty = a_full + 6;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 8);
+  uint64_t* t_full = a_full + 4;           // [kBufs]
+  uint64_t* t_empty = a_full + 8;          // [kBufs]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 12);
+  uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 14);  // [kColGroups][128] hit bits
+  int64_t* xfirst = reinterpret_cast<int64_t*>(xchg + kColGroups * 128) - 256;  // [1..][2][128]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -152,8 +256,10 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_addr(&a_full[i]), 2);
       mbar_init(smem_addr(&a_empty[i]), 1);
+    }
+    for (int i = 0; i < kBufs; ++i) {
       mbar_init(smem_addr(&t_full[i]), 1);
-      mbar_init(smem_addr(&t_empty[i]), 16);
+      mbar_init(smem_addr(&t_empty[i]), 2 * kEpiWarps);  // every epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -180,6 +286,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   cluster_sync_all();
   tc_fence_after();
   const int rot = (int)(((int64_t)cluster * p.nt_total) / n_clusters);
+  PROF_DECL;
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer (both CTAs)
@@ -201,12 +308,16 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                          g * 2 * kRowsA + (int)rank * kRowsA, 0);
       }
       __syncwarp();
+      int j = rot;
       for (int jj = 0; jj < p.nt_total; ++jj) {
-        const int j = tile_rot(jj, rot, p.nt_total);
         const bool low = j < p.nt_lower;
         const CUtensorMap* map = low ? &map_lower : &map_upper;
-        const int y = (low ? j : j - p.nt_lower) * kTileN4 + (int)rank * kHalfN;
+        const int y = (low ? j : j - p.nt_lower) * kTileN + (int)rank * kHalfRows;
+        if (++j == p.nt_total) j = 0;
+        PROF_T(q0);
         mbar_wait(bar_b_empty + 8 * stage, phase ^ 1);
+        PROF_T(q1);
+        PROF_ADD(6, q1 - q0);
         if (elect_one()) {
           if (leader)
             mbar_expect_tx(bar_b_full + 8 * stage, 2 * b_stage_bytes);
@@ -225,105 +336,126 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer (leader only)
     if (leader) {
-      constexpr uint32_t idesc = mxf4_idesc(2 * kRowsA, kTileN4);
+      constexpr uint32_t idesc = mxf4_idesc(2 * kRowsA, kTileN);
       const uint32_t tm0 = __shfl_sync(0xffffffffu, tmem_base, 0);
       const uint32_t sfa = tm0 + kSfaCol, sfb = tm0 + kSfbCol;
       const uint32_t a_lo0 = desc32_lo(smem_addr(sA)), b_lo0 = desc32_lo(smem_addr(sB));
       const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
+      const uint32_t bar_t_full = smem_addr(t_full), bar_t_empty = smem_addr(t_empty);
+      constexpr uint32_t kAstep = kChunkA >> 4, kBstep = kChunkB >> 4;
       const int cq = p.cq;
       int stage = 0, gi = 0;
-      uint32_t phase = 0, tc = 0;
+      uint32_t phase = 0, buf = 0, tphase = 0;
       for (int g = cluster; g < p.n_groups; g += n_clusters, ++gi) {
         const int ab = gi % p.a_bufs;
         mbar_wait(smem_addr(&a_full[ab]), (uint32_t)(gi / p.a_bufs) & 1);
         tc_fence_after();
         const uint32_t a_up = a_lo0 + (uint32_t)ab * (a_buf_bytes >> 4);
-        const uint32_t a_dn = a_up + (uint32_t)cq * (kChunkA >> 4);
-        for (int jj = 0; jj < p.nt_total; ++jj, ++tc) {
-          const int j = tile_rot(jj, rot, p.nt_total);
+        const uint32_t a_dn = a_up + (uint32_t)cq * kAstep;
+        PROF_T(l0);
+        // lean per-tile bookkeeping: this warp's instruction count per tile is
+        // on the critical path once a tile is only a few hundred MMA cycles
+        int j = rot;
+        for (int jj = 0; jj < p.nt_total; ++jj) {
           const uint32_t al = j < p.nt_lower ? a_dn : a_up;
-          const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
-          mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
-          tc_fence_after();
-          const uint32_t d = tm0 + buf * kTileN4;
-          mbar_wait(bar_b_full + 8 * stage, phase);
-          tc_fence_after();
+          if (++j == p.nt_total) j = 0;
+          const uint32_t d = tm0 + buf * kTileN;
           const uint32_t bl = b_lo0 + (uint32_t)stage * (b_stage_bytes >> 4);
+          PROF_T(m0);
+          mbar_wait(bar_t_empty + 8 * buf, tphase ^ 1);
+          PROF_T(m1);
+          mbar_wait(bar_b_full + 8 * stage, phase);
+          PROF_T(m2);
+          PROF_ADD(1, m1 - m0);
+          PROF_ADD(0, m2 - m1);
+          PROF_ADD(7, 1);
+          tc_fence_after();
           if (elect_one()) {
             for (int ks = 0; ks < cq; ++ks)
-              umma_mxf4_pair(d, al + ks * (kChunkA >> 4), bl + ks * (kChunkB >> 4), idesc, sfa,
-                             sfb, ks != 0);
+              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
+            umma_commit_pair(bar_t_full + 8 * buf);
             umma_commit_pair(bar_b_empty + 8 * stage);
-            umma_commit_pair(smem_addr(&t_full[buf]));
           }
           __syncwarp();
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
           }
+          if (++buf == kBufs) {
+            buf = 0;
+            tphase ^= 1;
+          }
         }
+        PROF_T(l1);
+        PROF_ADD(2, l1 - l0);
         if (elect_one()) umma_commit_pair(smem_addr(&a_empty[ab]));
         __syncwarp();
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------ epilogue (both CTAs)
-    const int quad = warp & 3;
-    const int colhalf = (warp - 4) >> 2;
-    uint32_t tc = 0;
+    const int quad = warp & 3;            // TMEM lane quarter (hardware: warp id % 4)
+    const int cg = (warp - 4) >> 2;       // column group
+    const int c0 = cg * kCols;
+    uint32_t buf = 0, tphase = 0;
     for (int g = cluster; g < p.n_groups; g += n_clusters) {
       uint32_t hit = 0;
       int64_t first[2] = {INT64_MAX, INT64_MAX};
-      for (int jj = 0; jj < p.nt_total; ++jj, ++tc) {
-        const int j = tile_rot(jj, rot, p.nt_total);
-        const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
+      int j = rot;
+      for (int jj = 0; jj < p.nt_total; ++jj) {
+        const bool low = j < p.nt_lower;
+        const int64_t t0 = (int64_t)(low ? j : j - p.nt_lower) * kTileN;
+        if (++j == p.nt_total) j = 0;
+        PROF_T(e0);
         mbar_wait(smem_addr(&t_full[buf]), tphase);
+        PROF_T(e1);
         tc_fence_after();
-        const uint32_t taddr =
-            tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN4 + colhalf * kHalfN;
-        uint32_t v[kHalfN];
-        RSR_LD32(taddr, v);
-        RSR_LD32(taddr + 32, (v + 32));
-        RSR_LD32(taddr + 64, (v + 64));
-        RSR_LD16(taddr + 96, (v + 96));
-        RSR_LD8(taddr + 112, (v + 112));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_leader(smem_addr(&t_empty[buf]));
-        uint32_t mn = 0xFFFFFFFFu;
-#pragma unroll
-        for (int i = 0; i < kHalfN; ++i) mn = min(mn, v[i]);
-        if (mn == 0) {
-          const bool low = j < p.nt_lower;
+        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN + c0;
+        const int64_t valid = (low ? p.n_lower : p.n_upper) - t0;
+        bool any;
+        int zref = 0;
+        long long t_loaded = 0;
+        epilogue_tile<FIRST>(taddr, smem_addr(&t_empty[buf]), lane, c0, valid, any, zref,
+                             t_loaded);
+        PROF_T(e2);
+        PROF_ADD(0, t_loaded - e1);
+        if (any) {
           hit |= low ? RSR_HIT_LOWER : RSR_HIT_UPPER;
           if (FIRST) {
-            int zc = 0;
-#pragma unroll
-            for (int i = kHalfN - 1; i >= 0; --i)
-              if (v[i] == 0) zc = i;
-            const int64_t ref = (low ? p.first_base_lower + (int64_t)j * kTileN4
-                                     : p.first_base_upper + (int64_t)(j - p.nt_lower) * kTileN4) +
-                                colhalf * kHalfN + zc;
+            const int64_t ref = (low ? p.first_base_lower : p.first_base_upper) + t0 + zref;
             first[low ? 0 : 1] = min(first[low ? 0 : 1], ref);
           }
         }
+        if (++buf == kBufs) {
+          buf = 0;
+          tphase ^= 1;
+        }
+        PROF_T(e3);
+        PROF_ADD(3, e1 - e0);
+        PROF_ADD(4, e2 - e1);
+        PROF_ADD(5, e3 - e2);
       }
-      // the two column halves of a row live in two warps: combine through shared memory
+      // the column groups of a row live in kColGroups warps: combine through shared memory
       const int64_t row = (int64_t)g * 2 * kRowsA + rank * kRowsA + quad * 32 + lane;
-      uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 10);  // [128]
-      int64_t* xfirst = reinterpret_cast<int64_t*>(xchg + 128);   // [2][128] (FIRST)
-      named_bar_sync(1, 256);
-      if (colhalf == 1) {
-        xchg[quad * 32 + lane] = hit;
+      const int r = quad * 32 + lane;
+      named_bar_sync(1, 32 * kEpiWarps);
+      if (cg != 0) {
+        xchg[cg * 128 + r] = hit;
         if (FIRST) {
-          xfirst[quad * 32 + lane] = first[0];
-          xfirst[128 + quad * 32 + lane] = first[1];
+          xfirst[(cg * 2 + 0) * 128 + r] = first[0];
+          xfirst[(cg * 2 + 1) * 128 + r] = first[1];
         }
       }
-      named_bar_sync(1, 256);
-      if (colhalf == 0) {
-        hit |= xchg[quad * 32 + lane];
+      named_bar_sync(1, 32 * kEpiWarps);
+      if (cg == 0) {
+#pragma unroll
+        for (int q = 1; q < kColGroups; ++q) {
+          hit |= xchg[q * 128 + r];
+          if (FIRST) {
+            first[0] = min(first[0], xfirst[(q * 2 + 0) * 128 + r]);
+            first[1] = min(first[1], xfirst[(q * 2 + 1) * 128 + r]);
+          }
+        }
         if (row < p.S) {
           const uint8_t prev = p.accumulate ? p.flags[row] : 0;
           p.flags[row] = (uint8_t)(prev | hit);
@@ -332,8 +464,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             for (int sd = 0; sd < 2; ++sd) {
               int64_t* out = sd ? p.first_upper : p.first_lower;
               if (!out) continue;
-              const int64_t f = min(first[sd], xfirst[sd * 128 + quad * 32 + lane]);
-              const int64_t mine = f == INT64_MAX ? -1 : f;
+              const int64_t mine = first[sd] == INT64_MAX ? -1 : first[sd];
               const int64_t old = p.accumulate ? out[row] : -1;  // earlier chunks win
               out[row] = old >= 0 ? old : mine;
             }
@@ -343,6 +474,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     }
   }
 
+  PROF_FLUSH;
   tc_fence_before();
   cluster_sync_all();
   if (warp == 2) {
@@ -389,7 +521,8 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   cudaStream_t st = rsr::as_stream(stream);
   if (S == 0) return RSR_OK;
   RSR_REQUIRE(flags != nullptr && A != nullptr, "rsr_classify_fp4: null pointer");
-  const int64_t nt_l = rsr::ceil_div(n_lower, kTileN4), nt_u = rsr::ceil_div(n_upper, kTileN4);
+  constexpr int TN = kTileN;
+  const int64_t nt_l = rsr::ceil_div(n_lower, TN), nt_u = rsr::ceil_div(n_upper, TN);
   if (nt_l + nt_u == 0) {
     if (!accumulate) {
       clear_flags4_kernel<<<(unsigned)rsr::ceil_div(S, 256), 256, 0, st>>>(flags, S);
@@ -419,13 +552,14 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   p.first_lower = first_lower;
   p.first_upper = first_upper;
   const size_t max_smem = 227 * 1024;
-  const size_t fixed = 1024 + 1024 + (want_first ? 2048 : 0);  // align slack, barriers, exchange
-  const size_t a_buf = (size_t)2 * cq * kChunkA, b_stage = (size_t)cq * kChunkB;
+  // align slack, barriers + hit exchange, first-match exchange
+  const size_t fixed = 1024 + 256 + kColGroups * 512 + (want_first ? (kColGroups - 1) * 2048 : 0);
+  const size_t a_buf = (size_t)2 * cq * kChunkA, b_stage = (size_t)cq * (TN / 2) * kChunk;
   p.a_bufs = 2;
   const char* ab_env = getenv("RSR_TC_ABUFS");
   if ((ab_env && atoi(ab_env) == 1) || fixed + 2 * a_buf + 4 * b_stage > max_smem) p.a_bufs = 1;
   int stages = (int)((max_smem - fixed - p.a_bufs * a_buf) / b_stage);
-  if (stages > 12) stages = 12;
+  if (stages > 16) stages = 16;
   RSR_REQUIRE(stages >= 2, "rsr_classify_fp4: row_bytes too large for shared memory");
   p.stages = stages;
   const size_t smem = fixed + p.a_bufs * a_buf + (size_t)stages * b_stage;
@@ -436,9 +570,9 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   if (p.n_groups < clusters) clusters = p.n_groups;
 
   // Reference chunks: a launch's B slice must stay L2-resident while every
-  // group streams it (512 tiles = 122,880 refs x row_bytes: 20 MB at 160 B).
+  // group streams it (~123K refs x row_bytes per launch: 20 MB at 160 B).
   const char* ct = getenv("RSR_TC_CHUNK_TILES");
-  const int64_t chunk = ct ? atoll(ct) : 512;
+  const int64_t chunk = ct ? atoll(ct) : 122880 / TN;
   const int64_t total = nt_l + nt_u;
   for (int64_t c0 = 0; c0 < total; c0 += chunk) {
     const int64_t c1 = c0 + chunk < total ? c0 + chunk : total;
@@ -448,16 +582,19 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
     q.nt_lower = (int)(l1 - l0);
     q.nt_total = (int)((l1 - l0) + (u1 - u0));
     q.accumulate = c0 == 0 ? accumulate : 1;
-    q.first_base_lower = l0 * kTileN4;
-    q.first_base_upper = u0 * kTileN4;
-    const uint8_t* lb = l1 > l0 ? B_lower + l0 * kTileN4 * (int64_t)row_bytes : nullptr;
-    const uint8_t* ub = u1 > u0 ? B_upper + u0 * kTileN4 * (int64_t)row_bytes : nullptr;
+    q.first_base_lower = l0 * TN;
+    q.first_base_upper = u0 * TN;
+    // reference rows of this launch (the last tile of a side may be partial)
+    q.n_lower = l1 > l0 ? (n_lower < l1 * TN ? n_lower : l1 * TN) - l0 * TN : 0;
+    q.n_upper = u1 > u0 ? (n_upper < u1 * TN ? n_upper : u1 * TN) - u0 * TN : 0;
+    const uint8_t* lb = l1 > l0 ? B_lower + l0 * TN * (int64_t)row_bytes : nullptr;
+    const uint8_t* ub = u1 > u0 ? B_upper + u0 * TN * (int64_t)row_bytes : nullptr;
     CUtensorMap cl, cu;
-    rc = make_map3(&cl, lb ? lb : ub, (lb ? l1 - l0 : u1 - u0) * kTileN4, row_bytes, cq, kHalfN);
+    rc = make_map3(&cl, lb ? lb : ub, lb ? q.n_lower : q.n_upper, row_bytes, cq, TN / 2);
     if (rc) return rc;
-    rc = make_map3(&cu, ub ? ub : lb, (ub ? u1 - u0 : l1 - l0) * kTileN4, row_bytes, cq, kHalfN);
+    rc = make_map3(&cu, ub ? ub : lb, ub ? q.n_upper : q.n_lower, row_bytes, cq, TN / 2);
     if (rc) return rc;
-    kern<<<2 * clusters, 384, smem, st>>>(ma, cl, cu, q);
+    kern<<<2 * clusters, kThreads, smem, st>>>(ma, cl, cu, q);
     rc = rsr::check_launch("classify_fp4_pair_kernel");
     if (rc) return rc;
   }
@@ -531,6 +668,17 @@ __global__ void encode_refs_fp4_kernel(const uint8_t* __restrict__ states, int64
 }
 
 }  // namespace
+
+#ifdef RSR_FP4_PROF
+extern "C" int rsr_fp4_prof(unsigned long long* host8, int reset) {
+  RSR_CUDA(cudaMemcpyFromSymbol(host8, g_prof, sizeof(g_prof)));
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    RSR_CUDA(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
+  }
+  return RSR_OK;
+}
+#endif
 
 extern "C" int rsr_fp4_row_bytes(int n_components, int n_states) {
   if (n_components < 1 || n_states < 2) return 0;

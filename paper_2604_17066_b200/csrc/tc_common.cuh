@@ -26,24 +26,31 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// Wait for the phase of parity `parity` to complete.  A wait that exceeds
-// ~2^34 cycles (several seconds) can only be a protocol bug: trap so the
-// launch fails loudly instead of hanging the device.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  long long t0 = 0;
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
+// Slow path of mbar_wait, out of line so the hot loops keep a two-instruction
+// fast path.  A wait that exceeds ~2^34 cycles (several seconds) can only be a
+// protocol bug: trap so the launch fails loudly instead of hanging the device.
+__device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
+  const long long t0 = clock64();
   int spins = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    if (!done && ++spins == 64) t0 = clock64();
-    if (!done && spins > 64 && (spins & 1023) == 0 && clock64() - t0 > (1ll << 34)) __trap();
-  } while (!done);
+  while (!mbar_try(bar, parity))
+    if ((++spins & 1023) == 0 && clock64() - t0 > (1ll << 34)) __trap();
+}
+
+// Wait for the phase of parity `parity` to complete.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (!mbar_try(bar, parity)) mbar_wait_slow(bar, parity);
 }
 
 // Remote (or local) arrive on the pair leader's copy of a barrier: clearing

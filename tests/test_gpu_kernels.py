@@ -215,7 +215,7 @@ def test_reference_chunked_launches(chunk_tiles, monkeypatch):
     assert np.array_equal(_classify_fp4(samples, lower, upper, n, m), _want_flags(samples, lower, upper, m))
 
 
-@pytest.mark.parametrize("n,m", [(295, 2), (295, 3), (440, 2), (120, 4), (895, 2)])
+@pytest.mark.parametrize("n,m", [(295, 2), (295, 3), (440, 2), (120, 4), (831, 2)])
 def test_fp4_first_match_and_widths(n, m):
     # every supported row width class (cq = 1 .. 14 chunks), first-match indices vs oracle
     rng = np.random.default_rng(n * 7 + m)

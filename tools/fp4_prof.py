@@ -1,0 +1,41 @@
+"""Per-role cycle counters of the FP4 classifier (instrumented build, timing
+experiments only): make -C paper_2604_17066_b200/csrc prof, then
+    RSR_LIB_OVERRIDE=tools/librsr_prof.so python tools/fp4_prof.py
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_17066_b200 as P  # noqa: E402
+from paper_2604_17066_b200 import _abi, workloads as W  # noqa: E402
+from paper_2604_17066_b200.classify import classify_flags  # noqa: E402
+
+lib = _abi.lib()
+fn = lib.rsr_fp4_prof
+fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+buf = (ctypes.c_ulonglong * 8)()
+lower, upper = W.cfg2_refs(0, 295, 10_000, 10_000)
+lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
+up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
+batch = P.sample_batch(P.ComponentDistribution.iid(295, [0.1, 0.9]), 1 << 20, seed=0)
+for it in range(3):
+    fn(buf, 1)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    classify_flags(batch, lo, up, 2)
+    e.record()
+    torch.cuda.synchronize()
+    fn(buf, 0)
+v = list(buf)
+tiles = v[7]
+print(f"kernel+encode {s.elapsed_time(e):.3f} ms; tiles (MMA warp) {tiles}")
+names = ["b_full (MMA) / tmem load (epi)", "mma wait t_empty", "mma loop total", "epi wait t_full",
+         "epi load+rel+min", "epi bookkeeping", "prod wait b_empty"]
+E = int(os.environ.get("EPI_WARPS", "16")) * 2  # epilogue warps per tile (both CTAs)
+per = [tiles + E * tiles, tiles, tiles, E * tiles, E * tiles, E * tiles, 2 * tiles]
+for n, x, d in zip(names, v, per):
+    print(f"{n:20s} {x / max(d, 1):8.1f} cycles per tile (per warp)")

@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(128, 1) check_kernel(const uint8_t* img, int i
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
 }
 
-template <int N>
+__device__ __forceinline__ uint64_t desc32(uint32_t s);
+template <int N, bool SW32>
 __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long long* cyc) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = sm + ((1024 - (sa(sm) & 1023)) & 1023);
@@ -139,7 +140,8 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long l
       const uint32_t d = tm + (uint32_t)((i & 1) * 240);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint64_t a = desc(A + k * 32), b = desc(B + k * 32);
+        const uint64_t a = SW32 ? desc32(A + k * 4096) : desc(A + k * 32),
+                       b = SW32 ? desc32(B + k * 8192) : desc(B + k * 32);
         asm volatile(
             "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
             "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(d),
@@ -358,19 +360,19 @@ int check_tma() {
   return bad;
 }
 
-template <int N>
+template <int N, bool SW32 = false>
 void rate(int sms) {
   const int iters = 20000;
   unsigned long long* d;
   cudaMalloc(&d, sms * 8);
-  const int smem = 16384 + 256 * 128 + 1024;
-  cudaFuncSetAttribute(rate_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  rate_kernel<N><<<sms, 128, smem>>>(100, d);
+  const int smem = 4 * 8192 + 4 * 8192 + 1024;
+  cudaFuncSetAttribute(rate_kernel<N, SW32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  rate_kernel<N, SW32><<<sms, 128, smem>>>(100, d);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  rate_kernel<N><<<sms, 128, smem>>>(iters, d);
+  rate_kernel<N, SW32><<<sms, 128, smem>>>(iters, d);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -379,8 +381,100 @@ void rate(int sms) {
   cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
   const double mmas = (double)iters * 4;
   const double ops = 2.0 * 128 * N * 64 * mmas * sms;
-  printf("rate mxf4 M=128 N=%d K=64: %.1f cycles/MMA (ideal %d at 2x int8), %.0f TOPS, %s\n", N, c / mmas,
+  printf("rate mxf4 %s M=128 N=%d K=64: %.1f cycles/MMA (ideal %d at 2x int8), %.0f TOPS, %s\n", SW32 ? "SW32" : "SW128", N, c / mmas,
          128 * N * 64 / 16384, ops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
+// ---- 4. CTA-pair issue rate: leader issues M=256 N x K=64 (cta_group::2) MMAs,
+// `per_commit` per commit (multicast to both CTAs' barrier), two accumulators.
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+pair_rate_kernel(int iters, int per_commit, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* base = sm + ((1024 - (sa(sm) & 1023)) & 1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sa(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = slot;
+  fill_scales(tm, 480);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0 && rank == 0) {
+    const uint32_t A = sa(base), B = A + 5 * 4096;
+    long long t0 = clock64();
+    int n = 0;
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t d = tm + (uint32_t)((i & 1) * 240);
+      for (int k = 0; k < 5; ++k) {
+        const uint64_t a = desc32(A + k * 4096), b = desc32(B + k * 4096);
+        asm volatile(
+            "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+            "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc_mxf4(256, N)), "r"(k), "r"(tm + 480), "r"(tm + 496));
+        if (++n == per_commit) {
+          n = 0;
+          asm volatile("{.reg .pred e; .reg .b16 m; mov.b16 m, 3; elect.sync _|e, 0xffffffff; @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;}" ::"r"(sa(&bar)));
+        }
+      }
+    }
+    asm volatile("{.reg .pred e; .reg .b16 m; mov.b16 m, 3; elect.sync _|e, 0xffffffff; @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;}" ::"r"(sa(&bar)));
+    // wait until the barrier has seen every commit: poll the phase count via try_wait on parity
+    long long t1;
+    {
+      // the last commit completes after all MMAs; spin on any phase flip after it
+      uint32_t ok = 0;
+      const int commits = (iters * 5) / per_commit + 1;
+      const uint32_t par = (commits - 1) & 1;
+      while (!ok)
+        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                     : "=r"(ok) : "r"(sa(&bar)), "r"(par));
+      t1 = clock64();
+    }
+    if (threadIdx.x == 0) cyc[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
+template <int N>
+void pair_rate(int sms, int per_commit) {
+  const int iters = 20000;
+  unsigned long long* d;
+  cudaMalloc(&d, sms * 8);
+  const int smem = 10 * 4096 + 1024;
+  cudaFuncSetAttribute(pair_rate_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  pair_rate_kernel<N><<<sms, 128, smem>>>(100, per_commit, d);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  pair_rate_kernel<N><<<sms, 128, smem>>>(iters, per_commit, d);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  unsigned long long c;
+  cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+  const double mmas = (double)iters * 5;
+  const double ops = 2.0 * 256 * N * 64 * mmas * (sms / 2);
+  printf("pair mxf4 M=256 N=%d K=64 commit/%d: %.1f cycles/MMA (ideal %d), %.0f TOPS, %s\n", N, per_commit,
+         c / mmas, 128 * N * 64 / 16384, ops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 
@@ -391,5 +485,11 @@ int main() {
   rate<256>(sms);
   rate<240>(sms);
   rate<224>(sms);
+  rate<240, true>(sms);
+  rate<256, true>(sms);
+  pair_rate<240>(sms, 1000000);
+  pair_rate<240>(sms, 5);
+  pair_rate<256>(sms, 5);
+  pair_rate<128>(sms, 5);
   return bad ? 1 : 0;
 }
