@@ -1,5 +1,6 @@
 // (2) Dominance classification on block-scaled FP4 tensor cores
-// (tcgen05.mma.cta_group::2.kind::mxf4, e2m1 operands, unit ue8m0 scales).
+// (tcgen05.mma.cta_group::2.kind::mxf4, e2m1 operands, ue8m0 scales chosen so
+// the fp32 accumulator's bit pattern is the integer violation count).
 //
 // Replaces the same reference code as classify_tc.cu -- classify.py:99-148
 // (_chunk_hits / _hits_for: any reference with popcount(sample & ~ref) == 0)
@@ -24,11 +25,12 @@
 //   * reference tiles of 240 rows (120 per CTA) stream through a ring of
 //     whole-tile stages; the leader issues cq MMAs M=256 N=240 K=64 per tile;
 //   * TMEM: accumulators at columns 0 and 240 (two buffers, the epilogue of
-//     tile j overlaps the MMAs of tile j+1), unit scale factors at 480..511;
-//   * 8 epilogue warps per CTA read the 128 x 240 fp32 accumulator
-//     (tcgen05.ld 32x32b), min-reduce the raw bits (all values are >= +0.0, so
-//     unsigned order = float order and 0 <=> hit), OR a hit bit per side, and
-//     optionally keep the first matching reference index (explain/strict).
+//     tile j overlaps the MMAs of tile j+1), scale factors at 480..511;
+//   * 8 epilogue warps per CTA read the 128 x 240 accumulator with packed
+//     16-bit loads (tcgen05.ld 32x32b .pack::16b: each accumulator is the
+//     denormal count * 2^-149, so its low 16 bits are the count), min-reduce
+//     with 16x2 SIMD mins, OR a hit bit per side, and optionally keep the
+//     first matching reference index (explain/strict).
 #include <stdlib.h>
 
 #include "tc_common.cuh"
@@ -39,16 +41,18 @@ constexpr int kRowsA = 128;      // sample rows per CTA
 constexpr int kChunk = 32;       // bytes per chunk = 64 e2m1 = one MMA K-step
 constexpr int kChunkA = kRowsA * kChunk;  // 4096 B
 constexpr uint32_t kSfaCol = 480, kSfbCol = 496;
+constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 
 // Reference tiles are 240 rows (120 per CTA).  TMEM holds two accumulator
 // buffers of 240 columns (0..479; 480..511 hold the scale factors), so the
 // epilogue of tile j overlaps the MMAs of tile j+1.  Reading a 128 x 240 fp32
-// accumulator out of TMEM is the epilogue's cost and it is latency bound per
-// warp (tools/tmem_bw.cu: 175 / 324 / 459 B/clk per SM with 4 / 8 / 16 reading
-// warps), so kEpiWarps warps (4 per TMEM lane quarter) each own 240 / (kEpiWarps
-// / 4) columns.
+// accumulator out of TMEM is the epilogue's cost (tools/tmem_bw.cu: 32x32b
+// loads reach 175 / 324 / 459 B/clk per SM with 4 / 8 / 16 warps, and twice that
+// with .pack::16b); kEpiWarps warps (kEpiWarps / 4 per TMEM lane quarter) each
+// own 240 / (kEpiWarps / 4) columns.  Measured on cfg2 (kernel ms): 4 warps
+// 1.70, 8 warps 1.67, 12 warps 1.67, 16 warps 1.76.
 #ifndef RSR_FP4_EPI_WARPS
-#define RSR_FP4_EPI_WARPS 16
+#define RSR_FP4_EPI_WARPS 8
 #endif
 #ifndef RSR_FP4_TILE_N
 #define RSR_FP4_TILE_N 240
@@ -152,35 +156,61 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
                  "=r"(v[6]), "=r"(v[7])                                                         \
                : "r"(addr))
 
-#define RSR_LD4(addr, v)                                                                    \
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"                 \
+// 32x32b loads with .pack::16b: register i holds the low 16 bits of columns
+// 2i (bits 0..15) and 2i+1 (bits 16..31), so one register covers two
+// accumulators and the TMEM -> register traffic halves (tools/tmem_bw.cu:
+// 905 vs 459 B/clk per SM with 16 warps).
+#define RSR_LDP16(addr, v)                                                                     \
+  asm volatile(                                                                                \
+      "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11," \
+      "%12,%13,%14,%15}, [%16];"                                                               \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),    \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),             \
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])                                                  \
+      : "r"(addr))
+#define RSR_LDP8(addr, v)                                                                       \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),        \
+                 "=r"(v[6]), "=r"(v[7])                                                         \
+               : "r"(addr))
+#define RSR_LDP4(addr, v)                                                                    \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.pack::16b.b32 {%0,%1,%2,%3}, [%4];"        \
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])                             \
                : "r"(addr))
+#define RSR_LDP2(addr, v)                                                                    \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.pack::16b.b32 {%0,%1}, [%2];"              \
+               : "=r"(v[0]), "=r"(v[1])                                                     \
+               : "r"(addr))
 
-// Load HN consecutive accumulator columns of this warp's 32 lanes.
+// Load HN consecutive accumulator columns (HN / 2 packed registers).
 template <int HN>
-__device__ __forceinline__ void ld_cols(uint32_t taddr, uint32_t* v) {
-  constexpr int n32 = HN / 32, r16 = (HN % 32) / 16, r8 = (HN % 16) / 8, r4 = (HN % 8) / 4;
-  constexpr int o16 = 32 * n32, o8 = o16 + 16 * r16, o4 = o8 + 8 * r8;
+__device__ __forceinline__ void ld_cols_packed(uint32_t taddr, uint32_t* v) {
+  constexpr int R = HN / 2;
+  constexpr int n16 = R / 16, r8 = (R % 16) / 8, r4 = (R % 8) / 4, r2 = (R % 4) / 2;
+  constexpr int o8 = 16 * n16, o4 = o8 + 8 * r8, o2 = o4 + 4 * r4;
 #pragma unroll
-  for (int i = 0; i < n32; ++i) RSR_LD32(taddr + 32 * i, (v + 32 * i));
-  if constexpr (r16 != 0) RSR_LD16(taddr + o16, (v + o16));
-  if constexpr (r8 != 0) RSR_LD8(taddr + o8, (v + o8));
-  if constexpr (r4 != 0) RSR_LD4(taddr + o4, (v + o4));
+  for (int i = 0; i < n16; ++i) RSR_LDP16(taddr + 32 * i, (v + 16 * i));
+  if constexpr (r8 != 0) RSR_LDP8(taddr + 2 * o8, (v + o8));
+  if constexpr (r4 != 0) RSR_LDP4(taddr + 2 * o4, (v + o4));
+  if constexpr (r2 != 0) RSR_LDP2(taddr + 2 * o2, (v + o2));
   static_assert(HN % 4 == 0, "HN must be a multiple of 4");
 }
 
-// Epilogue of one tile for one warp: load its kCols accumulator columns
-// (column c of the MMA is reference c of the tile: CTA c / kHalfRows's B row
-// c % kHalfRows), release the buffer (as early as possible: the MMA warp waits on
-// it), then min-reduce, mask columns past the side's last reference and find
-// the first zero column.  c0 = this warp's first column.
+// Epilogue of one tile for one warp.  The scale factors make every accumulator
+// an fp32 denormal whose bit pattern IS the violation count (count * 2^-149,
+// exact: tools/mxf4_check.cu), so the low 16 bits carry the whole count and the
+// packed load reads two columns per register.  Column c of the MMA is reference
+// c of the tile (CTA c / kHalfRows's B row c % kHalfRows); c0 = this warp's
+// first column.  Load, release the buffer (as early as possible: the MMA warp
+// waits on it), then mask columns past the side's last reference, min-reduce
+// the 16-bit halves and find the first zero column.
 template <bool FIRST>
 __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_bar, int lane,
                                               int c0, int64_t valid, bool& any, int& zref,
                                               long long& t_loaded) {
-  uint32_t v[kCols];
-  ld_cols<kCols>(taddr, v);
+  constexpr int R = kCols / 2;
+  uint32_t v[R];
+  ld_cols_packed<kCols>(taddr, v);
   tmem_ld_wait();
 #ifdef RSR_FP4_PROF
   t_loaded = clock64();
@@ -191,26 +221,23 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_b
   if (valid < c0 + kCols) {
 #pragma unroll
     for (int c = 0; c < kCols; ++c)
-      if (c0 + c >= valid) v[c] = 0xFFFFFFFFu;
+      if (c0 + c >= valid) v[c / 2] |= (c & 1) ? 0xFFFF0000u : 0x0000FFFFu;
   }
-  // independent 3-input min chains (one chain is latency bound), then a tree
-  constexpr int W = 4;
+  // independent SIMD (16x2) min chains, then a tree
+  constexpr int W = R >= 8 ? 4 : 2;
   uint32_t m[W];
 #pragma unroll
   for (int q = 0; q < W; ++q) m[q] = v[q];
 #pragma unroll
-  for (int c = W; c + 2 * W <= kCols; c += 2 * W)
+  for (int c = W; c < R; ++c) m[c % W] = __vminu2(m[c % W], v[c]);
 #pragma unroll
-    for (int q = 0; q < W; ++q) m[q] = min(m[q], min(v[c + q], v[c + W + q]));
-#pragma unroll
-  for (int c = W + (kCols - W) / (2 * W) * (2 * W); c < kCols; ++c) m[c % W] = min(m[c % W], v[c]);
-  const uint32_t mn = min(min(m[0], m[1]), min(m[2], m[3]));
-  any = mn == 0;
+  for (int q = 1; q < W; ++q) m[0] = __vminu2(m[0], m[q]);
+  any = (m[0] & 0xFFFFu) == 0 || (m[0] >> 16) == 0;
   if (FIRST && any) {
     int zc = kCols - 1;
 #pragma unroll
     for (int c = kCols - 1; c >= 0; --c)
-      if (v[c] == 0) zc = c;
+      if (((v[c / 2] >> (16 * (c & 1))) & 0xFFFFu) == 0) zc = c;
     zref = c0 + zc;
   }
 }
@@ -273,13 +300,17 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (warp >= 4 && warp < 8) {
-    // unit ue8m0 scale factors (0x7F = 2^0) for A and B in this CTA's TMEM
-    const uint32_t addr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + kSfaCol;
-    const uint32_t v = 0x7F7F7F7Fu;
+    // ue8m0 scale factors: A 2^-127 (0x00), B 2^-22 (0x69), so every product
+    // is 2^-149 and the fp32 accumulator's bits count the violations
+    const uint32_t addr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
     asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
-        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
-        "r"(v));
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1};" ::"r"(addr + kSfaCol),
+        "r"(kSfaByte * 0x01010101u));
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1};" ::"r"(addr + kSfbCol),
+        "r"(kSfbByte * 0x01010101u));
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   tc_fence_before();

@@ -44,14 +44,21 @@ __device__ __forceinline__ void wait0(uint32_t b, uint32_t par) {
 }
 
 // Fill TMEM columns [col0, col0+32) of all 128 lanes with unit ue8m0 scales.
-__device__ __forceinline__ void fill_scales(uint32_t tm, int col0) {
+__device__ __forceinline__ void fill_scales(uint32_t tm, int col0, uint32_t va = 0x7F7F7F7Fu,
+                                            uint32_t vb = 0x7F7F7F7Fu) {
   const int warp = threadIdx.x / 32;
-  const uint32_t v = 0x7F7F7F7Fu;
-  const uint32_t addr = tm + ((uint32_t)(warp * 32) << 16) + col0;
+  const uint32_t v = va;
+  uint32_t addr = tm + ((uint32_t)(warp * 32) << 16) + col0;
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
       "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
       "r"(v));
+  if (vb != va) {  // second 16 columns (SFB at col0 + 16) get vb
+    addr += 16;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
+        "r"(vb));
+  }
   asm volatile("tcgen05.wait::st.sync.aligned;");
 }
 
@@ -226,7 +233,8 @@ __device__ __forceinline__ uint64_t desc32(uint32_t s) {
 
 template <int NT>
 __global__ void __launch_bounds__(128, 1)
-check_tma_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, float* out) {
+check_tma_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, float* out,
+                 uint32_t sfa, uint32_t sfb) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = sm + ((1024 - (sa(sm) & 1023)) & 1023);
   __shared__ uint64_t bar, tbar;
@@ -236,6 +244,7 @@ check_tma_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&tbar)));
+    if (sfa == 0xFFFFFFFFu) return;  // never
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
@@ -246,7 +255,7 @@ check_tma_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm = slot;
-  fill_scales(tm, 480);
+  fill_scales(tm, 480, sfa, sfb);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -304,7 +313,7 @@ static int map3(CUtensorMap* m, void* base, int rows, int rowb, int box_rows) {
 }
 
 template <int NT>
-int check_tma() {
+int check_tma(uint32_t sfa = 0x7F7F7F7Fu, uint32_t sfb = 0x7F7F7F7Fu, bool denorm = false) {
   const int K = 320;  // 295 real + bias at 295 + zero pad
   static uint8_t a[128][K], b[NT][K];
   srand(11);
@@ -335,7 +344,7 @@ int check_tma() {
   if (map3(&ma, da, 128, 320, 128) || map3(&mb, db, NT, 160, NT)) return 1;
   const int smem = 10 * 128 * 32 + 5 * NT * 32 + 1024;
   cudaFuncSetAttribute(check_tma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  check_tma_kernel<NT><<<1, 128, smem>>>(ma, mb, dout);
+  check_tma_kernel<NT><<<1, 128, smem>>>(ma, mb, dout, sfa, sfb);
   cudaError_t e = cudaDeviceSynchronize();
   static float out[2 * 128 * NT];
   cudaMemcpy(out, dout, sizeof(out), cudaMemcpyDeviceToHost);
@@ -349,14 +358,16 @@ int check_tma() {
           s += av * b[n][k];
         }
         zeros += s == 0;
-        if (out[(side * 128 + r) * NT + n] != (float)s) {
+        uint32_t bits;
+        memcpy(&bits, &out[(side * 128 + r) * NT + n], 4);
+        if (denorm ? bits != (uint32_t)s : out[(side * 128 + r) * NT + n] != (float)s) {
           if (bad < 5) printf("  tma mismatch side=%d r=%d n=%d got %f want %d\n", side, r, n,
                               out[(side * 128 + r) * NT + n], s);
           ++bad;
         }
       }
-  printf("check TMA-SW32 N=%d: %s, %d mismatches of %d (exact zeros %d)\n", NT, cudaGetErrorString(e), bad,
-         2 * 128 * NT, zeros);
+  printf("check TMA-SW32 N=%d scales %08x/%08x%s: %s, %d mismatches of %d (exact zeros %d)\n", NT, sfa, sfb,
+         denorm ? " (denormal bits == count)" : "", cudaGetErrorString(e), bad, 2 * 128 * NT, zeros);
   return bad;
 }
 
@@ -482,14 +493,17 @@ int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int bad = check<256>() + check<240>() + check_tma<240>();
+  // D = count * 2^-127 * 2^-22 = count * 2^-149: fp32 denormal whose bits are the count
+  check_tma<240>(0x00000000u, 0x69696969u, true);
   rate<256>(sms);
   rate<240>(sms);
   rate<224>(sms);
   rate<240, true>(sms);
   rate<256, true>(sms);
-  pair_rate<240>(sms, 1000000);
   pair_rate<240>(sms, 5);
-  pair_rate<256>(sms, 5);
+  pair_rate<224>(sms, 5);
+  pair_rate<192>(sms, 5);
+  pair_rate<160>(sms, 5);
   pair_rate<128>(sms, 5);
   return bad ? 1 : 0;
 }

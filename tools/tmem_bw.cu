@@ -36,11 +36,13 @@ __global__ void tmem_read(int iters, unsigned long long* cyc, uint32_t* sink) {
   long long t0 = clock64();
   for (int i = 0; i < iters; ++i) {
     uint32_t v[32];
-    const uint32_t addr = tm + lane_base + ((col0 + (uint32_t)i * 64) & 255);
+    const uint32_t addr = tm + lane_base + ((col0 + (uint32_t)i * 128) & 255);
     if (SHAPE == 0) LD32("32x32b.x32", addr, v);
     if (SHAPE == 1) LD32("16x64b.x32", addr, v);
     if (SHAPE == 2) LD32("16x128b.x16", addr, v);
     if (SHAPE == 3) LD32("16x256b.x8", addr, v);
+    if (SHAPE == 4) LD32("32x32b.x32.pack::16b", addr, v);
+    if (SHAPE == 5) LD32("16x64b.x32.pack::16b", addr, v);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int k = 0; k < 32; ++k) acc ^= v[k];
@@ -66,7 +68,8 @@ void run(const char* name, int sms, int warps) {
   cudaDeviceSynchronize();
   unsigned long long c;
   cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
-  const double bytes = (double)iters * warps * 32 * 32 * 4;  // 32 regs x 4 B per thread
+  // 32 regs x 4 B per thread; pack::16b covers two 32-bit TMEM columns per register
+  const double bytes = (double)iters * warps * 32 * 32 * 4 * (SHAPE >= 4 ? 2 : 1);
   printf("%-12s warps=%2d: %.1f B/clk per SM (%s)\n", name, warps, bytes / c,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
@@ -81,6 +84,8 @@ int main() {
     run<1>("16x64b.x32", sms, w);
     run<2>("16x128b.x16", sms, w);
     run<3>("16x256b.x8", sms, w);
+    run<4>("32x32b.x64.p16", sms, w);
+    run<5>("16x64b.x64.p16", sms, w);
   }
   return 0;
 }
