@@ -25,6 +25,12 @@ int phi_bits_dispatch(const rsr_phi_desc& d, bool boundary, int threshold, const
                       const int64_t* idx, int64_t count, uint8_t* out, int64_t* count_leq,
                       uint8_t* out_side, int64_t* out_calls, cudaStream_t st);
 
+// csrc/boundary_graph.cu: boundary search by union-find / witness-path BFS for
+// s-t connectivity and widest-path Phi (returns -1 when not applicable).
+int boundary_graph_dispatch(const rsr_phi_desc& d, int threshold, const uint8_t* x0, int64_t B,
+                            uint8_t* out_refs, uint8_t* out_side, int64_t* out_calls,
+                            cudaStream_t st);
+
 // Thermometer geometry (see include/rsr_b200.h).
 inline int thermo_kdim(int n, int m) { return n * (m - 1); }
 inline int thermo_bias_cols(int n, int m) { return (thermo_kdim(n, m) + 126) / 127; }

@@ -383,6 +383,12 @@ extern "C" int rsr_boundary_search(const rsr_phi_desc* phi, int threshold, const
   if (rc) return rc;
   RSR_REQUIRE(B >= 0, "rsr_boundary_search: negative count");
   if (B == 0) return RSR_OK;
+  const char* graph_env = getenv("RSR_BOUNDARY_GRAPH");
+  if (!(graph_env && atoi(graph_env) == 0)) {
+    const int r = rsr::boundary_graph_dispatch(*phi, threshold, x0, B, out_refs, out_side,
+                                               out_calls, rsr::as_stream(stream));
+    if (r != -1) return r;
+  }
   const char* bits_env = getenv("RSR_PHI_BITS");
   if (!(bits_env && atoi(bits_env) == 0)) {
     const int r = rsr::phi_bits_dispatch(*phi, true, threshold, x0, nullptr, B, out_refs, nullptr,

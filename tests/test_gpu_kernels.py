@@ -293,11 +293,15 @@ def _nn_graph():
 
 
 # flags 0: edge-sweep label propagation (csrc/phi.cu); flags 1: bitset BFS (csrc/phi_bits.cu)
+# and, for boundary searches, union-find / witness-path search (csrc/boundary_graph.cu) unless
+# RSR_BOUNDARY_GRAPH=0
+@pytest.mark.parametrize("graph_search", ["1", "0"])
 @pytest.mark.parametrize("flags", [0, A.PHI_FLAG_SIMPLE])
 @pytest.mark.parametrize("graph", ["grid", "nn119"])
 @pytest.mark.parametrize("kind,m", [(A.PHI_ST, 2), (A.PHI_WIDEST, 3), (A.PHI_GLOBAL, 2),
-                                    (A.PHI_ST, 3)])
-def test_phi_eval_and_boundary(kind, m, graph, flags):
+                                    (A.PHI_ST, 3), (A.PHI_WIDEST, 4)])
+def test_phi_eval_and_boundary(kind, m, graph, flags, graph_search, monkeypatch):
+    monkeypatch.setenv("RSR_BOUNDARY_GRAPH", graph_search)
     if graph == "grid":
         nn, edges = _grid()
         s_node, t_node = 0, nn - 1

@@ -110,3 +110,39 @@ def test_sampling_random_tables_and_offsets():
         seed, gen = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**40))
         b = P.sample_batch(P.ComponentDistribution(probs), count, seed, gen, start)
         assert np.array_equal(b.states, oracle.sample_states(probs, count, seed, gen, start))
+
+
+@pytest.mark.parametrize("kind,m,p_hi", [("st", 2, 0.9), ("st", 2, 0.6), ("widest", 3, 0.8),
+                                         ("widest", 4, 0.7)])
+def test_boundary_graph_search_matches_bitset_walk(kind, m, p_hi, monkeypatch):
+    """Union-find / witness-path boundary search (csrc/boundary_graph.cu) against the
+    step-by-step bitset walk (csrc/phi_bits.cu) on 1024 random start vectors of the
+    cfg3-shaped graph: identical references, sides and Phi-call counts; the oracle
+    checks a slice."""
+    import torch
+    from paper_2604_17066_b200 import workloads as W
+    g = W.cfg3(0)
+    graph = P.Graph(g["n_nodes"], tuple(g["edges"]))
+    phi = (P.single_od_connectivity(graph, g["source"], g["target"]) if kind == "st"
+           else P.widest_path_level(graph, g["source"], g["target"]))
+    ms = 2 if kind == "st" else m
+    model = P.SystemModel(graph.n_edges, m, ms, phi)
+    rng = np.random.default_rng(int(p_hi * 100) + m)
+    lo = rng.random((1024, graph.n_edges))
+    xs = np.where(lo < p_hi, m - 1, rng.integers(0, m, size=lo.shape)).astype(np.uint8)
+    xd = torch.as_tensor(xs).cuda()
+    ref = (oracle.phi_st(g["n_nodes"], g["edges"], g["source"], g["target"]) if kind == "st"
+           else oracle.phi_widest(g["n_nodes"], g["edges"], g["source"], g["target"], m))
+    for thr in range(ms - 1):
+        out = {}
+        for mode in ("1", "0"):
+            monkeypatch.setenv("RSR_BOUNDARY_GRAPH", mode)
+            r, sd, c = P.boundary_search_batch(model, xd, thr)
+            out[mode] = (r.cpu().numpy(), sd.cpu().numpy(), c.cpu().numpy())
+        for a, b in zip(out["1"], out["0"]):
+            assert np.array_equal(a, b)
+        assert 0 < int((out["1"][1] == 0).sum()) < 1024 or kind == "widest"
+        for b in range(0, 1024, 97):
+            ev = oracle.CountingPhi(ref, graph.n_edges, m, ms)
+            vec, side = oracle.boundary_search(ev, xs[b].astype(np.int64), thr)
+            assert tuple(out["1"][0][b].tolist()) == vec and int(out["1"][2][b]) == ev.count
