@@ -104,6 +104,13 @@ int rsr_sample(const double* probs, int n_components, int n_states, uint64_t see
                uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
                int8_t* out_thermo, int ld_thermo, void* stream);
 
+/* Same draws, fused with the FP4 sample operand of rsr_classify_fp4 (default
+ * path): out_states u8 [count*N] (16-byte aligned) and/or out_fp4
+ * [count * 2*row_bytes] (row_bytes = rsr_fp4_row_bytes(N, M)); NULL skips. */
+int rsr_sample_fp4(const double* probs, int n_components, int n_states, uint64_t seed,
+                   uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+                   uint8_t* out_fp4, int row_bytes, void* stream);
+
 /* ---- (2) encodings: encoding.py:138-153 encode_batch ---------------------- */
 int rsr_encode_samples(const uint8_t* states, int64_t count, int n_components,
                        int n_states, int8_t* out, int ld, void* stream);

@@ -65,6 +65,7 @@ EXPORTED = {
     "rsr_philox_raw": (_I, [_U64, _U64, _I64, _I64, _P, _P]),
     "rsr_uniform_field": (_I, [_U64, _U64, _I64, _I64, _I, _P, _P]),
     "rsr_sample": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
+    "rsr_sample_fp4": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
     "rsr_encode_samples": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "rsr_encode_refs": (_I, [_P, _I64, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_encode_rows": (_I, [_P, _I64, _I, _I, _I, _P, _P]),

@@ -33,6 +33,7 @@
 //     first matching reference index (explain/strict).
 #include <stdlib.h>
 
+#include "fp4_encode.cuh"
 #include "tc_common.cuh"
 
 namespace {
@@ -635,39 +636,30 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
 // ---------------------------------------------------------------- encoders
 // Sample operand row i: [A_up (row_bytes) | A_lo (row_bytes)], element c in
 // byte c/2, low nibble for even c; e2m1 1.0 = 0x2.
-__global__ void encode_samples_fp4_kernel(const uint8_t* __restrict__ states, int64_t count,
-                                          int N, int M, uint8_t* __restrict__ out,
-                                          int row_bytes, int kdim) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= count * row_bytes) return;
-  const int64_t i = t / row_bytes;
-  const int b = (int)(t - i * row_bytes);
-  const uint8_t* x = states + i * N;
-  uint32_t up = 0, lo = 0;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int c = 2 * b + h;
-    uint32_t u, l;
-    if (c < kdim) {
-      int n, k;
-      if (M == 2) {
-        n = c;
-        k = 1;
-      } else {
-        n = c / (M - 1);
-        k = c - n * (M - 1) + 1;
-      }
-      u = x[n] < k;
-      l = 1 - u;
-    } else {
-      u = l = (c == kdim);
+// One warp per sample row: the row's states are staged in shared memory
+// (coalesced byte loads), then each lane builds whole 32-bit words (8 e2m1
+// elements) of A_up and A_lo and stores them.
+__global__ void __launch_bounds__(256) encode_samples_fp4_kernel(
+    const uint8_t* __restrict__ states, int64_t count, int N, int M, uint8_t* __restrict__ out,
+    int row_bytes, int kdim, int stage_bytes) {
+  extern __shared__ uint8_t stage[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* buf = stage + warp * stage_bytes;
+  const int words = row_bytes / 4;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < count; i += (int64_t)gridDim.x * 8) {
+    const uint8_t* x = states + i * N;
+    for (int n = lane; n < N; n += 32) buf[n] = x[n];
+    __syncwarp();
+    uint32_t* up_row = reinterpret_cast<uint32_t*>(out + i * (int64_t)(2 * row_bytes));
+    uint32_t* lo_row = up_row + words;
+    for (int w = lane; w < words; w += 32) {
+      uint32_t up, lo;
+      rsr::fp4_sample_word(buf, w, M, kdim, up, lo);
+      up_row[w] = up;
+      lo_row[w] = lo;
     }
-    up |= (u ? 0x2u : 0u) << (4 * h);
-    lo |= (l ? 0x2u : 0u) << (4 * h);
+    __syncwarp();
   }
-  uint8_t* row = out + i * (int64_t)(2 * row_bytes);
-  row[b] = (uint8_t)up;
-  row[row_bytes + b] = (uint8_t)lo;
 }
 
 // Reference operand rows: upper [r_n >= k], lower [r_n < k], bias column 0;
@@ -725,10 +717,15 @@ extern "C" int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int 
               rsr_fp4_row_bytes(N, M));
   if (count == 0) return RSR_OK;
   RSR_REQUIRE(states != nullptr && out != nullptr, "rsr_encode_samples_fp4: null pointer");
-  const int64_t total = count * row_bytes;
-  encode_samples_fp4_kernel<<<(unsigned)rsr::ceil_div(total, 256), 256, 0,
-                              rsr::as_stream(stream)>>>(states, count, N, M, out, row_bytes,
-                                                        N * (M - 1));
+  const int stage_bytes = (N + 15) / 16 * 16;
+  const size_t smem = 8 * (size_t)stage_bytes;
+  if (smem > 48 * 1024)
+    RSR_CUDA(cudaFuncSetAttribute(encode_samples_fp4_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t grid = rsr::ceil_div(count, 8);
+  if (grid > 148 * 64) grid = 148 * 64;
+  encode_samples_fp4_kernel<<<(unsigned)grid, 256, smem, rsr::as_stream(stream)>>>(
+      states, count, N, M, out, row_bytes, N * (M - 1), stage_bytes);
   return rsr::check_launch("encode_samples_fp4_kernel");
 }
 

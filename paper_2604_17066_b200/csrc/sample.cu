@@ -11,6 +11,7 @@
 // state = #{m < M-1 : r >= T_m} with T_m = ceil(cumsum(probs[n])[m] * 2^53).
 // The clip to M-1 (sampling.py:89) is implied by counting only m < M-1.
 #include "common.cuh"
+#include "fp4_encode.cuh"
 #include "philox.cuh"
 
 namespace {
@@ -110,6 +111,81 @@ sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uin
         }
         if (ns[j] == N - 1) thermo_tail(arow, kdim, nbias, ld);
       }
+    }
+  }
+}
+
+// Row-blocked sampler with the FP4 operand fused (the default path).  A CTA
+// owns kRowsPerCta whole rows: its threads compute every Philox block that
+// overlaps the rows' flat draw range (blocks straddling two CTAs are computed
+// by both, each keeping its own draws), drop the states into shared memory,
+// then write the uint8 state rows (16-byte stores: the chunk is 32-row
+// aligned) and the FP4 rows [A_up | A_lo] (whole 32-bit words) coalesced.
+constexpr int kRowsPerCta = 64;
+
+template <bool M2>
+__global__ void __launch_bounds__(kThreads)
+sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
+                   int64_t start_row, int64_t count, uint8_t* __restrict__ states,
+                   uint8_t* __restrict__ fp4, int row_bytes) {
+  extern __shared__ __align__(16) unsigned long long T[];
+  load_thresholds(probs, N, M, T);
+  // [rows][N] states, 16-byte aligned after the threshold table
+  uint8_t* st = reinterpret_cast<uint8_t*>(T) + ((size_t)N * (M - 1) * 8 + 15) / 16 * 16;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
+  const int rows = (int)(count - r0 < kRowsPerCta ? count - r0 : kRowsPerCta);
+  const int64_t span = (int64_t)rows * N;                       // draws of this CTA
+  const int64_t f0 = (start_row + r0) * (int64_t)N;              // first flat draw
+  const int64_t b0 = f0 >> 2, b1 = (f0 + span - 1) >> 2;         // Philox blocks
+  // local draw offset of word 0 of this thread's first block, and its column;
+  // each further block of the thread is 4 * blockDim.x draws later
+  int o0 = (int)(4 * (b0 + threadIdx.x) - f0);
+  int n0 = (o0 + N) % N;
+  const int ostep = 4 * (int)blockDim.x, nstep = ostep % N;
+  for (int64_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x, o0 += ostep) {
+    uint64_t w[4];
+    rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+    int n = n0;
+    n0 += nstep;
+    if (n0 >= N) n0 -= N;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int o = o0 + j;
+      if (o >= 0 && o < span) {
+        const unsigned long long r = w[j] >> 11;
+        int s;
+        if (M2) {
+          s = r >= T[n] ? 1 : 0;
+        } else {
+          s = 0;
+          const unsigned long long* Tn = T + n * (M - 1);
+          for (int m = 0; m < M - 1; ++m) s += (r >= Tn[m]) ? 1 : 0;
+        }
+        st[o] = (uint8_t)s;
+      }
+      if (++n == N) n = 0;
+    }
+  }
+  __syncthreads();
+  if (states) {
+    uint8_t* dst = states + r0 * (int64_t)N;
+    if (rows == kRowsPerCta) {  // 64 * N bytes, 16-byte aligned chunk
+      const int vecs = (int)(span / 16);
+      for (int i = threadIdx.x; i < vecs; i += blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(st)[i];
+    } else {
+      for (int64_t i = threadIdx.x; i < span; i += blockDim.x) dst[i] = st[i];
+    }
+  }
+  if (fp4) {
+    const int words = row_bytes / 4, kdim = N * (M - 1);
+    for (int i = threadIdx.x; i < rows * words; i += blockDim.x) {
+      const int r = i / words, w = i - r * words;
+      uint32_t up, lo;
+      rsr::fp4_sample_word(st + r * N, w, M, kdim, up, lo);
+      uint32_t* row = reinterpret_cast<uint32_t*>(fp4 + (r0 + r) * (int64_t)(2 * row_bytes));
+      row[w] = up;
+      row[words + w] = lo;
     }
   }
 }
@@ -330,4 +406,29 @@ extern "C" int rsr_encode_refs(const uint8_t* states, int64_t count, int64_t row
                                                  rsr::thermo_kdim(N, M),
                                                  rsr::thermo_bias_cols(N, M));
   return rsr::check_launch("encode_refs_kernel");
+}
+
+extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_states, uint64_t seed,
+                              uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+                              uint8_t* out_fp4, int row_bytes, void* stream) {
+  const int N = n_components, M = n_states;
+  RSR_REQUIRE(N >= 1 && M >= 2 && M <= 255, "rsr_sample_fp4: need N >= 1 and 2 <= M <= 255");
+  RSR_REQUIRE(start >= 0 && count >= 1, "rsr_sample_fp4: n_samples must be >= 1");
+  RSR_REQUIRE(probs != nullptr, "rsr_sample_fp4: null probs");
+  RSR_REQUIRE(out_states || out_fp4, "rsr_sample_fp4: no output requested");
+  if (out_fp4)
+    RSR_REQUIRE(row_bytes == rsr_fp4_row_bytes(N, M), "rsr_sample_fp4: row_bytes must be %d",
+                rsr_fp4_row_bytes(N, M));
+  if (out_states)
+    RSR_REQUIRE((reinterpret_cast<uintptr_t>(out_states) & 15) == 0,
+                "rsr_sample_fp4: out_states must be 16-byte aligned");
+  const size_t smem =
+      ((size_t)N * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 + (size_t)kRowsPerCta * N;
+  RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample_fp4: N*(M-1) too large for shared memory");
+  auto kern = M == 2 ? sample_rows_kernel<true> : sample_rows_kernel<false>;
+  if (smem > 48 * 1024)
+    RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)rsr::ceil_div(count, kRowsPerCta), kThreads, smem, rsr::as_stream(stream)>>>(
+      probs, N, M, seed, gen, start, count, out_states, out_fp4, row_bytes);
+  return rsr::check_launch("sample_rows_kernel");
 }

@@ -1,10 +1,11 @@
 """(1) Device-resident Monte Carlo batches (mirror of reference ``sampling.py``).
 
-``sample_batch`` runs ``rsr_sample``: numpy-compatible Philox4x64-10 keyed by
-(seed, generation_index), flat draw index (start+i)*N + n, inverse CDF on the
-cumulative probabilities (sampling.py:39-90), bit-exact with the reference.
-The kernel writes the uint8 state matrix and, fused, the int8 thermometer
-rows that feed the tensor-core classifier.  The batch stays in HBM; the
+``sample_batch`` runs ``rsr_sample_fp4``: numpy-compatible Philox4x64-10
+keyed by (seed, generation_index), flat draw index (start+i)*N + n, inverse
+CDF on the cumulative probabilities (sampling.py:39-90), bit-exact with the
+reference.  The kernel writes the uint8 state matrix and, fused, the FP4
+sample operand of the default classifier (``rsr_sample`` with the int8
+thermometer rows fused serves the int8 variant).  The batch stays in HBM; the
 host ``states`` array (int64, as in the reference) is materialised lazily.
 """
 
@@ -145,14 +146,16 @@ def uniform_field(seed: int, generation_index: int, start: int, count: int,
 
 def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
                  generation_index: int = 0, start: int = 0, *, encode: bool = False,
+                 fp4: bool | None = None,
                  out_states: torch.Tensor | None = None,
                  out_thermo: torch.Tensor | None = None,
                  out_fp4: torch.Tensor | None = None) -> SampleBatch:
     """Inverse-CDF draw on the counter-based stream (sampling.py:69-90), on device.
 
-    ``encode`` (or ``out_thermo``) also writes the int8 thermometer rows for
-    M = dist.n_states in the same kernel; ``out_fp4`` encodes the FP4 operand
-    of the default classifier into that buffer right after sampling.
+    By default (``fp4`` None -> on whenever the FP4 classifier handles the row
+    width) one kernel, ``rsr_sample_fp4``, writes the uint8 states and the FP4
+    sample operand of the default classifier.  ``encode`` (or ``out_thermo``)
+    instead runs ``rsr_sample`` with the int8 thermometer rows fused.
     ``out_*`` let callers reuse preallocated buffers.
     """
     if n_samples < 1:
@@ -161,12 +164,27 @@ def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
     dev = _device.device()
     states = out_states if out_states is not None else torch.empty(
         (n_samples, n), dtype=torch.uint8, device=dev)
+    mask = (1 << 64) - 1
+    int8_path = encode or out_thermo is not None
+    rb = _abi.fp4_row_bytes(n, m)
+    if fp4 is None:
+        fp4 = (not int8_path) and rb <= _abi.FP4_MAX_ROW_BYTES
+    if fp4 and not int8_path:
+        a4 = out_fp4[:n_samples] if out_fp4 is not None else torch.empty(
+            (n_samples, 2 * rb), dtype=torch.uint8, device=dev)
+        if a4.dtype != torch.uint8 or a4.shape != (n_samples, 2 * rb):
+            raise ValueError("fp4 buffer must be uint8 [>= H, 2 * row_bytes]")
+        _abi.call("rsr_sample_fp4", _abi.ptr(dist.device_probs()), n, m, seed & mask,
+                  generation_index & mask, start, n_samples, _abi.ptr(states), _abi.ptr(a4), rb,
+                  _device.stream())
+        batch = SampleBatch(states, seed, generation_index, state_bound=m)
+        batch._fp4[m] = a4
+        return batch
     thermo = None
     kpad = _abi.thermo_kpad(n, m)
-    if encode or out_thermo is not None:
+    if int8_path:
         thermo = out_thermo if out_thermo is not None else torch.empty(
             (n_samples, kpad), dtype=torch.int8, device=dev)
-    mask = (1 << 64) - 1
     _abi.call("rsr_sample", _abi.ptr(dist.device_probs()), n, m, seed & mask,
               generation_index & mask, start, n_samples, _abi.ptr(states), _abi.ptr(thermo),
               kpad, _device.stream())

@@ -49,6 +49,28 @@ def test_sample_states_and_thermo(n, m, count, start):
         assert np.array_equal(t[:, [j * (m - 1) + k - 1 for j in range(n)]], (want < k).astype(np.int64))
 
 
+@pytest.mark.parametrize("n,m,count,start", [(295, 2, 4099, 0), (40, 2, 1000, 3), (7, 3, 513, 11),
+                                             (5, 5, 300, 1), (295, 3, 129, 7), (64, 2, 64, 0),
+                                             (1, 2, 70, 5)])
+def test_sample_fp4_fused(n, m, count, start):
+    # row-blocked sampler: states identical to the oracle, FP4 rows identical to the encoder's
+    rng = np.random.default_rng(n * 17 + m)
+    raw = rng.random((n, m)) + 0.01
+    probs = raw / raw.sum(1, keepdims=True)
+    want = oracle.sample_states(probs, count, seed=99, generation_index=5, start=start)
+    rb = A.fp4_row_bytes(n, m)
+    st = torch.empty((count, n), dtype=torch.uint8, device="cuda")
+    a4 = torch.empty((count, 2 * rb), dtype=torch.uint8, device="cuda")
+    A.call("rsr_sample_fp4", A.ptr(_dev(probs)), n, m, 99, 5, start, count, A.ptr(st), A.ptr(a4), rb,
+           A.stream_ptr())
+    assert np.array_equal(st.cpu().numpy(), want)
+    assert np.array_equal(a4.cpu().numpy(), _fp4_want(want, None, n, m, None))
+    only = torch.empty_like(a4)
+    A.call("rsr_sample_fp4", A.ptr(_dev(probs)), n, m, 99, 5, start, count, None, A.ptr(only), rb,
+           A.stream_ptr())
+    assert torch.equal(only, a4)
+
+
 def _refs_dev(refs, n, m, side):
     kpad = A.thermo_kpad(n, m)
     k = refs.shape[0]

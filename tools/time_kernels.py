@@ -32,7 +32,15 @@ def main():
         st = torch.empty((S, 295), dtype=torch.uint8, device="cuda")
         th = torch.empty((S, P._abi.thermo_kpad(295, m)), dtype=torch.int8, device="cuda")
         ms = timed(lambda: P.sample_batch(d, S, 0, 1, out_states=st, out_thermo=th))
+        print(f"sample_batch+int8 thermo M={m} S=2^20 N=295: {ms:.3f} ms = {S * 295 / ms / 1e6:.1f} G draws/s")
+        ms = timed(lambda: P.sample_batch(d, S, 0, 1, out_states=st))
         print(f"sample_batch M={m} S=2^20 N=295: {ms:.3f} ms = {S * 295 / ms / 1e6:.1f} G draws/s")
+        rb = P._abi.fp4_row_bytes(295, m)
+        a4 = torch.empty((S, 2 * rb), dtype=torch.uint8, device="cuda")
+        ms = timed(lambda: P._abi.call("rsr_encode_samples_fp4", P._abi.ptr(st), S, 295, m,
+                                       P._abi.ptr(a4), rb, P._abi.stream_ptr()))
+        gbs = (S * 295 + S * 2 * rb) / ms / 1e6
+        print(f"encode_samples_fp4 M={m} S=2^20: {ms:.3f} ms = {gbs:.0f} GB/s")
     g = W.cfg3(0)
     graph = P.Graph(g["n_nodes"], tuple(g["edges"]))
     for name, phi, m in (("st", P.single_od_connectivity(graph, g["source"], g["target"]), 2),
