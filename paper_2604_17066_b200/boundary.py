@@ -149,19 +149,20 @@ class ReferenceSet:
         side = _side_code(self.side)
         st = _device.stream()
         dev = cands_dev.device
-        covered = torch.zeros(B, dtype=torch.uint8, device=dev)
-        covers = torch.zeros(B, dtype=torch.uint8, device=dev)
+        # covered [B] | covers [B] | rel [B x B] in one buffer: one device->host copy
+        scan = torch.zeros(2 * B + B * B, dtype=torch.uint8, device=dev)
+        covered, covers, rel = scan[:B], scan[B: 2 * B], scan[2 * B:].view(B, B)
         if self._n:
             mem = self.device_rows()
             _abi.call("rsr_dominance_scan", _abi.ptr(cands_dev), B, _abi.ptr(mem), self._n, N, side,
                       _abi.ptr(covered), _abi.ptr(covers), -1, None, st)
-        rel = torch.zeros((B, B), dtype=torch.uint8, device=dev)
         if B > 1:
             _abi.call("rsr_dominance_scan", _abi.ptr(cands_dev), B, _abi.ptr(cands_dev), B, N, side,
                       None, None, -1, _abi.ptr(rel), st)
-        covered_h = covered.cpu().numpy().astype(bool)
-        covers_h = covers.cpu().numpy().astype(bool)
-        rel_h = rel.cpu().numpy()
+        scan_h = scan.cpu().numpy()
+        covered_h = scan_h[:B].astype(bool)
+        covers_h = scan_h[B: 2 * B].astype(bool)
+        rel_h = scan_h[2 * B:].reshape(B, B)
         if not covers_h.any() and not np.tril(rel_h, -1).any():
             # common case (e.g. bulk loads of non-dominated sets): no candidate relates
             # to an earlier one and none drops a member -> inserted iff not covered

@@ -253,7 +253,30 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
         calls += xn - L + 1;  // steps down to L-1, the last one removes edge n
         const bool on = (onpath[n >> 5] >> (n & 31)) & 1u;
         if (on) {
-          toggle_edge(adj, W, eu[n], ev[n], lane);
+          const int u = eu[n], v = ev[n];
+          toggle_edge(adj, W, u, v, lane);
+          // cheap witness repair first: a common neighbour w of u and v turns
+          // the path into a walk through (u,w),(w,v) that still contains an s-t
+          // path (the witness may be a superset of a path: a later test of one
+          // of its edges then just runs the exact BFS below)
+          int wn = -1;
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            const uint32_t c = adj[u * W + q] & adj[v * W + q];
+            if (wn < 0 && c) wn = 32 * q + __ffs(c) - 1;
+          }
+          if (wn >= 0 && g.eid) {
+            if (lane == 0) {
+              const int e1 = g.eid[u * g.n + wn], e2 = g.eid[wn * g.n + v];
+              onpath[n >> 5] &= ~(1u << (n & 31));
+              onpath[e1 >> 5] |= 1u << (e1 & 31);
+              onpath[e2 >> 5] |= 1u << (e2 & 31);
+            }
+            calls += L - 1;
+            if (lane == 0) x[n] = 0;
+            __syncwarp();
+            continue;
+          }
           dd = bfs_layers<W>(adj, levels, g.n, g.s, g.t, lane);
           if (dd == 0) {  // crossing: reverted, walk moves to n + 1
             toggle_edge(adj, W, eu[n], ev[n], lane);

@@ -132,9 +132,55 @@ class _BatchBuffers:
                     if self.fp4_ok else None)
 
 
-def _classify_shard(model, dist_, seed, gen, lower, upper, comm, bufs, start, count):
-    batch = sample_batch(dist_, count, seed, gen, start, out_states=bufs.states,
-                         out_fp4=bufs.fp4 if bufs.fp4_ok else None)
+_STREAMS: dict = {}
+
+
+def _high_priority_stream() -> torch.cuda.Stream:
+    """One persistent high-priority stream per device (allocations made on it stay
+    in one caching-allocator pool across calls)."""
+    key = torch.cuda.current_device()
+    st = _STREAMS.get(key)
+    if st is None:
+        st = _STREAMS[key] = torch.cuda.Stream(priority=-1)
+    return st
+
+
+class _Prefetcher:
+    """Double-buffered sampling on a side stream: batch i+1 (generation i+1 does
+    not depend on the references) is drawn while iteration i searches and
+    inserts on the main stream."""
+
+    def __init__(self, dist_, seed, start, count):
+        self.dist, self.seed, self.start, self.count = dist_, seed, start, count
+        self.bufs = [_BatchBuffers(max(count, 1), dist_.n_components, dist_.n_states)
+                     for _ in range(2)]
+        self.stream = torch.cuda.Stream()
+        self.free = [None, None]  # main-stream events: slot no longer read
+
+    def launch(self, gen):
+        slot = gen & 1
+        b = self.bufs[slot]
+        with torch.cuda.stream(self.stream):
+            if self.free[slot] is not None:
+                self.stream.wait_event(self.free[slot])
+            batch = sample_batch(self.dist, self.count, self.seed, gen, self.start,
+                                 out_states=b.states, out_fp4=b.fp4 if b.fp4_ok else None)
+            ready = torch.cuda.Event()
+            ready.record(self.stream)
+        return batch, ready
+
+    def release(self, gen):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.free[gen & 1] = ev
+
+    def close(self):
+        torch.cuda.current_stream().wait_stream(self.stream)
+
+
+def _classify_shard(model, pending, lower, upper, comm):
+    batch, ready = pending
+    torch.cuda.current_stream().wait_event(ready)
     res = classify(batch, lower, upper, n_states=model.n_component_states)
     counts = comm.allreduce_sum_i64(list(res.counts)) if comm.distributed else np.array(res.counts)
     return batch, res, counts
@@ -148,19 +194,34 @@ def stage1_find_references(model: SystemModel, dist: ComponentDistribution, conf
     phi = model.device_phi()
     lower = ReferenceSet(Side.LOWER, threshold)
     upper = ReferenceSet(Side.UPPER, threshold)
-    trace: list[TraceRecord] = []
-    redundant = 0
     phi_start = model.evaluation_count
     t_start = time.perf_counter()
-    terminated_by = "r_max"
     H = config.n_samples
     start, count = shard_range(H, comm.world, comm.rank)
-    bufs = _BatchBuffers(max(count, 1), dist.n_components, dist.n_states)
+    # the loop's own kernels run on a high-priority stream so the prefetched
+    # sampler (low priority, all SMs) does not delay the small search kernels
+    caller = torch.cuda.current_stream()
+    loop_stream = _high_priority_stream()
+    loop_stream.wait_stream(caller)
+    with torch.cuda.stream(loop_stream):
+        result = _stage1_loop(model, dist, config, threshold, comm, phi, lower, upper, start,
+                              count, H, t_start, phi_start)
+    caller.wait_stream(loop_stream)
+    return result
+
+
+def _stage1_loop(model, dist, config, threshold, comm, phi, lower, upper, start, count, H,
+                 t_start, phi_start) -> Stage1Result:
+    trace: list[TraceRecord] = []
+    redundant = 0
+    terminated_by = "r_max"
+    pre = _Prefetcher(dist, config.seed, start, count)
+    pending = pre.launch(0)
     N = dist.n_components
     iteration = 0
     while True:
-        batch, res, counts = _classify_shard(model, dist, config.seed, iteration, lower, upper,
-                                             comm, bufs, start, count)
+        batch, res, counts = _classify_shard(model, pending, lower, upper, comm)
+        pending = pre.launch(iteration + 1)
         n_l, n_u, n_x = (int(c) for c in counts[:3])
         trace.append(TraceRecord(
             reference_count=len(lower) + len(upper),
@@ -179,15 +240,14 @@ def stage1_find_references(model: SystemModel, dist: ComponentDistribution, conf
         x0 = _gather_picks(batch, res, positions, comm, N)
         if config.boundary_search_enabled:
             refs_d, side_d, calls_d = boundary_search_batch(model, x0, threshold)
-            model.add_evaluations(int(calls_d.sum().item()))
         else:
             vals = torch.empty(n_pick, dtype=torch.uint8, device=x0.device)
             phi.eval_into(x0, None, n_pick, model.n_component_states, vals)
-            model.add_evaluations(n_pick)
             refs_d = x0
             side_d = torch.where(vals <= threshold, _abi.SIDE_LOWER, _abi.SIDE_UPPER).to(torch.uint8)
-        refs_h = refs_d.cpu().numpy()
-        side_h = side_d.cpu().numpy()
+            calls_d = None
+        refs_h, side_h, calls_h = _to_host(refs_d, side_d, calls_d)
+        model.add_evaluations(int(calls_h.sum()) if calls_h is not None else n_pick)
         for code, target in ((_abi.SIDE_LOWER, lower), (_abi.SIDE_UPPER, upper)):
             sel = np.flatnonzero(side_h == code)
             if sel.size == 0:
@@ -195,9 +255,25 @@ def stage1_find_references(model: SystemModel, dist: ComponentDistribution, conf
             sel_d = torch.as_tensor(sel, dtype=torch.int64, device=refs_d.device)
             outcome = target.insert_batch(refs_d.index_select(0, sel_d).contiguous(), refs_h[sel])
             redundant += sum(1 for o in outcome if o == "redundant")
+        pre.release(iteration)
         iteration += 1
+    pre.close()
     return Stage1Result(lower=lower, upper=upper, trace=trace, iterations=iteration + 1,
                         redundant_searches=redundant, terminated_by=terminated_by)
+
+
+def _to_host(*tensors):
+    """Several small device tensors -> numpy with a single stream synchronisation."""
+    outs = []
+    for t in tensors:
+        if t is None:
+            outs.append(None)
+            continue
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [None if h is None else h.numpy() for h in outs]
 
 
 def _gather_picks(batch, res, positions: np.ndarray, comm: Comm, N: int) -> torch.Tensor:
