@@ -293,8 +293,9 @@ class ReferenceSet:
         return t, self._n
 
     def device_fp4(self, n_states: int) -> tuple[torch.Tensor | None, int]:
-        """FP4 B rows ([r < k] lower / [r >= k] upper as packed e2m1, padded to
-        240-row tiles with never-hit rows) and the member count."""
+        """FP4 B rows ([r < k] lower / [r >= k] upper as packed e2m1) and the number
+        of rows to stream: the members padded to whole 240-row tiles with never-hit
+        rows, so the classifier's epilogue needs no column masking."""
         if self._n == 0:
             return None, 0
         rows_dev = self.device_rows()
@@ -315,7 +316,7 @@ class ReferenceSet:
             _abi.call("rsr_encode_refs_fp4", _abi.ptr(rows_dev[done:]), self._n - done, need - done,
                       N, n_states, _side_code(self.side), _abi.ptr(t[done:]), rb, _device.stream())
             ent[1] = self._n
-        return t, self._n
+        return t, need
 
     def device_bits(self, n_states: int) -> tuple[torch.Tensor | None, int]:
         """Packed thermometer bits ([r < k] lower / [r >= k] upper) and count."""

@@ -71,18 +71,19 @@ static_assert(kTileN % kColGroups == 0 && kCols % 4 == 0, "bad epilogue split");
 // RSR_FP4_PROF builds (tools/ only, never the product library) accumulate
 // per-role cycle counters into g_prof: 0 MMA wait b_full, 1 MMA wait t_empty,
 // 2 MMA loop total, 3 epilogue wait t_full, 4 epilogue load+release,
-// 5 epilogue compute, 6 producer wait b_empty, 7 tiles (MMA warp);
+// 5 epilogue compute, 6 producer wait b_empty, 7 tiles (MMA warp), 8 epilogue
+// group-end exchange, 9 MMA wait a_full, 10 producer wait a_empty, 11 groups (MMA);
 // 4 covers load + release + compute of the tile, 5 the bookkeeping after it.
 // Counters live in registers (prof[8] per thread) and are flushed once per
 // warp at the end, so the instrumentation barely perturbs the timing.
 #ifdef RSR_FP4_PROF
-__device__ unsigned long long g_prof[8];
-#define PROF_DECL unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+__device__ unsigned long long g_prof[12];
+#define PROF_DECL unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
 #define PROF_T(x) const long long x = clock64()
 #define PROF_ADD(i, v) (prof[i] += (unsigned long long)(v))
 #define PROF_FLUSH                                                   \
   if ((threadIdx.x & 31) == 0)                                       \
-    for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_prof[i_], prof[i_])
+    for (int i_ = 0; i_ < 12; ++i_) atomicAdd(&g_prof[i_], prof[i_])
 #else
 #define PROF_DECL
 #define PROF_T(x)
@@ -106,6 +107,7 @@ struct Fp4Params {
   int64_t first_base_upper;
   int64_t n_lower;  // reference rows of this launch per side (columns beyond are masked)
   int64_t n_upper;
+  int resident;     // every reference tile has its own stage: loaded once, reused by all groups
 };
 
 // SW32 K-major descriptor: 8-row core groups 256 B apart, version 1, layout 6.
@@ -258,12 +260,12 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * b_stage_bytes);
   uint64_t* b_full = bars;
   uint64_t* b_empty = bars + p.stages;
-  uint64_t* a_full = bars + 2 * p.stages;  // [2]
-  uint64_t* a_empty = a_full + 2;          // [2]
-  uint64_t* t_full = a_full + 4;           // [kBufs]
-  uint64_t* t_empty = a_full + 8;          // [kBufs]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 12);
-  uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 14);  // [kColGroups][128] hit bits
+  uint64_t* a_full = bars + 2 * p.stages;  // [a_bufs <= 4]
+  uint64_t* a_empty = a_full + 4;          // [a_bufs <= 4]
+  uint64_t* t_full = a_full + 8;           // [kBufs <= 4]
+  uint64_t* t_empty = a_full + 12;         // [kBufs <= 4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 16);
+  uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 18);  // [kColGroups][128] hit bits
   int64_t* xfirst = reinterpret_cast<int64_t*>(xchg + kColGroups * 128) - 256;  // [1..][2][128]
 
   const int warp = threadIdx.x >> 5;
@@ -281,7 +283,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_init(smem_addr(&b_full[i]), 2);
       mbar_init(smem_addr(&b_empty[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < p.a_bufs; ++i) {
       mbar_init(smem_addr(&a_full[i]), 2);
       mbar_init(smem_addr(&a_empty[i]), 1);
     }
@@ -330,7 +332,10 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       const int ab = gi % p.a_bufs;
       const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
       const uint32_t bar_af = smem_addr(&a_full[ab]);
+      PROF_T(p0);
       mbar_wait(smem_addr(&a_empty[ab]), a_par ^ 1);
+      PROF_T(p1);
+      PROF_ADD(10, p1 - p0);
       if (elect_one()) {
         if (leader)
           mbar_expect_tx(bar_af, 2 * a_buf_bytes);
@@ -340,6 +345,25 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                          g * 2 * kRowsA + (int)rank * kRowsA, 0);
       }
       __syncwarp();
+      if (p.resident) {
+        // small reference sets: tile j lives in stage j for the whole launch
+        if (gi == 0) {
+          for (int j = 0; j < p.nt_total; ++j) {
+            const bool low = j < p.nt_lower;
+            const int y = (low ? j : j - p.nt_lower) * kTileN + (int)rank * kHalfRows;
+            if (elect_one()) {
+              if (leader)
+                mbar_expect_tx(bar_b_full + 8 * j, 2 * b_stage_bytes);
+              else
+                mbar_arrive_leader(bar_b_full + 8 * j);
+              tma_load_3d_pair(sB0 + (uint32_t)j * b_stage_bytes, low ? &map_lower : &map_upper,
+                               bar_b_full + 8 * j, 0, y, 0);
+            }
+            __syncwarp();
+          }
+        }
+        continue;
+      }
       int j = rot;
       for (int jj = 0; jj < p.nt_total; ++jj) {
         const bool low = j < p.nt_lower;
@@ -380,7 +404,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       uint32_t phase = 0, buf = 0, tphase = 0;
       for (int g = cluster; g < p.n_groups; g += n_clusters, ++gi) {
         const int ab = gi % p.a_bufs;
+        PROF_T(w0);
         mbar_wait(smem_addr(&a_full[ab]), (uint32_t)(gi / p.a_bufs) & 1);
+        PROF_T(w1);
+        PROF_ADD(9, w1 - w0);
+        PROF_ADD(11, 1);
         tc_fence_after();
         const uint32_t a_up = a_lo0 + (uint32_t)ab * (a_buf_bytes >> 4);
         const uint32_t a_dn = a_up + (uint32_t)cq * kAstep;
@@ -390,13 +418,16 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         int j = rot;
         for (int jj = 0; jj < p.nt_total; ++jj) {
           const uint32_t al = j < p.nt_lower ? a_dn : a_up;
+          // resident B: tile j sits in stage j, whose only phase (0) completes once
+          const int bs = p.resident ? j : stage;
+          const uint32_t bpar = p.resident ? 0u : phase;
           if (++j == p.nt_total) j = 0;
           const uint32_t d = tm0 + buf * kTileN;
-          const uint32_t bl = b_lo0 + (uint32_t)stage * (b_stage_bytes >> 4);
+          const uint32_t bl = b_lo0 + (uint32_t)bs * (b_stage_bytes >> 4);
           PROF_T(m0);
           mbar_wait(bar_t_empty + 8 * buf, tphase ^ 1);
           PROF_T(m1);
-          mbar_wait(bar_b_full + 8 * stage, phase);
+          mbar_wait(bar_b_full + 8 * bs, bpar);
           PROF_T(m2);
           PROF_ADD(1, m1 - m0);
           PROF_ADD(0, m2 - m1);
@@ -406,7 +437,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             for (int ks = 0; ks < cq; ++ks)
               umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
             umma_commit_pair(bar_t_full + 8 * buf);
-            umma_commit_pair(bar_b_empty + 8 * stage);
+            if (!p.resident) umma_commit_pair(bar_b_empty + 8 * stage);
           }
           __syncwarp();
           if (++stage == p.stages) {
@@ -468,9 +499,10 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         PROF_ADD(5, e3 - e2);
       }
       // the column groups of a row live in kColGroups warps: combine through shared memory
+      PROF_T(x0);
       const int64_t row = (int64_t)g * 2 * kRowsA + rank * kRowsA + quad * 32 + lane;
       const int r = quad * 32 + lane;
-      named_bar_sync(1, 32 * kEpiWarps);
+      if constexpr (kColGroups > 1) named_bar_sync(1, 32 * kEpiWarps);
       if (cg != 0) {
         xchg[cg * 128 + r] = hit;
         if (FIRST) {
@@ -478,7 +510,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
           xfirst[(cg * 2 + 1) * 128 + r] = first[1];
         }
       }
-      named_bar_sync(1, 32 * kEpiWarps);
+      if constexpr (kColGroups > 1) named_bar_sync(1, 32 * kEpiWarps);
       if (cg == 0) {
 #pragma unroll
         for (int q = 1; q < kColGroups; ++q) {
@@ -503,6 +535,8 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
           }
         }
       }
+      PROF_T(x1);
+      PROF_ADD(8, x1 - x0);
     }
   }
 
@@ -584,15 +618,26 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   p.first_lower = first_lower;
   p.first_upper = first_upper;
   const size_t max_smem = 227 * 1024;
-  // align slack, barriers + hit exchange, first-match exchange
-  const size_t fixed = 1024 + 256 + kColGroups * 512 + (want_first ? (kColGroups - 1) * 2048 : 0);
+  // align slack, barriers (<= 16 stages x 2 + 18), hit exchange, first-match exchange
+  const size_t bars_bytes = (2 * 16 + 18) * 8;
+  const size_t fixed = 1024 + bars_bytes + kColGroups * 512 +
+                       (want_first ? (kColGroups - 1) * 2048 : 0);
   const size_t a_buf = (size_t)2 * cq * kChunkA, b_stage = (size_t)cq * (TN / 2) * kChunk;
-  p.a_bufs = 2;
+  // sample-group buffers: 3 when a group has few reference tiles (its MMAs are short,
+  // so the next groups' A loads must be further ahead), else 2; 1 if smem is short
   const char* ab_env = getenv("RSR_TC_ABUFS");
-  if ((ab_env && atoi(ab_env) == 1) || fixed + 2 * a_buf + 4 * b_stage > max_smem) p.a_bufs = 1;
+  p.a_bufs = ab_env ? atoi(ab_env) : (nt_l + nt_u <= 16 ? 3 : 2);
+  if (p.a_bufs < 1) p.a_bufs = 1;
+  if (p.a_bufs > 4) p.a_bufs = 4;
+  while (p.a_bufs > 1 && fixed + p.a_bufs * a_buf + 4 * b_stage > max_smem) --p.a_bufs;
   int stages = (int)((max_smem - fixed - p.a_bufs * a_buf) / b_stage);
   if (stages > 16) stages = 16;
   RSR_REQUIRE(stages >= 2, "rsr_classify_fp4: row_bytes too large for shared memory");
+  // a launch whose reference tiles all fit in the ring keeps them resident
+  const char* res_env = getenv("RSR_FP4_RESIDENT");
+  const bool allow_resident = !(res_env && atoi(res_env) == 0);
+  p.resident = allow_resident && nt_l + nt_u <= stages;
+  if (p.resident) stages = (int)(nt_l + nt_u);
   p.stages = stages;
   const size_t smem = fixed + p.a_bufs * a_buf + (size_t)stages * b_stage;
   p.n_groups = (int)rsr::ceil_div(S, (int64_t)2 * kRowsA);

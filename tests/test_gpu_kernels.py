@@ -205,7 +205,11 @@ def _want_flags(samples, lower, upper, m):
     (9, 4, 500, 20, 20, 0.5),
     (200, 4, 300, 64, 64, 0.5),
 ])
-def test_classifiers_match_oracle(n, m, s, kl, ku, p1):
+@pytest.mark.parametrize("resident", ["1", "0"])
+def test_classifiers_match_oracle(n, m, s, kl, ku, p1, resident, monkeypatch):
+    # resident: small reference sets stay in shared memory for the whole launch
+    # (RSR_FP4_RESIDENT=0 forces the streaming ring)
+    monkeypatch.setenv("RSR_FP4_RESIDENT", resident)
     rng = np.random.default_rng(n + 1000 * m + s)
     samples = rng.integers(0, m, size=(s, n))
     if m == 2:
@@ -223,10 +227,12 @@ def test_classifiers_match_oracle(n, m, s, kl, ku, p1):
     assert np.array_equal(got_bits, want)
 
 
+@pytest.mark.parametrize("resident", ["1", "0"])
 @pytest.mark.parametrize("chunk_tiles", ["1", "2", "3"])
-def test_reference_chunked_launches(chunk_tiles, monkeypatch):
+def test_reference_chunked_launches(chunk_tiles, resident, monkeypatch):
     # B split across several launches (lower tail + upper head in one chunk, etc.)
     monkeypatch.setenv("RSR_TC_CHUNK_TILES", chunk_tiles)
+    monkeypatch.setenv("RSR_FP4_RESIDENT", resident)
     n, m, s = 120, 2, 2500
     rng = np.random.default_rng(17)
     samples = (rng.random((s, n)) < 0.5).astype(np.int64)

@@ -17,11 +17,13 @@ from paper_2604_17066_b200.classify import classify_flags  # noqa: E402
 lib = _abi.lib()
 fn = lib.rsr_fp4_prof
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = (ctypes.c_ulonglong * 8)()
-lower, upper = W.cfg2_refs(0, 295, 10_000, 10_000)
+buf = (ctypes.c_ulonglong * 12)()
+K = int(os.environ.get("K", "10000"))
+S = int(os.environ.get("S", str(1 << 20)))
+lower, upper = W.cfg2_refs(0, 295, K, K)
 lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
 up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
-batch = P.sample_batch(P.ComponentDistribution.iid(295, [0.1, 0.9]), 1 << 20, seed=0)
+batch = P.sample_batch(P.ComponentDistribution.iid(295, [0.1, 0.9]), S, seed=0)
 for it in range(3):
     fn(buf, 1)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -39,3 +41,8 @@ E = int(os.environ.get("EPI_WARPS", "16")) * 2  # epilogue warps per tile (both 
 per = [tiles + E * tiles, tiles, tiles, E * tiles, E * tiles, E * tiles, 2 * tiles]
 for n, x, d in zip(names, v, per):
     print(f"{n:20s} {x / max(d, 1):8.1f} cycles per tile (per warp)")
+groups = max(v[11], 1)
+print(f"groups (MMA) {groups}, tiles per group {tiles / groups:.1f}")
+print(f"epi group-end exchange {v[8] / (E * groups):8.1f} cycles per group (per warp)")
+print(f"mma wait a_full        {v[9] / groups:8.1f} cycles per group")
+print(f"prod wait a_empty      {v[10] / (2 * groups):8.1f} cycles per group")
