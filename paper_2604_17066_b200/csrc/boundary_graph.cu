@@ -28,6 +28,19 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// experiment builds (make prof): 0 searches, 1 upper-side searches, 2 BFS runs,
+// 3 BFS levels, 4 cycles in BFS, 5 cycles in trace_path, 6 cycles in the initial
+// union-find, 7 total cycles
+#ifdef RSR_FP4_PROF
+__device__ unsigned long long g_bprof[8];
+#define BPROF_ADD(i, v) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_bprof[i], (unsigned long long)(v))
+#define BPROF_T(x) const long long x = clock64()
+#else
+#define BPROF_ADD(i, v)
+#define BPROF_T(x)
+#endif
+
 struct GraphSmem {
   int N, n, s, t;
   const int32_t* eu;
@@ -39,15 +52,15 @@ constexpr int kEidMaxNodes = 128;
 
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) / 16 * 16; }
 
-// per-warp scratch: x (N bytes), union-find parents (n int16), on-path bits
+// per-warp scratch: x (N bytes), union-find parents (n int32), on-path bits
 // (ceil(N/32) words), adjacency of G_L (n x W words), BFS levels (n x W words)
 template <int W>
 __host__ __device__ inline size_t warp_scratch(int N, int n) {
-  return align16(N) + align16(2 * (size_t)n) + align16(4 * (((size_t)N + 31) / 32)) +
-         2 * (size_t)n * W * 4;
+  return align16(N) + align16(4 * (size_t)n) + align16(4 * (((size_t)N + 31) / 32)) +
+         align16(2 * (size_t)n * W * 4);
 }
 
-__device__ __forceinline__ int uf_find(int16_t* par, int a) {
+__device__ __forceinline__ int uf_find(int32_t* par, int a) {
   while (par[a] != a) {
     par[a] = par[par[a]];  // path halving
     a = par[a];
@@ -55,57 +68,125 @@ __device__ __forceinline__ int uf_find(int16_t* par, int a) {
   return a;
 }
 
-// BFS from s in adj recording each level's new nodes; on success levels[0..d]
-// hold the layers and the return value is d (>= 1), else 0 (t unreachable).
+// Adjacency of G_L as node bitsets (node v = word v/32, bit v%32), two
+// storages behind one interface:
+//   AdjSmem: rows in shared memory (any n <= 256);
+//   AdjReg:  rows in registers, lane l owning the rows of nodes l, l+32, ...
+//            (n <= 128: W*W = 16 registers).
+// A BFS level is a pull step: lane l tests whether node 32q+l has a neighbour
+// in the frontier (W*W ANDs) and one ballot per word assembles the next
+// frontier -- no cross-lane OR reduction (redux.sync) on the critical path.
 template <int W>
-__device__ int bfs_layers(const uint32_t* adj, uint32_t* levels, int n, int s, int t, int lane) {
-  uint32_t F[W], V[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) F[w] = V[w] = (w == (s >> 5)) ? (1u << (s & 31)) : 0u;
-#pragma unroll
-  for (int w = 0; w < W; ++w)
-    if (lane == w) levels[w] = F[w];
-  for (int d = 1; d < n; ++d) {
-    uint32_t acc[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) acc[w] = 0;
+struct AdjSmem {
+  uint32_t* a;
+  // next[q] bit l = node 32q+l has a neighbour in F (pull step, one ballot per word)
+  __device__ void pull(const uint32_t (&F)[W], uint32_t (&next)[W], int n, int lane) const {
 #pragma unroll
     for (int q = 0; q < W; ++q) {
       const int v = 32 * q + lane;
-      if (v < n && ((F[q] >> lane) & 1u)) {
+      uint32_t hit = 0;
+      if (v < n) {
 #pragma unroll
-        for (int w = 0; w < W; ++w) acc[w] |= adj[v * W + w];
+        for (int w = 0; w < W; ++w) hit |= a[v * W + w] & F[w];
       }
+      next[q] = __ballot_sync(kFull, hit != 0);
     }
+  }
+  __device__ uint32_t row(int node, int w) const { return a[node * W + w]; }
+  __device__ void toggle(int u, int v, int lane) {
+    if (lane == 0) {
+      a[u * W + (v >> 5)] ^= 1u << (v & 31);
+      a[v * W + (u >> 5)] ^= 1u << (u & 31);
+    }
+    __syncwarp();
+  }
+};
+
+template <int W>
+struct AdjReg {
+  uint32_t r[W][W];
+  __device__ void load(const uint32_t* a, int n, int lane) {
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+#pragma unroll
+      for (int w = 0; w < W; ++w) r[q][w] = (32 * q + lane < n) ? a[(32 * q + lane) * W + w] : 0u;
+  }
+  __device__ void pull(const uint32_t (&F)[W], uint32_t (&next)[W], int, int) const {
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      uint32_t hit = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) hit |= r[q][w] & F[w];
+      next[q] = __ballot_sync(kFull, hit != 0);
+    }
+  }
+  // (selects are written as masks: a branch on q == node/32 lets the compiler
+  // turn r into a dynamically indexed, i.e. local-memory, array)
+  __device__ uint32_t row(int node, int w) const {  // node is warp-uniform
+    uint32_t val = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) val |= r[q][w] & (0u - (uint32_t)(q == (node >> 5)));
+    return __shfl_sync(kFull, val, node & 31);
+  }
+  __device__ void toggle(int u, int v, int lane) {
+    const uint32_t bu = (lane == (u & 31)) ? 1u << (v & 31) : 0u;
+    const uint32_t bv = (lane == (v & 31)) ? 1u << (u & 31) : 0u;
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        r[q][w] ^= (bu & (0u - (uint32_t)(q == (u >> 5) && w == (v >> 5)))) |
+                   (bv & (0u - (uint32_t)(q == (v >> 5) && w == (u >> 5))));
+  }
+};
+
+// BFS from s recording each level's new nodes; on success levels[0..d] hold the
+// layers and the return value is d (>= 1), else 0 (t unreachable).
+template <int W, class Adj>
+__device__ __forceinline__ int bfs_layers(const Adj& adj, uint32_t* levels, int n, int s, int t, int lane) {
+  uint32_t F[W], V[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) F[w] = V[w] = (w == (s >> 5)) ? (1u << (s & 31)) : 0u;
+  // lane w < W stores word w of each layer (mask select: no indexed registers)
+  auto word_of = [&](const uint32_t (&X)[W]) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) r |= X[w] & (0u - (uint32_t)(lane == w));
+    return r;
+  };
+  if (lane < W) levels[lane] = word_of(F);
+  for (int d = 1; d < n; ++d) {
+    uint32_t nxt[W];
+    adj.pull(F, nxt, n, lane);
     uint32_t any = 0;
     bool hit = false;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const uint32_t nw = __reduce_or_sync(kFull, acc[w]) & ~V[w];
+      const uint32_t nw = nxt[w] & ~V[w];
       V[w] |= nw;
       F[w] = nw;
       any |= nw;
       if (w == (t >> 5)) hit = (nw >> (t & 31)) & 1u;
     }
-    if (lane < W) {
-#pragma unroll
-      for (int w = 0; w < W; ++w)
-        if (w == lane) levels[d * W + w] = F[w];
-    }
+    if (lane < W) levels[d * W + lane] = word_of(F);
     if (hit) {
       __syncwarp();
+      BPROF_ADD(3, d);
       return d;
     }
-    if (!any) break;
+    if (!any) {
+      BPROF_ADD(3, d);
+      break;
+    }
   }
   __syncwarp();
   return 0;
 }
 
 // Mark the edges of one shortest s-t path (from bfs_layers) in `onpath`.
-template <int W>
-__device__ void trace_path(const GraphSmem& g, const uint32_t* adj, const uint32_t* levels,
-                           int d, uint32_t* onpath, int lane) {
+template <int W, class Adj>
+__device__ __forceinline__ void trace_path(const GraphSmem& g, const Adj& adj, const uint32_t* levels, int d,
+                           uint32_t* onpath, int lane) {
   const int words = (g.N + 31) / 32;
   for (int i = lane; i < words; i += 32) onpath[i] = 0;
   __syncwarp();
@@ -115,7 +196,7 @@ __device__ void trace_path(const GraphSmem& g, const uint32_t* adj, const uint32
     int p = -1;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const uint32_t c = adj[cur * W + w] & levels[(k - 1) * W + w];
+      const uint32_t c = adj.row(cur, w) & levels[(k - 1) * W + w];
       if (p < 0 && c) p = 32 * w + __ffs(c) - 1;
     }
     // the (unique, simple graph) edge joining p and cur
@@ -123,11 +204,8 @@ __device__ void trace_path(const GraphSmem& g, const uint32_t* adj, const uint32
     for (int e0 = 0; e_found < 0 && e0 < g.N; e0 += 32) {
       const int e = e0 + lane;
       const bool m = e < g.N && ((g.eu[e] == p && g.ev[e] == cur) || (g.eu[e] == cur && g.ev[e] == p));
-      const unsigned b = __ballot_sync(kFull, m);
-      if (b) {
-        e_found = e0 + __ffs(b) - 1;
-        break;
-      }
+      const unsigned bal = __ballot_sync(kFull, m);
+      if (bal) e_found = e0 + __ffs(bal) - 1;
     }
     if (lane == 0) onpath[e_found >> 5] |= 1u << (e_found & 31);
     cur = p;
@@ -135,12 +213,69 @@ __device__ void trace_path(const GraphSmem& g, const uint32_t* adj, const uint32
   __syncwarp();
 }
 
-__device__ __forceinline__ void toggle_edge(uint32_t* adj, int W, int u, int v, int lane) {
-  if (lane == 0) {
-    adj[u * W + (v >> 5)] ^= 1u << (v & 31);
-    adj[v * W + (u >> 5)] ^= 1u << (u & 31);
+// Upper side of the walk (start connected in G_L): witness path + BFS for edges
+// on it.  x[] is updated by lane 0; returns the Phi-call count of the walk
+// after the initial evaluation.
+template <int W, class Adj>
+__device__ __forceinline__ int64_t upper_walk(const GraphSmem& g, Adj& adj, uint8_t* x, uint32_t* levels,
+                              uint32_t* onpath, int L, int lane) {
+  int64_t calls = 0;
+  int dd = bfs_layers<W>(adj, levels, g.n, g.s, g.t, lane);
+  trace_path<W>(g, adj, levels, dd, onpath, lane);
+  BPROF_ADD(1, 1);
+  for (int n = 0; n < g.N; ++n) {
+    const int xn = x[n];
+    if (xn == 0) continue;
+    if (xn < L) {  // not in G_L: every step down leaves G_L unchanged
+      calls += xn;
+      if (lane == 0) x[n] = 0;
+      continue;
+    }
+    calls += xn - L + 1;  // steps down to L-1, the last one removes edge n
+    const int u = g.eu[n], v = g.ev[n];
+    adj.toggle(u, v, lane);
+    const bool on = (onpath[n >> 5] >> (n & 31)) & 1u;
+    if (on) {
+      // cheap witness repair first: a common neighbour w of u and v turns the
+      // path into a walk through (u,w),(w,v) that still contains an s-t path
+      // (the witness may be a superset of a path: a later test of one of its
+      // edges then just runs the exact BFS below)
+      int wn = -1;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        const uint32_t c = adj.row(u, q) & adj.row(v, q);
+        if (wn < 0 && c) wn = 32 * q + __ffs(c) - 1;
+      }
+      if (wn >= 0 && g.eid) {
+        if (lane == 0) {
+          const int e1 = g.eid[u * g.n + wn], e2 = g.eid[wn * g.n + v];
+          onpath[n >> 5] &= ~(1u << (n & 31));
+          onpath[e1 >> 5] |= 1u << (e1 & 31);
+          onpath[e2 >> 5] |= 1u << (e2 & 31);
+        }
+        __syncwarp();
+      } else {
+        BPROF_T(b0);
+        dd = bfs_layers<W>(adj, levels, g.n, g.s, g.t, lane);
+        BPROF_T(b1);
+        BPROF_ADD(2, 1);
+        BPROF_ADD(4, b1 - b0);
+        if (dd == 0) {  // crossing: reverted, walk moves to n + 1
+          adj.toggle(u, v, lane);
+          if (lane == 0) x[n] = (uint8_t)L;
+          continue;
+        }
+        BPROF_T(c0);
+        trace_path<W>(g, adj, levels, dd, onpath, lane);
+        BPROF_T(c1);
+        BPROF_ADD(5, c1 - c0);
+      }
+    }
+    calls += L - 1;
+    if (lane == 0) x[n] = 0;
   }
   __syncwarp();
+  return calls;
 }
 
 template <int W>
@@ -162,10 +297,12 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
   }
   g.eu = eu;
   g.ev = ev;
-  uint8_t* after = reinterpret_cast<uint8_t*>(ev + g.N);
+  // offsets (not integer-cast pointers) keep every scratch pointer in the
+  // shared address space, so the compiler emits LDS/STS instead of generic ops
+  size_t off = align16(2 * sizeof(int32_t) * (size_t)g.N);
   g.eid = nullptr;
   if (g.n <= kEidMaxNodes) {
-    int16_t* eid = reinterpret_cast<int16_t*>(after);
+    int16_t* eid = reinterpret_cast<int16_t*>(smem + off);
     for (int i = threadIdx.x; i < g.n * g.n; i += blockDim.x) eid[i] = -1;
     __syncthreads();
     for (int e = threadIdx.x; e < g.N; e += blockDim.x) {
@@ -173,37 +310,57 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
       eid[ev[e] * g.n + eu[e]] = (int16_t)e;
     }
     g.eid = eid;
-    after += align16(2 * (size_t)g.n * g.n);
+    off += align16(2 * (size_t)g.n * g.n);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, warps = blockDim.x >> 5;
-  uint8_t* mine = after + (size_t)warp * (warp_scratch<W>(g.N, g.n) + 16);
-  mine = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mine) + 15) & ~uintptr_t(15));
+  uint8_t* mine = smem + off + (size_t)warp * warp_scratch<W>(g.N, g.n);
   uint8_t* x = mine;
-  int16_t* par = reinterpret_cast<int16_t*>(mine + align16(g.N));
-  uint32_t* onpath = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(par) + align16(2 * g.n));
+  int32_t* par = reinterpret_cast<int32_t*>(mine + align16(g.N));
+  uint32_t* onpath = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(par) + align16(4 * g.n));
   uint32_t* adj = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(onpath) +
                                               align16(4 * ((g.N + 31) / 32)));
   uint32_t* levels = adj + g.n * W;
   const int M = d.n_states;
 
   for (int64_t b = (int64_t)blockIdx.x * warps + warp; b < B; b += (int64_t)gridDim.x * warps) {
+    BPROF_T(s0);
+    BPROF_ADD(0, 1);
     const uint8_t* src = x0 + b * g.N;
     for (int e = lane; e < g.N; e += 32) x[e] = src[e];
-    for (int v = lane; v < g.n; v += 32) par[v] = (int16_t)v;
+    for (int v = lane; v < g.n; v += 32) par[v] = v;
     __syncwarp();
-    // initial Phi(x0): connectivity of G_L by union-find (lane 0)
-    int connected = 0;
-    if (lane == 0) {
-      for (int e = 0; e < g.N; ++e) {
+    // initial Phi(x0): components of G_L by warp-parallel min-label propagation
+    // with pointer jumping; the converged labels (component minimum, roots point
+    // to themselves) are a depth-1 union-find forest for the lower-side walk
+    BPROF_T(i0);
+    while (true) {
+      bool changed = false;
+      for (int e = lane; e < g.N; e += 32) {
         if (x[e] >= L) {
-          const int a = uf_find(par, eu[e]), c = uf_find(par, ev[e]);
-          if (a != c) par[a] = (int16_t)c;
+          const int a = par[eu[e]], c = par[ev[e]];
+          if (a != c) {
+            const int m = a < c ? a : c;
+            atomicMin(&par[eu[e]], m);
+            atomicMin(&par[ev[e]], m);
+            atomicMin(&par[a], m);
+            atomicMin(&par[c], m);
+            changed = true;
+          }
         }
       }
-      connected = uf_find(par, g.s) == uf_find(par, g.t);
+      __syncwarp();
+      for (int v = lane; v < g.n; v += 32) {
+        int r = par[v];
+        while (par[r] != r) r = par[r];
+        par[v] = r;
+      }
+      __syncwarp();
+      if (!__any_sync(kFull, changed)) break;
     }
-    connected = __shfl_sync(kFull, connected, 0);
+    const int connected = par[g.s] == par[g.t];
+    BPROF_T(i1);
+    BPROF_ADD(6, i1 - i0);
     int64_t calls = 1;
     if (!connected) {
       // ---------------- lower side: union-find, no Phi evaluation needed
@@ -223,7 +380,7 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
             x[n] = (uint8_t)(L - 1);  // crossing: reverted, walk moves to n + 1
             continue;
           }
-          if (a != c) par[a] = (int16_t)c;
+          if (a != c) par[a] = c;
           calls += M - 1 - L;
           x[n] = (uint8_t)(M - 1);
         }
@@ -240,57 +397,13 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
         }
       }
       __syncwarp();
-      int dd = bfs_layers<W>(adj, levels, g.n, g.s, g.t, lane);
-      trace_path<W>(g, adj, levels, dd, onpath, lane);
-      for (int n = 0; n < g.N; ++n) {
-        const int xn = x[n];
-        if (xn == 0) continue;
-        if (xn < L) {  // not in G_L: every step down leaves G_L unchanged
-          calls += xn;
-          if (lane == 0) x[n] = 0;
-          continue;
-        }
-        calls += xn - L + 1;  // steps down to L-1, the last one removes edge n
-        const bool on = (onpath[n >> 5] >> (n & 31)) & 1u;
-        if (on) {
-          const int u = eu[n], v = ev[n];
-          toggle_edge(adj, W, u, v, lane);
-          // cheap witness repair first: a common neighbour w of u and v turns
-          // the path into a walk through (u,w),(w,v) that still contains an s-t
-          // path (the witness may be a superset of a path: a later test of one
-          // of its edges then just runs the exact BFS below)
-          int wn = -1;
-#pragma unroll
-          for (int q = 0; q < W; ++q) {
-            const uint32_t c = adj[u * W + q] & adj[v * W + q];
-            if (wn < 0 && c) wn = 32 * q + __ffs(c) - 1;
-          }
-          if (wn >= 0 && g.eid) {
-            if (lane == 0) {
-              const int e1 = g.eid[u * g.n + wn], e2 = g.eid[wn * g.n + v];
-              onpath[n >> 5] &= ~(1u << (n & 31));
-              onpath[e1 >> 5] |= 1u << (e1 & 31);
-              onpath[e2 >> 5] |= 1u << (e2 & 31);
-            }
-            calls += L - 1;
-            if (lane == 0) x[n] = 0;
-            __syncwarp();
-            continue;
-          }
-          dd = bfs_layers<W>(adj, levels, g.n, g.s, g.t, lane);
-          if (dd == 0) {  // crossing: reverted, walk moves to n + 1
-            toggle_edge(adj, W, eu[n], ev[n], lane);
-            if (lane == 0) x[n] = (uint8_t)L;
-            __syncwarp();
-            continue;
-          }
-          trace_path<W>(g, adj, levels, dd, onpath, lane);
-        } else {
-          toggle_edge(adj, W, eu[n], ev[n], lane);
-        }
-        calls += L - 1;
-        if (lane == 0) x[n] = 0;
-        __syncwarp();
+      if constexpr (W <= 4) {
+        AdjReg<W> ra;
+        ra.load(adj, g.n, lane);
+        calls += upper_walk<W>(g, ra, x, levels, onpath, L, lane);
+      } else {
+        AdjSmem<W> sa{adj};
+        calls += upper_walk<W>(g, sa, x, levels, onpath, L, lane);
       }
     }
     __syncwarp();
@@ -301,15 +414,17 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
       out_calls[b] = calls;
     }
     __syncwarp();
+    BPROF_T(s1);
+    BPROF_ADD(7, s1 - s0);
   }
 }
 
 template <int W>
 int launch_graph(const rsr_phi_desc& d, int L, const uint8_t* x0, int64_t B, uint8_t* out_refs,
                  uint8_t* out_side, int64_t* out_calls, cudaStream_t st) {
-  const size_t fixed = 2 * sizeof(int32_t) * (size_t)d.n_components + 16 +
+  const size_t fixed = align16(2 * sizeof(int32_t) * (size_t)d.n_components) +
                        (d.n_nodes <= kEidMaxNodes ? align16(2 * (size_t)d.n_nodes * d.n_nodes) : 0);
-  const size_t per_warp = warp_scratch<W>(d.n_components, d.n_nodes) + 16;
+  const size_t per_warp = warp_scratch<W>(d.n_components, d.n_nodes);
   int warps = (int)((160 * 1024 - fixed) / per_warp);
   if (warps > 4) warps = 4;
   if (warps < 1) return -1;
@@ -324,6 +439,17 @@ int launch_graph(const rsr_phi_desc& d, int L, const uint8_t* x0, int64_t B, uin
 }
 
 }  // namespace
+
+#ifdef RSR_FP4_PROF
+extern "C" int rsr_boundary_prof(unsigned long long* host8, int reset) {
+  RSR_CUDA(cudaMemcpyFromSymbol(host8, g_bprof, sizeof(g_bprof)));
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    RSR_CUDA(cudaMemcpyToSymbol(g_bprof, z, sizeof(z)));
+  }
+  return RSR_OK;
+}
+#endif
 
 namespace rsr {
 

@@ -26,6 +26,18 @@ __device__ __forceinline__ void fp4_sample_word(const uint8_t* x, int w, int M, 
     up = lo ^ 0x22222222u;        // [x < 1]
     return;
   }
+  if (M == 3 && c0 + 8 <= kdim) {
+    // 4 states (0..2) -> 4 bytes, one per component: nibbles [x<1], [x<2] (A_up)
+    // and [x>=1], [x>=2] (A_lo), by byte permutes over 3-entry tables
+    const int n0 = c0 / 2;
+    uint32_t a = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a |= (uint32_t)x[n0 + j] << (8 * j);
+    const uint32_t sel = (a & 0xFu) | ((a >> 4) & 0xF0u) | ((a >> 8) & 0xF00u) | ((a >> 12) & 0xF000u);
+    up = __byte_perm(0x00002022u, 0u, sel);  // x = 0, 1, 2 -> 0x22, 0x20, 0x00
+    lo = __byte_perm(0x00220200u, 0u, sel);  // x = 0, 1, 2 -> 0x00, 0x02, 0x22
+    return;
+  }
   up = lo = 0;
   int n = c0 / (M - 1), k = c0 - n * (M - 1) + 1;
 #pragma unroll

@@ -123,7 +123,7 @@ sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uin
 // aligned) and the FP4 rows [A_up | A_lo] (whole 32-bit words) coalesced.
 constexpr int kRowsPerCta = 64;
 
-template <bool M2>
+template <int MT>  // 2, 3: specialised state count; 0: any M
 __global__ void __launch_bounds__(kThreads)
 sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
                    int64_t start_row, int64_t count, uint8_t* __restrict__ states,
@@ -154,8 +154,10 @@ sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed
       if (o >= 0 && o < span) {
         const unsigned long long r = w[j] >> 11;
         int s;
-        if (M2) {
+        if (MT == 2) {
           s = r >= T[n] ? 1 : 0;
+        } else if (MT == 3) {
+          s = (r >= T[2 * n] ? 1 : 0) + (r >= T[2 * n + 1] ? 1 : 0);
         } else {
           s = 0;
           const unsigned long long* Tn = T + n * (M - 1);
@@ -425,7 +427,7 @@ extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_state
   const size_t smem =
       ((size_t)N * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 + (size_t)kRowsPerCta * N;
   RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample_fp4: N*(M-1) too large for shared memory");
-  auto kern = M == 2 ? sample_rows_kernel<true> : sample_rows_kernel<false>;
+  auto kern = M == 2 ? sample_rows_kernel<2> : M == 3 ? sample_rows_kernel<3> : sample_rows_kernel<0>;
   if (smem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)rsr::ceil_div(count, kRowsPerCta), kThreads, smem, rsr::as_stream(stream)>>>(
