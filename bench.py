@@ -393,13 +393,15 @@ def run_ours(args):
             tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
             dt = float(t.item())
         assert list(c) == final_counts[:3] or world > 1
+        e2e_packed = e2e_encoded_input(args, batch, lower, upper, S, K, world, comm, dev)
         e2e = {"value": world * S * K * args.steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": S * N_COMP, "d2h_bytes_per_step": S + 32,
                "ms_per_step": 1e3 * dt / args.steps,
                "api": "paper_2604_17066_b200.classify.classify_host (pinned host uint8 states -> "
                       "labels), chunked H2D overlapped with " +
                       ("rsr_encode_samples + rsr_classify_tc" if e2e_method == "tc8" else
-                       "rsr_encode_samples_fp4 + rsr_classify_fp4")}
+                       "rsr_encode_samples_fp4 + rsr_classify_fp4"),
+               "encoded_input": e2e_packed}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -433,6 +435,50 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
+
+
+def e2e_encoded_input(args, batch, lower, upper, S, K, world, comm, dev):
+    """Same metric end to end when the host holds the samples in the reference's
+    own classification input format, EncodedBatch(kind="sample").packed
+    (encoding.py:82-98: packed one-hot rows, 74 B/row at N=295, M=2):
+    pinned host rows -> chunked H2D -> rsr_unpack_onehot_fp4 + rsr_classify_fp4
+    -> labels D2H (classify.classify_host_encoded)."""
+    import torch
+    from paper_2604_17066_b200 import _abi
+    from paper_2604_17066_b200.classify import classify_host_encoded
+    if args.method == "tc8":
+        return None
+    m = 2
+    rows = torch.empty((S, N_COMP * m), dtype=torch.uint8, device=dev)
+    _abi.call("rsr_encode_rows", _abi.ptr(batch.device_states()), S, N_COMP, m, 0, _abi.ptr(rows),
+              _abi.stream_ptr())
+    nb = (N_COMP * m + 7) // 8
+    pk = torch.empty((S, nb), dtype=torch.uint8, device=dev)
+    _abi.call("rsr_packbits_rows", _abi.ptr(rows), S, N_COMP * m, 0, _abi.ptr(pk), _abi.stream_ptr())
+    del rows
+    host = torch.empty((S, nb), dtype=torch.uint8, pin_memory=True)
+    host.copy_(pk)
+    del pk
+    out = torch.empty(S, dtype=torch.uint8, pin_memory=True)
+    for _ in range(2):
+        classify_host_encoded(host, N_COMP, lower, upper, m, labels_out=out)
+    torch.cuda.synchronize()
+    comm.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        classify_host_encoded(host, N_COMP, lower, upper, m, labels_out=out)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as tdist
+        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": world * S * K * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": S * nb,
+            "d2h_bytes_per_step": S + 32, "ms_per_step": 1e3 * dt / args.steps,
+            "api": "paper_2604_17066_b200.classify.classify_host_encoded (pinned host rows of "
+                   "EncodedBatch(kind='sample').packed, the reference's classification input "
+                   "(encoding.py:82-98, classify.py:42-44) -> labels)"}
 
 
 # --------------------------------------------------------------- full loops

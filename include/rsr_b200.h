@@ -162,6 +162,12 @@ int rsr_classify_tc_explain(const int8_t* A, int64_t S, const int8_t* B_lower,
 int rsr_fp4_row_bytes(int n_components, int n_states);
 int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int n_components,
                            int n_states, uint8_t* out, int row_bytes, void* stream);
+/* FP4 sample operand from the reference's classification input: rows of
+ * EncodedBatch(kind="sample").packed (encoding.py:82-98, np.packbits of the
+ * one-hot N x M rows, MSB first, ceil(N*M/8) bytes per row; each component's
+ * M bits must hold exactly one 1).  out: [count x 2*row_bytes]. */
+int rsr_unpack_onehot_fp4(const uint8_t* packed, int64_t count, int n_components, int n_states,
+                          uint8_t* out, int row_bytes, void* stream);
 int rsr_encode_refs_fp4(const uint8_t* states, int64_t count, int64_t rows_total,
                         int n_components, int n_states, int side, uint8_t* out,
                         int row_bytes, void* stream);

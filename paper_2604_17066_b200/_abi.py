@@ -75,6 +75,7 @@ EXPORTED = {
     "rsr_fp4_row_bytes": (_I, [_I, _I]),
     "rsr_encode_samples_fp4": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "rsr_encode_refs_fp4": (_I, [_P, _I64, _I64, _I, _I, _I, _P, _I, _P]),
+    "rsr_unpack_onehot_fp4": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "rsr_classify_fp4": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _I, _P]),
     "rsr_classify_fp4_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),

@@ -41,7 +41,7 @@ if TYPE_CHECKING:  # pragma: no cover
     pass
 
 __all__ = ["ClassificationResult", "InconsistentReferenceSets", "violation_counts", "classify",
-           "cov", "DEFAULT_CHUNK_SIZE", "classify_flags"]
+           "cov", "DEFAULT_CHUNK_SIZE", "classify_flags", "classify_host", "classify_host_encoded"]
 
 DEFAULT_CHUNK_SIZE = 65536
 # widest thermometer row the tensor-core kernel keeps resident (6 x 128 bytes);
@@ -302,13 +302,60 @@ def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSe
         raise ValueError("states must be a uint8 S x N host matrix")
     if method not in ("tc", "tc8"):
         raise ValueError("method must be 'tc' or 'tc8'")
-    S, N = host.shape
+    return _classify_host_stream(host, host.shape[1], n_states, lower_set, upper_set, chunk_rows,
+                                 labels_out, "tc8" if method == "tc8" else "states")
+
+
+def classify_host_encoded(packed, n_components: int, lower_set: ReferenceSet | None,
+                          upper_set: ReferenceSet | None, n_states: int, *,
+                          chunk_rows: int = 1 << 17,
+                          labels_out: torch.Tensor | None = None
+                          ) -> tuple[torch.Tensor, tuple[int, int, int]]:
+    """Classify host samples given in the reference's own classification input:
+    rows of ``encode_batch(states, M, "sample").packed`` (encoding.py:82-98, the
+    packed one-hot rows classify.py:42-44 consumes; ceil(N*M/8) bytes per row).
+    Same streaming as ``classify_host``; the device decodes each chunk straight
+    into the FP4 operand (rsr_unpack_onehot_fp4)."""
+    host = packed if isinstance(packed, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(packed))
+    m_eff = max(2, n_states)
+    if host.dtype != torch.uint8 or host.dim() != 2 or host.shape[1] != (n_components * m_eff + 7) // 8:
+        raise ValueError("packed must be a uint8 S x ceil(N*M/8) host matrix")
+    return _classify_host_stream(host, n_components, n_states, lower_set, upper_set, chunk_rows,
+                                 labels_out, "onehot")
+
+
+_STREAM_CACHE: dict = {}
+
+
+def _stream_buffers(dev, chunk, width_in, opnd_shape, opnd_dtype):
+    """Copy stream, double buffers and events of the host-fed path, reused across
+    calls with the same geometry (creating them per call costs more than a chunk)."""
+    key = (dev.index, chunk, width_in, opnd_shape, opnd_dtype)
+    ent = _STREAM_CACHE.get(key)
+    if ent is None:
+        if len(_STREAM_CACHE) > 4:
+            _STREAM_CACHE.clear()
+        ent = (torch.cuda.Stream(),
+               [torch.empty((chunk, width_in), dtype=torch.uint8, device=dev) for _ in range(2)],
+               [torch.empty((chunk,) + opnd_shape, dtype=opnd_dtype, device=dev) for _ in range(2)],
+               [torch.cuda.Event() for _ in range(2)], [torch.cuda.Event() for _ in range(2)])
+        _STREAM_CACHE[key] = ent
+    # the previous call's copies and kernels must be done with the buffers
+    ent[0].wait_stream(torch.cuda.current_stream())
+    return ent
+
+
+def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, labels_out, mode):
+    S = host.shape[0]
+    width_in = host.shape[1]
     dev = _device.device()
     m_eff = max(2, n_states)
     for s in (lower_set, upper_set):
         if s is not None and len(s) and s.max_state >= m_eff:
             raise ValueError(f"states must lie in [0, {n_states - 1}]")
-    fp4 = method == "tc" and _abi.fp4_row_bytes(N, m_eff) <= _abi.FP4_MAX_ROW_BYTES
+    fp4 = mode != "tc8" and _abi.fp4_row_bytes(N, m_eff) <= _abi.FP4_MAX_ROW_BYTES
+    if mode == "onehot" and not fp4:
+        raise ValueError("encoded input needs the FP4 classifier (N(M-1) <= 831)")
     if fp4:
         width = _abi.fp4_row_bytes(N, m_eff)
         opnd_shape, opnd_dtype = (2 * width,), torch.uint8
@@ -322,12 +369,8 @@ def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSe
         bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
         bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
     comp = torch.cuda.current_stream()
-    copy = torch.cuda.Stream()
     chunk = max(1, min(chunk_rows, S))
-    bufs = [torch.empty((chunk, N), dtype=torch.uint8, device=dev) for _ in range(2)]
-    opnd = [torch.empty((chunk,) + opnd_shape, dtype=opnd_dtype, device=dev) for _ in range(2)]
-    ready = [torch.cuda.Event() for _ in range(2)]
-    free = [torch.cuda.Event() for _ in range(2)]
+    copy, bufs, opnd, ready, free = _stream_buffers(dev, chunk, width_in, opnd_shape, opnd_dtype)
     flags = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
     st = _device.stream()
     for i, lo in enumerate(range(0, S, chunk)):
@@ -339,14 +382,19 @@ def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSe
             bufs[slot][: hi - lo].copy_(host[lo:hi], non_blocking=True)
             ready[slot].record(copy)
         comp.wait_event(ready[slot])
-        if fp4:
+        if mode == "onehot":
+            _abi.call("rsr_unpack_onehot_fp4", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
+                      _abi.ptr(opnd[slot]), width, st)
+        elif fp4:
             _abi.call("rsr_encode_samples_fp4", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
                       _abi.ptr(opnd[slot]), width, st)
-            _abi.call("rsr_classify_fp4", _abi.ptr(opnd[slot]), hi - lo, _abi.ptr(bl), nl,
-                      _abi.ptr(bu), nu, width, _abi.ptr(flags[lo:hi]), 0, st)
         else:
             _abi.call("rsr_encode_samples", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
                       _abi.ptr(opnd[slot]), width, st)
+        if fp4:
+            _abi.call("rsr_classify_fp4", _abi.ptr(opnd[slot]), hi - lo, _abi.ptr(bl), nl,
+                      _abi.ptr(bu), nu, width, _abi.ptr(flags[lo:hi]), 0, st)
+        else:
             _abi.call("rsr_classify_tc", _abi.ptr(opnd[slot]), hi - lo, _abi.ptr(bl), nl,
                       _abi.ptr(bu), nu, width, _abi.ptr(flags[lo:hi]), 0, st)
         free[slot].record(comp)

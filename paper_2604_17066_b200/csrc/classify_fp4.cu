@@ -707,6 +707,115 @@ __global__ void __launch_bounds__(256) encode_samples_fp4_kernel(
   }
 }
 
+// Sample operand from the reference's own classification input: rows of
+// EncodedBatch(kind="sample").packed (encoding.py:82-98: np.packbits of the
+// one-hot N x M rows, MSB first).  One warp per row: the packed row is staged
+// in shared memory, decoded to states (x_n = position of the set bit of
+// component n), then encoded exactly like encode_samples_fp4_kernel.
+__global__ void __launch_bounds__(256) unpack_onehot_fp4_kernel(
+    const uint8_t* __restrict__ packed, int64_t count, int N, int M, int in_bytes,
+    uint8_t* __restrict__ out, int row_bytes, int kdim, int stage_bytes) {
+  extern __shared__ uint8_t stage[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* pk = stage + warp * stage_bytes;
+  uint8_t* xs = pk + (in_bytes + 15) / 16 * 16;
+  const int words = row_bytes / 4;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < count; i += (int64_t)gridDim.x * 8) {
+    const uint8_t* src = packed + i * in_bytes;
+    for (int b = lane; b < in_bytes; b += 32) pk[b] = src[b];
+    __syncwarp();
+    for (int n = lane; n < N; n += 32) {
+      int x = 0;
+      for (int m = 0; m < M; ++m) {
+        const int j = n * M + m;
+        if ((pk[j >> 3] >> (7 - (j & 7))) & 1) x = m;
+      }
+      xs[n] = (uint8_t)x;
+    }
+    __syncwarp();
+    uint32_t* up_row = reinterpret_cast<uint32_t*>(out + i * (int64_t)(2 * row_bytes));
+    uint32_t* lo_row = up_row + words;
+    for (int w = lane; w < words; w += 32) {
+      uint32_t up, lo;
+      rsr::fp4_sample_word(xs, w, M, kdim, up, lo);
+      up_row[w] = up;
+      lo_row[w] = lo;
+    }
+    __syncwarp();
+  }
+}
+
+// M = 2 fast path: a block converts kUnpackRows rows.  The rows' packed
+// bytes are one contiguous span, staged in shared memory with aligned 16-byte
+// loads (the per-thread byte loads of a naive version leave too few bytes in
+// flight to reach HBM speed).  Word w of a row is elements 8w..8w+7 = one-hot
+// bit pairs 16w..16w+15 = packed bytes 2w, 2w+1 (MSB first): bit 2n is
+// [x_n == 0] = A_up, bit 2n+1 is [x_n == 1] = A_lo.
+constexpr int kUnpackRows = 128;
+
+__global__ void __launch_bounds__(256) unpack_onehot_fp4_m2_kernel(
+    const uint8_t* __restrict__ packed, int64_t rows, int in_bytes, uint8_t* __restrict__ out,
+    int words, int kdim) {
+  extern __shared__ __align__(16) uint8_t span[];
+  const int64_t r0 = (int64_t)blockIdx.x * kUnpackRows;
+  const int nr = (int)(rows - r0 < kUnpackRows ? rows - r0 : kUnpackRows);
+  const int64_t beg = r0 * in_bytes, end = beg + (int64_t)nr * in_bytes;
+  const int64_t abeg = beg & ~(int64_t)15;
+  const int nvec = (int)((end - abeg + 15) >> 4);
+  const int64_t total = rows * in_bytes;
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const int64_t off = abeg + 16 * (int64_t)v;
+    if (off + 16 <= total) {
+      reinterpret_cast<uint4*>(span)[v] = *reinterpret_cast<const uint4*>(packed + off);
+    } else {
+      for (int j = 0; j < 16; ++j) span[16 * v + j] = off + j < total ? packed[off + j] : 0;
+    }
+  }
+  __syncthreads();
+  const int shift = (int)(beg - abeg);
+  // (r, w) of flat index t, advanced incrementally (no division per word)
+  int r = threadIdx.x / words, w = threadIdx.x - (threadIdx.x / words) * words;
+  const int dr = blockDim.x / words, dw = blockDim.x - dr * words;
+  for (; r < nr; r += dr, w += dw) {
+    if (w >= words) {
+      w -= words;
+      ++r;
+      if (r >= nr) break;
+    }
+    const uint8_t* src = span + shift + r * in_bytes;
+    uint32_t up = 0, lo = 0;
+    const int c0 = 8 * w;
+    if (c0 + 8 <= kdim) {
+      const uint32_t b0 = src[2 * w], b1 = src[2 * w + 1];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        up |= ((b0 >> (7 - 2 * j)) & 1u) << (4 * j + 1);
+        lo |= ((b0 >> (6 - 2 * j)) & 1u) << (4 * j + 1);
+        up |= ((b1 >> (7 - 2 * j)) & 1u) << (4 * j + 17);
+        lo |= ((b1 >> (6 - 2 * j)) & 1u) << (4 * j + 17);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = c0 + j;
+        uint32_t u, l;
+        if (c < kdim) {
+          const int bu = 2 * c, bl = 2 * c + 1;
+          u = (src[bu >> 3] >> (7 - (bu & 7))) & 1u;
+          l = (src[bl >> 3] >> (7 - (bl & 7))) & 1u;
+        } else {
+          u = l = (c == kdim);
+        }
+        up |= (u ? 0x2u : 0u) << (4 * j);
+        lo |= (l ? 0x2u : 0u) << (4 * j);
+      }
+    }
+    uint32_t* row = reinterpret_cast<uint32_t*>(out + (r0 + r) * (int64_t)(8 * words));
+    row[w] = up;
+    row[words + w] = lo;
+  }
+}
+
 // Reference operand rows: upper [r_n >= k], lower [r_n < k], bias column 0;
 // rows [count, rows_total) are never-hit pad rows (bias column 1).
 __global__ void encode_refs_fp4_kernel(const uint8_t* __restrict__ states, int64_t count,
@@ -806,4 +915,35 @@ extern "C" int rsr_classify_fp4_explain(const uint8_t* A, int64_t S, const uint8
                                         int64_t* first_upper, int accumulate, void* stream) {
   return classify_fp4_impl(A, S, B_lower, n_lower, B_upper, n_upper, row_bytes, flags,
                            first_lower, first_upper, accumulate, stream);
+}
+
+extern "C" int rsr_unpack_onehot_fp4(const uint8_t* packed, int64_t count, int n_components,
+                                     int n_states, uint8_t* out, int row_bytes, void* stream) {
+  const int N = n_components, M = n_states;
+  RSR_REQUIRE(N >= 1 && M >= 2 && M <= 255 && count >= 0, "rsr_unpack_onehot_fp4: bad shape");
+  RSR_REQUIRE(row_bytes == rsr_fp4_row_bytes(N, M), "rsr_unpack_onehot_fp4: row_bytes must be %d",
+              rsr_fp4_row_bytes(N, M));
+  if (count == 0) return RSR_OK;
+  RSR_REQUIRE(packed != nullptr && out != nullptr, "rsr_unpack_onehot_fp4: null pointer");
+  const int in_bytes = (N * M + 7) / 8;
+  if (M == 2) {
+    const size_t span = ((size_t)kUnpackRows * in_bytes + 31) / 16 * 16;
+    if (span > 48 * 1024)
+      RSR_CUDA(cudaFuncSetAttribute(unpack_onehot_fp4_m2_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)span));
+    unpack_onehot_fp4_m2_kernel<<<(unsigned)rsr::ceil_div(count, kUnpackRows), 256, span,
+                                   rsr::as_stream(stream)>>>(packed, count, in_bytes, out,
+                                                             row_bytes / 4, N);
+    return rsr::check_launch("unpack_onehot_fp4_m2_kernel");
+  }
+  const int stage_bytes = (in_bytes + 15) / 16 * 16 + (N + 15) / 16 * 16;
+  const size_t smem = 8 * (size_t)stage_bytes;
+  if (smem > 48 * 1024)
+    RSR_CUDA(cudaFuncSetAttribute(unpack_onehot_fp4_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t grid = rsr::ceil_div(count, 8);
+  if (grid > 148 * 64) grid = 148 * 64;
+  unpack_onehot_fp4_kernel<<<(unsigned)grid, 256, smem, rsr::as_stream(stream)>>>(
+      packed, count, N, M, in_bytes, out, row_bytes, N * (M - 1), stage_bytes);
+  return rsr::check_launch("unpack_onehot_fp4_kernel");
 }

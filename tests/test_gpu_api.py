@@ -334,3 +334,26 @@ def test_multistate_pmf_golden():
     assert rep.pmf.tolist() == g["pmf"]
     assert rep.cumulative_lower.tolist() == g["cumulative_lower"]
     assert rep.max_chain_discrepancy == g["max_chain_discrepancy"]
+
+
+@pytest.mark.parametrize("n,m,s", [(295, 2, 5000), (40, 3, 3000), (7, 5, 700)])
+def test_classify_host_paths_match(n, m, s):
+    # host-fed streaming paths (u8 states, reference packed one-hot rows, int8 variant)
+    # give the same labels as the device batch path and the oracle
+    from paper_2604_17066_b200.classify import classify_host, classify_host_encoded
+    rng = np.random.default_rng(n + m)
+    samples = rng.integers(0, m, size=(s, n))
+    lower = np.clip(samples[rng.integers(0, s, 300)] + rng.integers(0, 2, (300, n)), 0, m - 1)
+    upper = np.clip(samples[rng.integers(0, s, 200)] - rng.integers(0, 2, (200, n)), 0, m - 1)
+    want = oracle.classify_labels(samples, lower, upper, m)["labels"]
+    lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
+    u8 = samples.astype(np.uint8)
+    lab, counts = classify_host(u8, lo, up, m, chunk_rows=1024)
+    assert np.array_equal(lab.numpy(), want)
+    assert counts == (int((want == 0).sum()), int((want == 1).sum()), int((want == 2).sum()))
+    lab8, _ = classify_host(u8, lo, up, m, chunk_rows=777, method="tc8")
+    assert np.array_equal(lab8.numpy(), want)
+    packed = np.packbits(oracle.encode(samples, m, "sample"), axis=1)
+    labp, countsp = classify_host_encoded(packed, n, lo, up, m, chunk_rows=1000)
+    assert np.array_equal(labp.numpy(), want) and countsp == counts

@@ -58,3 +58,22 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def classify_m3():
+    """FP4 classifier at M = 3 (cfg5 shape): 2^20 x 2 x 10^4 refs, ops = 2 N (M-1) per pair."""
+    from paper_2604_17066_b200.classify import classify_flags
+    torch.cuda.set_device(0)
+    n, m, k = 295, 3, 10_000
+    rng = np.random.default_rng(5)
+    d = P.ComponentDistribution.iid(n, [0.05, 0.15, 0.8])
+    batch = P.sample_batch(d, 1 << 20, 0, 0)
+    lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, rng.integers(1, 3, size=(k, n)), trusted=True)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, rng.integers(0, 2, size=(k, n)), trusted=True)
+    ms = timed(lambda: classify_flags(batch, lo, up, m))
+    tops = (1 << 20) * 2 * k * 2 * n * (m - 1) / ms / 1e9
+    print(f"classify fp4 M=3 2^20 x 2x10^4: {ms:.3f} ms = {tops:.0f} TOPS = {tops / 9000:.3f} of FP4 peak")
+
+
+if __name__ == "__main__" and os.environ.get("CLASSIFY_M3"):
+    classify_m3()
