@@ -116,11 +116,22 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
+_CUDA_OK: bool | None = None
+_DEVICES: dict[int, torch.device] = {}
+
+
 def require_device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("the RSR hot path runs on CUDA devices only (no CPU fallback); "
-                           "torch.cuda.is_available() is False")
-    return torch.device("cuda", torch.cuda.current_device())
+    global _CUDA_OK
+    if not _CUDA_OK:  # checked once; torch.cuda.is_available() is slow in hot loops
+        _CUDA_OK = torch.cuda.is_available()
+        if not _CUDA_OK:
+            raise RuntimeError("the RSR hot path runs on CUDA devices only (no CPU fallback); "
+                               "torch.cuda.is_available() is False")
+    idx = torch._C._cuda_getDevice()
+    dev = _DEVICES.get(idx)
+    if dev is None:
+        dev = _DEVICES[idx] = torch.device("cuda", idx)
+    return dev
 
 
 def call(name: str, *args) -> int:
@@ -138,8 +149,11 @@ def call(name: str, *args) -> int:
 
 
 def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    # raw cudaStream_t of the current stream without torch.cuda.current_stream()'s
+    # per-call device-index bookkeeping (this runs once per library call)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def ptr(t: torch.Tensor | None) -> int | None:
