@@ -55,6 +55,12 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 #ifndef RSR_FP4_EPI_WARPS
 #define RSR_FP4_EPI_WARPS 8
 #endif
+#ifndef RSR_FP4_GROUP_RELEASE
+#define RSR_FP4_GROUP_RELEASE 0
+#endif
+#ifndef RSR_FP4_SPIN
+#define RSR_FP4_SPIN 0
+#endif
 #ifndef RSR_FP4_TILE_N
 #define RSR_FP4_TILE_N 240
 #endif
@@ -220,7 +226,13 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_b
 #endif
   tc_fence_before();
   __syncwarp();
+#if RSR_FP4_GROUP_RELEASE
+  // one arrival per CTA after a named barrier of its epilogue warps
+  named_bar_sync(2, 32 * kEpiWarps);
+  if (threadIdx.x == 128) mbar_arrive_leader(release_bar);
+#else
   if (lane == 0) mbar_arrive_leader(release_bar);
+#endif
   if (valid < c0 + kCols) {
 #pragma unroll
     for (int c = 0; c < kCols; ++c)
@@ -289,7 +301,8 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     for (int i = 0; i < kBufs; ++i) {
       mbar_init(smem_addr(&t_full[i]), 1);
-      mbar_init(smem_addr(&t_empty[i]), 2 * kEpiWarps);  // every epilogue warp of both CTAs
+      // every epilogue warp of both CTAs (or one arrival per CTA)
+      mbar_init(smem_addr(&t_empty[i]), RSR_FP4_GROUP_RELEASE ? 2 : 2 * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -425,7 +438,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
           const uint32_t d = tm0 + buf * kTileN;
           const uint32_t bl = b_lo0 + (uint32_t)bs * (b_stage_bytes >> 4);
           PROF_T(m0);
+#if RSR_FP4_SPIN
+          mbar_spin(bar_t_empty + 8 * buf, tphase ^ 1);
+#else
           mbar_wait(bar_t_empty + 8 * buf, tphase ^ 1);
+#endif
           PROF_T(m1);
           mbar_wait(bar_b_full + 8 * bs, bpar);
           PROF_T(m2);

@@ -53,6 +53,27 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (!mbar_try(bar, parity)) mbar_wait_slow(bar, parity);
 }
 
+// Non-suspending probe of a phase (mbarrier.test_wait).
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
+// Spin-wait (no suspension: lowest wake-up latency, for a single latency-
+// critical warp); falls back to the watchdog loop after many probes.
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+  for (int i = 0; i < 4096; ++i)
+    if (mbar_test(bar, parity)) return;
+  mbar_wait_slow(bar, parity);
+}
+
 // Remote (or local) arrive on the pair leader's copy of a barrier: clearing
 // bit 24 of a shared::cluster address selects CTA rank 0 of the CTA pair.
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
