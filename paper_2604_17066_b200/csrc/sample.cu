@@ -10,6 +10,8 @@
 // (exact), u >= cum  <=>  r >= ceil(cum * 2^53) (scaling by 2^53 is exact), so
 // state = #{m < M-1 : r >= T_m} with T_m = ceil(cumsum(probs[n])[m] * 2^53).
 // The clip to M-1 (sampling.py:89) is implied by counting only m < M-1.
+#include <algorithm>
+
 #include "common.cuh"
 #include "fp4_encode.cuh"
 #include "philox.cuh"
@@ -120,74 +122,180 @@ sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uin
 // overlaps the rows' flat draw range (blocks straddling two CTAs are computed
 // by both, each keeping its own draws), drop the states into shared memory,
 // then write the uint8 state rows (16-byte stores: the chunk is 32-row
-// aligned) and the FP4 rows [A_up | A_lo] (whole 32-bit words) coalesced.
+// aligned) and the FP4 rows [A_up | A_lo] (16-byte stores, 4 words a thread).
+//
+// The generator is bound by the 64-bit multiplies of Philox4x64-10 on the FMA
+// pipe (tools/philox_rate.cu: 0.79 ms per 2^20 x 295 draws for the bare
+// generator), so the rest is kept off that pipe and branch-free: the
+// threshold table has N + 3 rows (row n >= N repeats row n - N) so a block's
+// four draws index T without a wrap test, interior blocks store their four
+// states as one 32-bit word, and the FP4 pass reads each row segment with
+// aligned 32-bit loads + funnel shifts and converts 8 states per word with a
+// few shifts and one byte permute.
 constexpr int kRowsPerCta = 64;
+constexpr int kRowThreads = 256;
+constexpr int kTExtra = 3;  // extra threshold rows (no wrap within a block)
+#ifndef RSR_SAMPLE_MINB
+#define RSR_SAMPLE_MINB 3
+#endif
 
-template <int MT>  // 2, 3: specialised state count; 0: any M
-__global__ void __launch_bounds__(kThreads)
-sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
-                   int64_t start_row, int64_t count, uint8_t* __restrict__ states,
-                   uint8_t* __restrict__ fp4, int row_bytes) {
-  extern __shared__ __align__(16) unsigned long long T[];
-  load_thresholds(probs, N, M, T);
-  // [rows][N] states, 16-byte aligned after the threshold table
-  uint8_t* st = reinterpret_cast<uint8_t*>(T) + ((size_t)N * (M - 1) * 8 + 15) / 16 * 16;
-  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
-  const int rows = (int)(count - r0 < kRowsPerCta ? count - r0 : kRowsPerCta);
-  const int64_t span = (int64_t)rows * N;                       // draws of this CTA
-  const int64_t f0 = (start_row + r0) * (int64_t)N;              // first flat draw
-  const int64_t b0 = f0 >> 2, b1 = (f0 + span - 1) >> 2;         // Philox blocks
-  // local draw offset of word 0 of this thread's first block, and its column;
-  // each further block of the thread is 4 * blockDim.x draws later
-  int o0 = (int)(4 * (b0 + threadIdx.x) - f0);
-  int n0 = (o0 + N) % N;
-  const int ostep = 4 * (int)blockDim.x, nstep = ostep % N;
-  for (int64_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x, o0 += ostep) {
-    uint64_t w[4];
-    rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
-    int n = n0;
-    n0 += nstep;
-    if (n0 >= N) n0 -= N;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int o = o0 + j;
-      if (o >= 0 && o < span) {
-        const unsigned long long r = w[j] >> 11;
-        int s;
-        if (MT == 2) {
-          s = r >= T[n] ? 1 : 0;
-        } else if (MT == 3) {
-          s = (r >= T[2 * n] ? 1 : 0) + (r >= T[2 * n + 1] ? 1 : 0);
-        } else {
-          s = 0;
-          const unsigned long long* Tn = T + n * (M - 1);
-          for (int m = 0; m < M - 1; ++m) s += (r >= Tn[m]) ? 1 : 0;
-        }
-        st[o] = (uint8_t)s;
-      }
-      if (++n == N) n = 0;
+__device__ void load_thresholds_ext(const double* __restrict__ probs, int N, int M,
+                                    unsigned long long* T) {
+  for (int n = threadIdx.x; n < N + kTExtra; n += blockDim.x) {
+    const int src = n % N;
+    double cum = 0.0;
+    for (int m = 0; m < M - 1; ++m) {
+      cum = __dadd_rn(cum, probs[(int64_t)src * M + m]);
+      T[n * (M - 1) + m] = (unsigned long long)ceil(__dmul_rn(cum, 9007199254740992.0));
     }
   }
   __syncthreads();
-  if (states) {
-    uint8_t* dst = states + r0 * (int64_t)N;
-    if (rows == kRowsPerCta) {  // 64 * N bytes, 16-byte aligned chunk
-      const int vecs = (int)(span / 16);
-      for (int i = threadIdx.x; i < vecs; i += blockDim.x)
-        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(st)[i];
-    } else {
-      for (int64_t i = threadIdx.x; i < span; i += blockDim.x) dst[i] = st[i];
+}
+
+// 8 consecutive state bytes starting at shared byte offset `base` (any
+// alignment) as two 32-bit words, from aligned loads + funnel shifts.
+template <int W>
+__device__ __forceinline__ void load_state_words(const uint8_t* st, uint32_t base, uint32_t* x) {
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(st + (base & ~3u));
+  const uint32_t sh = (base & 3u) * 8u;
+  uint32_t raw[W + 1];
+#pragma unroll
+  for (int k = 0; k <= W; ++k) raw[k] = wp[k];
+#pragma unroll
+  for (int k = 0; k < W; ++k) x[k] = __funnelshift_r(raw[k], raw[k + 1], sh);
+}
+
+// FP4 words of one quad (4 words = 32 elements) of a state row, fast paths
+// for quads wholly below kdim (M = 2: 8 states per word; M = 3: 4 states).
+template <int MT>
+__device__ __forceinline__ void fp4_quad_fast(const uint8_t* st, uint32_t base, uint32_t* u,
+                                              uint32_t* l) {
+  if (MT == 2) {
+    uint32_t x[8];
+    load_state_words<8>(st, base, x);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      // bytes (e0..e3), (e4..e7) of 0/1 -> nibble j = e_j at bit 4j+1
+      const uint32_t ta = x[2 * t] | (x[2 * t] >> 4), tb = x[2 * t + 1] | (x[2 * t + 1] >> 4);
+      l[t] = __byte_perm(ta, tb, 0x6420) << 1;  // [x >= 1]
+      u[t] = l[t] ^ 0x22222222u;               // [x <  1]
+    }
+  } else {
+    uint32_t x[4];
+    load_state_words<4>(st, base, x);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t a = x[t];
+      const uint32_t sel =
+          (a & 0xFu) | ((a >> 4) & 0xF0u) | ((a >> 8) & 0xF00u) | ((a >> 12) & 0xF000u);
+      u[t] = __byte_perm(0x00002022u, 0u, sel);  // x = 0, 1, 2 -> 0x22, 0x20, 0x00
+      l[t] = __byte_perm(0x00220200u, 0u, sel);  // x = 0, 1, 2 -> 0x00, 0x02, 0x22
     }
   }
-  if (fp4) {
-    const int words = row_bytes / 4, kdim = N * (M - 1);
-    for (int i = threadIdx.x; i < rows * words; i += blockDim.x) {
-      const int r = i / words, w = i - r * words;
-      uint32_t up, lo;
-      rsr::fp4_sample_word(st + r * N, w, M, kdim, up, lo);
-      uint32_t* row = reinterpret_cast<uint32_t*>(fp4 + (r0 + r) * (int64_t)(2 * row_bytes));
-      row[w] = up;
-      row[words + w] = lo;
+}
+
+// Persistent: each CTA computes the threshold table once, then walks chunks
+// of kRowsPerCta rows (chunk c = blockIdx.x + k * gridDim.x) with the state
+// staging buffer double-buffered, so one barrier per chunk separates the
+// generator phase from the store phase (the next chunk's generator writes the
+// other buffer).
+template <int MT>  // 2, 3: specialised state count; 0: any M
+__global__ void __launch_bounds__(kRowThreads, RSR_SAMPLE_MINB)
+sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
+                   int64_t start_row, int64_t count, uint8_t* __restrict__ states,
+                   uint8_t* __restrict__ fp4, int row_bytes, int st_bytes) {
+  extern __shared__ __align__(16) unsigned long long T[];
+  load_thresholds_ext(probs, N, M, T);
+  const int Mm1 = MT ? MT - 1 : M - 1;
+  // two [rows][N] state buffers (+16 B slack each for the funnel loads)
+  uint8_t* st_base =
+      reinterpret_cast<uint8_t*>(T) + ((size_t)(N + kTExtra) * Mm1 * 8 + 15) / 16 * 16;
+  const int kdim = N * Mm1, words = row_bytes / 4, quads = words / 4;
+  const int fastq = MT ? kdim / 32 : 0;  // quads per row on the specialised path
+  const int64_t n_chunks = (count + kRowsPerCta - 1) / kRowsPerCta;
+  int buf = 0;
+  for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x, buf ^= 1) {
+    uint8_t* st = st_base + buf * st_bytes;
+    const int64_t r0 = chunk * kRowsPerCta;
+    const int rows = (int)(count - r0 < kRowsPerCta ? count - r0 : kRowsPerCta);
+    const int span = rows * N;                                     // draws of this chunk
+    const int64_t f0 = (start_row + r0) * (int64_t)N;              // first flat draw
+    const int64_t b0 = f0 >> 2, b1 = (f0 + span - 1) >> 2;         // Philox blocks
+    const bool aligned = (f0 & 3) == 0;                            // o0 % 4 == 0 for all blocks
+    // local draw offset of word 0 of this thread's first block, and its column;
+    // each further block of the thread is 4 * blockDim.x draws later
+    int o0 = (int)(4 * (b0 + threadIdx.x) - f0);
+    int n0 = (o0 + N) % N;
+    const int ostep = 4 * (int)blockDim.x, nstep = ostep % N;
+    for (int64_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x, o0 += ostep) {
+      uint64_t w[4];
+      rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+      const unsigned long long* Tn = T + n0 * Mm1;
+      n0 += nstep;
+      if (n0 >= N) n0 -= N;
+      uint32_t s[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const unsigned long long r = w[j] >> 11;
+        const unsigned long long* Tj = Tn + j * Mm1;
+        if (MT == 2) {
+          s[j] = r >= Tj[0];
+        } else if (MT == 3) {
+          s[j] = (uint32_t)(r >= Tj[0]) + (uint32_t)(r >= Tj[1]);
+        } else {
+          uint32_t c = 0;
+          for (int m = 0; m < Mm1; ++m) c += r >= Tj[m];
+          s[j] = c;
+        }
+      }
+      if (o0 >= 0 && o0 + 4 <= span) {
+        if (aligned) {
+          *reinterpret_cast<uint32_t*>(st + o0) = s[0] | (s[1] << 8) | (s[2] << 16) | (s[3] << 24);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) st[o0 + j] = (uint8_t)s[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (o0 + j >= 0 && o0 + j < span) st[o0 + j] = (uint8_t)s[j];
+      }
+    }
+    __syncthreads();
+    if (states) {
+      uint8_t* dst = states + r0 * (int64_t)N;
+      if (rows == kRowsPerCta) {  // 64 * N bytes, 16-byte aligned chunk
+        const int vecs = span / 16;
+        for (int i = threadIdx.x; i < vecs; i += blockDim.x)
+          reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(st)[i];
+      } else {
+        for (int i = threadIdx.x; i < span; i += blockDim.x) dst[i] = st[i];
+      }
+    }
+    if (fp4) {
+      // items (row, quad): the specialised quads first, then the quads holding
+      // the bias column / zero padding (generic per-word encoder), in separate
+      // loops so a warp does not diverge between the two
+      const int nfast = rows * fastq, slowq = quads - fastq;
+      for (int i = threadIdx.x; MT != 0 && i < nfast; i += blockDim.x) {
+        const int r = i / (MT ? fastq : 1), q = i - r * fastq;
+        uint4 up, lo;
+        fp4_quad_fast<MT>(st, (uint32_t)(r * N + (MT == 2 ? 32 : 16) * q), &up.x, &lo.x);
+        uint8_t* row = fp4 + (r0 + r) * (int64_t)(2 * row_bytes);
+        reinterpret_cast<uint4*>(row)[q] = up;
+        reinterpret_cast<uint4*>(row + row_bytes)[q] = lo;
+      }
+      for (int i = threadIdx.x; i < rows * slowq; i += blockDim.x) {
+        const int r = i / slowq, q = fastq + (i - r * slowq);
+        uint4 up, lo;
+        uint32_t* u = &up.x;
+        uint32_t* l = &lo.x;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) rsr::fp4_sample_word(st + r * N, 4 * q + t, M, kdim, u[t], l[t]);
+        uint8_t* row = fp4 + (r0 + r) * (int64_t)(2 * row_bytes);
+        reinterpret_cast<uint4*>(row)[q] = up;
+        reinterpret_cast<uint4*>(row + row_bytes)[q] = lo;
+      }
     }
   }
 }
@@ -424,13 +532,23 @@ extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_state
   if (out_states)
     RSR_REQUIRE((reinterpret_cast<uintptr_t>(out_states) & 15) == 0,
                 "rsr_sample_fp4: out_states must be 16-byte aligned");
-  const size_t smem =
-      ((size_t)N * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 + (size_t)kRowsPerCta * N;
+  if (out_fp4)
+    RSR_REQUIRE((reinterpret_cast<uintptr_t>(out_fp4) & 15) == 0,
+                "rsr_sample_fp4: out_fp4 must be 16-byte aligned");
+  const int st_bytes = (kRowsPerCta * N + 16 + 15) / 16 * 16;  // + funnel-load slack
+  const size_t smem = ((size_t)(N + kTExtra) * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 +
+                      2 * (size_t)st_bytes;
   RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample_fp4: N*(M-1) too large for shared memory");
   auto kern = M == 2 ? sample_rows_kernel<2> : M == 3 ? sample_rows_kernel<3> : sample_rows_kernel<0>;
   if (smem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(unsigned)rsr::ceil_div(count, kRowsPerCta), kThreads, smem, rsr::as_stream(stream)>>>(
-      probs, N, M, seed, gen, start, count, out_states, out_fp4, row_bytes);
+  int dev = 0, sms = 0, per_sm = 0;
+  RSR_CUDA(cudaGetDevice(&dev));
+  RSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  RSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, smem));
+  const int64_t chunks = rsr::ceil_div(count, kRowsPerCta);
+  const int64_t grid = std::min<int64_t>(chunks, (int64_t)sms * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, kRowThreads, smem, rsr::as_stream(stream)>>>(
+      probs, N, M, seed, gen, start, count, out_states, out_fp4, row_bytes, st_bytes);
   return rsr::check_launch("sample_rows_kernel");
 }
