@@ -10,6 +10,8 @@
 // (exact), u >= cum  <=>  r >= ceil(cum * 2^53) (scaling by 2^53 is exact), so
 // state = #{m < M-1 : r >= T_m} with T_m = ceil(cumsum(probs[n])[m] * 2^53).
 // The clip to M-1 (sampling.py:89) is implied by counting only m < M-1.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -134,6 +136,7 @@ sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uin
 // few shifts and one byte permute.
 constexpr int kRowsPerCta = 64;
 constexpr int kRowThreads = 256;
+constexpr int kChunksPerCta = 2;
 constexpr int kTExtra = 3;  // extra threshold rows (no wrap within a block)
 #ifndef RSR_SAMPLE_MINB
 #define RSR_SAMPLE_MINB 3
@@ -194,7 +197,7 @@ __device__ __forceinline__ void fp4_quad_fast(const uint8_t* st, uint32_t base, 
   }
 }
 
-// Persistent: each CTA computes the threshold table once, then walks chunks
+// Each CTA computes the threshold table once, then walks kChunksPerCta chunks
 // of kRowsPerCta rows (chunk c = blockIdx.x + k * gridDim.x) with the state
 // staging buffer double-buffered, so one barrier per chunk separates the
 // generator phase from the store phase (the next chunk's generator writes the
@@ -546,8 +549,16 @@ extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_state
   RSR_CUDA(cudaGetDevice(&dev));
   RSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   RSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, smem));
+  // CTAs walk a bounded number of chunks: short-lived CTAs let the Stage-1
+  // loop's high-priority kernels take SMs while a prefetched batch is drawn
+  // on the low-priority stream (a persistent grid would hold every SM)
+  static const int cpc = [] {
+    const char* e = getenv("RSR_SAMPLE_CPC");
+    return e ? std::max(1, atoi(e)) : kChunksPerCta;
+  }();
   const int64_t chunks = rsr::ceil_div(count, kRowsPerCta);
-  const int64_t grid = std::min<int64_t>(chunks, (int64_t)sms * std::max(per_sm, 1));
+  const int64_t grid = std::max<int64_t>(std::min<int64_t>(chunks, (int64_t)sms * std::max(per_sm, 1)),
+                                         rsr::ceil_div(chunks, cpc));
   kern<<<(unsigned)grid, kRowThreads, smem, rsr::as_stream(stream)>>>(
       probs, N, M, seed, gen, start, count, out_states, out_fp4, row_bytes, st_bytes);
   return rsr::check_launch("sample_rows_kernel");

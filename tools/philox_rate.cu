@@ -28,6 +28,39 @@ __device__ __forceinline__ void mulhilo_ptx(uint64_t a, uint64_t b, uint64_t& hi
   hi = ((uint64_t)r3 << 32) | r2;
 }
 
+// four independent 32x32->64 products, carries on the integer ALU pipe
+__device__ __forceinline__ void mulhilo_wide4(uint64_t a, uint64_t b, uint64_t& hi, uint64_t& lo) {
+  uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+  uint32_t m, h0, h1;
+  uint32_t l0;
+  asm("{\n\t.reg .u64 p00, p01, p10, p11;\n\t.reg .u32 q0, q1, r0, r1, s0, s1, t0, t1, c;\n\t"
+      "mul.wide.u32 p00, %4, %6;\n\t"
+      "mul.wide.u32 p01, %4, %7;\n\t"
+      "mul.wide.u32 p10, %5, %6;\n\t"
+      "mul.wide.u32 p11, %5, %7;\n\t"
+      "mov.b64 {q0, q1}, p00;\n\t"
+      "mov.b64 {r0, r1}, p01;\n\t"
+      "mov.b64 {s0, s1}, p10;\n\t"
+      "mov.b64 {t0, t1}, p11;\n\t"
+      "mov.b32 %0, q0;\n\t"
+      "add.cc.u32 %1, r0, s0;\n\t"
+      "addc.u32 c, 0, 0;\n\t"
+      "add.cc.u32 %1, %1, q1;\n\t"
+      "addc.u32 c, c, 0;\n\t"
+      "add.cc.u32 %2, t0, r1;\n\t"
+      "addc.u32 %3, t1, 0;\n\t"
+      "add.cc.u32 %2, %2, s1;\n\t"
+      "addc.u32 %3, %3, 0;\n\t"
+      "add.cc.u32 %2, %2, c;\n\t"
+      "addc.u32 %3, %3, 0;\n\t"
+      "}"
+      : "=r"(l0), "=r"(m), "=r"(h0), "=r"(h1)
+      : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+  lo = ((uint64_t)m << 32) | l0;
+  hi = ((uint64_t)h1 << 32) | h0;
+}
+
+template <bool W4>
 __device__ __forceinline__ void philox_ptx(uint64_t ctr0, uint64_t key0, uint64_t key1,
                                            uint64_t out[4]) {
   const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
@@ -40,8 +73,13 @@ __device__ __forceinline__ void philox_ptx(uint64_t ctr0, uint64_t key0, uint64_
       key1 += W1;
     }
     uint64_t hi0, lo0, hi1, lo1;
-    mulhilo_ptx(M0, c0, hi0, lo0);
-    mulhilo_ptx(M1, c2, hi1, lo1);
+    if (W4) {
+      mulhilo_wide4(M0, c0, hi0, lo0);
+      mulhilo_wide4(M1, c2, hi1, lo1);
+    } else {
+      mulhilo_ptx(M0, c0, hi0, lo0);
+      mulhilo_ptx(M1, c2, hi1, lo1);
+    }
     const uint64_t n0 = hi1 ^ c1 ^ key0, n2 = hi0 ^ c3 ^ key1;
     c0 = n0;
     c1 = lo1;
@@ -67,7 +105,9 @@ __global__ void __launch_bounds__(256) probe(int64_t nblk, uint64_t seed, uint64
        b += (int64_t)gridDim.x * blockDim.x) {
     uint64_t w[4];
     if (V == 1)
-      philox_ptx((uint64_t)b + 1, seed, gen, w);
+      philox_ptx<false>((uint64_t)b + 1, seed, gen, w);
+    else if (V == 3)
+      philox_ptx<true>((uint64_t)b + 1, seed, gen, w);
     else
       rsr::philox4x64_10((uint64_t)b + 1, seed, gen, w);
     if (V == 2) {
@@ -99,10 +139,24 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int v = 0; v < 3; ++v) {
-    for (int ctas_per_sm : {4, 8, 16, 32}) {
+  // correctness of variant 3 against the library generator
+  {
+    uint64_t *o0, *o3;
+    cudaMalloc(&o0, (size_t)sms * 4 * 256 * 8);
+    cudaMalloc(&o3, (size_t)sms * 4 * 256 * 8);
+    probe<0><<<sms * 4, 256>>>(1 << 20, 7, 9, o0, T);
+    probe<3><<<sms * 4, 256>>>(1 << 20, 7, 9, o3, T);
+    static uint64_t h0[148 * 4 * 256], h3[148 * 4 * 256];
+    cudaMemcpy(h0, o0, (size_t)sms * 4 * 256 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h3, o3, (size_t)sms * 4 * 256 * 8, cudaMemcpyDeviceToHost);
+    int bad = 0;
+    for (int i = 0; i < sms * 4 * 256; ++i) bad += h0[i] != h3[i];
+    printf("variant 3 mismatches vs variant 0: %d\n", bad);
+  }
+  for (int v = 0; v < 4; ++v) {
+    for (int ctas_per_sm : {4, 8}) {
       const int grid = sms * ctas_per_sm;
-      auto k = v == 0 ? probe<0> : v == 1 ? probe<1> : probe<2>;
+      auto k = v == 0 ? probe<0> : v == 1 ? probe<1> : v == 2 ? probe<2> : probe<3>;
       k<<<grid, 256>>>(nblk, 123, 4, out, T);
       cudaEventRecord(e0);
       for (int r = 0; r < 10; ++r) k<<<grid, 256>>>(nblk, 123, 4, out, T);
