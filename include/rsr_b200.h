@@ -248,6 +248,37 @@ int rsr_dominance_scan(const uint8_t* cands, int64_t B, const uint8_t* members,
                        uint8_t* covers, int mask_candidate, uint8_t* member_mask,
                        void* stream);
 
+/* ---- device-resident reference sets (Stage-1 loop) ----------------------
+ * ReferenceSet.insert (boundary.py:87-108) for a batch of boundary-search
+ * results, entirely on the device.  Per side: member rows u8 [cap, N] and
+ * their FP4 operand rows [cap, row_bytes] (rsr_encode_refs_fp4 layout; rows
+ * >= ctr[0] are never-hit pad rows, which the caller fills when allocating),
+ * alive flags u8 [cap] (dropped members stay in place, flagged 0), counters
+ * ctr int64 [2] = {rows, alive}.  n_bound: caller's upper bound on ctr[0]. */
+typedef struct rsr_refset_dev {
+  uint8_t* rows;
+  uint8_t* fp4;
+  uint8_t* alive;
+  int64_t* ctr;
+  int64_t cap;
+  int64_t n_bound;
+} rsr_refset_dev;
+/* scratch bytes for rsr_refset_insert with B candidates */
+int64_t rsr_refset_scratch(int64_t B, int row_bytes);
+/* Insert B candidates (u8 [B, N], side u8 [B], pick order) into the set of
+ * their side with the reference's sequential semantics: outcome u8 [B] =
+ * 1 inserted / 2 redundant; report int64 [8] = {lower rows, lower alive,
+ * upper rows, upper alive, redundant searches (+=), dropped members (+=),
+ * sum of calls[B] (may be NULL), capacity overflow (|=)}. */
+int rsr_refset_insert(const uint8_t* cands, const uint8_t* cand_side, int64_t B,
+                      int n_components, int n_states, const rsr_refset_dev* lower,
+                      const rsr_refset_dev* upper, const int64_t* calls, uint8_t* outcome,
+                      int64_t* report, void* scratch, void* stream);
+/* out[i] = states[idx[pos[i]]]: rows of the picked unclassified samples
+ * (workflow.py:172-176 with the positions drawn on the host). */
+int rsr_gather_picks(const uint8_t* states, int n_components, const int64_t* idx,
+                     const int64_t* pos, int64_t count, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

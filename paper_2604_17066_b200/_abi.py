@@ -14,7 +14,7 @@ import threading
 
 import torch
 
-__all__ = ["lib", "call", "stream_ptr", "ptr", "PhiDesc", "LIB_PATH", "require_device",
+__all__ = ["lib", "call", "stream_ptr", "ptr", "PhiDesc", "RefsetDev", "LIB_PATH", "require_device",
            "SIDE_LOWER", "SIDE_UPPER", "HIT_LOWER", "HIT_UPPER", "LABEL_LOWER", "LABEL_UPPER",
            "LABEL_UNCLASSIFIED", "PHI_ST", "PHI_WIDEST", "PHI_GLOBAL", "PHI_KOFN", "PHI_CONES",
            "thermo_kpad", "thermo_words", "fp4_row_bytes", "FP4_TILE_ROWS",
@@ -54,6 +54,19 @@ class PhiDesc(ctypes.Structure):
 PHI_FLAG_SIMPLE = 1
 
 
+class RefsetDev(ctypes.Structure):
+    """Mirror of ``rsr_refset_dev`` (include/rsr_b200.h)."""
+
+    _fields_ = [
+        ("rows", ctypes.c_void_p),
+        ("fp4", ctypes.c_void_p),
+        ("alive", ctypes.c_void_p),
+        ("ctr", ctypes.c_void_p),
+        ("cap", ctypes.c_int64),
+        ("n_bound", ctypes.c_int64),
+    ]
+
+
 _P, _I, _I64, _U64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
 
 # name -> (restype, argtypes); the full exported surface of include/rsr_b200.h
@@ -91,6 +104,10 @@ EXPORTED = {
     "rsr_enumerate_states": (_I, [_P, _I, _I, _I64, _I64, _P, _P, _P]),
     "rsr_state_mass": (_I, [_P, _P, _I64, _I, _P, _P, _P]),
     "rsr_dominance_scan": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P, _I, _P, _P]),
+    "rsr_refset_scratch": (_I64, [_I64, _I]),
+    "rsr_refset_insert": (_I, [_P, _P, _I64, _I, _I, ctypes.POINTER(RefsetDev),
+                               ctypes.POINTER(RefsetDev), _P, _P, _P, _P, _P]),
+    "rsr_gather_picks": (_I, [_P, _I, _P, _P, _I64, _P, _P]),
 }
 
 _lock = threading.Lock()
@@ -138,7 +155,8 @@ def call(name: str, *args) -> int:
     """Invoke an entry point, mapping status codes to Python exceptions."""
     L = lib()
     rc = getattr(L, name)(*args)
-    if name in ("rsr_compact_scratch", "rsr_thermo_kpad", "rsr_version", "rsr_fp4_row_bytes"):
+    if name in ("rsr_compact_scratch", "rsr_thermo_kpad", "rsr_version", "rsr_fp4_row_bytes",
+                "rsr_refset_scratch"):
         return rc
     if rc != RSR_OK:
         msg = (L.rsr_last_error() or b"").decode(errors="replace")

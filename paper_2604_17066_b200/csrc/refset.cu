@@ -1,0 +1,334 @@
+// (4) Device-resident reference sets for the Stage-1 loop: the insertion
+// semantics of ReferenceSet.insert (boundary.py:87-108, _redundant_under
+// :50-54) applied to a batch of boundary-search results without a host round
+// trip, so the loop can enqueue iteration i's insertion and iteration i+1's
+// classification back to back and read the outcome one iteration later.
+//
+// Dominance is tested on the FP4 operand rows the classifier streams: with
+// E = [r_n >= k] (upper set) or [r_n < k] (lower set) as e2m1 nibbles,
+//   candidate c redundant under member m  <=>  E_m & ~E_c == 0
+// on both sides (upper: c >= m componentwise <=> every [m_n >= k] bit is set
+// in c; lower: c <= m <=> every [m_n < k] bit is set in c), so a pair costs a
+// few 16-byte AND-NOTs instead of N byte compares.
+//
+// Members are never physically removed during the loop: a dropped member is
+// flagged dead (alive[m] = 0).  Classification is unaffected (a member is
+// dropped only by a candidate whose region contains it) and so is every later
+// redundancy decision (transitivity), so only the host's final member list
+// (alive rows in physical order = the reference's ordered list) needs the
+// flags.  FP4 rows past the member count are never-hit pad rows, so the
+// classifier may stream a host-side upper bound of the count.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kScanThreads = 128;
+constexpr int kScanStage = 32;      // candidates staged in shared memory per pass
+constexpr int kMaxWords = RSR_FP4_MAX_ROW_BYTES / 16;
+
+__device__ __forceinline__ uint32_t nib(int e) { return e ? 0x2u : 0u; }
+
+// Candidate c's FP4 row under its own side's encoding (bias column 0).
+__global__ void encode_cands_kernel(const uint8_t* __restrict__ cands,
+                                    const uint8_t* __restrict__ cand_side, int N, int M,
+                                    uint8_t* __restrict__ out, int row_bytes) {
+  const int c = blockIdx.x;
+  const uint8_t* x = cands + (int64_t)c * N;
+  const bool upper = cand_side[c] == RSR_SIDE_UPPER;
+  const int kdim = N * (M - 1);
+  for (int b = threadIdx.x; b < row_bytes; b += blockDim.x) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = 2 * b + h;
+      if (e < kdim) {
+        const int n = e / (M - 1), k = e - n * (M - 1) + 1;
+        const bool ge = x[n] >= k;
+        v |= nib(upper ? ge : !ge) << (4 * h);
+      }
+    }
+    out[(int64_t)c * row_bytes + b] = (uint8_t)v;
+  }
+}
+
+// covered[c] |= some alive member m makes c redundant; covers[c] |= c makes
+// some alive member redundant.  Thread = member (row words in registers),
+// candidates of the member's side staged in shared memory.
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(
+    const uint8_t* __restrict__ cand_fp4, const uint8_t* __restrict__ cand_side, int B,
+    rsr_refset_dev lower, rsr_refset_dev upper, int row_bytes, uint8_t* covered,
+    uint8_t* covers) {
+  __shared__ uint4 sc[kScanStage][kMaxWords];
+  __shared__ int sidx[kScanStage];
+  const int side = blockIdx.y;
+  const rsr_refset_dev& set = side == RSR_SIDE_UPPER ? upper : lower;
+  const int64_t n = set.ctr[0];
+  const int64_t m = (int64_t)blockIdx.x * kScanThreads + threadIdx.x;
+  if ((int64_t)blockIdx.x * kScanThreads >= n) return;  // block-uniform
+  const int nw = row_bytes / 16;
+  const bool live = m < n && set.alive[m];
+  uint4 mw[kMaxWords];
+  if (live) {
+    const uint4* src = reinterpret_cast<const uint4*>(set.fp4 + m * row_bytes);
+#pragma unroll
+    for (int w = 0; w < kMaxWords; ++w)
+      if (w < nw) mw[w] = src[w];
+  }
+  for (int c0 = 0; c0 < B; c0 += kScanStage) {
+    const int cn = min(kScanStage, B - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn * nw; i += kScanThreads) {
+      const int c = i / nw, w = i - c * nw;
+      sc[c][w] = reinterpret_cast<const uint4*>(cand_fp4 + (int64_t)(c0 + c) * row_bytes)[w];
+    }
+    if (threadIdx.x < cn) sidx[threadIdx.x] = cand_side[c0 + threadIdx.x] == side ? 1 : 0;
+    __syncthreads();
+    if (!live) continue;
+    for (int c = 0; c < cn; ++c) {
+      if (!sidx[c]) continue;
+      uint32_t red = 0, cov = 0;
+#pragma unroll
+      for (int w = 0; w < kMaxWords; ++w) {
+        if (w < nw) {
+          const uint4 e = sc[c][w];
+          red |= (mw[w].x & ~e.x) | (mw[w].y & ~e.y) | (mw[w].z & ~e.z) | (mw[w].w & ~e.w);
+          cov |= (e.x & ~mw[w].x) | (e.y & ~mw[w].y) | (e.z & ~mw[w].z) | (e.w & ~mw[w].w);
+        }
+      }
+      if (red == 0) covered[c0 + c] = 1;
+      if (cov == 0) covers[c0 + c] = 1;
+    }
+  }
+}
+
+// rel[c * B + j] (same side only): bit0 = j redundant under c, bit1 = c
+// redundant under j.
+__global__ void rel_kernel(const uint8_t* __restrict__ cand_fp4, const uint8_t* __restrict__ cand_side,
+                           int B, int row_bytes, uint8_t* rel) {
+  const int c = blockIdx.x;
+  const int nw = row_bytes / 16;
+  const uint4* ec = reinterpret_cast<const uint4*>(cand_fp4 + (int64_t)c * row_bytes);
+  for (int j = threadIdx.x; j < B; j += blockDim.x) {
+    uint8_t r = 0;
+    if (j != c && cand_side[j] == cand_side[c]) {
+      const uint4* ej = reinterpret_cast<const uint4*>(cand_fp4 + (int64_t)j * row_bytes);
+      uint32_t j_under_c = 0, c_under_j = 0;
+      for (int w = 0; w < nw; ++w) {
+        const uint4 a = ec[w], b = ej[w];
+        c_under_j |= (b.x & ~a.x) | (b.y & ~a.y) | (b.z & ~a.z) | (b.w & ~a.w);
+        j_under_c |= (a.x & ~b.x) | (a.y & ~b.y) | (a.z & ~b.z) | (a.w & ~b.w);
+      }
+      r = (uint8_t)((j_under_c == 0 ? 1 : 0) | (c_under_j == 0 ? 2 : 0));
+    }
+    rel[(int64_t)c * B + j] = r;
+  }
+}
+
+// One CTA: the ordered per-candidate decisions of boundary.py:100-108 (thread
+// 0; drops are rare), member drops by all threads, then the appends.
+// report (int64 [8]): {lower n, lower alive, upper n, upper alive, redundant
+// searches (cumulative), drop events (cumulative), Phi calls of this batch,
+// capacity overflow}.
+__global__ void __launch_bounds__(256) resolve_kernel(
+    const uint8_t* __restrict__ cands, const uint8_t* __restrict__ cand_side,
+    const uint8_t* __restrict__ cand_fp4, int B, int N, int row_bytes,
+    const uint8_t* __restrict__ covered, const uint8_t* __restrict__ covers,
+    const uint8_t* __restrict__ rel, rsr_refset_dev lower, rsr_refset_dev upper,
+    uint8_t* outcome, int64_t* row_of, const int64_t* calls, int64_t* report) {
+  __shared__ int64_t s_n[2], s_alive[2], s_n0[2];
+  __shared__ int s_drop_c;  // candidate whose member drops are being applied, -1 none
+  __shared__ int s_done;
+  __shared__ int64_t s_red, s_drops, s_over;
+  rsr_refset_dev* sets[2] = {&lower, &upper};
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      s_n[s] = s_n0[s] = sets[s]->ctr[0];
+      s_alive[s] = sets[s]->ctr[1];
+    }
+    s_red = s_drops = s_over = 0;
+    s_done = 0;
+  }
+  __syncthreads();
+  int c_next = 0;  // thread 0's scan position
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_drop_c = -1;
+      for (; c_next < B; ++c_next) {
+        const int c = c_next;
+        const int s = cand_side[c] == RSR_SIDE_UPPER ? 1 : 0;
+        rsr_refset_dev& set = *sets[s];
+        bool red = covered[c] != 0;
+        for (int j = 0; j < c && !red; ++j)
+          if (outcome[j] == 1 && cand_side[j] == cand_side[c] && (rel[(int64_t)c * B + j] & 2))
+            red = true;
+        if (red) {
+          outcome[c] = 2;
+          row_of[c] = -1;
+          ++s_red;
+          continue;
+        }
+        // earlier inserts of this batch that c makes redundant
+        for (int j = 0; j < c; ++j)
+          if (outcome[j] == 1 && row_of[j] >= 0 && cand_side[j] == cand_side[c] &&
+              (rel[(int64_t)c * B + j] & 1) && set.alive[row_of[j]]) {
+            set.alive[row_of[j]] = 0;
+            --s_alive[s];
+            ++s_drops;
+          }
+        const int64_t r = s_n[s];
+        if (r >= set.cap) {  // host sized the capacity too small: flag, do not write
+          outcome[c] = 2;
+          row_of[c] = -1;
+          s_over = 1;
+          continue;
+        }
+        s_n[s] = r + 1;
+        ++s_alive[s];
+        set.alive[r] = 1;
+        outcome[c] = 1;
+        row_of[c] = r;
+        if (covers[c]) {  // pre-batch members c makes redundant: all threads
+          s_drop_c = c;
+          ++c_next;
+          break;
+        }
+      }
+      if (c_next >= B && s_drop_c < 0) s_done = 1;
+    }
+    __syncthreads();
+    const int dc = s_drop_c;
+    if (dc >= 0) {
+      const int s = cand_side[dc] == RSR_SIDE_UPPER ? 1 : 0;
+      rsr_refset_dev& set = *sets[s];
+      const int nw = row_bytes / 16;
+      const uint4* ec = reinterpret_cast<const uint4*>(cand_fp4 + (int64_t)dc * row_bytes);
+      int local = 0;
+      for (int64_t m = threadIdx.x; m < s_n0[s]; m += blockDim.x) {
+        if (!set.alive[m]) continue;
+        const uint4* em = reinterpret_cast<const uint4*>(set.fp4 + m * row_bytes);
+        uint32_t acc = 0;
+        for (int w = 0; w < nw; ++w) {
+          const uint4 a = em[w], e = ec[w];  // member redundant under dc: E_dc & ~E_m == 0
+          acc |= (e.x & ~a.x) | (e.y & ~a.y) | (e.z & ~a.z) | (e.w & ~a.w);
+        }
+        if (acc == 0) {
+          set.alive[m] = 0;
+          ++local;
+        }
+      }
+      if (local) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_alive[s]), (unsigned long long)(-local));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_drops), (unsigned long long)local);
+      }
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+  // appends: member rows (u8 + FP4) of the inserted candidates
+  for (int c = 0; c < B; ++c) {
+    if (outcome[c] != 1) continue;
+    rsr_refset_dev& set = *sets[cand_side[c] == RSR_SIDE_UPPER ? 1 : 0];
+    const int64_t r = row_of[c];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) set.rows[r * N + i] = cands[(int64_t)c * N + i];
+    for (int i = threadIdx.x; i < row_bytes; i += blockDim.x)
+      set.fp4[r * row_bytes + i] = cand_fp4[(int64_t)c * row_bytes + i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t calls_sum = 0;
+    if (calls)
+      for (int c = 0; c < B; ++c) calls_sum += calls[c];
+    for (int s = 0; s < 2; ++s) {
+      sets[s]->ctr[0] = s_n[s];
+      sets[s]->ctr[1] = s_alive[s];
+    }
+    report[0] = s_n[0];
+    report[1] = s_alive[0];
+    report[2] = s_n[1];
+    report[3] = s_alive[1];
+    report[4] += s_red;
+    report[5] += s_drops;
+    report[6] = calls_sum;
+    report[7] |= s_over;
+  }
+}
+
+// out[i] = states[idx[pos[i]]] (N bytes each): rows of picked unclassified samples.
+__global__ void gather_picks_kernel(const uint8_t* __restrict__ states, int N,
+                                    const int64_t* __restrict__ idx, const int64_t* __restrict__ pos,
+                                    uint8_t* __restrict__ out) {
+  const int i = blockIdx.x;
+  const int64_t row = idx[pos[i]];
+  for (int n = threadIdx.x; n < N; n += blockDim.x) out[(int64_t)i * N + n] = states[row * N + n];
+}
+
+}  // namespace
+
+extern "C" int64_t rsr_refset_scratch(int64_t B, int row_bytes) {
+  if (B < 0 || row_bytes < 0) return 0;
+  // cand_fp4 [B*rb] | covered [B] | covers [B] | rel [B*B] | row_of int64 [B], 16-aligned parts
+  auto a16 = [](int64_t x) { return (x + 15) / 16 * 16; };
+  return a16(B * row_bytes) + a16(B) + a16(B) + a16(B * B) + a16(8 * B);
+}
+
+extern "C" int rsr_refset_insert(const uint8_t* cands, const uint8_t* cand_side, int64_t B,
+                                 int n_components, int n_states, const rsr_refset_dev* lower,
+                                 const rsr_refset_dev* upper, const int64_t* calls,
+                                 uint8_t* outcome, int64_t* report, void* scratch, void* stream) {
+  const int N = n_components, M = n_states;
+  RSR_REQUIRE(N >= 1 && M >= 2 && B >= 0, "rsr_refset_insert: bad shape");
+  RSR_REQUIRE(B <= 65535, "rsr_refset_insert: at most 65535 candidates per call");
+  RSR_REQUIRE(lower && upper && report, "rsr_refset_insert: null set/report");
+  const int rb = rsr_fp4_row_bytes(N, M);
+  RSR_REQUIRE(rb <= RSR_FP4_MAX_ROW_BYTES, "rsr_refset_insert: rows wider than %d bytes",
+              RSR_FP4_MAX_ROW_BYTES);
+  for (const rsr_refset_dev* s : {lower, upper})
+    RSR_REQUIRE(s->rows && s->fp4 && s->alive && s->ctr && s->cap >= 0 && s->n_bound >= 0,
+                "rsr_refset_insert: incomplete set descriptor");
+  cudaStream_t st = rsr::as_stream(stream);
+  if (B == 0) return RSR_OK;
+  RSR_REQUIRE(cands && cand_side && outcome && scratch, "rsr_refset_insert: null pointer");
+  auto a16 = [](int64_t x) { return (x + 15) / 16 * 16; };
+  uint8_t* p = static_cast<uint8_t*>(scratch);
+  uint8_t* cand_fp4 = p;
+  p += a16(B * rb);
+  uint8_t* covered = p;
+  p += a16(B);
+  uint8_t* covers = p;
+  p += a16(B);
+  uint8_t* rel = p;
+  p += a16(B * B);
+  int64_t* row_of = reinterpret_cast<int64_t*>(p);
+  RSR_CUDA(cudaMemsetAsync(covered, 0, a16(B) * 2, st));
+  encode_cands_kernel<<<(unsigned)B, 128, 0, st>>>(cands, cand_side, N, M, cand_fp4, rb);
+  int rc = rsr::check_launch("encode_cands_kernel");
+  if (rc) return rc;
+  const int64_t nb = std::max(lower->n_bound, upper->n_bound);
+  if (nb > 0) {
+    dim3 grid((unsigned)rsr::ceil_div(nb, kScanThreads), 2);
+    scan_kernel<<<grid, kScanThreads, 0, st>>>(cand_fp4, cand_side, (int)B, *lower, *upper, rb,
+                                               covered, covers);
+    rc = rsr::check_launch("scan_kernel");
+    if (rc) return rc;
+  }
+  if (B > 1) {
+    rel_kernel<<<(unsigned)B, 128, 0, st>>>(cand_fp4, cand_side, (int)B, rb, rel);
+    rc = rsr::check_launch("rel_kernel");
+    if (rc) return rc;
+  }
+  resolve_kernel<<<1, 256, 0, st>>>(cands, cand_side, cand_fp4, (int)B, N, rb, covered, covers, rel,
+                                    *lower, *upper, outcome, row_of, calls, report);
+  return rsr::check_launch("resolve_kernel");
+}
+
+extern "C" int rsr_gather_picks(const uint8_t* states, int n_components, const int64_t* idx,
+                                const int64_t* pos, int64_t count, uint8_t* out, void* stream) {
+  RSR_REQUIRE(n_components >= 1 && count >= 0 && count <= 0x7fffffff, "rsr_gather_picks: bad shape");
+  if (count == 0) return RSR_OK;
+  RSR_REQUIRE(states && idx && pos && out, "rsr_gather_picks: null pointer");
+  gather_picks_kernel<<<(unsigned)count, 128, 0, rsr::as_stream(stream)>>>(states, n_components, idx,
+                                                                            pos, out);
+  return rsr::check_launch("gather_picks_kernel");
+}

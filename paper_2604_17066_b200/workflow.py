@@ -20,6 +20,8 @@ results are identical to one device.
 
 from __future__ import annotations
 
+import ctypes
+import os
 import time
 from dataclasses import dataclass
 
@@ -203,9 +205,14 @@ def stage1_find_references(model: SystemModel, dist: ComponentDistribution, conf
     caller = torch.cuda.current_stream()
     loop_stream = _high_priority_stream()
     loop_stream.wait_stream(caller)
+    use_async = (not comm.distributed and os.environ.get("RSR_SYNC_LOOP") != "1"
+                 and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.FP4_MAX_ROW_BYTES
+                 and dist.n_states == model.n_component_states
+                 and config.parallel_searches <= 4096)
+    loop = _stage1_loop_async if use_async else _stage1_loop
     with torch.cuda.stream(loop_stream):
-        result = _stage1_loop(model, dist, config, threshold, comm, phi, lower, upper, start,
-                              count, H, t_start, phi_start)
+        result = loop(model, dist, config, threshold, comm, phi, lower, upper, start, count, H,
+                      t_start, phi_start)
     caller.wait_stream(loop_stream)
     return result
 
@@ -260,6 +267,203 @@ def _stage1_loop(model, dist, config, threshold, comm, phi, lower, upper, start,
     pre.close()
     return Stage1Result(lower=lower, upper=upper, trace=trace, iterations=iteration + 1,
                         redundant_searches=redundant, terminated_by=terminated_by)
+
+
+class _DeviceRefs:
+    """Both sides' members for one Stage-1 run, resident on the device.
+
+    Per side: u8 rows [cap, N], FP4 operand rows [cap, row_bytes] (rows past
+    the member count are never-hit pad rows, so the classifier may stream a
+    host-side upper bound of the count), alive flags and counters, all updated
+    by ``rsr_refset_insert`` (csrc/refset.cu).  The host learns the counts one
+    iteration later from the loop's report buffer.
+    """
+
+    def __init__(self, n: int, m: int, dev: torch.device):
+        self.N, self.M, self.dev = n, m, dev
+        self.rb = _abi.fp4_row_bytes(n, m)
+        self.ctr = torch.zeros((2, 2), dtype=torch.int64, device=dev)
+        self.cap = [0, 0]
+        self.rows: list = [None, None]
+        self.fp4: list = [None, None]
+        self.alive: list = [None, None]
+        self.known = [0, 0]   # rows as of the last report read
+        self.pending = 0      # candidates inserted since then (bound on new rows per side)
+        self.desc = [_abi.RefsetDev(), _abi.RefsetDev()]
+        for s in (0, 1):
+            self._grow(s, 4 * _abi.FP4_TILE_ROWS)
+
+    def _grow(self, s: int, need: int) -> None:
+        tile = _abi.FP4_TILE_ROWS
+        cap = max(need, 2 * self.cap[s])
+        cap = (cap + tile - 1) // tile * tile
+        rows = torch.zeros((cap, self.N), dtype=torch.uint8, device=self.dev)
+        fp4 = torch.empty((cap, self.rb), dtype=torch.uint8, device=self.dev)
+        alive = torch.zeros(cap, dtype=torch.uint8, device=self.dev)
+        # all pad rows (bias column 1): never hit until a member overwrites them
+        _abi.call("rsr_encode_refs_fp4", None, 0, cap, self.N, self.M, _side_code_int(s),
+                  _abi.ptr(fp4), self.rb, _device.stream())
+        old = self.cap[s]
+        if old:
+            rows[:old].copy_(self.rows[s])
+            fp4[:old].copy_(self.fp4[s])
+            alive[:old].copy_(self.alive[s])
+        self.rows[s], self.fp4[s], self.alive[s], self.cap[s] = rows, fp4, alive, cap
+        d = self.desc[s]
+        d.rows, d.fp4, d.alive = rows.data_ptr(), fp4.data_ptr(), alive.data_ptr()
+        d.ctr = self.ctr[s].data_ptr()
+        d.cap = cap
+
+    def bound(self, s: int) -> int:
+        return self.known[s] + self.pending
+
+    def prepare_insert(self, b: int) -> None:
+        for s in (0, 1):
+            if self.bound(s) + b > self.cap[s]:
+                self._grow(s, self.bound(s) + b)
+            self.desc[s].n_bound = self.bound(s)
+
+    def to_sets(self, lower: ReferenceSet, upper: ReferenceSet, dropped: bool) -> None:
+        """Hand the final members (alive rows in physical order) to the ReferenceSets."""
+        for s, target in ((0, lower), (1, upper)):
+            n = self.known[s]
+            if n == 0:
+                continue
+            rows_h = self.rows[s][:n].cpu().numpy()
+            if dropped:
+                alive_h = self.alive[s][:n].cpu().numpy().astype(bool)
+                if not alive_h.all():
+                    target._set_rows(rows_h[alive_h])
+                    continue
+            target._append_host(rows_h)
+            target._dev_rows, target._dev_n = self.rows[s], n
+            target._fp4[self.M] = [self.fp4[s], n]
+
+
+def _side_code_int(s: int) -> int:
+    return _abi.SIDE_UPPER if s == 1 else _abi.SIDE_LOWER
+
+
+def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, start, count, H,
+                       t_start, phi_start) -> Stage1Result:
+    """Stage-1 loop with one host synchronisation per iteration.
+
+    Stream order per iteration i: classify(i) -> finalize counts -> report
+    copy (also carries iteration i-1's insertion outcome) | host: trace,
+    termination tests, the reference's picks (default_rng([seed, i]).choice)
+    -> compact + gather picks -> boundary search -> rsr_refset_insert ->
+    classify(i+1).  The host's bookkeeping for iteration i+1 overlaps the
+    device's search and insertion of iteration i; results (ordered sets, trace,
+    redundant searches, Phi counts) are those of workflow.py:122-195.
+    """
+    dev = _device.device()
+    N, M = dist.n_components, model.n_component_states
+    B = config.parallel_searches
+    st_ptr = _device.stream()
+    main = torch.cuda.current_stream()
+    refs = _DeviceRefs(N, M, dev)
+    rb = refs.rb
+    report_d = torch.zeros(16, dtype=torch.int64, device=dev)  # [0:4] counts, [4:12] insert report
+    report_h = torch.empty(16, dtype=torch.int64, pin_memory=True)
+    rep = report_h.numpy()
+    flags = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
+    labels = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
+    idx = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    cscratch = torch.empty(max(1, _abi.call("rsr_compact_scratch", count)), dtype=torch.int64,
+                           device=dev)
+    pos_h = torch.empty(B, dtype=torch.int64, pin_memory=True)
+    pos_d = torch.empty(B, dtype=torch.int64, device=dev)
+    x0 = torch.empty((B, N), dtype=torch.uint8, device=dev)
+    out_refs = torch.empty((B, N), dtype=torch.uint8, device=dev)
+    out_side = torch.empty(B, dtype=torch.uint8, device=dev)
+    out_calls = torch.empty(B, dtype=torch.int64, device=dev)
+    outcome = torch.empty(B, dtype=torch.uint8, device=dev)
+    iscratch = torch.empty(max(1, _abi.call("rsr_refset_scratch", B, rb)), dtype=torch.uint8,
+                           device=dev)
+    phi_vals = torch.empty(B, dtype=torch.uint8, device=dev)
+    desc = phi.descriptor(M)
+    ready_ev = torch.cuda.Event()
+    lo_p = ctypes.byref(refs.desc[0])
+    up_p = ctypes.byref(refs.desc[1])
+
+    pre = _Prefetcher(dist, config.seed, start, count)
+    pending = pre.launch(0)
+
+    def launch_classify(batch_ready):
+        batch, ready = batch_ready
+        main.wait_event(ready)
+        a = batch.fp4(M)
+        nl, nu = refs.bound(0), refs.bound(1)
+        _abi.call("rsr_classify_fp4", _abi.ptr(a), count, _abi.ptr(refs.fp4[0]) if nl else None, nl,
+                  _abi.ptr(refs.fp4[1]) if nu else None, nu, rb, _abi.ptr(flags), 0, st_ptr)
+        _abi.call("rsr_finalize", _abi.ptr(flags), count, _abi.ptr(labels), _abi.ptr(report_d),
+                  st_ptr)
+        report_h.copy_(report_d, non_blocking=True)
+        ready_ev.record(main)
+        return batch
+
+    trace: list[TraceRecord] = []
+    terminated_by = "r_max"
+    batch = launch_classify(pending)
+    pending = pre.launch(1)
+    iteration = 0
+    searched = False          # an insertion report is outstanding
+    no_search_picks = 0       # Phi calls of the last batch when searches are disabled
+    while True:
+        ready_ev.synchronize()
+        n_l, n_u, n_x = int(rep[0]), int(rep[1]), int(rep[2])
+        if searched:
+            refs.known = [int(rep[4]), int(rep[6])]
+            refs.pending = 0
+            model.add_evaluations(int(rep[10]) if config.boundary_search_enabled else no_search_picks)
+            if rep[11]:
+                raise RuntimeError("rsr_refset_insert: reference capacity overflow")
+            searched = False
+        n_refs = int(rep[5] + rep[7]) if iteration else 0
+        trace.append(TraceRecord(
+            reference_count=n_refs,
+            elapsed_seconds=time.perf_counter() - t_start,
+            phi_evaluations=model.evaluation_count - phi_start,
+            p_lower=n_l / H, p_upper=n_u / H, p_unclassified=n_x / H,
+            resident_memory_bytes=_rss_bytes()))
+        if n_x / H <= config.eps_u:
+            terminated_by = "eps_u"
+            break
+        if n_refs >= config.r_max:
+            break
+        rng = np.random.default_rng([config.seed, iteration])
+        n_pick = min(B, n_x)
+        positions = rng.choice(n_x, size=n_pick, replace=False)
+        pos_h.numpy()[:n_pick] = positions
+        pos_d[:n_pick].copy_(pos_h[:n_pick], non_blocking=True)
+        _abi.call("rsr_compact", _abi.ptr(labels), count, _abi.LABEL_UNCLASSIFIED, _abi.ptr(idx),
+                  _abi.ptr(cnt), _abi.ptr(cscratch), st_ptr)
+        _abi.call("rsr_gather_picks", _abi.ptr(batch.device_states()), N, _abi.ptr(idx),
+                  _abi.ptr(pos_d), n_pick, _abi.ptr(x0), st_ptr)
+        pre.release(iteration)
+        if config.boundary_search_enabled:
+            _abi.call("rsr_boundary_search", ctypes.byref(desc), int(threshold), _abi.ptr(x0),
+                      n_pick, _abi.ptr(out_refs), _abi.ptr(out_side), _abi.ptr(out_calls), st_ptr)
+            cands, calls_p = out_refs, _abi.ptr(out_calls)
+        else:
+            phi.eval_into(x0, None, n_pick, M, phi_vals)
+            # SIDE_LOWER = 0 when Phi <= m', SIDE_UPPER = 1 otherwise
+            torch.gt(phi_vals[:n_pick], threshold, out=out_side[:n_pick])
+            cands, calls_p, no_search_picks = x0, None, n_pick
+        refs.prepare_insert(n_pick)
+        _abi.call("rsr_refset_insert", _abi.ptr(cands), _abi.ptr(out_side), n_pick, N, M, lo_p,
+                  up_p, calls_p, _abi.ptr(outcome), _abi.ptr(report_d[4:]), _abi.ptr(iscratch),
+                  st_ptr)
+        refs.pending = n_pick
+        searched = True
+        iteration += 1
+        batch = launch_classify(pending)
+        pending = pre.launch(iteration + 1)
+    pre.close()
+    refs.to_sets(lower, upper, dropped=bool(rep[9]))
+    return Stage1Result(lower=lower, upper=upper, trace=trace, iterations=iteration + 1,
+                        redundant_searches=int(rep[8]), terminated_by=terminated_by)
 
 
 def _to_host(*tensors):

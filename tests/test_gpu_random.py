@@ -24,14 +24,23 @@ def _random_system(rng):
     return n, m, ms, levels, probs
 
 
-@pytest.mark.parametrize("seed", range(12))
-def test_random_cone_systems_workflow(seed):
+@pytest.mark.parametrize("loop", ["async", "sync"])
+@pytest.mark.parametrize("seed", range(16))
+def test_random_cone_systems_workflow(seed, loop, monkeypatch):
+    # "async": device-resident reference sets (csrc/refset.cu, one host sync per
+    # iteration); "sync": the host-resolved insertion path.  Seeds >= 12 search
+    # wide batches without boundary search, where raw samples as references make
+    # candidates redundant and drop members within and across batches.
+    monkeypatch.setenv("RSR_SYNC_LOOP", "1" if loop == "sync" else "0")
     rng = np.random.default_rng(1000 + seed)
     n, m, ms, levels, probs = _random_system(rng)
     cfg = dict(n_samples=int(rng.integers(500, 4000)), eps_u=float(rng.choice([1e-2, 1e-3])),
                r_max=int(rng.integers(5, 200)), seed=int(rng.integers(0, 2**31)),
                parallel_searches=int(rng.integers(1, 9)),
                boundary_search_enabled=bool(rng.random() < 0.85))
+    if seed >= 12:
+        cfg.update(parallel_searches=int(rng.integers(16, 80)), boundary_search_enabled=False,
+                   r_max=int(rng.integers(50, 400)))
     model = P.SystemModel(n, m, ms, P.cone_sum(levels, n))
     dist = P.ComponentDistribution(probs)
     ev = oracle.CountingPhi(oracle.phi_cones(levels), n, m, ms)
