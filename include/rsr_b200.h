@@ -174,6 +174,12 @@ int rsr_encode_refs_fp4(const uint8_t* states, int64_t count, int64_t rows_total
 int rsr_classify_fp4(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64_t n_lower,
                      const uint8_t* B_upper, int64_t n_upper, int row_bytes,
                      uint8_t* flags, int accumulate, void* stream);
+/* rsr_classify_fp4 over the first *S_dev (device count, <= S_cap) rows of A:
+ * the sample count of a later pass is known only on the device. */
+int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,
+                         const uint8_t* B_lower, int64_t n_lower, const uint8_t* B_upper,
+                         int64_t n_upper, int row_bytes, uint8_t* flags, int accumulate,
+                         void* stream);
 int rsr_classify_fp4_explain(const uint8_t* A, int64_t S, const uint8_t* B_lower,
                              int64_t n_lower, const uint8_t* B_upper, int64_t n_upper,
                              int row_bytes, uint8_t* flags, int64_t* first_lower,
@@ -274,6 +280,15 @@ int rsr_refset_insert(const uint8_t* cands, const uint8_t* cand_side, int64_t B,
                       int n_components, int n_states, const rsr_refset_dev* lower,
                       const rsr_refset_dev* upper, const int64_t* calls, uint8_t* outcome,
                       int64_t* report, void* scratch, void* stream);
+/* dst[i] = src[idx[i]] (copy_bytes per row; multiples of 16) for i < *count_dev
+ * (device count, at most cap): gathers sample operand rows for a second
+ * classification pass without a host round trip. */
+int rsr_gather_rows_dev(const uint8_t* src, int64_t src_stride, int copy_bytes,
+                        const int64_t* idx, const int64_t* count_dev, int64_t cap,
+                        uint8_t* dst, int64_t dst_stride, void* stream);
+/* flags[idx[i]] |= vals[i] for i < *count_dev (at most cap). */
+int rsr_scatter_or_dev(const uint8_t* vals, const int64_t* idx, const int64_t* count_dev,
+                       int64_t cap, uint8_t* flags, void* stream);
 /* out[i] = states[idx[pos[i]]]: rows of the picked unclassified samples
  * (workflow.py:172-176 with the positions drawn on the host). */
 int rsr_gather_picks(const uint8_t* states, int n_components, const int64_t* idx,

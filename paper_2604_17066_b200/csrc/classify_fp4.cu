@@ -114,6 +114,7 @@ struct Fp4Params {
   int64_t n_lower;  // reference rows of this launch per side (columns beyond are masked)
   int64_t n_upper;
   int resident;     // every reference tile has its own stage: loaded once, reused by all groups
+  const int64_t* S_dev;  // optional device sample count (<= S): rows [S_dev, S) are skipped
 };
 
 // SW32 K-major descriptor: 8-row core groups 256 B apart, version 1, layout 6.
@@ -286,6 +287,14 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1;
   const int n_clusters = gridDim.x >> 1;
+  // sample count: the launch's capacity, or a device-side count (every role
+  // reads the same value, so all loops agree on the group range)
+  int64_t S_run = p.S;
+  if (p.S_dev) {
+    const int64_t sd = *p.S_dev;
+    S_run = sd < 0 ? 0 : (sd < p.S ? sd : p.S);
+  }
+  const int n_groups = (int)((S_run + 2 * kRowsA - 1) / (2 * kRowsA));
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
@@ -341,7 +350,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     uint32_t phase = 0;
     const uint32_t sA0 = smem_addr(sA), sB0 = smem_addr(sB);
     const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
-    for (int g = cluster; g < p.n_groups; g += n_clusters, ++gi) {
+    for (int g = cluster; g < n_groups; g += n_clusters, ++gi) {
       const int ab = gi % p.a_bufs;
       const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
       const uint32_t bar_af = smem_addr(&a_full[ab]);
@@ -415,7 +424,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       const int cq = p.cq;
       int stage = 0, gi = 0;
       uint32_t phase = 0, buf = 0, tphase = 0;
-      for (int g = cluster; g < p.n_groups; g += n_clusters, ++gi) {
+      for (int g = cluster; g < n_groups; g += n_clusters, ++gi) {
         const int ab = gi % p.a_bufs;
         PROF_T(w0);
         mbar_wait(smem_addr(&a_full[ab]), (uint32_t)(gi / p.a_bufs) & 1);
@@ -478,7 +487,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     const int cg = (warp - 4) >> 2;       // column group
     const int c0 = cg * kCols;
     uint32_t buf = 0, tphase = 0;
-    for (int g = cluster; g < p.n_groups; g += n_clusters) {
+    for (int g = cluster; g < n_groups; g += n_clusters) {
       uint32_t hit = 0;
       int64_t first[2] = {INT64_MAX, INT64_MAX};
       int j = rot;
@@ -537,7 +546,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             first[1] = min(first[1], xfirst[(q * 2 + 1) * 128 + r]);
           }
         }
-        if (row < p.S) {
+        if (row < S_run) {
           const uint8_t prev = p.accumulate ? p.flags[row] : 0;
           p.flags[row] = (uint8_t)(prev | hit);
           if (FIRST) {
@@ -593,7 +602,8 @@ int make_map3(CUtensorMap* map, const void* base, int64_t rows, int row_bytes, i
 
 int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64_t n_lower,
                       const uint8_t* B_upper, int64_t n_upper, int row_bytes, uint8_t* flags,
-                      int64_t* first_lower, int64_t* first_upper, int accumulate, void* stream) {
+                      int64_t* first_lower, int64_t* first_upper, int accumulate, void* stream,
+                      const int64_t* S_dev = nullptr) {
   const bool want_first = first_lower != nullptr || first_upper != nullptr;
   RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4: negative size");
   RSR_REQUIRE(row_bytes >= kChunk && row_bytes % kChunk == 0,
@@ -630,6 +640,7 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
 
   Fp4Params p;
   p.S = S;
+  p.S_dev = S_dev;
   p.cq = cq;
   p.flags = flags;
   p.first_lower = first_lower;
@@ -924,6 +935,15 @@ extern "C" int rsr_classify_fp4(const uint8_t* A, int64_t S, const uint8_t* B_lo
                                 int row_bytes, uint8_t* flags, int accumulate, void* stream) {
   return classify_fp4_impl(A, S, B_lower, n_lower, B_upper, n_upper, row_bytes, flags, nullptr,
                            nullptr, accumulate, stream);
+}
+
+extern "C" int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,
+                                    const uint8_t* B_lower, int64_t n_lower, const uint8_t* B_upper,
+                                    int64_t n_upper, int row_bytes, uint8_t* flags, int accumulate,
+                                    void* stream) {
+  RSR_REQUIRE(S_dev != nullptr, "rsr_classify_fp4_dev: null device count");
+  return classify_fp4_impl(A, S_cap, B_lower, n_lower, B_upper, n_upper, row_bytes, flags, nullptr,
+                           nullptr, accumulate, stream, S_dev);
 }
 
 extern "C" int rsr_classify_fp4_explain(const uint8_t* A, int64_t S, const uint8_t* B_lower,

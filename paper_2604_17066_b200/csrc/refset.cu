@@ -264,7 +264,60 @@ __global__ void gather_picks_kernel(const uint8_t* __restrict__ states, int N,
   for (int n = threadIdx.x; n < N; n += blockDim.x) out[(int64_t)i * N + n] = states[row * N + n];
 }
 
+// dst[i] = src[idx[i]] (copy_bytes per row, 16-byte vectors), i < *count:
+// one warp per row, grid-stride (the count lives on the device).
+__global__ void gather_rows_dev_kernel(const uint8_t* __restrict__ src, int64_t src_stride,
+                                       int vecs, const int64_t* __restrict__ idx,
+                                       const int64_t* __restrict__ count_dev, int64_t cap,
+                                       uint8_t* __restrict__ dst, int64_t dst_stride) {
+  const int64_t n = min(*count_dev, cap);
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint4* s = reinterpret_cast<const uint4*>(src + idx[i] * src_stride);
+    uint4* d = reinterpret_cast<uint4*>(dst + i * dst_stride);
+    for (int v = lane; v < vecs; v += 32) d[v] = s[v];
+  }
+}
+
+// flags[idx[i]] |= vals[i], i < *count.
+__global__ void scatter_or_dev_kernel(const uint8_t* __restrict__ vals,
+                                      const int64_t* __restrict__ idx,
+                                      const int64_t* __restrict__ count_dev, int64_t cap,
+                                      uint8_t* __restrict__ flags) {
+  const int64_t n = min(*count_dev, cap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (vals[i]) flags[idx[i]] |= vals[i];
+}
+
 }  // namespace
+
+extern "C" int rsr_gather_rows_dev(const uint8_t* src, int64_t src_stride, int copy_bytes,
+                                   const int64_t* idx, const int64_t* count_dev, int64_t cap,
+                                   uint8_t* dst, int64_t dst_stride, void* stream) {
+  RSR_REQUIRE(copy_bytes > 0 && copy_bytes % 16 == 0 && src_stride % 16 == 0 && dst_stride % 16 == 0,
+              "rsr_gather_rows_dev: rows must be whole 16-byte vectors");
+  RSR_REQUIRE(cap >= 0, "rsr_gather_rows_dev: bad capacity");
+  if (cap == 0) return RSR_OK;
+  RSR_REQUIRE(src && idx && count_dev && dst, "rsr_gather_rows_dev: null pointer");
+  RSR_REQUIRE(((uintptr_t)src | (uintptr_t)dst) % 16 == 0, "rsr_gather_rows_dev: unaligned rows");
+  const int64_t grid = std::min<int64_t>(rsr::ceil_div(cap, 8), 148 * 8);
+  gather_rows_dev_kernel<<<(unsigned)grid, 256, 0, rsr::as_stream(stream)>>>(
+      src, src_stride, copy_bytes / 16, idx, count_dev, cap, dst, dst_stride);
+  return rsr::check_launch("gather_rows_dev_kernel");
+}
+
+extern "C" int rsr_scatter_or_dev(const uint8_t* vals, const int64_t* idx, const int64_t* count_dev,
+                                  int64_t cap, uint8_t* flags, void* stream) {
+  RSR_REQUIRE(cap >= 0, "rsr_scatter_or_dev: bad capacity");
+  if (cap == 0) return RSR_OK;
+  RSR_REQUIRE(vals && idx && count_dev && flags, "rsr_scatter_or_dev: null pointer");
+  const int64_t grid = std::min<int64_t>(rsr::ceil_div(cap, 256), 148 * 4);
+  scatter_or_dev_kernel<<<(unsigned)grid, 256, 0, rsr::as_stream(stream)>>>(vals, idx, count_dev,
+                                                                            cap, flags);
+  return rsr::check_launch("scatter_or_dev_kernel");
+}
 
 extern "C" int64_t rsr_refset_scratch(int64_t B, int row_bytes) {
   if (B < 0 || row_bytes < 0) return 0;

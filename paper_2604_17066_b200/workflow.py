@@ -390,13 +390,46 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
     pre = _Prefetcher(dist, config.seed, start, count)
     pending = pre.launch(0)
 
+    # Two-pass classification: most samples are dominated by one of the first
+    # upper references (tools/first_match_hist.py: after 480 of cfg3's 10^4
+    # references 0.4 % remain), so pass 1 runs every lower reference and the
+    # first `pass1` upper rows over the whole batch, and pass 2 only the samples
+    # still without a hit (compacted and gathered on the device, count never
+    # leaves the device) against the remaining upper rows.  Labels are those of
+    # a single pass.
+    pass1 = int(os.environ.get("RSR_LOOP_PASS1_ROWS", str(2 * _abi.FP4_TILE_ROWS)))
+    pass2_min = int(os.environ.get("RSR_LOOP_PASS2_MIN", str(2 * _abi.FP4_TILE_ROWS)))
+    two_pass = {}
+
+    def two_pass_buffers():
+        if not two_pass:
+            two_pass["a2"] = torch.empty((max(count, 1), 2 * rb), dtype=torch.uint8, device=dev)
+            two_pass["f2"] = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
+            two_pass["idx"] = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+            two_pass["cnt"] = torch.empty(1, dtype=torch.int64, device=dev)
+        return two_pass["a2"], two_pass["f2"], two_pass["idx"], two_pass["cnt"]
+
     def launch_classify(batch_ready):
         batch, ready = batch_ready
         main.wait_event(ready)
         a = batch.fp4(M)
         nl, nu = refs.bound(0), refs.bound(1)
-        _abi.call("rsr_classify_fp4", _abi.ptr(a), count, _abi.ptr(refs.fp4[0]) if nl else None, nl,
-                  _abi.ptr(refs.fp4[1]) if nu else None, nu, rb, _abi.ptr(flags), 0, st_ptr)
+        bl = _abi.ptr(refs.fp4[0]) if nl else None
+        if pass1 > 0 and nu > pass1 + pass2_min:
+            a2, f2, idx2, cnt2 = two_pass_buffers()
+            _abi.call("rsr_classify_fp4", _abi.ptr(a), count, bl, nl, _abi.ptr(refs.fp4[1]), pass1,
+                      rb, _abi.ptr(flags), 0, st_ptr)
+            _abi.call("rsr_compact", _abi.ptr(flags), count, 0, _abi.ptr(idx2), _abi.ptr(cnt2),
+                      _abi.ptr(cscratch), st_ptr)
+            _abi.call("rsr_gather_rows_dev", _abi.ptr(a), 2 * rb, rb, _abi.ptr(idx2), _abi.ptr(cnt2),
+                      count, _abi.ptr(a2), 2 * rb, st_ptr)
+            _abi.call("rsr_classify_fp4_dev", _abi.ptr(a2), count, _abi.ptr(cnt2), None, 0,
+                      _abi.ptr(refs.fp4[1][pass1:]), nu - pass1, rb, _abi.ptr(f2), 0, st_ptr)
+            _abi.call("rsr_scatter_or_dev", _abi.ptr(f2), _abi.ptr(idx2), _abi.ptr(cnt2), count,
+                      _abi.ptr(flags), st_ptr)
+        else:
+            _abi.call("rsr_classify_fp4", _abi.ptr(a), count, bl, nl,
+                      _abi.ptr(refs.fp4[1]) if nu else None, nu, rb, _abi.ptr(flags), 0, st_ptr)
         _abi.call("rsr_finalize", _abi.ptr(flags), count, _abi.ptr(labels), _abi.ptr(report_d),
                   st_ptr)
         report_h.copy_(report_d, non_blocking=True)

@@ -289,7 +289,14 @@ _WORKFLOW_CASES = [("workflow.json", c["spec"]["name"]) for c in load_json("work
 
 
 @pytest.mark.parametrize("fname,case", _WORKFLOW_CASES)
-def test_workflow_golden(fname, case):
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_workflow_golden(fname, case, two_pass, monkeypatch):
+    # two_pass: the Stage-1 loop's split classification (first 16 upper rows over
+    # the batch, the rest over the samples still without a hit) from the first
+    # iteration with more than 16 upper references
+    if two_pass:
+        monkeypatch.setenv("RSR_LOOP_PASS1_ROWS", "16")
+        monkeypatch.setenv("RSR_LOOP_PASS2_MIN", "0")
     rec = next(c for c in load_json(fname) if c["spec"]["name"] == case)
     spec = rec["spec"]
     model = device_model(spec["model"])
