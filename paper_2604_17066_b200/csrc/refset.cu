@@ -126,131 +126,162 @@ __global__ void rel_kernel(const uint8_t* __restrict__ cand_fp4, const uint8_t* 
   }
 }
 
-// One CTA: the ordered per-candidate decisions of boundary.py:100-108 (thread
-// 0; drops are rare), member drops by all threads, then the appends.
-// report (int64 [8]): {lower n, lower alive, upper n, upper alive, redundant
-// searches (cumulative), drop events (cumulative), Phi calls of this batch,
-// capacity overflow}.
-__global__ void __launch_bounds__(256) resolve_kernel(
+// One CTA resolves the batch.  With "x <= y" for "x redundant under y"
+// (transitive) and the set an antichain before the batch, the reference's
+// sequential loop (boundary.py:100-108) has a closed form, so every candidate
+// is decided in parallel:
+//   c redundant    <=> covered[c] or c <= j for some earlier same-side j
+//                      (a redundant or dropped j leads, by transitivity, to a
+//                      current member above c);
+//   inserted j dead <=> j <= c for some later inserted c;
+//   member m dead   <=> m <= c for some inserted c (covers[c] flags the
+//                      candidates worth checking; rare).
+// Rows of inserted candidates follow their side's member count in pick order.
+// report (int64 [8]): {lower rows, lower alive, upper rows, upper alive,
+// redundant searches (+=), dropped members (+=), sum of calls (this batch),
+// capacity overflow (|=)}.
+constexpr int kResolveThreads = 1024;
+
+__global__ void __launch_bounds__(kResolveThreads) resolve_kernel(
     const uint8_t* __restrict__ cands, const uint8_t* __restrict__ cand_side,
     const uint8_t* __restrict__ cand_fp4, int B, int N, int row_bytes,
     const uint8_t* __restrict__ covered, const uint8_t* __restrict__ covers,
     const uint8_t* __restrict__ rel, rsr_refset_dev lower, rsr_refset_dev upper,
     uint8_t* outcome, int64_t* row_of, const int64_t* calls, int64_t* report) {
-  __shared__ int64_t s_n[2], s_alive[2], s_n0[2];
-  __shared__ int s_drop_c;  // candidate whose member drops are being applied, -1 none
-  __shared__ int s_done;
-  __shared__ int64_t s_red, s_drops, s_over;
-  rsr_refset_dev* sets[2] = {&lower, &upper};
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      s_n[s] = s_n0[s] = sets[s]->ctr[0];
-      s_alive[s] = sets[s]->ctr[1];
-    }
-    s_red = s_drops = s_over = 0;
-    s_done = 0;
+  extern __shared__ __align__(16) uint8_t smem[];
+  int64_t* s_row = reinterpret_cast<int64_t*>(smem);             // [B]
+  int* s_drop = reinterpret_cast<int*>(smem + 8 * (size_t)B);      // [B] member droppers
+  uint8_t* s_side = smem + 12 * (size_t)B;                        // [B] 0 lower, 1 upper
+  uint8_t* s_ins = s_side + B;                                    // [B]
+  __shared__ int64_t s_n0[2], s_nins[2], s_dead[2];
+  __shared__ int s_red, s_over, s_ndrop;
+  __shared__ long long s_calls;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_n0[0] = lower.ctr[0];
+    s_n0[1] = upper.ctr[0];
+    s_nins[0] = s_nins[1] = s_dead[0] = s_dead[1] = 0;
+    s_red = s_over = s_ndrop = 0;
+    s_calls = 0;
+  }
+  // redundancy (parallel over candidates)
+  for (int c = tid; c < B; c += blockDim.x) {
+    const uint8_t sd = cand_side[c] == RSR_SIDE_UPPER ? 1 : 0;
+    bool red = covered[c] != 0;
+    const uint8_t* rr = rel + (int64_t)c * B;
+    for (int j = 0; j < c && !red; ++j) red = (rr[j] & 2) != 0;  // rel is 0 across sides
+    s_side[c] = sd;
+    s_ins[c] = red ? 0 : 1;
   }
   __syncthreads();
-  int c_next = 0;  // thread 0's scan position
-  while (true) {
-    if (threadIdx.x == 0) {
-      s_drop_c = -1;
-      for (; c_next < B; ++c_next) {
-        const int c = c_next;
-        const int s = cand_side[c] == RSR_SIDE_UPPER ? 1 : 0;
-        rsr_refset_dev& set = *sets[s];
-        bool red = covered[c] != 0;
-        for (int j = 0; j < c && !red; ++j)
-          if (outcome[j] == 1 && cand_side[j] == cand_side[c] && (rel[(int64_t)c * B + j] & 2))
-            red = true;
-        if (red) {
-          outcome[c] = 2;
-          row_of[c] = -1;
-          ++s_red;
-          continue;
-        }
-        // earlier inserts of this batch that c makes redundant
-        for (int j = 0; j < c; ++j)
-          if (outcome[j] == 1 && row_of[j] >= 0 && cand_side[j] == cand_side[c] &&
-              (rel[(int64_t)c * B + j] & 1) && set.alive[row_of[j]]) {
-            set.alive[row_of[j]] = 0;
-            --s_alive[s];
-            ++s_drops;
+  // member rows of the inserted candidates: prefix counts per side (warp 0)
+  if (tid < 32) {
+    int64_t base[2] = {s_n0[0], s_n0[1]};
+    const int64_t cap[2] = {lower.cap, upper.cap};
+    int red = 0, over = 0;
+    for (int c0 = 0; c0 < B; c0 += 32) {
+      const int c = c0 + tid;
+      const bool in = c < B && s_ins[c];
+      const int sd = c < B ? s_side[c] : 0;
+      red += __popc(__ballot_sync(0xffffffffu, c < B && !in));
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const unsigned m = __ballot_sync(0xffffffffu, in && sd == s2);
+        if (in && sd == s2) {
+          const int64_t r = base[s2] + __popc(m & ((1u << tid) - 1u));
+          if (r < cap[s2]) {
+            s_row[c] = r;
+          } else {  // host sized the capacity too small: flag, do not write
+            s_row[c] = -1;
+            over = 1;
           }
-        const int64_t r = s_n[s];
-        if (r >= set.cap) {  // host sized the capacity too small: flag, do not write
-          outcome[c] = 2;
-          row_of[c] = -1;
-          s_over = 1;
-          continue;
         }
-        s_n[s] = r + 1;
-        ++s_alive[s];
-        set.alive[r] = 1;
-        outcome[c] = 1;
-        row_of[c] = r;
-        if (covers[c]) {  // pre-batch members c makes redundant: all threads
-          s_drop_c = c;
-          ++c_next;
-          break;
-        }
+        base[s2] += __popc(m);
       }
-      if (c_next >= B && s_drop_c < 0) s_done = 1;
+      if (c < B && !in) s_row[c] = -1;
     }
-    __syncthreads();
-    const int dc = s_drop_c;
-    if (dc >= 0) {
-      const int s = cand_side[dc] == RSR_SIDE_UPPER ? 1 : 0;
-      rsr_refset_dev& set = *sets[s];
-      const int nw = row_bytes / 16;
-      const uint4* ec = reinterpret_cast<const uint4*>(cand_fp4 + (int64_t)dc * row_bytes);
-      int local = 0;
-      for (int64_t m = threadIdx.x; m < s_n0[s]; m += blockDim.x) {
+    over = __any_sync(0xffffffffu, over);
+    if (tid == 0) {
+      s_nins[0] = base[0] - s_n0[0];
+      s_nins[1] = base[1] - s_n0[1];
+      s_red = red;
+      s_over = over;
+      if (over) {  // keep the counters consistent with the rows actually written
+        s_nins[0] = min(s_nins[0], lower.cap - s_n0[0]);
+        s_nins[1] = min(s_nins[1], upper.cap - s_n0[1]);
+      }
+    }
+  }
+  __syncthreads();
+  rsr_refset_dev* sets[2] = {&lower, &upper};
+  // outcomes, batch-internal drops, appends
+  int local_dead[2] = {0, 0};
+  long long local_calls = 0;
+  for (int c = tid; c < B; c += blockDim.x) {
+    const int64_t r = s_row[c];
+    outcome[c] = r >= 0 ? 1 : 2;
+    row_of[c] = r;
+    if (calls) local_calls += calls[c];
+    if (r < 0) continue;
+    bool dead = false;
+    for (int d = c + 1; d < B && !dead; ++d)
+      dead = s_row[d] >= 0 && (rel[(int64_t)d * B + c] & 1);  // c <= later inserted d
+    sets[s_side[c]]->alive[r] = dead ? 0 : 1;
+    if (dead) ++local_dead[s_side[c]];
+    if (covers[c]) s_drop[atomicAdd(&s_ndrop, 1)] = c;
+  }
+  for (int i = tid; i < B * N; i += blockDim.x) {
+    const int c = i / N, k = i - c * N;
+    if (s_row[c] >= 0) sets[s_side[c]]->rows[s_row[c] * N + k] = cands[i];
+  }
+  for (int i = tid; i < B * row_bytes; i += blockDim.x) {
+    const int c = i / row_bytes, k = i - c * row_bytes;
+    if (s_row[c] >= 0) sets[s_side[c]]->fp4[s_row[c] * row_bytes + k] = cand_fp4[i];
+  }
+  __syncthreads();
+  // pre-batch members made redundant by an inserted candidate (rare)
+  if (s_ndrop) {
+    const int nw = row_bytes / 16;
+    for (int s2 = 0; s2 < 2; ++s2) {
+      rsr_refset_dev& set = *sets[s2];
+      for (int64_t m = tid; m < s_n0[s2]; m += blockDim.x) {
         if (!set.alive[m]) continue;
         const uint4* em = reinterpret_cast<const uint4*>(set.fp4 + m * row_bytes);
-        uint32_t acc = 0;
-        for (int w = 0; w < nw; ++w) {
-          const uint4 a = em[w], e = ec[w];  // member redundant under dc: E_dc & ~E_m == 0
-          acc |= (e.x & ~a.x) | (e.y & ~a.y) | (e.z & ~a.z) | (e.w & ~a.w);
+        for (int q = 0; q < s_ndrop; ++q) {
+          const int c = s_drop[q];
+          if (s_side[c] != s2) continue;
+          const uint4* ec = reinterpret_cast<const uint4*>(cand_fp4 + (int64_t)c * row_bytes);
+          uint32_t acc = 0;  // m <= c: E_c & ~E_m == 0
+          for (int w = 0; w < nw; ++w) {
+            const uint4 a = em[w], e = ec[w];
+            acc |= (e.x & ~a.x) | (e.y & ~a.y) | (e.z & ~a.z) | (e.w & ~a.w);
+          }
+          if (acc == 0) {
+            set.alive[m] = 0;
+            ++local_dead[s2];
+            break;
+          }
         }
-        if (acc == 0) {
-          set.alive[m] = 0;
-          ++local;
-        }
-      }
-      if (local) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(&s_alive[s]), (unsigned long long)(-local));
-        atomicAdd(reinterpret_cast<unsigned long long*>(&s_drops), (unsigned long long)local);
       }
     }
-    __syncthreads();
-    if (s_done) break;
   }
-  // appends: member rows (u8 + FP4) of the inserted candidates
-  for (int c = 0; c < B; ++c) {
-    if (outcome[c] != 1) continue;
-    rsr_refset_dev& set = *sets[cand_side[c] == RSR_SIDE_UPPER ? 1 : 0];
-    const int64_t r = row_of[c];
-    for (int i = threadIdx.x; i < N; i += blockDim.x) set.rows[r * N + i] = cands[(int64_t)c * N + i];
-    for (int i = threadIdx.x; i < row_bytes; i += blockDim.x)
-      set.fp4[r * row_bytes + i] = cand_fp4[(int64_t)c * row_bytes + i];
-  }
+  for (int s2 = 0; s2 < 2; ++s2)
+    if (local_dead[s2]) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dead[s2]),
+                                  (unsigned long long)local_dead[s2]);
+  if (local_calls) atomicAdd(reinterpret_cast<unsigned long long*>(&s_calls),
+                             (unsigned long long)local_calls);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t calls_sum = 0;
-    if (calls)
-      for (int c = 0; c < B; ++c) calls_sum += calls[c];
-    for (int s = 0; s < 2; ++s) {
-      sets[s]->ctr[0] = s_n[s];
-      sets[s]->ctr[1] = s_alive[s];
+  if (tid == 0) {
+    for (int s2 = 0; s2 < 2; ++s2) {
+      sets[s2]->ctr[0] = s_n0[s2] + s_nins[s2];
+      sets[s2]->ctr[1] += s_nins[s2] - s_dead[s2];
     }
-    report[0] = s_n[0];
-    report[1] = s_alive[0];
-    report[2] = s_n[1];
-    report[3] = s_alive[1];
+    report[0] = lower.ctr[0];
+    report[1] = lower.ctr[1];
+    report[2] = upper.ctr[0];
+    report[3] = upper.ctr[1];
     report[4] += s_red;
-    report[5] += s_drops;
-    report[6] = calls_sum;
+    report[5] += s_dead[0] + s_dead[1];
+    report[6] = s_calls;
     report[7] |= s_over;
   }
 }
@@ -371,8 +402,14 @@ extern "C" int rsr_refset_insert(const uint8_t* cands, const uint8_t* cand_side,
     rc = rsr::check_launch("rel_kernel");
     if (rc) return rc;
   }
-  resolve_kernel<<<1, 256, 0, st>>>(cands, cand_side, cand_fp4, (int)B, N, rb, covered, covers, rel,
-                                    *lower, *upper, outcome, row_of, calls, report);
+  const size_t rsmem = 14 * (size_t)B + 16;
+  RSR_REQUIRE(rsmem <= 200 * 1024, "rsr_refset_insert: batch too large");
+  if (rsmem > 48 * 1024)
+    RSR_CUDA(cudaFuncSetAttribute(resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)rsmem));
+  resolve_kernel<<<1, kResolveThreads, rsmem, st>>>(cands, cand_side, cand_fp4, (int)B, N, rb,
+                                                    covered, covers, rel, *lower, *upper, outcome,
+                                                    row_of, calls, report);
   return rsr::check_launch("resolve_kernel");
 }
 
