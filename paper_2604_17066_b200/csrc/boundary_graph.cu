@@ -29,7 +29,7 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 
 // experiment builds (make prof): 0 searches, 1 upper-side searches, 2 BFS runs,
-// 3 BFS levels, 4 cycles in BFS, 5 cycles in trace_path, 6 cycles in the initial
+// 3 BFS steps, 4 cycles in BFS, 5 cycles in trace_bidir, 6 cycles in the initial
 // union-find, 7 total cycles
 #ifdef RSR_FP4_PROF
 __device__ unsigned long long g_bprof[8];
@@ -53,11 +53,12 @@ constexpr int kEidMaxNodes = 128;
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) / 16 * 16; }
 
 // per-warp scratch: x (N bytes), union-find parents (n int32), on-path bits
-// (ceil(N/32) words), adjacency of G_L (n x W words), BFS levels (n x W words)
+// (ceil(N/32) words), adjacency of G_L (n x W words), BFS levels from s and
+// from t (n x W words each)
 template <int W>
 __host__ __device__ inline size_t warp_scratch(int N, int n) {
   return align16(N) + align16(4 * (size_t)n) + align16(4 * (((size_t)N + 31) / 32)) +
-         align16(2 * (size_t)n * W * 4);
+         align16(3 * (size_t)n * W * 4);
 }
 
 __device__ __forceinline__ int uf_find(int32_t* par, int a) {
@@ -78,7 +79,9 @@ __device__ __forceinline__ int uf_find(int32_t* par, int a) {
 // frontier -- no cross-lane OR reduction (redux.sync) on the critical path.
 template <int W>
 struct AdjSmem {
+  static constexpr bool kRegisters = false;
   uint32_t* a;
+  __device__ void load(const uint32_t*, int, int) {}  // shared memory is the master copy
   // next[q] bit l = node 32q+l has a neighbour in F (pull step, one ballot per word)
   __device__ void pull(const uint32_t (&F)[W], uint32_t (&next)[W], int n, int lane) const {
 #pragma unroll
@@ -104,6 +107,7 @@ struct AdjSmem {
 
 template <int W>
 struct AdjReg {
+  static constexpr bool kRegisters = true;
   uint32_t r[W][W];
   __device__ void load(const uint32_t* a, int n, int lane) {
 #pragma unroll
@@ -140,76 +144,120 @@ struct AdjReg {
   }
 };
 
-// BFS from s recording each level's new nodes; on success levels[0..d] hold the
-// layers and the return value is d (>= 1), else 0 (t unreachable).
-template <int W, class Adj>
-__device__ __forceinline__ int bfs_layers(const Adj& adj, uint32_t* levels, int n, int s, int t, int lane) {
-  uint32_t F[W], V[W];
+// Bidirectional BFS: the frontiers from s and from t grow in lockstep (two
+// independent pull chains per step, so the latency of one step is about that
+// of a one-sided level) until they touch -- about half the levels of the
+// one-sided search -- or one side stops growing (t or s unreachable: for a
+// bridge near either end this takes only as many steps as that side's
+// component is deep).  Returns 1 and the meeting node with its levels on both
+// sides, or 0 when s and t are disconnected.
+struct Meet {
+  int m, ks, kt;
+};
+
+template <int W>
+__device__ __forceinline__ int level_of(const uint32_t* lev, const uint32_t (&F)[W], int k, int m) {
+  uint32_t in_f = 0;  // mask select: no dynamically indexed register array
 #pragma unroll
-  for (int w = 0; w < W; ++w) F[w] = V[w] = (w == (s >> 5)) ? (1u << (s & 31)) : 0u;
-  // lane w < W stores word w of each layer (mask select: no indexed registers)
+  for (int w = 0; w < W; ++w) in_f |= (F[w] >> (m & 31)) & (uint32_t)(w == (m >> 5));
+  if (in_f & 1u) return k;
+  for (int j = k - 1; j > 0; --j)
+    if ((lev[j * W + (m >> 5)] >> (m & 31)) & 1u) return j;
+  return 0;
+}
+
+template <int W, class Adj>
+__device__ __forceinline__ int bfs_bidir(const Adj& adj, uint32_t* lev_s, uint32_t* lev_t, int n,
+                                         int s, int t, int lane, Meet& mt) {
+  uint32_t Fs[W], Vs[W], Ft[W], Vt[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    Fs[w] = Vs[w] = (w == (s >> 5)) ? (1u << (s & 31)) : 0u;
+    Ft[w] = Vt[w] = (w == (t >> 5)) ? (1u << (t & 31)) : 0u;
+  }
   auto word_of = [&](const uint32_t (&X)[W]) {
     uint32_t r = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) r |= X[w] & (0u - (uint32_t)(lane == w));
     return r;
   };
-  if (lane < W) levels[lane] = word_of(F);
-  for (int d = 1; d < n; ++d) {
-    uint32_t nxt[W];
-    adj.pull(F, nxt, n, lane);
-    uint32_t any = 0;
-    bool hit = false;
+  if (lane < W) {
+    lev_s[lane] = word_of(Fs);
+    lev_t[lane] = word_of(Ft);
+  }
+  for (int k = 1; k < n; ++k) {
+    uint32_t ns[W], nt[W];
+    adj.pull(Fs, ns, n, lane);
+    adj.pull(Ft, nt, n, lane);
+    uint32_t anys = 0, anyt = 0;
+    int m = -1;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const uint32_t nw = nxt[w] & ~V[w];
-      V[w] |= nw;
-      F[w] = nw;
-      any |= nw;
-      if (w == (t >> 5)) hit = (nw >> (t & 31)) & 1u;
+      ns[w] &= ~Vs[w];
+      nt[w] &= ~Vt[w];
+      Vs[w] |= ns[w];
+      Vt[w] |= nt[w];
+      Fs[w] = ns[w];
+      Ft[w] = nt[w];
+      anys |= ns[w];
+      anyt |= nt[w];
+      const uint32_t c = Vs[w] & Vt[w];
+      if (m < 0 && c) m = 32 * w + __ffs(c) - 1;
     }
-    if (lane < W) levels[d * W + lane] = word_of(F);
-    if (hit) {
-      __syncwarp();
-      BPROF_ADD(3, d);
-      return d;
+    if (lane < W) {
+      lev_s[k * W + lane] = word_of(Fs);
+      lev_t[k * W + lane] = word_of(Ft);
     }
-    if (!any) {
-      BPROF_ADD(3, d);
-      break;
+    __syncwarp();
+    if (m >= 0) {
+      mt.m = m;
+      mt.ks = level_of<W>(lev_s, Fs, k, m);
+      mt.kt = level_of<W>(lev_t, Ft, k, m);
+      BPROF_ADD(3, k);
+      return 1;
+    }
+    if (!anys || !anyt) {
+      BPROF_ADD(3, k);
+      return 0;
     }
   }
-  __syncwarp();
   return 0;
 }
 
-// Mark the edges of one shortest s-t path (from bfs_layers) in `onpath`.
+// Mark the edges of a path from `start` down the recorded levels d..0.
 template <int W, class Adj>
-__device__ __forceinline__ void trace_path(const GraphSmem& g, const Adj& adj, const uint32_t* levels, int d,
-                           uint32_t* onpath, int lane) {
-  const int words = (g.N + 31) / 32;
-  for (int i = lane; i < words; i += 32) onpath[i] = 0;
-  __syncwarp();
-  int cur = g.t;
+__device__ __forceinline__ void trace_down(const GraphSmem& g, const Adj& adj, const uint32_t* levels,
+                                           int d, int start, uint32_t* onpath, int lane) {
+  int cur = start;
   for (int k = d; k >= 1; --k) {
-    // parent: lowest node of layer k-1 adjacent to cur
-    int p = -1;
+    int p = -1;  // lowest node of layer k-1 adjacent to cur
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       const uint32_t c = adj.row(cur, w) & levels[(k - 1) * W + w];
       if (p < 0 && c) p = 32 * w + __ffs(c) - 1;
     }
-    // the (unique, simple graph) edge joining p and cur
     int e_found = g.eid ? g.eid[p * g.n + cur] : -1;
     for (int e0 = 0; e_found < 0 && e0 < g.N; e0 += 32) {
       const int e = e0 + lane;
-      const bool m = e < g.N && ((g.eu[e] == p && g.ev[e] == cur) || (g.eu[e] == cur && g.ev[e] == p));
-      const unsigned bal = __ballot_sync(kFull, m);
+      const bool mm = e < g.N && ((g.eu[e] == p && g.ev[e] == cur) || (g.eu[e] == cur && g.ev[e] == p));
+      const unsigned bal = __ballot_sync(kFull, mm);
       if (bal) e_found = e0 + __ffs(bal) - 1;
     }
     if (lane == 0) onpath[e_found >> 5] |= 1u << (e_found & 31);
     cur = p;
   }
+}
+
+// New witness: the s-m and m-t halves of the bidirectional search.
+template <int W, class Adj>
+__device__ __forceinline__ void trace_bidir(const GraphSmem& g, const Adj& adj, const uint32_t* lev_s,
+                                            const uint32_t* lev_t, const Meet& mt, uint32_t* onpath,
+                                            int lane) {
+  const int words = (g.N + 31) / 32;
+  for (int i = lane; i < words; i += 32) onpath[i] = 0;
+  __syncwarp();
+  trace_down<W>(g, adj, lev_s, mt.ks, mt.m, onpath, lane);
+  trace_down<W>(g, adj, lev_t, mt.kt, mt.m, onpath, lane);
   __syncwarp();
 }
 
@@ -217,25 +265,62 @@ __device__ __forceinline__ void trace_path(const GraphSmem& g, const Adj& adj, c
 // on it.  x[] is updated by lane 0; returns the Phi-call count of the walk
 // after the initial evaluation.
 template <int W, class Adj>
-__device__ __forceinline__ int64_t upper_walk(const GraphSmem& g, Adj& adj, uint8_t* x, uint32_t* levels,
-                              uint32_t* onpath, int L, int lane) {
+__device__ __forceinline__ int64_t upper_walk(const GraphSmem& g, Adj& adj, uint32_t* adj_smem,
+                                              uint8_t* x, uint32_t* levels, uint32_t* onpath, int L,
+                                              int lane) {
   int64_t calls = 0;
-  int dd = bfs_layers<W>(adj, levels, g.n, g.s, g.t, lane);
-  trace_path<W>(g, adj, levels, dd, onpath, lane);
+  uint32_t* lev_t = levels + g.n * W;
+  Meet mt;
+  bfs_bidir<W>(adj, levels, lev_t, g.n, g.s, g.t, lane, mt);  // connected: the start is upper
+  trace_bidir<W>(g, adj, levels, lev_t, mt, onpath, lane);
   BPROF_ADD(1, 1);
-  for (int n = 0; n < g.N; ++n) {
-    const int xn = x[n];
-    if (xn == 0) continue;
-    if (xn < L) {  // not in G_L: every step down leaves G_L unchanged
-      calls += xn;
-      if (lane == 0) x[n] = 0;
-      continue;
+  const int words = (g.N + 31) / 32;
+  int n = 0;
+  while (n < g.N) {
+    // next witness-path edge at or after n (path edges are in G_L)
+    int nstar = g.N;
+    for (int w = n >> 5; w < words; ++w) {
+      uint32_t bits = onpath[w];
+      if (w == (n >> 5)) bits &= ~0u << (n & 31);
+      if (bits) {
+        nstar = 32 * w + __ffs(bits) - 1;
+        break;
+      }
     }
+    if (nstar > n) {
+      // edges n .. nstar-1 are off the witness path: every step down is taken
+      // (the path survives), so they all drop to 0 at once -- x_n Phi calls
+      // each -- and leave G_L together (bulk update of the shared-memory
+      // adjacency, then the register copy is reloaded)
+      int c = 0;
+      for (int e = n + lane; e < nstar; e += 32) {
+        const int xe = x[e];
+        if (xe) {
+          c += xe;
+          x[e] = 0;
+          if (xe >= L) {
+            const int u = g.eu[e], v = g.ev[e];
+            atomicAnd(&adj_smem[u * W + (v >> 5)], ~(1u << (v & 31)));
+            atomicAnd(&adj_smem[v * W + (u >> 5)], ~(1u << (u & 31)));
+          }
+        }
+      }
+      calls += __reduce_add_sync(kFull, (unsigned)c);
+      __syncwarp();
+      adj.load(adj_smem, g.n, lane);
+      n = nstar;
+      if (n >= g.N) break;
+    }
+    const int xn = x[n];
     calls += xn - L + 1;  // steps down to L-1, the last one removes edge n
     const int u = g.eu[n], v = g.ev[n];
     adj.toggle(u, v, lane);
-    const bool on = (onpath[n >> 5] >> (n & 31)) & 1u;
-    if (on) {
+    if (Adj::kRegisters && lane == 0) {  // keep the shared-memory master copy in step
+      adj_smem[u * W + (v >> 5)] ^= 1u << (v & 31);
+      adj_smem[v * W + (u >> 5)] ^= 1u << (u & 31);
+    }
+    __syncwarp();
+    {
       // cheap witness repair first: a common neighbour w of u and v turns the
       // path into a walk through (u,w),(w,v) that still contains an s-t path
       // (the witness may be a superset of a path: a later test of one of its
@@ -256,23 +341,33 @@ __device__ __forceinline__ int64_t upper_walk(const GraphSmem& g, Adj& adj, uint
         __syncwarp();
       } else {
         BPROF_T(b0);
-        dd = bfs_layers<W>(adj, levels, g.n, g.s, g.t, lane);
+        const int dd = bfs_bidir<W>(adj, levels, lev_t, g.n, g.s, g.t, lane, mt);
         BPROF_T(b1);
         BPROF_ADD(2, 1);
         BPROF_ADD(4, b1 - b0);
         if (dd == 0) {  // crossing: reverted, walk moves to n + 1
           adj.toggle(u, v, lane);
-          if (lane == 0) x[n] = (uint8_t)L;
+          if (lane == 0) {
+            if (Adj::kRegisters) {
+              adj_smem[u * W + (v >> 5)] ^= 1u << (v & 31);
+              adj_smem[v * W + (u >> 5)] ^= 1u << (u & 31);
+            }
+            x[n] = (uint8_t)L;
+          }
+          __syncwarp();
+          ++n;
           continue;
         }
         BPROF_T(c0);
-        trace_path<W>(g, adj, levels, dd, onpath, lane);
+        trace_bidir<W>(g, adj, levels, lev_t, mt, onpath, lane);
         BPROF_T(c1);
         BPROF_ADD(5, c1 - c0);
       }
     }
     calls += L - 1;
     if (lane == 0) x[n] = 0;
+    __syncwarp();
+    ++n;
   }
   __syncwarp();
   return calls;
@@ -400,10 +495,10 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
       if constexpr (W <= 4) {
         AdjReg<W> ra;
         ra.load(adj, g.n, lane);
-        calls += upper_walk<W>(g, ra, x, levels, onpath, L, lane);
+        calls += upper_walk<W>(g, ra, adj, x, levels, onpath, L, lane);
       } else {
         AdjSmem<W> sa{adj};
-        calls += upper_walk<W>(g, sa, x, levels, onpath, L, lane);
+        calls += upper_walk<W>(g, sa, adj, x, levels, onpath, L, lane);
       }
     }
     __syncwarp();
