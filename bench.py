@@ -262,8 +262,8 @@ def run_ours(args):
                            start=0 if shard_refs else rank * S)
     if args.method == "tc":
         A = batch.fp4(2)
-        bl, nl = lower.device_fp4(2)
-        bu, nu = upper.device_fp4(2)
+        bl, nl, al = lower.device_fp4_rows(2)
+        bu, nu, au = upper.device_fp4_rows(2)
         width = A.shape[1] // 2  # bytes per operand row
     else:
         A = batch.thermo(2)
@@ -288,8 +288,8 @@ def run_ours(args):
 
     def classify_kernel():
         if args.method == "tc":
-            _abi.call("rsr_classify_fp4", _abi.ptr(A), S, _abi.ptr(bl), nl, _abi.ptr(bu), nu, width,
-                      _abi.ptr(flags), 0, stream)
+            _abi.call("rsr_classify_fp4_ex", _abi.ptr(A), S, None, _abi.ptr(bl), nl, al, _abi.ptr(bu),
+                      nu, au, width, _abi.ptr(flags), None, None, 0, stream)
         elif args.method == "tc8":
             _abi.call("rsr_classify_tc", _abi.ptr(A), S, _abi.ptr(bl), nl, _abi.ptr(bu), nu, width,
                       _abi.ptr(flags), 0, stream)

@@ -174,6 +174,17 @@ int rsr_encode_refs_fp4(const uint8_t* states, int64_t count, int64_t rows_total
 int rsr_classify_fp4(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64_t n_lower,
                      const uint8_t* B_upper, int64_t n_upper, int row_bytes,
                      uint8_t* flags, int accumulate, void* stream);
+/* rsr_classify_fp4 with (a) n_* = the reference rows that count and avail_*
+ * >= n_* the rows readable from B (rows n..avail-1 must be never-hit pad
+ * rows, e.g. the tile padding of a reference set), so the launch can pick its
+ * MMA N (reference tile of 160..240 rows) by n without masking pad columns;
+ * (b) S_dev (may be NULL): device count of sample rows (<= S) to classify;
+ * (c) first_* (may be NULL): first-match indices as rsr_classify_fp4_explain. */
+int rsr_classify_fp4_ex(const uint8_t* A, int64_t S, const int64_t* S_dev,
+                        const uint8_t* B_lower, int64_t n_lower, int64_t avail_lower,
+                        const uint8_t* B_upper, int64_t n_upper, int64_t avail_upper,
+                        int row_bytes, uint8_t* flags, int64_t* first_lower,
+                        int64_t* first_upper, int accumulate, void* stream);
 /* rsr_classify_fp4 over the first *S_dev (device count, <= S_cap) rows of A:
  * the sample count of a later pass is known only on the device. */
 int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,

@@ -111,6 +111,8 @@ EXPORTED = {
     "rsr_gather_rows_dev": (_I, [_P, _I64, _I, _P, _P, _I64, _P, _I64, _P]),
     "rsr_scatter_or_dev": (_I, [_P, _P, _P, _I64, _P, _P]),
     "rsr_classify_fp4_dev": (_I, [_P, _I64, _P, _P, _I64, _P, _I64, _I, _P, _I, _P]),
+    "rsr_classify_fp4_ex": (_I, [_P, _I64, _P, _P, _I64, _I64, _P, _I64, _I64, _I, _P, _P, _P, _I,
+                                 _P]),
 }
 
 _lock = threading.Lock()

@@ -318,6 +318,12 @@ class ReferenceSet:
             ent[1] = self._n
         return t, need
 
+    def device_fp4_rows(self, n_states: int) -> tuple[torch.Tensor | None, int, int]:
+        """FP4 B rows, the member count and the readable rows (members plus the
+        never-hit tile padding) -- the (B, n, avail) triple of rsr_classify_fp4_ex."""
+        t, need = self.device_fp4(n_states)
+        return t, self._n, need
+
     def device_bits(self, n_states: int) -> tuple[torch.Tensor | None, int]:
         """Packed thermometer bits ([r < k] lower / [r >= k] upper) and count."""
         if self._n == 0:

@@ -203,16 +203,13 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
     if method in ("tc", "fp4") and fp4_ok:
         a = batch.fp4(m_eff)
         rb = a.shape[1] // 2
-        bl, nl = lower_set.device_fp4(m_eff) if lower_set is not None else (None, 0)
-        bu, nu = upper_set.device_fp4(m_eff) if upper_set is not None else (None, 0)
+        bl, nl, al = lower_set.device_fp4_rows(m_eff) if lower_set is not None else (None, 0, 0)
+        bu, nu, au = upper_set.device_fp4_rows(m_eff) if upper_set is not None else (None, 0, 0)
         if want_first:
             fl = torch.empty(H, dtype=torch.int64, device=dev)
             fu = torch.empty(H, dtype=torch.int64, device=dev)
-            _abi.call("rsr_classify_fp4_explain", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu),
-                      nu, rb, _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
-        else:
-            _abi.call("rsr_classify_fp4", _abi.ptr(a), H, _abi.ptr(bl), nl, _abi.ptr(bu), nu, rb,
-                      _abi.ptr(flags), 0, st)
+        _abi.call("rsr_classify_fp4_ex", _abi.ptr(a), H, None, _abi.ptr(bl), nl, al, _abi.ptr(bu),
+                  nu, au, rb, _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
     elif method in ("tc", "tc8", "fp4") and tc_ok:
         a = batch.thermo(m_eff)
         bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
@@ -359,8 +356,8 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
     if fp4:
         width = _abi.fp4_row_bytes(N, m_eff)
         opnd_shape, opnd_dtype = (2 * width,), torch.uint8
-        bl, nl = lower_set.device_fp4(m_eff) if lower_set is not None else (None, 0)
-        bu, nu = upper_set.device_fp4(m_eff) if upper_set is not None else (None, 0)
+        bl, nl, al = lower_set.device_fp4_rows(m_eff) if lower_set is not None else (None, 0, 0)
+        bu, nu, au = upper_set.device_fp4_rows(m_eff) if upper_set is not None else (None, 0, 0)
     else:
         width = _abi.thermo_kpad(N, m_eff)
         if width > TC_MAX_KPAD:
@@ -392,8 +389,8 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
             _abi.call("rsr_encode_samples", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
                       _abi.ptr(opnd[slot]), width, st)
         if fp4:
-            _abi.call("rsr_classify_fp4", _abi.ptr(opnd[slot]), hi - lo, _abi.ptr(bl), nl,
-                      _abi.ptr(bu), nu, width, _abi.ptr(flags[lo:hi]), 0, st)
+            _abi.call("rsr_classify_fp4_ex", _abi.ptr(opnd[slot]), hi - lo, None, _abi.ptr(bl), nl,
+                      al, _abi.ptr(bu), nu, au, width, _abi.ptr(flags[lo:hi]), None, None, 0, st)
         else:
             _abi.call("rsr_classify_tc", _abi.ptr(opnd[slot]), hi - lo, _abi.ptr(bl), nl,
                       _abi.ptr(bu), nu, width, _abi.ptr(flags[lo:hi]), 0, st)

@@ -61,18 +61,22 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 #ifndef RSR_FP4_SPIN
 #define RSR_FP4_SPIN 0
 #endif
-#ifndef RSR_FP4_TILE_N
-#define RSR_FP4_TILE_N 240
-#endif
 constexpr int kEpiWarps = RSR_FP4_EPI_WARPS;
 constexpr int kColGroups = kEpiWarps / 4;
-constexpr int kTileN = RSR_FP4_TILE_N;        // MMA N: 240 (2 buffers) or 160 (3 buffers)
-constexpr int kBufs = 480 / kTileN;           // accumulator buffers in TMEM columns 0..479
-constexpr int kHalfRows = kTileN / 2;         // reference rows per CTA per tile
-constexpr int kChunkB = kHalfRows * kChunk;   // 3840 B
-constexpr int kCols = kTileN / kColGroups;    // accumulator columns per epilogue warp
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-static_assert(kTileN % kColGroups == 0 && kCols % 4 == 0, "bad epilogue split");
+
+// Reference tile geometry for MMA N = TN (a multiple of 16; the launch picks
+// TN per call to minimise padded reference rows, e.g. 5 x 208 for 1000 refs):
+// TMEM columns 0..479 hold 480 / TN accumulator buffers, 480..511 the scales.
+template <int TN>
+struct Tile {
+  static constexpr int kBufs = 480 / TN;
+  static constexpr int kHalfRows = TN / 2;             // reference rows per CTA per tile
+  static constexpr int kChunkB = kHalfRows * kChunk;   // bytes per K-step per CTA
+  static constexpr int kCols = TN / kColGroups;        // accumulator columns per epilogue warp
+  static_assert(TN % 16 == 0 && TN <= 240 && kBufs >= 2 && kBufs <= 4, "bad tile N");
+  static_assert(kCols % 4 == 0, "bad epilogue split");
+};
 
 // RSR_FP4_PROF builds (tools/ only, never the product library) accumulate
 // per-role cycle counters into g_prof: 0 MMA wait b_full, 1 MMA wait t_empty,
@@ -214,10 +218,11 @@ __device__ __forceinline__ void ld_cols_packed(uint32_t taddr, uint32_t* v) {
 // first column.  Load, release the buffer (as early as possible: the MMA warp
 // waits on it), then mask columns past the side's last reference, min-reduce
 // the 16-bit halves and find the first zero column.
-template <bool FIRST>
+template <int TN, bool FIRST>
 __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_bar, int lane,
                                               int c0, int64_t valid, bool& any, int& zref,
                                               long long& t_loaded) {
+  constexpr int kCols = Tile<TN>::kCols;
   constexpr int R = kCols / 2;
   uint32_t v[R];
   ld_cols_packed<kCols>(taddr, v);
@@ -258,11 +263,16 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_b
   }
 }
 
-template <bool FIRST>
+template <int TN, bool FIRST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_lower,
                          const __grid_constant__ CUtensorMap map_upper, const Fp4Params p) {
+  constexpr int kTileN = TN;
+  constexpr int kBufs = Tile<TN>::kBufs;
+  constexpr int kHalfRows = Tile<TN>::kHalfRows;
+  constexpr int kChunkB = Tile<TN>::kChunkB;
+  constexpr int kCols = Tile<TN>::kCols;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_addr(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
@@ -504,8 +514,8 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         bool any;
         int zref = 0;
         long long t_loaded = 0;
-        epilogue_tile<FIRST>(taddr, smem_addr(&t_empty[buf]), lane, c0, valid, any, zref,
-                             t_loaded);
+        epilogue_tile<TN, FIRST>(taddr, smem_addr(&t_empty[buf]), lane, c0, valid, any, zref,
+                                 t_loaded);
         PROF_T(e2);
         PROF_ADD(0, t_loaded - e1);
         if (any) {
@@ -600,51 +610,37 @@ int make_map3(CUtensorMap* map, const void* base, int64_t rows, int row_bytes, i
   return RSR_OK;
 }
 
-int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64_t n_lower,
-                      const uint8_t* B_upper, int64_t n_upper, int row_bytes, uint8_t* flags,
-                      int64_t* first_lower, int64_t* first_upper, int accumulate, void* stream,
-                      const int64_t* S_dev = nullptr) {
-  const bool want_first = first_lower != nullptr || first_upper != nullptr;
-  RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4: negative size");
-  RSR_REQUIRE(row_bytes >= kChunk && row_bytes % kChunk == 0,
-              "rsr_classify_fp4: row_bytes must be a positive multiple of 32");
-  RSR_REQUIRE(row_bytes <= RSR_FP4_MAX_ROW_BYTES, "rsr_classify_fp4: row_bytes > %d unsupported",
-              RSR_FP4_MAX_ROW_BYTES);
-  RSR_REQUIRE(S <= ((int64_t)1 << 31) - 2 * kRowsA, "rsr_classify_fp4: S too large");
-  cudaStream_t st = rsr::as_stream(stream);
-  if (S == 0) return RSR_OK;
-  RSR_REQUIRE(flags != nullptr && A != nullptr, "rsr_classify_fp4: null pointer");
-  constexpr int TN = kTileN;
-  const int64_t nt_l = rsr::ceil_div(n_lower, TN), nt_u = rsr::ceil_div(n_upper, TN);
-  if (nt_l + nt_u == 0) {
-    if (!accumulate) {
-      clear_flags4_kernel<<<(unsigned)rsr::ceil_div(S, 256), 256, 0, st>>>(flags, S);
-      int rc0 = rsr::check_launch("clear_flags4_kernel");
-      if (rc0) return rc0;
-      for (int64_t* f : {first_lower, first_upper})
-        if (f) RSR_CUDA(cudaMemsetAsync(f, 0xFF, S * sizeof(int64_t), st));  // -1
-    }
-    return RSR_OK;
-  }
-  RSR_REQUIRE(nt_l + nt_u < (1 << 30), "rsr_classify_fp4: too many reference tiles");
-  RSR_REQUIRE((nt_l == 0 || B_lower) && (nt_u == 0 || B_upper), "rsr_classify_fp4: null refs");
+struct Fp4Call {
+  const uint8_t* A;
+  int64_t S;
+  const int64_t* S_dev;
+  const uint8_t* B[2];   // lower, upper
+  int64_t n[2];          // reference rows that count
+  int64_t avail[2];      // rows readable from B (rows n..avail-1 are never-hit pad rows)
+  int row_bytes;
+  uint8_t* flags;
+  int64_t* first[2];
+  int accumulate;
+  cudaStream_t st;
+  int sm_count;
+};
 
-  int dev = 0, sm_count = 0;
-  RSR_CUDA(cudaGetDevice(&dev));
-  RSR_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
-
-  const int cq = row_bytes / kChunk;
+template <int TN>
+int launch_fp4(const Fp4Call& c) {
+  const bool want_first = c.first[0] != nullptr || c.first[1] != nullptr;
+  const int64_t nt_l = rsr::ceil_div(c.n[0], TN), nt_u = rsr::ceil_div(c.n[1], TN);
+  const int cq = c.row_bytes / kChunk;
   CUtensorMap ma;
-  int rc = make_map3(&ma, A, S, 2 * row_bytes, 2 * cq, kRowsA);
+  int rc = make_map3(&ma, c.A, c.S, 2 * c.row_bytes, 2 * cq, kRowsA);
   if (rc) return rc;
 
   Fp4Params p;
-  p.S = S;
-  p.S_dev = S_dev;
+  p.S = c.S;
+  p.S_dev = c.S_dev;
   p.cq = cq;
-  p.flags = flags;
-  p.first_lower = first_lower;
-  p.first_upper = first_upper;
+  p.flags = c.flags;
+  p.first_lower = c.first[0];
+  p.first_upper = c.first[1];
   const size_t max_smem = 227 * 1024;
   // align slack, barriers (<= 16 stages x 2 + 18), hit exchange, first-match exchange
   const size_t bars_bytes = (2 * 16 + 18) * 8;
@@ -668,10 +664,10 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   if (p.resident) stages = (int)(nt_l + nt_u);
   p.stages = stages;
   const size_t smem = fixed + p.a_bufs * a_buf + (size_t)stages * b_stage;
-  p.n_groups = (int)rsr::ceil_div(S, (int64_t)2 * kRowsA);
-  auto kern = want_first ? classify_fp4_pair_kernel<true> : classify_fp4_pair_kernel<false>;
+  p.n_groups = (int)rsr::ceil_div(c.S, (int64_t)2 * kRowsA);
+  auto kern = want_first ? classify_fp4_pair_kernel<TN, true> : classify_fp4_pair_kernel<TN, false>;
   RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int clusters = sm_count / 2;
+  int clusters = c.sm_count / 2;
   if (p.n_groups < clusters) clusters = p.n_groups;
 
   // Reference chunks: a launch's B slice must stay L2-resident while every
@@ -681,29 +677,123 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   const int64_t total = nt_l + nt_u;
   for (int64_t c0 = 0; c0 < total; c0 += chunk) {
     const int64_t c1 = c0 + chunk < total ? c0 + chunk : total;
-    const int64_t l0 = c0 < nt_l ? c0 : nt_l, l1 = c1 < nt_l ? c1 : nt_l;
-    const int64_t u0 = (c0 > nt_l ? c0 : nt_l) - nt_l, u1 = (c1 > nt_l ? c1 : nt_l) - nt_l;
+    const int64_t lo[2] = {c0 < nt_l ? c0 : nt_l, (c0 > nt_l ? c0 : nt_l) - nt_l};
+    const int64_t hi[2] = {c1 < nt_l ? c1 : nt_l, (c1 > nt_l ? c1 : nt_l) - nt_l};
     Fp4Params q = p;
-    q.nt_lower = (int)(l1 - l0);
-    q.nt_total = (int)((l1 - l0) + (u1 - u0));
-    q.accumulate = c0 == 0 ? accumulate : 1;
-    q.first_base_lower = l0 * TN;
-    q.first_base_upper = u0 * TN;
-    // reference rows of this launch (the last tile of a side may be partial)
-    q.n_lower = l1 > l0 ? (n_lower < l1 * TN ? n_lower : l1 * TN) - l0 * TN : 0;
-    q.n_upper = u1 > u0 ? (n_upper < u1 * TN ? n_upper : u1 * TN) - u0 * TN : 0;
-    const uint8_t* lb = l1 > l0 ? B_lower + l0 * TN * (int64_t)row_bytes : nullptr;
-    const uint8_t* ub = u1 > u0 ? B_upper + u0 * TN * (int64_t)row_bytes : nullptr;
+    q.nt_lower = (int)(hi[0] - lo[0]);
+    q.nt_total = (int)((hi[0] - lo[0]) + (hi[1] - lo[1]));
+    q.accumulate = c0 == 0 ? c.accumulate : 1;
+    q.first_base_lower = lo[0] * TN;
+    q.first_base_upper = lo[1] * TN;
+    // per side: rows the launch's tiles span; when the caller's readable rows
+    // cover them (never-hit pad rows past n) no column is masked, otherwise
+    // the TMA box reads past n as zeros and the epilogue masks columns >= n
+    const uint8_t* base[2];
+    int64_t rows[2];
+    for (int sd = 0; sd < 2; ++sd) {
+      base[sd] = nullptr;
+      rows[sd] = 0;
+      if (hi[sd] == lo[sd]) continue;
+      const int64_t r0 = lo[sd] * TN, span = (hi[sd] - lo[sd]) * TN;
+      const int64_t real = (c.n[sd] < r0 + span ? c.n[sd] : r0 + span) - r0;
+      rows[sd] = c.avail[sd] - r0 >= span ? span : real;
+      base[sd] = c.B[sd] + r0 * (int64_t)c.row_bytes;
+    }
+    q.n_lower = rows[0];
+    q.n_upper = rows[1];
     CUtensorMap cl, cu;
-    rc = make_map3(&cl, lb ? lb : ub, lb ? q.n_lower : q.n_upper, row_bytes, cq, TN / 2);
+    rc = make_map3(&cl, base[0] ? base[0] : base[1], base[0] ? rows[0] : rows[1], c.row_bytes, cq,
+                   TN / 2);
     if (rc) return rc;
-    rc = make_map3(&cu, ub ? ub : lb, ub ? q.n_upper : q.n_lower, row_bytes, cq, TN / 2);
+    rc = make_map3(&cu, base[1] ? base[1] : base[0], base[1] ? rows[1] : rows[0], c.row_bytes, cq,
+                   TN / 2);
     if (rc) return rc;
-    kern<<<2 * clusters, kThreads, smem, st>>>(ma, cl, cu, q);
+    kern<<<2 * clusters, kThreads, smem, c.st>>>(ma, cl, cu, q);
     rc = rsr::check_launch("classify_fp4_pair_kernel");
     if (rc) return rc;
   }
   return RSR_OK;
+}
+
+// MMA N per call: fewest padded reference rows, each tile also charged a fixed
+// overhead of 16 columns (ties go to the larger tile).  RSR_FP4_TILE_N forces one.
+int pick_tile_n(int64_t n_lower, int64_t n_upper) {
+  const char* env = getenv("RSR_FP4_TILE_N");
+  const int forced = env ? atoi(env) : 0;
+  static const int kCand[] = {240, 224, 208, 192, 176, 160};
+  if (forced) {
+    for (int tn : kCand)
+      if (tn == forced) return tn;
+  }
+  int best = 240;
+  int64_t best_cost = INT64_MAX;
+  for (int tn : kCand) {
+    const int64_t tiles = rsr::ceil_div(n_lower, tn) + rsr::ceil_div(n_upper, tn);
+    const int64_t cost = tiles * (tn + 16);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = tn;
+    }
+  }
+  return best;
+}
+
+int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64_t n_lower,
+                      int64_t avail_lower, const uint8_t* B_upper, int64_t n_upper,
+                      int64_t avail_upper, int row_bytes, uint8_t* flags, int64_t* first_lower,
+                      int64_t* first_upper, int accumulate, void* stream,
+                      const int64_t* S_dev = nullptr) {
+  RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4: negative size");
+  RSR_REQUIRE(avail_lower >= n_lower && avail_upper >= n_upper,
+              "rsr_classify_fp4: readable rows below the reference count");
+  RSR_REQUIRE(row_bytes >= kChunk && row_bytes % kChunk == 0,
+              "rsr_classify_fp4: row_bytes must be a positive multiple of 32");
+  RSR_REQUIRE(row_bytes <= RSR_FP4_MAX_ROW_BYTES, "rsr_classify_fp4: row_bytes > %d unsupported",
+              RSR_FP4_MAX_ROW_BYTES);
+  RSR_REQUIRE(S <= ((int64_t)1 << 31) - 2 * kRowsA, "rsr_classify_fp4: S too large");
+  cudaStream_t st = rsr::as_stream(stream);
+  if (S == 0) return RSR_OK;
+  RSR_REQUIRE(flags != nullptr && A != nullptr, "rsr_classify_fp4: null pointer");
+  if (n_lower + n_upper == 0) {
+    if (!accumulate) {
+      clear_flags4_kernel<<<(unsigned)rsr::ceil_div(S, 256), 256, 0, st>>>(flags, S);
+      int rc0 = rsr::check_launch("clear_flags4_kernel");
+      if (rc0) return rc0;
+      for (int64_t* f : {first_lower, first_upper})
+        if (f) RSR_CUDA(cudaMemsetAsync(f, 0xFF, S * sizeof(int64_t), st));  // -1
+    }
+    return RSR_OK;
+  }
+  RSR_REQUIRE(rsr::ceil_div(n_lower, 160) + rsr::ceil_div(n_upper, 160) < (1 << 30),
+              "rsr_classify_fp4: too many reference tiles");
+  RSR_REQUIRE((n_lower == 0 || B_lower) && (n_upper == 0 || B_upper), "rsr_classify_fp4: null refs");
+  Fp4Call c;
+  c.A = A;
+  c.S = S;
+  c.S_dev = S_dev;
+  c.B[0] = B_lower;
+  c.B[1] = B_upper;
+  c.n[0] = n_lower;
+  c.n[1] = n_upper;
+  c.avail[0] = avail_lower;
+  c.avail[1] = avail_upper;
+  c.row_bytes = row_bytes;
+  c.flags = flags;
+  c.first[0] = first_lower;
+  c.first[1] = first_upper;
+  c.accumulate = accumulate;
+  c.st = st;
+  int dev = 0;
+  RSR_CUDA(cudaGetDevice(&dev));
+  RSR_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, dev));
+  switch (pick_tile_n(n_lower, n_upper)) {
+    case 224: return launch_fp4<224>(c);
+    case 208: return launch_fp4<208>(c);
+    case 192: return launch_fp4<192>(c);
+    case 176: return launch_fp4<176>(c);
+    case 160: return launch_fp4<160>(c);
+    default: return launch_fp4<240>(c);
+  }
 }
 
 // ---------------------------------------------------------------- encoders
@@ -933,8 +1023,17 @@ extern "C" int rsr_encode_refs_fp4(const uint8_t* states, int64_t count, int64_t
 extern "C" int rsr_classify_fp4(const uint8_t* A, int64_t S, const uint8_t* B_lower,
                                 int64_t n_lower, const uint8_t* B_upper, int64_t n_upper,
                                 int row_bytes, uint8_t* flags, int accumulate, void* stream) {
-  return classify_fp4_impl(A, S, B_lower, n_lower, B_upper, n_upper, row_bytes, flags, nullptr,
-                           nullptr, accumulate, stream);
+  return classify_fp4_impl(A, S, B_lower, n_lower, n_lower, B_upper, n_upper, n_upper, row_bytes,
+                           flags, nullptr, nullptr, accumulate, stream);
+}
+
+extern "C" int rsr_classify_fp4_ex(const uint8_t* A, int64_t S, const int64_t* S_dev,
+                                   const uint8_t* B_lower, int64_t n_lower, int64_t avail_lower,
+                                   const uint8_t* B_upper, int64_t n_upper, int64_t avail_upper,
+                                   int row_bytes, uint8_t* flags, int64_t* first_lower,
+                                   int64_t* first_upper, int accumulate, void* stream) {
+  return classify_fp4_impl(A, S, B_lower, n_lower, avail_lower, B_upper, n_upper, avail_upper,
+                           row_bytes, flags, first_lower, first_upper, accumulate, stream, S_dev);
 }
 
 extern "C" int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,
@@ -942,16 +1041,16 @@ extern "C" int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64
                                     int64_t n_upper, int row_bytes, uint8_t* flags, int accumulate,
                                     void* stream) {
   RSR_REQUIRE(S_dev != nullptr, "rsr_classify_fp4_dev: null device count");
-  return classify_fp4_impl(A, S_cap, B_lower, n_lower, B_upper, n_upper, row_bytes, flags, nullptr,
-                           nullptr, accumulate, stream, S_dev);
+  return classify_fp4_impl(A, S_cap, B_lower, n_lower, n_lower, B_upper, n_upper, n_upper,
+                           row_bytes, flags, nullptr, nullptr, accumulate, stream, S_dev);
 }
 
 extern "C" int rsr_classify_fp4_explain(const uint8_t* A, int64_t S, const uint8_t* B_lower,
                                         int64_t n_lower, const uint8_t* B_upper, int64_t n_upper,
                                         int row_bytes, uint8_t* flags, int64_t* first_lower,
                                         int64_t* first_upper, int accumulate, void* stream) {
-  return classify_fp4_impl(A, S, B_lower, n_lower, B_upper, n_upper, row_bytes, flags,
-                           first_lower, first_upper, accumulate, stream);
+  return classify_fp4_impl(A, S, B_lower, n_lower, n_lower, B_upper, n_upper, n_upper, row_bytes,
+                           flags, first_lower, first_upper, accumulate, stream);
 }
 
 extern "C" int rsr_unpack_onehot_fp4(const uint8_t* packed, int64_t count, int n_components,

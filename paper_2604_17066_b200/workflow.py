@@ -415,21 +415,26 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         a = batch.fp4(M)
         nl, nu = refs.bound(0), refs.bound(1)
         bl = _abi.ptr(refs.fp4[0]) if nl else None
+        # rows past a side's bound are never-hit pad rows up to its capacity
+        cl, cu = refs.cap
         if pass1 > 0 and nu > pass1 + pass2_min:
             a2, f2, idx2, cnt2 = two_pass_buffers()
-            _abi.call("rsr_classify_fp4", _abi.ptr(a), count, bl, nl, _abi.ptr(refs.fp4[1]), pass1,
-                      rb, _abi.ptr(flags), 0, st_ptr)
+            _abi.call("rsr_classify_fp4_ex", _abi.ptr(a), count, None, bl, nl, cl,
+                      _abi.ptr(refs.fp4[1]), pass1, pass1, rb, _abi.ptr(flags), None, None, 0,
+                      st_ptr)
             _abi.call("rsr_compact", _abi.ptr(flags), count, 0, _abi.ptr(idx2), _abi.ptr(cnt2),
                       _abi.ptr(cscratch), st_ptr)
             _abi.call("rsr_gather_rows_dev", _abi.ptr(a), 2 * rb, rb, _abi.ptr(idx2), _abi.ptr(cnt2),
                       count, _abi.ptr(a2), 2 * rb, st_ptr)
-            _abi.call("rsr_classify_fp4_dev", _abi.ptr(a2), count, _abi.ptr(cnt2), None, 0,
-                      _abi.ptr(refs.fp4[1][pass1:]), nu - pass1, rb, _abi.ptr(f2), 0, st_ptr)
+            _abi.call("rsr_classify_fp4_ex", _abi.ptr(a2), count, _abi.ptr(cnt2), None, 0, 0,
+                      _abi.ptr(refs.fp4[1][pass1:]), nu - pass1, cu - pass1, rb, _abi.ptr(f2), None,
+                      None, 0, st_ptr)
             _abi.call("rsr_scatter_or_dev", _abi.ptr(f2), _abi.ptr(idx2), _abi.ptr(cnt2), count,
                       _abi.ptr(flags), st_ptr)
         else:
-            _abi.call("rsr_classify_fp4", _abi.ptr(a), count, bl, nl,
-                      _abi.ptr(refs.fp4[1]) if nu else None, nu, rb, _abi.ptr(flags), 0, st_ptr)
+            _abi.call("rsr_classify_fp4_ex", _abi.ptr(a), count, None, bl, nl, cl,
+                      _abi.ptr(refs.fp4[1]) if nu else None, nu, cu, rb, _abi.ptr(flags), None,
+                      None, 0, st_ptr)
         _abi.call("rsr_finalize", _abi.ptr(flags), count, _abi.ptr(labels), _abi.ptr(report_d),
                   st_ptr)
         report_h.copy_(report_d, non_blocking=True)

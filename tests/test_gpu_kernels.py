@@ -369,3 +369,37 @@ def test_phi_eval_and_boundary(kind, m, graph, flags, graph_search, monkeypatch)
             assert tuple(refs[b].cpu().tolist()) == vec
             assert int(side[b]) == (A.SIDE_LOWER if sd == oracle.LOWER else A.SIDE_UPPER)
             assert int(calls[b]) == ev.count
+
+
+@pytest.mark.parametrize("tile_n", [160, 176, 192, 208, 224, 240])
+@pytest.mark.parametrize("n,m", [(295, 2), (120, 3)])
+def test_fp4_tile_widths_and_pad_rows(tile_n, n, m, monkeypatch):
+    # every MMA N the launch can pick (RSR_FP4_TILE_N forces one), reference
+    # counts that leave partial tiles, with the pad rows readable (avail = padded
+    # rows: no masking) and without (avail = n: masked columns); first-match too
+    monkeypatch.setenv("RSR_FP4_TILE_N", str(tile_n))
+    rng = np.random.default_rng(tile_n + n + m)
+    s, kl, ku = 700, 301, 517
+    samples = rng.integers(0, m, size=(s, n))
+    lower = np.clip(samples[rng.integers(0, s, kl)] + rng.integers(0, 2, (kl, n)), 0, m - 1)
+    upper = np.clip(samples[rng.integers(0, s, ku)] - rng.integers(0, 2, (ku, n)), 0, m - 1)
+    want = _want_flags(samples, lower, upper, m)
+    _, fl_want = oracle.dominance_hits(samples, lower, m, oracle.LOWER, want_first=True)
+    _, fu_want = oracle.dominance_hits(samples, upper, m, oracle.UPPER, want_first=True)
+    rb = A.fp4_row_bytes(n, m)
+    a = torch.empty((s, 2 * rb), dtype=torch.uint8, device="cuda")
+    A.call("rsr_encode_samples_fp4", A.ptr(_dev(samples.astype(np.uint8))), s, n, m, A.ptr(a), rb,
+           A.stream_ptr())
+    bl = _fp4_refs_dev(lower, n, m, A.SIDE_LOWER)
+    bu = _fp4_refs_dev(upper, n, m, A.SIDE_UPPER)
+    for al, au in ((kl, ku), (bl.shape[0], bu.shape[0])):
+        flags = torch.empty(s, dtype=torch.uint8, device="cuda")
+        fl = torch.empty(s, dtype=torch.int64, device="cuda")
+        fu = torch.empty(s, dtype=torch.int64, device="cuda")
+        A.call("rsr_classify_fp4_ex", A.ptr(a), s, None, A.ptr(bl), kl, al, A.ptr(bu), ku, au, rb,
+               A.ptr(flags), A.ptr(fl), A.ptr(fu), 0, A.stream_ptr())
+        assert np.array_equal(flags.cpu().numpy(), want)
+        assert np.array_equal(fl.cpu().numpy(), fl_want) and np.array_equal(fu.cpu().numpy(), fu_want)
+        A.call("rsr_classify_fp4_ex", A.ptr(a), s, None, A.ptr(bl), kl, al, A.ptr(bu), ku, au, rb,
+               A.ptr(flags), None, None, 0, A.stream_ptr())
+        assert np.array_equal(flags.cpu().numpy(), want)
