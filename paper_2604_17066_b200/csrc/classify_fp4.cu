@@ -715,21 +715,25 @@ int launch_fp4(const Fp4Call& c) {
   return RSR_OK;
 }
 
-// MMA N per call: fewest padded reference rows, each tile also charged a fixed
-// overhead of 16 columns (ties go to the larger tile).  RSR_FP4_TILE_N forces one.
+// MMA N per call: fewest tiles weighted by the measured cost of one tile of
+// each width (tools/tile_n_sweep.sh on cfg2: a tile costs about the same down
+// to N = 208 -- the per-tile pipeline round trip, not the MMA columns, sets
+// it), so narrower tiles only win when they save whole tiles, e.g. 5 x 224
+// instead of 5 x 240 is a wash but 1000 refs in 5 x 208 beat 5 x 240 rows of
+// which 200 are padding.  RSR_FP4_TILE_N forces one width.
 int pick_tile_n(int64_t n_lower, int64_t n_upper) {
   const char* env = getenv("RSR_FP4_TILE_N");
   const int forced = env ? atoi(env) : 0;
   static const int kCand[] = {240, 224, 208, 192, 176, 160};
-  if (forced) {
-    for (int tn : kCand)
-      if (tn == forced) return tn;
-  }
+  static const int kCost[] = {1000, 957, 971, 920, 843, 778};  // relative time per tile
+  for (int tn : kCand)
+    if (tn == forced) return tn;
   int best = 240;
   int64_t best_cost = INT64_MAX;
-  for (int tn : kCand) {
+  for (int i = 0; i < 6; ++i) {
+    const int tn = kCand[i];
     const int64_t tiles = rsr::ceil_div(n_lower, tn) + rsr::ceil_div(n_upper, tn);
-    const int64_t cost = tiles * (tn + 16);
+    const int64_t cost = tiles * kCost[i];
     if (cost < best_cost) {
       best_cost = cost;
       best = tn;
