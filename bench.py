@@ -307,7 +307,7 @@ def run_ours(args):
         if kev:
             kev[1].record()
         if shard_refs:
-            comm.allreduce_max_u8(flags)  # OR of hit bits across the ref shards
+            comm.allreduce_or_hits(flags)  # OR of hit bits across the ref shards
         _abi.call("rsr_finalize", _abi.ptr(flags), S, _abi.ptr(labels), _abi.ptr(counts), stream)
         launches += classify_launches + 1
         if world > 1 and not shard_refs:

@@ -76,6 +76,17 @@ class Comm:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t
 
+    def allreduce_or_hits(self, flags: torch.Tensor) -> torch.Tensor:
+        """In-place OR of classifier hit flags (bit0 lower hit, bit1 upper hit) across
+        ranks: MAX on the raw bytes would turn lower-on-one-rank + upper-on-another
+        (1, 2) into 2 instead of 3, so each bit travels as its own 0/1 plane."""
+        if not self.distributed:
+            return flags
+        planes = torch.stack([flags & 1, flags >> 1])
+        self.allreduce_max_u8(planes)
+        torch.bitwise_or(planes[0], planes[1] << 1, out=flags)
+        return flags
+
     def allgather_i64(self, value: int) -> np.ndarray:
         if not self.distributed:
             return np.array([value], dtype=np.int64)

@@ -43,7 +43,10 @@ def _worker(rank, world, port, q):
     picked = gathered[torch.as_tensor(inv)].numpy()
     flags = torch.tensor([rank % 2, 1 - rank % 2], dtype=torch.uint8)
     orf = comm.allreduce_max_u8(flags).tolist()
-    q.put((rank, counts.tolist(), picked.tolist(), orf))
+    # classifier hit flags (bit0 lower, bit1 upper) OR-reduced across reference shards
+    hits = torch.tensor([[1, 0, 2, 0, 3], [2, 0, 0, 1, 1]][rank], dtype=torch.uint8)
+    orh = comm.allreduce_or_hits(hits).tolist()
+    q.put((rank, counts.tolist(), picked.tolist(), orf, orh))
     import torch.distributed as dist
     dist.destroy_process_group()
 
@@ -64,7 +67,8 @@ def test_two_rank_sharding_matches_single_process():
     unc = np.flatnonzero(xs.sum(1) <= 3)
     pos = np.random.default_rng([5, 2]).choice(len(unc), size=min(6, len(unc)), replace=False)
     want = xs[unc[pos]].tolist()
-    for rank, counts, picked, orf in out:
+    for rank, counts, picked, orf, orh in out:
+        assert orh == [3, 0, 2, 1, 3]
         assert counts == [len(unc), 1001]
         assert picked == want  # every rank sees the picks in single-process order
         assert orf == [1, 1]
