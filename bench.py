@@ -47,7 +47,9 @@ def parse():
                    choices=["cfg2", "cfg2_mixed", "cfg4", "cfg1", "cfg3", "cfg5"])
     p.add_argument("--parallel-searches", type=int, default=64)
     p.add_argument("--shard-refs", action="store_true",
-                   help="N>1: shard reference states across ranks, OR-reduce hit flags")
+                   help="N>1: shard reference states across all ranks, OR-reduce hit flags")
+    p.add_argument("--ref-shards", type=int, default=1,
+                   help="N>1: G_k reference shards per sample shard (G_k divides N)")
     p.add_argument("--k", type=int, default=10_000, help="refs per side (cfg2) / path refs (cfg4)")
     p.add_argument("--samples", type=int, default=None, help="samples per GPU")
     p.add_argument("--method", choices=["tc", "tc8", "bits"], default="tc",
@@ -248,20 +250,24 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     p1, lower_rows, upper_rows, S, desc = workload(args)
     K_job = len(lower_rows) + len(upper_rows)
-    shard_refs = args.shard_refs and world > 1
+    # process grid G = G_s x G_k: G_k reference shards per sample shard
+    gk = world if args.shard_refs else args.ref_shards
+    shard_refs = gk > 1 and world > 1
+    sample_shard, ref_comm, samp_comm = rank, comm, comm
     if shard_refs:
-        # ref-sharded mode: every rank classifies the same S samples against its
-        # 1/world slice of each side; hit flags are OR-reduced (NCCL MAX on 0/1 bits)
+        # every rank of a reference group classifies the same S samples against its
+        # 1/G_k slice of each side; hit flags are OR-reduced over the group (NCCL MAX
+        # on 0/1 planes), counts summed over the sample groups
         from paper_2604_17066_b200.dist import shard_range
-        l0, lc = shard_range(len(lower_rows), world, rank)
-        u0, uc = shard_range(len(upper_rows), world, rank)
+        ref_comm, samp_comm, sample_shard, ref_shard = comm.grid(gk)
+        l0, lc = shard_range(len(lower_rows), gk, ref_shard)
+        u0, uc = shard_range(len(upper_rows), gk, ref_shard)
         lower_rows, upper_rows = lower_rows[l0:l0 + lc], upper_rows[u0:u0 + uc]
     lower = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower_rows, trusted=True)
     upper = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper_rows, trusted=True)
     K = len(lower) + len(upper)
     dist = P.ComponentDistribution.iid(N_COMP, [1 - p1, p1])
-    batch = P.sample_batch(dist, S, seed=0, generation_index=0,
-                           start=0 if shard_refs else rank * S)
+    batch = P.sample_batch(dist, S, seed=0, generation_index=0, start=sample_shard * S)
     if args.method == "tc":
         A = batch.fp4(2)
         bl, nl, al = lower.device_fp4_rows(2)
@@ -307,11 +313,11 @@ def run_ours(args):
         if kev:
             kev[1].record()
         if shard_refs:
-            comm.allreduce_or_hits(flags)  # OR of hit bits across the ref shards
+            ref_comm.allreduce_or_hits(flags)  # OR of hit bits across the ref shards
         _abi.call("rsr_finalize", _abi.ptr(flags), S, _abi.ptr(labels), _abi.ptr(counts), stream)
         launches += classify_launches + 1
-        if world > 1 and not shard_refs:
-            tdist.all_reduce(counts)
+        if samp_comm.distributed:
+            tdist.all_reduce(counts, group=samp_comm.group)
 
     for _ in range(args.warmup):
         step()
@@ -340,8 +346,8 @@ def run_ours(args):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         step_ms = float(t.item())
     ms_per_step = step_ms / args.steps
-    # whole-job pairs per step: replicated refs -> world x S x K; sharded refs -> S x K_job
-    job_pairs = S * K_job if shard_refs else world * S * K
+    # whole-job pairs per step: replicated refs -> world x S x K; G_s x G_k grid -> G_s x S x K_job
+    job_pairs = (world // gk) * S * K_job if shard_refs else world * S * K
     value = job_pairs / (ms_per_step * 1e-3)
     final_counts = counts.cpu().tolist()
 
@@ -435,8 +441,9 @@ def run_ours(args):
                 "data": "synthetic",
                 "config": {"workload": desc, "samples_per_gpu": S, "ref_states": K_job,
                            "ref_states_per_gpu": K, "n_components": N_COMP, "method": args.method,
-                           "parallelism": (f"ref-sharded x{world} (same samples on every rank, "
-                                           f"hit flags OR-reduced with NCCL MAX)" if shard_refs else
+                           "parallelism": (f"samples x{world // gk} by refs x{gk} (a reference "
+                                           f"group shares its samples; hit flags OR-reduced with "
+                                           f"NCCL MAX on 0/1 planes)" if shard_refs else
                                            f"dp{world} (samples sharded by stream offset, refs "
                                            f"replicated, counts all-reduced)"),
                            "l2": f"A operand {a_bytes / 1e6:.0f} MB > L2 and 256 MB "

@@ -65,7 +65,7 @@ class Comm:
             return arr
         import torch.distributed as dist
         t = torch.as_tensor(arr, device=self.device)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t.cpu().numpy()
 
     def allreduce_max_u8(self, t: torch.Tensor) -> torch.Tensor:
@@ -73,7 +73,7 @@ class Comm:
         if not self.distributed:
             return t
         import torch.distributed as dist
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return t
 
     def allreduce_or_hits(self, flags: torch.Tensor) -> torch.Tensor:
@@ -93,7 +93,7 @@ class Comm:
         import torch.distributed as dist
         t = torch.tensor([value], dtype=torch.int64, device=self.device)
         out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t)
+        dist.all_gather(out, t, group=self.group)
         return np.array([int(o.item()) for o in out], dtype=np.int64)
 
     def allgather_rows(self, rows: torch.Tensor, counts: np.ndarray) -> torch.Tensor:
@@ -107,13 +107,39 @@ class Comm:
         if rows.shape[0]:
             pad[: rows.shape[0]].copy_(rows.to(self.device))
         out = [torch.empty_like(pad) for _ in range(self.world)]
-        dist.all_gather(out, pad)
+        dist.all_gather(out, pad, group=self.group)
         return torch.cat([o[: int(c)] for o, c in zip(out, counts)], dim=0)
+
+    def grid(self, ref_shards: int) -> tuple["Comm", "Comm", int, int]:
+        """2-D process grid for reference-sharded classification:
+        G = G_s x G_k ranks, rank r -> sample shard r // G_k, reference shard r % G_k.
+        Returns (ref_group, sample_group, sample_shard, ref_shard): hit flags are
+        OR-reduced over ref_group (same samples, different references), counts
+        summed over sample_group (same reference shard, different samples).
+        Every rank must call this collectively (torch.distributed.new_group)."""
+        if ref_shards < 1 or self.world % ref_shards:
+            raise ValueError(f"ref_shards={ref_shards} must divide world={self.world}")
+        gs, gk = self.world // ref_shards, ref_shards
+        s_idx, k_idx = divmod(self.rank, gk)
+        if not self.distributed:
+            return Comm.single(), Comm.single(), 0, 0
+        import torch.distributed as dist
+        ref_group = sample_group = None
+        for s in range(gs):  # every rank creates every group, in the same order
+            g = dist.new_group([s * gk + k for k in range(gk)])
+            if s == s_idx:
+                ref_group = g
+        for k in range(gk):
+            g = dist.new_group([s * gk + k for s in range(gs)])
+            if k == k_idx:
+                sample_group = g
+        return (Comm(k_idx, gk, self.device, ref_group), Comm(s_idx, gs, self.device, sample_group),
+                s_idx, k_idx)
 
     def barrier(self) -> None:
         if self.distributed:
             import torch.distributed as dist
-            dist.barrier()
+            dist.barrier(group=self.group)
 
 
 def shard_range(n_samples: int, world: int, rank: int) -> tuple[int, int]:

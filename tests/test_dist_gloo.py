@@ -72,3 +72,50 @@ def test_two_rank_sharding_matches_single_process():
         assert counts == [len(unc), 1001]
         assert picked == want  # every rank sees the picks in single-process order
         assert orf == [1, 1]
+
+
+def _grid_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2604_17066_b200.dist import Comm
+    comm = Comm.from_env(backend="gloo")
+    ref_comm, samp_comm, s_idx, k_idx = comm.grid(2)
+    # rank (s, k): sample shard s classified against reference shard k; hit bits of
+    # sample i on shard k: lower if i % 4 == k, upper if i % 3 == k + s
+    flags = torch.tensor([(1 if i % 4 == k_idx else 0) | (2 if i % 3 == k_idx + s_idx else 0)
+                          for i in range(12)], dtype=torch.uint8)
+    ref_comm.allreduce_or_hits(flags)
+    lab = np.where(flags.numpy() & 1, 0, np.where(flags.numpy() & 2, 1, 2))
+    counts = samp_comm.allreduce_sum_i64([int((lab == c).sum()) for c in range(3)])
+    q.put((rank, s_idx, k_idx, ref_comm.world, samp_comm.world, flags.tolist(), counts.tolist()))
+    import torch.distributed as dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_four_rank_grid_or_reduce_and_counts():
+    """2 x 2 process grid (samples x reference shards): hit flags OR-reduced
+    inside each reference group, label counts summed across sample groups."""
+    world, port = 4, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_grid_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=100) for _ in range(world))
+    for p in procs:
+        p.join(timeout=30)
+    want_counts = np.zeros(3, dtype=np.int64)
+    for s in range(2):
+        f = [(1 if i % 4 in (0, 1) else 0) | (2 if i % 3 in (s, s + 1) else 0) for i in range(12)]
+        lab = np.where(np.array(f) & 1, 0, np.where(np.array(f) & 2, 1, 2))
+        want_counts += [int((lab == c).sum()) for c in range(3)]
+        for rank, s_idx, k_idx, gk, gs, flags, counts in out:
+            if s_idx == s:
+                assert flags == f and (gk, gs) == (2, 2)
+    for rank, s_idx, k_idx, gk, gs, flags, counts in out:
+        assert (s_idx, k_idx) == divmod(rank, 2)
+    for rank, *_, counts in out:
+        assert counts == want_counts.tolist()
