@@ -156,19 +156,23 @@ def require_device() -> torch.device:
     return dev
 
 
+_FN: dict = {}
+_VALUE_RESULT = frozenset(("rsr_compact_scratch", "rsr_thermo_kpad", "rsr_version",
+                           "rsr_fp4_row_bytes", "rsr_refset_scratch"))
+
+
 def call(name: str, *args) -> int:
     """Invoke an entry point, mapping status codes to Python exceptions."""
-    L = lib()
-    rc = getattr(L, name)(*args)
-    if name in ("rsr_compact_scratch", "rsr_thermo_kpad", "rsr_version", "rsr_fp4_row_bytes",
-                "rsr_refset_scratch"):
+    fn = _FN.get(name)
+    if fn is None:
+        fn = _FN[name] = getattr(lib(), name)
+    rc = fn(*args)
+    if rc == RSR_OK or name in _VALUE_RESULT:
         return rc
-    if rc != RSR_OK:
-        msg = (L.rsr_last_error() or b"").decode(errors="replace")
-        if rc in (RSR_EINVAL, RSR_EUNSUPPORTED):
-            raise ValueError(f"{name}: {msg}")
-        raise RuntimeError(f"{name}: {msg}")
-    return rc
+    msg = (lib().rsr_last_error() or b"").decode(errors="replace")
+    if rc in (RSR_EINVAL, RSR_EUNSUPPORTED):
+        raise ValueError(f"{name}: {msg}")
+    raise RuntimeError(f"{name}: {msg}")
 
 
 def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:

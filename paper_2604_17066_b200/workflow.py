@@ -340,6 +340,45 @@ class _DeviceRefs:
             target._fp4[self.M] = [self.fp4[s], n]
 
 
+class _LeanPrefetcher:
+    """`_Prefetcher` for the one-sync loop: preallocated double buffers and events,
+    `rsr_sample_fp4` called directly on the side stream (no per-batch Python objects)."""
+
+    def __init__(self, dist_, seed, start, count, m):
+        dev = _device.device()
+        n = dist_.n_components
+        self.n, self.m, self.seed, self.start, self.count = n, m, seed, start, count
+        self.rb = _abi.fp4_row_bytes(n, m)
+        self.probs = _abi.ptr(dist_.device_probs())
+        self.states = [torch.empty((max(count, 1), n), dtype=torch.uint8, device=dev)
+                       for _ in range(2)]
+        self.fp4 = [torch.empty((max(count, 1), 2 * self.rb), dtype=torch.uint8, device=dev)
+                    for _ in range(2)]
+        self.stream = torch.cuda.Stream()
+        self.sptr = self.stream.cuda_stream
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free_used = [False, False]
+
+    def launch(self, gen: int) -> int:
+        slot = gen & 1
+        if self.free_used[slot]:
+            self.stream.wait_event(self.free[slot])
+        mask = (1 << 64) - 1
+        _abi.call("rsr_sample_fp4", self.probs, self.n, self.m, self.seed & mask, gen & mask,
+                  self.start, self.count, _abi.ptr(self.states[slot]), _abi.ptr(self.fp4[slot]),
+                  self.rb, self.sptr)
+        self.ready[slot].record(self.stream)
+        return slot
+
+    def release(self, gen: int, stream: torch.cuda.Stream) -> None:
+        self.free[gen & 1].record(stream)
+        self.free_used[gen & 1] = True
+
+    def close(self, stream: torch.cuda.Stream) -> None:
+        stream.wait_stream(self.stream)
+
+
 def _side_code_int(s: int) -> int:
     return _abi.SIDE_UPPER if s == 1 else _abi.SIDE_LOWER
 
@@ -387,8 +426,7 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
     lo_p = ctypes.byref(refs.desc[0])
     up_p = ctypes.byref(refs.desc[1])
 
-    pre = _Prefetcher(dist, config.seed, start, count)
-    pending = pre.launch(0)
+    pre = _LeanPrefetcher(dist, config.seed, start, count, M)
 
     # Two-pass classification: most samples are dominated by one of the first
     # upper references (tools/first_match_hist.py: after 480 of cfg3's 10^4
@@ -409,10 +447,9 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
             two_pass["cnt"] = torch.empty(1, dtype=torch.int64, device=dev)
         return two_pass["a2"], two_pass["f2"], two_pass["idx"], two_pass["cnt"]
 
-    def launch_classify(batch_ready):
-        batch, ready = batch_ready
-        main.wait_event(ready)
-        a = batch.fp4(M)
+    def launch_classify(slot):
+        main.wait_event(pre.ready[slot])
+        a = pre.fp4[slot]
         nl, nu = refs.bound(0), refs.bound(1)
         bl = _abi.ptr(refs.fp4[0]) if nl else None
         # rows past a side's bound are never-hit pad rows up to its capacity
@@ -439,11 +476,11 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
                   st_ptr)
         report_h.copy_(report_d, non_blocking=True)
         ready_ev.record(main)
-        return batch
+        return slot
 
     trace: list[TraceRecord] = []
     terminated_by = "r_max"
-    batch = launch_classify(pending)
+    slot = launch_classify(pre.launch(0))
     pending = pre.launch(1)
     iteration = 0
     searched = False          # an insertion report is outstanding
@@ -477,9 +514,9 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         pos_d[:n_pick].copy_(pos_h[:n_pick], non_blocking=True)
         _abi.call("rsr_compact", _abi.ptr(labels), count, _abi.LABEL_UNCLASSIFIED, _abi.ptr(idx),
                   _abi.ptr(cnt), _abi.ptr(cscratch), st_ptr)
-        _abi.call("rsr_gather_picks", _abi.ptr(batch.device_states()), N, _abi.ptr(idx),
+        _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
                   _abi.ptr(pos_d), n_pick, _abi.ptr(x0), st_ptr)
-        pre.release(iteration)
+        pre.release(iteration, main)
         if config.boundary_search_enabled:
             _abi.call("rsr_boundary_search", ctypes.byref(desc), int(threshold), _abi.ptr(x0),
                       n_pick, _abi.ptr(out_refs), _abi.ptr(out_side), _abi.ptr(out_calls), st_ptr)
@@ -496,9 +533,9 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         refs.pending = n_pick
         searched = True
         iteration += 1
-        batch = launch_classify(pending)
+        slot = launch_classify(pending)
         pending = pre.launch(iteration + 1)
-    pre.close()
+    pre.close(main)
     refs.to_sets(lower, upper, dropped=bool(rep[9]))
     return Stage1Result(lower=lower, upper=upper, trace=trace, iterations=iteration + 1,
                         redundant_searches=int(rep[8]), terminated_by=terminated_by)
