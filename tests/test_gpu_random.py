@@ -155,3 +155,43 @@ def test_boundary_graph_search_matches_bitset_walk(kind, m, p_hi, monkeypatch):
             ev = oracle.CountingPhi(ref, graph.n_edges, m, ms)
             vec, side = oracle.boundary_search(ev, xs[b].astype(np.int64), thr)
             assert tuple(out["1"][0][b].tolist()) == vec and int(out["1"][2][b]) == ev.count
+
+
+@pytest.mark.parametrize("cfg_name", ["cfg3", "cfg5"])
+def test_loop_paths_agree_on_config_graphs(cfg_name, monkeypatch):
+    """Stage 1 on the BASELINE config 3 / 5 graphs at a reduced batch size: the
+    one-sync loop (device reference sets, two-pass classification with the default
+    480-row first pass) and the host-resolved loop give identical ordered sets,
+    traces, redundant-search and Phi counts; the oracle checks the first iterations."""
+    import torch  # noqa: F401
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from _specs import device_model
+    from paper_2604_17066_b200 import workloads as W
+    g = W.cfg3(0) if cfg_name == "cfg3" else W.cfg5(0)
+    m = 2 if cfg_name == "cfg3" else 3
+    spec = {"kind": "st" if m == 2 else "widest", "n_nodes": g["n_nodes"], "edges": g["edges"],
+            "s": g["source"], "t": g["target"], "m": m, "ms": m}
+    dist = P.ComponentDistribution(g["probs"])
+    cfg = P.RunConfig(n_samples=1 << 14, eps_u=1e-5, r_max=1500, seed=3, parallel_searches=64)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("RSR_SYNC_LOOP", mode)
+        model = device_model(spec)
+        s1 = P.stage1_find_references(model, dist, cfg, 0)
+        out[mode] = (s1.lower.members, s1.upper.members,
+                     [(t.reference_count, t.phi_evaluations, t.p_lower, t.p_upper,
+                       t.p_unclassified) for t in s1.trace],
+                     s1.iterations, s1.redundant_searches, s1.terminated_by,
+                     model.evaluation_count)
+    assert out["0"] == out["1"]
+    assert len(out["0"][1]) > 960  # the two-pass split was active
+    from _specs import oracle_phi
+    phi, n = oracle_phi(spec)
+    ev = oracle.CountingPhi(phi, n, m, m)
+    o1 = oracle.stage1(ev, g["probs"], 0, 1 << 14, eps_u=1e-5, r_max=100, seed=3,
+                       parallel_searches=64, fast=True)
+    k = len(o1["trace"])
+    assert [(t["reference_count"], t["phi_evaluations"], t["p_lower"], t["p_upper"],
+             t["p_unclassified"]) for t in o1["trace"]] == out["0"][2][:k]
