@@ -317,11 +317,17 @@ class _DeviceRefs:
     def bound(self, s: int) -> int:
         return self.known[s] + self.pending
 
-    def prepare_insert(self, b: int) -> None:
+    def prepare_insert(self, b: int, full_grid: bool = False) -> bool:
+        """Capacity for b more rows per side; returns True if a buffer moved.
+        full_grid sizes the member scan for the whole capacity (blocks past the
+        device-side count exit at once), so the call can be replayed from a graph."""
+        moved = False
         for s in (0, 1):
             if self.bound(s) + b > self.cap[s]:
                 self._grow(s, self.bound(s) + b)
-            self.desc[s].n_bound = self.bound(s)
+                moved = True
+            self.desc[s].n_bound = self.cap[s] if full_grid else self.bound(s)
+        return moved
 
     def to_sets(self, lower: ReferenceSet, upper: ReferenceSet, dropped: bool) -> None:
         """Hand the final members (alive rows in physical order) to the ReferenceSets."""
@@ -478,6 +484,32 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         ready_ev.record(main)
         return slot
 
+    def search_and_insert(slot, n_pick):
+        """positions -> picked rows -> boundary searches -> device insertion: fixed
+        pointers and sizes per (batch slot, number of picks), so after the first
+        iteration of each kind the sequence replays as one CUDA graph."""
+        pos_d[:n_pick].copy_(pos_h[:n_pick], non_blocking=True)
+        sp = _device.stream()
+        _abi.call("rsr_compact", _abi.ptr(labels), count, _abi.LABEL_UNCLASSIFIED, _abi.ptr(idx),
+                  _abi.ptr(cnt), _abi.ptr(cscratch), sp)
+        _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
+                  _abi.ptr(pos_d), n_pick, _abi.ptr(x0), sp)
+        if config.boundary_search_enabled:
+            _abi.call("rsr_boundary_search", ctypes.byref(desc), int(threshold), _abi.ptr(x0),
+                      n_pick, _abi.ptr(out_refs), _abi.ptr(out_side), _abi.ptr(out_calls), sp)
+            cands, calls_p = out_refs, _abi.ptr(out_calls)
+        else:
+            phi.eval_into(x0, None, n_pick, M, phi_vals)
+            # SIDE_LOWER = 0 when Phi <= m', SIDE_UPPER = 1 otherwise
+            torch.gt(phi_vals[:n_pick], threshold, out=out_side[:n_pick])
+            cands, calls_p = x0, None
+        _abi.call("rsr_refset_insert", _abi.ptr(cands), _abi.ptr(out_side), n_pick, N, M, lo_p,
+                  up_p, calls_p, _abi.ptr(outcome), _abi.ptr(report_d[4:]), _abi.ptr(iscratch), sp)
+
+    # graphs only for the boundary-search path (the raw-sample path runs torch ops)
+    use_graphs = (config.boundary_search_enabled
+                  and os.environ.get("RSR_LOOP_GRAPHS", "1") != "0")
+    graphs: dict = {}
     trace: list[TraceRecord] = []
     terminated_by = "r_max"
     slot = launch_classify(pre.launch(0))
@@ -511,25 +543,24 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         n_pick = min(B, n_x)
         positions = rng.choice(n_x, size=n_pick, replace=False)
         pos_h.numpy()[:n_pick] = positions
-        pos_d[:n_pick].copy_(pos_h[:n_pick], non_blocking=True)
-        _abi.call("rsr_compact", _abi.ptr(labels), count, _abi.LABEL_UNCLASSIFIED, _abi.ptr(idx),
-                  _abi.ptr(cnt), _abi.ptr(cscratch), st_ptr)
-        _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
-                  _abi.ptr(pos_d), n_pick, _abi.ptr(x0), st_ptr)
-        pre.release(iteration, main)
-        if config.boundary_search_enabled:
-            _abi.call("rsr_boundary_search", ctypes.byref(desc), int(threshold), _abi.ptr(x0),
-                      n_pick, _abi.ptr(out_refs), _abi.ptr(out_side), _abi.ptr(out_calls), st_ptr)
-            cands, calls_p = out_refs, _abi.ptr(out_calls)
+        if refs.prepare_insert(n_pick, full_grid=use_graphs):
+            graphs.clear()  # device buffers moved: captured launches are stale
+        key = (slot, n_pick)
+        g = graphs.get(key)
+        # capture only the steady state (a full batch of picks): the tail of a run,
+        # where fewer than B samples stay unclassified, changes n_pick every iteration
+        if g is None and use_graphs and n_pick == B:
+            g = graphs[key] = torch.cuda.CUDAGraph()
+            g.capture_begin(capture_error_mode="relaxed")
+            search_and_insert(slot, n_pick)
+            g.capture_end()
+        if g is not None:
+            g.replay()
         else:
-            phi.eval_into(x0, None, n_pick, M, phi_vals)
-            # SIDE_LOWER = 0 when Phi <= m', SIDE_UPPER = 1 otherwise
-            torch.gt(phi_vals[:n_pick], threshold, out=out_side[:n_pick])
-            cands, calls_p, no_search_picks = x0, None, n_pick
-        refs.prepare_insert(n_pick)
-        _abi.call("rsr_refset_insert", _abi.ptr(cands), _abi.ptr(out_side), n_pick, N, M, lo_p,
-                  up_p, calls_p, _abi.ptr(outcome), _abi.ptr(report_d[4:]), _abi.ptr(iscratch),
-                  st_ptr)
+            search_and_insert(slot, n_pick)
+            if not config.boundary_search_enabled:
+                no_search_picks = n_pick
+        pre.release(iteration, main)
         refs.pending = n_pick
         searched = True
         iteration += 1
