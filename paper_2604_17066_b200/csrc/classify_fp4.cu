@@ -61,6 +61,12 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 #ifndef RSR_FP4_SPIN
 #define RSR_FP4_SPIN 0
 #endif
+// experiment knobs, both measured slower (spinning warps take issue slots from
+// the MMA / TMA warps): RSR_FP4_SPIN spins the MMA warp on buffer release,
+// RSR_FP4_EPI_SPIN the epilogue warps on accumulator completion
+#ifndef RSR_FP4_EPI_SPIN
+#define RSR_FP4_EPI_SPIN 0
+#endif
 constexpr int kEpiWarps = RSR_FP4_EPI_WARPS;
 constexpr int kColGroups = kEpiWarps / 4;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
@@ -506,7 +512,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         const int64_t t0 = (int64_t)(low ? j : j - p.nt_lower) * kTileN;
         if (++j == p.nt_total) j = 0;
         PROF_T(e0);
+#if RSR_FP4_EPI_SPIN
+        mbar_spin(smem_addr(&t_full[buf]), tphase);
+#else
         mbar_wait(smem_addr(&t_full[buf]), tphase);
+#endif
         PROF_T(e1);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN + c0;

@@ -403,3 +403,60 @@ def test_fp4_tile_widths_and_pad_rows(tile_n, n, m, monkeypatch):
         A.call("rsr_classify_fp4_ex", A.ptr(a), s, None, A.ptr(bl), kl, al, A.ptr(bu), ku, au, rb,
                A.ptr(flags), None, None, 0, A.stream_ptr())
         assert np.array_equal(flags.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n,m,batch", [(9, 2, 1), (9, 3, 17), (40, 2, 64), (7, 4, 300), (295, 2, 64)])
+def test_refset_insert_matches_sequential_insert(n, m, batch):
+    """rsr_refset_insert (csrc/refset.cu) over several batches against the oracle's
+    sequential ReferenceSet.insert (boundary.py:87-108): candidates drawn near each other
+    so batches contain duplicates, redundant candidates and candidates that drop
+    earlier members (of the same batch and of previous batches), both sides mixed."""
+    import ctypes
+    rng = np.random.default_rng(n * 31 + m * 7 + batch)
+    rb = A.fp4_row_bytes(n, m)
+    cap = 4096
+    sets = []
+    for side in (A.SIDE_LOWER, A.SIDE_UPPER):
+        rows = torch.zeros((cap, n), dtype=torch.uint8, device="cuda")
+        fp4 = torch.empty((cap, rb), dtype=torch.uint8, device="cuda")
+        A.call("rsr_encode_refs_fp4", None, 0, cap, n, m, side, A.ptr(fp4), rb, A.stream_ptr())
+        alive = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+        ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
+        d = A.RefsetDev(rows.data_ptr(), fp4.data_ptr(), alive.data_ptr(), ctr.data_ptr(), cap, cap)
+        sets.append((rows, fp4, alive, ctr, d))
+    report = torch.zeros(8, dtype=torch.int64, device="cuda")
+    scratch = torch.empty(A.call("rsr_refset_scratch", batch, rb), dtype=torch.uint8, device="cuda")
+    outcome = torch.empty(batch, dtype=torch.uint8, device="cuda")
+    calls = torch.arange(batch, dtype=torch.int64, device="cuda")
+    want = {A.SIDE_LOWER: oracle.RefSet(oracle.LOWER, 0), A.SIDE_UPPER: oracle.RefSet(oracle.UPPER, 0)}
+    base = rng.integers(0, m, size=n)
+    redundant = 0
+    for _ in range(4):
+        cands = np.clip(base[None, :] + rng.integers(-1, 2, size=(batch, n)), 0, m - 1).astype(np.uint8)
+        dup = rng.random(batch) < 0.2
+        cands[1:][dup[1:]] = cands[:-1][dup[1:]]
+        side = rng.integers(0, 2, size=batch).astype(np.uint8)
+        want_out = []
+        for c in range(batch):
+            o = want[int(side[c])].insert(cands[c])
+            want_out.append(1 if o == "inserted" else 2)
+            redundant += o == "redundant"
+        cd, sd = _dev(cands), _dev(side)
+        A.call("rsr_refset_insert", A.ptr(cd), A.ptr(sd), batch, n, m, ctypes.byref(sets[0][4]),
+               ctypes.byref(sets[1][4]), A.ptr(calls), A.ptr(outcome), A.ptr(report),
+               A.ptr(scratch), A.stream_ptr())
+        assert outcome.cpu().tolist() == want_out
+        rep = report.cpu().tolist()
+        assert rep[4] == redundant and rep[6] == batch * (batch - 1) // 2 and rep[7] == 0
+        for k, s in ((0, A.SIDE_LOWER), (1, A.SIDE_UPPER)):
+            rows, fp4, alive, ctr, _ = sets[k]
+            nrow = int(ctr[0].item())
+            live = alive[:nrow].cpu().numpy().astype(bool)
+            got = [tuple(int(v) for v in r) for r in rows[:nrow].cpu().numpy()[live]]
+            assert got == want[s].members
+            assert int(ctr[1].item()) == len(want[s].members) == rep[2 * k + 1]
+            # the FP4 rows of the members are the encoder's, pad rows past the count
+            enc = torch.empty_like(fp4)
+            A.call("rsr_encode_refs_fp4", A.ptr(rows), nrow, cap, n, m, s, A.ptr(enc), rb,
+                   A.stream_ptr())
+            assert torch.equal(enc, fp4)
