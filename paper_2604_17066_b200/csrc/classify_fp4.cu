@@ -125,6 +125,8 @@ struct Fp4Params {
   int64_t n_upper;
   int resident;     // every reference tile has its own stage: loaded once, reused by all groups
   const int64_t* S_dev;  // optional device sample count (<= S): rows [S_dev, S) are skipped
+  int a_z0;              // first sample-operand chunk loaded: 0 (A_up...) or cq (A_lo only)
+  int a_chunks;          // chunks loaded per sample row: 2 cq (both sides) or cq (one side)
 };
 
 // SW32 K-major descriptor: 8-row core groups 256 B apart, version 1, layout 6.
@@ -375,12 +377,13 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       PROF_T(p1);
       PROF_ADD(10, p1 - p0);
       if (elect_one()) {
+        // only the sample half (A_up / A_lo) a launch's reference sides need
         if (leader)
-          mbar_expect_tx(bar_af, 2 * a_buf_bytes);
+          mbar_expect_tx(bar_af, 2 * (uint32_t)(p.a_chunks * kChunkA));
         else
           mbar_arrive_leader(bar_af);
-        tma_load_3d_pair(sA0 + (uint32_t)ab * a_buf_bytes, &map_a, bar_af, 0,
-                         g * 2 * kRowsA + (int)rank * kRowsA, 0);
+        tma_load_3d_pair(sA0 + (uint32_t)ab * a_buf_bytes + (uint32_t)(p.a_z0 * kChunkA), &map_a,
+                         bar_af, 0, g * 2 * kRowsA + (int)rank * kRowsA, p.a_z0);
       }
       __syncwarp();
       if (p.resident) {
@@ -601,14 +604,16 @@ __global__ void clear_flags4_kernel(uint8_t* flags, int64_t S) {
 }
 
 // rows of `row_bytes` viewed as {32 B, rows, chunks} (strides {row_bytes, 32});
-// one box = `box_rows` rows x `chunks` chunks, landing chunk-major, 32 B swizzle.
+// one box = `box_rows` rows x `box_chunks` (default: all) chunks, landing
+// chunk-major, 32 B swizzle.
 int make_map3(CUtensorMap* map, const void* base, int64_t rows, int row_bytes, int chunks,
-              int box_rows) {
+              int box_rows, int box_chunks = 0) {
   auto enc = tensor_map_encoder();
   RSR_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  if (box_chunks <= 0) box_chunks = chunks;
   cuuint64_t dims[3] = {(cuuint64_t)kChunk, (cuuint64_t)rows, (cuuint64_t)chunks};
   cuuint64_t strides[2] = {(cuuint64_t)row_bytes, (cuuint64_t)kChunk};
-  cuuint32_t box[3] = {(cuuint32_t)kChunk, (cuuint32_t)box_rows, (cuuint32_t)chunks};
+  cuuint32_t box[3] = {(cuuint32_t)kChunk, (cuuint32_t)box_rows, (cuuint32_t)box_chunks};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
@@ -640,8 +645,12 @@ int launch_fp4(const Fp4Call& c) {
   const bool want_first = c.first[0] != nullptr || c.first[1] != nullptr;
   const int64_t nt_l = rsr::ceil_div(c.n[0], TN), nt_u = rsr::ceil_div(c.n[1], TN);
   const int cq = c.row_bytes / kChunk;
-  CUtensorMap ma;
-  int rc = make_map3(&ma, c.A, c.S, 2 * c.row_bytes, 2 * cq, kRowsA);
+  // sample-operand maps: both halves, or only the half of a launch's single side
+  // (a launch against upper references alone streams half the sample bytes)
+  CUtensorMap ma_both, ma_half;
+  int rc = make_map3(&ma_both, c.A, c.S, 2 * c.row_bytes, 2 * cq, kRowsA);
+  if (rc) return rc;
+  rc = make_map3(&ma_half, c.A, c.S, 2 * c.row_bytes, 2 * cq, kRowsA, cq);
   if (rc) return rc;
 
   Fp4Params p;
@@ -711,6 +720,10 @@ int launch_fp4(const Fp4Call& c) {
     }
     q.n_lower = rows[0];
     q.n_upper = rows[1];
+    const bool has_l = hi[0] > lo[0], has_u = hi[1] > lo[1];
+    q.a_chunks = has_l && has_u ? 2 * cq : cq;
+    q.a_z0 = has_l && !has_u ? cq : 0;
+    const CUtensorMap& ma = has_l && has_u ? ma_both : ma_half;
     CUtensorMap cl, cu;
     rc = make_map3(&cl, base[0] ? base[0] : base[1], base[0] ? rows[0] : rows[1], c.row_bytes, cq,
                    TN / 2);
