@@ -21,6 +21,8 @@ buf = (ctypes.c_ulonglong * 12)()
 K = int(os.environ.get("K", "10000"))
 S = int(os.environ.get("S", str(1 << 20)))
 lower, upper = W.cfg2_refs(0, 295, K, K)
+if os.environ.get("UPPER_ONLY"):  # cfg4-like: survival references only
+    lower = lower[:0]
 lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
 up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
 batch = P.sample_batch(P.ComponentDistribution.iid(295, [0.1, 0.9]), S, seed=0)
