@@ -205,7 +205,7 @@ def stage1_find_references(model: SystemModel, dist: ComponentDistribution, conf
     caller = torch.cuda.current_stream()
     loop_stream = _high_priority_stream()
     loop_stream.wait_stream(caller)
-    use_async = (not comm.distributed and os.environ.get("RSR_SYNC_LOOP") != "1"
+    use_async = (os.environ.get("RSR_SYNC_LOOP") != "1"
                  and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.FP4_MAX_ROW_BYTES
                  and dist.n_states == model.n_component_states
                  and config.parallel_searches <= 4096)
@@ -484,16 +484,22 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         ready_ev.record(main)
         return slot
 
-    def search_and_insert(slot, n_pick):
-        """positions -> picked rows -> boundary searches -> device insertion: fixed
-        pointers and sizes per (batch slot, number of picks), so after the first
-        iteration of each kind the sequence replays as one CUDA graph."""
-        pos_d[:n_pick].copy_(pos_h[:n_pick], non_blocking=True)
+    def gather_local(slot, n_local, out):
+        """Rows of this rank's picks (local positions in pos_h) -> out[:n_local]."""
+        pos_d[:n_local].copy_(pos_h[:n_local], non_blocking=True)
         sp = _device.stream()
         _abi.call("rsr_compact", _abi.ptr(labels), count, _abi.LABEL_UNCLASSIFIED, _abi.ptr(idx),
                   _abi.ptr(cnt), _abi.ptr(cscratch), sp)
         _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
-                  _abi.ptr(pos_d), n_pick, _abi.ptr(x0), sp)
+                  _abi.ptr(pos_d), n_local, _abi.ptr(out), sp)
+
+    def search_and_insert(slot, n_pick, gather=True):
+        """positions -> picked rows -> boundary searches -> device insertion: fixed
+        pointers and sizes per (batch slot, number of picks), so after the first
+        iteration of each kind the sequence replays as one CUDA graph."""
+        if gather:
+            gather_local(slot, n_pick, x0)
+        sp = _device.stream()
         if config.boundary_search_enabled:
             _abi.call("rsr_boundary_search", ctypes.byref(desc), int(threshold), _abi.ptr(x0),
                       n_pick, _abi.ptr(out_refs), _abi.ptr(out_side), _abi.ptr(out_calls), sp)
@@ -507,7 +513,8 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
                   up_p, calls_p, _abi.ptr(outcome), _abi.ptr(report_d[4:]), _abi.ptr(iscratch), sp)
 
     # graphs only for the boundary-search path (the raw-sample path runs torch ops)
-    use_graphs = (config.boundary_search_enabled
+    # on one rank (a multi-rank iteration exchanges picked rows through the host)
+    use_graphs = (config.boundary_search_enabled and not comm.distributed
                   and os.environ.get("RSR_LOOP_GRAPHS", "1") != "0")
     graphs: dict = {}
     trace: list[TraceRecord] = []
@@ -520,6 +527,9 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
     while True:
         ready_ev.synchronize()
         n_l, n_u, n_x = int(rep[0]), int(rep[1]), int(rep[2])
+        if comm.distributed:  # shard counts -> batch counts; per-rank unclassified counts
+            per_rank = comm.allgather_i64(n_x)
+            n_l, n_u, n_x = (int(v) for v in comm.allreduce_sum_i64([n_l, n_u, n_x]))
         if searched:
             refs.known = [int(rep[4]), int(rep[6])]
             refs.pending = 0
@@ -542,7 +552,23 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         rng = np.random.default_rng([config.seed, iteration])
         n_pick = min(B, n_x)
         positions = rng.choice(n_x, size=n_pick, replace=False)
-        pos_h.numpy()[:n_pick] = positions
+        if comm.distributed:
+            # global positions (rank-ordered unclassified list) -> owners; every rank
+            # gathers its own rows, then all picked rows in pick order on every rank
+            owner, local = global_pick_owners(per_rank, np.asarray(positions, dtype=np.int64))
+            mine = np.flatnonzero(owner == comm.rank)
+            pos_h.numpy()[:len(mine)] = local[mine]
+            rows = torch.empty((len(mine), N), dtype=torch.uint8, device=dev)
+            if len(mine):
+                gather_local(slot, len(mine), rows)
+            gathered = comm.allgather_rows(rows, np.bincount(owner, minlength=comm.world)).to(dev)
+            order = np.argsort(owner, kind="stable")
+            inv = np.empty_like(order)
+            inv[order] = np.arange(len(order))
+            x0[:n_pick].copy_(gathered.index_select(
+                0, torch.as_tensor(inv, dtype=torch.int64, device=dev)))
+        else:
+            pos_h.numpy()[:n_pick] = positions
         if refs.prepare_insert(n_pick, full_grid=use_graphs):
             graphs.clear()  # device buffers moved: captured launches are stale
         key = (slot, n_pick)
@@ -557,7 +583,7 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         if g is not None:
             g.replay()
         else:
-            search_and_insert(slot, n_pick)
+            search_and_insert(slot, n_pick, gather=not comm.distributed)
             if not config.boundary_search_enabled:
                 no_search_picks = n_pick
         pre.release(iteration, main)

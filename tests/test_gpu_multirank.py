@@ -25,9 +25,9 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, sync_loop="0"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank), RSR_SYNC_LOOP=sync_loop)
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path.insert(0, os.path.dirname(here))
@@ -61,12 +61,16 @@ def _worker(rank, world, port, case, q):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("loop", ["async", "sync"])
 @pytest.mark.parametrize("case", CASES)
-def test_two_rank_workflow_matches_single_device(case):
+def test_two_rank_workflow_matches_single_device(case, loop):
+    # async: device-resident reference sets, rows of the picks exchanged per
+    # iteration; sync: the host-resolved insertion path
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q, "1" if loop == "sync" else "0"))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=280) for _ in range(2))
