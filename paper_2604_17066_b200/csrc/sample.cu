@@ -202,7 +202,10 @@ __device__ __forceinline__ void fp4_quad_fast(const uint8_t* st, uint32_t base, 
 // staging buffer double-buffered, so one barrier per chunk separates the
 // generator phase from the store phase (the next chunk's generator writes the
 // other buffer).
-template <int MT>  // 2, 3: specialised state count; 0: any M
+// C32: every Philox counter of the launch fits 32 bits (flat draws < 2^34), so
+// the first round's 64x64 multiply is a 64x32 one (two IMAD.WIDE fewer per block
+// on the FMA pipe, which bounds this kernel).
+template <int MT, bool C32>  // MT 2, 3: specialised state count; 0: any M
 __global__ void __launch_bounds__(kRowThreads, RSR_SAMPLE_MINB)
 sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
                    int64_t start_row, int64_t count, uint8_t* __restrict__ states,
@@ -232,7 +235,10 @@ sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed
     const int ostep = 4 * (int)blockDim.x, nstep = ostep % N;
     for (int64_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x, o0 += ostep) {
       uint64_t w[4];
-      rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+      if (C32)
+        rsr::philox4x64_10((uint64_t)(uint32_t)(b + 1), seed, gen, w);
+      else
+        rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
       const unsigned long long* Tn = T + n0 * Mm1;
       n0 += nstep;
       if (n0 >= N) n0 -= N;
@@ -542,7 +548,11 @@ extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_state
   const size_t smem = ((size_t)(N + kTExtra) * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 +
                       2 * (size_t)st_bytes;
   RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample_fp4: N*(M-1) too large for shared memory");
-  auto kern = M == 2 ? sample_rows_kernel<2> : M == 3 ? sample_rows_kernel<3> : sample_rows_kernel<0>;
+  const bool c32 = ((start + count) * (int64_t)N + 3) / 4 + 1 < ((int64_t)1 << 32);
+  auto kern = c32 ? (M == 2 ? sample_rows_kernel<2, true> : M == 3 ? sample_rows_kernel<3, true>
+                                                                 : sample_rows_kernel<0, true>)
+                  : (M == 2 ? sample_rows_kernel<2, false> : M == 3 ? sample_rows_kernel<3, false>
+                                                                  : sample_rows_kernel<0, false>);
   if (smem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 0, per_sm = 0;
