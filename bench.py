@@ -377,6 +377,18 @@ def run_ours(args):
                 "frac_of_int8_peak": achieved / int8_peak,
                 "cublas_int8_tops": cublas_peak, "cublas_int8_source": cublas_src,
                 "frac_of_cublas_int8": achieved / cublas_peak}
+    if args.method == "bits":
+        # the CUDA-core variant is bound by the integer ALU pipe: one LOP3
+        # (acc |= x & r) per 32-bit thermometer word and pair
+        words = -(-N_COMP * (2 - 1) // 32)
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        alu_peak = sm_count * 64 * 1.965e9 / 1e12  # 64 LOP3 lanes/clk/SM at 1965 MHz
+        ach = S * K * words / (kern_avg * 1e-3) / 1e12
+        roofline.update({"bound": "alu", "achieved": ach, "peak": alu_peak,
+                         "unit": "T word-ops/s", "frac": ach / alu_peak, "ops_per_pair": words,
+                         "peak_source": (f"ALU pipe: {sm_count} SMs x 64 LOP3/clk x 1965 MHz "
+                                         "(B300_MICROARCH: alu rt_SMSP = 2)"),
+                         "tensor_equivalent_tops": achieved})
 
     # ---- end to end through the public API with host buffers
     e2e = None
