@@ -26,7 +26,7 @@
 //     whole-tile stages; the leader issues cq MMAs M=256 N=240 K=64 per tile;
 //   * TMEM: accumulators at columns 0 and 240 (two buffers, the epilogue of
 //     tile j overlaps the MMAs of tile j+1), scale factors at 480..511;
-//   * 8 epilogue warps per CTA read the 128 x 240 accumulator with packed
+//   * 4 epilogue warps per CTA read the 128 x 240 accumulator with packed
 //     16-bit loads (tcgen05.ld 32x32b .pack::16b: each accumulator is the
 //     denormal count * 2^-149, so its low 16 bits are the count), min-reduce
 //     with 16x2 SIMD mins, OR a hit bit per side, and optionally keep the
@@ -50,10 +50,13 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 // accumulator out of TMEM is the epilogue's cost (tools/tmem_bw.cu: 32x32b
 // loads reach 175 / 324 / 459 B/clk per SM with 4 / 8 / 16 warps, and twice that
 // with .pack::16b); kEpiWarps warps (kEpiWarps / 4 per TMEM lane quarter) each
-// own 240 / (kEpiWarps / 4) columns.  Measured on cfg2 (kernel ms): 4 warps
-// 1.70, 8 warps 1.67, 12 warps 1.67, 16 warps 1.76.
+// own 240 / (kEpiWarps / 4) columns.  With 4 warps each row's whole tile sits
+// in one thread (120 packed registers, 254 registers per thread) and the group
+// end needs no cross-warp exchange.  Measured (kernel ms, current kernel):
+// cfg2 4 warps 1.607 / 8 warps 1.617 / 16 warps 1.70; cfg4 K=10^3 0.404 / 0.412;
+// K=10^4 3.143 / 3.18 (an earlier kernel version had preferred 8).
 #ifndef RSR_FP4_EPI_WARPS
-#define RSR_FP4_EPI_WARPS 8
+#define RSR_FP4_EPI_WARPS 4
 #endif
 #ifndef RSR_FP4_GROUP_RELEASE
 #define RSR_FP4_GROUP_RELEASE 0
