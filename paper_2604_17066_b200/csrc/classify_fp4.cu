@@ -128,8 +128,6 @@ struct Fp4Params {
   int64_t n_upper;
   int resident;     // every reference tile has its own stage: loaded once, reused by all groups
   const int64_t* S_dev;  // optional device sample count (<= S): rows [S_dev, S) are skipped
-  int a_z0;              // first sample-operand chunk loaded: 0 (A_up...) or cq (A_lo only)
-  int a_chunks;          // chunks loaded per sample row: 2 cq (both sides) or cq (one side)
 };
 
 // SW32 K-major descriptor: 8-row core groups 256 B apart, version 1, layout 6.
@@ -294,12 +292,13 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * b_stage_bytes);
   uint64_t* b_full = bars;
   uint64_t* b_empty = bars + p.stages;
-  uint64_t* a_full = bars + 2 * p.stages;  // [a_bufs <= 4]
-  uint64_t* a_empty = a_full + 4;          // [a_bufs <= 4]
-  uint64_t* t_full = a_full + 8;           // [kBufs <= 4]
-  uint64_t* t_empty = a_full + 12;         // [kBufs <= 4]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 16);
-  uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 18);  // [kColGroups][128] hit bits
+  // sample buffers are filled and released per half: [buffer][0 = A_lo, 1 = A_up]
+  uint64_t* a_full = bars + 2 * p.stages;  // [a_bufs <= 4][2]
+  uint64_t* a_empty = a_full + 8;          // [a_bufs <= 4][2]
+  uint64_t* t_full = a_full + 16;          // [kBufs <= 4]
+  uint64_t* t_empty = a_full + 20;         // [kBufs <= 4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 24);
+  uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 26);  // [kColGroups][128] hit bits
   int64_t* xfirst = reinterpret_cast<int64_t*>(xchg + kColGroups * 128) - 256;  // [1..][2][128]
 
   const int warp = threadIdx.x >> 5;
@@ -325,7 +324,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_init(smem_addr(&b_full[i]), 2);
       mbar_init(smem_addr(&b_empty[i]), 1);
     }
-    for (int i = 0; i < p.a_bufs; ++i) {
+    for (int i = 0; i < 2 * p.a_bufs; ++i) {
       mbar_init(smem_addr(&a_full[i]), 2);
       mbar_init(smem_addr(&a_empty[i]), 1);
     }
@@ -362,7 +361,23 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
-  const int rot = (int)(((int64_t)cluster * p.nt_total) / n_clusters);
+  // Tile sequence of every group (all three roles walk it): the lower tiles,
+  // then the upper ones, each side rotated per cluster to spread L2 load.
+  // Side-ordered, the lower half of a sample buffer (A_lo) is free once the
+  // group's lower tiles are issued, so the next group's A_lo loads while the
+  // upper tiles run (and A_up while the next lower tiles run): single-buffered
+  // wide rows (M = 3: 80 KB per buffer) still overlap their sample loads.
+  const int nt_l = p.nt_lower, nt_u = p.nt_total - p.nt_lower;
+  const int rot_l = (int)(((int64_t)cluster * nt_l) / n_clusters);
+  const int rot_u = (int)(((int64_t)cluster * nt_u) / n_clusters);
+  auto tile_of = [&](int jj) -> int {
+    if (jj < nt_l) {
+      const int j = rot_l + jj;
+      return j >= nt_l ? j - nt_l : j;
+    }
+    const int j = rot_u + (jj - nt_l);
+    return nt_l + (j >= nt_u ? j - nt_u : j);
+  };
   PROF_DECL;
 
   if (warp == 0) {
@@ -374,21 +389,25 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     for (int g = cluster; g < n_groups; g += n_clusters, ++gi) {
       const int ab = gi % p.a_bufs;
       const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
-      const uint32_t bar_af = smem_addr(&a_full[ab]);
-      PROF_T(p0);
-      mbar_wait(smem_addr(&a_empty[ab]), a_par ^ 1);
-      PROF_T(p1);
-      PROF_ADD(10, p1 - p0);
-      if (elect_one()) {
-        // only the sample half (A_up / A_lo) a launch's reference sides need
-        if (leader)
-          mbar_expect_tx(bar_af, 2 * (uint32_t)(p.a_chunks * kChunkA));
-        else
-          mbar_arrive_leader(bar_af);
-        tma_load_3d_pair(sA0 + (uint32_t)ab * a_buf_bytes + (uint32_t)(p.a_z0 * kChunkA), &map_a,
-                         bar_af, 0, g * 2 * kRowsA + (int)rank * kRowsA, p.a_z0);
+      // only the sample halves the launch's reference sides need, A_lo first
+      for (int h = 0; h < 2; ++h) {
+        if (h == 0 ? nt_l == 0 : nt_u == 0) continue;
+        const uint32_t bar_af = smem_addr(&a_full[2 * ab + h]);
+        const int z0 = h == 0 ? p.cq : 0;
+        PROF_T(p0);
+        mbar_wait(smem_addr(&a_empty[2 * ab + h]), a_par ^ 1);
+        PROF_T(p1);
+        PROF_ADD(10, p1 - p0);
+        if (elect_one()) {
+          if (leader)
+            mbar_expect_tx(bar_af, 2 * (uint32_t)(p.cq * kChunkA));
+          else
+            mbar_arrive_leader(bar_af);
+          tma_load_3d_pair(sA0 + (uint32_t)ab * a_buf_bytes + (uint32_t)(z0 * kChunkA), &map_a,
+                           bar_af, 0, g * 2 * kRowsA + (int)rank * kRowsA, z0);
+        }
+        __syncwarp();
       }
-      __syncwarp();
       if (p.resident) {
         // small reference sets: tile j lives in stage j for the whole launch
         if (gi == 0) {
@@ -408,12 +427,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         continue;
       }
-      int j = rot;
       for (int jj = 0; jj < p.nt_total; ++jj) {
+        const int j = tile_of(jj);
         const bool low = j < p.nt_lower;
         const CUtensorMap* map = low ? &map_lower : &map_upper;
         const int y = (low ? j : j - p.nt_lower) * kTileN + (int)rank * kHalfRows;
-        if (++j == p.nt_total) j = 0;
         PROF_T(q0);
         mbar_wait(bar_b_empty + 8 * stage, phase ^ 1);
         PROF_T(q1);
@@ -448,59 +466,68 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       uint32_t phase = 0, buf = 0, tphase = 0;
       for (int g = cluster; g < n_groups; g += n_clusters, ++gi) {
         const int ab = gi % p.a_bufs;
-        PROF_T(w0);
-        mbar_wait(smem_addr(&a_full[ab]), (uint32_t)(gi / p.a_bufs) & 1);
-        PROF_T(w1);
-        PROF_ADD(9, w1 - w0);
+        const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
         PROF_ADD(11, 1);
-        tc_fence_after();
         const uint32_t a_up = a_lo0 + (uint32_t)ab * (a_buf_bytes >> 4);
         const uint32_t a_dn = a_up + (uint32_t)cq * kAstep;
         PROF_T(l0);
         // lean per-tile bookkeeping: this warp's instruction count per tile is
-        // on the critical path once a tile is only a few hundred MMA cycles
-        int j = rot;
-        for (int jj = 0; jj < p.nt_total; ++jj) {
-          const uint32_t al = j < p.nt_lower ? a_dn : a_up;
-          // resident B: tile j sits in stage j, whose only phase (0) completes once
-          const int bs = p.resident ? j : stage;
-          const uint32_t bpar = p.resident ? 0u : phase;
-          if (++j == p.nt_total) j = 0;
-          const uint32_t d = tm0 + buf * kTileN;
-          const uint32_t bl = b_lo0 + (uint32_t)bs * (b_stage_bytes >> 4);
-          PROF_T(m0);
-#if RSR_FP4_SPIN
-          mbar_spin(bar_t_empty + 8 * buf, tphase ^ 1);
-#else
-          mbar_wait(bar_t_empty + 8 * buf, tphase ^ 1);
-#endif
-          PROF_T(m1);
-          mbar_wait(bar_b_full + 8 * bs, bpar);
-          PROF_T(m2);
-          PROF_ADD(1, m1 - m0);
-          PROF_ADD(0, m2 - m1);
-          PROF_ADD(7, 1);
+        // on the critical path once a tile is only a few hundred MMA cycles, so
+        // each side is its own loop with an incremental (rotated) tile index
+        for (int h = 0; h < 2; ++h) {
+          const int cnt = h == 0 ? nt_l : nt_u;
+          if (cnt == 0) continue;
+          PROF_T(w0);
+          mbar_wait(smem_addr(&a_full[2 * ab + h]), a_par);  // this side's sample half landed
+          PROF_T(w1);
+          PROF_ADD(9, w1 - w0);
           tc_fence_after();
-          if (elect_one()) {
-            for (int ks = 0; ks < cq; ++ks)
-              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
-            umma_commit_pair(bar_t_full + 8 * buf);
-            if (!p.resident) umma_commit_pair(bar_b_empty + 8 * stage);
+          const uint32_t al = h == 0 ? a_dn : a_up;
+          const int base = h == 0 ? 0 : nt_l;
+          int jt = h == 0 ? rot_l : rot_u;
+          for (int t = 0; t < cnt; ++t) {
+            const int j = base + jt;
+            if (++jt == cnt) jt = 0;
+            // resident B: tile j sits in stage j, whose only phase (0) completes once
+            const int bs = p.resident ? j : stage;
+            const uint32_t bpar = p.resident ? 0u : phase;
+            const uint32_t d = tm0 + buf * kTileN;
+            const uint32_t bl = b_lo0 + (uint32_t)bs * (b_stage_bytes >> 4);
+            PROF_T(m0);
+#if RSR_FP4_SPIN
+            mbar_spin(bar_t_empty + 8 * buf, tphase ^ 1);
+#else
+            mbar_wait(bar_t_empty + 8 * buf, tphase ^ 1);
+#endif
+            PROF_T(m1);
+            mbar_wait(bar_b_full + 8 * bs, bpar);
+            PROF_T(m2);
+            PROF_ADD(1, m1 - m0);
+            PROF_ADD(0, m2 - m1);
+            PROF_ADD(7, 1);
+            tc_fence_after();
+            if (elect_one()) {
+              for (int ks = 0; ks < cq; ++ks)
+                umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
+              umma_commit_pair(bar_t_full + 8 * buf);
+              if (!p.resident) umma_commit_pair(bar_b_empty + 8 * stage);
+            }
+            __syncwarp();
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            if (++buf == kBufs) {
+              buf = 0;
+              tphase ^= 1;
+            }
           }
+          // the side's sample half is released once its MMAs complete
+          if (elect_one()) umma_commit_pair(smem_addr(&a_empty[2 * ab + h]));
           __syncwarp();
-          if (++stage == p.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
-          if (++buf == kBufs) {
-            buf = 0;
-            tphase ^= 1;
-          }
         }
         PROF_T(l1);
         PROF_ADD(2, l1 - l0);
-        if (elect_one()) umma_commit_pair(smem_addr(&a_empty[ab]));
-        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -512,11 +539,10 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     for (int g = cluster; g < n_groups; g += n_clusters) {
       uint32_t hit = 0;
       int64_t first[2] = {INT64_MAX, INT64_MAX};
-      int j = rot;
       for (int jj = 0; jj < p.nt_total; ++jj) {
+        const int j = tile_of(jj);
         const bool low = j < p.nt_lower;
         const int64_t t0 = (int64_t)(low ? j : j - p.nt_lower) * kTileN;
-        if (++j == p.nt_total) j = 0;
         PROF_T(e0);
 #if RSR_FP4_EPI_SPIN
         mbar_spin(smem_addr(&t_full[buf]), tphase);
@@ -648,12 +674,11 @@ int launch_fp4(const Fp4Call& c) {
   const bool want_first = c.first[0] != nullptr || c.first[1] != nullptr;
   const int64_t nt_l = rsr::ceil_div(c.n[0], TN), nt_u = rsr::ceil_div(c.n[1], TN);
   const int cq = c.row_bytes / kChunk;
-  // sample-operand maps: both halves, or only the half of a launch's single side
-  // (a launch against upper references alone streams half the sample bytes)
-  CUtensorMap ma_both, ma_half;
-  int rc = make_map3(&ma_both, c.A, c.S, 2 * c.row_bytes, 2 * cq, kRowsA);
-  if (rc) return rc;
-  rc = make_map3(&ma_half, c.A, c.S, 2 * c.row_bytes, 2 * cq, kRowsA, cq);
+  // sample operand: one box = one half (A_up or A_lo) of 128 rows; a launch
+  // loads only the halves its reference sides need (upper references alone
+  // stream half the sample bytes)
+  CUtensorMap ma;
+  int rc = make_map3(&ma, c.A, c.S, 2 * c.row_bytes, 2 * cq, kRowsA, cq);
   if (rc) return rc;
 
   Fp4Params p;
@@ -665,7 +690,7 @@ int launch_fp4(const Fp4Call& c) {
   p.first_upper = c.first[1];
   const size_t max_smem = 227 * 1024;
   // align slack, barriers (<= 16 stages x 2 + 18), hit exchange, first-match exchange
-  const size_t bars_bytes = (2 * 16 + 18) * 8;
+  const size_t bars_bytes = (2 * 16 + 26) * 8;
   const size_t fixed = 1024 + bars_bytes + kColGroups * 512 +
                        (want_first ? (kColGroups - 1) * 2048 : 0);
   const size_t a_buf = (size_t)2 * cq * kChunkA, b_stage = (size_t)cq * (TN / 2) * kChunk;
@@ -723,10 +748,7 @@ int launch_fp4(const Fp4Call& c) {
     }
     q.n_lower = rows[0];
     q.n_upper = rows[1];
-    const bool has_l = hi[0] > lo[0], has_u = hi[1] > lo[1];
-    q.a_chunks = has_l && has_u ? 2 * cq : cq;
-    q.a_z0 = has_l && !has_u ? cq : 0;
-    const CUtensorMap& ma = has_l && has_u ? ma_both : ma_half;
+
     CUtensorMap cl, cu;
     rc = make_map3(&cl, base[0] ? base[0] : base[1], base[0] ? rows[0] : rows[1], c.row_bytes, cq,
                    TN / 2);
