@@ -153,3 +153,22 @@ def test_device_calls_fail_loudly_without_cuda():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         P.sample_batch(P.ComponentDistribution.iid(3, [0.5, 0.5]), 10, seed=0)
+
+
+@pytest.mark.timeout(180)
+def test_bench_reference_arm_runs_on_cpu():
+    """`bench.py --impl reference` (the driver's reference arm: the oracle port of the
+    reference classifier on the host cores) prints one well-formed JSON line."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "1"], cwd=root, env=env, check=True,
+                         capture_output=True, text=True, timeout=170).stdout
+    line = json.loads([x for x in out.splitlines() if x.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "pairs/s"
+    assert line["e2e"]["value"] == line["value"] and line["cpu_baseline"]["cores"] >= 1
+    assert line["config"]["ref_states"] == 20_000
