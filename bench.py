@@ -549,6 +549,7 @@ def measure_loop(config, parallel_searches, cpu_seconds=None):
     import torch
 
     import paper_2604_17066_b200 as P
+    from paper_2604_17066_b200 import _abi
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _specs import device_model
     spec, probs, kw, thresholds, desc = loop_problem(config, parallel_searches)
@@ -571,9 +572,14 @@ def measure_loop(config, parallel_searches, cpu_seconds=None):
     clk = ClockSampler(0)  # NVML init outside the timed region
     with clk:
         t0 = time.perf_counter()
+        # thresholds share the sample stream: the drawn batches stay in HBM between
+        # them, as in multistate_pmf (workflow._BatchCache)
+        from paper_2604_17066_b200.workflow import _BatchCache
+        cache = (_BatchCache(cfg.n_samples, _abi.fp4_row_bytes(dist.n_components, dist.n_states))
+                 if len(thresholds) > 1 and os.environ.get("RSR_BATCH_CACHE", "1") != "0" else None)
         for thr in thresholds:
             ts = time.perf_counter()
-            s1 = P.stage1_find_references(model, dist, cfg, thr)
+            s1 = P.stage1_find_references(model, dist, cfg, thr, _batch_cache=cache)
             t1 = time.perf_counter()
             s1_first = s1_first or s1
             if config == "cfg1":

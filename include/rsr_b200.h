@@ -300,6 +300,12 @@ int rsr_gather_rows_dev(const uint8_t* src, int64_t src_stride, int copy_bytes,
 /* flags[idx[i]] |= vals[i] for i < *count_dev (at most cap). */
 int rsr_scatter_or_dev(const uint8_t* vals, const int64_t* idx, const int64_t* count_dev,
                        int64_t cap, uint8_t* flags, void* stream);
+/* rsr_gather_picks with the rows decoded from the FP4 sample operand
+ * (x_n = number of set [x_n >= k] elements of the A_lo half): for batches kept
+ * only in their classifier layout. */
+int rsr_gather_picks_fp4(const uint8_t* fp4, int row_bytes, int n_components, int n_states,
+                         const int64_t* idx, const int64_t* pos, int64_t count, uint8_t* out,
+                         void* stream);
 /* out[i] = states[idx[pos[i]]]: rows of the picked unclassified samples
  * (workflow.py:172-176 with the positions drawn on the host). */
 int rsr_gather_picks(const uint8_t* states, int n_components, const int64_t* idx,

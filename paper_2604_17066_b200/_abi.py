@@ -108,6 +108,7 @@ EXPORTED = {
     "rsr_refset_insert": (_I, [_P, _P, _I64, _I, _I, ctypes.POINTER(RefsetDev),
                                ctypes.POINTER(RefsetDev), _P, _P, _P, _P, _P]),
     "rsr_gather_picks": (_I, [_P, _I, _P, _P, _I64, _P, _P]),
+    "rsr_gather_picks_fp4": (_I, [_P, _I, _I, _I, _P, _P, _I64, _P, _P]),
     "rsr_gather_rows_dev": (_I, [_P, _I64, _I, _P, _P, _I64, _P, _I64, _P]),
     "rsr_scatter_or_dev": (_I, [_P, _P, _P, _I64, _P, _P]),
     "rsr_classify_fp4_dev": (_I, [_P, _I64, _P, _P, _I64, _P, _I64, _I, _P, _I, _P]),

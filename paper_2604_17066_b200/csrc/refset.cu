@@ -322,7 +322,38 @@ __global__ void scatter_or_dev_kernel(const uint8_t* __restrict__ vals,
     if (vals[i]) flags[idx[i]] |= vals[i];
 }
 
+// Same rows decoded from the FP4 sample operand (A_lo half: element n(M-1)+k-1
+// is e2m1 1.0 = 0x2 iff x_n >= k, so x_n = sum_k of those bits).
+__global__ void gather_picks_fp4_kernel(const uint8_t* __restrict__ fp4, int row_bytes, int N,
+                                        int M, const int64_t* __restrict__ idx,
+                                        const int64_t* __restrict__ pos, uint8_t* __restrict__ out) {
+  const int i = blockIdx.x;
+  const uint8_t* lo = fp4 + idx[pos[i]] * (int64_t)(2 * row_bytes) + row_bytes;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    int x = 0;
+    for (int k = 1; k < M; ++k) {
+      const int e = n * (M - 1) + k - 1;
+      x += (lo[e >> 1] >> (4 * (e & 1) + 1)) & 1;
+    }
+    out[(int64_t)i * N + n] = (uint8_t)x;
+  }
+}
+
 }  // namespace
+
+extern "C" int rsr_gather_picks_fp4(const uint8_t* fp4, int row_bytes, int n_components,
+                                    int n_states, const int64_t* idx, const int64_t* pos,
+                                    int64_t count, uint8_t* out, void* stream) {
+  RSR_REQUIRE(n_components >= 1 && n_states >= 2 && count >= 0 && count <= 0x7fffffff,
+              "rsr_gather_picks_fp4: bad shape");
+  RSR_REQUIRE(row_bytes == rsr_fp4_row_bytes(n_components, n_states),
+              "rsr_gather_picks_fp4: row_bytes must be %d", rsr_fp4_row_bytes(n_components, n_states));
+  if (count == 0) return RSR_OK;
+  RSR_REQUIRE(fp4 && idx && pos && out, "rsr_gather_picks_fp4: null pointer");
+  gather_picks_fp4_kernel<<<(unsigned)count, 128, 0, rsr::as_stream(stream)>>>(
+      fp4, row_bytes, n_components, n_states, idx, pos, out);
+  return rsr::check_launch("gather_picks_fp4_kernel");
+}
 
 extern "C" int rsr_gather_rows_dev(const uint8_t* src, int64_t src_stride, int copy_bytes,
                                    const int64_t* idx, const int64_t* count_dev, int64_t cap,

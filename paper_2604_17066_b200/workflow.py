@@ -189,7 +189,8 @@ def _classify_shard(model, pending, lower, upper, comm):
 
 
 def stage1_find_references(model: SystemModel, dist: ComponentDistribution, config: RunConfig,
-                           threshold: int, comm: Comm | None = None) -> Stage1Result:
+                           threshold: int, comm: Comm | None = None, *,
+                           _batch_cache: "_BatchCache | None" = None) -> Stage1Result:
     """Discover boundary reference sets for one threshold (workflow.py:122-195)."""
     _check_threshold(model, threshold)
     comm = comm or Comm.single()
@@ -209,10 +210,13 @@ def stage1_find_references(model: SystemModel, dist: ComponentDistribution, conf
                  and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.FP4_MAX_ROW_BYTES
                  and dist.n_states == model.n_component_states
                  and config.parallel_searches <= 4096)
-    loop = _stage1_loop_async if use_async else _stage1_loop
     with torch.cuda.stream(loop_stream):
-        result = loop(model, dist, config, threshold, comm, phi, lower, upper, start, count, H,
-                      t_start, phi_start)
+        if use_async:
+            result = _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper,
+                                        start, count, H, t_start, phi_start, _batch_cache)
+        else:
+            result = _stage1_loop(model, dist, config, threshold, comm, phi, lower, upper, start,
+                                  count, H, t_start, phi_start)
     caller.wait_stream(loop_stream)
     return result
 
@@ -346,11 +350,39 @@ class _DeviceRefs:
             target._fp4[self.M] = [self.fp4[s], n]
 
 
+class _BatchCache:
+    """FP4 sample operands by generation, kept in HBM across the thresholds of
+    `multistate_pmf`.  Every threshold's Stage 1 walks generations 0, 1, ... of the
+    same (seed, start, count) stream, so each threshold after the first reads the
+    batches the first one drew instead of drawing them again (identical bits).
+    Bounded by a share of the free device memory (B200: 180 GB; config 5 needs
+    ~111 GB for 166 generations); generations past the budget are drawn as usual."""
+
+    def __init__(self, count: int, row_bytes: int):
+        free, total = torch.cuda.mem_get_info()
+        self.budget = max(0, free - max(16 << 30, total // 8))
+        self.nbytes = max(count, 1) * 2 * row_bytes
+        self.shape = (max(count, 1), 2 * row_bytes)
+        self.batches: dict[int, torch.Tensor] = {}
+
+    def get(self, gen: int):
+        return self.batches.get(gen)
+
+    def reserve(self, gen: int):
+        if (len(self.batches) + 1) * self.nbytes > self.budget:
+            return None
+        t = torch.empty(self.shape, dtype=torch.uint8, device=_device.device())
+        self.batches[gen] = t
+        return t
+
+
 class _LeanPrefetcher:
     """`_Prefetcher` for the one-sync loop: preallocated double buffers and events,
-    `rsr_sample_fp4` called directly on the side stream (no per-batch Python objects)."""
+    `rsr_sample_fp4` called directly on the side stream (no per-batch Python objects).
+    With a `_BatchCache`, generations already drawn are read from it (their picks are
+    decoded from the FP4 rows) and new ones are drawn into it."""
 
-    def __init__(self, dist_, seed, start, count, m):
+    def __init__(self, dist_, seed, start, count, m, cache: _BatchCache | None = None):
         dev = _device.device()
         n = dist_.n_components
         self.n, self.m, self.seed, self.start, self.count = n, m, seed, start, count
@@ -365,15 +397,25 @@ class _LeanPrefetcher:
         self.ready = [torch.cuda.Event(), torch.cuda.Event()]
         self.free = [torch.cuda.Event(), torch.cuda.Event()]
         self.free_used = [False, False]
+        self.cache = cache
+        self.src = list(self.fp4)        # FP4 operand of the batch in each slot
+        self.has_states = [True, True]   # u8 state rows in self.states[slot]
 
     def launch(self, gen: int) -> int:
         slot = gen & 1
         if self.free_used[slot]:
             self.stream.wait_event(self.free[slot])
-        mask = (1 << 64) - 1
-        _abi.call("rsr_sample_fp4", self.probs, self.n, self.m, self.seed & mask, gen & mask,
-                  self.start, self.count, _abi.ptr(self.states[slot]), _abi.ptr(self.fp4[slot]),
-                  self.rb, self.sptr)
+        cached = self.cache.get(gen) if self.cache is not None else None
+        if cached is not None:
+            self.src[slot], self.has_states[slot] = cached, False
+        else:
+            dst = self.cache.reserve(gen) if self.cache is not None else None
+            dst = self.fp4[slot] if dst is None else dst
+            mask = (1 << 64) - 1
+            _abi.call("rsr_sample_fp4", self.probs, self.n, self.m, self.seed & mask, gen & mask,
+                      self.start, self.count, _abi.ptr(self.states[slot]), _abi.ptr(dst), self.rb,
+                      self.sptr)
+            self.src[slot], self.has_states[slot] = dst, True
         self.ready[slot].record(self.stream)
         return slot
 
@@ -390,7 +432,7 @@ def _side_code_int(s: int) -> int:
 
 
 def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, start, count, H,
-                       t_start, phi_start) -> Stage1Result:
+                       t_start, phi_start, batch_cache=None) -> Stage1Result:
     """Stage-1 loop with one host synchronisation per iteration.
 
     Stream order per iteration i: classify(i) -> finalize counts -> report
@@ -432,7 +474,7 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
     lo_p = ctypes.byref(refs.desc[0])
     up_p = ctypes.byref(refs.desc[1])
 
-    pre = _LeanPrefetcher(dist, config.seed, start, count, M)
+    pre = _LeanPrefetcher(dist, config.seed, start, count, M, batch_cache)
 
     # Two-pass classification: most samples are dominated by one of the first
     # upper references (tools/first_match_hist.py: after 480 of cfg3's 10^4
@@ -455,7 +497,7 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
 
     def launch_classify(slot):
         main.wait_event(pre.ready[slot])
-        a = pre.fp4[slot]
+        a = pre.src[slot]
         nl, nu = refs.bound(0), refs.bound(1)
         bl = _abi.ptr(refs.fp4[0]) if nl else None
         # rows past a side's bound are never-hit pad rows up to its capacity
@@ -490,8 +532,12 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         sp = _device.stream()
         _abi.call("rsr_compact", _abi.ptr(labels), count, _abi.LABEL_UNCLASSIFIED, _abi.ptr(idx),
                   _abi.ptr(cnt), _abi.ptr(cscratch), sp)
-        _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
-                  _abi.ptr(pos_d), n_local, _abi.ptr(out), sp)
+        if pre.has_states[slot]:
+            _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
+                      _abi.ptr(pos_d), n_local, _abi.ptr(out), sp)
+        else:
+            _abi.call("rsr_gather_picks_fp4", _abi.ptr(pre.src[slot]), rb, N, M, _abi.ptr(idx),
+                      _abi.ptr(pos_d), n_local, _abi.ptr(out), sp)
 
     def search_and_insert(slot, n_pick, gather=True):
         """positions -> picked rows -> boundary searches -> device insertion: fixed
@@ -514,8 +560,9 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
 
     # graphs only for the boundary-search path (the raw-sample path runs torch ops)
     # on one rank (a multi-rank iteration exchanges picked rows through the host)
+    # (and not with a batch cache, whose source buffers change per generation)
     use_graphs = (config.boundary_search_enabled and not comm.distributed
-                  and os.environ.get("RSR_LOOP_GRAPHS", "1") != "0")
+                  and batch_cache is None and os.environ.get("RSR_LOOP_GRAPHS", "1") != "0")
     graphs: dict = {}
     trace: list[TraceRecord] = []
     terminated_by = "r_max"
@@ -723,8 +770,16 @@ def multistate_pmf(model: SystemModel, dist: ComponentDistribution, config: RunC
     """Both stages for every threshold, composed into the PMF (workflow.py:274-321)."""
     m_s = model.n_system_states
     s1s, reps = [], []
+    # thresholds share the sample stream: keep the drawn batches in HBM between them
+    cache = None
+    if (m_s > 2 and torch.cuda.is_available() and os.environ.get("RSR_BATCH_CACHE", "1") != "0"
+            and dist.n_states == model.n_component_states
+            and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.FP4_MAX_ROW_BYTES):
+        comm_ = comm or Comm.single()
+        _, count = shard_range(config.n_samples, comm_.world, comm_.rank)
+        cache = _BatchCache(count, _abi.fp4_row_bytes(dist.n_components, dist.n_states))
     for threshold in range(m_s - 1):
-        s1 = stage1_find_references(model, dist, config, threshold, comm)
+        s1 = stage1_find_references(model, dist, config, threshold, comm, _batch_cache=cache)
         s2 = stage2_evaluate(model, dist, s1.lower, s1.upper, config, threshold, comm)
         s1s.append(s1)
         reps.append(s2)

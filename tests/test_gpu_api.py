@@ -364,3 +364,25 @@ def test_classify_host_paths_match(n, m, s):
     packed = np.packbits(oracle.encode(samples, m, "sample"), axis=1)
     labp, countsp = classify_host_encoded(packed, n, lo, up, m, chunk_rows=1000)
     assert np.array_equal(labp.numpy(), want) and countsp == counts
+
+
+@pytest.mark.parametrize("cache", ["1", "0"])
+def test_multistate_pmf_batch_cache(cache, monkeypatch):
+    """multistate_pmf keeps the drawn batches in HBM between thresholds (their picks
+    decoded from the FP4 rows); every threshold's Stage 1 equals the golden run."""
+    monkeypatch.setenv("RSR_BATCH_CACHE", cache)
+    rec = next(c for c in load_json("workflow.json") if c["spec"]["name"] == "grid_widest_m3")
+    spec = rec["spec"]
+    model = device_model(spec["model"])
+    dist = P.ComponentDistribution(np.array(spec["probs"]))
+    cfg = P.RunConfig(**spec["config"])
+    rep = P.multistate_pmf(model, dist, cfg)
+    assert len(rep.stage1_results) == len(rec["stages"])
+    for s1, st in zip(rep.stage1_results, rec["stages"]):
+        want = st["stage1"]
+        assert [list(v) for v in s1.lower.members] == want["lower"]
+        assert [list(v) for v in s1.upper.members] == want["upper"]
+        assert [[t.reference_count, t.phi_evaluations, t.p_lower, t.p_upper, t.p_unclassified]
+                for t in s1.trace] == want["trace"]
+    for r, st in zip(rep.stage2_reports, rec["stages"]):
+        assert r.p_lower == st["stage2"]["p_lower"]
