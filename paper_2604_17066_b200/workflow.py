@@ -360,18 +360,29 @@ class _BatchCache:
 
     def __init__(self, count: int, row_bytes: int):
         free, total = torch.cuda.mem_get_info()
-        self.budget = max(0, free - max(16 << 30, total // 8))
-        self.nbytes = max(count, 1) * 2 * row_bytes
         self.shape = (max(count, 1), 2 * row_bytes)
+        self.nbytes = self.shape[0] * self.shape[1]
+        self.max_batches = max(0, free - max(16 << 30, total // 8)) // self.nbytes
         self.batches: dict[int, torch.Tensor] = {}
+        self.slabs: list[torch.Tensor] = []
+        self.free_in_slab = 0
 
     def get(self, gen: int):
         return self.batches.get(gen)
 
     def reserve(self, gen: int):
-        if (len(self.batches) + 1) * self.nbytes > self.budget:
+        if len(self.batches) >= self.max_batches:
             return None
-        t = torch.empty(self.shape, dtype=torch.uint8, device=_device.device())
+        if self.free_in_slab == 0:
+            # slabs doubling from 16 batches: a handful of allocations (each cudaMalloc
+            # costs milliseconds regardless of size, one per 671 MB batch would add up)
+            n = min(max(16, len(self.batches)), self.max_batches - len(self.batches))
+            self.slabs.append(torch.empty((n,) + self.shape, dtype=torch.uint8,
+                                          device=_device.device()))
+            self.free_in_slab = n
+        slab = self.slabs[-1]
+        t = slab[slab.shape[0] - self.free_in_slab]
+        self.free_in_slab -= 1
         self.batches[gen] = t
         return t
 
