@@ -363,6 +363,9 @@ class _BatchCache:
         self.shape = (max(count, 1), 2 * row_bytes)
         self.nbytes = self.shape[0] * self.shape[1]
         self.max_batches = max(0, free - max(16 << 30, total // 8)) // self.nbytes
+        cap = os.environ.get("RSR_BATCH_CACHE_MAX")  # tests: force a partial cache
+        if cap is not None:
+            self.max_batches = min(self.max_batches, int(cap))
         self.batches: dict[int, torch.Tensor] = {}
         self.slabs: list[torch.Tensor] = []
         self.free_in_slab = 0

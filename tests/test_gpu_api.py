@@ -366,11 +366,14 @@ def test_classify_host_paths_match(n, m, s):
     assert np.array_equal(labp.numpy(), want) and countsp == counts
 
 
-@pytest.mark.parametrize("cache", ["1", "0"])
+@pytest.mark.parametrize("cache", ["1", "0", "partial"])
 def test_multistate_pmf_batch_cache(cache, monkeypatch):
     """multistate_pmf keeps the drawn batches in HBM between thresholds (their picks
-    decoded from the FP4 rows); every threshold's Stage 1 equals the golden run."""
-    monkeypatch.setenv("RSR_BATCH_CACHE", cache)
+    decoded from the FP4 rows); every threshold's Stage 1 equals the golden run, also
+    when only the first generations fit the cache."""
+    monkeypatch.setenv("RSR_BATCH_CACHE", "0" if cache == "0" else "1")
+    if cache == "partial":
+        monkeypatch.setenv("RSR_BATCH_CACHE_MAX", "3")
     rec = next(c for c in load_json("workflow.json") if c["spec"]["name"] == "grid_widest_m3")
     spec = rec["spec"]
     model = device_model(spec["model"])
