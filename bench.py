@@ -111,13 +111,30 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
+        """index: the CUDA device ordinal of this process; NVML is addressed by the
+        device's PCI bus id (NVML ordinals ignore CUDA_VISIBLE_DEVICES)."""
         self.samples, self.reasons, self.stop = [], set(), threading.Event()
         self.max_mhz = None
         try:
             import pynvml
+            import torch
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.h = None
+            try:  # match the CUDA device's PCI location against NVML's devices
+                prop = torch.cuda.get_device_properties(index)
+                want = (int(prop.pci_domain_id), int(prop.pci_bus_id), int(prop.pci_device_id))
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    pci = pynvml.nvmlDeviceGetPciInfo(h)
+                    if (int(pci.domain), int(pci.bus), int(pci.device)) == want:
+                        self.h = h
+                        break
+            except Exception:
+                self.h = None
+            if self.h is None:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(
+                    min(index, pynvml.nvmlDeviceGetCount() - 1))
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
             self.nv = None
@@ -243,7 +260,8 @@ def run_ours(args):
     from paper_2604_17066_b200 import _abi
     from paper_2604_17066_b200.dist import Comm
 
-    comm = Comm.from_env("nccl")
+    # RSR_DIST_BACKEND=gloo: functional check of the multi-rank path on one GPU
+    comm = Comm.from_env(os.environ.get("RSR_DIST_BACKEND", "nccl"))
     rank, world = comm.rank, comm.world
     if world == 1:
         torch.cuda.set_device(0)
@@ -328,10 +346,7 @@ def run_ours(args):
           for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-    nv_index = int(vis.split(",")[local_rank]) if vis and vis.split(",")[0].isdigit() else local_rank
-    with ClockSampler(nv_index) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the step events)
             ev[k][0].record()
