@@ -282,7 +282,7 @@ def classify(batch: SampleBatch, lower_set: ReferenceSet | None, upper_set: Refe
 
 
 def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSet | None,
-                  n_states: int, *, chunk_rows: int = 1 << 17,
+                  n_states: int, *, chunk_rows: int = 1 << 16,
                   labels_out: torch.Tensor | None = None,
                   method: str = "tc") -> tuple[torch.Tensor, tuple[int, int, int]]:
     """Classify host-resident uint8 samples, streaming them through the GPU.
