@@ -585,7 +585,12 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
     iteration = 0
     searched = False          # an insertion report is outstanding
     no_search_picks = 0       # Phi calls of the last batch when searches are disabled
+    nvtx = torch.cuda.nvtx if os.environ.get("RSR_NVTX") == "1" else None  # profiler ranges
     while True:
+        if nvtx is not None:
+            if iteration:
+                nvtx.range_pop()
+            nvtx.range_push(f"rsr.stage1 m'={threshold} it={iteration}")
         ready_ev.synchronize()
         n_l, n_u, n_x = int(rep[0]), int(rep[1]), int(rep[2])
         if comm.distributed:  # shard counts -> batch counts; per-rank unclassified counts
@@ -653,6 +658,8 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         iteration += 1
         slot = launch_classify(pending)
         pending = pre.launch(iteration + 1)
+    if nvtx is not None:
+        nvtx.range_pop()
     pre.close(main)
     refs.to_sets(lower, upper, dropped=bool(rep[9]))
     return Stage1Result(lower=lower, upper=upper, trace=trace, iterations=iteration + 1,
