@@ -628,8 +628,14 @@ int classify_tc_impl(const int8_t* A, int64_t S, const int8_t* B_lower, int64_t 
   p.first_lower = first_lower;
   p.first_upper = first_upper;
   p.first_base_lower = p.first_base_upper = 0;
+#ifdef RSR_TC_EXPERIMENTS
+  // timing experiments only (results are wrong when set): compiled out of the
+  // product library
   const char* dbg = getenv("RSR_TC_DEBUG");
   p.debug = dbg ? atoi(dbg) : 0;
+#else
+  p.debug = 0;
+#endif
   const size_t max_smem = 227 * 1024;
 
   if (impl != 1) {
