@@ -501,13 +501,16 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
     pass2_min = int(os.environ.get("RSR_LOOP_PASS2_MIN", str(2 * _abi.FP4_TILE_ROWS)))
     two_pass = {}
 
-    def two_pass_buffers():
+    def two_pass_buffers():  # allocated up front: a large first allocation costs milliseconds
         if not two_pass:
             two_pass["a2"] = torch.empty((max(count, 1), 2 * rb), dtype=torch.uint8, device=dev)
             two_pass["f2"] = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
             two_pass["idx"] = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
             two_pass["cnt"] = torch.empty(1, dtype=torch.int64, device=dev)
         return two_pass["a2"], two_pass["f2"], two_pass["idx"], two_pass["cnt"]
+
+    if pass1 > 0:
+        two_pass_buffers()
 
     def launch_classify(slot):
         main.wait_event(pre.ready[slot])
