@@ -173,6 +173,68 @@ class ClockSampler:
 
 # -------------------------------------------------------------------- peaks
 
+def secondary_kernels():
+    """Device time of the path's other kernels on their config shapes (CUDA events,
+    mean of 10 launches): the sampler (Philox4x64-10 + inverse CDF + FP4 operand,
+    integer-multiply bound; HBM write rate reported against the measured copy
+    bandwidth), Stage-2 Phi evaluation and the loop's boundary searches."""
+    import numpy as np
+    import torch
+
+    import paper_2604_17066_b200 as P
+    from paper_2604_17066_b200 import _abi, workloads as W
+
+    def timed(fn, reps=10):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        e.synchronize()
+        return s.elapsed_time(e) / reps
+
+    out = {}
+    S = 1 << 20
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs") or peaks.get("hbm_GBps") or peaks.get("copy_gbs")
+    for m, probs in ((2, [0.1, 0.9]), (3, [0.05, 0.15, 0.8])):
+        d = P.ComponentDistribution.iid(N_COMP, probs)
+        rb = _abi.fp4_row_bytes(N_COMP, m)
+        st = torch.empty((S, N_COMP), dtype=torch.uint8, device="cuda")
+        a4 = torch.empty((S, 2 * rb), dtype=torch.uint8, device="cuda")
+        pr = _abi.ptr(d.device_probs())
+        ms = timed(lambda: _abi.call("rsr_sample_fp4", pr, N_COMP, m, 0, 1, 0, S, _abi.ptr(st),
+                                     _abi.ptr(a4), rb, _abi.stream_ptr()))
+        wbytes = S * (N_COMP + 2 * rb)
+        out[f"sample_rows_kernel_M{m}"] = {
+            "shape": f"2^20 x {N_COMP} draws", "ms": ms, "draws_per_s": S * N_COMP / (ms * 1e-3),
+            "hbm_write_gbs": wbytes / (ms * 1e-3) / 1e9, "hbm_peak_gbs": hbm,
+            "bound": "integer multiply (FMA pipe), not HBM"}
+        del st, a4
+    g = W.cfg3(0)
+    graph = P.Graph(g["n_nodes"], tuple(g["edges"]))
+    phi = P.single_od_connectivity(graph, g["source"], g["target"])
+    model = P.SystemModel(graph.n_edges, 2, 2, phi)
+    rng = np.random.default_rng(0)
+    x = torch.as_tensor((rng.random((4096, graph.n_edges)) < 0.9).astype(np.uint8)).cuda()
+    vals = torch.empty(4096, dtype=torch.uint8, device="cuda")
+    ms = timed(lambda: phi.eval_into(x, None, 4096, 2, vals))
+    out["phi_eval (s-t, 119 nodes / 295 edges)"] = {"ms_per_4096": ms,
+                                                      "phi_per_s": 4096 / (ms * 1e-3)}
+    x0 = x[:64].contiguous()
+    ms = timed(lambda: P.boundary_search_batch(model, x0, 0), reps=5)
+    out["boundary_search (64 s-t searches, 119 / 295)"] = {"ms": ms,
+                                                             "searches_per_s": 64 / (ms * 1e-3)}
+    return out
+
+
 def int8_peak_tops():
     """Measured dense int8 GEMM throughput (cuBLASLt via torch._int_mm), best of 10.
 
@@ -441,6 +503,7 @@ def run_ours(args):
     # second half of BASELINE.json's metric: wall time of the full RSR loop to
     # c.o.v. 0.05 on config 3 (one GPU; the loop has no data-parallel split);
     # measured before the CPU baseline keeps the host cores busy
+    kernels2 = secondary_kernels() if rank == 0 and args.config == "cfg2" and not args.no_loop else None
     cov_loop = None
     if rank == 0 and world == 1 and args.config == "cfg2" and not args.no_loop:
         r = measure_loop("cfg3", args.parallel_searches)
@@ -482,6 +545,8 @@ def run_ours(args):
                 "gpu_launches": launches, "clocks": clk.summary()}
         if cov_loop is not None:
             line["wall_time_to_cov"] = cov_loop
+        if kernels2 is not None:
+            line["secondary_kernels"] = kernels2
         print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
