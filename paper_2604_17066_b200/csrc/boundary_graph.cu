@@ -28,6 +28,12 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// experiment knob: a three-edge detour repair before the BFS (measured a wash on
+// the config 3/5 loops: -2 % / +5 %), off
+#ifndef RSR_BOUNDARY_HOP3
+#define RSR_BOUNDARY_HOP3 0
+#endif
+
 // experiment builds (make prof): 0 searches, 1 upper-side searches, 2 BFS runs,
 // 3 BFS steps, 4 cycles in BFS, 5 cycles in trace_bidir, 6 cycles in the initial
 // union-find, 7 total cycles
@@ -331,12 +337,43 @@ __device__ __forceinline__ int64_t upper_walk(const GraphSmem& g, Adj& adj, uint
         const uint32_t c = adj.row(u, q) & adj.row(v, q);
         if (wn < 0 && c) wn = 32 * q + __ffs(c) - 1;
       }
+      int wa = -1, wb = -1;
+#if RSR_BOUNDARY_HOP3
+      // next cheapest: a detour u-a-b-v (a neighbour a of u sharing a neighbour b
+      // with v; edge (u,v) is already gone from the adjacency)
+      if (wn < 0 && g.eid) {
+        for (int q = 0; q < W && wa < 0; ++q) {
+          uint32_t na = adj.row(u, q);
+          while (na && wa < 0) {
+            const int a = 32 * q + __ffs(na) - 1;
+            na &= na - 1;
+#pragma unroll
+            for (int q2 = 0; q2 < W; ++q2) {
+              const uint32_t c = adj.row(a, q2) & adj.row(v, q2);
+              if (wa < 0 && c) {
+                wa = a;
+                wb = 32 * q2 + __ffs(c) - 1;
+              }
+            }
+          }
+        }
+      }
+#endif
       if (wn >= 0 && g.eid) {
         if (lane == 0) {
           const int e1 = g.eid[u * g.n + wn], e2 = g.eid[wn * g.n + v];
           onpath[n >> 5] &= ~(1u << (n & 31));
           onpath[e1 >> 5] |= 1u << (e1 & 31);
           onpath[e2 >> 5] |= 1u << (e2 & 31);
+        }
+        __syncwarp();
+      } else if (wa >= 0) {
+        if (lane == 0) {
+          const int e1 = g.eid[u * g.n + wa], e2 = g.eid[wa * g.n + wb], e3 = g.eid[wb * g.n + v];
+          onpath[n >> 5] &= ~(1u << (n & 31));
+          onpath[e1 >> 5] |= 1u << (e1 & 31);
+          onpath[e2 >> 5] |= 1u << (e2 & 31);
+          onpath[e3 >> 5] |= 1u << (e3 & 31);
         }
         __syncwarp();
       } else {
