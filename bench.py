@@ -621,53 +621,73 @@ def loop_problem(cfg: str, parallel_searches: int):
 
 
 def run_loop(args):
-    """Wall time of the full RSR loop (Stage 1 + Stage 2 to c.o.v. 0.05) on one GPU."""
-    print(json.dumps(measure_loop(args.config, args.parallel_searches,
-                                  None if args.no_cpu_baseline else args.cpu_seconds)), flush=True)
+    """Wall time of the full RSR loop (Stage 1 + Stage 2 to c.o.v. 0.05).  Under torchrun
+    the batch's samples shard across the ranks (same stream, start offsets; identical
+    results to one GPU) and the per-iteration counts / picked rows are exchanged."""
+    from paper_2604_17066_b200.dist import Comm
+    comm = Comm.from_env(os.environ.get("RSR_DIST_BACKEND", "nccl"))
+    out = measure_loop(args.config, args.parallel_searches,
+                       None if args.no_cpu_baseline or comm.world > 1 else args.cpu_seconds,
+                       comm=comm)
+    if comm.rank == 0:
+        print(json.dumps(out), flush=True)
+    if comm.distributed:
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
 
 
-def measure_loop(config, parallel_searches, cpu_seconds=None):
+def measure_loop(config, parallel_searches, cpu_seconds=None, comm=None):
     import torch
 
     import paper_2604_17066_b200 as P
     from paper_2604_17066_b200 import _abi
+    from paper_2604_17066_b200.dist import shard_range
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _specs import device_model
     spec, probs, kw, thresholds, desc = loop_problem(config, parallel_searches)
     dist = P.ComponentDistribution(probs)
-    torch.cuda.set_device(0)
+    world = comm.world if comm is not None else 1
+    if world == 1:
+        torch.cuda.set_device(0)
     out = {"metric": "wall-time to c.o.v.=0.05", "unit": "s", "higher_is_better": False,
-           "n_gpus": 1, "dtype": "e2m1 classifier, u8 states", "data": "synthetic",
-           "config": {"workload": desc}}
+           "n_gpus": world, "dtype": "e2m1 classifier, u8 states", "data": "synthetic",
+           "scaling": "strong",
+           "config": {"workload": desc,
+                      "parallelism": (f"dp{world}: each batch's samples sharded by stream offset, "
+                                      "counts all-reduced, picked rows all-gathered, reference "
+                                      "sets identical on every rank" if world > 1 else "dp1")}}
     # warm-up on the same batch size (a few iterations + Stage 2), so the timed
     # run finds the CUDA context, library state and cached device buffers ready
     wm = device_model(spec)
     wcfg = P.RunConfig(**{**kw, "r_max": 5, "seed": kw.get("seed", 0) + 1})
-    ws1 = P.stage1_find_references(wm, dist, wcfg, thresholds[0])
-    P.stage2_evaluate(wm, dist, ws1.lower, ws1.upper, wcfg, thresholds[0])
+    ws1 = P.stage1_find_references(wm, dist, wcfg, thresholds[0], comm)
+    P.stage2_evaluate(wm, dist, ws1.lower, ws1.upper, wcfg, thresholds[0], comm)
     torch.cuda.synchronize()
+    if comm is not None:
+        comm.barrier()
     model = device_model(spec)
     cfg = P.RunConfig(**kw)
     stages = []
     s1_first = None
-    clk = ClockSampler(0)  # NVML init outside the timed region
+    clk = ClockSampler(torch.cuda.current_device())  # NVML init outside the timed region
     with clk:
         t0 = time.perf_counter()
         # thresholds share the sample stream: the drawn batches stay in HBM between
         # them, as in multistate_pmf (workflow._BatchCache)
         from paper_2604_17066_b200.workflow import _BatchCache
-        cache = (_BatchCache(cfg.n_samples, _abi.fp4_row_bytes(dist.n_components, dist.n_states))
+        shard = shard_range(cfg.n_samples, world, comm.rank if comm is not None else 0)[1]
+        cache = (_BatchCache(shard, _abi.fp4_row_bytes(dist.n_components, dist.n_states))
                  if len(thresholds) > 1 and os.environ.get("RSR_BATCH_CACHE", "1") != "0" else None)
         for thr in thresholds:
             ts = time.perf_counter()
-            s1 = P.stage1_find_references(model, dist, cfg, thr, _batch_cache=cache)
+            s1 = P.stage1_find_references(model, dist, cfg, thr, comm, _batch_cache=cache)
             t1 = time.perf_counter()
             s1_first = s1_first or s1
             if config == "cfg1":
-                rep = P.stage2_evaluate(model, dist, s1.lower, s1.upper, cfg, thr)
+                rep = P.stage2_evaluate(model, dist, s1.lower, s1.upper, cfg, thr, comm)
             else:
                 rep = P.stage2_until_cov(model, dist, s1.lower, s1.upper, cfg, thr, 0.05,
-                                         side="lower")
+                                         side="lower", comm=comm)
             t2 = time.perf_counter()
             stages.append({"threshold": thr, "stage1_s": t1 - ts, "stage2_s": t2 - t1,
                            "refs": [len(s1.lower), len(s1.upper)], "iterations": s1.iterations,
@@ -677,6 +697,11 @@ def measure_loop(config, parallel_searches, cpu_seconds=None):
                            "stage2_samples": rep.n_samples})
         torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    if comm is not None and comm.distributed:  # job wall time = slowest rank
+        import torch.distributed as tdist
+        t = torch.tensor([wall], dtype=torch.float64, device=comm.device)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        wall = float(t.item())
     out.update({"value": wall, "stages": stages, "phi_evaluations": model.evaluation_count,
                 "clocks": clk.summary()})
     if cpu_seconds is not None:

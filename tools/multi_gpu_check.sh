@@ -14,3 +14,11 @@ for n in 2 4 8; do
     --master-port $PORT bench.py --gpus $n --config cfg4 --k 500000 --ref-shards $n \
     --steps 3 --warmup 3 --no-e2e | tail -1
 done
+for n in 2 4 8; do
+  [ "$n" -le "$MAX" ] || break
+  echo "== RSR loops on $n GPUs (samples of every batch sharded)"
+  for c in cfg3 cfg5; do
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+      --master-port $PORT bench.py --gpus $n --config $c | tail -1
+  done
+done
