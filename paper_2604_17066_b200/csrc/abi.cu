@@ -1,6 +1,10 @@
 // Library-level entry points: version, error string, device info.
 #include <stdarg.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 
 namespace rsr {
@@ -20,6 +24,22 @@ int check_launch(const char* what) {
     set_error("%s launch failed: %s", what, cudaGetErrorString(e));
     return RSR_ECUDA;
   }
+  return RSR_OK;
+}
+
+int ensure_dynamic_smem(const void* fn, size_t bytes) {
+  // cudaFuncSetAttribute costs microseconds per call and the per-iteration
+  // launches of the Stage-1 loop repeat it: remember what each (device, kernel)
+  // already allows
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> granted;
+  int dev = 0;
+  RSR_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = granted[{dev, fn}];
+  if (bytes <= have) return RSR_OK;
+  RSR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  have = bytes;
   return RSR_OK;
 }
 

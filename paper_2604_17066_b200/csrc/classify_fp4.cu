@@ -713,7 +713,8 @@ int launch_fp4(const Fp4Call& c) {
   const size_t smem = fixed + p.a_bufs * a_buf + (size_t)stages * b_stage;
   p.n_groups = (int)rsr::ceil_div(c.S, (int64_t)2 * kRowsA);
   auto kern = want_first ? classify_fp4_pair_kernel<TN, true> : classify_fp4_pair_kernel<TN, false>;
-  RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  rc = rsr::ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+  if (rc) return rc;
   int clusters = c.sm_count / 2;
   if (p.n_groups < clusters) clusters = p.n_groups;
 

@@ -17,6 +17,10 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Return RSR_ECUDA with a message if the last launch failed.
 int check_launch(const char* what);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= bytes for kernel fn on the
+// current device, set once per (device, kernel) and size.
+int ensure_dynamic_smem(const void* fn, size_t bytes);
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // csrc/phi_bits.cu: bitset-BFS Phi / boundary search for simple graphs

@@ -553,8 +553,10 @@ extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_state
                                                                  : sample_rows_kernel<0, true>)
                   : (M == 2 ? sample_rows_kernel<2, false> : M == 3 ? sample_rows_kernel<3, false>
                                                                   : sample_rows_kernel<0, false>);
-  if (smem > 48 * 1024)
-    RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) {
+    const int rc = rsr::ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+    if (rc) return rc;
+  }
   int dev = 0, sms = 0, per_sm = 0;
   RSR_CUDA(cudaGetDevice(&dev));
   RSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
