@@ -20,17 +20,24 @@ fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = (ctypes.c_ulonglong * 12)()
 K = int(os.environ.get("K", "10000"))
 S = int(os.environ.get("S", str(1 << 20)))
-lower, upper = W.cfg2_refs(0, 295, K, K)
+M = int(os.environ.get("M", "2"))
+if M == 2:
+    lower, upper = W.cfg2_refs(0, 295, K, K)
+    probs = [0.1, 0.9]
+else:  # the M=3 classification shape of tools/time_kernels.py classify_m3
+    rng = np.random.default_rng(5)
+    lower, upper = rng.integers(1, 3, size=(K, 295)), rng.integers(0, 2, size=(K, 295))
+    probs = [0.05, 0.15, 0.8]
 if os.environ.get("UPPER_ONLY"):  # cfg4-like: survival references only
     lower = lower[:0]
 lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
 up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
-batch = P.sample_batch(P.ComponentDistribution.iid(295, [0.1, 0.9]), S, seed=0)
+batch = P.sample_batch(P.ComponentDistribution.iid(295, probs), S, seed=0)
 for it in range(3):
     fn(buf, 1)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    classify_flags(batch, lo, up, 2)
+    classify_flags(batch, lo, up, M)
     e.record()
     torch.cuda.synchronize()
     fn(buf, 0)
