@@ -195,3 +195,22 @@ def test_loop_paths_agree_on_config_graphs(cfg_name, monkeypatch):
     k = len(o1["trace"])
     assert [(t["reference_count"], t["phi_evaluations"], t["p_lower"], t["p_upper"],
              t["p_unclassified"]) for t in o1["trace"]] == out["0"][2][:k]
+
+
+def test_wide_row_system_workflow_vs_oracle():
+    """A system too wide for the FP4 / int8 tensor-core rows (N(M-1) = 900 > 831): the
+    Stage-1 loop falls back to the host-resolved path and the bit-packed classifier;
+    results equal the oracle's."""
+    n, k = 900, 890
+    model = P.SystemModel(n, 2, 2, P.k_out_of_n(k, n))
+    probs = np.tile([0.01, 0.99], (n, 1))
+    dist = P.ComponentDistribution(probs)
+    cfg = dict(n_samples=3000, eps_u=1e-3, r_max=40, seed=5, parallel_searches=4)
+    s1 = P.stage1_find_references(model, dist, P.RunConfig(**cfg), 0)
+    ev = oracle.CountingPhi(oracle.phi_kofn(k, n), n, 2, 2)
+    o1 = oracle.stage1(ev, probs, 0, **cfg)
+    assert s1.lower.members == o1["lower"] and s1.upper.members == o1["upper"]
+    assert [[t.reference_count, t.phi_evaluations, t.p_lower, t.p_upper, t.p_unclassified]
+            for t in s1.trace] == [[t["reference_count"], t["phi_evaluations"], t["p_lower"],
+                                    t["p_upper"], t["p_unclassified"]] for t in o1["trace"]]
+    assert model.evaluation_count == ev.count
