@@ -118,6 +118,7 @@ struct Fp4Params {
   int nt_total;
   int stages;
   int a_bufs;
+  int a_halves;     // sample halves per buffer: 2, or 1 when every tile is of one side
   uint8_t* flags;
   int accumulate;
   int64_t* first_lower;
@@ -285,7 +286,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_addr(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
-  const uint32_t a_buf_bytes = (uint32_t)(2 * p.cq * kChunkA);
+  const uint32_t a_buf_bytes = (uint32_t)(p.a_halves * p.cq * kChunkA);
   const uint32_t b_stage_bytes = (uint32_t)(p.cq * kChunkB);
   uint8_t* sA = smem;
   uint8_t* sB = sA + (size_t)p.a_bufs * a_buf_bytes;
@@ -403,7 +404,8 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             mbar_expect_tx(bar_af, 2 * (uint32_t)(p.cq * kChunkA));
           else
             mbar_arrive_leader(bar_af);
-          tma_load_3d_pair(sA0 + (uint32_t)ab * a_buf_bytes + (uint32_t)(z0 * kChunkA), &map_a,
+          const uint32_t off = p.a_halves == 2 ? (uint32_t)(z0 * kChunkA) : 0u;
+          tma_load_3d_pair(sA0 + (uint32_t)ab * a_buf_bytes + off, &map_a,
                            bar_af, 0, g * 2 * kRowsA + (int)rank * kRowsA, z0);
         }
         __syncwarp();
@@ -469,7 +471,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
         PROF_ADD(11, 1);
         const uint32_t a_up = a_lo0 + (uint32_t)ab * (a_buf_bytes >> 4);
-        const uint32_t a_dn = a_up + (uint32_t)cq * kAstep;
+        const uint32_t a_dn = a_up + (p.a_halves == 2 ? (uint32_t)cq * kAstep : 0u);
         PROF_T(l0);
         // lean per-tile bookkeeping: this warp's instruction count per tile is
         // on the critical path once a tile is only a few hundred MMA cycles, so
@@ -693,7 +695,11 @@ int launch_fp4(const Fp4Call& c) {
   const size_t bars_bytes = (2 * 16 + 26) * 8;
   const size_t fixed = 1024 + bars_bytes + kColGroups * 512 +
                        (want_first ? (kColGroups - 1) * 2048 : 0);
-  const size_t a_buf = (size_t)2 * cq * kChunkA, b_stage = (size_t)cq * (TN / 2) * kChunk;
+  // one-sided launches buffer only the sample half they read: more room for
+  // resident reference tiles (cfg4 K = 2000: 9 tiles of 224 fit)
+  p.a_halves = (nt_l == 0 || nt_u == 0) ? 1 : 2;
+  const size_t a_buf = (size_t)p.a_halves * cq * kChunkA;
+  const size_t b_stage = (size_t)cq * (TN / 2) * kChunk;
   // sample-group buffers: 3 when a group has few reference tiles (its MMAs are short,
   // so the next groups' A loads must be further ahead), else 2; 1 if smem is short
   const char* ab_env = getenv("RSR_TC_ABUFS");
