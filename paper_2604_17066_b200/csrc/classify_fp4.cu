@@ -671,6 +671,52 @@ struct Fp4Call {
   int sm_count;
 };
 
+// Shared-memory plan of one launch: sample buffers (one or both halves), the
+// reference ring, and whether every tile stays resident for the whole launch.
+struct Fp4Layout {
+  int a_halves, a_bufs, stages;
+  int ring;  // stages that fit next to the sample buffers
+  bool resident;
+  size_t smem;
+};
+
+Fp4Layout fp4_layout(int tn, int64_t nt_l, int64_t nt_u, int cq, bool want_first) {
+  Fp4Layout L;
+  const size_t max_smem = 227 * 1024;
+  // align slack, barriers (<= 16 stages x 2 + 18), hit exchange, first-match exchange
+  const size_t bars_bytes = (2 * 16 + 26) * 8;
+  const size_t fixed = 1024 + bars_bytes + kColGroups * 512 +
+                       (want_first ? (kColGroups - 1) * 2048 : 0);
+  // one-sided launches buffer only the sample half they read
+  L.a_halves = (nt_l == 0 || nt_u == 0) ? 1 : 2;
+  const size_t a_buf = (size_t)L.a_halves * cq * kChunkA;
+  const size_t b_stage = (size_t)cq * (tn / 2) * kChunk;
+  const int64_t nt = nt_l + nt_u;
+  // sample-group buffers: 3 when a group has few reference tiles (its MMAs are short,
+  // so the next groups' A loads must be further ahead), else 2; 1 if smem is short
+  const char* ab_env = getenv("RSR_TC_ABUFS");
+  L.a_bufs = ab_env ? atoi(ab_env) : (nt <= 16 ? 3 : 2);
+  if (L.a_bufs < 1) L.a_bufs = 1;
+  if (L.a_bufs > 4) L.a_bufs = 4;
+  while (L.a_bufs > 1 && fixed + L.a_bufs * a_buf + 4 * b_stage > max_smem) --L.a_bufs;
+  const char* res_env = getenv("RSR_FP4_RESIDENT");
+  const bool allow_resident = !(res_env && atoi(res_env) == 0);
+  // resident reference tiles are worth more than a third sample buffer
+  if (allow_resident && !ab_env && L.a_bufs == 3 && nt <= 16 &&
+      fixed + 3 * a_buf + (size_t)nt * b_stage > max_smem &&
+      fixed + 2 * a_buf + (size_t)nt * b_stage <= max_smem)
+    L.a_bufs = 2;
+  int stages = (int)((max_smem - fixed - L.a_bufs * a_buf) / b_stage);
+  if (stages > 16) stages = 16;
+  L.ring = stages;
+  // a launch whose reference tiles all fit in the ring keeps them resident
+  L.resident = allow_resident && nt <= stages;
+  if (L.resident) stages = (int)nt;
+  L.stages = stages;
+  L.smem = fixed + L.a_bufs * a_buf + (size_t)stages * b_stage;
+  return L;
+}
+
 template <int TN>
 int launch_fp4(const Fp4Call& c) {
   const bool want_first = c.first[0] != nullptr || c.first[1] != nullptr;
@@ -690,33 +736,13 @@ int launch_fp4(const Fp4Call& c) {
   p.flags = c.flags;
   p.first_lower = c.first[0];
   p.first_upper = c.first[1];
-  const size_t max_smem = 227 * 1024;
-  // align slack, barriers (<= 16 stages x 2 + 18), hit exchange, first-match exchange
-  const size_t bars_bytes = (2 * 16 + 26) * 8;
-  const size_t fixed = 1024 + bars_bytes + kColGroups * 512 +
-                       (want_first ? (kColGroups - 1) * 2048 : 0);
-  // one-sided launches buffer only the sample half they read: more room for
-  // resident reference tiles (cfg4 K = 2000: 9 tiles of 224 fit)
-  p.a_halves = (nt_l == 0 || nt_u == 0) ? 1 : 2;
-  const size_t a_buf = (size_t)p.a_halves * cq * kChunkA;
-  const size_t b_stage = (size_t)cq * (TN / 2) * kChunk;
-  // sample-group buffers: 3 when a group has few reference tiles (its MMAs are short,
-  // so the next groups' A loads must be further ahead), else 2; 1 if smem is short
-  const char* ab_env = getenv("RSR_TC_ABUFS");
-  p.a_bufs = ab_env ? atoi(ab_env) : (nt_l + nt_u <= 16 ? 3 : 2);
-  if (p.a_bufs < 1) p.a_bufs = 1;
-  if (p.a_bufs > 4) p.a_bufs = 4;
-  while (p.a_bufs > 1 && fixed + p.a_bufs * a_buf + 4 * b_stage > max_smem) --p.a_bufs;
-  int stages = (int)((max_smem - fixed - p.a_bufs * a_buf) / b_stage);
-  if (stages > 16) stages = 16;
-  RSR_REQUIRE(stages >= 2, "rsr_classify_fp4: row_bytes too large for shared memory");
-  // a launch whose reference tiles all fit in the ring keeps them resident
-  const char* res_env = getenv("RSR_FP4_RESIDENT");
-  const bool allow_resident = !(res_env && atoi(res_env) == 0);
-  p.resident = allow_resident && nt_l + nt_u <= stages;
-  if (p.resident) stages = (int)(nt_l + nt_u);
-  p.stages = stages;
-  const size_t smem = fixed + p.a_bufs * a_buf + (size_t)stages * b_stage;
+  const Fp4Layout L = fp4_layout(TN, nt_l, nt_u, cq, want_first);
+  RSR_REQUIRE(L.ring >= 2, "rsr_classify_fp4: row_bytes too large for shared memory");
+  p.a_halves = L.a_halves;
+  p.a_bufs = L.a_bufs;
+  p.resident = L.resident;
+  p.stages = L.stages;
+  const size_t smem = L.smem;
   p.n_groups = (int)rsr::ceil_div(c.S, (int64_t)2 * kRowsA);
   auto kern = want_first ? classify_fp4_pair_kernel<TN, true> : classify_fp4_pair_kernel<TN, false>;
   rc = rsr::ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
@@ -776,19 +802,24 @@ int launch_fp4(const Fp4Call& c) {
 // it), so narrower tiles only win when they save whole tiles, e.g. 5 x 224
 // instead of 5 x 240 is a wash but 1000 refs in 5 x 208 beat 5 x 240 rows of
 // which 200 are padding.  RSR_FP4_TILE_N forces one width.
-int pick_tile_n(int64_t n_lower, int64_t n_upper) {
+int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
   const char* env = getenv("RSR_FP4_TILE_N");
   const int forced = env ? atoi(env) : 0;
   static const int kCand[] = {240, 224, 208, 192, 176, 160};
   static const int kCost[] = {1000, 957, 971, 920, 843, 778};  // relative time per tile
+  // streaming a small set costs about 1700 cycles (2.5 tiles) per sample group
+  // more than keeping it resident (cfg4 K = 2000: 9 resident tiles of 224 take
+  // 0.670 ms, 9 streamed tiles of 240 0.891 ms; profiles/r1_tile_n_small_k.txt)
+  constexpr int64_t kStreamGroupCost = 2500;
   for (int tn : kCand)
     if (tn == forced) return tn;
   int best = 240;
   int64_t best_cost = INT64_MAX;
   for (int i = 0; i < 6; ++i) {
     const int tn = kCand[i];
-    const int64_t tiles = rsr::ceil_div(n_lower, tn) + rsr::ceil_div(n_upper, tn);
-    const int64_t cost = tiles * kCost[i];
+    const int64_t nt_l = rsr::ceil_div(n_lower, tn), nt_u = rsr::ceil_div(n_upper, tn);
+    int64_t cost = (nt_l + nt_u) * kCost[i];
+    if (!fp4_layout(tn, nt_l, nt_u, cq, want_first).resident) cost += kStreamGroupCost;
     if (cost < best_cost) {
       best_cost = cost;
       best = tn;
@@ -845,7 +876,8 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   int dev = 0;
   RSR_CUDA(cudaGetDevice(&dev));
   RSR_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, dev));
-  switch (pick_tile_n(n_lower, n_upper)) {
+  switch (pick_tile_n(n_lower, n_upper, row_bytes / kChunk,
+                      first_lower != nullptr || first_upper != nullptr)) {
     case 224: return launch_fp4<224>(c);
     case 208: return launch_fp4<208>(c);
     case 192: return launch_fp4<192>(c);

@@ -461,3 +461,32 @@ def test_refset_insert_matches_sequential_insert(n, m, batch):
             A.call("rsr_encode_refs_fp4", A.ptr(rows), nrow, cap, n, m, s, A.ptr(enc), rb,
                    A.stream_ptr())
             assert torch.equal(enc, fp4)
+
+
+@pytest.mark.parametrize("kl,ku", [(0, 1500), (0, 2200), (0, 2600), (2000, 0), (600, 600), (900, 1000)])
+@pytest.mark.parametrize("first", [False, True])
+def test_fp4_mid_size_sets_resident_and_streamed(kl, ku, first):
+    # one-sided launches buffer one sample half, and a set that fits only next to
+    # two sample buffers drops the third: the tile width and residency the launch
+    # picks change across these sizes; the hitting references sit in the last tile
+    n, m, s = 295, 2, 1500
+    rng = np.random.default_rng(kl * 7 + ku)
+    samples = (rng.random((s, n)) < 0.9).astype(np.int64)
+    # non-hitting bulk: lower refs with many zeros, upper refs with many ones
+    lower = (rng.random((kl, n)) < 0.2).astype(np.int64)
+    upper = (rng.random((ku, n)) < 0.98).astype(np.int64)
+    for refs, sign in ((lower, 1), (upper, -1)):
+        k = refs.shape[0]
+        if k:
+            near = samples[rng.integers(0, s, 8)]
+            refs[k - 8:] = np.clip(near + sign * rng.integers(0, 2, near.shape), 0, 1)
+    want = _want_flags(samples, lower, upper, m)
+    assert bool((want & 1).any()) == (kl > 0) and bool((want & 2).any()) == (ku > 0)
+    if first:
+        got, fl, fu = _classify_fp4(samples, lower, upper, n, m, first=True)
+        _, wl = oracle.dominance_hits(samples, lower, m, oracle.LOWER, want_first=True)
+        _, wu = oracle.dominance_hits(samples, upper, m, oracle.UPPER, want_first=True)
+        assert np.array_equal(fl, wl) and np.array_equal(fu, wu)
+    else:
+        got = _classify_fp4(samples, lower, upper, n, m)
+    assert np.array_equal(got, want), f"mismatch at {np.flatnonzero(got != want)[:10]}"
