@@ -96,13 +96,13 @@ struct Tile {
 // Counters live in registers (prof[8] per thread) and are flushed once per
 // warp at the end, so the instrumentation barely perturbs the timing.
 #ifdef RSR_FP4_PROF
-__device__ unsigned long long g_prof[12];
-#define PROF_DECL unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
+__device__ unsigned long long g_prof[14];
+#define PROF_DECL unsigned long long prof[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
 #define PROF_T(x) const long long x = clock64()
 #define PROF_ADD(i, v) (prof[i] += (unsigned long long)(v))
 #define PROF_FLUSH                                                   \
   if ((threadIdx.x & 31) == 0)                                       \
-    for (int i_ = 0; i_ < 12; ++i_) atomicAdd(&g_prof[i_], prof[i_])
+    for (int i_ = 0; i_ < 14; ++i_) atomicAdd(&g_prof[i_], prof[i_])
 #else
 #define PROF_DECL
 #define PROF_T(x)
@@ -284,6 +284,9 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   constexpr int kChunkB = Tile<TN>::kChunkB;
   constexpr int kCols = Tile<TN>::kCols;
   extern __shared__ uint8_t smem_raw[];
+#ifdef RSR_FP4_PROF
+  const long long k_entry = clock64();
+#endif
   const uint32_t raw_addr = smem_addr(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
   const uint32_t a_buf_bytes = (uint32_t)(p.a_halves * p.cq * kChunkA);
@@ -466,6 +469,9 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       const int cq = p.cq;
       int stage = 0, gi = 0;
       uint32_t phase = 0, buf = 0, tphase = 0;
+#ifdef RSR_FP4_PROF
+      PROF_ADD(12, clock64() - k_entry);  // setup before the first group
+#endif
       for (int g = cluster; g < n_groups; g += n_clusters, ++gi) {
         const int ab = gi % p.a_bufs;
         const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
@@ -620,9 +626,15 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     }
   }
 
-  PROF_FLUSH;
+#ifdef RSR_FP4_PROF
+  const long long k_loop_end = clock64();
+#endif
   tc_fence_before();
   cluster_sync_all();
+#ifdef RSR_FP4_PROF
+  if (warp == 1 && leader) PROF_ADD(13, clock64() - k_loop_end);  // wait for the other roles
+#endif
+  PROF_FLUSH;
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
@@ -1059,7 +1071,7 @@ __global__ void encode_refs_fp4_kernel(const uint8_t* __restrict__ states, int64
 extern "C" int rsr_fp4_prof(unsigned long long* host8, int reset) {
   RSR_CUDA(cudaMemcpyFromSymbol(host8, g_prof, sizeof(g_prof)));
   if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[14] = {0};
     RSR_CUDA(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
   }
   return RSR_OK;

@@ -17,7 +17,7 @@ from paper_2604_17066_b200.classify import classify_flags  # noqa: E402
 lib = _abi.lib()
 fn = lib.rsr_fp4_prof
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = (ctypes.c_ulonglong * 12)()
+buf = (ctypes.c_ulonglong * 14)()
 K = int(os.environ.get("K", "10000"))
 S = int(os.environ.get("S", str(1 << 20)))
 M = int(os.environ.get("M", "2"))
@@ -28,6 +28,8 @@ else:  # the M=3 classification shape of tools/time_kernels.py classify_m3
     rng = np.random.default_rng(5)
     lower, upper = rng.integers(1, 3, size=(K, 295)), rng.integers(0, 2, size=(K, 295))
     probs = [0.05, 0.15, 0.8]
+if os.environ.get("REFS") == "paths":  # bench.py cfg4: s-t path references of the cfg3 graph
+    lower, upper = lower[:0], W.random_st_paths(W.cfg3(0), K, seed=0)
 if os.environ.get("UPPER_ONLY"):  # cfg4-like: survival references only
     lower = lower[:0]
 lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
@@ -51,7 +53,11 @@ per = [tiles + E * tiles, tiles, tiles, E * tiles, E * tiles, E * tiles, 2 * til
 for n, x, d in zip(names, v, per):
     print(f"{n:20s} {x / max(d, 1):8.1f} cycles per tile (per warp)")
 groups = max(v[11], 1)
-print(f"groups (MMA) {groups}, tiles per group {tiles / groups:.1f}")
+print(f"groups (MMA) {groups}, tiles per group {tiles / groups:.1f}; MMA-loop cycles per group "
+      f"{v[2] / groups:.0f}")
 print(f"epi group-end exchange {v[8] / (E * groups):8.1f} cycles per group (per warp)")
 print(f"mma wait a_full        {v[9] / groups:8.1f} cycles per group")
 print(f"prod wait a_empty      {v[10] / (2 * groups):8.1f} cycles per group")
+ncl = max(v[12] and 74, 1)
+print(f"MMA warp setup {v[12] / ncl:.0f} cycles, teardown wait {v[13] / ncl:.0f} cycles per cluster; "
+      f"groups per cluster {groups / ncl:.1f}, MMA-loop cycles per cluster {v[2] / ncl:.0f}")
