@@ -48,3 +48,14 @@ for mode in ("flush", "no flush", "flush+sleep"):
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     print(f"K={K} {mode:12s} kernel ms median {np.median(ts):.4f} min {min(ts):.4f}")
+
+# host cost of one launch call (enqueue only; the GPU is kept busy by a spin)
+import time  # noqa: E402
+torch.cuda._sleep(50_000_000)
+hs = []
+for _ in range(20):
+    t0 = time.perf_counter()
+    launch()
+    hs.append((time.perf_counter() - t0) * 1e6)
+torch.cuda.synchronize()
+print(f"host enqueue us per launch: median {np.median(hs):.1f} min {min(hs):.1f} max {max(hs):.1f}")
