@@ -1,3 +1,4 @@
+"""e2e probe: host-fed classification on the packed one-hot rows (classify_host_encoded), cfg2 shape."""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

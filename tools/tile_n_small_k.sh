@@ -1,3 +1,5 @@
+#!/bin/bash
+# FP4 classifier kernel ms / roofline fraction per forced MMA N on small cfg4 path-reference sets.
 for k in 500 1000 2000; do
   for tn in 160 176 192 208 224 240; do
     RSR_FP4_TILE_N=$tn timeout 200 python bench.py --config cfg4 --k $k --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | \
