@@ -685,6 +685,8 @@ struct Fp4Call {
 
 // Shared-memory plan of one launch: sample buffers (one or both halves), the
 // reference ring, and whether every tile stays resident for the whole launch.
+constexpr size_t kMinSmem = 120 * 1024;  // > half of the SM's 228 KB
+
 struct Fp4Layout {
   int a_halves, a_bufs, stages;
   int ring;  // stages that fit next to the sample buffers
@@ -726,6 +728,9 @@ Fp4Layout fp4_layout(int tn, int64_t nt_l, int64_t nt_u, int cq, bool want_first
   if (L.resident) stages = (int)nt;
   L.stages = stages;
   L.smem = fixed + L.a_bufs * a_buf + (size_t)stages * b_stage;
+  // one CTA per SM: a small resident launch must not let a second CTA onto the
+  // SM, whose tcgen05.alloc of all 512 columns would wait for the first to exit
+  if (L.smem < kMinSmem) L.smem = kMinSmem;
   return L;
 }
 
