@@ -683,10 +683,10 @@ struct Fp4Call {
   int sm_count;
 };
 
-// Shared-memory plan of one launch: sample buffers (one or both halves), the
-// reference ring, and whether every tile stays resident for the whole launch.
 constexpr size_t kMinSmem = 120 * 1024;  // > half of the SM's 228 KB
 
+// Shared-memory plan of one launch: sample buffers (one or both halves), the
+// reference ring, and whether every tile stays resident for the whole launch.
 struct Fp4Layout {
   int a_halves, a_bufs, stages;
   int ring;  // stages that fit next to the sample buffers
