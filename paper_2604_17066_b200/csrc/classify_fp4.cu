@@ -824,6 +824,8 @@ int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
   const int forced = env ? atoi(env) : 0;
   static const int kCand[] = {240, 224, 208, 192, 176, 160};
   static const int kCost[] = {1000, 957, 971, 920, 843, 778};  // relative time per tile
+  // resident tiles (cfg4 K = 10^3 per-tile times, profiles/r1_tile_n_small_k.txt)
+  static const int kCostResident[] = {1000, 956, 935, 869, 862, 779};
   // streaming a small set costs about 1700 cycles (2.5 tiles) per sample group
   // more than keeping it resident (cfg4 K = 2000: 9 resident tiles of 224 take
   // 0.670 ms, 9 streamed tiles of 240 0.891 ms; profiles/r1_tile_n_small_k.txt)
@@ -835,8 +837,9 @@ int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
   for (int i = 0; i < 6; ++i) {
     const int tn = kCand[i];
     const int64_t nt_l = rsr::ceil_div(n_lower, tn), nt_u = rsr::ceil_div(n_upper, tn);
-    int64_t cost = (nt_l + nt_u) * kCost[i];
-    if (!fp4_layout(tn, nt_l, nt_u, cq, want_first).resident) cost += kStreamGroupCost;
+    const bool resident = fp4_layout(tn, nt_l, nt_u, cq, want_first).resident;
+    int64_t cost = (nt_l + nt_u) * (resident ? kCostResident[i] : kCost[i]);
+    if (!resident) cost += kStreamGroupCost;
     if (cost < best_cost) {
       best_cost = cost;
       best = tn;
