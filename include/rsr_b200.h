@@ -54,6 +54,10 @@ extern "C" {
 #define RSR_LABEL_UNCLASSIFIED 2
 
 /* flags bits written by the classifiers */
+/* sampler streams: the reference's (bit-exact) and the independent device one */
+#define RSR_RNG_SHARED 0 /* Philox4x64-10 = numpy.random.Philox, sampling.py:39-66   */
+#define RSR_RNG_DEVICE 1 /* Philox4x32-10, counter (block, gen), key seed; 2^-32 CDF */
+
 #define RSR_HIT_LOWER 1
 #define RSR_HIT_UPPER 2
 
@@ -110,6 +114,21 @@ int rsr_sample(const double* probs, int n_components, int n_states, uint64_t see
 int rsr_sample_fp4(const double* probs, int n_components, int n_states, uint64_t seed,
                    uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
                    uint8_t* out_fp4, int row_bytes, void* stream);
+
+/* Independent device stream (north_star: "independent device RNG"): the same
+ * calls with rng = RSR_RNG_DEVICE draw flat index f = (start+i)*N + n from word
+ * f%4 of Philox4x32-10 block f/4 (counter [f/4 lo, f/4 hi, gen lo, gen hi], key
+ * [seed lo, seed hi]); state = #{m < M-1 : raw32 >= ceil(cum_m * 2^32)}.
+ * rng = RSR_RNG_SHARED is rsr_sample / rsr_sample_fp4. */
+int rsr_sample_ex(const double* probs, int n_components, int n_states, uint64_t seed,
+                  uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+                  int8_t* out_thermo, int ld_thermo, int rng, void* stream);
+int rsr_sample_fp4_ex(const double* probs, int n_components, int n_states, uint64_t seed,
+                      uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+                      uint8_t* out_fp4, int row_bytes, int rng, void* stream);
+/* Raw 32-bit words first..first+count-1 of the device stream (seed, gen). */
+int rsr_device_raw(uint64_t seed, uint64_t gen, int64_t first, int64_t count, uint32_t* out,
+                   void* stream);
 
 /* ---- (2) encodings: encoding.py:138-153 encode_batch ---------------------- */
 int rsr_encode_samples(const uint8_t* states, int64_t count, int n_components,

@@ -32,18 +32,27 @@ UPPER = "upper"
 
 
 def sample_states(probs: np.ndarray, n_samples: int, seed: int, generation_index: int = 0,
-                  start: int = 0, fast: bool = False) -> np.ndarray:
+                  start: int = 0, fast: bool = False, rng: str = "shared") -> np.ndarray:
     """Inverse-CDF draw on the Philox field (``sampling.py:69-90``).
 
     state[i, n] = #{m : cumsum(probs[n])[m] <= u[i, n]} clipped to M-1, which is
     ``np.searchsorted(cum[n], u, side="right")`` for the non-decreasing cum.
     ``fast`` uses numpy's own Philox as the reference does (timing runs).
+    ``rng="device"``: the independent device stream (not in the reference), u =
+    raw32 * 2^-32 from Philox4x32-10 (philox.device_raw), same inverse CDF.
     """
     if n_samples < 1:
         raise ValueError("n_samples must be >= 1")
     probs = np.asarray(probs, dtype=np.float64)
     n, m = probs.shape
-    u = uniform_field(seed, generation_index, start, n_samples, n, fast=fast)
+    if rng == "device":
+        from .philox import device_raw
+        u = (device_raw(seed, generation_index, start * n, n_samples * n).astype(np.float64)
+             * 2.0 ** -32).reshape(n_samples, n)
+    elif rng == "shared":
+        u = uniform_field(seed, generation_index, start, n_samples, n, fast=fast)
+    else:
+        raise ValueError(f"rng must be 'shared' or 'device', got {rng!r}")
     cum = np.cumsum(probs, axis=1)
     out = np.empty((n_samples, n), dtype=np.int64)
     for comp in range(n):
@@ -87,7 +96,7 @@ def _zero_violation(sample_bits: np.ndarray, refbar_bits: np.ndarray,
     step = max(1, min(refbar_bits.shape[0], _BLOCK_BYTES // max(1, rows * width)))
     for r0 in range(0, refbar_bits.shape[0], step):
         blk = refbar_bits[r0:r0 + step]
-        viol = np.bitwise_count(sample_bits[:, None, :] & blk[None, :, :]).sum(axis=2)
+        viol = np.bitwise_count(sample_bits[:, None, :] & blk[None, :, :]).sum(axis=2, dtype=np.int32)
         z = viol == 0
         zh = z.any(axis=1)
         if want_first:
@@ -374,7 +383,7 @@ def stage1(ev: CountingPhi, probs: np.ndarray, threshold: int, n_samples: int,
            eps_u: float = 1e-5, r_max: int = 10_000, seed: int = 0,
            parallel_searches: int = 1, boundary_search_enabled: bool = True,
            chunk_size: int = 65536, n_workers: int = 1, time_budget: float | None = None,
-           fast: bool = False) -> dict:
+           fast: bool = False, rng: str = "shared") -> dict:
     """Reference discovery loop (``workflow.py:122-195``).
 
     Trace records omit elapsed time and RSS (host-dependent); everything else
@@ -393,7 +402,7 @@ def stage1(ev: CountingPhi, probs: np.ndarray, threshold: int, n_samples: int,
         if time_budget is not None and trace and time.perf_counter() - t0 > time_budget:
             terminated_by = "budget"
             break
-        xs = sample_states(probs, n_samples, seed, it, fast=fast)
+        xs = sample_states(probs, n_samples, seed, it, fast=fast, rng=rng)
         res = classify_labels(xs, lower.array(ev.n), upper.array(ev.n), ev.m,
                               chunk_size, n_workers)
         n_l, n_u = res["lower_indices"].size, res["upper_indices"].size
@@ -410,8 +419,8 @@ def stage1(ev: CountingPhi, probs: np.ndarray, threshold: int, n_samples: int,
             break
         if len(lower) + len(upper) >= r_max:
             break
-        rng = np.random.default_rng([seed, it])
-        picks = rng.choice(res["unclassified_indices"], size=min(parallel_searches, n_x),
+        gen = np.random.default_rng([seed, it])
+        picks = gen.choice(res["unclassified_indices"], size=min(parallel_searches, n_x),
                            replace=False)
         for idx in picks:
             x0 = xs[int(idx)]
@@ -433,13 +442,13 @@ def stage1(ev: CountingPhi, probs: np.ndarray, threshold: int, n_samples: int,
 
 def stage2(ev: CountingPhi, probs: np.ndarray, lower_members, upper_members, threshold: int,
            n_samples: int, seed: int = 0, chunk_size: int = 65536, n_workers: int = 1,
-           start: int = 0) -> dict:
+           start: int = 0, rng: str = "shared") -> dict:
     """One generation-0 batch, Phi on the unclassified (``workflow.py:198-245``).
 
     ``start`` extends the generation-0 index space for the run-to-c.o.v. loop
     (SURVEY a16); start = 0 is exactly the reference Stage 2.
     """
-    xs = sample_states(probs, n_samples, seed, 0, start)
+    xs = sample_states(probs, n_samples, seed, 0, start, rng=rng)
     lo = np.array(lower_members, dtype=np.int64).reshape(-1, ev.n)
     up = np.array(upper_members, dtype=np.int64).reshape(-1, ev.n)
     res = classify_labels(xs, lo, up, ev.m, chunk_size, n_workers)
@@ -473,7 +482,8 @@ def multistate_pmf(ev: CountingPhi, probs: np.ndarray, **cfg) -> dict:
     for thr in range(ev.ms - 1):
         s1 = stage1(ev, probs, thr, **cfg)
         s2 = stage2(ev, probs, s1["lower"], s1["upper"], thr, cfg["n_samples"],
-                    cfg.get("seed", 0), cfg.get("chunk_size", 65536), cfg.get("n_workers", 1))
+                    cfg.get("seed", 0), cfg.get("chunk_size", 65536), cfg.get("n_workers", 1),
+                    rng=cfg.get("rng", "shared"))
         s1s.append(s1)
         s2s.append(s2)
     cum = np.array([r["p_lower"] for r in s2s])

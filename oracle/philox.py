@@ -97,3 +97,48 @@ def uniform_field(seed: int, generation_index: int, start: int, count: int,
         raw = random_raw(seed, generation_index, start * n_components, count * n_components)
     u = (raw >> np.uint64(11)).astype(np.float64) * float(2.0 ** -53)
     return u.reshape(count, n_components)
+
+
+# ------------------------------------------------- independent device stream
+# Not in the reference: the north_star's "independent device RNG" mode
+# (include/rsr_b200.h RSR_RNG_DEVICE).  Philox4x32-10 is the published
+# Random123 generator (Salmon et al., SC'11): 32-bit multipliers
+# 0xD2511F53 / 0xCD9E8D57, Weyl key increments 0x9E3779B9 / 0xBB67AE85.  The
+# restatement is pinned by the Random123 known-answer vectors in
+# tests/test_oracle_golden.py.
+
+P32_M0, P32_M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+P32_W0, P32_W1 = 0x9E3779B9, 0xBB67AE85
+_M32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_blocks(c0, c1, c2, c3, k0: int, k1: int) -> np.ndarray:
+    """Philox4x32-10 of counter arrays (c0..c3) under key (k0, k1): uint32 [n, 4]."""
+    c = [np.asarray(x, dtype=np.uint64) & _M32 for x in (c0, c1, c2, c3)]
+    c0, c1, c2, c3 = np.broadcast_arrays(*c)
+    k0, k1 = k0 & 0xFFFFFFFF, k1 & 0xFFFFFFFF
+    for r in range(10):
+        if r:
+            k0 = (k0 + P32_W0) & 0xFFFFFFFF
+            k1 = (k1 + P32_W1) & 0xFFFFFFFF
+        p0 = P32_M0 * c0  # < 2^64: exact in uint64
+        p1 = P32_M1 * c2
+        c0, c1, c2, c3 = ((p1 >> np.uint64(32)) ^ c1 ^ np.uint64(k0), p1 & _M32,
+                          (p0 >> np.uint64(32)) ^ c3 ^ np.uint64(k1), p0 & _M32)
+    return np.stack([c0, c1, c2, c3], axis=-1).astype(np.uint32)
+
+
+def device_raw(seed: int, generation_index: int, first: int, count: int) -> np.ndarray:
+    """uint32 words first..first+count-1 of the device stream (seed, gen): flat word f is
+    word f % 4 of block b = f // 4, counter [b lo, b hi, gen lo, gen hi], key [seed lo,
+    seed hi]."""
+    if count <= 0:
+        return np.zeros(0, dtype=np.uint32)
+    mask = (1 << 64) - 1
+    seed, gen = seed & mask, generation_index & mask
+    b_lo, b_hi = first // 4, (first + count - 1) // 4
+    b = np.arange(b_lo, b_hi + 1, dtype=np.uint64)
+    blocks = philox4x32_blocks(b & _M32, b >> np.uint64(32), gen & 0xFFFFFFFF, gen >> 32,
+                               seed & 0xFFFFFFFF, seed >> 32)
+    off = first - 4 * b_lo
+    return blocks.reshape(-1)[off:off + count]

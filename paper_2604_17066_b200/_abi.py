@@ -27,6 +27,7 @@ LIB_PATH = os.environ.get("RSR_LIB_OVERRIDE", LIB_PATH)
 RSR_OK, RSR_EINVAL, RSR_ECUDA, RSR_EUNSUPPORTED = 0, 1, 2, 3
 SIDE_LOWER, SIDE_UPPER = 0, 1
 HIT_LOWER, HIT_UPPER = 1, 2
+RNG_SHARED, RNG_DEVICE = 0, 1  # reference Philox4x64-10 stream / independent Philox4x32-10
 LABEL_LOWER, LABEL_UPPER, LABEL_UNCLASSIFIED = 0, 1, 2
 PHI_ST, PHI_WIDEST, PHI_GLOBAL, PHI_KOFN, PHI_CONES, PHI_EDGE_DISJOINT = 0, 1, 2, 3, 4, 5
 
@@ -79,6 +80,9 @@ EXPORTED = {
     "rsr_uniform_field": (_I, [_U64, _U64, _I64, _I64, _I, _P, _P]),
     "rsr_sample": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
     "rsr_sample_fp4": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
+    "rsr_sample_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I, _P]),
+    "rsr_sample_fp4_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I, _P]),
+    "rsr_device_raw": (_I, [_U64, _U64, _I64, _I64, _P, _P]),
     "rsr_encode_samples": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "rsr_encode_refs": (_I, [_P, _I64, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_encode_rows": (_I, [_P, _I64, _I, _I, _I, _P, _P]),

@@ -53,6 +53,58 @@ class InconsistentReferenceSets(ValueError):
     """A sample matched both a lower and an upper reference in strict mode."""
 
 
+_FP4_EXACT: dict[int, bool] = {}
+
+
+def fp4_exact() -> bool:
+    """Known-answer self-check of the FP4 classifier, once per device.
+
+    The FP4 kernel reads violation counts out of fp32 *denormals* (scale factors
+    2^-127 x 2^-22 make every 0/1 product 2^-149; csrc/classify_fp4.cu), so a part
+    or driver that flushed accumulator denormals would read every count as 0 and
+    label every sample a hit.  This runs the FP4 kernel on 512 samples x 2 x 240
+    references whose minimum violation counts include exactly 1 (the smallest
+    denormal) and compares its hit flags with the bit-packed CUDA-core kernel's.
+    On a mismatch the default classifier (``method="tc"``) uses the int8 tcgen05
+    kernel instead -- on the device, there is no CPU fallback.
+    ``RSR_FP4_SELFCHECK=fail`` forces the failure branch (tests)."""
+    dev = _device.device()
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    ok = _FP4_EXACT.get(key)
+    if ok is not None:
+        return ok
+    import os
+    if os.environ.get("RSR_FP4_SELFCHECK") == "fail":
+        _FP4_EXACT[key] = False
+        return False
+    rng = np.random.default_rng(20260419)
+    n, h, k = 64, 512, 240
+    x = (rng.random((h, n)) < 0.5).astype(np.uint8)
+    x[0], x[1] = 0, 1
+    up = np.zeros((k, n), dtype=np.uint8)
+    lo = np.ones((k, n), dtype=np.uint8)
+    for j in range(k):  # 1-3 ones (upper) / zeros (lower): many counts of exactly 1
+        up[j, rng.choice(n, size=1 + j % 3, replace=False)] = 1
+        lo[j, rng.choice(n, size=1 + j % 3, replace=False)] = 0
+    batch = SampleBatch(_device.to_device(x), 0, 0, state_bound=2)
+    lset = ReferenceSet.from_array(Side.LOWER, 0, lo, trusted=True)
+    uset = ReferenceSet.from_array(Side.UPPER, 0, up, trusted=True)
+    f4, _, _ = classify_flags(batch, lset, uset, 2, "fp4")
+    fb, _, _ = classify_flags(batch, lset, uset, 2, "bits")
+    got, want = f4.cpu().numpy(), fb.cpu().numpy()
+    # the data must exercise count-1 non-hits on both sides
+    min_up = (up[None, :, :] & (1 - x[:, None, :])).sum(2).min(1)
+    min_lo = ((1 - lo[None, :, :]) & x[:, None, :]).sum(2).min(1)
+    assert (min_up == 1).any() and (min_lo == 1).any() and (want == 3).any()
+    ok = bool(np.array_equal(got, want))
+    _FP4_EXACT[key] = ok
+    if not ok:
+        import warnings
+        warnings.warn("FP4 classifier self-check failed (accumulator denormals not exact on "
+                      "this device): using the int8 tcgen05 classifier", RuntimeWarning)
+    return ok
+
+
 def violation_counts(samples: EncodedBatch, refs: EncodedBatch, chunk_size: int = DEFAULT_CHUNK_SIZE,
                      method: str = "packed") -> np.ndarray:
     """Full H x R violation matrix (classify.py:57-96), ``rsr_violation_counts_rows``."""
@@ -200,7 +252,7 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
         raise ValueError("method must be 'tc', 'tc8', 'fp4' or 'bits'")
     fp4_ok = _abi.fp4_row_bytes(batch.n_components, m_eff) <= _abi.FP4_MAX_ROW_BYTES
     tc_ok = _abi.thermo_kpad(batch.n_components, m_eff) <= TC_MAX_KPAD
-    if method in ("tc", "fp4") and fp4_ok:
+    if fp4_ok and (method == "fp4" or (method == "tc" and fp4_exact())):
         a = batch.fp4(m_eff)
         rb = a.shape[1] // 2
         bl, nl, al = lower_set.device_fp4_rows(m_eff) if lower_set is not None else (None, 0, 0)
@@ -353,6 +405,11 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
     fp4 = mode != "tc8" and _abi.fp4_row_bytes(N, m_eff) <= _abi.FP4_MAX_ROW_BYTES
     if mode == "onehot" and not fp4:
         raise ValueError("encoded input needs the FP4 classifier (N(M-1) <= 831)")
+    if fp4 and not fp4_exact():
+        if mode == "onehot":
+            raise RuntimeError("encoded input needs the FP4 classifier, whose self-check "
+                               "failed on this device")
+        fp4 = False  # int8 tcgen05 classifier
     if fp4:
         width = _abi.fp4_row_bytes(N, m_eff)
         opnd_shape, opnd_dtype = (2 * width,), torch.uint8

@@ -46,7 +46,7 @@ __device__ __forceinline__ void thermo_tail(int8_t* arow, int kdim, int nbias, i
 // binary case (state = [r >= T_n], thermometer byte = 1 - state).  The row of
 // flat index fb is fb / N computed as a multiply-high by magic = floor(2^64/N)
 // plus one correction step.
-template <bool M2>
+template <bool M2, int RNG>
 __global__ void __launch_bounds__(kThreads)
 sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
               int64_t f0, int64_t f1, int64_t b_lo, int64_t nblk, uint8_t* __restrict__ states,
@@ -57,8 +57,8 @@ sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uin
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nblk) return;
   const int64_t b = b_lo + t;
-  uint64_t w[4];
-  rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+  unsigned long long rr[4];
+  rsr::draw_block<RNG, false>(b, seed, gen, rr);
   const uint64_t fb = 4ull * (uint64_t)b;
   uint64_t row = __umul64hi(fb, magic);
   int n = (int)(fb - row * (uint64_t)N);
@@ -71,7 +71,7 @@ sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uin
   int64_t rows[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const unsigned long long r = w[j] >> 11;
+    const unsigned long long r = rr[j];
     int s;
     if (M2) {
       s = r >= T[n] ? 1 : 0;
@@ -205,7 +205,7 @@ __device__ __forceinline__ void fp4_quad_fast(const uint8_t* st, uint32_t base, 
 // C32: every Philox counter of the launch fits 32 bits (flat draws < 2^34), so
 // the first round's 64x64 multiply is a 64x32 one (two IMAD.WIDE fewer per block
 // on the FMA pipe, which bounds this kernel).
-template <int MT, bool C32>  // MT 2, 3: specialised state count; 0: any M
+template <int MT, bool C32, int RNG>  // MT 2, 3: specialised state count; 0: any M
 __global__ void __launch_bounds__(kRowThreads, RSR_SAMPLE_MINB)
 sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
                    int64_t start_row, int64_t count, uint8_t* __restrict__ states,
@@ -234,18 +234,15 @@ sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed
     int n0 = (o0 + N) % N;
     const int ostep = 4 * (int)blockDim.x, nstep = ostep % N;
     for (int64_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x, o0 += ostep) {
-      uint64_t w[4];
-      if (C32)
-        rsr::philox4x64_10((uint64_t)(uint32_t)(b + 1), seed, gen, w);
-      else
-        rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+      unsigned long long rr[4];
+      rsr::draw_block<RNG, C32>(b, seed, gen, rr);
       const unsigned long long* Tn = T + n0 * Mm1;
       n0 += nstep;
       if (n0 >= N) n0 -= N;
       uint32_t s[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const unsigned long long r = w[j] >> 11;
+        const unsigned long long r = rr[j];
         const unsigned long long* Tj = Tn + j * Mm1;
         if (MT == 2) {
           s[j] = r >= Tj[0];
@@ -316,6 +313,20 @@ __global__ void philox_raw_kernel(uint64_t seed, uint64_t gen, int64_t first, in
   const int64_t b = b_lo + t;
   uint64_t w[4];
   rsr::philox4x64_10((uint64_t)b + 1ull, seed, gen, w);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t f = 4 * b + j;
+    if (f >= first && f < first + count) out[f - first] = w[j];
+  }
+}
+
+__global__ void device_raw_kernel(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
+                                  int64_t b_lo, int64_t nblk, uint32_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nblk) return;
+  const int64_t b = b_lo + t;
+  uint32_t w[4];
+  rsr::device_block((uint64_t)b, seed, gen, w);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int64_t f = 4 * b + j;
@@ -459,6 +470,17 @@ extern "C" int rsr_philox_raw(uint64_t seed, uint64_t gen, int64_t first, int64_
   return rsr::check_launch("philox_raw_kernel");
 }
 
+extern "C" int rsr_device_raw(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
+                              uint32_t* out, void* stream) {
+  RSR_REQUIRE(first >= 0 && count >= 0, "rsr_device_raw: negative range");
+  if (count == 0) return RSR_OK;
+  RSR_REQUIRE(out != nullptr, "rsr_device_raw: null output");
+  const int64_t b_lo = first / 4, b_hi = (first + count - 1) / 4, nblk = b_hi - b_lo + 1;
+  device_raw_kernel<<<(unsigned)rsr::ceil_div(nblk, kThreads), kThreads, 0,
+                      rsr::as_stream(stream)>>>(seed, gen, first, count, b_lo, nblk, out);
+  return rsr::check_launch("device_raw_kernel");
+}
+
 extern "C" int rsr_uniform_field(uint64_t seed, uint64_t gen, int64_t start, int64_t count,
                                  int n_components, double* out, void* stream) {
   RSR_REQUIRE(start >= 0 && count >= 0 && n_components >= 1, "rsr_uniform_field: bad shape");
@@ -471,10 +493,11 @@ extern "C" int rsr_uniform_field(uint64_t seed, uint64_t gen, int64_t start, int
   return rsr::check_launch("uniform_kernel");
 }
 
-extern "C" int rsr_sample(const double* probs, int n_components, int n_states, uint64_t seed,
-                          uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
-                          int8_t* out_thermo, int ld_thermo, void* stream) {
+extern "C" int rsr_sample_ex(const double* probs, int n_components, int n_states, uint64_t seed,
+                             uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+                             int8_t* out_thermo, int ld_thermo, int rng, void* stream) {
   const int N = n_components, M = n_states;
+  RSR_REQUIRE(rng == RSR_RNG_SHARED || rng == RSR_RNG_DEVICE, "rsr_sample: bad rng %d", rng);
   RSR_REQUIRE(N >= 1 && M >= 2 && M <= 255, "rsr_sample: need N >= 1 and 2 <= M <= 255");
   RSR_REQUIRE(start >= 0 && count >= 1, "rsr_sample: n_samples must be >= 1");
   RSR_REQUIRE(probs != nullptr, "rsr_sample: null probs");
@@ -485,7 +508,8 @@ extern "C" int rsr_sample(const double* probs, int n_components, int n_states, u
                 rsr::thermo_kpad(N, M));
   const size_t smem = (size_t)N * (M - 1) * sizeof(unsigned long long);
   RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample: N*(M-1) too large for the threshold table");
-  auto kern = M == 2 ? sample_kernel<true> : sample_kernel<false>;
+  auto kern = rng == RSR_RNG_DEVICE ? (M == 2 ? sample_kernel<true, 1> : sample_kernel<false, 1>)
+                                    : (M == 2 ? sample_kernel<true, 0> : sample_kernel<false, 0>);
   if (smem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t f0 = start * N, f1 = (start + count) * N;
@@ -495,6 +519,13 @@ extern "C" int rsr_sample(const double* probs, int n_components, int n_states, u
       probs, N, M, seed, gen, f0, f1, b_lo, nblk, out_states, out_thermo, ld_thermo, kdim, nbias,
       magic, start);
   return rsr::check_launch("sample_kernel");
+}
+
+extern "C" int rsr_sample(const double* probs, int n_components, int n_states, uint64_t seed,
+                          uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+                          int8_t* out_thermo, int ld_thermo, void* stream) {
+  return rsr_sample_ex(probs, n_components, n_states, seed, gen, start, count, out_states,
+                       out_thermo, ld_thermo, RSR_RNG_SHARED, stream);
 }
 
 extern "C" int rsr_encode_samples(const uint8_t* states, int64_t count, int n_components,
@@ -527,10 +558,25 @@ extern "C" int rsr_encode_refs(const uint8_t* states, int64_t count, int64_t row
   return rsr::check_launch("encode_refs_kernel");
 }
 
-extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_states, uint64_t seed,
-                              uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
-                              uint8_t* out_fp4, int row_bytes, void* stream) {
+namespace {
+template <int RNG>
+const void* rows_kernel(int M, bool c32) {
+  if (c32)
+    return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, true, RNG>)
+           : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, true, RNG>)
+                    : reinterpret_cast<const void*>(sample_rows_kernel<0, true, RNG>);
+  return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, false, RNG>)
+         : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, false, RNG>)
+                  : reinterpret_cast<const void*>(sample_rows_kernel<0, false, RNG>);
+}
+}  // namespace
+
+extern "C" int rsr_sample_fp4_ex(const double* probs, int n_components, int n_states,
+                                 uint64_t seed, uint64_t gen, int64_t start, int64_t count,
+                                 uint8_t* out_states, uint8_t* out_fp4, int row_bytes, int rng,
+                                 void* stream) {
   const int N = n_components, M = n_states;
+  RSR_REQUIRE(rng == RSR_RNG_SHARED || rng == RSR_RNG_DEVICE, "rsr_sample_fp4: bad rng %d", rng);
   RSR_REQUIRE(N >= 1 && M >= 2 && M <= 255, "rsr_sample_fp4: need N >= 1 and 2 <= M <= 255");
   RSR_REQUIRE(start >= 0 && count >= 1, "rsr_sample_fp4: n_samples must be >= 1");
   RSR_REQUIRE(probs != nullptr, "rsr_sample_fp4: null probs");
@@ -548,13 +594,12 @@ extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_state
   const size_t smem = ((size_t)(N + kTExtra) * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 +
                       2 * (size_t)st_bytes;
   RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample_fp4: N*(M-1) too large for shared memory");
-  const bool c32 = ((start + count) * (int64_t)N + 3) / 4 + 1 < ((int64_t)1 << 32);
-  auto kern = c32 ? (M == 2 ? sample_rows_kernel<2, true> : M == 3 ? sample_rows_kernel<3, true>
-                                                                 : sample_rows_kernel<0, true>)
-                  : (M == 2 ? sample_rows_kernel<2, false> : M == 3 ? sample_rows_kernel<3, false>
-                                                                  : sample_rows_kernel<0, false>);
+  // the device stream's counter is 64-bit anyway (two 32-bit words)
+  const bool c32 = rng == RSR_RNG_SHARED &&
+                   ((start + count) * (int64_t)N + 3) / 4 + 1 < ((int64_t)1 << 32);
+  const void* kern = rng == RSR_RNG_DEVICE ? rows_kernel<1>(M, false) : rows_kernel<0>(M, c32);
   if (smem > 48 * 1024) {
-    const int rc = rsr::ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+    const int rc = rsr::ensure_dynamic_smem(kern, smem);
     if (rc) return rc;
   }
   int dev = 0, sms = 0, per_sm = 0;
@@ -571,7 +616,17 @@ extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_state
   const int64_t chunks = rsr::ceil_div(count, kRowsPerCta);
   const int64_t grid = std::max<int64_t>(std::min<int64_t>(chunks, (int64_t)sms * std::max(per_sm, 1)),
                                          rsr::ceil_div(chunks, cpc));
-  kern<<<(unsigned)grid, kRowThreads, smem, rsr::as_stream(stream)>>>(
-      probs, N, M, seed, gen, start, count, out_states, out_fp4, row_bytes, st_bytes);
+  void* args[] = {(void*)&probs, (void*)&N, (void*)&M, (void*)&seed, (void*)&gen,
+                  (void*)&start, (void*)&count, (void*)&out_states, (void*)&out_fp4,
+                  (void*)&row_bytes, (void*)&st_bytes};
+  RSR_CUDA(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(kRowThreads), args, smem,
+                            rsr::as_stream(stream)));
   return rsr::check_launch("sample_rows_kernel");
+}
+
+extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_states, uint64_t seed,
+                              uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
+                              uint8_t* out_fp4, int row_bytes, void* stream) {
+  return rsr_sample_fp4_ex(probs, n_components, n_states, seed, gen, start, count, out_states,
+                           out_fp4, row_bytes, RSR_RNG_SHARED, stream);
 }

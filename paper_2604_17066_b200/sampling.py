@@ -26,9 +26,11 @@ class SampleBatch:
     ``states`` may be a host array (any integer dtype) or a CUDA uint8 tensor.
     """
 
-    def __init__(self, states, seed: int, generation_index: int, *, state_bound: int | None = None):
+    def __init__(self, states, seed: int, generation_index: int, *, state_bound: int | None = None,
+                 rng: str = "shared"):
         self.seed = int(seed)
         self.generation_index = int(generation_index)
+        self.rng = rng  # the stream that regenerates the batch (sample_batch)
         self._host: np.ndarray | None = None
         self._dev: torch.Tensor | None = None
         self._thermo: dict[int, torch.Tensor] = {}
@@ -144,22 +146,36 @@ def uniform_field(seed: int, generation_index: int, start: int, count: int,
     return out.cpu().numpy()
 
 
+RNG_KINDS = {"shared": _abi.RNG_SHARED, "device": _abi.RNG_DEVICE}
+
+
+def rng_code(rng: str) -> int:
+    try:
+        return RNG_KINDS[rng]
+    except KeyError:
+        raise ValueError(f"rng must be 'shared' or 'device', got {rng!r}") from None
+
+
 def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
                  generation_index: int = 0, start: int = 0, *, encode: bool = False,
                  fp4: bool | None = None,
                  out_states: torch.Tensor | None = None,
                  out_thermo: torch.Tensor | None = None,
-                 out_fp4: torch.Tensor | None = None) -> SampleBatch:
+                 out_fp4: torch.Tensor | None = None,
+                 rng: str = "shared") -> SampleBatch:
     """Inverse-CDF draw on the counter-based stream (sampling.py:69-90), on device.
 
     By default (``fp4`` None -> on whenever the FP4 classifier handles the row
     width) one kernel, ``rsr_sample_fp4``, writes the uint8 states and the FP4
     sample operand of the default classifier.  ``encode`` (or ``out_thermo``)
     instead runs ``rsr_sample`` with the int8 thermometer rows fused.
-    ``out_*`` let callers reuse preallocated buffers.
+    ``out_*`` let callers reuse preallocated buffers.  ``rng="shared"`` is the
+    reference's Philox4x64-10 stream (bit-exact); ``rng="device"`` the independent
+    Philox4x32-10 device stream (include/rsr_b200.h RSR_RNG_DEVICE).
     """
     if n_samples < 1:
         raise ValueError("n_samples must be >= 1")
+    code = rng_code(rng)
     n, m = dist.n_components, dist.n_states
     dev = _device.device()
     states = out_states if out_states is not None else torch.empty(
@@ -174,10 +190,10 @@ def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
             (n_samples, 2 * rb), dtype=torch.uint8, device=dev)
         if a4.dtype != torch.uint8 or a4.shape != (n_samples, 2 * rb):
             raise ValueError("fp4 buffer must be uint8 [>= H, 2 * row_bytes]")
-        _abi.call("rsr_sample_fp4", _abi.ptr(dist.device_probs()), n, m, seed & mask,
+        _abi.call("rsr_sample_fp4_ex", _abi.ptr(dist.device_probs()), n, m, seed & mask,
                   generation_index & mask, start, n_samples, _abi.ptr(states), _abi.ptr(a4), rb,
-                  _device.stream())
-        batch = SampleBatch(states, seed, generation_index, state_bound=m)
+                  code, _device.stream())
+        batch = SampleBatch(states, seed, generation_index, state_bound=m, rng=rng)
         batch._fp4[m] = a4
         return batch
     thermo = None
@@ -185,10 +201,10 @@ def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
     if int8_path:
         thermo = out_thermo if out_thermo is not None else torch.empty(
             (n_samples, kpad), dtype=torch.int8, device=dev)
-    _abi.call("rsr_sample", _abi.ptr(dist.device_probs()), n, m, seed & mask,
+    _abi.call("rsr_sample_ex", _abi.ptr(dist.device_probs()), n, m, seed & mask,
               generation_index & mask, start, n_samples, _abi.ptr(states), _abi.ptr(thermo),
-              kpad, _device.stream())
-    batch = SampleBatch(states, seed, generation_index, state_bound=m)
+              kpad, code, _device.stream())
+    batch = SampleBatch(states, seed, generation_index, state_bound=m, rng=rng)
     if thermo is not None:
         batch._thermo[m] = thermo
     if out_fp4 is not None:

@@ -23,6 +23,7 @@ from __future__ import annotations
 import ctypes
 import os
 import time
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -30,9 +31,11 @@ import torch
 
 from . import _abi, _device
 from .boundary import ReferenceSet, ReferenceState, Side, boundary_search_batch
-from .classify import cov, classify
-from .dist import Comm, global_pick_owners, shard_range
+from .classify import classify, cov, fp4_exact
+from .dist import (Comm, counts_record, global_pick_owners, picks_in_prefix, shard_range,
+                   split_records)
 from .model import ComponentDistribution, SystemModel
+from .sampling import rng_code as _rng_code
 from .sampling import sample_batch
 
 __all__ = ["RunConfig", "TraceRecord", "Stage1Result", "Stage2Report", "PmfReport",
@@ -63,6 +66,10 @@ class RunConfig:
     n_workers: int = 1
     stage2_samples: int | None = None
     boundary_search_enabled: bool = True
+    # not in the reference: "shared" draws the reference's Philox4x64-10 stream
+    # (bit-exact results); "device" the independent Philox4x32-10 device stream
+    # (statistically equivalent estimates, north_star "independent device RNG")
+    rng: str = "shared"
 
     def __post_init__(self) -> None:
         if self.n_samples < 1:
@@ -73,6 +80,8 @@ class RunConfig:
             raise ValueError("r_max must be >= 1")
         if self.parallel_searches < 1:
             raise ValueError("parallel_searches must be >= 1")
+        if self.rng not in ("shared", "device"):
+            raise ValueError("rng must be 'shared' or 'device'")
 
 
 @dataclass(frozen=True)
@@ -152,8 +161,9 @@ class _Prefetcher:
     not depend on the references) is drawn while iteration i searches and
     inserts on the main stream."""
 
-    def __init__(self, dist_, seed, start, count):
+    def __init__(self, dist_, seed, start, count, rng="shared"):
         self.dist, self.seed, self.start, self.count = dist_, seed, start, count
+        self.rng = rng
         self.bufs = [_BatchBuffers(max(count, 1), dist_.n_components, dist_.n_states)
                      for _ in range(2)]
         self.stream = torch.cuda.Stream()
@@ -166,7 +176,8 @@ class _Prefetcher:
             if self.free[slot] is not None:
                 self.stream.wait_event(self.free[slot])
             batch = sample_batch(self.dist, self.count, self.seed, gen, self.start,
-                                 out_states=b.states, out_fp4=b.fp4 if b.fp4_ok else None)
+                                 out_states=b.states, out_fp4=b.fp4 if b.fp4_ok else None,
+                                 rng=self.rng)
             ready = torch.cuda.Event()
             ready.record(self.stream)
         return batch, ready
@@ -184,8 +195,11 @@ def _classify_shard(model, pending, lower, upper, comm):
     batch, ready = pending
     torch.cuda.current_stream().wait_event(ready)
     res = classify(batch, lower, upper, n_states=model.n_component_states)
-    counts = comm.allreduce_sum_i64(list(res.counts)) if comm.distributed else np.array(res.counts)
-    return batch, res, counts
+    if not comm.distributed:
+        return batch, res, np.array(res.counts), None
+    # one all-gather of every rank's counts: sums and per-rank unclassified counts
+    per = comm.allgather_i64_vec(list(res.counts))
+    return batch, res, per.sum(0), per[:, 2].copy()
 
 
 def stage1_find_references(model: SystemModel, dist: ComponentDistribution, config: RunConfig,
@@ -208,6 +222,7 @@ def stage1_find_references(model: SystemModel, dist: ComponentDistribution, conf
     loop_stream.wait_stream(caller)
     use_async = (os.environ.get("RSR_SYNC_LOOP") != "1"
                  and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.FP4_MAX_ROW_BYTES
+                 and fp4_exact()
                  and dist.n_states == model.n_component_states
                  and config.parallel_searches <= 4096)
     with torch.cuda.stream(loop_stream):
@@ -226,12 +241,12 @@ def _stage1_loop(model, dist, config, threshold, comm, phi, lower, upper, start,
     trace: list[TraceRecord] = []
     redundant = 0
     terminated_by = "r_max"
-    pre = _Prefetcher(dist, config.seed, start, count)
+    pre = _Prefetcher(dist, config.seed, start, count, config.rng)
     pending = pre.launch(0)
     N = dist.n_components
     iteration = 0
     while True:
-        batch, res, counts = _classify_shard(model, pending, lower, upper, comm)
+        batch, res, counts, per_rank = _classify_shard(model, pending, lower, upper, comm)
         pending = pre.launch(iteration + 1)
         n_l, n_u, n_x = (int(c) for c in counts[:3])
         trace.append(TraceRecord(
@@ -248,7 +263,7 @@ def _stage1_loop(model, dist, config, threshold, comm, phi, lower, upper, start,
         rng = np.random.default_rng([config.seed, iteration])
         n_pick = min(config.parallel_searches, n_x)
         positions = rng.choice(n_x, size=n_pick, replace=False)
-        x0 = _gather_picks(batch, res, positions, comm, N)
+        x0 = _gather_picks(batch, res, positions, comm, N, per_rank)
         if config.boundary_search_enabled:
             refs_d, side_d, calls_d = boundary_search_batch(model, x0, threshold)
         else:
@@ -396,8 +411,10 @@ class _LeanPrefetcher:
     With a `_BatchCache`, generations already drawn are read from it (their picks are
     decoded from the FP4 rows) and new ones are drawn into it."""
 
-    def __init__(self, dist_, seed, start, count, m, cache: _BatchCache | None = None):
+    def __init__(self, dist_, seed, start, count, m, cache: _BatchCache | None = None,
+                 rng: str = "shared"):
         dev = _device.device()
+        self.rng = _rng_code(rng)
         n = dist_.n_components
         self.n, self.m, self.seed, self.start, self.count = n, m, seed, start, count
         self.rb = _abi.fp4_row_bytes(n, m)
@@ -426,9 +443,9 @@ class _LeanPrefetcher:
             dst = self.cache.reserve(gen) if self.cache is not None else None
             dst = self.fp4[slot] if dst is None else dst
             mask = (1 << 64) - 1
-            _abi.call("rsr_sample_fp4", self.probs, self.n, self.m, self.seed & mask, gen & mask,
-                      self.start, self.count, _abi.ptr(self.states[slot]), _abi.ptr(dst), self.rb,
-                      self.sptr)
+            _abi.call("rsr_sample_fp4_ex", self.probs, self.n, self.m, self.seed & mask,
+                      gen & mask, self.start, self.count, _abi.ptr(self.states[slot]),
+                      _abi.ptr(dst), self.rb, self.rng, self.sptr)
             self.src[slot], self.has_states[slot] = dst, True
         self.ready[slot].record(self.stream)
         return slot
@@ -469,10 +486,18 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
     rep = report_h.numpy()
     flags = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
     labels = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
-    idx = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+    # zero-initialised: the speculative prefix gather may read entries past the count
+    idx = torch.zeros(max(count, 1), dtype=torch.int64, device=dev)
     cnt = torch.empty(1, dtype=torch.int64, device=dev)
     cscratch = torch.empty(max(1, _abi.call("rsr_compact_scratch", count)), dtype=torch.int64,
                            device=dev)
+    # multi-rank: one all-gather per iteration of [counts | rows of the first C
+    # unclassified samples] (dist.py); C = B covers every pick of a rank with at most
+    # B unclassified samples
+    C = B if comm.distributed else 0
+    pref_pos = torch.arange(max(C, 1), dtype=torch.int64, device=dev)
+    pref_rows = torch.zeros((max(C, 1), N), dtype=torch.uint8, device=dev)
+    exch = {}
     pos_h = torch.empty(B, dtype=torch.int64, pin_memory=True)
     pos_d = torch.empty(B, dtype=torch.int64, device=dev)
     x0 = torch.empty((B, N), dtype=torch.uint8, device=dev)
@@ -488,7 +513,7 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
     lo_p = ctypes.byref(refs.desc[0])
     up_p = ctypes.byref(refs.desc[1])
 
-    pre = _LeanPrefetcher(dist, config.seed, start, count, M, batch_cache)
+    pre = _LeanPrefetcher(dist, config.seed, start, count, M, batch_cache, config.rng)
 
     # Two-pass classification: most samples are dominated by one of the first
     # upper references (tools/first_match_hist.py: after 480 of cfg3's 10^4
@@ -539,9 +564,23 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
                       None, 0, st_ptr)
         _abi.call("rsr_finalize", _abi.ptr(flags), count, _abi.ptr(labels), _abi.ptr(report_d),
                   st_ptr)
+        if comm.distributed:
+            _abi.call("rsr_compact", _abi.ptr(labels), count, _abi.LABEL_UNCLASSIFIED,
+                      _abi.ptr(idx), _abi.ptr(cnt), _abi.ptr(cscratch), st_ptr)
+            gather_rows_at(slot, pref_pos, C, pref_rows, st_ptr)
+            exch["recs"] = comm.allgather_bytes(counts_record(report_d[:4], pref_rows))
         report_h.copy_(report_d, non_blocking=True)
         ready_ev.record(main)
         return slot
+
+    def gather_rows_at(slot, pos_dev, n, out, sp):
+        """out[j] = state row of local unclassified position pos_dev[j] (idx compacted)."""
+        if pre.has_states[slot]:
+            _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
+                      _abi.ptr(pos_dev), n, _abi.ptr(out), sp)
+        else:
+            _abi.call("rsr_gather_picks_fp4", _abi.ptr(pre.src[slot]), rb, N, M, _abi.ptr(idx),
+                      _abi.ptr(pos_dev), n, _abi.ptr(out), sp)
 
     def gather_local(slot, n_local, out):
         """Rows of this rank's picks (local positions in pos_h) -> out[:n_local]."""
@@ -549,12 +588,7 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         sp = _device.stream()
         _abi.call("rsr_compact", _abi.ptr(labels), count, _abi.LABEL_UNCLASSIFIED, _abi.ptr(idx),
                   _abi.ptr(cnt), _abi.ptr(cscratch), sp)
-        if pre.has_states[slot]:
-            _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
-                      _abi.ptr(pos_d), n_local, _abi.ptr(out), sp)
-        else:
-            _abi.call("rsr_gather_picks_fp4", _abi.ptr(pre.src[slot]), rb, N, M, _abi.ptr(idx),
-                      _abi.ptr(pos_d), n_local, _abi.ptr(out), sp)
+        gather_rows_at(slot, pos_d, n_local, out, sp)
 
     def search_and_insert(slot, n_pick, gather=True):
         """positions -> picked rows -> boundary searches -> device insertion: fixed
@@ -597,8 +631,9 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
         ready_ev.synchronize()
         n_l, n_u, n_x = int(rep[0]), int(rep[1]), int(rep[2])
         if comm.distributed:  # shard counts -> batch counts; per-rank unclassified counts
-            per_rank = comm.allgather_i64(n_x)
-            n_l, n_u, n_x = (int(v) for v in comm.allreduce_sum_i64([n_l, n_u, n_x]))
+            counts_all, prefix = split_records(exch.pop("recs"), 4, C, N)
+            per_rank = counts_all[:, 2].copy()
+            n_l, n_u, n_x = (int(v) for v in counts_all[:, :3].sum(0))
         if searched:
             refs.known = [int(rep[4]), int(rep[6])]
             refs.pending = 0
@@ -625,17 +660,22 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
             # global positions (rank-ordered unclassified list) -> owners; every rank
             # gathers its own rows, then all picked rows in pick order on every rank
             owner, local = global_pick_owners(per_rank, np.asarray(positions, dtype=np.int64))
-            mine = np.flatnonzero(owner == comm.rank)
-            pos_h.numpy()[:len(mine)] = local[mine]
-            rows = torch.empty((len(mine), N), dtype=torch.uint8, device=dev)
-            if len(mine):
-                gather_local(slot, len(mine), rows)
-            gathered = comm.allgather_rows(rows, np.bincount(owner, minlength=comm.world)).to(dev)
-            order = np.argsort(owner, kind="stable")
-            inv = np.empty_like(order)
-            inv[order] = np.arange(len(order))
-            x0[:n_pick].copy_(gathered.index_select(
-                0, torch.as_tensor(inv, dtype=torch.int64, device=dev)))
+            if picks_in_prefix(owner, local, C):
+                # every picked row arrived with the counts: no second exchange
+                sel = torch.as_tensor(owner * C + local, dtype=torch.int64).to(dev, non_blocking=True)
+                torch.index_select(prefix.reshape(-1, N), 0, sel, out=x0[:n_pick])
+            else:
+                mine = np.flatnonzero(owner == comm.rank)
+                pos_h.numpy()[:len(mine)] = local[mine]
+                rows = torch.empty((len(mine), N), dtype=torch.uint8, device=dev)
+                if len(mine):
+                    gather_local(slot, len(mine), rows)
+                gathered = comm.allgather_rows(rows, np.bincount(owner, minlength=comm.world)).to(dev)
+                order = np.argsort(owner, kind="stable")
+                inv = np.empty_like(order)
+                inv[order] = np.arange(len(order))
+                x0[:n_pick].copy_(gathered.index_select(
+                    0, torch.as_tensor(inv, dtype=torch.int64, device=dev)))
         else:
             pos_h.numpy()[:n_pick] = positions
         if refs.prepare_insert(n_pick, full_grid=use_graphs):
@@ -683,7 +723,8 @@ def _to_host(*tensors):
     return [None if h is None else h.numpy() for h in outs]
 
 
-def _gather_picks(batch, res, positions: np.ndarray, comm: Comm, N: int) -> torch.Tensor:
+def _gather_picks(batch, res, positions: np.ndarray, comm: Comm, N: int,
+                  per_rank: np.ndarray | None = None) -> torch.Tensor:
     """Rows of the picked unclassified samples, in pick order, on every rank."""
     dev = batch.device_states().device
     if not comm.distributed:
@@ -693,7 +734,8 @@ def _gather_picks(batch, res, positions: np.ndarray, comm: Comm, N: int) -> torc
         _abi.call("rsr_gather_rows", _abi.ptr(batch.device_states()), N, _abi.ptr(sel),
                   len(positions), _abi.ptr(out), _device.stream())
         return out
-    per_rank = comm.allgather_i64(res.counts[2])
+    if per_rank is None:
+        per_rank = comm.allgather_i64(res.counts[2])
     owner, local = global_pick_owners(per_rank, np.asarray(positions, dtype=np.int64))
     mine = np.flatnonzero(owner == comm.rank)
     rows = torch.empty((len(mine), N), dtype=torch.uint8, device=dev)
@@ -710,10 +752,10 @@ def _gather_picks(batch, res, positions: np.ndarray, comm: Comm, N: int) -> torc
     return gathered.index_select(0, torch.as_tensor(inv, dtype=torch.int64, device=dev)).contiguous()
 
 
-def _stage2_counts(model, dist, lower, upper, threshold, seed, start, count, comm):
+def _stage2_counts(model, dist, lower, upper, threshold, seed, start, count, comm, rng="shared"):
     """(n_low, n_up, unclassified) of samples [start, start+count) of generation 0."""
     phi = model.device_phi()
-    batch = sample_batch(dist, count, seed, _STAGE2_GENERATION, start)
+    batch = sample_batch(dist, count, seed, _STAGE2_GENERATION, start, rng=rng)
     res = classify(batch, lower, upper, n_states=model.n_component_states)
     n_low, n_up, n_x = res.counts
     leq = 0
@@ -738,7 +780,8 @@ def stage2_evaluate(model: SystemModel, dist: ComponentDistribution, lower: Refe
     h = config.stage2_samples or config.n_samples
     start, count = shard_range(h, comm.world, comm.rank)
     n_low, n_up, n_x = (int(v) for v in _stage2_counts(model, dist, lower, upper, threshold,
-                                                       config.seed, start, count, comm))
+                                                       config.seed, start, count, comm,
+                                                       config.rng))
     model.add_evaluations(n_x)
     p_low, p_up = n_low / h, n_up / h
     return Stage2Report(p_lower=p_low, p_upper=p_up, cov_lower=cov(p_low, h),
@@ -749,27 +792,45 @@ def stage2_evaluate(model: SystemModel, dist: ComponentDistribution, lower: Refe
 def stage2_until_cov(model: SystemModel, dist: ComponentDistribution, lower, upper,
                      config: RunConfig, threshold: int, target_cov: float = 0.05,
                      batch_samples: int | None = None, max_batches: int = 1_000_000,
-                     side: str = "lower", comm: Comm | None = None) -> Stage2Report:
+                     side: str = "lower", comm: Comm | None = None,
+                     max_samples: int | None = 1 << 36) -> Stage2Report:
     """Run-to-c.o.v. loop (not in the reference).
 
     Batch j is samples [j*H, (j+1)*H) of the generation-0 stream, so batch 0
     is exactly ``stage2_evaluate``; integer counts accumulate until the
-    c.o.v. of the chosen side's estimate is <= ``target_cov``.
+    c.o.v. of the chosen side's estimate is <= ``target_cov``.  The loop also
+    stops after ``max_batches`` batches or ``max_samples`` samples (an estimate
+    that stays 0 has no c.o.v.), with a RuntimeWarning.
     """
     _check_threshold(model, threshold)
+    if side not in ("lower", "upper"):
+        raise ValueError(f"side must be 'lower' or 'upper', got {side!r}")
+    if not target_cov > 0.0:
+        raise ValueError("target_cov must be > 0")
+    for s in (lower, upper):
+        if s is not None and s.threshold != threshold:
+            raise ValueError(f"reference set threshold {s.threshold} != requested m'={threshold}")
     comm = comm or Comm.single()
     h = batch_samples or config.stage2_samples or config.n_samples
+    if h < 1:
+        raise ValueError("batch_samples must be >= 1")
+    limit = max_batches if max_samples is None else max(1, min(max_batches, max_samples // h))
     tot = np.zeros(3, dtype=np.int64)
     n = 0
-    for j in range(max_batches):
+    reached = False
+    for j in range(limit):
         start, count = shard_range(h, comm.world, comm.rank)
         tot += _stage2_counts(model, dist, lower, upper, threshold, config.seed, j * h + start,
-                              count, comm)
+                              count, comm, config.rng)
         n += h
         p = (tot[0] if side == "lower" else tot[1]) / n
         c = cov(p, n)
         if c is not None and c <= target_cov:
+            reached = True
             break
+    if not reached:
+        warnings.warn(f"stage2_until_cov stopped after {n} samples without reaching c.o.v. "
+                      f"{target_cov} on the {side} estimate", RuntimeWarning, stacklevel=2)
     model.add_evaluations(int(tot[2]))
     p_low, p_up = tot[0] / n, tot[1] / n
     return Stage2Report(p_lower=p_low, p_upper=p_up, cov_lower=cov(p_low, n),

@@ -119,3 +119,93 @@ def test_four_rank_grid_or_reduce_and_counts():
         assert (s_idx, k_idx) == divmod(rank, 2)
     for rank, *_, counts in out:
         assert counts == want_counts.tolist()
+
+
+def _fused_worker(rank, world, port, q):
+    """The Stage-1 iteration exchange of workflow._stage1_loop_async on gloo: one
+    all-gather of [counts | first C unclassified rows] per iteration, the picks taken
+    from the exchanged prefixes when they all fall inside them, a second all-gather of
+    the picked rows otherwise."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    from paper_2604_17066_b200.dist import (Comm, counts_record, global_pick_owners,
+                                            picks_in_prefix, shard_range, split_records)
+    import oracle
+    comm = Comm.from_env(backend="gloo")
+    calls = {"n": 0}
+    for name in ("all_gather_into_tensor", "all_gather", "all_reduce"):
+        orig = getattr(dist, name)
+
+        def counted(*a, _orig=orig, **k):
+            calls["n"] += 1
+            return _orig(*a, **k)
+        setattr(dist, name, counted)
+    H, N, B = 997, 9, 6
+    probs = np.tile([0.35, 0.65], (N, 1))
+    start, count = shard_range(H, world, rank)
+    results = []
+    for it, thr in enumerate((6, 3, 1)):  # many, fewer, few unclassified samples
+        xs = oracle.sample_states(probs, count, seed=9, generation_index=it, start=start)
+        unc = np.flatnonzero(xs.sum(1) <= thr)
+        counts = [7, 11, len(unc), 0]
+        C = B
+        pref = np.zeros((C, N), dtype=np.uint8)
+        pref[:min(C, len(unc))] = xs[unc[:C]]
+        before = calls["n"]
+        recs = comm.allgather_bytes(counts_record(counts, torch.as_tensor(pref)))
+        all_counts, prefix = split_records(recs, 4, C, N)
+        per_rank = all_counts[:, 2].copy()
+        total = int(per_rank.sum())
+        pos = np.random.default_rng([9, it]).choice(total, size=min(B, total), replace=False)
+        owner, local = global_pick_owners(per_rank, pos)
+        fused = picks_in_prefix(owner, local, C)
+        if fused:
+            rows = prefix.reshape(-1, N)[torch.as_tensor(owner * C + local)]
+        else:
+            mine = np.flatnonzero(owner == comm.rank)
+            g = comm.allgather_rows(torch.as_tensor(xs[unc[local[mine]]].astype(np.uint8)),
+                                    np.bincount(owner, minlength=world))
+            order = np.argsort(owner, kind="stable")
+            inv = np.empty_like(order)
+            inv[order] = np.arange(len(order))
+            rows = g[torch.as_tensor(inv)]
+        results.append((rows.tolist(), all_counts.sum(0).tolist(), fused, calls["n"] - before))
+    # counts matrix of several values in one all-gather
+    per = comm.allgather_i64_vec([rank, 10 * rank + 1])
+    # in-place OR of hit planes twice (the planes buffer is reused)
+    for _ in range(2):
+        hits = torch.tensor([[1, 0, 2, 0, 3], [2, 0, 0, 1, 1]][rank], dtype=torch.uint8)
+        comm.allreduce_or_hits(hits)
+    q.put((rank, results, per.tolist(), hits.tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_fused_iteration_exchange_two_ranks():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=100) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=30)
+    import oracle
+    fused_seen = set()
+    for it, thr in enumerate((6, 3, 1)):
+        xs = oracle.sample_states(np.tile([0.35, 0.65], (9, 1)), 997, seed=9, generation_index=it)
+        unc = np.flatnonzero(xs.sum(1) <= thr)
+        pos = np.random.default_rng([9, it]).choice(len(unc), size=min(6, len(unc)), replace=False)
+        want = xs[unc[pos]].tolist()
+        for rank, results, per, hits in out:
+            rows, sums, fused, n_coll = results[it]
+            assert rows == want and sums == [14, 22, len(unc), 0]
+            assert n_coll == (1 if fused else 2)  # one collective when the prefix covers the picks
+            fused_seen.add(fused)
+    assert fused_seen == {True, False}
+    for rank, results, per, hits in out:
+        assert per == [[0, 1], [1, 11]] and hits == [3, 0, 2, 1, 3]

@@ -156,19 +156,43 @@ def test_device_calls_fail_loudly_without_cuda():
 
 
 @pytest.mark.timeout(180)
-def test_bench_reference_arm_runs_on_cpu():
-    """`bench.py --impl reference` (the driver's reference arm: the oracle port of the
-    reference classifier on the host cores) prints one well-formed JSON line."""
+def _bench(args, env_extra=None, timeout=240):
     import json
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
-    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
-                          "--steps", "1", "--warmup", "1"], cwd=root, env=env, check=True,
-                         capture_output=True, text=True, timeout=170).stdout
-    line = json.loads([x for x in out.splitlines() if x.startswith("{")][-1])
+    env.pop("WORLD_SIZE", None)
+    env.update(env_extra or {})
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, cwd=root, env=env,
+                       capture_output=True, text=True, timeout=timeout)
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    return r, lines
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """`bench.py --impl reference` (the driver's reference arm: the reference's own
+    classification on the host cores) prints one well-formed JSON line."""
+    r, lines = _bench(["--impl", "reference", "--config", "cfg2", "--steps", "1", "--warmup", "1",
+                       "--cpu-seconds", "1"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = lines[-1]
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "pairs/s"
     assert line["e2e"]["value"] == line["value"] and line["cpu_baseline"]["cores"] >= 1
     assert line["config"]["ref_states"] == 20_000
+    assert line["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+def test_bench_gpus_flag_relaunches_under_torchrun():
+    """`python bench.py --gpus 2` without torchrun runs two ranks (the reference arm:
+    rank 0 prints, rank 1 exits without work); a WORLD_SIZE that disagrees with
+    --gpus fails loudly instead of measuring another world size."""
+    r, lines = _bench(["--impl", "reference", "--gpus", "2", "--config", "cfg4", "--k", "300",
+                       "--steps", "1", "--warmup", "1", "--cpu-seconds", "1"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "launching 2 ranks" in r.stderr
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["config"]["ref_states"] == 300
+    r, lines = _bench(["--impl", "reference", "--gpus", "2", "--steps", "1"],
+                      env_extra={"WORLD_SIZE": "1"})
+    assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr and not lines

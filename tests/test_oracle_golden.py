@@ -138,3 +138,31 @@ def test_stage1_time_budget_records_elapsed():
     r = oracle.stage1(ev, np.tile([0.1, 0.9], (3, 1)), 0, 2000, eps_u=1e-3, r_max=50, seed=7,
                       time_budget=1e-9)
     assert r["terminated_by"] == "budget" and "elapsed" in r["trace"][0]
+
+
+def test_device_stream_philox4x32_known_answers():
+    # Random123 known-answer vectors of Philox4x32-10 (the independent device
+    # stream, include/rsr_b200.h RSR_RNG_DEVICE, is not part of the reference)
+    from oracle.philox import device_raw, philox4x32_blocks
+    f = 0xFFFFFFFF
+    kat = [((0, 0, 0, 0, 0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+           ((f, f, f, f, f, f), (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+           ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344, 0xA4093822, 0x299F31D0),
+            (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1))]
+    for args, want in kat:
+        assert tuple(int(v) for v in philox4x32_blocks(*args)) == want
+    # stream layout: word f of (seed, gen) is word f % 4 of block f // 4, counter
+    # [b lo, b hi, gen lo, gen hi], key [seed lo, seed hi]
+    seed, gen = (1 << 63) + 12345, (1 << 40) + 7
+    b = (1 << 33) + 5
+    blk = philox4x32_blocks(b & f, b >> 32, gen & f, gen >> 32, seed & f, seed >> 32)
+    assert np.array_equal(device_raw(seed, gen, 4 * b + 1, 3), blk[1:])
+    # inverse CDF at 2^-32 resolution on the same fp64 cumsum
+    probs = np.array([[0.25, 0.5, 0.25], [0.1, 0.0, 0.9]])
+    xs = oracle.sample_states(probs, 1000, 3, 2, 17, rng="device")
+    raw = device_raw(3, 2, 17 * 2, 2000).reshape(1000, 2).astype(np.float64)
+    cum = np.cumsum(probs, axis=1)
+    want = np.minimum((raw[:, :, None] >= np.ceil(cum * 2.0 ** 32)[None]).sum(2), 2)
+    assert np.array_equal(xs, want)
+    with pytest.raises(ValueError):
+        oracle.sample_states(probs, 4, 0, rng="numpy")
