@@ -1,8 +1,9 @@
 """Sharded Stage 1 / Stage 2 over 2 ranks reproduces the single-device results.
 
-Both ranks run on the one visible GPU with gloo collectives (host-side); no
-kernel waits on another rank, so sharing the device is safe.  On an 8-GPU node
-the same code runs with NCCL, one GPU per rank.
+gloo: both ranks run on the one visible GPU with host-side collectives; no
+kernel waits on another rank, so sharing the device is safe.  nccl: one GPU per
+rank (skipped with fewer than 2 GPUs) -- the same code with CUDA tensors in the
+collectives (dist.Comm: fused per-iteration all-gather, row all-gather).
 """
 
 import os
@@ -25,7 +26,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, q, sync_loop="0"):
+def _worker(rank, world, port, case, q, sync_loop="0", backend="gloo"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank), RSR_SYNC_LOOP=sync_loop)
     import sys
@@ -33,13 +34,13 @@ def _worker(rank, world, port, case, q, sync_loop="0"):
     sys.path.insert(0, os.path.dirname(here))
     sys.path.insert(0, here)
     import torch
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(rank if backend == "nccl" else 0)
     import paper_2604_17066_b200 as P
     from paper_2604_17066_b200.dist import Comm
     from _specs import device_model, load_json as lj
     rec = next(c for c in lj("workflow.json") if c["spec"]["name"] == case)
     spec = rec["spec"]
-    comm = Comm.from_env(backend="gloo")
+    comm = Comm.from_env(backend=backend)
     model = device_model(spec["model"])
     dist = P.ComponentDistribution(np.array(spec["probs"]))
     cfg = P.RunConfig(**spec["config"])
@@ -61,15 +62,20 @@ def _worker(rank, world, port, case, q, sync_loop="0"):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
 @pytest.mark.parametrize("loop", ["async", "sync"])
 @pytest.mark.parametrize("case", CASES)
-def test_two_rank_workflow_matches_single_device(case, loop):
+def test_two_rank_workflow_matches_single_device(case, loop, backend):
     # async: device-resident reference sets, rows of the picks exchanged per
     # iteration; sync: the host-resolved insertion path
+    import torch
+    if backend == "nccl" and torch.cuda.device_count() < 2:
+        pytest.skip("NCCL ranks need one GPU each")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q, "1" if loop == "sync" else "0"))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, 2, port, case, q, "1" if loop == "sync" else "0", backend))
              for r in range(2)]
     for p in procs:
         p.start()

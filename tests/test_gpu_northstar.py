@@ -190,7 +190,8 @@ def test_full_batch_loop_prefix_vs_oracle(cfg_name):
 
 @pytest.fixture
 def fp4_selfcheck_reset():
-    from paper_2604_17066_b200 import classify as C
+    import importlib
+    C = importlib.import_module("paper_2604_17066_b200.classify")
     saved = dict(C._FP4_EXACT)
     C._FP4_EXACT.clear()
     yield C
