@@ -49,17 +49,18 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 // epilogue of tile j overlaps the MMAs of tile j+1.  Reading a 128 x 240 fp32
 // accumulator out of TMEM is the epilogue's cost (tools/tmem_bw.cu: 32x32b
 // loads reach 175 / 324 / 459 B/clk per SM with 4 / 8 / 16 warps, and twice that
-// with .pack::16b); kEpiWarps warps (kEpiWarps / 4 per TMEM lane quarter) each
-// own 240 / (kEpiWarps / 4) columns.  With 4 warps each row's whole tile sits
-// in one thread (120 packed registers, 254 registers per thread) and the group
-// end needs no cross-warp exchange.  Measured (kernel ms, current kernel):
-// cfg2 4 warps 1.607 / 8 warps 1.617 / 16 warps 1.70; cfg4 K=10^3 0.404 / 0.412;
-// K=10^4 3.143 / 3.18 (an earlier kernel version had preferred 8).
-#ifndef RSR_FP4_EPI_WARPS
-#define RSR_FP4_EPI_WARPS 4
-#endif
-#ifndef RSR_FP4_GROUP_RELEASE
-#define RSR_FP4_GROUP_RELEASE 0
+// with .pack::16b).  Each epilogue warp owns one TMEM lane quarter and a row's
+// whole tile (up to 120 packed registers).  kEpiSets sets of 4 warps take turns
+// by tile: set e handles tiles e, e + kEpiSets, ... of the cluster's sequence, so
+// a set has kEpiSets tile times for each tile's load, release and reduction, and a
+// finished tile always finds its set idle.  With one set (r1) the epilogue was
+// busy ~430 of each 208-column tile's ~630 cycles and its queueing delayed the
+// buffer release (tools/fp4_prof.py; an RSR_FP4_X_NOMIN build that skips the
+// reduction ran cfg4 K = 10^3 6 % faster).  Splitting a tile's columns over two
+// warps per lane quarter instead (r1) cost more than it saved: 16 arrivals per
+// tile and a cross-warp exchange per group.
+#ifndef RSR_FP4_EPI_SETS
+#define RSR_FP4_EPI_SETS 2
 #endif
 #ifndef RSR_FP4_SPIN
 #define RSR_FP4_SPIN 0
@@ -70,8 +71,9 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 #ifndef RSR_FP4_EPI_SPIN
 #define RSR_FP4_EPI_SPIN 0
 #endif
-constexpr int kEpiWarps = RSR_FP4_EPI_WARPS;
-constexpr int kColGroups = kEpiWarps / 4;
+constexpr int kEpiSets = RSR_FP4_EPI_SETS;
+static_assert(kEpiSets == 1 || kEpiSets == 2 || kEpiSets == 4, "epilogue sets: 1, 2 or 4");
+constexpr int kEpiWarps = 4 * kEpiSets;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 
 // Reference tile geometry for MMA N = TN (a multiple of 16; the launch picks
@@ -82,9 +84,8 @@ struct Tile {
   static constexpr int kBufs = 480 / TN;
   static constexpr int kHalfRows = TN / 2;             // reference rows per CTA per tile
   static constexpr int kChunkB = kHalfRows * kChunk;   // bytes per K-step per CTA
-  static constexpr int kCols = TN / kColGroups;        // accumulator columns per epilogue warp
+  static constexpr int kCols = TN;                      // accumulator columns per epilogue warp
   static_assert(TN % 16 == 0 && TN <= 240 && kBufs >= 2 && kBufs <= 4, "bad tile N");
-  static_assert(kCols % 4 == 0, "bad epilogue split");
 };
 
 // RSR_FP4_PROF builds (tools/ only, never the product library) accumulate
@@ -96,13 +97,13 @@ struct Tile {
 // Counters live in registers (prof[8] per thread) and are flushed once per
 // warp at the end, so the instrumentation barely perturbs the timing.
 #ifdef RSR_FP4_PROF
-__device__ unsigned long long g_prof[14];
-#define PROF_DECL unsigned long long prof[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
+__device__ unsigned long long g_prof[16];
+#define PROF_DECL unsigned long long prof[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
 #define PROF_T(x) const long long x = clock64()
 #define PROF_ADD(i, v) (prof[i] += (unsigned long long)(v))
 #define PROF_FLUSH                                                   \
   if ((threadIdx.x & 31) == 0)                                       \
-    for (int i_ = 0; i_ < 14; ++i_) atomicAdd(&g_prof[i_], prof[i_])
+    for (int i_ = 0; i_ < 16; ++i_) atomicAdd(&g_prof[i_], prof[i_])
 #else
 #define PROF_DECL
 #define PROF_T(x)
@@ -242,18 +243,17 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_b
 #endif
   tc_fence_before();
   __syncwarp();
-#if RSR_FP4_GROUP_RELEASE
-  // one arrival per CTA after a named barrier of its epilogue warps
-  named_bar_sync(2, 32 * kEpiWarps);
-  if (threadIdx.x == 128) mbar_arrive_leader(release_bar);
-#else
   if (lane == 0) mbar_arrive_leader(release_bar);
-#endif
   if (valid < c0 + kCols) {
 #pragma unroll
     for (int c = 0; c < kCols; ++c)
       if (c0 + c >= valid) v[c / 2] |= (c & 1) ? 0xFFFF0000u : 0x0000FFFFu;
   }
+#ifdef RSR_FP4_X_NOMIN
+  // timing experiment only (wrong results): no reduction
+  any = v[0] == 0u;
+  return;
+#endif
   // independent SIMD (16x2) min chains, then a tree
   constexpr int W = R >= 8 ? 4 : 2;
   uint32_t m[W];
@@ -273,6 +273,119 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_b
   }
 }
 
+// MMA issuer of the pair kernel (leader CTA, warp 1).  CQ > 0: compile-time K-steps.
+struct MmaRole {
+  uint32_t tm0, a_lo0, b_lo0;
+  uint32_t bar_b_full, bar_b_empty, bar_t_full, bar_t_empty, bar_a_full, bar_a_empty;
+  uint32_t a_buf_desc, b_stage_desc;
+  int cluster, n_clusters, n_groups, nt_l, nt_u, rot_l, rot_u;
+#ifdef RSR_FP4_PROF
+  long long k_entry;
+#endif
+};
+
+#ifdef RSR_FP4_PROF
+#define PROF_PARAM , unsigned long long* prof
+#define PROF_ARG , prof
+#else
+#define PROF_PARAM
+#define PROF_ARG
+#endif
+
+template <int TN, int CQ>
+__device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PROF_PARAM) {
+  constexpr uint32_t idesc = mxf4_idesc(2 * kRowsA, TN);
+  constexpr int kBufs = Tile<TN>::kBufs;
+  constexpr uint32_t kAstep = kChunkA >> 4, kBstep = Tile<TN>::kChunkB >> 4;
+  const uint32_t sfa = m.tm0 + kSfaCol, sfb = m.tm0 + kSfbCol;
+  // launch constants in registers (the asm statements' memory clobbers would
+  // otherwise reload them from the parameter bank on every tile)
+  const int cq = CQ > 0 ? CQ : p.cq;
+  const int stages = p.stages, a_bufs = p.a_bufs;
+  const bool resident = p.resident != 0;
+  const uint32_t a_half_desc = p.a_halves == 2 ? (uint32_t)cq * kAstep : 0u;
+  int stage = 0, gi = 0;
+  uint32_t phase = 0, buf = 0, tphase = 0;
+  int ab = 0;
+  uint32_t a_par = 0;
+#ifdef RSR_FP4_PROF
+  PROF_ADD(12, clock64() - m.k_entry);  // setup before the first group
+#endif
+  for (int g = m.cluster; g < m.n_groups; g += m.n_clusters, ++gi) {
+    PROF_ADD(11, 1);
+    const uint32_t a_up = m.a_lo0 + (uint32_t)ab * m.a_buf_desc;
+    const uint32_t a_dn = a_up + a_half_desc;
+    // resident reference tiles: every tile's stage completed during group 0
+    const bool wait_b = !resident || gi == 0;
+    PROF_T(l0);
+    for (int h = 0; h < 2; ++h) {
+      const int cnt = h == 0 ? m.nt_l : m.nt_u;
+      if (cnt == 0) continue;
+      PROF_T(w0);
+      mbar_wait(m.bar_a_full + 8 * (2 * ab + h), a_par);  // this side's sample half landed
+      PROF_T(w1);
+      PROF_ADD(9, w1 - w0);
+      tc_fence_after();
+      const uint32_t al = h == 0 ? a_dn : a_up;
+      const int base = h == 0 ? 0 : m.nt_l;
+      int jt = h == 0 ? m.rot_l : m.rot_u;
+      for (int t = 0; t < cnt; ++t) {
+        const int j = base + jt;
+        if (++jt == cnt) jt = 0;
+        // resident B: tile j sits in stage j, whose only phase (0) completes once
+        const int bs = resident ? j : stage;
+        const uint32_t d = m.tm0 + buf * TN;
+        const uint32_t bl = m.b_lo0 + (uint32_t)bs * m.b_stage_desc;
+        PROF_T(m0);
+#if RSR_FP4_SPIN
+        mbar_spin(m.bar_t_empty + 8 * buf, tphase ^ 1);
+#elif defined(RSR_FP4_X_NOWAIT)
+        // timing experiment only (wrong results): never wait for the epilogue
+#else
+        mbar_wait(m.bar_t_empty + 8 * buf, tphase ^ 1);
+#endif
+        PROF_T(m1);
+        if (wait_b) mbar_wait(m.bar_b_full + 8 * bs, resident ? 0u : phase);
+        PROF_T(m2);
+        PROF_ADD(1, m1 - m0);
+        PROF_ADD(0, m2 - m1);
+        PROF_ADD(7, 1);
+        tc_fence_after();
+        if (elect_one()) {
+          if constexpr (CQ > 0) {
+#pragma unroll
+            for (int ks = 0; ks < CQ; ++ks)
+              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
+          } else {
+            for (int ks = 0; ks < cq; ++ks)
+              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
+          }
+          umma_commit_pair(m.bar_t_full + 8 * buf);
+          if (!resident) umma_commit_pair(m.bar_b_empty + 8 * stage);
+        }
+        __syncwarp();
+        if (!resident && ++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++buf == kBufs) {
+          buf = 0;
+          tphase ^= 1;
+        }
+      }
+      // the side's sample half is released once its MMAs complete
+      if (elect_one()) umma_commit_pair(m.bar_a_empty + 8 * (2 * ab + h));
+      __syncwarp();
+    }
+    if (++ab == a_bufs) {
+      ab = 0;
+      a_par ^= 1;
+    }
+    PROF_T(l1);
+    PROF_ADD(2, l1 - l0);
+  }
+}
+
 template <int TN, bool FIRST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -282,10 +395,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   constexpr int kBufs = Tile<TN>::kBufs;
   constexpr int kHalfRows = Tile<TN>::kHalfRows;
   constexpr int kChunkB = Tile<TN>::kChunkB;
-  constexpr int kCols = Tile<TN>::kCols;
   extern __shared__ uint8_t smem_raw[];
 #ifdef RSR_FP4_PROF
   const long long k_entry = clock64();
+  unsigned long long g_entry;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
 #endif
   const uint32_t raw_addr = smem_addr(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
@@ -302,8 +416,10 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   uint64_t* t_full = a_full + 16;          // [kBufs <= 4]
   uint64_t* t_empty = a_full + 20;         // [kBufs <= 4]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 24);
-  uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 26);  // [kColGroups][128] hit bits
-  int64_t* xfirst = reinterpret_cast<int64_t*>(xchg + kColGroups * 128) - 256;  // [1..][2][128]
+  // group-end exchange of the epilogue sets, double-buffered by group parity:
+  // hit bits [2][kEpiSets][128] and first-match indices [2][kEpiSets][2][128]
+  uint32_t* xchg = reinterpret_cast<uint32_t*>(a_full + 26);
+  int64_t* xfirst = reinterpret_cast<int64_t*>(xchg + 2 * kEpiSets * 128);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -334,8 +450,8 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     for (int i = 0; i < kBufs; ++i) {
       mbar_init(smem_addr(&t_full[i]), 1);
-      // every epilogue warp of both CTAs (or one arrival per CTA)
-      mbar_init(smem_addr(&t_empty[i]), RSR_FP4_GROUP_RELEASE ? 2 : 2 * kEpiWarps);
+      // the 4 warps of the tile's epilogue set in both CTAs
+      mbar_init(smem_addr(&t_empty[i]), 2 * 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -459,95 +575,50 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer (leader only)
     if (leader) {
-      constexpr uint32_t idesc = mxf4_idesc(2 * kRowsA, kTileN);
-      const uint32_t tm0 = __shfl_sync(0xffffffffu, tmem_base, 0);
-      const uint32_t sfa = tm0 + kSfaCol, sfb = tm0 + kSfbCol;
-      const uint32_t a_lo0 = desc32_lo(smem_addr(sA)), b_lo0 = desc32_lo(smem_addr(sB));
-      const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
-      const uint32_t bar_t_full = smem_addr(t_full), bar_t_empty = smem_addr(t_empty);
-      constexpr uint32_t kAstep = kChunkA >> 4, kBstep = kChunkB >> 4;
-      const int cq = p.cq;
-      int stage = 0, gi = 0;
-      uint32_t phase = 0, buf = 0, tphase = 0;
+      MmaRole m;
+      m.tm0 = __shfl_sync(0xffffffffu, tmem_base, 0);
+      m.a_lo0 = desc32_lo(smem_addr(sA));
+      m.b_lo0 = desc32_lo(smem_addr(sB));
+      m.bar_b_full = smem_addr(b_full);
+      m.bar_b_empty = smem_addr(b_empty);
+      m.bar_t_full = smem_addr(t_full);
+      m.bar_t_empty = smem_addr(t_empty);
+      m.bar_a_full = smem_addr(a_full);
+      m.bar_a_empty = smem_addr(a_empty);
+      m.a_buf_desc = a_buf_bytes >> 4;
+      m.b_stage_desc = b_stage_bytes >> 4;
+      m.cluster = cluster;
+      m.n_clusters = n_clusters;
+      m.n_groups = n_groups;
+      m.nt_l = nt_l;
+      m.nt_u = nt_u;
+      m.rot_l = rot_l;
+      m.rot_u = rot_u;
 #ifdef RSR_FP4_PROF
-      PROF_ADD(12, clock64() - k_entry);  // setup before the first group
+      m.k_entry = k_entry;
 #endif
-      for (int g = cluster; g < n_groups; g += n_clusters, ++gi) {
-        const int ab = gi % p.a_bufs;
-        const uint32_t a_par = (uint32_t)(gi / p.a_bufs) & 1;
-        PROF_ADD(11, 1);
-        const uint32_t a_up = a_lo0 + (uint32_t)ab * (a_buf_bytes >> 4);
-        const uint32_t a_dn = a_up + (p.a_halves == 2 ? (uint32_t)cq * kAstep : 0u);
-        PROF_T(l0);
-        // lean per-tile bookkeeping: this warp's instruction count per tile is
-        // on the critical path once a tile is only a few hundred MMA cycles, so
-        // each side is its own loop with an incremental (rotated) tile index
-        for (int h = 0; h < 2; ++h) {
-          const int cnt = h == 0 ? nt_l : nt_u;
-          if (cnt == 0) continue;
-          PROF_T(w0);
-          mbar_wait(smem_addr(&a_full[2 * ab + h]), a_par);  // this side's sample half landed
-          PROF_T(w1);
-          PROF_ADD(9, w1 - w0);
-          tc_fence_after();
-          const uint32_t al = h == 0 ? a_dn : a_up;
-          const int base = h == 0 ? 0 : nt_l;
-          int jt = h == 0 ? rot_l : rot_u;
-          for (int t = 0; t < cnt; ++t) {
-            const int j = base + jt;
-            if (++jt == cnt) jt = 0;
-            // resident B: tile j sits in stage j, whose only phase (0) completes once
-            const int bs = p.resident ? j : stage;
-            const uint32_t bpar = p.resident ? 0u : phase;
-            const uint32_t d = tm0 + buf * kTileN;
-            const uint32_t bl = b_lo0 + (uint32_t)bs * (b_stage_bytes >> 4);
-            PROF_T(m0);
-#if RSR_FP4_SPIN
-            mbar_spin(bar_t_empty + 8 * buf, tphase ^ 1);
-#else
-            mbar_wait(bar_t_empty + 8 * buf, tphase ^ 1);
-#endif
-            PROF_T(m1);
-            mbar_wait(bar_b_full + 8 * bs, bpar);
-            PROF_T(m2);
-            PROF_ADD(1, m1 - m0);
-            PROF_ADD(0, m2 - m1);
-            PROF_ADD(7, 1);
-            tc_fence_after();
-            if (elect_one()) {
-              for (int ks = 0; ks < cq; ++ks)
-                umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
-              umma_commit_pair(bar_t_full + 8 * buf);
-              if (!p.resident) umma_commit_pair(bar_b_empty + 8 * stage);
-            }
-            __syncwarp();
-            if (++stage == p.stages) {
-              stage = 0;
-              phase ^= 1;
-            }
-            if (++buf == kBufs) {
-              buf = 0;
-              tphase ^= 1;
-            }
-          }
-          // the side's sample half is released once its MMAs complete
-          if (elect_one()) umma_commit_pair(smem_addr(&a_empty[2 * ab + h]));
-          __syncwarp();
-        }
-        PROF_T(l1);
-        PROF_ADD(2, l1 - l0);
+      // the K loop fully unrolled for the common row widths (N(M-1) <= 319: 5 K-steps;
+      // <= 639: 10): the MMA warp's instruction count per tile is on the critical path
+      // once a tile is only ~500 MMA cycles
+      switch (p.cq) {
+        case 5: mma_role<TN, 5>(m, p PROF_ARG); break;
+        case 10: mma_role<TN, 10>(m, p PROF_ARG); break;
+        default: mma_role<TN, 0>(m, p PROF_ARG); break;
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------ epilogue (both CTAs)
     const int quad = warp & 3;            // TMEM lane quarter (hardware: warp id % 4)
-    const int cg = (warp - 4) >> 2;       // column group
-    const int c0 = cg * kCols;
-    uint32_t buf = 0, tphase = 0;
-    for (int g = cluster; g < n_groups; g += n_clusters) {
+    const int set = (warp - 4) >> 2;      // epilogue set: tiles T with T % kEpiSets == set
+    const int r = quad * 32 + lane;       // sample row of this thread within the CTA
+    uint32_t T = 0;                       // the cluster's tile counter (every set counts all)
+    int gpar = 0;
+    for (int g = cluster; g < n_groups; g += n_clusters, gpar ^= 1) {
       uint32_t hit = 0;
       int64_t first[2] = {INT64_MAX, INT64_MAX};
-      for (int jj = 0; jj < p.nt_total; ++jj) {
+      for (int jj = 0; jj < p.nt_total; ++jj, ++T) {
+        if ((int)(T % kEpiSets) != set) continue;
+        const uint32_t buf = T % kBufs, tphase = (T / kBufs) & 1;
         const int j = tile_of(jj);
         const bool low = j < p.nt_lower;
         const int64_t t0 = (int64_t)(low ? j : j - p.nt_lower) * kTileN;
@@ -559,12 +630,12 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
 #endif
         PROF_T(e1);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN + c0;
+        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN;
         const int64_t valid = (low ? p.n_lower : p.n_upper) - t0;
         bool any;
         int zref = 0;
         long long t_loaded = 0;
-        epilogue_tile<TN, FIRST>(taddr, smem_addr(&t_empty[buf]), lane, c0, valid, any, zref,
+        epilogue_tile<TN, FIRST>(taddr, smem_addr(&t_empty[buf]), lane, 0, valid, any, zref,
                                  t_loaded);
         PROF_T(e2);
         PROF_ADD(0, t_loaded - e1);
@@ -575,35 +646,36 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             first[low ? 0 : 1] = min(first[low ? 0 : 1], ref);
           }
         }
-        if (++buf == kBufs) {
-          buf = 0;
-          tphase ^= 1;
-        }
         PROF_T(e3);
         PROF_ADD(3, e1 - e0);
         PROF_ADD(4, e2 - e1);
         PROF_ADD(5, e3 - e2);
       }
-      // the column groups of a row live in kColGroups warps: combine through shared memory
+      // the sets' partial results for the group's rows meet in shared memory; set 0
+      // writes the flags.  One barrier per group: the exchange buffers alternate by
+      // group parity, so a set may write group g+1's entries while set 0 still reads
+      // group g's.
       PROF_T(x0);
-      const int64_t row = (int64_t)g * 2 * kRowsA + rank * kRowsA + quad * 32 + lane;
-      const int r = quad * 32 + lane;
-      if constexpr (kColGroups > 1) named_bar_sync(1, 32 * kEpiWarps);
-      if (cg != 0) {
-        xchg[cg * 128 + r] = hit;
-        if (FIRST) {
-          xfirst[(cg * 2 + 0) * 128 + r] = first[0];
-          xfirst[(cg * 2 + 1) * 128 + r] = first[1];
-        }
-      }
-      if constexpr (kColGroups > 1) named_bar_sync(1, 32 * kEpiWarps);
-      if (cg == 0) {
-#pragma unroll
-        for (int q = 1; q < kColGroups; ++q) {
-          hit |= xchg[q * 128 + r];
+      const int64_t row = (int64_t)g * 2 * kRowsA + rank * kRowsA + r;
+      uint32_t* xh = xchg + gpar * kEpiSets * 128;
+      int64_t* xf = xfirst + gpar * kEpiSets * 256;
+      if constexpr (kEpiSets > 1) {
+        if (set != 0) {
+          xh[set * 128 + r] = hit;
           if (FIRST) {
-            first[0] = min(first[0], xfirst[(q * 2 + 0) * 128 + r]);
-            first[1] = min(first[1], xfirst[(q * 2 + 1) * 128 + r]);
+            xf[(set * 2 + 0) * 128 + r] = first[0];
+            xf[(set * 2 + 1) * 128 + r] = first[1];
+          }
+        }
+        named_bar_sync(1, 32 * kEpiWarps);
+      }
+      if (set == 0) {
+#pragma unroll
+        for (int q = 1; q < kEpiSets; ++q) {
+          hit |= xh[q * 128 + r];
+          if (FIRST) {
+            first[0] = min(first[0], xf[(q * 2 + 0) * 128 + r]);
+            first[1] = min(first[1], xf[(q * 2 + 1) * 128 + r]);
           }
         }
         if (row < S_run) {
@@ -632,7 +704,13 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   tc_fence_before();
   cluster_sync_all();
 #ifdef RSR_FP4_PROF
-  if (warp == 1 && leader) PROF_ADD(13, clock64() - k_loop_end);  // wait for the other roles
+  if (warp == 1 && leader) {
+    PROF_ADD(13, clock64() - k_loop_end);  // wait for the other roles
+    unsigned long long g_exit;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+    PROF_ADD(14, g_exit - g_entry);          // ns, entry .. teardown (clock = cycles / ns)
+    PROF_ADD(15, clock64() - k_entry);       // cycles over the same span
+  }
 #endif
   PROF_FLUSH;
   if (warp == 2) {
@@ -699,8 +777,7 @@ Fp4Layout fp4_layout(int tn, int64_t nt_l, int64_t nt_u, int cq, bool want_first
   const size_t max_smem = 227 * 1024;
   // align slack, barriers (<= 16 stages x 2 + 18), hit exchange, first-match exchange
   const size_t bars_bytes = (2 * 16 + 26) * 8;
-  const size_t fixed = 1024 + bars_bytes + kColGroups * 512 +
-                       (want_first ? (kColGroups - 1) * 2048 : 0);
+  const size_t fixed = 1024 + bars_bytes + 2 * kEpiSets * 512 + (want_first ? 2 * kEpiSets * 2048 : 0);
   // one-sided launches buffer only the sample half they read
   L.a_halves = (nt_l == 0 || nt_u == 0) ? 1 : 2;
   const size_t a_buf = (size_t)L.a_halves * cq * kChunkA;
@@ -1079,7 +1156,7 @@ __global__ void encode_refs_fp4_kernel(const uint8_t* __restrict__ states, int64
 extern "C" int rsr_fp4_prof(unsigned long long* host8, int reset) {
   RSR_CUDA(cudaMemcpyFromSymbol(host8, g_prof, sizeof(g_prof)));
   if (reset) {
-    unsigned long long z[14] = {0};
+    unsigned long long z[16] = {0};
     RSR_CUDA(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
   }
   return RSR_OK;

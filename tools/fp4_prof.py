@@ -17,7 +17,7 @@ from paper_2604_17066_b200.classify import classify_flags  # noqa: E402
 lib = _abi.lib()
 fn = lib.rsr_fp4_prof
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = (ctypes.c_ulonglong * 14)()
+buf = (ctypes.c_ulonglong * 16)()
 K = int(os.environ.get("K", "10000"))
 S = int(os.environ.get("S", str(1 << 20)))
 M = int(os.environ.get("M", "2"))
@@ -61,3 +61,6 @@ print(f"prod wait a_empty      {v[10] / (2 * groups):8.1f} cycles per group")
 ncl = max(v[12] and 74, 1)
 print(f"MMA warp setup {v[12] / ncl:.0f} cycles, teardown wait {v[13] / ncl:.0f} cycles per cluster; "
       f"groups per cluster {groups / ncl:.1f}, MMA-loop cycles per cluster {v[2] / ncl:.0f}")
+if v[14]:
+    print(f"SM clock over the MMA warp's run: {v[15] / v[14]:.3f} GHz "
+          f"({v[15] / ncl:.0f} cycles, {v[14] / ncl / 1e3:.1f} us per cluster)")

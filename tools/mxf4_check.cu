@@ -502,7 +502,9 @@ int main() {
   rate<256, true>(sms);
   pair_rate<240>(sms, 5);
   pair_rate<224>(sms, 5);
+  pair_rate<208>(sms, 5);
   pair_rate<192>(sms, 5);
+  pair_rate<176>(sms, 5);
   pair_rate<160>(sms, 5);
   pair_rate<128>(sms, 5);
   return bad ? 1 : 0;
