@@ -97,13 +97,14 @@ struct Tile {
 // Counters live in registers (prof[8] per thread) and are flushed once per
 // warp at the end, so the instrumentation barely perturbs the timing.
 #ifdef RSR_FP4_PROF
-__device__ unsigned long long g_prof[16];
-#define PROF_DECL unsigned long long prof[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
+constexpr int kProf = 24;
+__device__ unsigned long long g_prof[kProf];
+#define PROF_DECL unsigned long long prof[kProf] = {}
 #define PROF_T(x) const long long x = clock64()
 #define PROF_ADD(i, v) (prof[i] += (unsigned long long)(v))
 #define PROF_FLUSH                                                   \
   if ((threadIdx.x & 31) == 0)                                       \
-    for (int i_ = 0; i_ < 16; ++i_) atomicAdd(&g_prof[i_], prof[i_])
+    for (int i_ = 0; i_ < kProf; ++i_) atomicAdd(&g_prof[i_], prof[i_])
 #else
 #define PROF_DECL
 #define PROF_T(x)
@@ -232,7 +233,7 @@ __device__ __forceinline__ void ld_cols_packed(uint32_t taddr, uint32_t* v) {
 template <int TN, bool FIRST>
 __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_bar, int lane,
                                               int c0, int64_t valid, bool& any, int& zref,
-                                              long long& t_loaded) {
+                                              long long& t_loaded, long long* ts_release) {
   constexpr int kCols = Tile<TN>::kCols;
   constexpr int R = kCols / 2;
   uint32_t v[R];
@@ -243,6 +244,9 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_b
 #endif
   tc_fence_before();
   __syncwarp();
+#ifdef RSR_FP4_PROF
+  if (ts_release && lane == 0) *(volatile long long*)ts_release = clock64();
+#endif
   if (lane == 0) mbar_arrive_leader(release_bar);
   if (valid < c0 + kCols) {
 #pragma unroll
@@ -281,6 +285,7 @@ struct MmaRole {
   int cluster, n_clusters, n_groups, nt_l, nt_u, rot_l, rot_u;
 #ifdef RSR_FP4_PROF
   long long k_entry;
+  long long* ts;  // [0][buf] commit issued (MMA warp), [1][buf] CTA-0 release (epilogue)
 #endif
 };
 
@@ -345,6 +350,12 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
         mbar_wait(m.bar_t_empty + 8 * buf, tphase ^ 1);
 #endif
         PROF_T(m1);
+#ifdef RSR_FP4_PROF
+        if (gi > 0) {  // release (CTA 0 epilogue, just before its arrive) -> MMA warp sees it
+          PROF_ADD(17, m1 - *(volatile long long*)(m.ts + 4 + buf));
+          PROF_ADD(21, 1);
+        }
+#endif
         if (wait_b) mbar_wait(m.bar_b_full + 8 * bs, resident ? 0u : phase);
         PROF_T(m2);
         PROF_ADD(1, m1 - m0);
@@ -362,6 +373,11 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
           }
           umma_commit_pair(m.bar_t_full + 8 * buf);
           if (!resident) umma_commit_pair(m.bar_b_empty + 8 * stage);
+#ifdef RSR_FP4_PROF
+          const long long tc = clock64();
+          *(volatile long long*)(m.ts + buf) = tc;
+          PROF_ADD(18, tc - m2);  // issue of the tile's MMAs + commits
+#endif
         }
         __syncwarp();
         if (!resident && ++stage == stages) {
@@ -499,6 +515,9 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     return nt_l + (j >= nt_u ? j - nt_u : j);
   };
   PROF_DECL;
+#ifdef RSR_FP4_PROF
+  __shared__ long long prof_ts[8];
+#endif
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer (both CTAs)
@@ -596,6 +615,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       m.rot_u = rot_u;
 #ifdef RSR_FP4_PROF
       m.k_entry = k_entry;
+      m.ts = prof_ts;
 #endif
       // the K loop fully unrolled for the common row widths (N(M-1) <= 319: 5 K-steps;
       // <= 639: 10): the MMA warp's instruction count per tile is on the critical path
@@ -629,14 +649,25 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         mbar_wait(smem_addr(&t_full[buf]), tphase);
 #endif
         PROF_T(e1);
+#ifdef RSR_FP4_PROF
+        if (rank == 0 && quad == 0) {  // commit issued (MMA warp) -> this warp sees the tile
+          PROF_ADD(16, e1 - *(volatile long long*)(prof_ts + buf));
+          PROF_ADD(20, 1);
+        }
+#endif
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN;
         const int64_t valid = (low ? p.n_lower : p.n_upper) - t0;
         bool any;
         int zref = 0;
         long long t_loaded = 0;
+#ifdef RSR_FP4_PROF
+        long long* tsr = (rank == 0 && quad == 0) ? prof_ts + 4 + buf : nullptr;
+#else
+        long long* tsr = nullptr;
+#endif
         epilogue_tile<TN, FIRST>(taddr, smem_addr(&t_empty[buf]), lane, 0, valid, any, zref,
-                                 t_loaded);
+                                 t_loaded, tsr);
         PROF_T(e2);
         PROF_ADD(0, t_loaded - e1);
         if (any) {
@@ -1156,7 +1187,7 @@ __global__ void encode_refs_fp4_kernel(const uint8_t* __restrict__ states, int64
 extern "C" int rsr_fp4_prof(unsigned long long* host8, int reset) {
   RSR_CUDA(cudaMemcpyFromSymbol(host8, g_prof, sizeof(g_prof)));
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[kProf] = {0};
     RSR_CUDA(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
   }
   return RSR_OK;

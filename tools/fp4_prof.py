@@ -17,7 +17,7 @@ from paper_2604_17066_b200.classify import classify_flags  # noqa: E402
 lib = _abi.lib()
 fn = lib.rsr_fp4_prof
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 24)()
 K = int(os.environ.get("K", "10000"))
 S = int(os.environ.get("S", str(1 << 20)))
 M = int(os.environ.get("M", "2"))
@@ -64,3 +64,7 @@ print(f"MMA warp setup {v[12] / ncl:.0f} cycles, teardown wait {v[13] / ncl:.0f}
 if v[14]:
     print(f"SM clock over the MMA warp's run: {v[15] / v[14]:.3f} GHz "
           f"({v[15] / ncl:.0f} cycles, {v[14] / ncl / 1e3:.1f} us per cluster)")
+if v[20]:
+    print(f"chain: commit issued -> epilogue (CTA 0) sees t_full {v[16] / v[20]:.0f} cycles; "
+          f"CTA-0 release -> MMA warp sees t_empty {v[17] / max(v[21], 1):.0f}; "
+          f"MMA issue of a tile {v[18] / max(tiles, 1):.0f}")
