@@ -175,8 +175,12 @@ int rsr_classify_tc_explain(const int8_t* A, int64_t S, const int8_t* B_lower,
  * a side; pad rows written by rsr_encode_refs_fp4 are harmless).  D = A_up.B_up
  * (upper) or A_lo.B_lo (lower) counts violated thermometer columns exactly
  * (fp32 accumulation of 0/1 products); D == 0 <=> dominance.  flags and
- * accumulate as rsr_classify_tc.  row_bytes <= RSR_FP4_MAX_ROW_BYTES. */
-#define RSR_FP4_MAX_ROW_BYTES 416
+ * accumulate as rsr_classify_tc.  row_bytes <= RSR_FP4_MAX_ROW_BYTES (N(M-1) <= 1535;
+ * rows wider than 416 bytes run lower and upper references as separate one-sided
+ * launches).  The Stage-1 loop's device reference sets (rsr_refset_insert) take
+ * rows up to RSR_REFSET_MAX_ROW_BYTES. */
+#define RSR_FP4_MAX_ROW_BYTES 768
+#define RSR_REFSET_MAX_ROW_BYTES 416
 #define RSR_FP4_TILE_ROWS 240
 int rsr_fp4_row_bytes(int n_components, int n_states);
 int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int n_components,

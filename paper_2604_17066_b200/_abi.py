@@ -18,7 +18,7 @@ __all__ = ["lib", "call", "stream_ptr", "ptr", "PhiDesc", "RefsetDev", "LIB_PATH
            "SIDE_LOWER", "SIDE_UPPER", "HIT_LOWER", "HIT_UPPER", "LABEL_LOWER", "LABEL_UPPER",
            "LABEL_UNCLASSIFIED", "PHI_ST", "PHI_WIDEST", "PHI_GLOBAL", "PHI_KOFN", "PHI_CONES",
            "thermo_kpad", "thermo_words", "fp4_row_bytes", "FP4_TILE_ROWS",
-           "FP4_MAX_ROW_BYTES", "EXPORTED"]
+           "FP4_MAX_ROW_BYTES", "REFSET_MAX_ROW_BYTES", "EXPORTED"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librsr_b200.so")
 # timing experiments (tools/fp4_prof.py) may load an instrumented build instead
@@ -204,7 +204,8 @@ def thermo_kpad(n: int, m: int) -> int:
 
 
 FP4_TILE_ROWS = 240
-FP4_MAX_ROW_BYTES = 416
+FP4_MAX_ROW_BYTES = 768      # classifier (include/rsr_b200.h)
+REFSET_MAX_ROW_BYTES = 416   # Stage-1 loop's device reference sets
 
 
 def fp4_row_bytes(n: int, m: int) -> int:

@@ -861,35 +861,45 @@ int launch_fp4(const Fp4Call& c) {
   p.flags = c.flags;
   p.first_lower = c.first[0];
   p.first_upper = c.first[1];
-  const Fp4Layout L = fp4_layout(TN, nt_l, nt_u, cq, want_first);
-  RSR_REQUIRE(L.ring >= 2, "rsr_classify_fp4: row_bytes too large for shared memory");
-  p.a_halves = L.a_halves;
-  p.a_bufs = L.a_bufs;
-  p.resident = L.resident;
-  p.stages = L.stages;
-  const size_t smem = L.smem;
   p.n_groups = (int)rsr::ceil_div(c.S, (int64_t)2 * kRowsA);
   auto kern = want_first ? classify_fp4_pair_kernel<TN, true> : classify_fp4_pair_kernel<TN, false>;
-  rc = rsr::ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
-  if (rc) return rc;
   int clusters = c.sm_count / 2;
   if (p.n_groups < clusters) clusters = p.n_groups;
+  // Wide rows (N(M-1) >= 832, e.g. N = 295 at M >= 4) leave no room for a sample
+  // buffer holding both halves next to a reference ring: such calls run the lower
+  // and the upper tiles as separate one-sided launches (one sample half each,
+  // flags and first matches accumulated), so they stay on the tensor cores.
+  const bool split_sides =
+      nt_l > 0 && nt_u > 0 && fp4_layout(TN, nt_l, nt_u, cq, want_first).ring < 2;
 
   // Reference chunks: a launch's B slice must stay L2-resident while every
   // group streams it (~123K refs x row_bytes per launch: 20 MB at 160 B).
   const char* ct = getenv("RSR_TC_CHUNK_TILES");
   const int64_t chunk = ct ? atoll(ct) : 122880 / TN;
   const int64_t total = nt_l + nt_u;
-  for (int64_t c0 = 0; c0 < total; c0 += chunk) {
-    const int64_t c1 = c0 + chunk < total ? c0 + chunk : total;
+  bool first_launch = true;
+  for (int64_t c0 = 0; c0 < total;) {
+    // a chunk never straddles the side boundary when the sides are split
+    const int64_t lim = (split_sides && c0 < nt_l) ? nt_l : total;
+    const int64_t c1 = c0 + chunk < lim ? c0 + chunk : lim;
     const int64_t lo[2] = {c0 < nt_l ? c0 : nt_l, (c0 > nt_l ? c0 : nt_l) - nt_l};
     const int64_t hi[2] = {c1 < nt_l ? c1 : nt_l, (c1 > nt_l ? c1 : nt_l) - nt_l};
     Fp4Params q = p;
     q.nt_lower = (int)(hi[0] - lo[0]);
     q.nt_total = (int)((hi[0] - lo[0]) + (hi[1] - lo[1]));
-    q.accumulate = c0 == 0 ? c.accumulate : 1;
+    q.accumulate = first_launch ? c.accumulate : 1;
     q.first_base_lower = lo[0] * TN;
     q.first_base_upper = lo[1] * TN;
+    // shared-memory plan of this launch's tiles (one-sided launches buffer one
+    // sample half; small launches keep their tiles resident)
+    const Fp4Layout L = fp4_layout(TN, q.nt_lower, q.nt_total - q.nt_lower, cq, want_first);
+    RSR_REQUIRE(L.ring >= 2, "rsr_classify_fp4: row_bytes too large for shared memory");
+    q.a_halves = L.a_halves;
+    q.a_bufs = L.a_bufs;
+    q.resident = L.resident;
+    q.stages = L.stages;
+    int rc2 = rsr::ensure_dynamic_smem(reinterpret_cast<const void*>(kern), L.smem);
+    if (rc2) return rc2;
     // per side: rows the launch's tiles span; when the caller's readable rows
     // cover them (never-hit pad rows past n) no column is masked, otherwise
     // the TMA box reads past n as zeros and the epilogue masks columns >= n
@@ -914,9 +924,11 @@ int launch_fp4(const Fp4Call& c) {
     rc = make_map3(&cu, base[1] ? base[1] : base[0], base[1] ? rows[1] : rows[0], c.row_bytes, cq,
                    TN / 2);
     if (rc) return rc;
-    kern<<<2 * clusters, kThreads, smem, c.st>>>(ma, cl, cu, q);
+    kern<<<2 * clusters, kThreads, L.smem, c.st>>>(ma, cl, cu, q);
     rc = rsr::check_launch("classify_fp4_pair_kernel");
     if (rc) return rc;
+    first_launch = false;
+    c0 = c1;
   }
   return RSR_OK;
 }
@@ -927,6 +939,14 @@ int launch_fp4(const Fp4Call& c) {
 // it), so narrower tiles only win when they save whole tiles, e.g. 5 x 224
 // instead of 5 x 240 is a wash but 1000 refs in 5 x 208 beat 5 x 240 rows of
 // which 200 are padding.  RSR_FP4_TILE_N forces one width.
+// Whether a call's tiles at width tn fit shared memory: one two-sided launch, or
+// (wide rows) the one-sided launches of each side (see launch_fp4).
+bool fp4_feasible(int tn, int64_t nt_l, int64_t nt_u, int cq, bool want_first) {
+  if (fp4_layout(tn, nt_l, nt_u, cq, want_first).ring >= 2) return true;
+  return (nt_l == 0 || fp4_layout(tn, nt_l, 0, cq, want_first).ring >= 2) &&
+         (nt_u == 0 || fp4_layout(tn, 0, nt_u, cq, want_first).ring >= 2);
+}
+
 int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
   const char* env = getenv("RSR_FP4_TILE_N");
   const int forced = env ? atoi(env) : 0;
@@ -940,11 +960,12 @@ int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
   constexpr int64_t kStreamGroupCost = 2500;
   for (int tn : kCand)
     if (tn == forced) return tn;
-  int best = 240;
+  int best = 160;  // narrowest: the last resort for the widest rows
   int64_t best_cost = INT64_MAX;
   for (int i = 0; i < 6; ++i) {
     const int tn = kCand[i];
     const int64_t nt_l = rsr::ceil_div(n_lower, tn), nt_u = rsr::ceil_div(n_upper, tn);
+    if (!fp4_feasible(tn, nt_l, nt_u, cq, want_first)) continue;
     const bool resident = fp4_layout(tn, nt_l, nt_u, cq, want_first).resident;
     int64_t cost = (nt_l + nt_u) * (resident ? kCostResident[i] : kCost[i]);
     if (!resident) cost += kStreamGroupCost;

@@ -26,7 +26,7 @@ namespace {
 
 constexpr int kScanThreads = 128;
 constexpr int kScanStage = 32;      // candidates staged in shared memory per pass
-constexpr int kMaxWords = RSR_FP4_MAX_ROW_BYTES / 16;
+constexpr int kMaxWords = RSR_REFSET_MAX_ROW_BYTES / 16;
 
 __device__ __forceinline__ uint32_t nib(int e) { return e ? 0x2u : 0u; }
 
@@ -397,8 +397,8 @@ extern "C" int rsr_refset_insert(const uint8_t* cands, const uint8_t* cand_side,
   RSR_REQUIRE(B <= 65535, "rsr_refset_insert: at most 65535 candidates per call");
   RSR_REQUIRE(lower && upper && report, "rsr_refset_insert: null set/report");
   const int rb = rsr_fp4_row_bytes(N, M);
-  RSR_REQUIRE(rb <= RSR_FP4_MAX_ROW_BYTES, "rsr_refset_insert: rows wider than %d bytes",
-              RSR_FP4_MAX_ROW_BYTES);
+  RSR_REQUIRE(rb <= RSR_REFSET_MAX_ROW_BYTES, "rsr_refset_insert: rows wider than %d bytes",
+              RSR_REFSET_MAX_ROW_BYTES);
   for (const rsr_refset_dev* s : {lower, upper})
     RSR_REQUIRE(s->rows && s->fp4 && s->alive && s->ctr && s->cap >= 0 && s->n_bound >= 0,
                 "rsr_refset_insert: incomplete set descriptor");

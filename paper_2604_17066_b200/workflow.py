@@ -221,7 +221,7 @@ def stage1_find_references(model: SystemModel, dist: ComponentDistribution, conf
     loop_stream = _high_priority_stream()
     loop_stream.wait_stream(caller)
     use_async = (os.environ.get("RSR_SYNC_LOOP") != "1"
-                 and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.FP4_MAX_ROW_BYTES
+                 and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.REFSET_MAX_ROW_BYTES
                  and fp4_exact()
                  and dist.n_states == model.n_component_states
                  and config.parallel_searches <= 4096)
@@ -859,7 +859,7 @@ def multistate_pmf(model: SystemModel, dist: ComponentDistribution, config: RunC
     cache = None
     if (m_s > 2 and torch.cuda.is_available() and os.environ.get("RSR_BATCH_CACHE", "1") != "0"
             and dist.n_states == model.n_component_states
-            and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.FP4_MAX_ROW_BYTES):
+            and _abi.fp4_row_bytes(dist.n_components, dist.n_states) <= _abi.REFSET_MAX_ROW_BYTES):
         comm_ = comm or Comm.single()
         _, count = shard_range(config.n_samples, comm_.world, comm_.rank)
         cache = _BatchCache(count, _abi.fp4_row_bytes(dist.n_components, dist.n_states))

@@ -177,9 +177,10 @@ def test_explain_first_match_tensor_core_chunked(chunk_tiles, method, monkeypatc
     assert np.array_equal(r.first_match_upper, want["first_upper"])
 
 
-@pytest.mark.parametrize("n,m", [(300, 4), (400, 4), (700, 3)])
+@pytest.mark.parametrize("n,m", [(300, 4), (400, 4), (700, 3), (800, 3)])
 def test_classify_wide_rows_vs_oracle(n, m):
-    # N(M-1) beyond the tensor-core row limit (and beyond 32 bit-words): bit-packed path
+    # wide rows: N(M-1) = 900 / 1200 / 1400 run the FP4 tensor-core kernel as one-sided
+    # launches per side; 1600 is past its limit (bit-packed CUDA-core path)
     rng = np.random.default_rng(n * m)
     h = 700
     samples = rng.integers(0, m, size=(h, n))

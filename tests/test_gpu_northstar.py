@@ -236,3 +236,42 @@ def test_fp4_selfcheck_failure_routes_to_int8_tensor_cores(fp4_selfcheck_reset, 
     assert s1.lower.members == o1["lower"] and s1.upper.members == o1["upper"]
     assert "rsr_classify_tc" in calls
     assert not any(c.startswith("rsr_classify_fp4") for c in calls)
+
+
+# ---------------------------------- wide multi-state rows on the tensor cores
+
+@pytest.mark.parametrize("m", [4, 5])
+def test_wide_multistate_rows_stay_on_tensor_cores(m, monkeypatch):
+    """N = 295 at M = 4 / 5 (N(M-1) = 885 / 1180 > 831): the FP4 tensor-core kernel runs
+    the lower and upper references as separate one-sided launches
+    with labels and first matches equal to the oracle (classify.py:99-148)."""
+    from paper_2604_17066_b200 import _abi
+    n, h, k = 295, 3000, 700
+    rng = np.random.default_rng(m)
+    probs = rng.dirichlet([1.0] + [3.0] * (m - 2) + [16.0], size=n)
+    samples = oracle.sample_states(probs, h, 5, 0, 0)
+    lower = np.clip(samples[rng.integers(0, h, k)] + rng.integers(0, 2, (k, n)), 0, m - 1)
+    upper = np.clip(samples[rng.integers(0, h, k)] - rng.integers(0, 2, (k, n)), 0, m - 1)
+    want = oracle.classify_labels(samples, lower, upper, m, want_first=True, n_workers=CORES)
+    assert len(set(want["labels"].tolist())) == 3
+    calls = []
+    real = _abi.call
+
+    def spy(name, *a):
+        calls.append(name)
+        return real(name, *a)
+    monkeypatch.setattr(_abi, "call", spy)
+    lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower, trusted=True)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper, trusted=True)
+    r = P.classify(P.SampleBatch(samples, 0, 0), lo, up, n_states=m, explain=True)
+    assert np.array_equal(r.labels_device.cpu().numpy(), want["labels"])
+    assert np.array_equal(r.first_match_lower, want["first_lower"])
+    assert np.array_equal(r.first_match_upper, want["first_upper"])
+    assert "rsr_classify_fp4_ex" in calls and "rsr_classify_bits" not in calls
+    # the device sampler's fused FP4 operand at this width, full classify path
+    d = P.ComponentDistribution(probs)
+    b = P.sample_batch(d, h, seed=9)
+    r2 = P.classify(b, lo, up, n_states=m)
+    want2 = oracle.classify_labels(oracle.sample_states(probs, h, 9, 0, 0), lower, upper, m,
+                                   n_workers=CORES)
+    assert np.array_equal(r2.labels_device.cpu().numpy(), want2["labels"])
