@@ -960,6 +960,12 @@ int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
   constexpr int64_t kStreamGroupCost = 2500;
   for (int tn : kCand)
     if (tn == forced) return tn;
+  // wide rows (>= 12 K-steps, e.g. N = 295 at M >= 4): N = 160 tiles with three
+  // accumulator buffers measured 15 % faster than any wider tile (M = 4: 0.895 of
+  // peak vs 0.736-0.776; profiles/r2_wide_rows_m2_m5.txt)
+  if (cq >= 12 && fp4_feasible(160, rsr::ceil_div(n_lower, 160), rsr::ceil_div(n_upper, 160), cq,
+                               want_first))
+    return 160;
   int best = 160;  // narrowest: the last resort for the widest rows
   int64_t best_cost = INT64_MAX;
   for (int i = 0; i < 6; ++i) {

@@ -254,6 +254,8 @@ def test_wide_multistate_rows_stay_on_tensor_cores(m, monkeypatch):
     upper = np.clip(samples[rng.integers(0, h, k)] - rng.integers(0, 2, (k, n)), 0, m - 1)
     want = oracle.classify_labels(samples, lower, upper, m, want_first=True, n_workers=CORES)
     assert len(set(want["labels"].tolist())) == 3
+    from paper_2604_17066_b200.classify import fp4_exact
+    assert fp4_exact()  # the one-time self-check runs the bit-packed kernel: before the spy
     calls = []
     real = _abi.call
 
