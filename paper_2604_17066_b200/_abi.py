@@ -215,3 +215,17 @@ def fp4_row_bytes(n: int, m: int) -> int:
 
 def thermo_words(n: int, m: int) -> int:
     return (n * (m - 1) + 31) // 32
+
+
+_SM_COUNT: dict = {}
+
+
+def device_sm_count() -> int:
+    """SM count of the current device (rsr_device_info), cached per device."""
+    idx = require_device().index
+    n = _SM_COUNT.get(idx)
+    if n is None:
+        sm, ma, mi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        call("rsr_device_info", ctypes.byref(sm), ctypes.byref(ma), ctypes.byref(mi))
+        n = _SM_COUNT[idx] = int(sm.value)
+    return n

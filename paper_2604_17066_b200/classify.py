@@ -334,7 +334,7 @@ def classify(batch: SampleBatch, lower_set: ReferenceSet | None, upper_set: Refe
 
 
 def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSet | None,
-                  n_states: int, *, chunk_rows: int = 1 << 16,
+                  n_states: int, *, chunk_rows: int | None = None,
                   labels_out: torch.Tensor | None = None,
                   method: str = "tc") -> tuple[torch.Tensor, tuple[int, int, int]]:
     """Classify host-resident uint8 samples, streaming them through the GPU.
@@ -357,7 +357,7 @@ def classify_host(states, lower_set: ReferenceSet | None, upper_set: ReferenceSe
 
 def classify_host_encoded(packed, n_components: int, lower_set: ReferenceSet | None,
                           upper_set: ReferenceSet | None, n_states: int, *,
-                          chunk_rows: int = 1 << 17,
+                          chunk_rows: int | None = None,
                           labels_out: torch.Tensor | None = None
                           ) -> tuple[torch.Tensor, tuple[int, int, int]]:
     """Classify host samples given in the reference's own classification input:
@@ -423,6 +423,12 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
         bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
         bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
     comp = torch.cuda.current_stream()
+    if chunk_rows is None:
+        # whole waves of the persistent classifier: 16 sample groups (256 rows) per CTA
+        # pair.  A chunk of 2^16 rows is 256 groups = 3.46 waves of 74 pairs, so a
+        # quarter of every chunk's last wave idled (cfg4 K = 5x10^5 e2e: 183 ms for a
+        # 151 ms kernel); larger chunks also amortise the reference-chunk launches
+        chunk_rows = 16 * 256 * max(1, _abi.device_sm_count() // 2)
     chunk = max(1, min(chunk_rows, S))
     copy, bufs, opnd, ready, free = _stream_buffers(dev, chunk, width_in, opnd_shape, opnd_dtype)
     flags = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
