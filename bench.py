@@ -351,14 +351,18 @@ def secondary_kernels():
         rb = _abi.fp4_row_bytes(N_COMP, m)
         st = torch.empty((S, N_COMP), dtype=torch.uint8, device="cuda")
         a4 = torch.empty((S, 2 * rb), dtype=torch.uint8, device="cuda")
-        pr = _abi.ptr(d.device_probs())
-        ms = timed(lambda: _abi.call("rsr_sample_fp4", pr, N_COMP, m, 0, 1, 0, S, _abi.ptr(st),
-                                     _abi.ptr(a4), rb, _abi.stream_ptr()))
-        wbytes = S * (N_COMP + 2 * rb)
-        out[f"sample_rows_kernel_M{m}"] = {
-            "shape": f"2^20 x {N_COMP} draws", "ms": ms, "draws_per_s": S * N_COMP / (ms * 1e-3),
-            "hbm_write_gbs": wbytes / (ms * 1e-3) / 1e9, "hbm_peak_gbs": hbm,
-            "bound": "integer multiply (FMA pipe), not HBM"}
+        pr = d.device_probs()
+        for rng, code in (("shared", _abi.RNG_SHARED), ("device", _abi.RNG_DEVICE)):
+            ms = timed(lambda: _abi.call("rsr_sample_fp4_ex", _abi.ptr(pr), N_COMP, m, 0, 1, 0, S,
+                                         _abi.ptr(st), _abi.ptr(a4), rb, code, _abi.stream_ptr()))
+            wbytes = S * (N_COMP + 2 * rb)
+            out[f"sample_rows_kernel_M{m}_{rng}"] = {
+                "shape": f"2^20 x {N_COMP} draws", "ms": ms,
+                "draws_per_s": S * N_COMP / (ms * 1e-3),
+                "hbm_write_gbs": wbytes / (ms * 1e-3) / 1e9, "hbm_peak_gbs": hbm,
+                "stream": ("Philox4x64-10 (reference stream, bit-exact)" if rng == "shared" else
+                           "Philox4x32-10 (independent device stream)"),
+                "bound": "integer multiply (FMA pipe), not HBM"}
         del st, a4
     g = W.cfg3(0)
     graph = P.Graph(g["n_nodes"], tuple(g["edges"]))

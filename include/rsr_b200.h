@@ -12,7 +12,8 @@
  * Conventions
  *   - every function returns int status: RSR_OK (0), RSR_EINVAL (bad argument,
  *     mapped to ValueError), RSR_ECUDA (CUDA error, RuntimeError),
- *     RSR_EUNSUPPORTED (shape outside what the kernels handle, ValueError);
+ *     RSR_EUNSUPPORTED (shape outside what the kernels handle, ValueError),
+ *     RSR_ENCCL (NCCL error in the rsr_comm_* / exchange calls, RuntimeError);
  *     rsr_last_error() returns a thread-local message for the last failure;
  *   - all array arguments are caller-owned DEVICE pointers (the library never
  *     allocates or frees them) unless the name ends in _host;
@@ -44,6 +45,7 @@ extern "C" {
 #define RSR_EINVAL 1
 #define RSR_ECUDA 2
 #define RSR_EUNSUPPORTED 3
+#define RSR_ENCCL 4
 
 #define RSR_SIDE_LOWER 0
 #define RSR_SIDE_UPPER 1
@@ -333,6 +335,26 @@ int rsr_gather_picks_fp4(const uint8_t* fp4, int row_bytes, int n_components, in
  * (workflow.py:172-176 with the positions drawn on the host). */
 int rsr_gather_picks(const uint8_t* states, int n_components, const int64_t* idx,
                      const int64_t* pos, int64_t count, uint8_t* out, void* stream);
+
+/* ---- (e) multi-GPU exchange (the reference has no
+ * communication -- its only parallel seam is the chunk thread pool of
+ * classify.py:140-142).  One process per GPU; NCCL over NVLink, bound at run time
+ * (libnccl.so.2).  The Python package does the same exchanges with
+ * torch.distributed (dist.py).  comm: opaque communicator handle. */
+#define RSR_COMM_ID_BYTES 128
+/* 128-byte unique id (rank 0 creates it and broadcasts it out of band). */
+int rsr_comm_unique_id(uint8_t* out_id_host);
+int rsr_comm_init(const uint8_t* unique_id_host, int world, int rank, void** out_comm_host);
+int rsr_comm_destroy(void* comm);
+/* In-place sum of per-rank int64 class counts (labels / Phi calls of a sample shard). */
+int rsr_allreduce_counts(void* comm, int64_t* counts, int n, void* stream);
+/* Concatenation in rank order of every rank's bytes_per_rank bytes (new reference
+ * rows, picked sample rows) into recv [world * bytes_per_rank]. */
+int rsr_allgather_refs(void* comm, const uint8_t* send, int64_t bytes_per_rank, uint8_t* recv,
+                       void* stream);
+/* In-place OR of classifier hit flags [S] across reference shards (bit 0 lower,
+ * bit 1 upper): two 0/1 planes in scratch [2*S], NCCL MAX, merged back. */
+int rsr_or_reduce_flags(void* comm, uint8_t* flags, int64_t S, uint8_t* scratch, void* stream);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librsr_b200
 # timing experiments (tools/fp4_prof.py) may load an instrumented build instead
 LIB_PATH = os.environ.get("RSR_LIB_OVERRIDE", LIB_PATH)
 
-RSR_OK, RSR_EINVAL, RSR_ECUDA, RSR_EUNSUPPORTED = 0, 1, 2, 3
+RSR_OK, RSR_EINVAL, RSR_ECUDA, RSR_EUNSUPPORTED, RSR_ENCCL = 0, 1, 2, 3, 4
 SIDE_LOWER, SIDE_UPPER = 0, 1
 HIT_LOWER, HIT_UPPER = 1, 2
 RNG_SHARED, RNG_DEVICE = 0, 1  # reference Philox4x64-10 stream / independent Philox4x32-10
@@ -83,6 +83,12 @@ EXPORTED = {
     "rsr_sample_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I, _P]),
     "rsr_sample_fp4_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I, _P]),
     "rsr_device_raw": (_I, [_U64, _U64, _I64, _I64, _P, _P]),
+    "rsr_comm_unique_id": (_I, [_P]),
+    "rsr_comm_init": (_I, [_P, _I, _I, _P]),
+    "rsr_comm_destroy": (_I, [_P]),
+    "rsr_allreduce_counts": (_I, [_P, _P, _I, _P]),
+    "rsr_allgather_refs": (_I, [_P, _P, _I64, _P, _P]),
+    "rsr_or_reduce_flags": (_I, [_P, _P, _I64, _P, _P]),
     "rsr_encode_samples": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "rsr_encode_refs": (_I, [_P, _I64, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_encode_rows": (_I, [_P, _I64, _I, _I, _I, _P, _P]),

@@ -93,3 +93,34 @@ def test_two_rank_workflow_matches_single_device(case, loop, backend):
             assert got["p_lower"] == st["stage2"]["p_lower"]
             assert got["unclassified_resolved"] == st["stage2"]["unclassified_resolved"]
             assert got["phi_total"] == st["stage2"]["phi_total"]
+
+
+def test_c_abi_comm_single_rank():
+    """The C-ABI exchange entry points (include/rsr_b200.h) on a
+    one-rank NCCL communicator: counts sum, rows gather and hit-flag OR are the
+    identity; bad ranks raise ValueError."""
+    import ctypes
+
+    import torch
+
+    from paper_2604_17066_b200 import _abi
+    torch.cuda.set_device(0)
+    uid = (ctypes.c_uint8 * 128)()
+    _abi.call("rsr_comm_unique_id", uid)
+    comm = ctypes.c_void_p()
+    with pytest.raises(ValueError):
+        _abi.call("rsr_comm_init", uid, 2, 2, ctypes.byref(comm))
+    _abi.call("rsr_comm_init", uid, 1, 0, ctypes.byref(comm))
+    st = _abi.stream_ptr()
+    counts = torch.tensor([3, 5, 7], dtype=torch.int64, device="cuda")
+    _abi.call("rsr_allreduce_counts", comm, _abi.ptr(counts), 3, st)
+    rows = torch.randint(0, 3, (64, 295), dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(rows)
+    _abi.call("rsr_allgather_refs", comm, _abi.ptr(rows), rows.numel(), _abi.ptr(out), st)
+    flags = torch.randint(0, 4, (10_001,), dtype=torch.uint8, device="cuda")
+    want = flags.clone()
+    scratch = torch.empty(2 * flags.numel(), dtype=torch.uint8, device="cuda")
+    _abi.call("rsr_or_reduce_flags", comm, _abi.ptr(flags), flags.numel(), _abi.ptr(scratch), st)
+    torch.cuda.synchronize()
+    assert counts.tolist() == [3, 5, 7] and torch.equal(out, rows) and torch.equal(flags, want)
+    _abi.call("rsr_comm_destroy", comm)
