@@ -407,7 +407,7 @@ def run_reference(args):
     p1, lower, upper, S, desc = workload(args.config, args.k, args.samples)
     cpu = CpuClassify(p1, lower, upper)
     # each step one bounded slice; the whole --steps/--warmup run within a few minutes
-    per_step = cpu_slice_seconds(args, min(8.0, max(1.0, 150.0 / (args.steps + args.warmup))))
+    per_step = cpu_slice_seconds(args, min(6.0, max(1.0, 150.0 / (args.steps + args.warmup))))
     rows = cpu.calibrate(per_step)
     for w in range(args.warmup):
         cpu.run(rows, start=(1 << 41) + w * rows)
