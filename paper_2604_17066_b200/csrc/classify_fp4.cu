@@ -33,6 +33,8 @@
 //     first matching reference index (explain/strict).
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "fp4_encode.cuh"
 #include "tc_common.cuh"
 
@@ -130,6 +132,8 @@ struct Fp4Params {
   int64_t n_lower;  // reference rows of this launch per side (columns beyond are masked)
   int64_t n_upper;
   int resident;     // every reference tile has its own stage: loaded once, reused by all groups
+  int n_res;        // tiles j < n_res are resident in stage j (loaded once); the others stream
+                    // through stages n_res .. stages-1 (n_res = nt_total when resident)
   const int64_t* S_dev;  // optional device sample count (<= S): rows [S_dev, S) are skipped
 };
 
@@ -307,9 +311,9 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
   // otherwise reload them from the parameter bank on every tile)
   const int cq = CQ > 0 ? CQ : p.cq;
   const int stages = p.stages, a_bufs = p.a_bufs;
-  const bool resident = p.resident != 0;
+  const int n_res = p.n_res;  // tiles j < n_res sit in stage j for the whole launch
   const uint32_t a_half_desc = p.a_halves == 2 ? (uint32_t)cq * kAstep : 0u;
-  int stage = 0, gi = 0;
+  int stage = n_res, gi = 0;
   uint32_t phase = 0, buf = 0, tphase = 0;
   int ab = 0;
   uint32_t a_par = 0;
@@ -320,8 +324,8 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
     PROF_ADD(11, 1);
     const uint32_t a_up = m.a_lo0 + (uint32_t)ab * m.a_buf_desc;
     const uint32_t a_dn = a_up + a_half_desc;
-    // resident reference tiles: every tile's stage completed during group 0
-    const bool wait_b = !resident || gi == 0;
+    // resident reference tiles: every such stage completed during group 0
+    const bool first_group = gi == 0;
     PROF_T(l0);
     for (int h = 0; h < 2; ++h) {
       const int cnt = h == 0 ? m.nt_l : m.nt_u;
@@ -338,7 +342,8 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
         const int j = base + jt;
         if (++jt == cnt) jt = 0;
         // resident B: tile j sits in stage j, whose only phase (0) completes once
-        const int bs = resident ? j : stage;
+        const bool res_tile = j < n_res;
+        const int bs = res_tile ? j : stage;
         const uint32_t d = m.tm0 + buf * TN;
         const uint32_t bl = m.b_lo0 + (uint32_t)bs * m.b_stage_desc;
         PROF_T(m0);
@@ -356,7 +361,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
           PROF_ADD(21, 1);
         }
 #endif
-        if (wait_b) mbar_wait(m.bar_b_full + 8 * bs, resident ? 0u : phase);
+        if (!res_tile || first_group) mbar_wait(m.bar_b_full + 8 * bs, res_tile ? 0u : phase);
         PROF_T(m2);
         PROF_ADD(1, m1 - m0);
         PROF_ADD(0, m2 - m1);
@@ -372,7 +377,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
               umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
           }
           umma_commit_pair(m.bar_t_full + 8 * buf);
-          if (!resident) umma_commit_pair(m.bar_b_empty + 8 * stage);
+          if (!res_tile) umma_commit_pair(m.bar_b_empty + 8 * stage);
 #ifdef RSR_FP4_PROF
           const long long tc = clock64();
           *(volatile long long*)(m.ts + buf) = tc;
@@ -380,8 +385,8 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
 #endif
         }
         __syncwarp();
-        if (!resident && ++stage == stages) {
-          stage = 0;
+        if (!res_tile && ++stage == stages) {
+          stage = n_res;
           phase ^= 1;
         }
         if (++buf == kBufs) {
@@ -521,7 +526,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer (both CTAs)
-    int stage = 0, gi = 0;
+    int stage = p.n_res, gi = 0;
     uint32_t phase = 0;
     const uint32_t sA0 = smem_addr(sA), sB0 = smem_addr(sB);
     const uint32_t bar_b_full = smem_addr(b_full), bar_b_empty = smem_addr(b_empty);
@@ -548,10 +553,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         __syncwarp();
       }
-      if (p.resident) {
-        // small reference sets: tile j lives in stage j for the whole launch
+      if (p.n_res > 0) {
+        // small reference sets (or the first n_res tiles of a mid-size set): tile j
+        // lives in stage j for the whole launch
         if (gi == 0) {
-          for (int j = 0; j < p.nt_total; ++j) {
+          for (int j = 0; j < p.n_res; ++j) {
             const bool low = j < p.nt_lower;
             const int y = (low ? j : j - p.nt_lower) * kTileN + (int)rank * kHalfRows;
             if (elect_one()) {
@@ -565,10 +571,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             __syncwarp();
           }
         }
-        continue;
+        if (p.resident) continue;
       }
       for (int jj = 0; jj < p.nt_total; ++jj) {
         const int j = tile_of(jj);
+        if (j < p.n_res) continue;  // resident
         const bool low = j < p.nt_lower;
         const CUtensorMap* map = low ? &map_lower : &map_upper;
         const int y = (low ? j : j - p.nt_lower) * kTileN + (int)rank * kHalfRows;
@@ -586,7 +593,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         __syncwarp();
         if (++stage == p.stages) {
-          stage = 0;
+          stage = p.n_res;
           phase ^= 1;
         }
       }
@@ -800,6 +807,7 @@ struct Fp4Layout {
   int a_halves, a_bufs, stages;
   int ring;  // stages that fit next to the sample buffers
   bool resident;
+  int n_res;  // resident tiles (all when `resident`; a prefix of a mid-size set otherwise)
   size_t smem;
 };
 
@@ -830,10 +838,39 @@ Fp4Layout fp4_layout(int tn, int64_t nt_l, int64_t nt_u, int cq, bool want_first
     L.a_bufs = 2;
   int stages = (int)((max_smem - fixed - L.a_bufs * a_buf) / b_stage);
   if (stages > 16) stages = 16;
-  L.ring = stages;
   // a launch whose reference tiles all fit in the ring keeps them resident
   L.resident = allow_resident && nt <= stages;
-  if (L.resident) stages = (int)nt;
+  L.n_res = 0;
+  if (L.resident) {
+    L.ring = stages;
+    stages = (int)nt;
+    L.n_res = (int)nt;
+  } else {
+    // mid-size sets (up to twice the ring): all but kHybridRing stages hold a resident
+    // prefix of the tiles, the rest stream through a short ring, so each sample group
+    // re-loads only the tail of the set (the whole set re-streamed per group cost about
+    // 2500 cycles per group just past residency: cfg4 K = 2500, 0.67 of peak).  Resident
+    // stages are worth more than a third sample buffer here too.
+    const char* hy_env = getenv("RSR_FP4_HYBRID");
+    const bool allow_hybrid = allow_resident && !(hy_env && atoi(hy_env) == 0);
+    constexpr int kHybridRing = 3;
+    // streaming more than kHybridTail tiles through the short ring measured slower than
+    // streaming the whole set through the full ring (profiles/r2_fp4_hybrid.txt: K = 2500 /
+    // 3000 gain 0.67 -> 0.73 / 0.72 -> 0.76, K = 3500 / 4000 lose 0.82 -> 0.77 / 0.83 -> 0.79)
+    constexpr int kHybridTail = 7;
+    auto hybrid_ok = [&](int st) {
+      return allow_hybrid && st >= kHybridRing + 2 && nt - (st - kHybridRing) <= kHybridTail;
+    };
+    if (!ab_env && L.a_bufs == 3) {
+      const int st2 = (int)std::min<size_t>(16, (max_smem - fixed - 2 * a_buf) / b_stage);
+      if (hybrid_ok(st2)) {
+        L.a_bufs = 2;
+        stages = st2;
+      }
+    }
+    if (hybrid_ok(stages)) L.n_res = stages - kHybridRing;
+    L.ring = stages;
+  }
   L.stages = stages;
   L.smem = fixed + L.a_bufs * a_buf + (size_t)stages * b_stage;
   // one CTA per SM: a small resident launch must not let a second CTA onto the
@@ -897,6 +934,7 @@ int launch_fp4(const Fp4Call& c) {
     q.a_halves = L.a_halves;
     q.a_bufs = L.a_bufs;
     q.resident = L.resident;
+    q.n_res = L.n_res;
     q.stages = L.stages;
     int rc2 = rsr::ensure_dynamic_smem(reinterpret_cast<const void*>(kern), L.smem);
     if (rc2) return rc2;

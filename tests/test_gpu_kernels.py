@@ -463,7 +463,8 @@ def test_refset_insert_matches_sequential_insert(n, m, batch):
             assert torch.equal(enc, fp4)
 
 
-@pytest.mark.parametrize("kl,ku", [(0, 1500), (0, 2200), (0, 2600), (2000, 0), (600, 600), (900, 1000)])
+@pytest.mark.parametrize("kl,ku", [(0, 1500), (0, 2200), (0, 2600), (0, 3000), (2000, 0), (600, 600),
+                                   (900, 1000), (1300, 1400)])
 @pytest.mark.parametrize("first", [False, True])
 def test_fp4_mid_size_sets_resident_and_streamed(kl, ku, first):
     # one-sided launches buffer one sample half, and a set that fits only next to
