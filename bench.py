@@ -205,11 +205,13 @@ class CpuClassify:
         return rows * self.K / dt, dt, np.bincount(labels, minlength=3).tolist()
 
     def calibrate(self, target_s):
-        """Rows per slice so that one slice takes about `target_s` seconds."""
-        probe = max(64, 4 * self.cores * 4)
-        rate, dt, _ = self.run(probe, start=1 << 40)
-        rows = int(rate * target_s / max(1, self.K))
-        return int(max(probe, min(1 << 20, rows)))
+        """Rows per slice so that one slice takes about `target_s` seconds, in whole
+        rounds of 4 x cores chunks of 16 rows (so both CPU legs -- this line's
+        cpu_baseline and the reference arm -- land on the same slice size)."""
+        quantum = 4 * self.cores * 16
+        rate, dt, _ = self.run(quantum, start=1 << 40)
+        rounds = max(1, round(rate * target_s / max(1, self.K) / quantum))
+        return int(min(1 << 20, rounds * quantum))
 
     def public_api(self, rows):
         """One call of the reference's public `rsr.classify` on a slice, including
