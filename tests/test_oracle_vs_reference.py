@@ -51,3 +51,45 @@ def test_rgg_st_stage1(reference_rsr, seed):
                       parallel_searches=4)
     assert o["lower"] == ref.lower.members and o["upper"] == ref.upper.members
     assert o["iterations"] == ref.iterations and ev.count == model.evaluation_count
+
+
+def test_model_api_matches_reference(reference_rsr):
+    """SystemModel / ComponentDistribution / check_coherency behave as the reference's
+    (model.py): same violations in the same order, same evaluation counts, same error
+    messages."""
+    import paper_2604_17066_b200 as P
+    import rsr
+
+    def phi(x):  # incoherent on purpose: component 0 helps, component 1 hurts
+        return int(x[0] >= 1) if x[1] == 0 else 0
+
+    for seed in range(3):
+        mine = P.SystemModel(5, 3, 2, phi)
+        ref = rsr.SystemModel(5, 3, 2, phi)
+        a = P.check_coherency(mine, 40, seed)
+        b = rsr.check_coherency(ref, 40, seed)
+        assert len(a) == len(b) > 0
+        assert all(np.array_equal(x, y) for p, q in zip(a, b) for x, y in zip(p, q))
+        assert mine.evaluation_count == ref.evaluation_count == 80
+    for args in ((0, 2, 2, phi), (3, 1, 2, phi), (3, 2, 1, phi)):
+        with pytest.raises(ValueError) as e1:
+            P.SystemModel(*args)
+        with pytest.raises(ValueError) as e2:
+            rsr.SystemModel(*args)
+        assert str(e1.value) == str(e2.value)
+    m1, m2 = P.SystemModel(3, 2, 2, phi), rsr.SystemModel(3, 2, 2, phi)
+    for bad in ([0, 1], [0, 1, 2], [[0, 1, 1]]):
+        with pytest.raises(ValueError) as e1:
+            m1.evaluate(bad)
+        with pytest.raises(ValueError) as e2:
+            m2.evaluate(bad)
+        assert str(e1.value) == str(e2.value)
+    for probs in ([[0.5, 0.6]], [[1.5, -0.5]], [0.5, 0.5], [[0.3, 0.7], [0.2, 0.7]]):
+        with pytest.raises(ValueError) as e1:
+            P.ComponentDistribution(np.array(probs))
+        with pytest.raises(ValueError) as e2:
+            rsr.ComponentDistribution(np.array(probs))
+        assert str(e1.value) == str(e2.value)
+    d1 = P.ComponentDistribution.iid(4, [0.25, 0.75])
+    d2 = rsr.ComponentDistribution.iid(4, [0.25, 0.75])
+    assert np.array_equal(d1.probs, d2.probs) and (d1.n_components, d1.n_states) == (4, 2)
