@@ -22,6 +22,8 @@
 // runs the union-find, the warp runs the BFS.  Simple graphs (no parallel
 // edges: RSR_PHI_FLAG_SIMPLE) with <= 256 nodes; other cases use csrc/phi_bits.cu
 // or csrc/phi.cu.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace {
@@ -410,11 +412,118 @@ __device__ __forceinline__ int64_t upper_walk(const GraphSmem& g, Adj& adj, uint
   return calls;
 }
 
+// Upper side in closed form (default).  With edge weights = component index, the
+// reference's walk deletes, in index order, every edge of G_L whose removal keeps s
+// and t connected; the edges it keeps are exactly the s-t path of the MAXIMUM
+// spanning forest of G_L (proof: an edge e off that path P is deleted because P
+// survives without it; an edge e on P is the heaviest edge across its fundamental
+// cut, so every other edge across the cut has a smaller index, was considered
+// earlier and deleted while P was intact, and removing e then disconnects s and t).
+// So: Kruskal by descending index on lane 0 until s and t meet (later unions cannot
+// change their tree path), one bitset BFS over the tree edges for the path, and the
+// result and Phi-call count follow per component: an edge of P stops at L after
+// x_n - L + 1 calls, every other component drops to 0 after x_n calls.  One BFS
+// instead of one per witness-path edge (~36 per cfg3 search).
+template <int W>
+__device__ __forceinline__ int64_t upper_mst(const GraphSmem& g, uint32_t* tree, uint8_t* x,
+                                             int32_t* par, uint32_t* levels, uint32_t* onpath,
+                                             int L, int lane) {
+  for (int v = lane; v < g.n; v += 32) par[v] = v;
+  for (int i = lane; i < g.n * W; i += 32) tree[i] = 0;
+  __syncwarp();
+  BPROF_T(k0);
+  // The maximum spanning forest by Boruvka rounds, warp-parallel (distinct weights =
+  // edge indices, so the forest is Kruskal's): every component picks its largest-index
+  // edge to another component (atomicMax per component), the picks join the forest,
+  // components link along them (a mutual pick links the larger label to the smaller,
+  // the only cycles being such pairs) and pointer jumping relabels; ~log2(n) rounds.
+  // The rounds stop once s and t share a component: the forest then holds their
+  // whole tree path.  (A lane-0 Kruskal union-find took ~105K cycles per search.)
+  int32_t* lab = par;                      // component label (= parent pointer of roots)
+  int32_t* best = reinterpret_cast<int32_t*>(levels);  // scratch until the BFS below
+  while (true) {
+    for (int v = lane; v < g.n; v += 32) best[v] = -1;
+    __syncwarp();
+    for (int e = lane; e < g.N; e += 32) {
+      if (x[e] < L) continue;
+      const int a = lab[g.eu[e]], c = lab[g.ev[e]];
+      if (a != c) {
+        atomicMax(&best[a], e);
+        atomicMax(&best[c], e);
+      }
+    }
+    __syncwarp();
+    int link[W];  // new parent of each root this lane owns (read phase, then write)
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const int r = 32 * q + lane;
+      link[q] = -1;
+      if (r < g.n && lab[r] == r && best[r] >= 0) {
+        const int e = best[r];
+        const int a = lab[g.eu[e]], c = lab[g.ev[e]];
+        const int o = a == r ? c : a;
+        const uint32_t u = g.eu[e], v = g.ev[e];
+        atomicOr(&tree[u * W + (v >> 5)], 1u << (v & 31));
+        atomicOr(&tree[v * W + (u >> 5)], 1u << (u & 31));
+        link[q] = (best[o] == e && o > r) ? -1 : o;  // mutual pick: the larger label links
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      if (link[q] >= 0) lab[32 * q + lane] = link[q];
+    __syncwarp();
+    while (true) {  // pointer jumping to the roots
+      bool moved = false;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        const int v = 32 * q + lane;
+        if (v < g.n) {
+          const int p = lab[v], pp = lab[p];
+          if (pp != p) {
+            lab[v] = pp;
+            moved = true;
+          }
+        }
+      }
+      __syncwarp();
+      if (!__any_sync(kFull, moved)) break;
+    }
+    if (lab[g.s] == lab[g.t]) break;
+  }
+  __syncwarp();
+  BPROF_T(k1);
+  BPROF_ADD(2, k1 - k0);
+  AdjSmem<W> ta{tree};
+  static_assert(!AdjSmem<W>::kRegisters, "tree adjacency lives in shared memory");
+  uint32_t* lev_t = levels + g.n * W;
+  Meet mt;
+  bfs_bidir<W>(ta, levels, lev_t, g.n, g.s, g.t, lane, mt);  // s, t are connected in the tree
+  trace_bidir<W>(g, ta, levels, lev_t, mt, onpath, lane);
+  BPROF_T(k2);
+  BPROF_ADD(4, k2 - k1);
+  BPROF_ADD(1, 1);
+  unsigned c = 0;
+  for (int e = lane; e < g.N; e += 32) {
+    const int xe = x[e];
+    if (xe >= L && ((onpath[e >> 5] >> (e & 31)) & 1u)) {
+      c += (unsigned)(xe - L + 1);
+      x[e] = (uint8_t)L;
+    } else {
+      c += (unsigned)xe;
+      x[e] = 0;
+    }
+  }
+  const unsigned calls = __reduce_add_sync(kFull, c);
+  __syncwarp();
+  return calls;
+}
+
 template <int W>
 __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t* __restrict__ x0,
                                       int64_t B, uint8_t* __restrict__ out_refs,
                                       uint8_t* __restrict__ out_side,
-                                      int64_t* __restrict__ out_calls) {
+                                      int64_t* __restrict__ out_calls, int mst) {
   extern __shared__ __align__(16) uint8_t smem[];
   GraphSmem g;
   g.N = d.n_components;
@@ -517,8 +626,11 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
           x[n] = (uint8_t)(M - 1);
         }
       }
+    } else if (mst) {
+      // ---------------- upper side: maximum spanning forest path (closed form)
+      calls += upper_mst<W>(g, adj, x, par, levels, onpath, L, lane);
     } else {
-      // ---------------- upper side: witness path + BFS for edges on it
+      // ---------------- upper side: witness path + BFS for edges on it (round 1)
       for (int i = lane; i < g.n * W; i += 32) adj[i] = 0;
       __syncwarp();
       for (int e = lane; e < g.N; e += 32) {
@@ -566,7 +678,12 @@ int launch_graph(const rsr_phi_desc& d, int L, const uint8_t* x0, int64_t B, uin
   auto k = boundary_graph_kernel<W>;
   if (smem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<(unsigned)grid, warps * 32, smem, st>>>(d, L, x0, B, out_refs, out_side, out_calls);
+  // RSR_BOUNDARY_MST=0: the round-1 witness-path walk (A/B and cross-checks)
+  static const int mst = [] {
+    const char* e = getenv("RSR_BOUNDARY_MST");
+    return e && atoi(e) == 0 ? 0 : 1;
+  }();
+  k<<<(unsigned)grid, warps * 32, smem, st>>>(d, L, x0, B, out_refs, out_side, out_calls, mst);
   return rsr::check_launch("boundary_graph_kernel");
 }
 

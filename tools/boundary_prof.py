@@ -37,6 +37,13 @@ for name, m, thr, p_hi in (("st", 2, 0, 0.9), ("widest", 3, 0, 0.8), ("widest", 
     fn(buf, 0)
     v = list(buf)
     up = max(v[1], 1)
+    if os.environ.get("RSR_BOUNDARY_MST", "1") != "0":  # closed-form upper side
+        print(f"{name} m'={thr}: {s.elapsed_time(e):.3f} ms; searches {v[0]} (upper {v[1]}); per upper "
+              f"search: spanning-forest cycles {v[2] / up:.0f}, tree BFS + trace cycles "
+              f"{v[4] / up:.0f}; "
+              f"init union-find cycles/search {v[6] / max(v[0], 1):.0f}; cycles/search "
+              f"{v[7] / max(v[0], 1):.0f}")
+        continue
     print(f"{name} m'={thr}: {s.elapsed_time(e):.3f} ms; searches {v[0]} (upper {v[1]}); per upper search: "
           f"BFS {v[2] / up:.1f}, levels/BFS {v[3] / max(v[2], 1):.1f}, cycles/BFS {v[4] / max(v[2], 1):.0f}, "
           f"trace cycles/BFS {v[5] / max(v[2], 1):.0f}, init union-find cycles/search {v[6] / max(v[0], 1):.0f}; "
