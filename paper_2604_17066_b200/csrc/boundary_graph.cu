@@ -606,6 +606,8 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
     if (!connected) {
       // ---------------- lower side: union-find, no Phi evaluation needed
       if (lane == 0) {
+        // the roots of s and t are tracked through the links (no finds for them)
+        int rs = uf_find(par, g.s), rt = uf_find(par, g.t);
         for (int n = 0; n < g.N; ++n) {
           const int xn = x[n];
           if (xn >= M - 1) continue;
@@ -616,12 +618,15 @@ __global__ void boundary_graph_kernel(const rsr_phi_desc d, int L, const uint8_t
           }
           calls += L - xn;  // steps up to L, the last one adds edge n to G_L
           const int a = uf_find(par, eu[n]), c = uf_find(par, ev[n]);
-          const int rs = uf_find(par, g.s), rt = uf_find(par, g.t);
           if ((a == rs && c == rt) || (a == rt && c == rs)) {
             x[n] = (uint8_t)(L - 1);  // crossing: reverted, walk moves to n + 1
             continue;
           }
-          if (a != c) par[a] = c;
+          if (a != c) {
+            par[a] = c;
+            if (rs == a) rs = c;
+            if (rt == a) rt = c;
+          }
           calls += M - 1 - L;
           x[n] = (uint8_t)(M - 1);
         }
