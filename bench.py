@@ -356,7 +356,8 @@ def secondary_kernels():
         pr = d.device_probs()
         for rng, code in (("shared", _abi.RNG_SHARED), ("device", _abi.RNG_DEVICE)):
             ms = timed(lambda: _abi.call("rsr_sample_fp4_ex", _abi.ptr(pr), N_COMP, m, 0, 1, 0, S,
-                                         _abi.ptr(st), _abi.ptr(a4), rb, code, _abi.stream_ptr()))
+                                         _abi.ptr(st), _abi.ptr(a4), rb, S * rb, code,
+                                         _abi.stream_ptr()))
             wbytes = S * (N_COMP + 2 * rb)
             out[f"sample_rows_kernel_M{m}_{rng}"] = {
                 "shape": f"2^20 x {N_COMP} draws", "ms": ms,
@@ -480,10 +481,11 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     dist = P.ComponentDistribution.iid(N_COMP, [1 - p1, p1])
     batch = P.sample_batch(dist, S, seed=0, generation_index=0, start=start)
     if method == "tc":
-        A = batch.fp4(2)
+        A = batch.fp4(2)  # planar A_up / A_lo planes (sample_batch's default layout)
+        plane = batch.fp4_plane_stride(2)
         bl, nl, al = lower.device_fp4_rows(2)
         bu, nu, au = upper.device_fp4_rows(2)
-        width = A.shape[1] // 2  # bytes per operand row
+        width = _abi.fp4_row_bytes(N_COMP, 2)  # bytes per operand row
     else:
         A = batch.thermo(2)
         bl, nl = lower.device_thermo(2)
@@ -506,8 +508,8 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
 
     def classify_kernel():
         if method == "tc":
-            _abi.call("rsr_classify_fp4_ex", _abi.ptr(A), S, None, _abi.ptr(bl), nl, al, _abi.ptr(bu),
-                      nu, au, width, _abi.ptr(flags), None, None, 0, stream)
+            _abi.call("rsr_classify_fp4_planar", _abi.ptr(A), plane, S, None, _abi.ptr(bl), nl, al,
+                      _abi.ptr(bu), nu, au, width, _abi.ptr(flags), None, None, 0, stream)
         elif method == "tc8":
             _abi.call("rsr_classify_tc", _abi.ptr(A), S, _abi.ptr(bl), nl, _abi.ptr(bu), nu, width,
                       _abi.ptr(flags), 0, stream)

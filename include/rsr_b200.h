@@ -121,13 +121,18 @@ int rsr_sample_fp4(const double* probs, int n_components, int n_states, uint64_t
  * calls with rng = RSR_RNG_DEVICE draw flat index f = (start+i)*N + n from word
  * f%4 of Philox4x32-10 block f/4 (counter [f/4 lo, f/4 hi, gen lo, gen hi], key
  * [seed lo, seed hi]); state = #{m < M-1 : raw32 >= ceil(cum_m * 2^32)}.
- * rng = RSR_RNG_SHARED is rsr_sample / rsr_sample_fp4. */
+ * rng = RSR_RNG_SHARED is rsr_sample / rsr_sample_fp4.  rsr_sample_fp4_ex also takes
+ * the FP4 operand layout: fp4_plane_stride = 0 writes interleaved rows [A_up | A_lo]
+ * (2*row_bytes per row); > 0 writes planar A_up rows of row_bytes and the A_lo plane
+ * fp4_plane_stride bytes further (a multiple of 16, >= count*row_bytes), which a
+ * one-sided classification streams without reading the other half. */
 int rsr_sample_ex(const double* probs, int n_components, int n_states, uint64_t seed,
                   uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
                   int8_t* out_thermo, int ld_thermo, int rng, void* stream);
 int rsr_sample_fp4_ex(const double* probs, int n_components, int n_states, uint64_t seed,
                       uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
-                      uint8_t* out_fp4, int row_bytes, int rng, void* stream);
+                      uint8_t* out_fp4, int row_bytes, int64_t fp4_plane_stride, int rng,
+                      void* stream);
 /* Raw 32-bit words first..first+count-1 of the device stream (seed, gen). */
 int rsr_device_raw(uint64_t seed, uint64_t gen, int64_t first, int64_t count, uint32_t* out,
                    void* stream);
@@ -187,6 +192,10 @@ int rsr_classify_tc_explain(const int8_t* A, int64_t S, const int8_t* B_lower,
 int rsr_fp4_row_bytes(int n_components, int n_states);
 int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int n_components,
                            int n_states, uint8_t* out, int row_bytes, void* stream);
+/* Same with the operand layout of rsr_sample_fp4_ex (plane_stride 0: interleaved). */
+int rsr_encode_samples_fp4_ex(const uint8_t* states, int64_t count, int n_components,
+                              int n_states, uint8_t* out, int row_bytes, int64_t plane_stride,
+                              void* stream);
 /* FP4 sample operand from the reference's classification input: rows of
  * EncodedBatch(kind="sample").packed (encoding.py:82-98, np.packbits of the
  * one-hot N x M rows, MSB first, ceil(N*M/8) bytes per row; each component's
@@ -210,6 +219,15 @@ int rsr_classify_fp4_ex(const uint8_t* A, int64_t S, const int64_t* S_dev,
                         const uint8_t* B_upper, int64_t n_upper, int64_t avail_upper,
                         int row_bytes, uint8_t* flags, int64_t* first_lower,
                         int64_t* first_upper, int accumulate, void* stream);
+/* rsr_classify_fp4_ex on a planar sample operand (A_up rows of row_bytes, A_lo plane
+ * a_plane_stride bytes further; rsr_sample_fp4_ex / rsr_encode_samples_fp4_ex with the
+ * same stride). */
+int rsr_classify_fp4_planar(const uint8_t* A, int64_t a_plane_stride, int64_t S,
+                            const int64_t* S_dev, const uint8_t* B_lower, int64_t n_lower,
+                            int64_t avail_lower, const uint8_t* B_upper, int64_t n_upper,
+                            int64_t avail_upper, int row_bytes, uint8_t* flags,
+                            int64_t* first_lower, int64_t* first_upper, int accumulate,
+                            void* stream);
 /* rsr_classify_fp4 over the first *S_dev (device count, <= S_cap) rows of A:
  * the sample count of a later pass is known only on the device. */
 int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,

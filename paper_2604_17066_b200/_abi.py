@@ -81,7 +81,7 @@ EXPORTED = {
     "rsr_sample": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
     "rsr_sample_fp4": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
     "rsr_sample_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I, _P]),
-    "rsr_sample_fp4_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I, _P]),
+    "rsr_sample_fp4_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I64, _I, _P]),
     "rsr_device_raw": (_I, [_U64, _U64, _I64, _I64, _P, _P]),
     "rsr_comm_unique_id": (_I, [_P]),
     "rsr_comm_init": (_I, [_P, _I, _I, _P]),
@@ -97,9 +97,12 @@ EXPORTED = {
     "rsr_classify_tc_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_fp4_row_bytes": (_I, [_I, _I]),
     "rsr_encode_samples_fp4": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
+    "rsr_encode_samples_fp4_ex": (_I, [_P, _I64, _I, _I, _P, _I, _I64, _P]),
     "rsr_encode_refs_fp4": (_I, [_P, _I64, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_unpack_onehot_fp4": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "rsr_classify_fp4": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _I, _P]),
+    "rsr_classify_fp4_planar": (_I, [_P, _I64, _I64, _P, _P, _I64, _I64, _P, _I64, _I64, _I, _P,
+                                     _P, _P, _I, _P]),
     "rsr_classify_fp4_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_classify_bits": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),

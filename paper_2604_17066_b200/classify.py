@@ -254,14 +254,19 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
     tc_ok = _abi.thermo_kpad(batch.n_components, m_eff) <= TC_MAX_KPAD
     if fp4_ok and (method == "fp4" or (method == "tc" and fp4_exact())):
         a = batch.fp4(m_eff)
-        rb = a.shape[1] // 2
+        plane = batch.fp4_plane_stride(m_eff)
+        rb = _abi.fp4_row_bytes(batch.n_components, m_eff)
         bl, nl, al = lower_set.device_fp4_rows(m_eff) if lower_set is not None else (None, 0, 0)
         bu, nu, au = upper_set.device_fp4_rows(m_eff) if upper_set is not None else (None, 0, 0)
         if want_first:
             fl = torch.empty(H, dtype=torch.int64, device=dev)
             fu = torch.empty(H, dtype=torch.int64, device=dev)
-        _abi.call("rsr_classify_fp4_ex", _abi.ptr(a), H, None, _abi.ptr(bl), nl, al, _abi.ptr(bu),
-                  nu, au, rb, _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
+        if plane:
+            _abi.call("rsr_classify_fp4_planar", _abi.ptr(a), plane, H, None, _abi.ptr(bl), nl, al,
+                      _abi.ptr(bu), nu, au, rb, _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
+        else:
+            _abi.call("rsr_classify_fp4_ex", _abi.ptr(a), H, None, _abi.ptr(bl), nl, al,
+                      _abi.ptr(bu), nu, au, rb, _abi.ptr(flags), _abi.ptr(fl), _abi.ptr(fu), 0, st)
     elif method in ("tc", "tc8", "fp4") and tc_ok:
         a = batch.thermo(m_eff)
         bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)

@@ -172,6 +172,15 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int x, int y, int z, int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & kPeerMask), "r"(x), "r"(y), "r"(z), "r"(w)
+      : "memory");
+}
+
 #define RSR_LD16(addr, v)                                                                      \
   asm volatile(                                                                                \
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
@@ -537,7 +546,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       for (int h = 0; h < 2; ++h) {
         if (h == 0 ? nt_l == 0 : nt_u == 0) continue;
         const uint32_t bar_af = smem_addr(&a_full[2 * ab + h]);
-        const int z0 = h == 0 ? p.cq : 0;
+        const int plane = h == 0 ? 1 : 0;  // A_lo is plane 1, A_up plane 0
         PROF_T(p0);
         mbar_wait(smem_addr(&a_empty[2 * ab + h]), a_par ^ 1);
         PROF_T(p1);
@@ -547,9 +556,9 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             mbar_expect_tx(bar_af, 2 * (uint32_t)(p.cq * kChunkA));
           else
             mbar_arrive_leader(bar_af);
-          const uint32_t off = p.a_halves == 2 ? (uint32_t)(z0 * kChunkA) : 0u;
-          tma_load_3d_pair(sA0 + (uint32_t)ab * a_buf_bytes + off, &map_a,
-                           bar_af, 0, g * 2 * kRowsA + (int)rank * kRowsA, z0);
+          const uint32_t off = p.a_halves == 2 ? (uint32_t)(plane * p.cq * kChunkA) : 0u;
+          tma_load_4d_pair(sA0 + (uint32_t)ab * a_buf_bytes + off, &map_a, bar_af, 0,
+                           g * 2 * kRowsA + (int)rank * kRowsA, 0, plane);
         }
         __syncwarp();
       }
@@ -784,8 +793,34 @@ int make_map3(CUtensorMap* map, const void* base, int64_t rows, int row_bytes, i
   return RSR_OK;
 }
 
+// Sample operand: {32 B, rows, chunks, 2 halves} with strides {row stride, 32, plane
+// stride}; one box = one half (A_up or A_lo) of 128 rows, landing chunk-major.  The
+// interleaved layout ([A_up | A_lo] rows) is row stride 2 x row_bytes, plane stride
+// row_bytes; the planar one (A_up and A_lo planes) row stride row_bytes: a launch that
+// reads one half then streams exactly its bytes (interleaved rows cost 256 B of DRAM
+// traffic per 160-byte half: access granularity).
+int make_map_a(CUtensorMap* map, const void* base, int64_t rows, int64_t row_stride,
+               int64_t plane_stride, int chunks) {
+  auto enc = tensor_map_encoder();
+  RSR_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {(cuuint64_t)kChunk, (cuuint64_t)rows, (cuuint64_t)chunks, 2};
+  cuuint64_t strides[3] = {(cuuint64_t)row_stride, (cuuint64_t)kChunk, (cuuint64_t)plane_stride};
+  cuuint32_t box[4] = {(cuuint32_t)kChunk, (cuuint32_t)kRowsA, (cuuint32_t)chunks, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    rsr::set_error("cuTensorMapEncodeTiled (fp4 samples) failed (%d)", (int)r);
+    return RSR_ECUDA;
+  }
+  return RSR_OK;
+}
+
 struct Fp4Call {
   const uint8_t* A;
+  int64_t a_row_stride;    // bytes between sample rows (2 x row_bytes interleaved, row_bytes planar)
+  int64_t a_plane_stride;  // bytes from a row's A_up half to its A_lo half
   int64_t S;
   const int64_t* S_dev;
   const uint8_t* B[2];   // lower, upper
@@ -888,7 +923,7 @@ int launch_fp4(const Fp4Call& c) {
   // loads only the halves its reference sides need (upper references alone
   // stream half the sample bytes)
   CUtensorMap ma;
-  int rc = make_map3(&ma, c.A, c.S, 2 * c.row_bytes, 2 * cq, kRowsA, cq);
+  int rc = make_map_a(&ma, c.A, c.S, c.a_row_stride, c.a_plane_stride, cq);
   if (rc) return rc;
 
   Fp4Params p;
@@ -1025,7 +1060,7 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
                       int64_t avail_lower, const uint8_t* B_upper, int64_t n_upper,
                       int64_t avail_upper, int row_bytes, uint8_t* flags, int64_t* first_lower,
                       int64_t* first_upper, int accumulate, void* stream,
-                      const int64_t* S_dev = nullptr) {
+                      const int64_t* S_dev = nullptr, int64_t a_plane_stride = 0) {
   RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4: negative size");
   RSR_REQUIRE(avail_lower >= n_lower && avail_upper >= n_upper,
               "rsr_classify_fp4: readable rows below the reference count");
@@ -1050,8 +1085,12 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   RSR_REQUIRE(rsr::ceil_div(n_lower, 160) + rsr::ceil_div(n_upper, 160) < (1 << 30),
               "rsr_classify_fp4: too many reference tiles");
   RSR_REQUIRE((n_lower == 0 || B_lower) && (n_upper == 0 || B_upper), "rsr_classify_fp4: null refs");
+  RSR_REQUIRE(a_plane_stride == 0 || (a_plane_stride % 16 == 0 && a_plane_stride >= S * row_bytes),
+              "rsr_classify_fp4: a_plane_stride must be 0 or a multiple of 16 >= S*row_bytes");
   Fp4Call c;
   c.A = A;
+  c.a_row_stride = a_plane_stride ? row_bytes : 2 * (int64_t)row_bytes;
+  c.a_plane_stride = a_plane_stride ? a_plane_stride : row_bytes;
   c.S = S;
   c.S_dev = S_dev;
   c.B[0] = B_lower;
@@ -1088,7 +1127,7 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
 // elements) of A_up and A_lo and stores them.
 __global__ void __launch_bounds__(256) encode_samples_fp4_kernel(
     const uint8_t* __restrict__ states, int64_t count, int N, int M, uint8_t* __restrict__ out,
-    int row_bytes, int kdim, int stage_bytes) {
+    int row_bytes, int kdim, int stage_bytes, int64_t row_stride, int64_t plane) {
   extern __shared__ uint8_t stage[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* buf = stage + warp * stage_bytes;
@@ -1097,8 +1136,8 @@ __global__ void __launch_bounds__(256) encode_samples_fp4_kernel(
     const uint8_t* x = states + i * N;
     for (int n = lane; n < N; n += 32) buf[n] = x[n];
     __syncwarp();
-    uint32_t* up_row = reinterpret_cast<uint32_t*>(out + i * (int64_t)(2 * row_bytes));
-    uint32_t* lo_row = up_row + words;
+    uint32_t* up_row = reinterpret_cast<uint32_t*>(out + i * row_stride);
+    uint32_t* lo_row = reinterpret_cast<uint32_t*>(out + i * row_stride + plane);
     for (int w = lane; w < words; w += 32) {
       uint32_t up, lo;
       rsr::fp4_sample_word(buf, w, M, kdim, up, lo);
@@ -1265,9 +1304,12 @@ extern "C" int rsr_fp4_row_bytes(int n_components, int n_states) {
   return (kdim + 1 + 63) / 64 * 32;
 }
 
-extern "C" int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int n_components,
-                                      int n_states, uint8_t* out, int row_bytes, void* stream) {
+extern "C" int rsr_encode_samples_fp4_ex(const uint8_t* states, int64_t count, int n_components,
+                                         int n_states, uint8_t* out, int row_bytes,
+                                         int64_t plane_stride, void* stream) {
   const int N = n_components, M = n_states;
+  RSR_REQUIRE(plane_stride == 0 || (plane_stride % 16 == 0 && plane_stride >= count * row_bytes),
+              "rsr_encode_samples_fp4: plane_stride must be 0 or a multiple of 16 >= count*row_bytes");
   RSR_REQUIRE(N >= 1 && M >= 2 && count >= 0, "rsr_encode_samples_fp4: bad shape");
   RSR_REQUIRE(row_bytes == rsr_fp4_row_bytes(N, M), "rsr_encode_samples_fp4: row_bytes must be %d",
               rsr_fp4_row_bytes(N, M));
@@ -1281,8 +1323,15 @@ extern "C" int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int 
   int64_t grid = rsr::ceil_div(count, 8);
   if (grid > 148 * 64) grid = 148 * 64;
   encode_samples_fp4_kernel<<<(unsigned)grid, 256, smem, rsr::as_stream(stream)>>>(
-      states, count, N, M, out, row_bytes, N * (M - 1), stage_bytes);
+      states, count, N, M, out, row_bytes, N * (M - 1), stage_bytes,
+      plane_stride ? row_bytes : 2 * (int64_t)row_bytes, plane_stride ? plane_stride : row_bytes);
   return rsr::check_launch("encode_samples_fp4_kernel");
+}
+
+extern "C" int rsr_encode_samples_fp4(const uint8_t* states, int64_t count, int n_components,
+                                      int n_states, uint8_t* out, int row_bytes, void* stream) {
+  return rsr_encode_samples_fp4_ex(states, count, n_components, n_states, out, row_bytes, 0,
+                                   stream);
 }
 
 extern "C" int rsr_encode_refs_fp4(const uint8_t* states, int64_t count, int64_t rows_total,
@@ -1318,6 +1367,19 @@ extern "C" int rsr_classify_fp4_ex(const uint8_t* A, int64_t S, const int64_t* S
                                    int64_t* first_upper, int accumulate, void* stream) {
   return classify_fp4_impl(A, S, B_lower, n_lower, avail_lower, B_upper, n_upper, avail_upper,
                            row_bytes, flags, first_lower, first_upper, accumulate, stream, S_dev);
+}
+
+extern "C" int rsr_classify_fp4_planar(const uint8_t* A, int64_t a_plane_stride, int64_t S,
+                                       const int64_t* S_dev, const uint8_t* B_lower,
+                                       int64_t n_lower, int64_t avail_lower,
+                                       const uint8_t* B_upper, int64_t n_upper,
+                                       int64_t avail_upper, int row_bytes, uint8_t* flags,
+                                       int64_t* first_lower, int64_t* first_upper,
+                                       int accumulate, void* stream) {
+  RSR_REQUIRE(a_plane_stride > 0, "rsr_classify_fp4_planar: a_plane_stride must be > 0");
+  return classify_fp4_impl(A, S, B_lower, n_lower, avail_lower, B_upper, n_upper, avail_upper,
+                           row_bytes, flags, first_lower, first_upper, accumulate, stream, S_dev,
+                           a_plane_stride);
 }
 
 extern "C" int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,

@@ -209,7 +209,8 @@ template <int MT, bool C32, int RNG>  // MT 2, 3: specialised state count; 0: an
 __global__ void __launch_bounds__(kRowThreads, RSR_SAMPLE_MINB)
 sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
                    int64_t start_row, int64_t count, uint8_t* __restrict__ states,
-                   uint8_t* __restrict__ fp4, int row_bytes, int st_bytes) {
+                   uint8_t* __restrict__ fp4, int row_bytes, int st_bytes, int64_t fp4_row_stride,
+                   int64_t fp4_plane) {
   extern __shared__ __align__(16) unsigned long long T[];
   load_thresholds_ext(probs, N, M, T);
   const int Mm1 = MT ? MT - 1 : M - 1;
@@ -287,9 +288,9 @@ sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed
         const int r = i / (MT ? fastq : 1), q = i - r * fastq;
         uint4 up, lo;
         fp4_quad_fast<MT>(st, (uint32_t)(r * N + (MT == 2 ? 32 : 16) * q), &up.x, &lo.x);
-        uint8_t* row = fp4 + (r0 + r) * (int64_t)(2 * row_bytes);
+        uint8_t* row = fp4 + (r0 + r) * fp4_row_stride;
         reinterpret_cast<uint4*>(row)[q] = up;
-        reinterpret_cast<uint4*>(row + row_bytes)[q] = lo;
+        reinterpret_cast<uint4*>(row + fp4_plane)[q] = lo;
       }
       for (int i = threadIdx.x; i < rows * slowq; i += blockDim.x) {
         const int r = i / slowq, q = fastq + (i - r * slowq);
@@ -298,9 +299,9 @@ sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed
         uint32_t* l = &lo.x;
 #pragma unroll
         for (int t = 0; t < 4; ++t) rsr::fp4_sample_word(st + r * N, 4 * q + t, M, kdim, u[t], l[t]);
-        uint8_t* row = fp4 + (r0 + r) * (int64_t)(2 * row_bytes);
+        uint8_t* row = fp4 + (r0 + r) * fp4_row_stride;
         reinterpret_cast<uint4*>(row)[q] = up;
-        reinterpret_cast<uint4*>(row + row_bytes)[q] = lo;
+        reinterpret_cast<uint4*>(row + fp4_plane)[q] = lo;
       }
     }
   }
@@ -573,8 +574,8 @@ const void* rows_kernel(int M, bool c32) {
 
 extern "C" int rsr_sample_fp4_ex(const double* probs, int n_components, int n_states,
                                  uint64_t seed, uint64_t gen, int64_t start, int64_t count,
-                                 uint8_t* out_states, uint8_t* out_fp4, int row_bytes, int rng,
-                                 void* stream) {
+                                 uint8_t* out_states, uint8_t* out_fp4, int row_bytes,
+                                 int64_t fp4_plane_stride, int rng, void* stream) {
   const int N = n_components, M = n_states;
   RSR_REQUIRE(rng == RSR_RNG_SHARED || rng == RSR_RNG_DEVICE, "rsr_sample_fp4: bad rng %d", rng);
   RSR_REQUIRE(N >= 1 && M >= 2 && M <= 255, "rsr_sample_fp4: need N >= 1 and 2 <= M <= 255");
@@ -590,6 +591,13 @@ extern "C" int rsr_sample_fp4_ex(const double* probs, int n_components, int n_st
   if (out_fp4)
     RSR_REQUIRE((reinterpret_cast<uintptr_t>(out_fp4) & 15) == 0,
                 "rsr_sample_fp4: out_fp4 must be 16-byte aligned");
+  // FP4 operand layout: interleaved rows [A_up | A_lo] (plane stride 0), or planar --
+  // A_up rows of row_bytes, the A_lo plane fp4_plane_stride bytes further
+  RSR_REQUIRE(fp4_plane_stride == 0 ||
+                  (fp4_plane_stride % 16 == 0 && fp4_plane_stride >= count * (int64_t)row_bytes),
+              "rsr_sample_fp4: fp4_plane_stride must be 0 or a multiple of 16 >= count*row_bytes");
+  const int64_t fp4_row_stride = fp4_plane_stride ? row_bytes : 2 * (int64_t)row_bytes;
+  const int64_t fp4_plane = fp4_plane_stride ? fp4_plane_stride : row_bytes;
   const int st_bytes = (kRowsPerCta * N + 16 + 15) / 16 * 16;  // + funnel-load slack
   const size_t smem = ((size_t)(N + kTExtra) * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 +
                       2 * (size_t)st_bytes;
@@ -616,9 +624,11 @@ extern "C" int rsr_sample_fp4_ex(const double* probs, int n_components, int n_st
   const int64_t chunks = rsr::ceil_div(count, kRowsPerCta);
   const int64_t grid = std::max<int64_t>(std::min<int64_t>(chunks, (int64_t)sms * std::max(per_sm, 1)),
                                          rsr::ceil_div(chunks, cpc));
-  void* args[] = {(void*)&probs, (void*)&N, (void*)&M, (void*)&seed, (void*)&gen,
-                  (void*)&start, (void*)&count, (void*)&out_states, (void*)&out_fp4,
-                  (void*)&row_bytes, (void*)&st_bytes};
+  void* args[] = {(void*)&probs,     (void*)&N,         (void*)&M,
+                  (void*)&seed,      (void*)&gen,       (void*)&start,
+                  (void*)&count,     (void*)&out_states, (void*)&out_fp4,
+                  (void*)&row_bytes, (void*)&st_bytes,  (void*)&fp4_row_stride,
+                  (void*)&fp4_plane};
   RSR_CUDA(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(kRowThreads), args, smem,
                             rsr::as_stream(stream)));
   return rsr::check_launch("sample_rows_kernel");
@@ -628,5 +638,5 @@ extern "C" int rsr_sample_fp4(const double* probs, int n_components, int n_state
                               uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
                               uint8_t* out_fp4, int row_bytes, void* stream) {
   return rsr_sample_fp4_ex(probs, n_components, n_states, seed, gen, start, count, out_states,
-                           out_fp4, row_bytes, RSR_RNG_SHARED, stream);
+                           out_fp4, row_bytes, 0, RSR_RNG_SHARED, stream);
 }

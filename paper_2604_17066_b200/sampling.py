@@ -36,6 +36,7 @@ class SampleBatch:
         self._thermo: dict[int, torch.Tensor] = {}
         self._bits: dict[int, torch.Tensor] = {}
         self._fp4: dict[int, torch.Tensor] = {}
+        self._fp4_plane: dict[int, int] = {}  # FP4 layout per M: 0 interleaved, > 0 planar
         if isinstance(states, torch.Tensor):
             if states.dim() != 2:
                 raise ValueError("states must be an H x N matrix")
@@ -99,8 +100,10 @@ class SampleBatch:
         return t
 
     def fp4(self, n_states: int, out: torch.Tensor | None = None) -> torch.Tensor:
-        """FP4 sample operand [H, 2 * row_bytes] = [A_up | A_lo] packed e2m1 rows
-        (A operand of the FP4 classifier, include/rsr_b200.h), cached per M."""
+        """FP4 sample operand (A operand of the FP4 classifier, include/rsr_b200.h), cached
+        per M: planar [2, H, row_bytes] (A_up plane, A_lo plane) by default, or
+        interleaved rows [H, 2 * row_bytes] = [A_up | A_lo] written into ``out``.
+        ``fp4_plane_stride`` tells which."""
         t = self._fp4.get(n_states)
         if t is None:
             n = self.n_components
@@ -109,13 +112,21 @@ class SampleBatch:
             if out is not None:
                 if out.dtype != torch.uint8 or out.shape[0] < self.n_samples or out.shape[1] != 2 * rb:
                     raise ValueError("fp4 buffer must be uint8 [>= H, 2 * row_bytes]")
-                t = out[: self.n_samples]
+                t, plane = out[: self.n_samples], 0
             else:
-                t = torch.empty((self.n_samples, 2 * rb), dtype=torch.uint8, device=st.device)
-            _abi.call("rsr_encode_samples_fp4", _abi.ptr(st), self.n_samples, n, n_states,
-                      _abi.ptr(t), rb, _device.stream())
+                t = torch.empty((2, self.n_samples, rb), dtype=torch.uint8, device=st.device)
+                plane = self.n_samples * rb
+            _abi.call("rsr_encode_samples_fp4_ex", _abi.ptr(st), self.n_samples, n, n_states,
+                      _abi.ptr(t), rb, plane, _device.stream())
             self._fp4[n_states] = t
+            self._fp4_plane[n_states] = plane
         return t
+
+    def fp4_plane_stride(self, n_states: int) -> int:
+        """Layout of ``fp4(n_states)``: 0 = interleaved rows, else the byte offset of the
+        A_lo plane (planar; a one-sided classification then reads only its half)."""
+        self.fp4(n_states)
+        return self._fp4_plane[n_states]
 
     def thermo_bits(self, n_states: int) -> torch.Tensor:
         """Packed thermometer bits [H, words] (bit-packed classifier operand)."""
@@ -186,15 +197,19 @@ def sample_batch(dist: ComponentDistribution, n_samples: int, seed: int,
     if fp4 is None:
         fp4 = (not int8_path) and rb <= _abi.FP4_MAX_ROW_BYTES
     if fp4 and not int8_path:
-        a4 = out_fp4[:n_samples] if out_fp4 is not None else torch.empty(
-            (n_samples, 2 * rb), dtype=torch.uint8, device=dev)
-        if a4.dtype != torch.uint8 or a4.shape != (n_samples, 2 * rb):
-            raise ValueError("fp4 buffer must be uint8 [>= H, 2 * row_bytes]")
+        if out_fp4 is not None:  # caller's interleaved rows [H, 2 * row_bytes]
+            a4, plane = out_fp4[:n_samples], 0
+            if a4.dtype != torch.uint8 or a4.shape != (n_samples, 2 * rb):
+                raise ValueError("fp4 buffer must be uint8 [>= H, 2 * row_bytes]")
+        else:  # planar: one-sided classifications stream only their half
+            a4 = torch.empty((2, n_samples, rb), dtype=torch.uint8, device=dev)
+            plane = n_samples * rb
         _abi.call("rsr_sample_fp4_ex", _abi.ptr(dist.device_probs()), n, m, seed & mask,
                   generation_index & mask, start, n_samples, _abi.ptr(states), _abi.ptr(a4), rb,
-                  code, _device.stream())
+                  plane, code, _device.stream())
         batch = SampleBatch(states, seed, generation_index, state_bound=m, rng=rng)
         batch._fp4[m] = a4
+        batch._fp4_plane[m] = plane
         return batch
     thermo = None
     kpad = _abi.thermo_kpad(n, m)

@@ -445,7 +445,7 @@ class _LeanPrefetcher:
             mask = (1 << 64) - 1
             _abi.call("rsr_sample_fp4_ex", self.probs, self.n, self.m, self.seed & mask,
                       gen & mask, self.start, self.count, _abi.ptr(self.states[slot]),
-                      _abi.ptr(dst), self.rb, self.rng, self.sptr)
+                      _abi.ptr(dst), self.rb, 0, self.rng, self.sptr)
             self.src[slot], self.has_states[slot] = dst, True
         self.ready[slot].record(self.stream)
         return slot
