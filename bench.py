@@ -494,7 +494,7 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     sb = batch.thermo_bits(2) if method == "bits" else None
     lb, _ = lower.device_bits(2) if method == "bits" else (None, 0)
     ub, _ = upper.device_bits(2) if method == "bits" else (None, 0)
-    a_bytes = A.shape[0] * A.shape[1]
+    a_bytes = A.numel()
     flags = torch.empty(S, dtype=torch.uint8, device=dev)
     labels = torch.empty(S, dtype=torch.uint8, device=dev)
     counts = torch.empty(4, dtype=torch.int64, device=dev)
