@@ -67,6 +67,9 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 #ifndef RSR_FP4_SPIN
 #define RSR_FP4_SPIN 0
 #endif
+#ifndef RSR_FP4_SET_RELEASE
+#define RSR_FP4_SET_RELEASE 0
+#endif
 // experiment knobs, both measured slower (spinning warps take issue slots from
 // the MMA / TMA warps): RSR_FP4_SPIN spins the MMA warp on buffer release,
 // RSR_FP4_EPI_SPIN the epilogue warps on accumulator completion
@@ -246,7 +249,8 @@ __device__ __forceinline__ void ld_cols_packed(uint32_t taddr, uint32_t* v) {
 template <int TN, bool FIRST>
 __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_bar, int lane,
                                               int c0, int64_t valid, bool& any, int& zref,
-                                              long long& t_loaded, long long* ts_release) {
+                                              long long& t_loaded, long long* ts_release,
+                                              int set_id) {
   constexpr int kCols = Tile<TN>::kCols;
   constexpr int R = kCols / 2;
   uint32_t v[R];
@@ -260,7 +264,14 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_b
 #ifdef RSR_FP4_PROF
   if (ts_release && lane == 0) *(volatile long long*)ts_release = clock64();
 #endif
+#if RSR_FP4_SET_RELEASE
+  // experiment: the set's 4 warps of this CTA meet on a named barrier (id 2 + set),
+  // then one arrival per CTA (t_empty count 2)
+  named_bar_sync(2 + set_id, 128);
+  if ((threadIdx.x & 127) == 0) mbar_arrive_leader(release_bar);
+#else
   if (lane == 0) mbar_arrive_leader(release_bar);
+#endif
   if (valid < c0 + kCols) {
 #pragma unroll
     for (int c = 0; c < kCols; ++c)
@@ -480,8 +491,8 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     for (int i = 0; i < kBufs; ++i) {
       mbar_init(smem_addr(&t_full[i]), 1);
-      // the 4 warps of the tile's epilogue set in both CTAs
-      mbar_init(smem_addr(&t_empty[i]), 2 * 4);
+      // the 4 warps of the tile's epilogue set in both CTAs (or one arrival per CTA)
+      mbar_init(smem_addr(&t_empty[i]), RSR_FP4_SET_RELEASE ? 2 : 2 * 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -683,7 +694,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         long long* tsr = nullptr;
 #endif
         epilogue_tile<TN, FIRST>(taddr, smem_addr(&t_empty[buf]), lane, 0, valid, any, zref,
-                                 t_loaded, tsr);
+                                 t_loaded, tsr, set);
         PROF_T(e2);
         PROF_ADD(0, t_loaded - e1);
         if (any) {
