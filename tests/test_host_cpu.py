@@ -196,3 +196,85 @@ def test_bench_gpus_flag_relaunches_under_torchrun():
     r, lines = _bench(["--impl", "reference", "--gpus", "2", "--steps", "1"],
                       env_extra={"WORLD_SIZE": "1"})
     assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr and not lines
+
+
+def _msf_upper_walk(n_nodes, edges, s, t, x, L):
+    """Closed form of the reference's upper-side boundary walk (boundary.py:116-147) used by
+    csrc/boundary_graph.cu: keep the s-t path of the maximum spanning forest (weight =
+    component index) of G_L = {e : x_e >= L}; path edges stop at L after x_e - L + 1 Phi
+    calls, every other component drops to 0 after x_e calls."""
+    par = list(range(n_nodes))
+
+    def find(a):
+        while par[a] != a:
+            par[a] = par[par[a]]
+            a = par[a]
+        return a
+    tree = [[] for _ in range(n_nodes)]
+    for e in range(len(edges) - 1, -1, -1):
+        if x[e] < L:
+            continue
+        u, v = edges[e]
+        a, b = find(u), find(v)
+        if a == b:
+            continue
+        par[a] = b
+        tree[u].append((v, e))
+        tree[v].append((u, e))
+        if find(s) == find(t):
+            break
+    prev = {s: None}
+    stack = [s]
+    while stack:
+        u = stack.pop()
+        for v, e in tree[u]:
+            if v not in prev:
+                prev[v] = (u, e)
+                stack.append(v)
+    path = set()
+    node = t
+    while prev[node] is not None:
+        node, e = prev[node]
+        path.add(e)
+    out, calls = [], 1
+    for e, xe in enumerate(x):
+        if xe >= L and e in path:
+            out.append(L)
+            calls += xe - L + 1
+        else:
+            out.append(0)
+            calls += xe
+    return tuple(out), calls
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_upper_boundary_walk_is_max_spanning_forest_path(seed):
+    """The closed form the device's upper-side boundary search uses equals the reference
+    walk (oracle restatement) on random graphs, states and thresholds: same reference
+    state, same Phi-call count."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    n_nodes = int(rng.integers(6, 30))
+    pairs = [(i, j) for i in range(n_nodes) for j in range(i + 1, n_nodes)]
+    k = min(len(pairs), int(rng.integers(n_nodes, 3 * n_nodes)))
+    edges = [pairs[i] for i in rng.choice(len(pairs), size=k, replace=False)]
+    s, t = 0, n_nodes - 1
+    m = int(rng.integers(2, 5))
+    kinds = [("st", oracle.phi_st(n_nodes, edges, s, t), 2, 2)]
+    kinds.append(("widest", oracle.phi_widest(n_nodes, edges, s, t, m), m, m))
+    checked = 0
+    for name, phi, mm, ms in kinds:
+        for trial in range(40):
+            x = rng.integers(0, mm, size=len(edges))
+            x[rng.random(len(edges)) < 0.6] = mm - 1
+            for thr in range(ms - 1):
+                ev = oracle.CountingPhi(phi, len(edges), mm, ms)
+                if ev(x) <= thr:
+                    continue  # lower side: union-find walk (no closed form needed)
+                ev.count = 0
+                vec, side = oracle.boundary_search(ev, x, thr)
+                assert side == oracle.UPPER
+                got, calls = _msf_upper_walk(n_nodes, edges, s, t, [int(v) for v in x], thr + 1)
+                assert got == vec and calls == ev.count, (name, thr, trial)
+                checked += 1
+    assert checked > 10
