@@ -13,7 +13,8 @@ for c in cfg1 cfg3 cfg5; do
 done
 CMD="python bench.py --steps 2 --warmup 3 --no-loop --no-cpu-baseline --no-secondary --no-e2e"
 $CMD > gpurun_out/prof_plain.log 2>&1 &&
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none \
+    -k 'regex:classify|finalize|sample_rows|encode' -c 200 --csv \
     --log-file gpurun_out/prof_launches.csv $CMD > gpurun_out/prof_ncu_launches.log 2>&1
 $CMD > gpurun_out/prof_plain2.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:classify_fp4_pair -s 15 -c 5 \
