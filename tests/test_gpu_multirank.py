@@ -124,3 +124,69 @@ def test_c_abi_comm_single_rank():
     torch.cuda.synchronize()
     assert counts.tolist() == [3, 5, 7] and torch.equal(out, rows) and torch.equal(flags, want)
     _abi.call("rsr_comm_destroy", comm)
+
+
+def _cov_worker(rank, world, port, q, rng):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    sys.path.insert(0, here)
+    import torch
+    torch.cuda.set_device(0)
+    import paper_2604_17066_b200 as P
+    from paper_2604_17066_b200 import workloads as W
+    from paper_2604_17066_b200.dist import Comm
+    from _specs import device_model
+    comm = Comm.from_env(backend="gloo")
+    g = W.cfg1(0)
+    spec = {"kind": "st", "n_nodes": g["n_nodes"], "edges": g["edges"], "s": 0, "t": 24,
+            "m": 2, "ms": 2}
+    model = device_model(spec)
+    dist = P.ComponentDistribution(g["probs"])
+    cfg = P.RunConfig(n_samples=3001, eps_u=1e-3, r_max=60, seed=4, parallel_searches=4, rng=rng)
+    s1 = P.stage1_find_references(model, dist, cfg, 0, comm)
+    rep = P.stage2_until_cov(model, dist, s1.lower, s1.upper, cfg, 0, 0.05, batch_samples=5001,
+                             comm=comm)
+    q.put((rank, [list(v) for v in s1.lower.members], [list(v) for v in s1.upper.members],
+           s1.iterations, rep.n_samples, rep.p_lower, rep.unclassified_resolved,
+           model.evaluation_count))
+    import torch.distributed as dist_
+    dist_.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("rng", ["shared", "device"])
+def test_two_rank_run_to_cov_matches_single_device(rng):
+    """Stage 1 and the run-to-c.o.v. loop sharded over 2 ranks (odd batch
+    sizes: uneven shards) equal the single-device run, on both sample streams."""
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    import paper_2604_17066_b200 as P
+    from paper_2604_17066_b200 import workloads as W
+    from _specs import device_model
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cov_worker, args=(r, 2, port, q, rng)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=280) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+    g = W.cfg1(0)
+    spec = {"kind": "st", "n_nodes": g["n_nodes"], "edges": g["edges"], "s": 0, "t": 24,
+            "m": 2, "ms": 2}
+    model = device_model(spec)
+    dist = P.ComponentDistribution(g["probs"])
+    cfg = P.RunConfig(n_samples=3001, eps_u=1e-3, r_max=60, seed=4, parallel_searches=4, rng=rng)
+    s1 = P.stage1_find_references(model, dist, cfg, 0)
+    rep = P.stage2_until_cov(model, dist, s1.lower, s1.upper, cfg, 0, 0.05, batch_samples=5001)
+    want = ([list(v) for v in s1.lower.members], [list(v) for v in s1.upper.members],
+            s1.iterations, rep.n_samples, rep.p_lower, rep.unclassified_resolved,
+            model.evaluation_count)
+    assert rep.n_samples > 5001  # several batches
+    for rank in (0, 1):
+        assert tuple(res[rank]) == want
