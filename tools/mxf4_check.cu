@@ -507,5 +507,8 @@ int main() {
   pair_rate<176>(sms, 5);
   pair_rate<160>(sms, 5);
   pair_rate<128>(sms, 5);
+  pair_rate<112>(sms, 5);
+  pair_rate<96>(sms, 5);
+  pair_rate<144>(sms, 5);
   return bad ? 1 : 0;
 }
