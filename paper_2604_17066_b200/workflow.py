@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _abi, _device
-from .boundary import ReferenceSet, ReferenceState, Side, boundary_search_batch
+from .boundary import ReferenceSet, Side, boundary_search_batch
 from .classify import classify, cov, fp4_exact
 from .dist import (Comm, counts_record, global_pick_owners, picks_in_prefix, shard_range,
                    split_records)
