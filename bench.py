@@ -734,7 +734,7 @@ def run_ours(args):
             r = measure_loop("cfg3", args.parallel_searches, rng=rng)
             cov_loop[rng] = {"value": r["value"], "unit": "s", "workload": r["config"]["workload"],
                              "stages": r["stages"], "phi_evaluations": r["phi_evaluations"],
-                             "trace": r.get("trace_s1")}
+                             "clocks": r.get("clocks"), "trace": r.get("trace_s1")}
         cov_loop = {"metric": "wall-time to c.o.v.=0.05", "unit": "s", "higher_is_better": False,
                     "value": cov_loop["shared"]["value"], **cov_loop}
 

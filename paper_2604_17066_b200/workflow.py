@@ -375,6 +375,11 @@ class _BatchCache:
 
     def __init__(self, count: int, row_bytes: int):
         free, total = torch.cuda.mem_get_info()
+        # memory torch's caching allocator holds but does not use (e.g. a previous run's
+        # cache slabs) is available too: counting only the driver's free memory left a
+        # repeated multistate_pmf in one process with a smaller cache (config 5:
+        # 0.37 -> 0.44 s on the second run)
+        free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
         self.shape = (max(count, 1), 2 * row_bytes)
         self.nbytes = self.shape[0] * self.shape[1]
         self.max_batches = max(0, free - max(16 << 30, total // 8)) // self.nbytes
