@@ -428,18 +428,32 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
         bl, nl = lower_set.device_thermo(m_eff) if lower_set is not None else (None, 0)
         bu, nu = upper_set.device_thermo(m_eff) if upper_set is not None else (None, 0)
     comp = torch.cuda.current_stream()
+    wave = 256 * max(1, _abi.device_sm_count() // 2)  # one sample group per CTA pair
     if chunk_rows is None:
-        # whole waves of the persistent classifier: 16 sample groups (256 rows) per CTA
-        # pair.  A chunk of 2^16 rows is 256 groups = 3.46 waves of 74 pairs, so a
-        # quarter of every chunk's last wave idled (cfg4 K = 5x10^5 e2e: 183 ms for a
-        # 151 ms kernel); larger chunks also amortise the reference-chunk launches
-        chunk_rows = 16 * 256 * max(1, _abi.device_sm_count() // 2)
+        # whole waves of the persistent classifier, 16 per chunk.  A chunk of 2^16 rows
+        # is 256 groups = 3.46 waves of 74 pairs, so a quarter of every chunk's last wave
+        # idled (cfg4 K = 5x10^5 e2e: 183 ms for a 151 ms kernel).  The first chunks ramp
+        # up from one wave (1, 2, 4, 8, 16): the copy of the first chunk is the part of
+        # the transfer nothing overlaps
+        chunk_rows = 16 * wave
+        sizes, tot, k = [], 0, 1
+        while tot < S:
+            n = min(k * wave, chunk_rows, S - tot)
+            sizes.append(n)
+            tot += n
+            k = min(2 * k, 16)
+    else:
+        sizes = [min(chunk_rows, S - lo) for lo in range(0, S, chunk_rows)]
     chunk = max(1, min(chunk_rows, S))
     copy, bufs, opnd, ready, free = _stream_buffers(dev, chunk, width_in, opnd_shape, opnd_dtype)
+    # encoded chunks are planar (A_up plane, A_lo plane of `chunk` rows): a one-sided
+    # classification streams only its half
+    plane = chunk * width if (fp4 and mode != "onehot") else 0
     flags = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
     st = _device.stream()
-    for i, lo in enumerate(range(0, S, chunk)):
-        hi = min(S, lo + chunk)
+    lo = 0
+    for i, n_rows in enumerate(sizes):
+        hi = lo + n_rows
         slot = i & 1
         with torch.cuda.stream(copy):
             if i >= 2:
@@ -451,18 +465,23 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
             _abi.call("rsr_unpack_onehot_fp4", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
                       _abi.ptr(opnd[slot]), width, st)
         elif fp4:
-            _abi.call("rsr_encode_samples_fp4", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
-                      _abi.ptr(opnd[slot]), width, st)
+            _abi.call("rsr_encode_samples_fp4_ex", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
+                      _abi.ptr(opnd[slot]), width, plane, st)
         else:
             _abi.call("rsr_encode_samples", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
                       _abi.ptr(opnd[slot]), width, st)
-        if fp4:
+        if fp4 and plane:
+            _abi.call("rsr_classify_fp4_planar", _abi.ptr(opnd[slot]), plane, hi - lo, None,
+                      _abi.ptr(bl), nl, al, _abi.ptr(bu), nu, au, width, _abi.ptr(flags[lo:hi]),
+                      None, None, 0, st)
+        elif fp4:
             _abi.call("rsr_classify_fp4_ex", _abi.ptr(opnd[slot]), hi - lo, None, _abi.ptr(bl), nl,
                       al, _abi.ptr(bu), nu, au, width, _abi.ptr(flags[lo:hi]), None, None, 0, st)
         else:
             _abi.call("rsr_classify_tc", _abi.ptr(opnd[slot]), hi - lo, _abi.ptr(bl), nl,
                       _abi.ptr(bu), nu, width, _abi.ptr(flags[lo:hi]), 0, st)
         free[slot].record(comp)
+        lo = hi
     labels = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
     counts_d = torch.empty(4, dtype=torch.int64, device=dev)
     _abi.call("rsr_finalize", _abi.ptr(flags), S, _abi.ptr(labels), _abi.ptr(counts_d), st)
