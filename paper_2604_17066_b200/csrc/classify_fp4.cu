@@ -138,6 +138,8 @@ struct Fp4Params {
   int n_res;        // tiles j < n_res are resident in stage j (loaded once); the others stream
                     // through stages n_res .. stages-1 (n_res = nt_total when resident)
   const int64_t* S_dev;  // optional device sample count (<= S): rows [S_dev, S) are skipped
+  int flag_or;      // flags merged with 32-bit atomic ORs (no FIRST; flags 4-byte aligned,
+                    // zeroed before the first launch unless accumulating)
 };
 
 // SW32 K-major descriptor: 8-row core groups 256 B apart, version 1, layout 6.
@@ -709,15 +711,31 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         PROF_ADD(4, e2 - e1);
         PROF_ADD(5, e3 - e2);
       }
+      PROF_T(x0);
+      const int64_t row = (int64_t)g * 2 * kRowsA + rank * kRowsA + r;
+      if (!FIRST && p.flag_or) {
+        // every set ORs its hit bits straight into the flags (zeroed by the launch when
+        // not accumulating): four rows' bytes per 32-bit red.or from one lane, no
+        // barrier between the sets (the group-end exchange below cost ~4 % at cfg4
+        // K = 10^3: profiles/r2_fp4_epilogue_experiments.txt)
+        const uint32_t mine = row < S_run ? hit << (8 * (lane & 3)) : 0u;
+        uint32_t word = mine | __shfl_xor_sync(0xffffffffu, mine, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        if ((lane & 3) == 0 && word)
+          atomicOr(reinterpret_cast<unsigned int*>(p.flags + row), word);
+      } else {
       // the sets' partial results for the group's rows meet in shared memory; set 0
       // writes the flags.  One barrier per group: the exchange buffers alternate by
       // group parity, so a set may write group g+1's entries while set 0 still reads
       // group g's.
-      PROF_T(x0);
-      const int64_t row = (int64_t)g * 2 * kRowsA + rank * kRowsA + r;
       uint32_t* xh = xchg + gpar * kEpiSets * 128;
       int64_t* xf = xfirst + gpar * kEpiSets * 256;
+#ifdef RSR_FP4_X_NOEXCH
+      // timing experiment only (wrong results): no group-end exchange between the sets
+      if (false) {
+#else
       if constexpr (kEpiSets > 1) {
+#endif
         if (set != 0) {
           xh[set * 128 + r] = hit;
           if (FIRST) {
@@ -750,6 +768,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             }
           }
         }
+      }
       }
       PROF_T(x1);
       PROF_ADD(8, x1 - x0);
@@ -948,6 +967,12 @@ int launch_fp4(const Fp4Call& c) {
   auto kern = want_first ? classify_fp4_pair_kernel<TN, true> : classify_fp4_pair_kernel<TN, false>;
   int clusters = c.sm_count / 2;
   if (p.n_groups < clusters) clusters = p.n_groups;
+  p.flag_or = (!want_first && kEpiSets > 1 && (reinterpret_cast<uintptr_t>(c.flags) & 3) == 0 &&
+               !getenv("RSR_FP4_FLAG_EXCHANGE"))
+                  ? 1
+                  : 0;
+  if (p.flag_or && !c.accumulate)  // the atomic ORs need zeroed flags: S bytes, one memset
+    RSR_CUDA(cudaMemsetAsync(c.flags, 0, (size_t)c.S, c.st));
   // Wide rows (N(M-1) >= 832, e.g. N = 295 at M >= 4) leave no room for a sample
   // buffer holding both halves next to a reference ring: such calls run the lower
   // and the upper tiles as separate one-sided launches (one sample half each,
