@@ -118,9 +118,10 @@ int rsr_sample_fp4(const double* probs, int n_components, int n_states, uint64_t
                    uint8_t* out_fp4, int row_bytes, void* stream);
 
 /* Independent device stream (north_star: "independent device RNG"): the same
- * calls with rng = RSR_RNG_DEVICE draw flat index f = (start+i)*N + n from word
- * f%4 of Philox4x32-10 block f/4 (counter [f/4 lo, f/4 hi, gen lo, gen hi], key
- * [seed lo, seed hi]); state = #{m < M-1 : raw32 >= ceil(cum_m * 2^32)}.
+ * calls with rng = RSR_RNG_DEVICE draw (row R = start+i, component n) from word n%4
+ * of the Philox4x32-10 block with counter [n/4, R lo, R hi, gen lo] and key
+ * [seed lo ^ gen hi, seed hi] (row-aligned blocks); state = #{m < M-1 : raw32 >=
+ * ceil(cum_m * 2^32)}.
  * rng = RSR_RNG_SHARED is rsr_sample / rsr_sample_fp4.  rsr_sample_fp4_ex also takes
  * the FP4 operand layout: fp4_plane_stride = 0 writes interleaved rows [A_up | A_lo]
  * (2*row_bytes per row); > 0 writes planar A_up rows of row_bytes and the A_lo plane
@@ -133,9 +134,10 @@ int rsr_sample_fp4_ex(const double* probs, int n_components, int n_states, uint6
                       uint64_t gen, int64_t start, int64_t count, uint8_t* out_states,
                       uint8_t* out_fp4, int row_bytes, int64_t fp4_plane_stride, int rng,
                       void* stream);
-/* Raw 32-bit words first..first+count-1 of the device stream (seed, gen). */
-int rsr_device_raw(uint64_t seed, uint64_t gen, int64_t first, int64_t count, uint32_t* out,
-                   void* stream);
+/* Raw 32-bit draws of rows start..start+count-1 of the device stream (seed, gen) for
+ * n_components components: out[i * n_components + n]. */
+int rsr_device_raw(uint64_t seed, uint64_t gen, int64_t start, int64_t count, int n_components,
+                   uint32_t* out, void* stream);
 
 /* ---- (2) encodings: encoding.py:138-153 encode_batch ---------------------- */
 int rsr_encode_samples(const uint8_t* states, int64_t count, int n_components,

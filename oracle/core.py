@@ -39,7 +39,7 @@ def sample_states(probs: np.ndarray, n_samples: int, seed: int, generation_index
     ``np.searchsorted(cum[n], u, side="right")`` for the non-decreasing cum.
     ``fast`` uses numpy's own Philox as the reference does (timing runs).
     ``rng="device"``: the independent device stream (not in the reference), u =
-    raw32 * 2^-32 from Philox4x32-10 (philox.device_raw), same inverse CDF.
+    raw32 * 2^-32 from row-aligned Philox4x32-10 (philox.device_raw), same inverse CDF.
     """
     if n_samples < 1:
         raise ValueError("n_samples must be >= 1")
@@ -47,8 +47,7 @@ def sample_states(probs: np.ndarray, n_samples: int, seed: int, generation_index
     n, m = probs.shape
     if rng == "device":
         from .philox import device_raw
-        u = (device_raw(seed, generation_index, start * n, n_samples * n).astype(np.float64)
-             * 2.0 ** -32).reshape(n_samples, n)
+        u = device_raw(seed, generation_index, start, n_samples, n).astype(np.float64) * 2.0 ** -32
     elif rng == "shared":
         u = uniform_field(seed, generation_index, start, n_samples, n, fast=fast)
     else:

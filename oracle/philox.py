@@ -128,17 +128,19 @@ def philox4x32_blocks(c0, c1, c2, c3, k0: int, k1: int) -> np.ndarray:
     return np.stack([c0, c1, c2, c3], axis=-1).astype(np.uint32)
 
 
-def device_raw(seed: int, generation_index: int, first: int, count: int) -> np.ndarray:
-    """uint32 words first..first+count-1 of the device stream (seed, gen): flat word f is
-    word f % 4 of block b = f // 4, counter [b lo, b hi, gen lo, gen hi], key [seed lo,
-    seed hi]."""
+def device_raw(seed: int, generation_index: int, start: int, count: int,
+               n_components: int) -> np.ndarray:
+    """uint32 draws [count, n_components] of rows start..start+count-1 of the device
+    stream (seed, gen): draw (row R, component n) is word n % 4 of the block with
+    counter [n // 4, R lo, R hi, gen lo] and key [seed lo ^ gen hi, seed hi]
+    (include/rsr_b200.h, csrc/philox.cuh device_row_block)."""
     if count <= 0:
-        return np.zeros(0, dtype=np.uint32)
+        return np.zeros((0, n_components), dtype=np.uint32)
     mask = (1 << 64) - 1
     seed, gen = seed & mask, generation_index & mask
-    b_lo, b_hi = first // 4, (first + count - 1) // 4
-    b = np.arange(b_lo, b_hi + 1, dtype=np.uint64)
-    blocks = philox4x32_blocks(b & _M32, b >> np.uint64(32), gen & 0xFFFFFFFF, gen >> 32,
-                               seed & 0xFFFFFFFF, seed >> 32)
-    off = first - 4 * b_lo
-    return blocks.reshape(-1)[off:off + count]
+    qb = (n_components + 3) // 4
+    rows = np.arange(start, start + count, dtype=np.uint64)[:, None]
+    q = np.arange(qb, dtype=np.uint64)[None, :]
+    blocks = philox4x32_blocks(q, rows & _M32, rows >> np.uint64(32), gen & 0xFFFFFFFF,
+                               (seed & 0xFFFFFFFF) ^ (gen >> 32), seed >> 32)
+    return blocks.reshape(count, 4 * qb)[:, :n_components]

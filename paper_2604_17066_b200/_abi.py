@@ -82,7 +82,7 @@ EXPORTED = {
     "rsr_sample_fp4": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _P]),
     "rsr_sample_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I, _P]),
     "rsr_sample_fp4_ex": (_I, [_P, _I, _I, _U64, _U64, _I64, _I64, _P, _P, _I, _I64, _I, _P]),
-    "rsr_device_raw": (_I, [_U64, _U64, _I64, _I64, _P, _P]),
+    "rsr_device_raw": (_I, [_U64, _U64, _I64, _I64, _I, _P, _P]),
     "rsr_comm_unique_id": (_I, [_P]),
     "rsr_comm_init": (_I, [_P, _I, _I, _P]),
     "rsr_comm_destroy": (_I, [_P]),

@@ -57,14 +57,36 @@ sample_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uin
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nblk) return;
   const int64_t b = b_lo + t;
-  unsigned long long rr[4];
-  rsr::draw_block<RNG, false>(b, seed, gen, rr);
   const uint64_t fb = 4ull * (uint64_t)b;
   uint64_t row = __umul64hi(fb, magic);
   int n = (int)(fb - row * (uint64_t)N);
   if (n >= N) {
     n -= N;
     ++row;
+  }
+  unsigned long long rr[4];
+  if (RNG == 0) {
+    rsr::draw_block<false>(b, seed, gen, rr);
+  } else {
+    // device stream: draw (row, n) from that row's block n / 4 (rows are block-aligned,
+    // so the four flat draws may come from two blocks)
+    uint64_t r = row;
+    int nn = n;
+    uint32_t w[4];
+    int q = -1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if ((nn >> 2) != q) {
+        q = nn >> 2;
+        rsr::device_row_block(r, (uint32_t)q, seed, gen, w);
+      }
+      rr[j] = (unsigned long long)w[nn & 3] << 21;
+      if (++nn == N) {
+        nn = 0;
+        ++r;
+        q = -1;
+      }
+    }
   }
   uint8_t st[4];
   int ns[4];
@@ -205,7 +227,7 @@ __device__ __forceinline__ void fp4_quad_fast(const uint8_t* st, uint32_t base, 
 // C32: every Philox counter of the launch fits 32 bits (flat draws < 2^34), so
 // the first round's 64x64 multiply is a 64x32 one (two IMAD.WIDE fewer per block
 // on the FMA pipe, which bounds this kernel).
-template <int MT, bool C32, int RNG>  // MT 2, 3: specialised state count; 0: any M
+template <int MT, bool C32>  // MT 2, 3: specialised state count; 0: any M
 __global__ void __launch_bounds__(kRowThreads, RSR_SAMPLE_MINB)
 sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
                    int64_t start_row, int64_t count, uint8_t* __restrict__ states,
@@ -236,7 +258,7 @@ sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed
     const int ostep = 4 * (int)blockDim.x, nstep = ostep % N;
     for (int64_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x, o0 += ostep) {
       unsigned long long rr[4];
-      rsr::draw_block<RNG, C32>(b, seed, gen, rr);
+      rsr::draw_block<C32>(b, seed, gen, rr);
       const unsigned long long* Tn = T + n0 * Mm1;
       n0 += nstep;
       if (n0 >= N) n0 -= N;
@@ -321,19 +343,185 @@ __global__ void philox_raw_kernel(uint64_t seed, uint64_t gen, int64_t first, in
   }
 }
 
-__global__ void device_raw_kernel(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
-                                  int64_t b_lo, int64_t nblk, uint32_t* __restrict__ out) {
+// Raw draws of rows [start, start + count) of the device stream, one thread per block.
+__global__ void device_raw_kernel(uint64_t seed, uint64_t gen, int64_t start, int64_t count,
+                                  int N, uint32_t* __restrict__ out) {
+  const int qb = (N + 3) / 4;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nblk) return;
-  const int64_t b = b_lo + t;
+  if (t >= count * qb) return;
+  const int64_t i = t / qb;
+  const int q = (int)(t - i * qb);
   uint32_t w[4];
-  rsr::device_block((uint64_t)b, seed, gen, w);
+  rsr::device_row_block((uint64_t)(start + i), (uint32_t)q, seed, gen, w);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int64_t f = 4 * b + j;
-    if (f >= first && f < first + count) out[f - first] = w[j];
+  for (int j = 0; j < 4; ++j)
+    if (4 * q + j < N) out[i * N + 4 * q + j] = w[j];
+}
+
+// Row-aligned sampler of the device stream with the FP4 operand fused.  Thread
+// (rr, w) of a CTA owns FP4 word w (columns 8w .. 8w+7 of both halves) of rows
+// rr, rr + R, rr + 2R, ... of the CTA's row chunk, and the states of the components
+// those columns belong to -- M = 2: components 8w .. 8w+7 (two Philox blocks), M = 3:
+// 4w .. 4w+3 (one block), other M generic.  Each thread derives its 8 column
+// thresholds once, into registers: no shared memory, no barriers, no per-item division
+// (the flat-indexed reference stream needs shared-memory staging of its draws).
+//
+// Column c = n (M-1) + k - 1 of the operand is [x_n >= k] in the lower half and its
+// complement in the upper one, and x_n >= k <=> raw32_n >= T32 = ceil(cum_{n,k-1} 2^32)
+// (T53 = ceil(cum 2^53) from the sampler's sequential fp64 cumsum, T32 = ceil(T53 / 2^21)).
+// A threshold of 2^32 is out of 32-bit range; such a column never counts (its value v
+// is 0), which also covers the columns past kdim.
+__device__ __forceinline__ void column_threshold(const double* __restrict__ probs, int M, int Mm1,
+                                                 int c, uint32_t& t, bool& valid) {
+  const int n = c / Mm1, m = c - n * Mm1;
+  double cum = 0.0;
+  for (int i = 0; i <= m; ++i) cum = __dadd_rn(cum, probs[(int64_t)n * M + i]);
+  const unsigned long long t53 = (unsigned long long)ceil(__dmul_rn(cum, 9007199254740992.0));
+  const unsigned long long t32 = (t53 + ((1ull << 21) - 1)) >> 21;
+  valid = !(t32 >> 32);
+  t = valid ? (uint32_t)t32 : ~0u;
+}
+
+template <int MT>
+__global__ void __launch_bounds__(1024) sample_dev_rows_kernel(
+    const double* __restrict__ probs, int N, int M, const rsr::Philox32Keys K, uint64_t gen,
+    int64_t start, int64_t count, uint8_t* __restrict__ states, uint8_t* __restrict__ fp4,
+    int words, int R, int passes, int64_t row_stride, int64_t plane) {
+  // state rows of a pass, staged (double-buffered) so they leave as aligned 16-byte
+  // stores: rows of N bytes are not word aligned, and a lane's 8 state bytes would
+  // otherwise need up to four differently sized stores
+  extern __shared__ __align__(16) uint8_t stage[];
+  const int stage_bytes = (R * N + 16 + 15) & ~15;
+  const int w = threadIdx.x % words, rr = threadIdx.x / words;
+  const bool lane_on = rr < R;
+  const int Mm1 = MT ? MT - 1 : M - 1;
+  const int kdim = N * Mm1;
+  // per-thread column constants
+  uint32_t T[8], v[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int c = 8 * w + s;
+    T[s] = ~0u;
+    v[s] = 0;
+    if (lane_on && c < kdim) {
+      bool ok;
+      column_threshold(probs, M, Mm1, c, T[s], ok);
+      if (ok) v[s] = MT == 2 ? 1u << (8 * (s & 3)) : MT == 3 ? 1u << (8 * (s >> 1)) : 2u << (4 * s);
+    }
+  }
+  const int rem = kdim - 8 * w;  // columns of this word below kdim
+  const uint32_t flip = rem >= 8 ? 0x22222222u : rem > 0 ? (0x22222222u & ((1u << (4 * rem)) - 1u)) : 0u;
+  const uint32_t bias = rem >= 0 && rem < 8 ? 2u << (4 * rem) : 0u;
+  const bool has_cols = lane_on && rem > 0;
+  const int nst = MT == 2 ? min(8, N - 8 * w) : MT == 3 ? min(4, N - 4 * w) : 0;
+  const int64_t c0 = (int64_t)blockIdx.x * R * passes;  // first row of this CTA
+  const int64_t left = (count - c0 + R - 1) / R;
+  const int np = left < passes ? (int)left : passes;
+  for (int p = 0; p < np; ++p) {
+    const int64_t pr = c0 + (int64_t)p * R;  // first row of the pass
+    const int prows = count - pr < R ? (int)(count - pr) : R;
+    const int64_t li = pr + rr;
+    uint8_t* buf = stage + (p & 1) * stage_bytes;
+    const int sb = states ? (int)(reinterpret_cast<uintptr_t>(states + pr * N) & 15u) : 0;
+    uint8_t* srow = buf + sb + rr * N;
+    const uint64_t row = (uint64_t)(start + li);
+    uint32_t lo = 0;
+    if (has_cols && rr < prows) {
+      if (MT == 2) {
+        uint32_t d[8];
+        rsr::device_row_block(row, (uint32_t)(2 * w), gen, K, d);
+        if (8 * w + 4 < N) rsr::device_row_block(row, (uint32_t)(2 * w + 1), gen, K, d + 4);
+        uint32_t s0 = 0, s1 = 0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          s0 += d[s] >= T[s] ? v[s] : 0u;
+          s1 += d[s + 4] >= T[s + 4] ? v[s + 4] : 0u;
+        }
+        // state bytes (0/1) -> nibbles at bit 4j + 1 (cf. fp4_quad_fast)
+        lo = __byte_perm(s0 | (s0 >> 4), s1 | (s1 >> 4), 0x6420) << 1;
+        if (states) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < nst) srow[8 * w + j] = (uint8_t)((j < 4 ? s0 : s1) >> (8 * (j & 3)));
+        }
+      } else if (MT == 3) {
+        uint32_t d[4];
+        rsr::device_row_block(row, (uint32_t)w, gen, K, d);
+        uint32_t s0 = 0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) s0 += d[s >> 1] >= T[s] ? v[s] : 0u;
+        const uint32_t sel = (s0 & 0xFu) | ((s0 >> 4) & 0xF0u) | ((s0 >> 8) & 0xF00u) |
+                             ((s0 >> 12) & 0xF000u);
+        lo = __byte_perm(0x00220200u, 0u, sel);  // x = 0, 1, 2 -> 0x00, 0x02, 0x22
+        if (states) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < nst) srow[4 * w + j] = (uint8_t)(s0 >> (8 * j));
+        }
+      } else {
+        uint32_t d[4];
+        int q = -1;
+        for (int s = 0; s < 8; ++s) {
+          const int n = (8 * w + s) / Mm1;
+          if (n >= N) break;
+          if ((n >> 2) != q) {
+            q = n >> 2;
+            rsr::device_row_block(row, (uint32_t)q, gen, K, d);
+          }
+          lo |= d[n & 3] >= T[s] ? v[s] : 0u;
+        }
+        if (states) {
+          // component n is written by the word holding its first column; x_n counts its
+          // columns set (columns in later words are compared here directly)
+          for (int s = 0; s < 8; ++s) {
+            const int c = 8 * w + s;
+            if (c >= kdim) break;
+            if (c % Mm1) continue;
+            const int n = c / Mm1;
+            uint32_t dd[4];
+            rsr::device_row_block(row, (uint32_t)(n >> 2), gen, K, dd);
+            int x = 0;
+            for (int k = 0; k < Mm1; ++k) {
+              const int cc = c + k;
+              if ((cc >> 3) == w) {
+                x += (lo >> (4 * (cc & 7) + 1)) & 1u;
+              } else {
+                uint32_t t;
+                bool ok;
+                column_threshold(probs, M, Mm1, cc, t, ok);
+                x += ok && dd[n & 3] >= t;
+              }
+            }
+            srow[n] = (uint8_t)x;
+          }
+        }
+      }
+    }
+    if (fp4 && lane_on && rr < prows) {
+      lo |= bias;
+      uint8_t* prow = fp4 + li * row_stride;
+      reinterpret_cast<uint32_t*>(prow)[w] = lo ^ flip;
+      reinterpret_cast<uint32_t*>(prow + plane)[w] = lo;
+    }
+    if (states) {
+      __syncthreads();  // the pass's rows are staged (the other buffer is free again)
+      // buf[sb + i] = global byte pr * N + i, with the same alignment mod 16
+      uint8_t* g = states + pr * N;
+      const int L = prows * N;
+      const int head = min(L, (16 - sb) & 15);
+      const int nvec = (L - head) >> 4;
+      for (int i = threadIdx.x; i < nvec; i += blockDim.x)
+        reinterpret_cast<uint4*>(g + head)[i] = reinterpret_cast<const uint4*>(buf + sb + head)[i];
+      const int tail0 = head + (nvec << 4);
+      const int t = threadIdx.x;
+      if (t < head) g[t] = buf[sb + t];
+      else if (t < head + (L - tail0)) g[tail0 + t - head] = buf[sb + tail0 + t - head];
+    }
   }
 }
+
+
+
 
 __global__ void uniform_kernel(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
                                int64_t b_lo, int64_t nblk, double* __restrict__ out) {
@@ -471,14 +659,14 @@ extern "C" int rsr_philox_raw(uint64_t seed, uint64_t gen, int64_t first, int64_
   return rsr::check_launch("philox_raw_kernel");
 }
 
-extern "C" int rsr_device_raw(uint64_t seed, uint64_t gen, int64_t first, int64_t count,
-                              uint32_t* out, void* stream) {
-  RSR_REQUIRE(first >= 0 && count >= 0, "rsr_device_raw: negative range");
+extern "C" int rsr_device_raw(uint64_t seed, uint64_t gen, int64_t start, int64_t count,
+                              int n_components, uint32_t* out, void* stream) {
+  RSR_REQUIRE(start >= 0 && count >= 0 && n_components >= 1, "rsr_device_raw: bad shape");
   if (count == 0) return RSR_OK;
   RSR_REQUIRE(out != nullptr, "rsr_device_raw: null output");
-  const int64_t b_lo = first / 4, b_hi = (first + count - 1) / 4, nblk = b_hi - b_lo + 1;
-  device_raw_kernel<<<(unsigned)rsr::ceil_div(nblk, kThreads), kThreads, 0,
-                      rsr::as_stream(stream)>>>(seed, gen, first, count, b_lo, nblk, out);
+  const int64_t total = count * ((n_components + 3) / 4);
+  device_raw_kernel<<<(unsigned)rsr::ceil_div(total, kThreads), kThreads, 0,
+                      rsr::as_stream(stream)>>>(seed, gen, start, count, n_components, out);
   return rsr::check_launch("device_raw_kernel");
 }
 
@@ -560,15 +748,56 @@ extern "C" int rsr_encode_refs(const uint8_t* states, int64_t count, int64_t row
 }
 
 namespace {
-template <int RNG>
 const void* rows_kernel(int M, bool c32) {
   if (c32)
-    return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, true, RNG>)
-           : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, true, RNG>)
-                    : reinterpret_cast<const void*>(sample_rows_kernel<0, true, RNG>);
-  return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, false, RNG>)
-         : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, false, RNG>)
-                  : reinterpret_cast<const void*>(sample_rows_kernel<0, false, RNG>);
+    return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, true>)
+           : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, true>)
+                    : reinterpret_cast<const void*>(sample_rows_kernel<0, true>);
+  return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, false>)
+         : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, false>)
+                  : reinterpret_cast<const void*>(sample_rows_kernel<0, false>);
+}
+
+int launch_dev_rows(const double* probs, int N, int M, uint64_t seed, uint64_t gen, int64_t start,
+                    int64_t count, uint8_t* states, uint8_t* fp4, int row_bytes,
+                    int64_t row_stride, int64_t plane, cudaStream_t st) {
+  const void* kern = M == 2   ? reinterpret_cast<const void*>(sample_dev_rows_kernel<2>)
+                     : M == 3 ? reinterpret_cast<const void*>(sample_dev_rows_kernel<3>)
+                              : reinterpret_cast<const void*>(sample_dev_rows_kernel<0>);
+  // FP4 words per row (both halves share them): all row_bytes / 4 when the operand is
+  // written (padding words are zero), else just those holding components
+  int words = fp4 ? row_bytes / 4 : (N * (M - 1) + 7) / 8;
+  RSR_REQUIRE(words <= 1024, "rsr_sample_fp4: N*(M-1) too large for the device-stream sampler");
+  // R rows per pass: the thread count words * R rounded up to whole warps wastes the
+  // fewest lanes (ties: the larger CTA up to 512 threads)
+  // (measured, N = 295: 160-thread CTAs beat 480-thread ones by 15-30%)
+  int R = 1;
+  double best = -1e9;
+  for (int r = 1; r * words <= 1024; ++r) {
+    const int th = (r * words + 31) / 32 * 32;
+    const double score = (double)(r * words) / th - 0.0005 * th - (th < 128 ? 0.2 : 0.0);
+    if (score > best) {
+      best = score;
+      R = r;
+    }
+  }
+  const int threads = (R * words + 31) / 32 * 32;
+  // ~128 rows per CTA: short-lived CTAs (the loop's low-priority prefetch must not hold
+  // SMs for long), each deriving its column constants once
+  const int passes = std::max(1, 128 / R);
+  const int64_t grid = rsr::ceil_div(count, (int64_t)R * passes);
+  const rsr::Philox32Keys keys = rsr::device_keys(seed, gen);
+  void* args[] = {(void*)&probs, (void*)&N,      (void*)&M,     (void*)&keys,
+                  (void*)&gen,   (void*)&start,  (void*)&count, (void*)&states,
+                  (void*)&fp4,   (void*)&words,  (void*)&R,     (void*)&passes,
+                  (void*)&row_stride, (void*)&plane};
+  const size_t smem = states ? 2 * (size_t)((R * N + 16 + 15) & ~15) : 0;
+  if (smem > 48 * 1024) {
+    const int rc = rsr::ensure_dynamic_smem(kern, smem);
+    if (rc) return rc;
+  }
+  RSR_CUDA(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), args, smem, st));
+  return rsr::check_launch("sample_dev_rows_kernel");
 }
 }  // namespace
 
@@ -602,10 +831,11 @@ extern "C" int rsr_sample_fp4_ex(const double* probs, int n_components, int n_st
   const size_t smem = ((size_t)(N + kTExtra) * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 +
                       2 * (size_t)st_bytes;
   RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample_fp4: N*(M-1) too large for shared memory");
-  // the device stream's counter is 64-bit anyway (two 32-bit words)
-  const bool c32 = rng == RSR_RNG_SHARED &&
-                   ((start + count) * (int64_t)N + 3) / 4 + 1 < ((int64_t)1 << 32);
-  const void* kern = rng == RSR_RNG_DEVICE ? rows_kernel<1>(M, false) : rows_kernel<0>(M, c32);
+  if (rng == RSR_RNG_DEVICE)
+    return launch_dev_rows(probs, N, M, seed, gen, start, count, out_states, out_fp4, row_bytes,
+                           fp4_row_stride, fp4_plane, rsr::as_stream(stream));
+  const bool c32 = ((start + count) * (int64_t)N + 3) / 4 + 1 < ((int64_t)1 << 32);
+  const void* kern = rows_kernel(M, c32);
   if (smem > 48 * 1024) {
     const int rc = rsr::ensure_dynamic_smem(kern, smem);
     if (rc) return rc;

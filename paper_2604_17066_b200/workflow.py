@@ -424,8 +424,6 @@ class _LeanPrefetcher:
         self.n, self.m, self.seed, self.start, self.count = n, m, seed, start, count
         self.rb = _abi.fp4_row_bytes(n, m)
         self.probs = _abi.ptr(dist_.device_probs())
-        self.states = [torch.empty((max(count, 1), n), dtype=torch.uint8, device=dev)
-                       for _ in range(2)]
         self.fp4 = [torch.empty((max(count, 1), 2 * self.rb), dtype=torch.uint8, device=dev)
                     for _ in range(2)]
         self.stream = torch.cuda.Stream()
@@ -435,7 +433,6 @@ class _LeanPrefetcher:
         self.free_used = [False, False]
         self.cache = cache
         self.src = list(self.fp4)        # FP4 operand of the batch in each slot
-        self.has_states = [True, True]   # u8 state rows in self.states[slot]
 
     def launch(self, gen: int) -> int:
         slot = gen & 1
@@ -443,15 +440,17 @@ class _LeanPrefetcher:
             self.stream.wait_event(self.free[slot])
         cached = self.cache.get(gen) if self.cache is not None else None
         if cached is not None:
-            self.src[slot], self.has_states[slot] = cached, False
+            self.src[slot] = cached
         else:
             dst = self.cache.reserve(gen) if self.cache is not None else None
             dst = self.fp4[slot] if dst is None else dst
             mask = (1 << 64) - 1
+            # FP4 operand only: the picks are decoded from its rows (rsr_gather_picks_fp4),
+            # so the u8 state rows are not written at all
             _abi.call("rsr_sample_fp4_ex", self.probs, self.n, self.m, self.seed & mask,
-                      gen & mask, self.start, self.count, _abi.ptr(self.states[slot]),
-                      _abi.ptr(dst), self.rb, 0, self.rng, self.sptr)
-            self.src[slot], self.has_states[slot] = dst, True
+                      gen & mask, self.start, self.count, None, _abi.ptr(dst), self.rb, 0,
+                      self.rng, self.sptr)
+            self.src[slot] = dst
         self.ready[slot].record(self.stream)
         return slot
 
@@ -580,12 +579,8 @@ def _stage1_loop_async(model, dist, config, threshold, comm, phi, lower, upper, 
 
     def gather_rows_at(slot, pos_dev, n, out, sp):
         """out[j] = state row of local unclassified position pos_dev[j] (idx compacted)."""
-        if pre.has_states[slot]:
-            _abi.call("rsr_gather_picks", _abi.ptr(pre.states[slot]), N, _abi.ptr(idx),
-                      _abi.ptr(pos_dev), n, _abi.ptr(out), sp)
-        else:
-            _abi.call("rsr_gather_picks_fp4", _abi.ptr(pre.src[slot]), rb, N, M, _abi.ptr(idx),
-                      _abi.ptr(pos_dev), n, _abi.ptr(out), sp)
+        _abi.call("rsr_gather_picks_fp4", _abi.ptr(pre.src[slot]), rb, N, M, _abi.ptr(idx),
+                  _abi.ptr(pos_dev), n, _abi.ptr(out), sp)
 
     def gather_local(slot, n_local, out):
         """Rows of this rank's picks (local positions in pos_h) -> out[:n_local]."""

@@ -31,18 +31,21 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from _specs import device_model, oracle_phi  # noqa: E402
 
 
-@pytest.mark.parametrize("seed,gen,first,count", [(0, 0, 0, 1), (7, 3, 1, 4099),
-                                                  ((1 << 63) + 5, (1 << 40) + 1, 1 << 34, 1023)])
-def test_device_raw_matches_oracle(seed, gen, first, count):
-    out = torch.empty(count, dtype=torch.int32, device="cuda")
-    _abi.call("rsr_device_raw", seed, gen, first, count, _abi.ptr(out), _abi.stream_ptr())
-    got = out.cpu().numpy().view(np.uint32)
+@pytest.mark.parametrize("seed,gen,start,count,n", [(0, 0, 0, 1, 4), (7, 3, 1, 4099, 295),
+                                                     ((1 << 63) + 5, (1 << 40) + 1, 1 << 34, 1023,
+                                                      7)])
+def test_device_raw_matches_oracle(seed, gen, start, count, n):
+    out = torch.empty(count * n, dtype=torch.int32, device="cuda")
+    _abi.call("rsr_device_raw", seed, gen, start, count, n, _abi.ptr(out), _abi.stream_ptr())
+    got = out.cpu().numpy().view(np.uint32).reshape(count, n)
     from oracle.philox import device_raw
-    assert np.array_equal(got, device_raw(seed, gen, first, count))
+    assert np.array_equal(got, device_raw(seed, gen, start, count, n))
 
 
 @pytest.mark.parametrize("n,m,h,start", [(295, 2, 4099, 0), (295, 3, 2000, 12345),
-                                         (40, 5, 3000, 1 << 20), (7, 2, 777, 3)])
+                                         (40, 5, 3000, 1 << 20), (7, 2, 777, 3),
+                                         (8, 2, 130, 0), (64, 3, 200, 9), (3, 4, 65, 1),
+                                         (100, 2, 1, (1 << 32) + 3)])
 @pytest.mark.parametrize("fp4", [True, False])
 def test_device_stream_samples_match_oracle(n, m, h, start, fp4):
     rng = np.random.default_rng(n * m + h)

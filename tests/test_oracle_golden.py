@@ -151,16 +151,21 @@ def test_device_stream_philox4x32_known_answers():
             (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1))]
     for args, want in kat:
         assert tuple(int(v) for v in philox4x32_blocks(*args)) == want
-    # stream layout: word f of (seed, gen) is word f % 4 of block f // 4, counter
-    # [b lo, b hi, gen lo, gen hi], key [seed lo, seed hi]
+    # stream layout: draw (row R, component n) of (seed, gen) is word n % 4 of the block
+    # with counter [n // 4, R lo, R hi, gen lo], key [seed lo ^ gen hi, seed hi]
     seed, gen = (1 << 63) + 12345, (1 << 40) + 7
-    b = (1 << 33) + 5
-    blk = philox4x32_blocks(b & f, b >> 32, gen & f, gen >> 32, seed & f, seed >> 32)
-    assert np.array_equal(device_raw(seed, gen, 4 * b + 1, 3), blk[1:])
+    row, q = (1 << 33) + 5, 3
+    blk = philox4x32_blocks(q, row & f, row >> 32, gen & f, (seed & f) ^ (gen >> 32), seed >> 32)
+    got = device_raw(seed, gen, row - 1, 2, 14)
+    assert got.shape == (2, 14) and np.array_equal(got[1, 12:], blk[:2])
+    # rows are whole blocks: row R's draws do not depend on N beyond truncation
+    assert np.array_equal(device_raw(seed, gen, row, 1, 9)[0], device_raw(seed, gen, row, 1, 14)[0, :9])
+    # the generation's high word feeds the key, so gen and gen + 2^32 differ
+    assert not np.array_equal(device_raw(1, 5, 0, 1, 8), device_raw(1, 5 + (1 << 32), 0, 1, 8))
     # inverse CDF at 2^-32 resolution on the same fp64 cumsum
     probs = np.array([[0.25, 0.5, 0.25], [0.1, 0.0, 0.9]])
     xs = oracle.sample_states(probs, 1000, 3, 2, 17, rng="device")
-    raw = device_raw(3, 2, 17 * 2, 2000).reshape(1000, 2).astype(np.float64)
+    raw = device_raw(3, 2, 17, 1000, 2).astype(np.float64)
     cum = np.cumsum(probs, axis=1)
     want = np.minimum((raw[:, :, None] >= np.ceil(cum * 2.0 ** 32)[None]).sum(2), 2)
     assert np.array_equal(xs, want)

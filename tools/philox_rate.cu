@@ -2,7 +2,9 @@
 // 1.37 ms per 2^20 x 295 draws) to the cost of the bit-exact generator alone?
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/philox_rate tools/philox_rate.cu
 // Variants: (0) compiler __umul64hi, (1) explicit 32-bit mad chains (PTX
-// mad.lo/hi.cc), (2) (0) plus the M=2 threshold compare into shared memory.
+// mad.lo/hi.cc), (2) (0) plus the M=2 threshold compare into shared memory,
+// (3) four independent 32x32->64 products, (4) the independent device stream's
+// Philox4x32-10 (same number of draws).
 #include <cstdio>
 #include <cstdint>
 
@@ -104,7 +106,11 @@ __global__ void __launch_bounds__(256) probe(int64_t nblk, uint64_t seed, uint64
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblk;
        b += (int64_t)gridDim.x * blockDim.x) {
     uint64_t w[4];
-    if (V == 1)
+    if (V == 4) {  // the independent device stream (Philox4x32-10): 4 x 32-bit draws
+      uint32_t u[4];
+      rsr::device_row_block((uint64_t)b / 74, (uint32_t)(b % 74), seed, gen, u);
+      w[0] = u[0]; w[1] = u[1]; w[2] = u[2]; w[3] = u[3];
+    } else if (V == 1)
       philox_ptx<false>((uint64_t)b + 1, seed, gen, w);
     else if (V == 3)
       philox_ptx<true>((uint64_t)b + 1, seed, gen, w);
@@ -153,10 +159,14 @@ int main() {
     for (int i = 0; i < sms * 4 * 256; ++i) bad += h0[i] != h3[i];
     printf("variant 3 mismatches vs variant 0: %d\n", bad);
   }
-  for (int v = 0; v < 4; ++v) {
+  for (int v = 0; v < 5; ++v) {
     for (int ctas_per_sm : {4, 8}) {
       const int grid = sms * ctas_per_sm;
-      auto k = v == 0 ? probe<0> : v == 1 ? probe<1> : v == 2 ? probe<2> : probe<3>;
+      auto k = v == 0   ? probe<0>
+               : v == 1 ? probe<1>
+               : v == 2 ? probe<2>
+               : v == 3 ? probe<3>
+                        : probe<4>;
       k<<<grid, 256>>>(nblk, 123, 4, out, T);
       cudaEventRecord(e0);
       for (int r = 0; r < 10; ++r) k<<<grid, 256>>>(nblk, 123, 4, out, T);
