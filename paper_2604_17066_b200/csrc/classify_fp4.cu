@@ -76,6 +76,12 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 #ifndef RSR_FP4_EPI_SPIN
 #define RSR_FP4_EPI_SPIN 0
 #endif
+// 1: every set takes every tile, set e reading columns [e TN/kEpiSets, (e+1) TN/kEpiSets)
+// (the tile's TMEM load is kEpiSets x shorter, so the buffer returns to the MMA warp
+// sooner); 0: sets take turns by tile, each reading whole tiles
+#ifndef RSR_FP4_SPLIT_COLS
+#define RSR_FP4_SPLIT_COLS 0
+#endif
 constexpr int kEpiSets = RSR_FP4_EPI_SETS;
 static_assert(kEpiSets == 1 || kEpiSets == 2 || kEpiSets == 4, "epilogue sets: 1, 2 or 4");
 constexpr int kEpiWarps = 4 * kEpiSets;
@@ -248,12 +254,12 @@ __device__ __forceinline__ void ld_cols_packed(uint32_t taddr, uint32_t* v) {
 // first column.  Load, release the buffer (as early as possible: the MMA warp
 // waits on it), then mask columns past the side's last reference, min-reduce
 // the 16-bit halves and find the first zero column.
-template <int TN, bool FIRST>
+template <int HC, bool FIRST>
 __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_bar, int lane,
                                               int c0, int64_t valid, bool& any, int& zref,
                                               long long& t_loaded, long long* ts_release,
                                               int set_id) {
-  constexpr int kCols = Tile<TN>::kCols;
+  constexpr int kCols = HC;  // columns this warp reads, starting at tile column c0
   constexpr int R = kCols / 2;
   uint32_t v[R];
   ld_cols_packed<kCols>(taddr, v);
@@ -494,7 +500,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     for (int i = 0; i < kBufs; ++i) {
       mbar_init(smem_addr(&t_full[i]), 1);
       // the 4 warps of the tile's epilogue set in both CTAs (or one arrival per CTA)
-      mbar_init(smem_addr(&t_empty[i]), RSR_FP4_SET_RELEASE ? 2 : 2 * 4);
+      mbar_init(smem_addr(&t_empty[i]), RSR_FP4_SET_RELEASE ? 2 : RSR_FP4_SPLIT_COLS ? 2 * kEpiWarps : 2 * 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -666,7 +672,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       uint32_t hit = 0;
       int64_t first[2] = {INT64_MAX, INT64_MAX};
       for (int jj = 0; jj < p.nt_total; ++jj, ++T) {
-        if ((int)(T % kEpiSets) != set) continue;
+        if (!RSR_FP4_SPLIT_COLS && (int)(T % kEpiSets) != set) continue;
         const uint32_t buf = T % kBufs, tphase = (T / kBufs) & 1;
         const int j = tile_of(jj);
         const bool low = j < p.nt_lower;
@@ -685,7 +691,9 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         }
 #endif
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN;
+        constexpr int kHC = RSR_FP4_SPLIT_COLS ? kTileN / kEpiSets : kTileN;  // columns per warp
+        const int c0 = RSR_FP4_SPLIT_COLS ? set * kHC : 0;
+        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN + c0;
         const int64_t valid = (low ? p.n_lower : p.n_upper) - t0;
         bool any;
         int zref = 0;
@@ -695,8 +703,8 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
 #else
         long long* tsr = nullptr;
 #endif
-        epilogue_tile<TN, FIRST>(taddr, smem_addr(&t_empty[buf]), lane, 0, valid, any, zref,
-                                 t_loaded, tsr, set);
+        epilogue_tile<kHC, FIRST>(taddr, smem_addr(&t_empty[buf]), lane, c0, valid, any, zref,
+                                  t_loaded, tsr, set);
         PROF_T(e2);
         PROF_ADD(0, t_loaded - e1);
         if (any) {
@@ -862,6 +870,7 @@ struct Fp4Call {
   int accumulate;
   cudaStream_t st;
   int sm_count;
+  int64_t chunk_tiles;  // reference tiles per launch (0: the L2-sized default)
 };
 
 constexpr size_t kMinSmem = 120 * 1024;  // > half of the SM's 228 KB
@@ -982,8 +991,10 @@ int launch_fp4(const Fp4Call& c) {
 
   // Reference chunks: a launch's B slice must stay L2-resident while every
   // group streams it (~123K refs x row_bytes per launch: 20 MB at 160 B).
+  // Sets a little past residency run as consecutive resident-sized launches (see
+  // pick_tile_n: c.chunk_tiles).
   const char* ct = getenv("RSR_TC_CHUNK_TILES");
-  const int64_t chunk = ct ? atoll(ct) : 122880 / TN;
+  const int64_t chunk = ct ? atoll(ct) : c.chunk_tiles > 0 ? c.chunk_tiles : 122880 / TN;
   const int64_t total = nt_l + nt_u;
   bool first_launch = true;
   for (int64_t c0 = 0; c0 < total;) {
@@ -1056,7 +1067,25 @@ bool fp4_feasible(int tn, int64_t nt_l, int64_t nt_u, int cq, bool want_first) {
          (nt_u == 0 || fp4_layout(tn, 0, nt_u, cq, want_first).ring >= 2);
 }
 
-int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
+// Reference tiles one resident launch can hold at width tn (a two-sided call's chunks
+// hold both sides: sized with both sample halves buffered).
+int64_t resident_cap(int tn, bool two_sided, int cq, bool want_first) {
+  int64_t cap = 0;
+  for (int64_t c = 1; c <= 16; ++c) {
+    const Fp4Layout L = two_sided && c >= 2 ? fp4_layout(tn, 1, c - 1, cq, want_first)
+                                             : fp4_layout(tn, 0, c, cq, want_first);
+    if (!L.resident) break;
+    cap = c;
+  }
+  return cap;
+}
+
+struct TilePlan {
+  int tn;
+  int64_t chunk_tiles;  // 0: default (L2-sized chunks, tiles streamed per sample group)
+};
+
+TilePlan pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
   const char* env = getenv("RSR_FP4_TILE_N");
   const int forced = env ? atoi(env) : 0;
   static const int kCand[] = {240, 224, 208, 192, 176, 160};
@@ -1067,16 +1096,24 @@ int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
   // more than keeping it resident (cfg4 K = 2000: 9 resident tiles of 224 take
   // 0.670 ms, 9 streamed tiles of 240 0.891 ms; profiles/r1_tile_n_small_k.txt)
   constexpr int64_t kStreamGroupCost = 2500;
+  // Past residency, the set can instead run as several resident launches, each
+  // re-reading the sample operand: about one tile per sample group per extra launch
+  // (fitted on cfg4 K = 2500 .. 10^4: 0.75 - 1.5 tiles; profiles/r2_fp4_chunked_residency.txt),
+  // so up to four launches beat streaming the tiles through the ring for every group
+  // (K = 3000: 0.78 -> 0.83 of peak, 6000: 0.863 -> 0.879); at 10^4 the two tie.
+  constexpr int64_t kChunkGroupCost = 1000;
+  constexpr int64_t kMaxChunks = 4;
   for (int tn : kCand)
-    if (tn == forced) return tn;
+    if (tn == forced) return {tn, 0};
   // wide rows (>= 12 K-steps, e.g. N = 295 at M >= 4): N = 160 tiles with three
   // accumulator buffers measured 15 % faster than any wider tile (M = 4: 0.895 of
   // peak vs 0.736-0.776; profiles/r2_wide_rows_m2_m5.txt)
   if (cq >= 12 && fp4_feasible(160, rsr::ceil_div(n_lower, 160), rsr::ceil_div(n_upper, 160), cq,
                                want_first))
-    return 160;
-  int best = 160;  // narrowest: the last resort for the widest rows
+    return {160, 0};
+  TilePlan best{160, 0};  // narrowest: the last resort for the widest rows
   int64_t best_cost = INT64_MAX;
+  const bool chunk_ok = !getenv("RSR_FP4_NO_CHUNK_RESIDENT");
   for (int i = 0; i < 6; ++i) {
     const int tn = kCand[i];
     const int64_t nt_l = rsr::ceil_div(n_lower, tn), nt_u = rsr::ceil_div(n_upper, tn);
@@ -1086,7 +1123,19 @@ int pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
     if (!resident) cost += kStreamGroupCost;
     if (cost < best_cost) {
       best_cost = cost;
-      best = tn;
+      best = {tn, 0};
+    }
+    if (resident || !chunk_ok) continue;
+    const int64_t nt = nt_l + nt_u;
+    const int64_t cap = resident_cap(tn, nt_l > 0 && nt_u > 0, cq, want_first);
+    if (cap < 2) continue;
+    const int64_t n_ch = rsr::ceil_div(nt, cap);
+    if (n_ch > kMaxChunks) continue;
+    const int64_t per = rsr::ceil_div(nt, n_ch);
+    const int64_t ccost = nt * kCostResident[i] + (n_ch - 1) * kChunkGroupCost;
+    if (ccost < best_cost) {
+      best_cost = ccost;
+      best = {tn, per};
     }
   }
   return best;
@@ -1144,8 +1193,10 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   int dev = 0;
   RSR_CUDA(cudaGetDevice(&dev));
   RSR_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, dev));
-  switch (pick_tile_n(n_lower, n_upper, row_bytes / kChunk,
-                      first_lower != nullptr || first_upper != nullptr)) {
+  const TilePlan plan = pick_tile_n(n_lower, n_upper, row_bytes / kChunk,
+                                    first_lower != nullptr || first_upper != nullptr);
+  c.chunk_tiles = plan.chunk_tiles;
+  switch (plan.tn) {
     case 224: return launch_fp4<224>(c);
     case 208: return launch_fp4<208>(c);
     case 192: return launch_fp4<192>(c);
