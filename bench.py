@@ -502,9 +502,12 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     stream = _abi.stream_ptr()
     launches = 0
     # reference-chunked launches of the classifier (L2-resident B slices)
-    tiles = {"tc": lambda n: -(-n // 240), "tc8": lambda n: -(-n // 256), "bits": lambda n: 0}[method]
-    per_launch = {"tc": 512, "tc8": 256, "bits": 1}[method]
-    classify_launches = max(1, -(-(tiles(nl) + tiles(nu)) // per_launch))
+    if method == "tc":  # the library's own launch plan (tile width, chunked launches)
+        classify_launches = max(1, _abi.fp4_plan(nl, nu, width)[1])
+    else:
+        tiles = {"tc8": lambda n: -(-n // 256), "bits": lambda n: 0}[method]
+        per_launch = {"tc8": 256, "bits": 1}[method]
+        classify_launches = max(1, -(-(tiles(nl) + tiles(nu)) // per_launch))
 
     def classify_kernel():
         if method == "tc":

@@ -953,6 +953,29 @@ Fp4Layout fp4_layout(int tn, int64_t nt_l, int64_t nt_u, int cq, bool want_first
   return L;
 }
 
+// Reference chunks: a launch's B slice must stay L2-resident while every group streams
+// it (~123K refs x row_bytes per launch: 20 MB at 160 B).  Sets a little past residency
+// run as consecutive resident-sized launches instead (pick_tile_n's chunk_tiles).
+int64_t launch_chunk_tiles(int tn, int64_t plan_chunk) {
+  const char* ct = getenv("RSR_TC_CHUNK_TILES");
+  return ct ? atoll(ct) : plan_chunk > 0 ? plan_chunk : 122880 / tn;
+}
+
+// Wide rows (N(M-1) >= 832, e.g. N = 295 at M >= 4) leave no room for a sample buffer
+// holding both halves next to a reference ring: such calls run the lower and the upper
+// tiles as separate one-sided launches (one sample half each, flags and first matches
+// accumulated), so they stay on the tensor cores.
+bool split_sides_needed(int tn, int64_t nt_l, int64_t nt_u, int cq, bool want_first) {
+  return nt_l > 0 && nt_u > 0 && fp4_layout(tn, nt_l, nt_u, cq, want_first).ring < 2;
+}
+
+// End of the launch chunk starting at tile c0 (a chunk never straddles the side
+// boundary when the sides are split).
+int64_t next_chunk_end(int64_t c0, int64_t chunk, int64_t nt_l, int64_t total, bool split_sides) {
+  const int64_t lim = (split_sides && c0 < nt_l) ? nt_l : total;
+  return c0 + chunk < lim ? c0 + chunk : lim;
+}
+
 template <int TN>
 int launch_fp4(const Fp4Call& c) {
   const bool want_first = c.first[0] != nullptr || c.first[1] != nullptr;
@@ -982,25 +1005,12 @@ int launch_fp4(const Fp4Call& c) {
                   : 0;
   if (p.flag_or && !c.accumulate)  // the atomic ORs need zeroed flags: S bytes, one memset
     RSR_CUDA(cudaMemsetAsync(c.flags, 0, (size_t)c.S, c.st));
-  // Wide rows (N(M-1) >= 832, e.g. N = 295 at M >= 4) leave no room for a sample
-  // buffer holding both halves next to a reference ring: such calls run the lower
-  // and the upper tiles as separate one-sided launches (one sample half each,
-  // flags and first matches accumulated), so they stay on the tensor cores.
-  const bool split_sides =
-      nt_l > 0 && nt_u > 0 && fp4_layout(TN, nt_l, nt_u, cq, want_first).ring < 2;
-
-  // Reference chunks: a launch's B slice must stay L2-resident while every
-  // group streams it (~123K refs x row_bytes per launch: 20 MB at 160 B).
-  // Sets a little past residency run as consecutive resident-sized launches (see
-  // pick_tile_n: c.chunk_tiles).
-  const char* ct = getenv("RSR_TC_CHUNK_TILES");
-  const int64_t chunk = ct ? atoll(ct) : c.chunk_tiles > 0 ? c.chunk_tiles : 122880 / TN;
+  const int64_t chunk = launch_chunk_tiles(TN, c.chunk_tiles);
+  const bool split_sides = split_sides_needed(TN, nt_l, nt_u, cq, want_first);
   const int64_t total = nt_l + nt_u;
   bool first_launch = true;
   for (int64_t c0 = 0; c0 < total;) {
-    // a chunk never straddles the side boundary when the sides are split
-    const int64_t lim = (split_sides && c0 < nt_l) ? nt_l : total;
-    const int64_t c1 = c0 + chunk < lim ? c0 + chunk : lim;
+    const int64_t c1 = next_chunk_end(c0, chunk, nt_l, total, split_sides);
     const int64_t lo[2] = {c0 < nt_l ? c0 : nt_l, (c0 > nt_l ? c0 : nt_l) - nt_l};
     const int64_t hi[2] = {c1 < nt_l ? c1 : nt_l, (c1 > nt_l ? c1 : nt_l) - nt_l};
     Fp4Params q = p;
@@ -1484,6 +1494,24 @@ extern "C" int rsr_classify_fp4_explain(const uint8_t* A, int64_t S, const uint8
                                         int64_t* first_upper, int accumulate, void* stream) {
   return classify_fp4_impl(A, S, B_lower, n_lower, n_lower, B_upper, n_upper, n_upper, row_bytes,
                            flags, first_lower, first_upper, accumulate, stream);
+}
+
+extern "C" int rsr_classify_fp4_plan(int64_t n_lower, int64_t n_upper, int row_bytes,
+                                     int want_first, int* tile_n, int64_t* launches) {
+  RSR_REQUIRE(n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4_plan: negative size");
+  RSR_REQUIRE(row_bytes >= kChunk && row_bytes % kChunk == 0 && row_bytes <= RSR_FP4_MAX_ROW_BYTES,
+              "rsr_classify_fp4_plan: bad row_bytes");
+  RSR_REQUIRE(tile_n && launches, "rsr_classify_fp4_plan: null output");
+  const int cq = row_bytes / kChunk;
+  const TilePlan plan = pick_tile_n(n_lower, n_upper, cq, want_first != 0);
+  const int64_t nt_l = rsr::ceil_div(n_lower, plan.tn), nt_u = rsr::ceil_div(n_upper, plan.tn);
+  const int64_t total = nt_l + nt_u, chunk = launch_chunk_tiles(plan.tn, plan.chunk_tiles);
+  const bool split = split_sides_needed(plan.tn, nt_l, nt_u, cq, want_first != 0);
+  int64_t n = 0;
+  for (int64_t c0 = 0; c0 < total; c0 = next_chunk_end(c0, chunk, nt_l, total, split)) ++n;
+  *tile_n = plan.tn;
+  *launches = n;
+  return RSR_OK;
 }
 
 extern "C" int rsr_unpack_onehot_fp4(const uint8_t* packed, int64_t count, int n_components,

@@ -57,3 +57,17 @@ def test_shared_object_is_sm100a_only():
     out = subprocess.run(["cuobjdump", "--list-elf", _abi.LIB_PATH], capture_output=True, text=True)
     archs = set(re.findall(r"sm_\d+a?", out.stdout))
     assert archs == {"sm_100a"}, archs
+
+
+def test_fp4_launch_plan_is_host_only():
+    # the planner runs on the host (no device needed): tile width and launch count of
+    # the FP4 classifier for the cfg4 sweep's reference counts (one side, 160-byte rows)
+    rb = _abi.fp4_row_bytes(295, 2)
+    assert _abi.fp4_plan(0, 1000, rb) == (208, 1)          # 5 resident tiles of 208
+    tn, n = _abi.fp4_plan(0, 3000, rb)                      # past residency: 2 resident launches
+    assert n == 2 and tn in (208, 224, 240)
+    tn, n = _abi.fp4_plan(0, 500_000, rb)                   # L2-sized chunks of 512 tiles
+    assert n == -(-(-(-500_000 // tn)) // (122880 // tn))
+    assert _abi.fp4_plan(0, 0, rb)[1] == 0
+    with pytest.raises(ValueError):
+        _abi.fp4_plan(-1, 0, rb)
