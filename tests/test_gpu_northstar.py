@@ -86,6 +86,42 @@ def test_cfg4_first_match_chunked_launches(cfg4_paths):
     assert int((want[1] >= dense).sum()) > 500  # first matches in the second launch
 
 
+@pytest.mark.parametrize("k_low,k_up", [(0, 3000), (1500, 1500), (0, 6000)])
+def test_resident_chunked_launches_match_oracle(cfg4_paths, k_low, k_up):
+    # sets just past shared-memory residency run as 2-4 resident-sized launches
+    # (rsr_classify_fp4_plan); labels and first matches (explain) must be those of one
+    # pass over the whole set: flags OR-accumulated, the earliest chunk's match kept
+    from paper_2604_17066_b200 import _abi
+    rb = _abi.fp4_row_bytes(295, 2)
+    tn, launches = _abi.fp4_plan(k_low, k_up, rb)
+    assert 2 <= launches <= 4, (tn, launches)
+    rng = np.random.default_rng(k_low + k_up)
+    upper_rows = cfg4_paths[:k_up].copy()
+    # the earlier references rarely hit, so first matches fall in later launches too
+    upper_rows[: k_up // 2] |= (rng.random((k_up // 2, 295)) < 0.05).astype(np.uint8)
+    lower_rows = (rng.random((k_low, 295)) < 0.985).astype(np.uint8)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, upper_rows, trusted=True)
+    lo = P.ReferenceSet.from_array(P.Side.LOWER, 0, lower_rows, trusted=True)
+    d = P.ComponentDistribution.iid(295, [0.1, 0.9])
+    b = P.sample_batch(d, 6144, seed=3, start=1 << 20)
+    r = P.classify(b, lo, up, n_states=2, explain=True)
+    bits = P.classify(b, lo, up, n_states=2, method="bits")
+    assert torch.equal(r.labels_device, bits.labels_device)
+    xs = b.device_states().cpu().numpy().astype(np.int64)
+    want_u = oracle.dominance_hits(xs, upper_rows, 2, oracle.UPPER, chunk_size=512,
+                                   n_workers=CORES, want_first=True)
+    assert np.array_equal(r.first_match_upper, want_u[1])
+    nt = -(-k_low // tn) + -(-k_up // tn)
+    first_launch_rows = -(-nt // launches) * tn - (-(-k_low // tn)) * tn  # upper rows in launch 1
+    if first_launch_rows < k_up:
+        assert int((want_u[1] >= max(first_launch_rows, 0)).sum()) > 50  # matches in later launches
+    if k_low:
+        want_l = oracle.dominance_hits(xs, lower_rows, 2, oracle.LOWER, chunk_size=512,
+                                       n_workers=CORES, want_first=True)
+        assert np.array_equal(r.first_match_lower, want_l[1])
+        assert (want_l[1] >= 0).any()
+
+
 # ----------------------------------------------------------- run-to-c.o.v. loop
 
 def _grid():
