@@ -387,11 +387,15 @@ __global__ void __launch_bounds__(1024) sample_dev_rows_kernel(
     const double* __restrict__ probs, int N, int M, const rsr::Philox32Keys K, uint64_t gen,
     int64_t start, int64_t count, uint8_t* __restrict__ states, uint8_t* __restrict__ fp4,
     int words, int R, int passes, int64_t row_stride, int64_t plane) {
+  // U rows per thread per pass (M = 2, 3): their Philox chains are independent, so the
+  // scheduler interleaves them (a chain is 10 dependent multiply-xor rounds)
+  constexpr int U = MT ? 2 : 1;
+  const int PR = U * R;  // rows per pass
   // state rows of a pass, staged (double-buffered) so they leave as aligned 16-byte
   // stores: rows of N bytes are not word aligned, and a lane's 8 state bytes would
   // otherwise need up to four differently sized stores
   extern __shared__ __align__(16) uint8_t stage[];
-  const int stage_bytes = (R * N + 16 + 15) & ~15;
+  const int stage_bytes = (PR * N + 16 + 15) & ~15;
   const int w = threadIdx.x % words, rr = threadIdx.x / words;
   const bool lane_on = rr < R;
   const int Mm1 = MT ? MT - 1 : M - 1;
@@ -414,51 +418,67 @@ __global__ void __launch_bounds__(1024) sample_dev_rows_kernel(
   const uint32_t bias = rem >= 0 && rem < 8 ? 2u << (4 * rem) : 0u;
   const bool has_cols = lane_on && rem > 0;
   const int nst = MT == 2 ? min(8, N - 8 * w) : MT == 3 ? min(4, N - 4 * w) : 0;
-  const int64_t c0 = (int64_t)blockIdx.x * R * passes;  // first row of this CTA
-  const int64_t left = (count - c0 + R - 1) / R;
+  const int64_t c0 = (int64_t)blockIdx.x * PR * passes;  // first row of this CTA
+  const int64_t left = (count - c0 + PR - 1) / PR;
   const int np = left < passes ? (int)left : passes;
   for (int p = 0; p < np; ++p) {
-    const int64_t pr = c0 + (int64_t)p * R;  // first row of the pass
-    const int prows = count - pr < R ? (int)(count - pr) : R;
-    const int64_t li = pr + rr;
+    const int64_t pr = c0 + (int64_t)p * PR;  // first row of the pass
+    const int prows = count - pr < PR ? (int)(count - pr) : PR;
     uint8_t* buf = stage + (p & 1) * stage_bytes;
     const int sb = states ? (int)(reinterpret_cast<uintptr_t>(states + pr * N) & 15u) : 0;
-    uint8_t* srow = buf + sb + rr * N;
-    const uint64_t row = (uint64_t)(start + li);
-    uint32_t lo = 0;
-    if (has_cols && rr < prows) {
+    uint32_t lo[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) lo[u] = 0;
+    if (has_cols) {
       if (MT == 2) {
-        uint32_t d[8];
-        rsr::device_row_block(row, (uint32_t)(2 * w), gen, K, d);
-        if (8 * w + 4 < N) rsr::device_row_block(row, (uint32_t)(2 * w + 1), gen, K, d + 4);
-        uint32_t s0 = 0, s1 = 0;
+        // both blocks of every row, unconditionally (a word past N/8 + 1/2 has v = 0 on
+        // its upper half), so the U x 2 chains form one straight-line block
+        uint32_t d[U][8];
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          s0 += d[s] >= T[s] ? v[s] : 0u;
-          s1 += d[s + 4] >= T[s + 4] ? v[s + 4] : 0u;
+        for (int u = 0; u < U; ++u) {
+          const uint64_t row = (uint64_t)(start + pr + u * R + rr);
+          rsr::device_row_block(row, (uint32_t)(2 * w), gen, K, d[u]);
+          rsr::device_row_block(row, (uint32_t)(2 * w + 1), gen, K, d[u] + 4);
         }
-        // state bytes (0/1) -> nibbles at bit 4j + 1 (cf. fp4_quad_fast)
-        lo = __byte_perm(s0 | (s0 >> 4), s1 | (s1 >> 4), 0x6420) << 1;
-        if (states) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (j < nst) srow[8 * w + j] = (uint8_t)((j < 4 ? s0 : s1) >> (8 * (j & 3)));
+        for (int u = 0; u < U; ++u) {
+          uint32_t s0 = 0, s1 = 0;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            s0 += d[u][s] >= T[s] ? v[s] : 0u;
+            s1 += d[u][s + 4] >= T[s + 4] ? v[s + 4] : 0u;
+          }
+          // state bytes (0/1) -> nibbles at bit 4j + 1 (cf. fp4_quad_fast)
+          lo[u] = __byte_perm(s0 | (s0 >> 4), s1 | (s1 >> 4), 0x6420) << 1;
+          if (states && u * R + rr < prows) {
+            uint8_t* srow = buf + sb + (u * R + rr) * N;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < nst) srow[8 * w + j] = (uint8_t)((j < 4 ? s0 : s1) >> (8 * (j & 3)));
+          }
         }
       } else if (MT == 3) {
-        uint32_t d[4];
-        rsr::device_row_block(row, (uint32_t)w, gen, K, d);
-        uint32_t s0 = 0;
+        uint32_t d[U][4];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) s0 += d[s >> 1] >= T[s] ? v[s] : 0u;
-        const uint32_t sel = (s0 & 0xFu) | ((s0 >> 4) & 0xF0u) | ((s0 >> 8) & 0xF00u) |
-                             ((s0 >> 12) & 0xF000u);
-        lo = __byte_perm(0x00220200u, 0u, sel);  // x = 0, 1, 2 -> 0x00, 0x02, 0x22
-        if (states) {
+        for (int u = 0; u < U; ++u)
+          rsr::device_row_block((uint64_t)(start + pr + u * R + rr), (uint32_t)w, gen, K, d[u]);
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < nst) srow[4 * w + j] = (uint8_t)(s0 >> (8 * j));
+        for (int u = 0; u < U; ++u) {
+          uint32_t s0 = 0;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) s0 += d[u][s >> 1] >= T[s] ? v[s] : 0u;
+          const uint32_t sel = (s0 & 0xFu) | ((s0 >> 4) & 0xF0u) | ((s0 >> 8) & 0xF00u) |
+                               ((s0 >> 12) & 0xF000u);
+          lo[u] = __byte_perm(0x00220200u, 0u, sel);  // x = 0, 1, 2 -> 0x00, 0x02, 0x22
+          if (states && u * R + rr < prows) {
+            uint8_t* srow = buf + sb + (u * R + rr) * N;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < nst) srow[4 * w + j] = (uint8_t)(s0 >> (8 * j));
+          }
         }
-      } else {
+      } else if (rr < prows) {
+        const uint64_t row = (uint64_t)(start + pr + rr);
         uint32_t d[4];
         int q = -1;
         for (int s = 0; s < 8; ++s) {
@@ -468,11 +488,12 @@ __global__ void __launch_bounds__(1024) sample_dev_rows_kernel(
             q = n >> 2;
             rsr::device_row_block(row, (uint32_t)q, gen, K, d);
           }
-          lo |= d[n & 3] >= T[s] ? v[s] : 0u;
+          lo[0] |= d[n & 3] >= T[s] ? v[s] : 0u;
         }
         if (states) {
           // component n is written by the word holding its first column; x_n counts its
           // columns set (columns in later words are compared here directly)
+          uint8_t* srow = buf + sb + rr * N;
           for (int s = 0; s < 8; ++s) {
             const int c = 8 * w + s;
             if (c >= kdim) break;
@@ -484,7 +505,7 @@ __global__ void __launch_bounds__(1024) sample_dev_rows_kernel(
             for (int k = 0; k < Mm1; ++k) {
               const int cc = c + k;
               if ((cc >> 3) == w) {
-                x += (lo >> (4 * (cc & 7) + 1)) & 1u;
+                x += (lo[0] >> (4 * (cc & 7) + 1)) & 1u;
               } else {
                 uint32_t t;
                 bool ok;
@@ -497,11 +518,15 @@ __global__ void __launch_bounds__(1024) sample_dev_rows_kernel(
         }
       }
     }
-    if (fp4 && lane_on && rr < prows) {
-      lo |= bias;
-      uint8_t* prow = fp4 + li * row_stride;
-      reinterpret_cast<uint32_t*>(prow)[w] = lo ^ flip;
-      reinterpret_cast<uint32_t*>(prow + plane)[w] = lo;
+    if (fp4 && lane_on) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u * R + rr >= prows) break;
+        const uint32_t l = lo[u] | bias;
+        uint8_t* prow = fp4 + (pr + u * R + rr) * row_stride;
+        reinterpret_cast<uint32_t*>(prow)[w] = l ^ flip;
+        reinterpret_cast<uint32_t*>(prow + plane)[w] = l;
+      }
     }
     if (states) {
       __syncthreads();  // the pass's rows are staged (the other buffer is free again)
@@ -782,16 +807,25 @@ int launch_dev_rows(const double* probs, int N, int M, uint64_t seed, uint64_t g
     }
   }
   const int threads = (R * words + 31) / 32 * 32;
-  // ~128 rows per CTA: short-lived CTAs (the loop's low-priority prefetch must not hold
-  // SMs for long), each deriving its column constants once
-  const int passes = std::max(1, 128 / R);
-  const int64_t grid = rsr::ceil_div(count, (int64_t)R * passes);
+  // 32 rows per CTA: short-lived CTAs, so the Stage-1 loop's high-priority kernels
+  // (searches, insertion) find SM space within a few microseconds while a prefetched
+  // batch is drawn on the low-priority stream (cfg3 loop on this stream: 0.117 s with
+  // 128-row CTAs, 0.0965 s with 32; the sampler alone is 10 % slower: every CTA derives
+  // its column constants once).  M = 2, 3 threads take two rows per pass.
+  // RSR_DEVROWS_CTA_ROWS overrides (experiments).
+  const int U = (M == 2 || M == 3) ? 2 : 1;
+  static const int cta_rows = [] {
+    const char* e = getenv("RSR_DEVROWS_CTA_ROWS");
+    return e ? std::max(1, atoi(e)) : 32;
+  }();
+  const int passes = std::max(1, cta_rows / (U * R));
+  const int64_t grid = rsr::ceil_div(count, (int64_t)U * R * passes);
   const rsr::Philox32Keys keys = rsr::device_keys(seed, gen);
   void* args[] = {(void*)&probs, (void*)&N,      (void*)&M,     (void*)&keys,
                   (void*)&gen,   (void*)&start,  (void*)&count, (void*)&states,
                   (void*)&fp4,   (void*)&words,  (void*)&R,     (void*)&passes,
                   (void*)&row_stride, (void*)&plane};
-  const size_t smem = states ? 2 * (size_t)((R * N + 16 + 15) & ~15) : 0;
+  const size_t smem = states ? 2 * (size_t)((U * R * N + 16 + 15) & ~15) : 0;
   if (smem > 48 * 1024) {
     const int rc = rsr::ensure_dynamic_smem(kern, smem);
     if (rc) return rc;
