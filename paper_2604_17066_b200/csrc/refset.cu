@@ -55,7 +55,11 @@ __global__ void encode_cands_kernel(const uint8_t* __restrict__ cands,
 
 // covered[c] |= some alive member m makes c redundant; covers[c] |= c makes
 // some alive member redundant.  Thread = member (row words in registers),
-// candidates of the member's side staged in shared memory.
+// candidates of the member's side staged in shared memory; blockIdx.z takes a
+// slice of kScanSlice candidates, so a 64-candidate batch against ~10^4 members
+// runs as ~600 CTAs instead of ~80 (the scan is latency-bound, not work-bound).
+constexpr int kScanSlice = 16;
+
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(
     const uint8_t* __restrict__ cand_fp4, const uint8_t* __restrict__ cand_side, int B,
     rsr_refset_dev lower, rsr_refset_dev upper, int row_bytes, uint8_t* covered,
@@ -76,8 +80,9 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(
     for (int w = 0; w < kMaxWords; ++w)
       if (w < nw) mw[w] = src[w];
   }
-  for (int c0 = 0; c0 < B; c0 += kScanStage) {
-    const int cn = min(kScanStage, B - c0);
+  const int cz = blockIdx.z * kScanSlice, cend = min(B, cz + kScanSlice);
+  for (int c0 = cz; c0 < cend; c0 += kScanStage) {
+    const int cn = min(kScanStage, cend - c0);
     __syncthreads();
     for (int i = threadIdx.x; i < cn * nw; i += kScanThreads) {
       const int c = i / nw, w = i - c * nw;
@@ -146,13 +151,22 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(
     const uint8_t* __restrict__ cands, const uint8_t* __restrict__ cand_side,
     const uint8_t* __restrict__ cand_fp4, int B, int N, int row_bytes,
     const uint8_t* __restrict__ covered, const uint8_t* __restrict__ covers,
-    const uint8_t* __restrict__ rel, rsr_refset_dev lower, rsr_refset_dev upper,
-    uint8_t* outcome, int64_t* row_of, const int64_t* calls, int64_t* report) {
+    const uint8_t* __restrict__ rel_g, rsr_refset_dev lower, rsr_refset_dev upper,
+    uint8_t* outcome, int64_t* row_of, const int64_t* calls, int64_t* report, int stage_rel) {
   extern __shared__ __align__(16) uint8_t smem[];
   int64_t* s_row = reinterpret_cast<int64_t*>(smem);             // [B]
   int* s_drop = reinterpret_cast<int*>(smem + 8 * (size_t)B);      // [B] member droppers
   uint8_t* s_side = smem + 12 * (size_t)B;                        // [B] 0 lower, 1 upper
   uint8_t* s_ins = s_side + B;                                    // [B]
+  // the B x B relation, staged in shared memory when it fits: the scans below read
+  // it row by row (a chain of dependent global loads was most of this kernel's time)
+  const uint8_t* rel = rel_g;
+  if (stage_rel) {
+    uint8_t* s_rel = s_ins + B;                                   // [B][B]
+    for (int i = threadIdx.x; i < B * B; i += blockDim.x) s_rel[i] = rel_g[i];
+    rel = s_rel;
+    __syncthreads();
+  }
   __shared__ int64_t s_n0[2], s_nins[2], s_dead[2];
   __shared__ int s_red, s_over, s_ndrop;
   __shared__ long long s_calls;
@@ -167,9 +181,10 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(
   // redundancy (parallel over candidates)
   for (int c = tid; c < B; c += blockDim.x) {
     const uint8_t sd = cand_side[c] == RSR_SIDE_UPPER ? 1 : 0;
-    bool red = covered[c] != 0;
     const uint8_t* rr = rel + (int64_t)c * B;
-    for (int j = 0; j < c && !red; ++j) red = (rr[j] & 2) != 0;  // rel is 0 across sides
+    uint32_t any2 = 0;
+    for (int j = 0; j < c; ++j) any2 |= rr[j];  // rel is 0 across sides
+    const bool red = covered[c] != 0 || (any2 & 2) != 0;
     s_side[c] = sd;
     s_ins[c] = red ? 0 : 1;
   }
@@ -223,19 +238,27 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(
     if (calls) local_calls += calls[c];
     if (r < 0) continue;
     bool dead = false;
-    for (int d = c + 1; d < B && !dead; ++d)
-      dead = s_row[d] >= 0 && (rel[(int64_t)d * B + c] & 1);  // c <= later inserted d
+    for (int d = c + 1; d < B; ++d)
+      dead |= s_row[d] >= 0 && (rel[(int64_t)d * B + c] & 1);  // c <= later inserted d
     sets[s_side[c]]->alive[r] = dead ? 0 : 1;
     if (dead) ++local_dead[s_side[c]];
     if (covers[c]) s_drop[atomicAdd(&s_ndrop, 1)] = c;
   }
-  for (int i = tid; i < B * N; i += blockDim.x) {
-    const int c = i / N, k = i - c * N;
-    if (s_row[c] >= 0) sets[s_side[c]]->rows[s_row[c] * N + k] = cands[i];
-  }
-  for (int i = tid; i < B * row_bytes; i += blockDim.x) {
-    const int c = i / row_bytes, k = i - c * row_bytes;
-    if (s_row[c] >= 0) sets[s_side[c]]->fp4[s_row[c] * row_bytes + k] = cand_fp4[i];
+  // appends: one warp per inserted candidate row (u8 row bytewise, FP4 row as 16-byte
+  // words; a per-byte index division over the whole batch was this kernel's main cost)
+  {
+    const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+    for (int c = warp; c < B; c += nwarps) {
+      const int64_t r = s_row[c];
+      if (r < 0) continue;
+      const rsr_refset_dev& set = s_side[c] ? upper : lower;
+      uint8_t* dst = set.rows + r * N;
+      const uint8_t* src = cands + (int64_t)c * N;
+      for (int k = lane; k < N; k += 32) dst[k] = src[k];
+      uint4* fd = reinterpret_cast<uint4*>(set.fp4 + r * row_bytes);
+      const uint4* fs = reinterpret_cast<const uint4*>(cand_fp4 + (int64_t)c * row_bytes);
+      for (int k = lane; k < row_bytes / 16; k += 32) fd[k] = fs[k];
+    }
   }
   __syncthreads();
   // pre-batch members made redundant by an inserted candidate (rare)
@@ -422,7 +445,7 @@ extern "C" int rsr_refset_insert(const uint8_t* cands, const uint8_t* cand_side,
   if (rc) return rc;
   const int64_t nb = std::max(lower->n_bound, upper->n_bound);
   if (nb > 0) {
-    dim3 grid((unsigned)rsr::ceil_div(nb, kScanThreads), 2);
+    dim3 grid((unsigned)rsr::ceil_div(nb, kScanThreads), 2, (unsigned)rsr::ceil_div(B, kScanSlice));
     scan_kernel<<<grid, kScanThreads, 0, st>>>(cand_fp4, cand_side, (int)B, *lower, *upper, rb,
                                                covered, covers);
     rc = rsr::check_launch("scan_kernel");
@@ -433,14 +456,15 @@ extern "C" int rsr_refset_insert(const uint8_t* cands, const uint8_t* cand_side,
     rc = rsr::check_launch("rel_kernel");
     if (rc) return rc;
   }
-  const size_t rsmem = 14 * (size_t)B + 16;
+  const int stage_rel = (size_t)B * B <= 64 * 1024 ? 1 : 0;
+  const size_t rsmem = 14 * (size_t)B + 16 + (stage_rel ? (size_t)B * B : 0);
   RSR_REQUIRE(rsmem <= 200 * 1024, "rsr_refset_insert: batch too large");
   if (rsmem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)rsmem));
   resolve_kernel<<<1, kResolveThreads, rsmem, st>>>(cands, cand_side, cand_fp4, (int)B, N, rb,
                                                     covered, covers, rel, *lower, *upper, outcome,
-                                                    row_of, calls, report);
+                                                    row_of, calls, report, stage_rel);
   return rsr::check_launch("resolve_kernel");
 }
 
