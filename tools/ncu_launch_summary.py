@@ -12,11 +12,14 @@ for r in data:
     if len(r) <= vi: continue
     name = r[ki].replace("void ", "").replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
     name = name.split("(")[0].split("<")[0]
-    v = float(r[vi].replace(",", ""))
-    if r[ui] == "nsecond": v /= 1e3
-    elif r[ui] == "msecond": v *= 1e3
+    v = float(r[vi].replace(",", ""))  # -> microseconds
+    unit = r[ui]
+    if unit in ("ns", "nsecond"):
+        v /= 1e3
+    elif unit in ("ms", "msecond"):
+        v *= 1e3
     tot[name] += v; cnt[name] += 1
 T = sum(tot.values())
-print(f"total kernel time {T/1e3:.2f} ms over {sum(cnt.values())} launches")
+print(f"total kernel time {T/1e3:.2f} ms over {sum(cnt.values())} launches (serialised by ncu)")
 for k, v in tot.most_common(20):
-    print(f"{k:45s} {v/1e3:8.2f} ms {100*v/T:5.1f}%  n={cnt[k]}  avg {v/cnt[k]:.1f} us")
+    print(f"{k:45s} {v/1e3:8.3f} ms {100*v/T:5.1f}%  n={cnt[k]}  avg {v/cnt[k]:.1f} us")
