@@ -96,7 +96,6 @@ struct Tile {
   static constexpr int kBufs = 480 / TN;
   static constexpr int kHalfRows = TN / 2;             // reference rows per CTA per tile
   static constexpr int kChunkB = kHalfRows * kChunk;   // bytes per K-step per CTA
-  static constexpr int kCols = TN;                      // accumulator columns per epilogue warp
   static_assert(TN % 16 == 0 && TN <= 240 && kBufs >= 2 && kBufs <= 4, "bad tile N");
 };
 
@@ -381,7 +380,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
 #elif defined(RSR_FP4_X_NOWAIT)
         // timing experiment only (wrong results): never wait for the epilogue
 #else
-        mbar_wait(m.bar_t_empty + 8 * buf, tphase ^ 1);
+        mbar_wait_inline(m.bar_t_empty + 8 * buf, tphase ^ 1);  // tc_common.cuh: why inline
 #endif
         PROF_T(m1);
 #ifdef RSR_FP4_PROF

@@ -53,6 +53,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (!mbar_try(bar, parity)) mbar_wait_slow(bar, parity);
 }
 
+// Inline wait loop for the hottest barrier of the FP4 classifier: the MMA warp's wait for
+// an accumulator buffer to be released.  mbar_wait's out-of-line slow path is a call from
+// the MMA warp's loop (caller-saved registers spilled and restored around it on every
+// failed first probe), and at small reference sets that wait fails on most tiles: cfg4
+// K = 10^3 0.77 -> 0.82 of peak, 10^4 0.866 -> 0.876, 5x10^5 unchanged.  A try_wait
+// suspend-time hint (20 .. 1000 ns) made no difference; any timeout bookkeeping in the
+// loop (probe counter, clock checks) cost 1-3 % at K = 5x10^5, so this wait has none: a
+// protocol failure still traps in the epilogue's or the producer's mbar_wait
+// (profiles/r2_fp4_small_k_experiments.txt).
+__device__ __forceinline__ void mbar_wait_inline(uint32_t bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+
+
 // Non-suspending probe of a phase (mbarrier.test_wait).
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   uint32_t done;
