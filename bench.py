@@ -503,7 +503,7 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     launches = 0
     # reference-chunked launches of the classifier (L2-resident B slices)
     if method == "tc":  # the library's own launch plan (tile width, chunked launches)
-        classify_launches = max(1, _abi.fp4_plan(nl, nu, width)[1])
+        classify_launches = max(1, _abi.fp4_plan(S, nl, nu, width)[1])
     else:
         tiles = {"tc8": lambda n: -(-n // 256), "bits": lambda n: 0}[method]
         per_launch = {"tc8": 256, "bits": 1}[method]

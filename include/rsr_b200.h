@@ -230,13 +230,13 @@ int rsr_classify_fp4_planar(const uint8_t* A, int64_t a_plane_stride, int64_t S,
                             int64_t avail_upper, int row_bytes, uint8_t* flags,
                             int64_t* first_lower, int64_t* first_upper, int accumulate,
                             void* stream);
-/* The launch plan rsr_classify_fp4* would use for these reference counts (host only,
- * no device work): MMA N per reference tile (160..240) and the number of kernel
- * launches (L2-sized reference chunks, or 2-4 resident-sized launches for sets just
- * past shared-memory residency).  An all-empty call reports 0 launches (the flags are
- * cleared by a separate kernel unless accumulating). */
-int rsr_classify_fp4_plan(int64_t n_lower, int64_t n_upper, int row_bytes, int want_first,
-                          int* tile_n, int64_t* launches);
+/* The launch plan rsr_classify_fp4* would use for S samples and these reference counts
+ * (host only, no device work): MMA N per reference tile (160..240) and the number of
+ * kernel launches (L2-sized reference chunks, or resident-sized launches for sets past
+ * shared-memory residency, fewer for smaller S).  An all-empty call reports 0 launches
+ * (the flags are cleared by a separate kernel unless accumulating). */
+int rsr_classify_fp4_plan(int64_t S, int64_t n_lower, int64_t n_upper, int row_bytes,
+                          int want_first, int* tile_n, int64_t* launches);
 /* rsr_classify_fp4 over the first *S_dev (device count, <= S_cap) rows of A:
  * the sample count of a later pass is known only on the device. */
 int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,

@@ -104,7 +104,7 @@ EXPORTED = {
     "rsr_classify_fp4_planar": (_I, [_P, _I64, _I64, _P, _P, _I64, _I64, _P, _I64, _I64, _I, _P,
                                      _P, _P, _I, _P]),
     "rsr_classify_fp4_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
-    "rsr_classify_fp4_plan": (_I, [_I64, _I64, _I, _I, _P, _P]),
+    "rsr_classify_fp4_plan": (_I, [_I64, _I64, _I64, _I, _I, _P, _P]),
     "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_classify_bits": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_finalize": (_I, [_P, _I64, _P, _P, _P]),
@@ -223,12 +223,13 @@ def fp4_row_bytes(n: int, m: int) -> int:
     return (n * (m - 1) + 1 + 63) // 64 * 32
 
 
-def fp4_plan(n_lower: int, n_upper: int, row_bytes: int, want_first: bool = False) -> tuple[int, int]:
-    """(MMA N per reference tile, kernel launches) of an rsr_classify_fp4* call with these
-    reference counts (rsr_classify_fp4_plan; host only)."""
+def fp4_plan(n_samples: int, n_lower: int, n_upper: int, row_bytes: int,
+             want_first: bool = False) -> tuple[int, int]:
+    """(MMA N per reference tile, kernel launches) of an rsr_classify_fp4* call over
+    n_samples samples with these reference counts (rsr_classify_fp4_plan; host only)."""
     tn = ctypes.c_int(0)
     launches = ctypes.c_int64(0)
-    call("rsr_classify_fp4_plan", n_lower, n_upper, row_bytes, int(want_first),
+    call("rsr_classify_fp4_plan", n_samples, n_lower, n_upper, row_bytes, int(want_first),
          ctypes.addressof(tn), ctypes.addressof(launches))
     return tn.value, launches.value
 

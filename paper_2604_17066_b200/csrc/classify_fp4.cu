@@ -1095,24 +1095,31 @@ struct TilePlan {
   int64_t chunk_tiles;  // 0: default (L2-sized chunks, tiles streamed per sample group)
 };
 
-TilePlan pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) {
+TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, int cq,
+                     bool want_first) {
   const char* env = getenv("RSR_FP4_TILE_N");
   const int forced = env ? atoi(env) : 0;
   static const int kCand[] = {240, 224, 208, 192, 176, 160};
   static const int kCost[] = {1000, 957, 971, 920, 843, 778};  // relative time per tile
   // resident tiles (cfg4 K = 10^3 per-tile times, profiles/r1_tile_n_small_k.txt)
   static const int kCostResident[] = {1000, 956, 935, 869, 862, 779};
-  // streaming a small set costs about 1700 cycles (2.5 tiles) per sample group
-  // more than keeping it resident (cfg4 K = 2000: 9 resident tiles of 224 take
-  // 0.670 ms, 9 streamed tiles of 240 0.891 ms; profiles/r1_tile_n_small_k.txt)
-  constexpr int64_t kStreamGroupCost = 2500;
+  // Streaming the tiles through the ring costs per sample group, over keeping them
+  // resident, about 2.5 tiles for short sets (cfg4 K = 2000: 9 resident tiles of 224 take
+  // 0.670 ms, 9 streamed tiles of 240 0.891 ms; profiles/r1_tile_n_small_k.txt) and about
+  // one tile for long ones (K >= 7000, fitted below).
   // Past residency, the set can instead run as several resident launches, each
-  // re-reading the sample operand: about one tile per sample group per extra launch
-  // (fitted on cfg4 K = 2500 .. 10^4: 0.75 - 1.5 tiles; profiles/r2_fp4_chunked_residency.txt),
-  // so up to four launches beat streaming the tiles through the ring for every group
-  // (K = 3000: 0.78 -> 0.83 of peak, 6000: 0.863 -> 0.879); at 10^4 the two tie.
-  constexpr int64_t kChunkGroupCost = 1000;
-  constexpr int64_t kMaxChunks = 4;
+  // re-reading the sample operand: a launch's fixed cost (start, prologue, tail; ~24
+  // tile-times per cluster) spread over the cluster's sample groups, plus a little per
+  // group (cfg4, 2^22 samples: ~0.12 tile per group per extra launch, so 9-tile resident
+  // chunks beat streaming up to K ~ 2x10^4: K = 3000 0.78 -> 0.85, 7000 0.844 -> 0.867,
+  // 10^4 0.876 -> 0.887, 2x10^4 tie, 4x10^4 streaming ahead;
+  // profiles/r2_fp4_chunked_residency.txt).  Smaller batches have fewer groups per cluster
+  // and chunk less.
+  const int64_t clusters = std::max(1, sm_count / 2);
+  const int64_t gpc = std::max<int64_t>(1, rsr::ceil_div(rsr::ceil_div(S, (int64_t)2 * kRowsA),
+                                                          clusters));
+  const int64_t kChunkGroupCost = 50 + 24000 / gpc;
+  constexpr int64_t kMaxChunks = 16;
   for (int tn : kCand)
     if (tn == forced) return {tn, 0};
   // wide rows (>= 12 K-steps, e.g. N = 295 at M >= 4): N = 160 tiles with three
@@ -1130,7 +1137,7 @@ TilePlan pick_tile_n(int64_t n_lower, int64_t n_upper, int cq, bool want_first) 
     if (!fp4_feasible(tn, nt_l, nt_u, cq, want_first)) continue;
     const bool resident = fp4_layout(tn, nt_l, nt_u, cq, want_first).resident;
     int64_t cost = (nt_l + nt_u) * (resident ? kCostResident[i] : kCost[i]);
-    if (!resident) cost += kStreamGroupCost;
+    if (!resident) cost += nt_l + nt_u <= 16 ? 2500 : 1000;  // streaming penalty (above)
     if (cost < best_cost) {
       best_cost = cost;
       best = {tn, 0};
@@ -1203,7 +1210,7 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   int dev = 0;
   RSR_CUDA(cudaGetDevice(&dev));
   RSR_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, dev));
-  const TilePlan plan = pick_tile_n(n_lower, n_upper, row_bytes / kChunk,
+  const TilePlan plan = pick_tile_n(S, c.sm_count, n_lower, n_upper, row_bytes / kChunk,
                                     first_lower != nullptr || first_upper != nullptr);
   c.chunk_tiles = plan.chunk_tiles;
   switch (plan.tn) {
@@ -1496,14 +1503,22 @@ extern "C" int rsr_classify_fp4_explain(const uint8_t* A, int64_t S, const uint8
                            flags, first_lower, first_upper, accumulate, stream);
 }
 
-extern "C" int rsr_classify_fp4_plan(int64_t n_lower, int64_t n_upper, int row_bytes,
+extern "C" int rsr_classify_fp4_plan(int64_t S, int64_t n_lower, int64_t n_upper, int row_bytes,
                                      int want_first, int* tile_n, int64_t* launches) {
-  RSR_REQUIRE(n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4_plan: negative size");
+  RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4_plan: negative size");
   RSR_REQUIRE(row_bytes >= kChunk && row_bytes % kChunk == 0 && row_bytes <= RSR_FP4_MAX_ROW_BYTES,
               "rsr_classify_fp4_plan: bad row_bytes");
   RSR_REQUIRE(tile_n && launches, "rsr_classify_fp4_plan: null output");
   const int cq = row_bytes / kChunk;
-  const TilePlan plan = pick_tile_n(n_lower, n_upper, cq, want_first != 0);
+  int sm_count = 148;  // host-only query: the current device's SM count when there is one
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      sm_count = v;
+  }
+  cudaGetLastError();  // no device: clear the sticky error of the probe
+  const TilePlan plan = pick_tile_n(S, sm_count, n_lower, n_upper, cq, want_first != 0);
   const int64_t nt_l = rsr::ceil_div(n_lower, plan.tn), nt_u = rsr::ceil_div(n_upper, plan.tn);
   const int64_t total = nt_l + nt_u, chunk = launch_chunk_tiles(plan.tn, plan.chunk_tiles);
   const bool split = split_sides_needed(plan.tn, nt_l, nt_u, cq, want_first != 0);

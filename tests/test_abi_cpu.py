@@ -63,11 +63,16 @@ def test_fp4_launch_plan_is_host_only():
     # the planner runs on the host (no device needed): tile width and launch count of
     # the FP4 classifier for the cfg4 sweep's reference counts (one side, 160-byte rows)
     rb = _abi.fp4_row_bytes(295, 2)
-    assert _abi.fp4_plan(0, 1000, rb) == (208, 1)          # 5 resident tiles of 208
-    tn, n = _abi.fp4_plan(0, 3000, rb)                      # past residency: 2 resident launches
+    S = 1 << 22
+    assert _abi.fp4_plan(S, 0, 1000, rb) == (208, 1)       # 5 resident tiles of 208
+    tn, n = _abi.fp4_plan(S, 0, 3000, rb)                   # past residency: 2 resident launches
     assert n == 2 and tn in (208, 224, 240)
-    tn, n = _abi.fp4_plan(0, 500_000, rb)                   # L2-sized chunks of 512 tiles
+    tn, n = _abi.fp4_plan(S, 0, 10_000, rb)                 # resident-sized launches up to ~2x10^4
+    assert n >= 4
+    tn, n = _abi.fp4_plan(S, 0, 500_000, rb)                # L2-sized chunks of 512 tiles
     assert n == -(-(-(-500_000 // tn)) // (122880 // tn))
-    assert _abi.fp4_plan(0, 0, rb)[1] == 0
+    # a small batch has few sample groups per CTA pair: extra launches do not pay
+    assert _abi.fp4_plan(4096, 0, 10_000, rb)[1] == 1
+    assert _abi.fp4_plan(S, 0, 0, rb)[1] == 0
     with pytest.raises(ValueError):
-        _abi.fp4_plan(-1, 0, rb)
+        _abi.fp4_plan(S, -1, 0, rb)
