@@ -172,7 +172,7 @@ classify_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       tc_fence_after();
       for (int j = 0; j < p.nt_total; ++j, ++tc) {
         const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
-        mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
+        mbar_wait_inline(smem_addr(&t_empty[buf]), tphase ^ 1);  // tc_common.cuh: why inline
         tc_fence_after();
         const uint32_t d0 = tm0 + buf * MT * kTileN;
         for (int kb = 0; kb < p.kb; ++kb) {
@@ -404,7 +404,7 @@ classify_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         const uint32_t a_lo_g = a_lo0 + (uint32_t)(ab * p.kb) * (kTileBytes >> 4);
         for (int j = 0; j < p.nt_total; ++j, ++tc) {
           const uint32_t buf = tc & 1, tphase = (tc >> 1) & 1;
-          mbar_wait(smem_addr(&t_empty[buf]), tphase ^ 1);
+          mbar_wait_inline(smem_addr(&t_empty[buf]), tphase ^ 1);  // tc_common.cuh: why inline
           tc_fence_after();
           const uint32_t d = tm0 + buf * kPairN;
           for (int kb = 0; kb < p.kb; ++kb) {
