@@ -7,8 +7,9 @@ device Philox sampler) against K = 5x10^5 random simple s-t path references
 (upper side) on the 119-node / 295-edge config-3 graph.  Strong scaling: with
 N GPUs each rank owns 2^22 / N samples of the same stream (start offsets) and
 the whole reference set.  A step is one classification of the resident
-samples against all K references: rsr_classify_fp4_ex (tcgen05 block-scaled
-FP4 0/1 contraction, fused any-zero epilogue; reference-chunked launches) +
+samples against all K references: rsr_classify_fp4_planar (tcgen05 block-scaled
+FP4 0/1 contraction on the planar sample operand, fused any-zero epilogue; the
+launches of rsr_classify_fp4_plan: L2-sized reference chunks at K = 5x10^5) +
 rsr_finalize (labels + counts), plus an NCCL all-reduce of the counts when
 N > 1.  Metric: classified samples x reference states per second (pairs/s).
 `--method tc8` / `bits` time the int8 tcgen05 and bit-packed CUDA-core
