@@ -234,7 +234,9 @@ int rsr_classify_fp4_planar(const uint8_t* A, int64_t a_plane_stride, int64_t S,
  * (host only, no device work): MMA N per reference tile (160..240) and the number of
  * kernel launches (L2-sized reference chunks, or resident-sized launches for sets past
  * shared-memory residency, fewer for smaller S).  An all-empty call reports 0 launches
- * (the flags are cleared by a separate kernel unless accumulating). */
+ * (the flags are cleared by a separate kernel unless accumulating); tile_n 0 means no
+ * tile width fits shared memory (768-byte rows with first matches) and rsr_classify_fp4*
+ * would return RSR_EUNSUPPORTED: use rsr_classify_tc or rsr_classify_bits. */
 int rsr_classify_fp4_plan(int64_t S, int64_t n_lower, int64_t n_upper, int row_bytes,
                           int want_first, int* tile_n, int64_t* launches);
 /* rsr_classify_fp4 over the first *S_dev (device count, <= S_cap) rows of A:

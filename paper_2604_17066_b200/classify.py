@@ -250,7 +250,14 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
     st = _device.stream()
     if method not in ("tc", "tc8", "fp4", "bits"):
         raise ValueError("method must be 'tc', 'tc8', 'fp4' or 'bits'")
-    fp4_ok = _abi.fp4_row_bytes(batch.n_components, m_eff) <= _abi.FP4_MAX_ROW_BYTES
+    rb4 = _abi.fp4_row_bytes(batch.n_components, m_eff)
+    fp4_ok = rb4 <= _abi.FP4_MAX_ROW_BYTES
+    if fp4_ok and rb4 > _abi.REFSET_MAX_ROW_BYTES:
+        # the widest rows: ask the planner whether a tile width fits shared memory (768-byte
+        # rows with first matches do not); otherwise the int8 / bit-packed kernels run
+        nl0 = len(lower_set) if lower_set is not None else 0
+        nu0 = len(upper_set) if upper_set is not None else 0
+        fp4_ok = _abi.fp4_plan(H, nl0, nu0, rb4, want_first)[0] > 0
     tc_ok = _abi.thermo_kpad(batch.n_components, m_eff) <= TC_MAX_KPAD
     if fp4_ok and (method == "fp4" or (method == "tc" and fp4_exact())):
         a = batch.fp4(m_eff)

@@ -1128,7 +1128,8 @@ TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, 
   if (cq >= 12 && fp4_feasible(160, rsr::ceil_div(n_lower, 160), rsr::ceil_div(n_upper, 160), cq,
                                want_first))
     return {160, 0};
-  TilePlan best{160, 0};  // narrowest: the last resort for the widest rows
+  TilePlan best{0, 0};  // tn 0: no width fits shared memory (rows near the 768-byte limit
+                         // with first-match exchange buffers)
   int64_t best_cost = INT64_MAX;
   const bool chunk_ok = !getenv("RSR_FP4_NO_CHUNK_RESIDENT");
   for (int i = 0; i < 6; ++i) {
@@ -1212,6 +1213,12 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   RSR_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, dev));
   const TilePlan plan = pick_tile_n(S, c.sm_count, n_lower, n_upper, row_bytes / kChunk,
                                     first_lower != nullptr || first_upper != nullptr);
+  if (plan.tn == 0) {
+    rsr::set_error("rsr_classify_fp4: %d-byte rows%s do not fit shared memory "
+                   "(rsr_classify_fp4_plan reports tile_n 0; use rsr_classify_tc / _bits)",
+                   row_bytes, (first_lower || first_upper) ? " with first matches" : "");
+    return RSR_EUNSUPPORTED;
+  }
   c.chunk_tiles = plan.chunk_tiles;
   switch (plan.tn) {
     case 224: return launch_fp4<224>(c);
@@ -1519,6 +1526,9 @@ extern "C" int rsr_classify_fp4_plan(int64_t S, int64_t n_lower, int64_t n_upper
   }
   cudaGetLastError();  // no device: clear the sticky error of the probe
   const TilePlan plan = pick_tile_n(S, sm_count, n_lower, n_upper, cq, want_first != 0);
+  *tile_n = plan.tn;
+  *launches = 0;
+  if (plan.tn == 0) return RSR_OK;  // infeasible: no width fits shared memory
   const int64_t nt_l = rsr::ceil_div(n_lower, plan.tn), nt_u = rsr::ceil_div(n_upper, plan.tn);
   const int64_t total = nt_l + nt_u, chunk = launch_chunk_tiles(plan.tn, plan.chunk_tiles);
   const bool split = split_sides_needed(plan.tn, nt_l, nt_u, cq, want_first != 0);

@@ -227,7 +227,9 @@ __device__ __forceinline__ void fp4_quad_fast(const uint8_t* st, uint32_t base, 
 // C32: every Philox counter of the launch fits 32 bits (flat draws < 2^34), so
 // the first round's 64x64 multiply is a 64x32 one (two IMAD.WIDE fewer per block
 // on the FMA pipe, which bounds this kernel).
-template <int MT, bool C32>  // MT 2, 3: specialised state count; 0: any M
+// RPC: rows per chunk (64; 16 for the widest rows, whose 64-row staging buffers would not
+// fit shared memory)
+template <int MT, bool C32, int RPC = kRowsPerCta>  // MT 2, 3: specialised state count; 0: any M
 __global__ void __launch_bounds__(kRowThreads, RSR_SAMPLE_MINB)
 sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed, uint64_t gen,
                    int64_t start_row, int64_t count, uint8_t* __restrict__ states,
@@ -241,12 +243,12 @@ sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed
       reinterpret_cast<uint8_t*>(T) + ((size_t)(N + kTExtra) * Mm1 * 8 + 15) / 16 * 16;
   const int kdim = N * Mm1, words = row_bytes / 4, quads = words / 4;
   const int fastq = MT ? kdim / 32 : 0;  // quads per row on the specialised path
-  const int64_t n_chunks = (count + kRowsPerCta - 1) / kRowsPerCta;
+  const int64_t n_chunks = (count + RPC - 1) / RPC;
   int buf = 0;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x, buf ^= 1) {
     uint8_t* st = st_base + buf * st_bytes;
-    const int64_t r0 = chunk * kRowsPerCta;
-    const int rows = (int)(count - r0 < kRowsPerCta ? count - r0 : kRowsPerCta);
+    const int64_t r0 = chunk * RPC;
+    const int rows = (int)(count - r0 < RPC ? count - r0 : RPC);
     const int span = rows * N;                                     // draws of this chunk
     const int64_t f0 = (start_row + r0) * (int64_t)N;              // first flat draw
     const int64_t b0 = f0 >> 2, b1 = (f0 + span - 1) >> 2;         // Philox blocks
@@ -293,7 +295,7 @@ sample_rows_kernel(const double* __restrict__ probs, int N, int M, uint64_t seed
     __syncthreads();
     if (states) {
       uint8_t* dst = states + r0 * (int64_t)N;
-      if (rows == kRowsPerCta) {  // 64 * N bytes, 16-byte aligned chunk
+      if (rows == RPC) {  // RPC * N bytes, 16-byte aligned chunk
         const int vecs = span / 16;
         for (int i = threadIdx.x; i < vecs; i += blockDim.x)
           reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(st)[i];
@@ -773,14 +775,19 @@ extern "C" int rsr_encode_refs(const uint8_t* states, int64_t count, int64_t row
 }
 
 namespace {
-const void* rows_kernel(int M, bool c32) {
+template <int RPC>
+const void* rows_kernel_rpc(int M, bool c32) {
   if (c32)
-    return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, true>)
-           : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, true>)
-                    : reinterpret_cast<const void*>(sample_rows_kernel<0, true>);
-  return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, false>)
-         : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, false>)
-                  : reinterpret_cast<const void*>(sample_rows_kernel<0, false>);
+    return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, true, RPC>)
+           : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, true, RPC>)
+                    : reinterpret_cast<const void*>(sample_rows_kernel<0, true, RPC>);
+  return M == 2   ? reinterpret_cast<const void*>(sample_rows_kernel<2, false, RPC>)
+         : M == 3 ? reinterpret_cast<const void*>(sample_rows_kernel<3, false, RPC>)
+                  : reinterpret_cast<const void*>(sample_rows_kernel<0, false, RPC>);
+}
+
+const void* rows_kernel(int M, bool c32, int rpc) {
+  return rpc == kRowsPerCta ? rows_kernel_rpc<kRowsPerCta>(M, c32) : rows_kernel_rpc<16>(M, c32);
 }
 
 int launch_dev_rows(const double* probs, int N, int M, uint64_t seed, uint64_t gen, int64_t start,
@@ -861,15 +868,18 @@ extern "C" int rsr_sample_fp4_ex(const double* probs, int n_components, int n_st
               "rsr_sample_fp4: fp4_plane_stride must be 0 or a multiple of 16 >= count*row_bytes");
   const int64_t fp4_row_stride = fp4_plane_stride ? row_bytes : 2 * (int64_t)row_bytes;
   const int64_t fp4_plane = fp4_plane_stride ? fp4_plane_stride : row_bytes;
-  const int st_bytes = (kRowsPerCta * N + 16 + 15) / 16 * 16;  // + funnel-load slack
-  const size_t smem = ((size_t)(N + kTExtra) * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16 +
-                      2 * (size_t)st_bytes;
-  RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample_fp4: N*(M-1) too large for shared memory");
   if (rng == RSR_RNG_DEVICE)
     return launch_dev_rows(probs, N, M, seed, gen, start, count, out_states, out_fp4, row_bytes,
                            fp4_row_stride, fp4_plane, rsr::as_stream(stream));
+  // 64-row chunks, or 16-row ones when two 64-row staging buffers do not fit
+  const size_t t_bytes = ((size_t)(N + kTExtra) * (M - 1) * sizeof(unsigned long long) + 15) / 16 * 16;
+  int rpc = kRowsPerCta;
+  if (t_bytes + 2 * (size_t)((kRowsPerCta * N + 16 + 15) / 16 * 16) > 200 * 1024) rpc = 16;
+  const int st_bytes = (rpc * N + 16 + 15) / 16 * 16;  // + funnel-load slack
+  const size_t smem = t_bytes + 2 * (size_t)st_bytes;
+  RSR_REQUIRE(smem <= 200 * 1024, "rsr_sample_fp4: N*(M-1) too large for shared memory");
   const bool c32 = ((start + count) * (int64_t)N + 3) / 4 + 1 < ((int64_t)1 << 32);
-  const void* kern = rows_kernel(M, c32);
+  const void* kern = rows_kernel(M, c32, rpc);
   if (smem > 48 * 1024) {
     const int rc = rsr::ensure_dynamic_smem(kern, smem);
     if (rc) return rc;
@@ -885,7 +895,7 @@ extern "C" int rsr_sample_fp4_ex(const double* probs, int n_components, int n_st
     const char* e = getenv("RSR_SAMPLE_CPC");
     return e ? std::max(1, atoi(e)) : kChunksPerCta;
   }();
-  const int64_t chunks = rsr::ceil_div(count, kRowsPerCta);
+  const int64_t chunks = rsr::ceil_div(count, rpc);
   const int64_t grid = std::max<int64_t>(std::min<int64_t>(chunks, (int64_t)sms * std::max(per_sm, 1)),
                                          rsr::ceil_div(chunks, cpc));
   void* args[] = {(void*)&probs,     (void*)&N,         (void*)&M,

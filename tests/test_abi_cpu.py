@@ -74,5 +74,9 @@ def test_fp4_launch_plan_is_host_only():
     # a small batch has few sample groups per CTA pair: extra launches do not pay
     assert _abi.fp4_plan(4096, 0, 10_000, rb)[1] == 1
     assert _abi.fp4_plan(S, 0, 0, rb)[1] == 0
+    # the widest rows (768 bytes, N(M-1) up to 1535) fit without first matches only
+    assert _abi.fp4_plan(S, 3000, 700, 768)[0] > 0
+    assert _abi.fp4_plan(S, 3000, 700, 768, want_first=True) == (0, 0)
+    assert _abi.fp4_plan(S, 3000, 700, 736, want_first=True)[0] > 0
     with pytest.raises(ValueError):
         _abi.fp4_plan(S, -1, 0, rb)

@@ -131,3 +131,20 @@ def test_loop_estimates_agree_within_3_combined_se(cfg_name):
         assert 0 < p1 < 1 and 0 < p2 < 1
         assert abs(p1 - p2) <= 3 * se, (cfg_name, p1, p2, se)
         assert p1 != p2  # independent streams
+
+
+@pytest.mark.parametrize("stream", ["shared", "device"])
+@pytest.mark.parametrize("n,m", [(1475, 2), (767, 3)])
+def test_widest_rows_sample_like_the_oracle(stream, n, m):
+    # rows whose 64-row staging buffers exceed shared memory run 16-row chunks (reference
+    # stream) / row-aligned threads (device stream); both equal the oracle, FP4 operand
+    # included (it equals the encoder's rows of the same states)
+    rng = np.random.default_rng(n + m)
+    raw = rng.random((n, m)) + 0.05
+    probs = raw / raw.sum(1, keepdims=True)
+    b = P.sample_batch(P.ComponentDistribution(probs), 300, seed=4, generation_index=2, start=77,
+                       rng=stream)
+    want = oracle.sample_states(probs, 300, 4, 2, 77, rng=stream)
+    assert np.array_equal(b.device_states().cpu().numpy(), want)
+    enc = P.SampleBatch(b.device_states().clone(), 0, 0, state_bound=m).fp4(m)
+    assert torch.equal(b.fp4(m), enc)

@@ -320,3 +320,27 @@ def test_wide_multistate_rows_stay_on_tensor_cores(m, monkeypatch):
     want2 = oracle.classify_labels(oracle.sample_states(probs, h, 9, 0, 0), lower, upper, m,
                                    n_workers=CORES)
     assert np.array_equal(r2.labels_device.cpu().numpy(), want2["labels"])
+
+
+def test_widest_rows_with_first_matches_leave_fp4_cleanly():
+    # 768-byte FP4 rows (N(M-1) = 1475) fit shared memory without first matches but not
+    # with them: explain=True must route to another tensor-core / CUDA-core kernel (the
+    # planner reports tile_n 0) and still give the bit-packed kernel's answers
+    from paper_2604_17066_b200 import _abi
+    n, m, s = 1475, 2, 6000
+    rb = _abi.fp4_row_bytes(n, m)
+    assert rb == 768 and _abi.fp4_plan(s, 500, 300, rb, want_first=True)[0] == 0
+    rng = np.random.default_rng(5)
+    b = P.sample_batch(P.ComponentDistribution.iid(n, [0.03, 0.97]), s, seed=9)
+    up = (rng.random((300, n)) < 0.002).astype(np.uint8)
+    lo = 1 - (rng.random((500, n)) < 0.02).astype(np.uint8)
+    uset = P.ReferenceSet.from_array(P.Side.UPPER, 0, up, trusted=True)
+    lset = P.ReferenceSet.from_array(P.Side.LOWER, 0, lo, trusted=True)
+    for explain in (False, True):
+        r = P.classify(b, lset, uset, n_states=m, explain=explain)
+        rb_ = P.classify(b, lset, uset, n_states=m, method="bits", explain=explain)
+        assert torch.equal(r.labels_device, rb_.labels_device)
+        if explain:
+            assert np.array_equal(r.first_match_upper, rb_.first_match_upper)
+            assert np.array_equal(r.first_match_lower, rb_.first_match_lower)
+    assert min(r.counts) > 0 or r.counts[0] + r.counts[1] > 0
