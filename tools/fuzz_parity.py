@@ -16,11 +16,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
 import paper_2604_17066_b200 as P  # noqa: E402
 from paper_2604_17066_b200 import _abi  # noqa: E402
+from paper_2604_17066_b200.classify import classify_host  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
 rng = np.random.default_rng(int(os.environ.get("SEED", "1")))
 t_end = time.time() + budget
-n_cls = n_smp = 0
+n_cls = n_smp = n_host = 0
 while time.time() < t_end:
     kind = rng.integers(0, 4)
     if kind < 3:  # classification
@@ -56,6 +57,21 @@ while time.time() < t_end:
             print("MISMATCH classify", dict(n=n, m=m, s=s, kl=kl, ku=ku, explain=explain, plan=plan),
                   flush=True)
             sys.exit(1)
+        if rng.random() < 0.25:  # the host-fed end-to-end path on the same samples
+            method = "tc" if rng.random() < 0.7 else "tc8"
+            host = b.device_states().cpu()
+            chunk = int(rng.integers(1, s + 1)) if rng.random() < 0.5 else None
+            try:
+                lab, cnt = classify_host(host, lset, uset, m, chunk_rows=chunk, method=method)
+            except ValueError as e:  # rows too wide for the tensor-core kernels: declared
+                lab = None
+                if "too wide" not in str(e):
+                    raise
+            if lab is not None and not np.array_equal(np.asarray(lab), rb.labels_device.cpu().numpy()):
+                print("MISMATCH classify_host", dict(n=n, m=m, s=s, kl=kl, ku=ku, chunk=chunk,
+                                                     method=method), flush=True)
+                sys.exit(1)
+            n_host += 1
         n_cls += 1
     else:  # sampling vs the oracle
         m = int(rng.integers(2, 6))
@@ -74,5 +90,6 @@ while time.time() < t_end:
             print("MISMATCH sample", dict(n=n, m=m, h=h, start=start, rng=stream, fp4=fp4), flush=True)
             sys.exit(1)
         n_smp += 1
-print(f"fuzz parity: {n_cls} classification cases and {n_smp} sampling cases equal "
+print(f"fuzz parity: {n_cls} classification cases ({n_host} also through classify_host) and "
+      f"{n_smp} sampling cases equal "
       f"({budget:.0f} s, seed {os.environ.get('SEED', '1')})")
