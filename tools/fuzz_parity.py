@@ -21,7 +21,7 @@ from paper_2604_17066_b200.classify import classify_host  # noqa: E402
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
 rng = np.random.default_rng(int(os.environ.get("SEED", "1")))
 t_end = time.time() + budget
-n_cls = n_smp = n_host = 0
+n_cls = n_smp = n_host = n_enc = 0
 while time.time() < t_end:
     kind = rng.integers(0, 4)
     if kind < 3:  # classification
@@ -73,6 +73,27 @@ while time.time() < t_end:
                 sys.exit(1)
             n_host += 1
         n_cls += 1
+    elif rng.random() < 0.15:  # encodings and the full violation-count matrix vs the oracle
+        m = int(rng.integers(2, 7))
+        n = int(rng.integers(1, 200))
+        h, r = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+        xs = rng.integers(0, m, (h, n))
+        rs = rng.integers(0, m, (r, n))
+        kind = "lower_ref" if rng.random() < 0.5 else "upper_ref"
+        es = P.encode_batch(xs, m, "sample")
+        er = P.encode_batch(rs, m, kind)
+        eo_s, eo_r = oracle.encode(xs, m, "sample"), oracle.encode(rs, m, kind)
+        if not np.array_equal(es.data, eo_s) or not np.array_equal(er.data, eo_r) or \
+                not np.array_equal(er.packed, np.packbits(eo_r.astype(np.uint8), axis=1)) or \
+                not np.array_equal(er.packed_complement,
+                                   np.packbits((1 - eo_r).astype(np.uint8), axis=1)):
+            print("MISMATCH encode", dict(n=n, m=m, h=h, r=r, kind=kind), flush=True)
+            sys.exit(1)
+        vc = P.violation_counts(es, er, method="packed" if rng.random() < 0.5 else "unpacked")
+        if not np.array_equal(np.asarray(vc), oracle.violation_counts(xs, rs, m, kind)):
+            print("MISMATCH violation_counts", dict(n=n, m=m, h=h, r=r, kind=kind), flush=True)
+            sys.exit(1)
+        n_enc += 1
     else:  # sampling vs the oracle
         m = int(rng.integers(2, 6))
         n = int(rng.integers(1, 400))
@@ -91,5 +112,5 @@ while time.time() < t_end:
             sys.exit(1)
         n_smp += 1
 print(f"fuzz parity: {n_cls} classification cases ({n_host} also through classify_host) and "
-      f"{n_smp} sampling cases equal "
+      f"{n_smp} sampling cases and {n_enc} encoding / violation-count cases equal "
       f"({budget:.0f} s, seed {os.environ.get('SEED', '1')})")

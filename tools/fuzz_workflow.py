@@ -22,6 +22,7 @@ budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
 rng = np.random.default_rng(int(os.environ.get("SEED", "3")))
 t_end = time.time() + budget
 cases = 0
+n_pmf = 0
 
 
 def random_graph(n_nodes, n_edges):
@@ -57,6 +58,30 @@ while time.time() < t_end:
     thr = int(rng.integers(0, m - 1))
     model = device_model(spec)
     dist = P.ComponentDistribution(probs)
+    if m > 2 and rng.random() < 0.3:  # the whole PMF (thresholds share the batch cache)
+        try:
+            rep = P.multistate_pmf(model, dist, P.RunConfig(**cfg, rng=stream))
+            err = None
+        except ValueError as e:
+            rep, err = None, str(e)
+        phi, nc = oracle_phi(spec)
+        ev = oracle.CountingPhi(phi, nc, m, m)
+        try:
+            want = oracle.multistate_pmf(ev, probs, rng=stream, **cfg)
+            werr = None
+        except ValueError as e:
+            want, werr = None, str(e)
+        if (err is None) != (werr is None) or (rep is not None and (
+                not np.array_equal(rep.pmf, want["pmf"])
+                or not np.array_equal(rep.cumulative_lower, want["cumulative_lower"])
+                or [(r.lower.members, r.upper.members) for r in rep.stage1_results]
+                != [(o["lower"], o["upper"]) for o in want["stage1"]]
+                or model.evaluation_count != ev.count)):
+            print("MISMATCH pmf", spec, cfg, stream, err, werr, flush=True)
+            sys.exit(1)
+        cases += 1
+        n_pmf += 1
+        continue
     s1 = P.stage1_find_references(model, dist, P.RunConfig(**cfg, rng=stream), thr)
     rep = P.stage2_evaluate(model, dist, s1.lower, s1.upper, P.RunConfig(**cfg, rng=stream), thr)
     phi, nc = oracle_phi(spec)
@@ -79,5 +104,6 @@ while time.time() < t_end:
                 print(" got ", str(g_)[:300], "\n want", str(w_)[:300])
         sys.exit(1)
     cases += 1
-print(f"fuzz workflow: {cases} random Stage 1 + Stage 2 cases equal to the oracle "
+print(f"fuzz workflow: {cases} random cases ({n_pmf} whole multistate PMFs, the rest Stage 1 + "
+      f"Stage 2) equal to the oracle "
       f"({budget:.0f} s, seed {os.environ.get('SEED', '3')})")
