@@ -1231,31 +1231,58 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
 }
 
 // ---------------------------------------------------------------- encoders
-// Sample operand row i: [A_up (row_bytes) | A_lo (row_bytes)], element c in
-// byte c/2, low nibble for even c; e2m1 1.0 = 0x2.
-// One warp per sample row: the row's states are staged in shared memory
-// (coalesced byte loads), then each lane builds whole 32-bit words (8 e2m1
-// elements) of A_up and A_lo and stores them.
+// Sample operand row i: [A_up (row_bytes) | A_lo (row_bytes)] (interleaved) or A_up / A_lo
+// planes, element c in byte c/2, low nibble for even c; e2m1 1.0 = 0x2.  A block converts
+// kEncRows rows: their states are one contiguous span, staged in shared memory with aligned
+// 16-byte loads (one warp per row with byte loads left too few bytes in flight: 0.41 ms per
+// 2^20 rows of N = 295, a quarter of the HBM rate), then the threads build whole 32-bit
+// words (8 elements) of both halves, item (row, word).
+constexpr int kEncRows = 32;
+
 __global__ void __launch_bounds__(256) encode_samples_fp4_kernel(
     const uint8_t* __restrict__ states, int64_t count, int N, int M, uint8_t* __restrict__ out,
-    int row_bytes, int kdim, int stage_bytes, int64_t row_stride, int64_t plane) {
-  extern __shared__ uint8_t stage[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* buf = stage + warp * stage_bytes;
-  const int words = row_bytes / 4;
-  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < count; i += (int64_t)gridDim.x * 8) {
-    const uint8_t* x = states + i * N;
-    for (int n = lane; n < N; n += 32) buf[n] = x[n];
-    __syncwarp();
-    uint32_t* up_row = reinterpret_cast<uint32_t*>(out + i * row_stride);
-    uint32_t* lo_row = reinterpret_cast<uint32_t*>(out + i * row_stride + plane);
-    for (int w = lane; w < words; w += 32) {
-      uint32_t up, lo;
-      rsr::fp4_sample_word(buf, w, M, kdim, up, lo);
-      up_row[w] = up;
-      lo_row[w] = lo;
+    int row_bytes, int kdim, int64_t row_stride, int64_t plane) {
+  extern __shared__ __align__(16) uint8_t span[];
+  const int64_t r0 = (int64_t)blockIdx.x * kEncRows;
+  const int nr = (int)(count - r0 < kEncRows ? count - r0 : kEncRows);
+  // aligned 16-byte loads from the span's first aligned address (within the allocation:
+  // device allocations are 256-byte aligned), bytewise at the end of the data
+  const uint8_t* pbeg = states + r0 * N;
+  const uint8_t* pend = pbeg + (int64_t)nr * N;
+  const uint8_t* plim = states + count * N;
+  const uint8_t* pa = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(pbeg) & ~(uintptr_t)15);
+  const int nvec = (int)((pend - pa + 15) >> 4);
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const uint8_t* q = pa + 16 * (int64_t)v;
+    if (q + 16 <= plim) {
+      reinterpret_cast<uint4*>(span)[v] = *reinterpret_cast<const uint4*>(q);
+    } else {
+      for (int j = 0; j < 16; ++j) span[16 * v + j] = q + j < plim ? q[j] : 0;
     }
-    __syncwarp();
+  }
+  __syncthreads();
+  const uint8_t* rows = span + (pbeg - pa);
+  const uint32_t* span32 = reinterpret_cast<const uint32_t*>(span);
+  const int words = row_bytes / 4;
+  for (int t = threadIdx.x; t < nr * words; t += blockDim.x) {
+    const int r = t / words, w = t - r * words;
+    uint32_t up, lo;
+    const int c0 = 8 * w;
+    if (M == 2 && c0 + 8 <= kdim) {
+      // 8 states from three aligned shared-memory words and two funnel shifts
+      const uint32_t o = (uint32_t)(rows - span) + (uint32_t)(r * N + c0);
+      const uint32_t sh = (o & 3u) * 8u, q = o >> 2;
+      const uint32_t w0 = span32[q], w1 = span32[q + 1], w2 = span32[q + 2];
+      const uint32_t a = __funnelshift_r(w0, w1, sh), b = __funnelshift_r(w1, w2, sh);
+      const uint32_t ta = a | (a >> 4), tb = b | (b >> 4);
+      lo = __byte_perm(ta, tb, 0x6420) << 1;  // [x >= 1]
+      up = lo ^ 0x22222222u;                  // [x <  1]
+    } else {
+      rsr::fp4_sample_word(rows + r * N, w, M, kdim, up, lo);
+    }
+    uint8_t* row = out + (r0 + r) * row_stride;
+    reinterpret_cast<uint32_t*>(row)[w] = up;
+    reinterpret_cast<uint32_t*>(row + plane)[w] = lo;
   }
 }
 
@@ -1426,15 +1453,16 @@ extern "C" int rsr_encode_samples_fp4_ex(const uint8_t* states, int64_t count, i
               rsr_fp4_row_bytes(N, M));
   if (count == 0) return RSR_OK;
   RSR_REQUIRE(states != nullptr && out != nullptr, "rsr_encode_samples_fp4: null pointer");
-  const int stage_bytes = (N + 15) / 16 * 16;
-  const size_t smem = 8 * (size_t)stage_bytes;
+  RSR_REQUIRE((reinterpret_cast<uintptr_t>(out) & 3) == 0,
+              "rsr_encode_samples_fp4: out must be 4-byte aligned");
+  const size_t smem = ((size_t)kEncRows * N + 48 + 15) / 16 * 16;  // + funnel-load slack
   if (smem > 48 * 1024)
     RSR_CUDA(cudaFuncSetAttribute(encode_samples_fp4_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int64_t grid = rsr::ceil_div(count, 8);
-  if (grid > 148 * 64) grid = 148 * 64;
+  const int64_t grid = rsr::ceil_div(count, kEncRows);
+  RSR_REQUIRE(grid < (int64_t)1 << 31, "rsr_encode_samples_fp4: count too large");
   encode_samples_fp4_kernel<<<(unsigned)grid, 256, smem, rsr::as_stream(stream)>>>(
-      states, count, N, M, out, row_bytes, N * (M - 1), stage_bytes,
+      states, count, N, M, out, row_bytes, N * (M - 1),
       plane_stride ? row_bytes : 2 * (int64_t)row_bytes, plane_stride ? plane_stride : row_bytes);
   return rsr::check_launch("encode_samples_fp4_kernel");
 }
