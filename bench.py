@@ -385,7 +385,7 @@ def secondary_kernels():
     return out
 
 
-def ncu_traffic(kernel: str, config: str, k: int):
+def ncu_traffic(kernel: str, config: str, k: int, variant: str = ""):
     """DRAM bytes per launch of `kernel` on this workload from the committed ncu
     --set full capture (profiles/ncu_traffic.json: {kernel: {"cfg4_k500000": B, ...}}),
     if present."""
@@ -396,7 +396,7 @@ def ncu_traffic(kernel: str, config: str, k: int):
     except Exception:
         return None
     if isinstance(entry, dict):
-        return entry.get(f"{config}_k{k}")
+        return entry.get(f"{config}_k{k}{variant}")
     return entry if config == "cfg2" else None
 
 
@@ -510,8 +510,33 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
         per_launch = {"tc8": 256, "bits": 1}[method]
         classify_launches = max(1, -(-(tiles(nl) + tiles(nu)) // per_launch))
 
-    def classify_kernel():
-        if method == "tc":
+    # support compaction (classify.fp4_compaction): the library's cost model decides; when
+    # it applies, every step re-packs the resident sample planes over the references'
+    # column support (rsr_fp4_gather_columns, timed inside the step) and the classifier
+    # runs on the narrower rows
+    import importlib
+    C = importlib.import_module("paper_2604_17066_b200.classify")
+    cplan = C.fp4_compaction(S, N_COMP, 2, lower, upper) if method == "tc" else None
+    cbuf = (torch.empty((2, S, cplan.row_bytes), dtype=torch.uint8, device=dev)
+            if cplan is not None else None)
+    if cplan is not None:
+        classify_launches = max(1, _abi.fp4_plan(S, nl, nu, cplan.row_bytes)[1])
+    gev = []  # (start, end) events around the re-pack of each timed step
+
+    def classify_kernel(kev=None):
+        if method == "tc" and cplan is not None:
+            if kev:
+                gev.append((torch.cuda.Event(enable_timing=True),
+                            torch.cuda.Event(enable_timing=True)))
+                gev[-1][0].record()
+            a2, pl2, rb2, (bl2, nl2, al2), (bu2, nu2, au2) = C.fp4_compact_operands(
+                cplan, A, plane, S, width, 2, lower, upper, out=cbuf)
+            if kev:
+                gev[-1][1].record()
+                kev[0].record()
+            _abi.call("rsr_classify_fp4_planar", _abi.ptr(a2), pl2, S, None, _abi.ptr(bl2), nl2,
+                      al2, _abi.ptr(bu2), nu2, au2, rb2, _abi.ptr(flags), None, None, 0, stream)
+        elif method == "tc":
             _abi.call("rsr_classify_fp4_planar", _abi.ptr(A), plane, S, None, _abi.ptr(bl), nl, al,
                       _abi.ptr(bu), nu, au, width, _abi.ptr(flags), None, None, 0, stream)
         elif method == "tc8":
@@ -523,15 +548,15 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
 
     def step(kev=None):
         nonlocal launches
-        if kev:
+        if kev and cplan is None:
             kev[0].record()
-        classify_kernel()
+        classify_kernel(kev)
         if kev:
             kev[1].record()
         if shard_refs:
             ref_comm.allreduce_or_hits(flags)  # OR of hit bits across the ref shards
         _abi.call("rsr_finalize", _abi.ptr(flags), S, _abi.ptr(labels), _abi.ptr(counts), stream)
-        launches += classify_launches + 1
+        launches += classify_launches + 1 + (len(cplan.cols) if cplan is not None else 0)
         if samp_comm.distributed:
             tdist.all_reduce(counts, group=samp_comm.group)
 
@@ -561,9 +586,24 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     ms_per_step = step_ms / steps
     value = S_job * K_job / (ms_per_step * 1e-3)
     final_counts = counts.cpu().tolist()
+    gather_ms = sum(s.elapsed_time(e) for s, e in gev) / len(gev) if gev else 0.0
+    if world > 1 and gev:
+        t = torch.tensor([gather_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        gather_ms = float(t.item())
 
-    # ---- roofline of the dominant kernel (algorithmic ops, unpadded K, per rank)
-    ops_per_pair = 2 * N_COMP * (2 - 1)
+    # ---- roofline of the dominant kernel (algorithmic ops per rank).  The contraction's
+    # algorithmic work per pair is 2 x the thermometer columns it must inspect: all
+    # N(M-1) without compaction, the reference side's column support with it (the
+    # columns no reference uses cannot add a violation); the MMA issues 2 x 64 ops per
+    # 64-column K-step of the padded row
+    if cplan is not None:
+        k_cols = max(c.size - 1 for c in cplan.cols.values())  # bias column not counted
+        mma_cols = cplan.row_bytes * 2
+    else:
+        k_cols = N_COMP * (2 - 1)
+        mma_cols = width * 2 if method == "tc" else width
+    ops_per_pair = 2 * k_cols
     achieved = S * K * ops_per_pair / (kern_avg * 1e-3) / 1e12
     kname = {"tc": "classify_fp4_pair_kernel", "tc8": "classify_tc_pair_kernel",
              "bits": "classify_bits_kernel"}[method]
@@ -575,7 +615,8 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     int8_peak = 4500.0
     peak = 9000.0 if method == "tc" else int8_peak
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
-                "frac": achieved / peak, "traffic": ncu_traffic(kname, config, K), "kernel": kname,
+                "frac": achieved / peak, "traffic": ncu_traffic(kname, config, K,
+                                       f"_rb{cplan.row_bytes}" if cplan is not None else ""), "kernel": kname,
                 "kernel_ms": kern_avg, "kernel_launches_per_step": classify_launches,
                 "ops_per_pair": ops_per_pair, "pairs_per_rank_step": S * K,
                 "peak_source": ("B200 dense FP4 spec = measured tcgen05 kind::mxf4 rate "
@@ -583,7 +624,16 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
                                 "B200 dense int8 spec = measured tcgen05 kind::i8 rate "
                                 "(tools/mma_rate.cu: 4409-4544 TOPS)") +
                                "; MEASURED_PEAKS.json has no int8/fp4 figure",
-                "frac_of_int8_peak": achieved / int8_peak}
+                "frac_of_int8_peak": achieved / int8_peak,
+                "mma_ops_per_pair": 2 * mma_cols,
+                "frac_mma_issued": S * K * 2 * mma_cols / (kern_avg * 1e-3) / 1e12 / peak,
+                "support_compaction": (None if cplan is None else {
+                    "columns": k_cols, "of": N_COMP * (2 - 1),
+                    "row_bytes": [width, cplan.row_bytes],
+                    "repack_ms": gather_ms,
+                    "kernel": "gather_columns_kernel (rsr_fp4_gather_columns)",
+                    "repack_gbs": (S * len(cplan.cols) * (width + cplan.row_bytes) /
+                                   (gather_ms * 1e-3) / 1e9) if gather_ms else None})}
     if method == "bits":
         # the CUDA-core variant is bound by the integer ALU pipe: one LOP3
         # (acc |= x & r) per 32-bit thermometer word and pair

@@ -239,6 +239,20 @@ int rsr_classify_fp4_planar(const uint8_t* A, int64_t a_plane_stride, int64_t S,
  * would return RSR_EUNSUPPORTED: use rsr_classify_tc or rsr_classify_bits. */
 int rsr_classify_fp4_plan(int64_t S, int64_t n_lower, int64_t n_upper, int row_bytes,
                           int want_first, int* tile_n, int64_t* launches);
+/* Support compaction of the FP4 contraction (csrc/fp4_compact.cu).  A thermometer
+ * column in which no reference row of a side is 1 adds 0 to every violation count of
+ * that side (classify.py:42-44; encoding.py:138-153), so the contraction may run over
+ * the side's column support only -- labels, first matches and counts are unchanged.
+ * rsr_fp4_or_rows: out (row_bytes/4 words, cleared by the call) = OR of the first
+ * rows rows of B (rsr_encode_refs_fp4 layout).  rsr_fp4_gather_columns: dst column j =
+ * src column cols[j] for j < n_cols, 0 for j >= n_cols (cols on the device; append the
+ * bias column kdim = N(M-1) so sample rows keep their 1 and pad reference rows stay
+ * never-hit); src / dst rows start every *_stride bytes (multiples of 16, 16-byte
+ * aligned), one sample plane or a reference buffer per call. */
+int rsr_fp4_or_rows(const uint8_t* B, int64_t rows, int row_bytes, uint32_t* out, void* stream);
+int rsr_fp4_gather_columns(const uint8_t* src, int64_t src_stride, int64_t count,
+                           int src_row_bytes, const int32_t* cols, int n_cols, uint8_t* dst,
+                           int64_t dst_stride, int dst_row_bytes, void* stream);
 /* rsr_classify_fp4 over the first *S_dev (device count, <= S_cap) rows of A:
  * the sample count of a later pass is known only on the device. */
 int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,

@@ -105,6 +105,8 @@ EXPORTED = {
                                      _P, _P, _I, _P]),
     "rsr_classify_fp4_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_classify_fp4_plan": (_I, [_I64, _I64, _I64, _I, _I, _P, _P]),
+    "rsr_fp4_or_rows": (_I, [_P, _I64, _I, _P, _P]),
+    "rsr_fp4_gather_columns": (_I, [_P, _I64, _I64, _I, _P, _I, _P, _I64, _I, _P]),
     "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_classify_bits": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_finalize": (_I, [_P, _I64, _P, _P, _P]),

@@ -85,6 +85,7 @@ class ReferenceSet:
         self._thermo: dict[int, list] = {}  # M -> [tensor, encoded_rows]
         self._bits: dict[int, list] = {}
         self._fp4: dict[int, list] = {}  # M -> [tensor, encoded_rows]
+        self._fp4c: dict = {}  # support-compaction caches (device_fp4_support / _compact)
         for m in members:
             self.insert(ReferenceState(tuple(m), side, threshold))
 
@@ -243,6 +244,7 @@ class ReferenceSet:
         self._thermo.clear()
         self._bits.clear()
         self._fp4.clear()
+        self._fp4c.clear()
 
     def _ensure_dev_capacity(self, n: int) -> None:
         cap = 0 if self._dev_rows is None else self._dev_rows.shape[0]
@@ -323,6 +325,49 @@ class ReferenceSet:
         never-hit tile padding) -- the (B, n, avail) triple of rsr_classify_fp4_ex."""
         t, need = self.device_fp4(n_states)
         return t, self._n, need
+
+    def device_fp4_support(self, n_states: int) -> np.ndarray:
+        """Thermometer columns (< kdim) in which some member's FP4 row is 1: the only
+        columns that can add a violation for this side (classify.py:42-44), from an OR
+        of the encoded rows on the device (rsr_fp4_or_rows).  Cached per member count."""
+        key = ("support", n_states)
+        ent = self._fp4c.get(key)
+        if ent is not None and ent[0] == self._n:
+            return ent[1]
+        t, _ = self.device_fp4(n_states)
+        kdim = self._width * (n_states - 1)
+        if t is None:
+            cols = np.zeros(0, dtype=np.int32)
+        else:
+            rb = t.shape[1]
+            words = torch.empty(rb // 4, dtype=torch.int32, device=t.device)
+            _abi.call("rsr_fp4_or_rows", _abi.ptr(t), self._n, rb, _abi.ptr(words), _device.stream())
+            nib = np.frombuffer(words.cpu().numpy().tobytes(), dtype=np.uint8)
+            nib = np.stack([nib & 0xF, nib >> 4], axis=1).reshape(-1)
+            cols = np.flatnonzero(nib[:kdim]).astype(np.int32)
+        self._fp4c[key] = (self._n, cols)
+        return cols
+
+    def device_fp4_compact(self, n_states: int, cols: np.ndarray, row_bytes: int
+                           ) -> tuple[torch.Tensor | None, int, int]:
+        """(B, n, avail) of device_fp4_rows over the column map ``cols`` (host int32,
+        bias column kdim last) in rows of ``row_bytes`` (rsr_fp4_gather_columns);
+        cached for one map per member count."""
+        t, need = self.device_fp4(n_states)
+        if t is None:
+            return None, 0, 0
+        key = ("compact", n_states)
+        ent = self._fp4c.get(key)
+        sig = (self._n, row_bytes, np.asarray(cols, dtype=np.int32).tobytes())
+        if ent is not None and ent[0] == sig:
+            return ent[1], self._n, need
+        cols_dev = torch.from_numpy(np.asarray(cols, dtype=np.int32)).to(t.device)
+        out = torch.empty((need, row_bytes), dtype=torch.uint8, device=t.device)
+        _abi.call("rsr_fp4_gather_columns", _abi.ptr(t), t.shape[1], need, t.shape[1],
+                  _abi.ptr(cols_dev), cols_dev.numel(), _abi.ptr(out), row_bytes, row_bytes,
+                  _device.stream())
+        self._fp4c[key] = (sig, out, cols_dev)
+        return out, self._n, need
 
     def device_bits(self, n_states: int) -> tuple[torch.Tensor | None, int]:
         """Packed thermometer bits ([r < k] lower / [r >= k] upper) and count."""

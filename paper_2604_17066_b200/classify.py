@@ -27,6 +27,7 @@ internally).
 from __future__ import annotations
 
 import math
+import os
 from typing import TYPE_CHECKING
 
 import numpy as np
@@ -213,6 +214,107 @@ class ClassificationResult:
         return cov(self.p_upper, self.n_samples)
 
 
+# Support compaction (csrc/fp4_compact.cu): a thermometer column in which no reference of
+# a side is 1 adds nothing to that side's violation counts, so the FP4 contraction may run
+# over the side's column support only.  It pays when the K-steps it saves on the tensor
+# cores outweigh re-packing the sample planes (HBM): the plan below compares the two.
+# RSR_FP4_COMPACT: "1" (default) cost model, "0" never, "force" whenever columns drop
+_FP4_COMPACT = os.environ.get("RSR_FP4_COMPACT", "1")
+_MMA_OPS_PER_S = 8.8e15     # kind::mxf4 rate of the classifier's issued K-steps
+_REPACK_BYTES_PER_S = 2.5e12  # gather kernel: read + write of the sample planes
+
+
+def _fp4_step_cost(cq: int) -> float:
+    """Classifier time per reference tile in K-step units for rows of cq 64-column K-steps.
+    Below 5 K-steps a tile's MMAs no longer cover the accumulator round trip (commit ->
+    epilogue TMEM load -> release -> issuer, two buffers), so the time stops shrinking
+    in proportion (cfg4, tools/compact_tile_sweep.sh: issued-MMA fraction 0.98 at 5
+    K-steps, 0.855 at 4, 0.69 at 3)."""
+    return {1: 3.5, 2: 4.0, 3: 4.35, 4: 4.68}.get(cq, cq / 0.98)
+_COLS_DEV: dict = {}
+
+
+class Fp4Compaction:
+    """Column maps (bias column kdim last) of the non-empty sides and the compacted row
+    width; ``cols[side]`` is host int32, ``dev[side]`` the device copy."""
+
+    def __init__(self, row_bytes: int, cols: dict):
+        self.row_bytes = row_bytes
+        self.cols = cols
+        self.dev = {}
+        for side, c in cols.items():
+            key = (_device.device().index, c.tobytes())
+            t = _COLS_DEV.get(key)
+            if t is None:
+                if len(_COLS_DEV) > 64:
+                    _COLS_DEV.clear()
+                t = torch.from_numpy(c).to(_device.device())
+                _COLS_DEV[key] = t
+            self.dev[side] = t
+
+
+def fp4_compaction(n_samples: int, n_components: int, n_states: int,
+                   lower_set: ReferenceSet | None, upper_set: ReferenceSet | None,
+                   force: bool | None = None) -> Fp4Compaction | None:
+    """The support-compaction plan of one FP4 classification, or None when it would not
+    save time (``force`` True / False overrides the cost model; RSR_FP4_COMPACT=0 turns
+    it off).  Labels, first matches and counts are the same either way."""
+    if force is None:
+        mode = os.environ.get("RSR_FP4_COMPACT", _FP4_COMPACT)
+        if mode == "0":
+            return None
+        if mode == "force":
+            force = True
+    if force is False:
+        return None
+    rb = _abi.fp4_row_bytes(n_components, n_states)
+    kdim = n_components * (n_states - 1)
+    cols, k_total, rb_out = {}, 0, 32
+    for side, s in ((Side.LOWER, lower_set), (Side.UPPER, upper_set)):
+        if s is None or not len(s):
+            continue
+        sup = s.device_fp4_support(n_states)
+        c = np.concatenate([sup, np.array([kdim], dtype=np.int32)]).astype(np.int32)
+        cols[side] = c
+        k_total += len(s)
+        rb_out = max(rb_out, (c.size + 63) // 64 * 32)
+    if not cols or rb_out >= rb:
+        return None
+    if force is None:
+        saved = (n_samples * k_total * 128 / _MMA_OPS_PER_S *
+                 (_fp4_step_cost(rb // 32) - _fp4_step_cost(rb_out // 32)))
+        cost = n_samples * len(cols) * (rb + rb_out) / _REPACK_BYTES_PER_S + 20e-6
+        if saved <= cost:
+            return None
+    return Fp4Compaction(rb_out, cols)
+
+
+def fp4_compact_operands(plan: Fp4Compaction, a: torch.Tensor, plane: int, n_samples: int,
+                         row_bytes: int, n_states: int, lower_set, upper_set,
+                         out: torch.Tensor | None = None):
+    """Gather the sample planes (planar output [2, H, rb_out]) and the reference rows over
+    the plan's column maps.  Returns (A, plane_stride, row_bytes, (bl, nl, al), (bu, nu, au))
+    for rsr_classify_fp4_planar."""
+    rbo = plan.row_bytes
+    H = n_samples
+    if out is None or out.numel() < 2 * H * rbo:
+        out = torch.empty((2, max(H, 1), rbo), dtype=torch.uint8, device=a.device)
+    st = _device.stream()
+    stride = row_bytes if plane else 2 * row_bytes
+    lo_off = plane if plane else row_bytes
+    base, obase = _abi.ptr(a), _abi.ptr(out)
+    for side, off, ooff in ((Side.UPPER, 0, 0), (Side.LOWER, lo_off, H * rbo)):
+        if side in plan.dev:
+            c = plan.dev[side]
+            _abi.call("rsr_fp4_gather_columns", base + off, stride, H, row_bytes, _abi.ptr(c),
+                      c.numel(), obase + ooff, rbo, rbo, st)
+    bl = (lower_set.device_fp4_compact(n_states, plan.cols[Side.LOWER], rbo)
+          if Side.LOWER in plan.cols else (None, 0, 0))
+    bu = (upper_set.device_fp4_compact(n_states, plan.cols[Side.UPPER], rbo)
+          if Side.UPPER in plan.cols else (None, 0, 0))
+    return out, H * rbo, rbo, bl, bu
+
+
 def _infer_n_states(batch: SampleBatch, lower_set, upper_set) -> int:
     """Largest state in samples or refs + 1 (classify.py:252-262)."""
     if batch._host is not None:
@@ -263,8 +365,13 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
         a = batch.fp4(m_eff)
         plane = batch.fp4_plane_stride(m_eff)
         rb = _abi.fp4_row_bytes(batch.n_components, m_eff)
-        bl, nl, al = lower_set.device_fp4_rows(m_eff) if lower_set is not None else (None, 0, 0)
-        bu, nu, au = upper_set.device_fp4_rows(m_eff) if upper_set is not None else (None, 0, 0)
+        cplan = fp4_compaction(H, batch.n_components, m_eff, lower_set, upper_set)
+        if cplan is not None:
+            a, plane, rb, (bl, nl, al), (bu, nu, au) = fp4_compact_operands(
+                cplan, a, plane, H, rb, m_eff, lower_set, upper_set)
+        else:
+            bl, nl, al = lower_set.device_fp4_rows(m_eff) if lower_set is not None else (None, 0, 0)
+            bu, nu, au = upper_set.device_fp4_rows(m_eff) if upper_set is not None else (None, 0, 0)
         if want_first:
             fl = torch.empty(H, dtype=torch.int64, device=dev)
             fu = torch.empty(H, dtype=torch.int64, device=dev)
@@ -427,6 +534,9 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
         opnd_shape, opnd_dtype = (2 * width,), torch.uint8
         bl, nl, al = lower_set.device_fp4_rows(m_eff) if lower_set is not None else (None, 0, 0)
         bu, nu, au = upper_set.device_fp4_rows(m_eff) if upper_set is not None else (None, 0, 0)
+        # support compaction: each encoded chunk is re-packed over the sides' column
+        # supports before the classifier (fp4_compaction decides for the whole job)
+        cplan = fp4_compaction(S, N, m_eff, lower_set, upper_set)
     else:
         width = _abi.thermo_kpad(N, m_eff)
         if width > TC_MAX_KPAD:
@@ -458,6 +568,9 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
     plane = chunk * width if (fp4 and mode != "onehot") else 0
     flags = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
     st = _device.stream()
+    cbuf = None
+    if fp4 and cplan is not None:  # one buffer: the gather and the classifier share `comp`
+        cbuf = torch.empty((2, chunk, cplan.row_bytes), dtype=torch.uint8, device=dev)
     lo = 0
     for i, n_rows in enumerate(sizes):
         hi = lo + n_rows
@@ -477,7 +590,13 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
         else:
             _abi.call("rsr_encode_samples", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
                       _abi.ptr(opnd[slot]), width, st)
-        if fp4 and plane:
+        if cbuf is not None:
+            a2, pl2, rb2, (bl2, nl2, al2), (bu2, nu2, au2) = fp4_compact_operands(
+                cplan, opnd[slot], plane, hi - lo, width, m_eff, lower_set, upper_set, out=cbuf)
+            _abi.call("rsr_classify_fp4_planar", _abi.ptr(a2), pl2, hi - lo, None, _abi.ptr(bl2),
+                      nl2, al2, _abi.ptr(bu2), nu2, au2, rb2, _abi.ptr(flags[lo:hi]), None, None,
+                      0, st)
+        elif fp4 and plane:
             _abi.call("rsr_classify_fp4_planar", _abi.ptr(opnd[slot]), plane, hi - lo, None,
                       _abi.ptr(bl), nl, al, _abi.ptr(bu), nu, au, width, _abi.ptr(flags[lo:hi]),
                       None, None, 0, st)
