@@ -7,11 +7,14 @@ device Philox sampler) against K = 5x10^5 random simple s-t path references
 (upper side) on the 119-node / 295-edge config-3 graph.  Strong scaling: with
 N GPUs each rank owns 2^22 / N samples of the same stream (start offsets) and
 the whole reference set.  A step is one classification of the resident
-samples against all K references: rsr_classify_fp4_planar (tcgen05 block-scaled
-FP4 0/1 contraction on the planar sample operand, fused any-zero epilogue; the
-launches of rsr_classify_fp4_plan: L2-sized reference chunks at K = 5x10^5) +
-rsr_finalize (labels + counts), plus an NCCL all-reduce of the counts when
-N > 1.  Metric: classified samples x reference states per second (pairs/s).
+samples against all K references: the support-compaction re-pack of the sample
+plane (rsr_fp4_gather_columns: only the ~222 of 295 components some path uses can
+add a violation, so rows shrink from 5 to 4 64-column K-steps; the library's cost
+model decides, classify.fp4_compaction), rsr_classify_fp4_planar (tcgen05
+block-scaled FP4 0/1 contraction, paired accumulators at 4 K-steps, fused any-zero
+epilogue; the launches of rsr_classify_fp4_plan: L2-sized reference chunks at
+K = 5x10^5) + rsr_finalize (labels + counts), plus an NCCL all-reduce of the counts
+when N > 1.  Metric: classified samples x reference states per second (pairs/s).
 `--method tc8` / `bits` time the int8 tcgen05 and bit-packed CUDA-core
 variants instead.
 

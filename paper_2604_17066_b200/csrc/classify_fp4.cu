@@ -45,6 +45,16 @@ constexpr int kChunk = 32;       // bytes per chunk = 64 e2m1 = one MMA K-step
 constexpr int kChunkA = kRowsA * kChunk;  // 4096 B
 constexpr uint32_t kSfaCol = 480, kSfbCol = 496;
 constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
+// Paired accumulators (rows of <= 4 K-steps, no first matches): two reference tiles share
+// one accumulator buffer.  The second tile's MMAs read B scale 2^-6 (ue8m0 0x79) from TMEM
+// column kSfbHiCol, so its products are 2^-133 = 2^16 * 2^-149 and each fp32 accumulator's
+// bit pattern is c1 + 2^16 c2 (both counts <= 255 real columns < 2^8, the sum < 2^24:
+// exact, and bits 16..23 hold c2 even once the value leaves the denormal range).  The MMA
+// time per buffer doubles while the epilogue reads the same 32-bit values (both halves
+// min-reduced by the same 16x2 SIMD mins), so the accumulator round trip that bounds
+// 4-K-step tiles (~600 cycles vs ~500 of MMAs per tile: 0.855 of the MMA rate) is
+// covered again.  Needs kBufs * TN <= kSfbHiCol (TN <= 224).
+constexpr uint32_t kSfbHiCol = 464, kSfbHiByte = 0x79;
 
 // Reference tiles are 240 rows (120 per CTA).  TMEM holds two accumulator
 // buffers of 240 columns (0..479; 480..511 hold the scale factors), so the
@@ -309,6 +319,52 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, uint32_t release_b
   }
 }
 
+// Load HN consecutive full 32-bit accumulator columns (HN registers, HN % 8 == 0).
+template <int HN>
+__device__ __forceinline__ void ld_cols_full(uint32_t taddr, uint32_t* v) {
+  static_assert(HN % 8 == 0, "HN must be a multiple of 8");
+#pragma unroll
+  for (int i = 0; i < HN / 16; ++i) RSR_LD16(taddr + 16 * i, (v + 16 * i));
+  if constexpr (HN % 16 != 0) RSR_LD8(taddr + HN / 16 * 16, (v + HN / 16 * 16));
+}
+
+// Epilogue of one paired buffer (two reference tiles, see kSfbHiCol) for one warp: two
+// rounds of TN/2 full columns (the registers of one packed tile load), the buffer
+// released after the second; 16x2 SIMD mins reduce both tiles' counts at once (low
+// halves: tile a, high halves: tile b).  Columns past a tile's last reference
+// (valid_*) are masked; a missing second tile has valid_b = 0.
+template <int TN>
+__device__ __forceinline__ void epilogue_pair(uint32_t taddr, uint32_t release_bar, int lane,
+                                              int64_t valid_a, int64_t valid_b, bool& any_a,
+                                              bool& any_b) {
+  constexpr int H = TN / 2;
+  uint32_t m[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+#pragma unroll
+  for (int part = 0; part < 2; ++part) {
+    uint32_t v[H];
+    ld_cols_full<H>(taddr + part * H, v);
+    tmem_ld_wait();
+    if (part == 1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(release_bar);
+    }
+    const int c0 = part * H;
+    if (valid_a < c0 + H || valid_b < c0 + H) {
+#pragma unroll
+      for (int c = 0; c < H; ++c) {
+        if (c0 + c >= valid_a) v[c] |= 0x0000FFFFu;
+        if (c0 + c >= valid_b) v[c] |= 0xFFFF0000u;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < H; ++c) m[c & 3] = __vminu2(m[c & 3], v[c]);
+  }
+  const uint32_t r = __vminu2(__vminu2(m[0], m[1]), __vminu2(m[2], m[3]));
+  any_a = (r & 0xFFFFu) == 0;
+  any_b = (r >> 16) == 0;
+}
+
 // MMA issuer of the pair kernel (leader CTA, warp 1).  CQ > 0: compile-time K-steps.
 struct MmaRole {
   uint32_t tm0, a_lo0, b_lo0;
@@ -329,12 +385,12 @@ struct MmaRole {
 #define PROF_ARG
 #endif
 
-template <int TN, int CQ>
+template <int TN, int CQ, bool PAIR>
 __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PROF_PARAM) {
   constexpr uint32_t idesc = mxf4_idesc(2 * kRowsA, TN);
   constexpr int kBufs = Tile<TN>::kBufs;
   constexpr uint32_t kAstep = kChunkA >> 4, kBstep = Tile<TN>::kChunkB >> 4;
-  const uint32_t sfa = m.tm0 + kSfaCol, sfb = m.tm0 + kSfbCol;
+  const uint32_t sfa = m.tm0 + kSfaCol, sfb = m.tm0 + kSfbCol, sfb_hi = m.tm0 + kSfbHiCol;
   // launch constants in registers (the asm statements' memory clobbers would
   // otherwise reload them from the parameter bank on every tile)
   const int cq = CQ > 0 ? CQ : p.cq;
@@ -374,7 +430,11 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
         const int bs = res_tile ? j : stage;
         const uint32_t d = m.tm0 + buf * TN;
         const uint32_t bl = m.b_lo0 + (uint32_t)bs * m.b_stage_desc;
+        // PAIR: odd tiles of the side accumulate into the even tile's buffer
+        const bool second = PAIR && (t & 1);
+        const bool close = !PAIR || second || t + 1 == cnt;
         PROF_T(m0);
+        if (!second) {
 #if RSR_FP4_SPIN
         mbar_spin(m.bar_t_empty + 8 * buf, tphase ^ 1);
 #elif defined(RSR_FP4_X_NOWAIT)
@@ -382,6 +442,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
 #else
         mbar_wait_inline(m.bar_t_empty + 8 * buf, tphase ^ 1);  // tc_common.cuh: why inline
 #endif
+        }
         PROF_T(m1);
 #ifdef RSR_FP4_PROF
         if (gi > 0) {  // release (CTA 0 epilogue, just before its arrive) -> MMA warp sees it
@@ -396,15 +457,18 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
         PROF_ADD(7, 1);
         tc_fence_after();
         if (elect_one()) {
+          const uint32_t sb = second ? sfb_hi : sfb;
           if constexpr (CQ > 0) {
 #pragma unroll
             for (int ks = 0; ks < CQ; ++ks)
-              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
+              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sb,
+                             second || ks != 0);
           } else {
             for (int ks = 0; ks < cq; ++ks)
-              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sfb, ks != 0);
+              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sb,
+                             second || ks != 0);
           }
-          umma_commit_pair(m.bar_t_full + 8 * buf);
+          if (close) umma_commit_pair(m.bar_t_full + 8 * buf);
           if (!res_tile) umma_commit_pair(m.bar_b_empty + 8 * stage);
 #ifdef RSR_FP4_PROF
           const long long tc = clock64();
@@ -417,7 +481,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
           stage = n_res;
           phase ^= 1;
         }
-        if (++buf == kBufs) {
+        if (close && ++buf == kBufs) {
           buf = 0;
           tphase ^= 1;
         }
@@ -435,7 +499,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
   }
 }
 
-template <int TN, bool FIRST>
+template <int TN, bool FIRST, bool PAIR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_lower,
@@ -444,6 +508,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   constexpr int kBufs = Tile<TN>::kBufs;
   constexpr int kHalfRows = Tile<TN>::kHalfRows;
   constexpr int kChunkB = Tile<TN>::kChunkB;
+  static_assert(!PAIR || (!FIRST && kBufs * TN <= (int)kSfbHiCol), "paired accumulators");
   extern __shared__ uint8_t smem_raw[];
 #ifdef RSR_FP4_PROF
   const long long k_entry = clock64();
@@ -525,6 +590,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
         "%1,%1};" ::"r"(addr + kSfbCol),
         "r"(kSfbByte * 0x01010101u));
+    if (PAIR)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+          "%1,%1,%1};" ::"r"(addr + kSfbHiCol),
+          "r"(kSfbHiByte * 0x01010101u));
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
@@ -656,9 +726,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       // <= 639: 10): the MMA warp's instruction count per tile is on the critical path
       // once a tile is only ~500 MMA cycles
       switch (p.cq) {
-        case 5: mma_role<TN, 5>(m, p PROF_ARG); break;
-        case 10: mma_role<TN, 10>(m, p PROF_ARG); break;
-        default: mma_role<TN, 0>(m, p PROF_ARG); break;
+        case 3: mma_role<TN, 3, PAIR>(m, p PROF_ARG); break;
+        case 4: mma_role<TN, 4, PAIR>(m, p PROF_ARG); break;
+        case 5: mma_role<TN, 5, PAIR>(m, p PROF_ARG); break;
+        case 10: mma_role<TN, 10, PAIR>(m, p PROF_ARG); break;
+        default: mma_role<TN, 0, PAIR>(m, p PROF_ARG); break;
       }
     }
   } else if (warp >= 4) {
@@ -671,7 +743,29 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     for (int g = cluster; g < n_groups; g += n_clusters, gpar ^= 1) {
       uint32_t hit = 0;
       int64_t first[2] = {INT64_MAX, INT64_MAX};
-      for (int jj = 0; jj < p.nt_total; ++jj, ++T) {
+      if constexpr (PAIR) {
+        // buffers hold tile pairs of one side in the MMA warp's order (mma_role)
+        for (int h = 0; h < 2; ++h) {
+          const int cnt = h == 0 ? nt_l : nt_u;
+          const int base = h == 0 ? 0 : nt_l;
+          const int64_t n_side = h == 0 ? p.n_lower : p.n_upper;
+          for (int s2 = 0; s2 < cnt; s2 += 2, ++T) {
+            if ((int)(T % kEpiSets) != set) continue;
+            const uint32_t buf = T % kBufs, tphase = (T / kBufs) & 1;
+            const int ja = tile_of(base + s2) - base;
+            const int jb = s2 + 1 < cnt ? tile_of(base + s2 + 1) - base : -1;
+            const int64_t va = n_side - (int64_t)ja * kTileN;
+            const int64_t vb = jb >= 0 ? n_side - (int64_t)jb * kTileN : 0;
+            mbar_wait(smem_addr(&t_full[buf]), tphase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN;
+            bool any_a, any_b;
+            epilogue_pair<kTileN>(taddr, smem_addr(&t_empty[buf]), lane, va, vb, any_a, any_b);
+            if (any_a || any_b) hit |= h == 0 ? RSR_HIT_LOWER : RSR_HIT_UPPER;
+          }
+        }
+      }
+      for (int jj = 0; jj < (PAIR ? 0 : p.nt_total); ++jj, ++T) {
         if (!RSR_FP4_SPLIT_COLS && (int)(T % kEpiSets) != set) continue;
         const uint32_t buf = T % kBufs, tphase = (T / kBufs) & 1;
         const int j = tile_of(jj);
@@ -871,6 +965,7 @@ struct Fp4Call {
   cudaStream_t st;
   int sm_count;
   int64_t chunk_tiles;  // reference tiles per launch (0: the L2-sized default)
+  bool pair;            // paired accumulators (kSfbHiCol)
 };
 
 constexpr size_t kMinSmem = 120 * 1024;  // > half of the SM's 228 KB
@@ -996,7 +1091,10 @@ int launch_fp4(const Fp4Call& c) {
   p.first_lower = c.first[0];
   p.first_upper = c.first[1];
   p.n_groups = (int)rsr::ceil_div(c.S, (int64_t)2 * kRowsA);
-  auto kern = want_first ? classify_fp4_pair_kernel<TN, true> : classify_fp4_pair_kernel<TN, false>;
+  auto kern = want_first ? classify_fp4_pair_kernel<TN, true, false>
+                         : classify_fp4_pair_kernel<TN, false, false>;
+  if constexpr (Tile<TN>::kBufs * TN <= (int)kSfbHiCol)
+    if (c.pair) kern = classify_fp4_pair_kernel<TN, false, true>;
   int clusters = c.sm_count / 2;
   if (p.n_groups < clusters) clusters = p.n_groups;
   p.flag_or = (!want_first && kEpiSets > 1 && (reinterpret_cast<uintptr_t>(c.flags) & 3) == 0 &&
@@ -1093,7 +1191,24 @@ int64_t resident_cap(int tn, bool two_sided, int cq, bool want_first) {
 struct TilePlan {
   int tn;
   int64_t chunk_tiles;  // 0: default (L2-sized chunks, tiles streamed per sample group)
+  bool pair;            // paired accumulators: rows of <= 4 K-steps, no first matches
 };
+
+// Paired accumulators (kSfbHiCol) apply to rows of at most 4 K-steps (every count <= 255)
+// without first matches, at the widths that leave TMEM room for the second B scale;
+// RSR_FP4_PAIR=0 turns them off.
+bool pair_eligible(int cq, bool want_first) {
+  const char* env = getenv("RSR_FP4_PAIR");
+  // 3 K-steps: the paired epilogue's full-width TMEM loads (twice the bytes of the packed
+  // loads) outweigh the longer MMA time per buffer (cfg4 K = 10^4: 2.55 ms paired vs
+  // 2.45 unpaired); at 4 K-steps pairing lifts the issued-MMA fraction 0.855 -> 0.98
+  // (RSR_FP4_PAIR=force: every width up to 4 K-steps, for measurements)
+  // Rows of 1-2 K-steps and resident sets measured slower paired too (the paired
+  // epilogue's second load round sits on the round trip: tools/pair_small_n.py), so the
+  // planner pairs only streamed sets at 4 K-steps (see pick_tile_n).
+  if (want_first || cq > 4 || (env && env[0] == '0')) return false;
+  return cq == 4 || (env && env[0] == 'f');
+}
 
 TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, int cq,
                      bool want_first) {
@@ -1103,6 +1218,11 @@ TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, 
   static const int kCost[] = {1000, 957, 971, 920, 843, 778};  // relative time per tile
   // resident tiles (cfg4 K = 10^3 per-tile times, profiles/r1_tile_n_small_k.txt)
   static const int kCostResident[] = {1000, 956, 935, 869, 862, 779};
+  // paired accumulators: the round trip no longer sets a tile's time, which follows TN
+  // (cfg4 K = 10^5 / 5x10^5 at 4 K-steps: a 208 tile takes 0.924 of a 224 tile;
+  // tools/compact_tile_sweep.sh)
+  static const int kCostPair[] = {0, 1000, 924, 870, 810, 0};
+  (void)kCostPair;
   // Streaming the tiles through the ring costs per sample group, over keeping them
   // resident, about 2.5 tiles for short sets (cfg4 K = 2000: 9 resident tiles of 224 take
   // 0.670 ms, 9 streamed tiles of 240 0.891 ms; profiles/r1_tile_n_small_k.txt) and about
@@ -1120,29 +1240,34 @@ TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, 
                                                           clusters));
   const int64_t kChunkGroupCost = 50 + 24000 / gpc;
   constexpr int64_t kMaxChunks = 16;
+  const bool pair_ok = pair_eligible(cq, want_first);
   for (int tn : kCand)
-    if (tn == forced) return {tn, 0};
+    if (tn == forced) return {tn, 0, pair_ok && tn != 240 && tn != 160};
+  constexpr bool pair = false;  // the unpaired plan first
   // wide rows (>= 12 K-steps, e.g. N = 295 at M >= 4): N = 160 tiles with three
   // accumulator buffers measured 15 % faster than any wider tile (M = 4: 0.895 of
   // peak vs 0.736-0.776; profiles/r2_wide_rows_m2_m5.txt)
   if (cq >= 12 && fp4_feasible(160, rsr::ceil_div(n_lower, 160), rsr::ceil_div(n_upper, 160), cq,
                                want_first))
-    return {160, 0};
-  TilePlan best{0, 0};  // tn 0: no width fits shared memory (rows near the 768-byte limit
+    return {160, 0, false};
+  TilePlan best{0, 0, false};  // tn 0: no width fits shared memory (rows near the 768-byte limit
                          // with first-match exchange buffers)
   int64_t best_cost = INT64_MAX;
   const bool chunk_ok = !getenv("RSR_FP4_NO_CHUNK_RESIDENT");
   for (int i = 0; i < 6; ++i) {
     const int tn = kCand[i];
+    if (pair && (tn == 240 || tn == 160)) continue;  // no TMEM room for the second scale
     const int64_t nt_l = rsr::ceil_div(n_lower, tn), nt_u = rsr::ceil_div(n_upper, tn);
     if (!fp4_feasible(tn, nt_l, nt_u, cq, want_first)) continue;
     const bool resident = fp4_layout(tn, nt_l, nt_u, cq, want_first).resident;
-    int64_t cost = (nt_l + nt_u) * (resident ? kCostResident[i] : kCost[i]);
+    int64_t cost = (nt_l + nt_u) * (pair ? kCostPair[i] : resident ? kCostResident[i] : kCost[i]);
     if (!resident) cost += nt_l + nt_u <= 16 ? 2500 : 1000;  // streaming penalty (above)
     if (cost < best_cost) {
       best_cost = cost;
-      best = {tn, 0};
+      best = {tn, 0, pair};
     }
+    // resident-sized chunks of a streamed set measured slower paired (cfg4 K = 10^4 at 3
+    // K-steps: 3.39 vs 2.55 ms streamed)
     if (resident || !chunk_ok) continue;
     const int64_t nt = nt_l + nt_u;
     const int64_t cap = resident_cap(tn, nt_l > 0 && nt_u > 0, cq, want_first);
@@ -1153,7 +1278,30 @@ TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, 
     const int64_t ccost = nt * kCostResident[i] + (n_ch - 1) * kChunkGroupCost;
     if (ccost < best_cost) {
       best_cost = ccost;
-      best = {tn, per};
+      best = {tn, per, pair};
+    }
+  }
+  // a streamed set at 4 K-steps: paired accumulators, the width by kCostPair (cfg4 K =
+  // 10^5 / 5x10^5: 0.855-0.90 -> 0.97-0.98 of the MMA rate; a set the unpaired plan keeps
+  // resident, whole or in chunks, stays unpaired: K = 2x10^4 0.918 vs 0.85 paired)
+  const char* penv = getenv("RSR_FP4_PAIR");
+  const bool force = penv && penv[0] == 'f';  // tests / measurements: pair every plan
+  if (pair_ok && best.tn && (force || best.chunk_tiles == 0)) {
+    const int64_t bl = rsr::ceil_div(n_lower, best.tn), bu = rsr::ceil_div(n_upper, best.tn);
+    if (force || !fp4_layout(best.tn, bl, bu, cq, want_first).resident) {
+      TilePlan pb{0, 0, true};
+      int64_t pc = INT64_MAX;
+      for (int i = 1; i < 5; ++i) {
+        const int tn = kCand[i];
+        const int64_t nt_l = rsr::ceil_div(n_lower, tn), nt_u = rsr::ceil_div(n_upper, tn);
+        if (!fp4_feasible(tn, nt_l, nt_u, cq, want_first)) continue;
+        const int64_t cost = (nt_l + nt_u) * kCostPair[i];
+        if (cost < pc) {
+          pc = cost;
+          pb.tn = tn;
+        }
+      }
+      if (pb.tn) return pb;
     }
   }
   return best;
@@ -1220,6 +1368,7 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
     return RSR_EUNSUPPORTED;
   }
   c.chunk_tiles = plan.chunk_tiles;
+  c.pair = plan.pair;
   switch (plan.tn) {
     case 224: return launch_fp4<224>(c);
     case 208: return launch_fp4<208>(c);
