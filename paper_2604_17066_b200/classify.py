@@ -57,6 +57,41 @@ class InconsistentReferenceSets(ValueError):
 _FP4_EXACT: dict[int, bool] = {}
 
 
+def _fp4_pair_selfcheck(rng) -> None:
+    """Known answer for the paired accumulators (csrc/classify_fp4.cu kSfbHiCol): the
+    second tile of a buffer counts in bits 16..23 of the fp32 accumulator, which leaves
+    the denormal range once that count reaches 128.  N = 250 rows (4 K-steps), 481
+    references with up to 250 ones (counts 0..~250 in both halves, the three tiles an
+    odd count), paired kernel forced, flags compared with the bit-packed kernel.  On a
+    mismatch pairing is switched off for the process (RSR_FP4_PAIR=0)."""
+    import os
+    n, h, k = 250, 512, 481
+    x = (rng.random((h, n)) < 0.5).astype(np.uint8)
+    up = np.zeros((k, n), dtype=np.uint8)
+    for j in range(k):
+        w = (1 + j % 3) if j % 2 else 150 + j % 100
+        up[j, rng.choice(n, size=w, replace=False)] = 1
+    x[:64] = rng.random((64, n)) < 0.1  # mostly-failed samples: counts of 128..249
+    x[64:, :5] = 1  # some samples dominate some sparse references
+    batch = SampleBatch(_device.to_device(x), 0, 0, state_bound=2)
+    uset = ReferenceSet.from_array(Side.UPPER, 0, up, trusted=True)
+    prev = os.environ.get("RSR_FP4_PAIR")
+    os.environ["RSR_FP4_PAIR"] = "force"
+    try:
+        f4, _, _ = classify_flags(batch, None, uset, 2, "fp4")
+    finally:
+        if prev is None:
+            del os.environ["RSR_FP4_PAIR"]
+        else:
+            os.environ["RSR_FP4_PAIR"] = prev
+    fb, _, _ = classify_flags(batch, None, uset, 2, "bits")
+    if not np.array_equal(f4.cpu().numpy(), fb.cpu().numpy()):
+        import warnings
+        warnings.warn("FP4 paired-accumulator self-check failed: pairing disabled",
+                      RuntimeWarning)
+        os.environ["RSR_FP4_PAIR"] = "0"
+
+
 def fp4_exact() -> bool:
     """Known-answer self-check of the FP4 classifier, once per device.
 
@@ -98,6 +133,8 @@ def fp4_exact() -> bool:
     min_lo = ((1 - lo[None, :, :]) & x[:, None, :]).sum(2).min(1)
     assert (min_up == 1).any() and (min_lo == 1).any() and (want == 3).any()
     ok = bool(np.array_equal(got, want))
+    if ok:
+        _fp4_pair_selfcheck(rng)
     _FP4_EXACT[key] = ok
     if not ok:
         import warnings

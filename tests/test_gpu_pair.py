@@ -119,3 +119,14 @@ def test_plan_reports_paired_widths(monkeypatch):
     for k in (1, 224, 1000, 30_000, 500_000):
         tn, launches = _abi.fp4_plan(1 << 22, 0, k, 128)
         assert tn in (176, 192, 208, 224) and launches >= 1
+
+
+def test_paired_selfcheck_passes(monkeypatch):
+    """classify._fp4_pair_selfcheck (run by fp4_exact on first use): counts of 128..249 in
+    the second tile of a buffer (fp32 normal range) read back exactly, so pairing stays on."""
+    import importlib
+    import os
+    C = importlib.import_module("paper_2604_17066_b200.classify")
+    monkeypatch.delenv("RSR_FP4_PAIR", raising=False)
+    C._fp4_pair_selfcheck(np.random.default_rng(20260419))
+    assert os.environ.get("RSR_FP4_PAIR") is None
