@@ -55,6 +55,12 @@ constexpr uint32_t kSfaByte = 0x00, kSfbByte = 0x69;  // ue8m0 2^-127 and 2^-22
 // 4-K-step tiles (~600 cycles vs ~500 of MMAs per tile: 0.855 of the MMA rate) is
 // covered again.  Needs kBufs * TN <= kSfbHiCol (TN <= 224).
 constexpr uint32_t kSfbHiCol = 464, kSfbHiByte = 0x79;
+// PAIR = 2 ("packed pairs"): the second tile's scale is 2^-14 (0x71), so an accumulator holds
+// c1 + 2^8 c2 < 2^16 -- a denormal whose low 16 bits carry both counts, read with the same
+// .pack::16b loads as an unpaired tile (half the TMEM bytes of PAIR = 1).  The epilogue
+// tests tile b by min16 < 256 and tile a by min16 of the low bytes moved up (one PRMT per
+// register): two 16x2 min chains instead of one, after the buffer is released.
+constexpr uint32_t kSfbHi8Byte = 0x71;
 
 // Reference tiles are 240 rows (120 per CTA).  TMEM holds two accumulator
 // buffers of 240 columns (0..479; 480..511 hold the scale factors), so the
@@ -365,6 +371,40 @@ __device__ __forceinline__ void epilogue_pair(uint32_t taddr, uint32_t release_b
   any_b = (r >> 16) == 0;
 }
 
+// Epilogue of one packed-pair buffer (PAIR = 2) for one warp: one packed load of the TN
+// columns (register i: columns 2i, 2i+1, each c1 + 256 c2), release, then per register
+// chain b takes min16(x) (< 256 <=> some c2 == 0) and chain a min16 of the low bytes moved
+// to the high bytes (< 256 <=> some c1 == 0).  Masked columns get 0xFF in the tile's byte.
+template <int TN>
+__device__ __forceinline__ void epilogue_pair8(uint32_t taddr, uint32_t release_bar, int lane,
+                                               int64_t valid_a, int64_t valid_b, bool& any_a,
+                                               bool& any_b) {
+  constexpr int R = TN / 2;
+  uint32_t v[R];
+  ld_cols_packed<TN>(taddr, v);
+  tmem_ld_wait();
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive_leader(release_bar);
+  if (valid_a < TN || valid_b < TN) {
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      const uint32_t sh = 16 * (c & 1);
+      if (c >= valid_a) v[c / 2] |= 0x00FFu << sh;
+      if (c >= valid_b) v[c / 2] |= 0xFF00u << sh;
+    }
+  }
+  uint32_t ma[2] = {0xFFFFFFFFu, 0xFFFFFFFFu}, mb[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    mb[i & 1] = __vminu2(mb[i & 1], v[i]);
+    ma[i & 1] = __vminu2(ma[i & 1], __byte_perm(v[i], 0u, 0x2404));
+  }
+  const uint32_t a = __vminu2(ma[0], ma[1]), b = __vminu2(mb[0], mb[1]);
+  any_a = (a & 0xFFFFu) < 256u || (a >> 16) < 256u;
+  any_b = (b & 0xFFFFu) < 256u || (b >> 16) < 256u;
+}
+
 // MMA issuer of the pair kernel (leader CTA, warp 1).  CQ > 0: compile-time K-steps.
 struct MmaRole {
   uint32_t tm0, a_lo0, b_lo0;
@@ -385,7 +425,7 @@ struct MmaRole {
 #define PROF_ARG
 #endif
 
-template <int TN, int CQ, bool PAIR>
+template <int TN, int CQ, int PAIR>
 __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PROF_PARAM) {
   constexpr uint32_t idesc = mxf4_idesc(2 * kRowsA, TN);
   constexpr int kBufs = Tile<TN>::kBufs;
@@ -431,7 +471,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
         const uint32_t d = m.tm0 + buf * TN;
         const uint32_t bl = m.b_lo0 + (uint32_t)bs * m.b_stage_desc;
         // PAIR: odd tiles of the side accumulate into the even tile's buffer
-        const bool second = PAIR && (t & 1);
+        const bool second = PAIR != 0 && (t & 1);
         const bool close = !PAIR || second || t + 1 == cnt;
         PROF_T(m0);
         if (!second) {
@@ -499,7 +539,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
   }
 }
 
-template <int TN, bool FIRST, bool PAIR>
+template <int TN, bool FIRST, int PAIR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_lower,
@@ -594,7 +634,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
       asm volatile(
           "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
           "%1,%1,%1};" ::"r"(addr + kSfbHiCol),
-          "r"(kSfbHiByte * 0x01010101u));
+          "r"((PAIR == 2 ? kSfbHi8Byte : kSfbHiByte) * 0x01010101u));
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
@@ -760,7 +800,10 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN;
             bool any_a, any_b;
-            epilogue_pair<kTileN>(taddr, smem_addr(&t_empty[buf]), lane, va, vb, any_a, any_b);
+            if constexpr (PAIR == 2)
+              epilogue_pair8<kTileN>(taddr, smem_addr(&t_empty[buf]), lane, va, vb, any_a, any_b);
+            else
+              epilogue_pair<kTileN>(taddr, smem_addr(&t_empty[buf]), lane, va, vb, any_a, any_b);
             if (any_a || any_b) hit |= h == 0 ? RSR_HIT_LOWER : RSR_HIT_UPPER;
           }
         }
@@ -965,7 +1008,7 @@ struct Fp4Call {
   cudaStream_t st;
   int sm_count;
   int64_t chunk_tiles;  // reference tiles per launch (0: the L2-sized default)
-  bool pair;            // paired accumulators (kSfbHiCol)
+  int pair;             // paired accumulators (kSfbHiCol): 0 off, 1 2^16 halves, 2 packed 2^8
 };
 
 constexpr size_t kMinSmem = 120 * 1024;  // > half of the SM's 228 KB
@@ -1091,10 +1134,12 @@ int launch_fp4(const Fp4Call& c) {
   p.first_lower = c.first[0];
   p.first_upper = c.first[1];
   p.n_groups = (int)rsr::ceil_div(c.S, (int64_t)2 * kRowsA);
-  auto kern = want_first ? classify_fp4_pair_kernel<TN, true, false>
-                         : classify_fp4_pair_kernel<TN, false, false>;
-  if constexpr (Tile<TN>::kBufs * TN <= (int)kSfbHiCol)
-    if (c.pair) kern = classify_fp4_pair_kernel<TN, false, true>;
+  auto kern = want_first ? classify_fp4_pair_kernel<TN, true, 0>
+                         : classify_fp4_pair_kernel<TN, false, 0>;
+  if constexpr (Tile<TN>::kBufs * TN <= (int)kSfbHiCol) {
+    if (c.pair == 1) kern = classify_fp4_pair_kernel<TN, false, 1>;
+    if (c.pair == 2) kern = classify_fp4_pair_kernel<TN, false, 2>;
+  }
   int clusters = c.sm_count / 2;
   if (p.n_groups < clusters) clusters = p.n_groups;
   p.flag_or = (!want_first && kEpiSets > 1 && (reinterpret_cast<uintptr_t>(c.flags) & 3) == 0 &&
@@ -1191,8 +1236,14 @@ int64_t resident_cap(int tn, bool two_sided, int cq, bool want_first) {
 struct TilePlan {
   int tn;
   int64_t chunk_tiles;  // 0: default (L2-sized chunks, tiles streamed per sample group)
-  bool pair;            // paired accumulators: rows of <= 4 K-steps, no first matches
+  int pair;             // paired accumulators: rows of <= 4 K-steps, no first matches
 };
+
+// Which paired encoding (RSR_FP4_PAIR8=1: packed c1 + 2^8 c2 instead of c1 + 2^16 c2).
+int pair_mode() {
+  const char* e = getenv("RSR_FP4_PAIR8");
+  return e && e[0] == '1' ? 2 : 1;
+}
 
 // Paired accumulators (kSfbHiCol) apply to rows of at most 4 K-steps (every count <= 255)
 // without first matches, at the widths that leave TMEM room for the second B scale;
@@ -1242,15 +1293,15 @@ TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, 
   constexpr int64_t kMaxChunks = 16;
   const bool pair_ok = pair_eligible(cq, want_first);
   for (int tn : kCand)
-    if (tn == forced) return {tn, 0, pair_ok && tn != 240 && tn != 160};
-  constexpr bool pair = false;  // the unpaired plan first
+    if (tn == forced) return {tn, 0, pair_ok && tn != 240 && tn != 160 ? pair_mode() : 0};
+  constexpr int pair = 0;  // the unpaired plan first
   // wide rows (>= 12 K-steps, e.g. N = 295 at M >= 4): N = 160 tiles with three
   // accumulator buffers measured 15 % faster than any wider tile (M = 4: 0.895 of
   // peak vs 0.736-0.776; profiles/r2_wide_rows_m2_m5.txt)
   if (cq >= 12 && fp4_feasible(160, rsr::ceil_div(n_lower, 160), rsr::ceil_div(n_upper, 160), cq,
                                want_first))
-    return {160, 0, false};
-  TilePlan best{0, 0, false};  // tn 0: no width fits shared memory (rows near the 768-byte limit
+    return {160, 0, 0};
+  TilePlan best{0, 0, 0};  // tn 0: no width fits shared memory (rows near the 768-byte limit
                          // with first-match exchange buffers)
   int64_t best_cost = INT64_MAX;
   const bool chunk_ok = !getenv("RSR_FP4_NO_CHUNK_RESIDENT");
@@ -1289,7 +1340,7 @@ TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, 
   if (pair_ok && best.tn && (force || best.chunk_tiles == 0)) {
     const int64_t bl = rsr::ceil_div(n_lower, best.tn), bu = rsr::ceil_div(n_upper, best.tn);
     if (force || !fp4_layout(best.tn, bl, bu, cq, want_first).resident) {
-      TilePlan pb{0, 0, true};
+      TilePlan pb{0, 0, pair_mode()};
       int64_t pc = INT64_MAX;
       for (int i = 1; i < 5; ++i) {
         const int tn = kCand[i];

@@ -30,7 +30,9 @@ def _refs(rng, k, n, m, density, side):
 
 
 def _classify(batch, lo, up, m, pair, monkeypatch, method="tc"):
+    """pair: False (unpaired), True / 16 (c1 + 2^16 c2), 8 (packed c1 + 2^8 c2)."""
     monkeypatch.setenv("RSR_FP4_PAIR", "force" if pair else "0")
+    monkeypatch.setenv("RSR_FP4_PAIR8", "1" if pair == 8 else "0")
     monkeypatch.setenv("RSR_FP4_COMPACT", "0")
     r = P.classify(batch, lo, up, n_states=m, method=method)
     return r.labels_device.cpu().numpy(), r.counts
@@ -52,9 +54,11 @@ def test_paired_equals_unpaired_bits_and_oracle(n, m, kl, ku, p_top, monkeypatch
     d = P.ComponentDistribution.iid(n, probs.tolist())
     b = P.sample_batch(d, 70_001, seed=n + m)
     paired, cp = _classify(b, lo, up, m, True, monkeypatch)
+    paired8, cp8 = _classify(b, lo, up, m, 8, monkeypatch)
     plain, c0 = _classify(b, lo, up, m, False, monkeypatch)
     bits, cb = _classify(b, lo, up, m, False, monkeypatch, method="bits")
     assert np.array_equal(paired, plain) and cp == c0
+    assert np.array_equal(paired8, plain) and cp8 == c0
     assert np.array_equal(paired, bits)
     xs = b.device_states()[:1500].cpu().numpy()
     want = oracle.classify_labels(xs, lo_rows, up_rows, m)
@@ -78,13 +82,14 @@ def test_paired_unpadded_reference_buffers(n, k, monkeypatch):
     a = b.fp4(2)
     plane = b.fp4_plane_stride(2)
     out = {}
-    for pair in ("force", "0"):
-        monkeypatch.setenv("RSR_FP4_PAIR", pair)
+    for pair in ("force", "force8", "0"):
+        monkeypatch.setenv("RSR_FP4_PAIR", pair[:5])
+        monkeypatch.setenv("RSR_FP4_PAIR8", "1" if pair == "force8" else "0")
         flags = torch.empty(9001, dtype=torch.uint8, device=dev)
         _abi.call("rsr_classify_fp4_planar", _abi.ptr(a), plane, 9001, None, None, 0, 0,
                   _abi.ptr(bu), k, k, rb, _abi.ptr(flags), None, None, 0, _device.stream())
         out[pair] = flags.cpu().numpy()
-    assert np.array_equal(out["force"], out["0"])
+    assert np.array_equal(out["force"], out["0"]) and np.array_equal(out["force8"], out["0"])
     want = oracle.classify_labels(b.device_states()[:2000].cpu().numpy(),
                                   np.zeros((0, n), np.int64), up_rows, 2)
     got = np.where(out["force"][:2000] & _abi.HIT_UPPER, 1, 2)
@@ -103,12 +108,13 @@ def test_paired_largest_counts(monkeypatch):
     states = np.zeros((4096, n), dtype=np.uint8)
     states[::2, ::3] = 1
     b = P.SampleBatch(states, 0, 0)
-    paired, cp = _classify(b, lo, up, 2, True, monkeypatch)
-    assert cp[1] == 4096 and (paired == 1).all()
-    up2 = P.ReferenceSet.from_array(P.Side.UPPER, 0, np.ones((481, n), np.uint8), trusted=True)
-    paired2, cp2 = _classify(b, lo, up2, 2, True, monkeypatch)
-    plain2, _ = _classify(b, lo, up2, 2, False, monkeypatch)
-    assert cp2[1] == 0 and np.array_equal(paired2, plain2)
+    for mode in (16, 8):
+        paired, cp = _classify(b, lo, up, 2, mode, monkeypatch)
+        assert cp[1] == 4096 and (paired == 1).all()
+        up2 = P.ReferenceSet.from_array(P.Side.UPPER, 0, np.ones((481, n), np.uint8), trusted=True)
+        paired2, cp2 = _classify(b, lo, up2, 2, mode, monkeypatch)
+        plain2, _ = _classify(b, lo, up2, 2, False, monkeypatch)
+        assert cp2[1] == 0 and np.array_equal(paired2, plain2)
 
 
 def test_plan_reports_paired_widths(monkeypatch):

@@ -23,8 +23,9 @@ for n in (40, 120, 180, 250):
         rb = _abi.fp4_row_bytes(n, 2)
         flags = torch.empty(S, dtype=torch.uint8, device=_device.device())
         res = {}
-        for pair in ("0", "force"):
-            os.environ["RSR_FP4_PAIR"] = pair
+        for pair in ("0", "force", "force8"):
+            os.environ["RSR_FP4_PAIR"] = pair[:5]
+            os.environ["RSR_FP4_PAIR8"] = "1" if pair == "force8" else "0"
             tn = _abi.fp4_plan(S, 0, nu, rb)[0]
             run = lambda: _abi.call("rsr_classify_fp4_planar", _abi.ptr(a), plane, S, None, None, 0,
                                     0, _abi.ptr(bu), nu, au, rb, _abi.ptr(flags), None, None, 0,
@@ -41,5 +42,5 @@ for n in (40, 120, 180, 250):
             ms = e0.elapsed_time(e1) / reps
             frac = S * k * 2 * 64 * (rb // 32) / (ms * 1e-3) / 9e15
             res[pair] = (tn, round(ms, 4), round(frac, 3))
-        print(f"N={n} cq={rb // 32} K={k}: unpaired tn/ms/mma_frac {res['0']}  paired {res["force"]}",
+        print(f"N={n} cq={rb // 32} K={k}: unpaired tn/ms/mma_frac {res['0']}  paired16 {res['force']}  paired8 {res['force8']}",
               flush=True)
