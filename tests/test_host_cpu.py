@@ -278,3 +278,25 @@ def test_upper_boundary_walk_is_max_spanning_forest_path(seed):
                 assert got == vec and calls == ev.count, (name, thr, trial)
                 checked += 1
     assert checked > 10
+
+
+@pytest.mark.parametrize("m", [2, 3])
+def test_support_compaction_preserves_violation_counts(m):
+    """The identity behind the FP4 support compaction (csrc/fp4_compact.cu): dropping the
+    thermometer columns no reference of a side uses leaves every violation count of that
+    side unchanged (oracle.violation_counts, classify.py:57-96), so labels cannot change.
+    Checked here on the oracle: components outside the references' support removed from
+    samples and references alike."""
+    import oracle
+    rng = np.random.default_rng(m)
+    n, h, k = 60, 300, 80
+    x = rng.integers(0, m, size=(h, n))
+    up = rng.integers(0, m, size=(k, n)) * (rng.random((k, n)) < 0.15)
+    up[:, 10:25] = 0  # upper references never require these components
+    lo = (m - 1) - rng.integers(0, m, size=(k, n)) * (rng.random((k, n)) < 0.15)
+    lo[:, 40:] = m - 1  # lower references never fall below the top level here
+    for refs, kind in ((up, "upper_ref"), (lo, "lower_ref")):
+        keep = (refs > 0).any(0) if kind == "upper_ref" else (refs < m - 1).any(0)
+        full = oracle.violation_counts(x, refs, m, kind)
+        comp = oracle.violation_counts(x[:, keep], refs[:, keep], m, kind)
+        assert not keep.all() and np.array_equal(full, comp)
