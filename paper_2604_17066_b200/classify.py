@@ -334,8 +334,9 @@ def fp4_compact_operands(plan: Fp4Compaction, a: torch.Tensor, plane: int, n_sam
     for rsr_classify_fp4_planar."""
     rbo = plan.row_bytes
     H = n_samples
-    if out is None or out.numel() < 2 * H * rbo:
-        out = torch.empty((2, max(H, 1), rbo), dtype=torch.uint8, device=a.device)
+    planes = 2 if Side.LOWER in plan.cols else 1  # upper alone reads only the A_up plane
+    if out is None or out.numel() < planes * H * rbo:
+        out = torch.empty((planes, max(H, 1), rbo), dtype=torch.uint8, device=a.device)
     st = _device.stream()
     stride = row_bytes if plane else 2 * row_bytes
     lo_off = plane if plane else row_bytes
