@@ -523,22 +523,18 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     cbuf = (torch.empty((2, S, cplan.row_bytes), dtype=torch.uint8, device=dev)
             if cplan is not None else None)
     if cplan is not None:
-        classify_launches = max(1, _abi.fp4_plan(S, nl, nu, cplan.row_bytes)[1])
+        classify_launches = max(1, _abi.fp4_plan(
+            S, nl, cplan.n_pad if cplan.tail_tn else nu, cplan.row_bytes)[1])
     gev = []  # (start, end) events around the re-pack of each timed step
 
     def classify_kernel(kev=None):
         if method == "tc" and cplan is not None:
-            if kev:
-                gev.append((torch.cuda.Event(enable_timing=True),
-                            torch.cuda.Event(enable_timing=True)))
-                gev[-1][0].record()
-            a2, pl2, rb2, (bl2, nl2, al2), (bu2, nu2, au2) = C.fp4_compact_operands(
-                cplan, A, plane, S, width, 2, lower, upper, out=cbuf)
-            if kev:
-                gev[-1][1].record()
-                kev[0].record()
-            _abi.call("rsr_classify_fp4_planar", _abi.ptr(a2), pl2, S, None, _abi.ptr(bl2), nl2,
-                      al2, _abi.ptr(bu2), nu2, au2, rb2, _abi.ptr(flags), None, None, 0, stream)
+            evs = None
+            if kev:  # re-pack start, classifier start (= re-pack end)
+                gev.append((torch.cuda.Event(enable_timing=True), kev[0]))
+                evs = gev[-1]
+            C.fp4_classify_compacted(cplan, A, plane, S, width, 2, lower, upper, flags,
+                                     out=cbuf, events=evs)
         elif method == "tc":
             _abi.call("rsr_classify_fp4_planar", _abi.ptr(A), plane, S, None, _abi.ptr(bl), nl, al,
                       _abi.ptr(bu), nu, au, width, _abi.ptr(flags), None, None, 0, stream)
@@ -602,7 +598,8 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     # 64-column K-step of the padded row
     if cplan is not None:
         k_cols = max(c.size - 1 for c in cplan.cols.values())  # bias column not counted
-        mma_cols = cplan.row_bytes * 2
+        # shared tail: 7 of the 8 K-steps of a tile pair are issued
+        mma_cols = cplan.row_bytes * 2 * (7 / 8 if cplan.tail_tn else 1)
     else:
         k_cols = N_COMP * (2 - 1)
         mma_cols = width * 2 if method == "tc" else width
@@ -633,6 +630,7 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
                 "support_compaction": (None if cplan is None else {
                     "columns": k_cols, "of": N_COMP * (2 - 1),
                     "row_bytes": [width, cplan.row_bytes],
+                    "shared_tail_tile_n": cplan.tail_tn or None,
                     "repack_ms": gather_ms,
                     "kernel": "gather_columns_kernel (rsr_fp4_gather_columns)",
                     "repack_gbs": (S * len(cplan.cols) * (width + cplan.row_bytes) /

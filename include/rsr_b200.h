@@ -253,6 +253,19 @@ int rsr_fp4_or_rows(const uint8_t* B, int64_t rows, int row_bytes, uint32_t* out
 int rsr_fp4_gather_columns(const uint8_t* src, int64_t src_stride, int64_t count,
                            int src_row_bytes, const int32_t* cols, int n_cols, uint8_t* dst,
                            int64_t dst_stride, int dst_row_bytes, void* stream);
+/* Shared-tail paired classification (upper side only, no first matches): A is the planar
+ * sample operand re-packed to 128-byte rows [192 main columns | 32 tail | the same 32 tail]
+ * and B_upper holds n_upper rows (whole pairs of tile_n-row tiles, never-hit pad rows at the
+ * end) of [192 main | own tail | 32 zero] in which every even tile's last 16 bytes carry the
+ * next tile's tail (the host layout of classify.fp4_compaction).  tile_n must be the tile
+ * width rsr_classify_fp4_plan_ex reports as paired for these sizes; otherwise
+ * RSR_EUNSUPPORTED.  Labels equal rsr_classify_fp4 on the same columns. */
+int rsr_classify_fp4_tail(const uint8_t* A, int64_t a_plane_stride, int64_t S,
+                          const uint8_t* B_upper, int64_t n_upper, int row_bytes, int tile_n,
+                          uint8_t* flags, int accumulate, void* stream);
+/* rsr_classify_fp4_plan plus whether the plan pairs accumulators (streamed, 4 K-steps). */
+int rsr_classify_fp4_plan_ex(int64_t S, int64_t n_lower, int64_t n_upper, int row_bytes,
+                             int want_first, int* tile_n, int64_t* launches, int* paired);
 /* rsr_classify_fp4 over the first *S_dev (device count, <= S_cap) rows of A:
  * the sample count of a later pass is known only on the device. */
 int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,

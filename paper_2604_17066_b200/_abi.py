@@ -106,6 +106,8 @@ EXPORTED = {
     "rsr_classify_fp4_explain": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
     "rsr_classify_fp4_plan": (_I, [_I64, _I64, _I64, _I, _I, _P, _P]),
     "rsr_fp4_or_rows": (_I, [_P, _I64, _I, _P, _P]),
+    "rsr_classify_fp4_tail": (_I, [_P, _I64, _I64, _P, _I64, _I, _I, _P, _I, _P]),
+    "rsr_classify_fp4_plan_ex": (_I, [_I64, _I64, _I64, _I, _I, _P, _P, _P]),
     "rsr_fp4_gather_columns": (_I, [_P, _I64, _I64, _I, _P, _I, _P, _I64, _I, _P]),
     "rsr_pack_thermo_bits": (_I, [_P, _I64, _I, _I, _I, _P, _I, _P]),
     "rsr_classify_bits": (_I, [_P, _I64, _P, _I64, _P, _I64, _I, _P, _P, _P, _I, _P]),
@@ -234,6 +236,15 @@ def fp4_plan(n_samples: int, n_lower: int, n_upper: int, row_bytes: int,
     call("rsr_classify_fp4_plan", n_samples, n_lower, n_upper, row_bytes, int(want_first),
          ctypes.addressof(tn), ctypes.addressof(launches))
     return tn.value, launches.value
+
+
+def fp4_plan_ex(n_samples: int, n_lower: int, n_upper: int, row_bytes: int,
+                want_first: bool = False) -> tuple[int, int, bool]:
+    """(tile_n, launches, paired) of rsr_classify_fp4_plan_ex (host only)."""
+    tn, nl, pr = ctypes.c_int(0), ctypes.c_int64(0), ctypes.c_int(0)
+    call("rsr_classify_fp4_plan_ex", n_samples, n_lower, n_upper, row_bytes, int(want_first),
+         ctypes.addressof(tn), ctypes.addressof(nl), ctypes.addressof(pr))
+    return tn.value, nl.value, bool(pr.value)
 
 
 def thermo_words(n: int, m: int) -> int:

@@ -369,6 +369,31 @@ class ReferenceSet:
         self._fp4c[key] = (sig, out, cols_dev)
         return out, self._n, need
 
+    def device_fp4_tail(self, n_states: int, cols: np.ndarray, tile_n: int, n_pad: int
+                        ) -> torch.Tensor:
+        """Reference rows in the shared-tail layout of rsr_classify_fp4_tail: the FP4 rows
+        re-packed over ``cols`` ([bias + 191 main | 32 tail | 32 unused], host int32, -1 =
+        empty), ``n_pad`` rows (whole pairs of ``tile_n``-row tiles; rows past the members
+        never-hit), and in every even tile the last 16 bytes (columns 224..255) holding the
+        next tile's tail (columns 192..223).  Cached for one layout per member count."""
+        t, need = self.device_fp4(n_states)
+        key = ("tail", n_states)
+        sig = (self._n, tile_n, n_pad, np.asarray(cols, dtype=np.int32).tobytes())
+        ent = self._fp4c.get(key)
+        if ent is not None and ent[0] == sig:
+            return ent[1]
+        dev = t.device
+        out = torch.zeros((n_pad, 128), dtype=torch.uint8, device=dev)
+        out[:, 0] = 0x02  # never-hit pad rows: the bias column (column 0) only
+        cols_dev = torch.from_numpy(np.asarray(cols, dtype=np.int32)).to(dev)
+        rows = min(need, n_pad)
+        _abi.call("rsr_fp4_gather_columns", _abi.ptr(t), t.shape[1], rows, t.shape[1],
+                  _abi.ptr(cols_dev), cols_dev.numel(), _abi.ptr(out), 128, 128, _device.stream())
+        v = out.view(n_pad // (2 * tile_n), 2, tile_n, 128)
+        v[:, 0, :, 112:128] = v[:, 1, :, 96:112]
+        self._fp4c[key] = (sig, out, cols_dev)
+        return out
+
     def device_bits(self, n_states: int) -> tuple[torch.Tensor | None, int]:
         """Packed thermometer bits ([r < k] lower / [r >= k] upper) and count."""
         if self._n == 0:

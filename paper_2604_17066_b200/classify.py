@@ -278,6 +278,9 @@ class Fp4Compaction:
     def __init__(self, row_bytes: int, cols: dict):
         self.row_bytes = row_bytes
         self.cols = cols
+        self.tail_tn = 0  # > 0: shared-tail layout (rsr_classify_fp4_tail) of tile_n tiles
+        self.n_pad = 0
+        self.tail_cols = None  # (sample map, reference map)
         self.dev = {}
         for side, c in cols.items():
             key = (_device.device().index, c.tobytes())
@@ -292,7 +295,7 @@ class Fp4Compaction:
 
 def fp4_compaction(n_samples: int, n_components: int, n_states: int,
                    lower_set: ReferenceSet | None, upper_set: ReferenceSet | None,
-                   force: bool | None = None) -> Fp4Compaction | None:
+                   force: bool | None = None, want_first: bool = False) -> Fp4Compaction | None:
     """The support-compaction plan of one FP4 classification, or None when it would not
     save time (``force`` True / False overrides the cost model; RSR_FP4_COMPACT=0 turns
     it off).  Labels, first matches and counts are the same either way."""
@@ -323,7 +326,76 @@ def fp4_compaction(n_samples: int, n_components: int, n_states: int,
         cost = n_samples * len(cols) * (rb + rb_out) / _REPACK_BYTES_PER_S + 20e-6
         if saved <= cost:
             return None
-    return Fp4Compaction(rb_out, cols)
+    plan = Fp4Compaction(rb_out, cols)
+    if not want_first and list(cols) == [Side.UPPER] and rb_out == 128:
+        _fp4_tail_layout(plan, n_samples, len(upper_set), n_components * (n_states - 1))
+    return plan
+
+
+def _fp4_tail_layout(plan: Fp4Compaction, n_samples: int, n_refs: int, kdim: int) -> None:
+    """Shared-tail layout (csrc/classify_fp4.cu PAIR = 3) when the compacted upper rows have
+    193..224 columns and the library pairs this set's accumulators: 192 main columns (the
+    bias first) plus a tail of <= 32 that tile pairs share in one MMA (7 MMAs per pair
+    instead of 8).  Off by default (RSR_FP4_TAIL=1 turns it on): exact, but measured no
+    faster -- cfg4 K = 5x10^5 121.9 ms with it, 121.3 without (profiles/r2_pair_sweep.txt):
+    with 7 K-steps per buffer the paired accumulator round trip sets the pace again."""
+    c = plan.cols[Side.UPPER]
+    if os.environ.get("RSR_FP4_TAIL", "0") != "1" or not (192 < c.size <= 224):
+        return
+    tn, _, paired = _abi.fp4_plan_ex(n_samples, 0, n_refs, 128)
+    if not paired:
+        return
+    n_pad = -(-n_refs // (2 * tn)) * 2 * tn
+    tn2, _, paired2 = _abi.fp4_plan_ex(n_samples, 0, n_pad, 128)
+    if not paired2 or tn2 != tn:
+        return
+    sup = c[:-1]
+    main = np.concatenate([np.array([kdim], np.int32), sup[:191]])
+    tail = np.full(32, -1, np.int32)
+    tail[: sup.size - 191] = sup[191:]
+    plan.tail_tn, plan.n_pad = tn, n_pad
+    plan.tail_cols = (np.concatenate([main, tail, tail]).astype(np.int32),
+                      np.concatenate([main, tail, np.full(32, -1, np.int32)]).astype(np.int32))
+    key = (_device.device().index, plan.tail_cols[0].tobytes())
+    t = _COLS_DEV.get(key)
+    if t is None:
+        t = torch.from_numpy(plan.tail_cols[0]).to(_device.device())
+        _COLS_DEV[key] = t
+    plan.dev["tail"] = t
+
+
+def fp4_classify_compacted(plan: Fp4Compaction, a: torch.Tensor, plane: int, n_samples: int,
+                           row_bytes: int, n_states: int, lower_set, upper_set,
+                           flags: torch.Tensor, first_lower=None, first_upper=None,
+                           out: torch.Tensor | None = None, accumulate: int = 0,
+                           events=None) -> None:
+    """Re-pack the samples over the plan's column maps and run the classifier on them
+    (rsr_classify_fp4_tail for the shared-tail layout, else rsr_classify_fp4_planar).
+    ``events``: optional (re-pack start, classifier start) CUDA events (bench.py)."""
+    st = _device.stream()
+    H = n_samples
+    if events:
+        events[0].record()
+    if plan.tail_tn:
+        if out is None or out.numel() < H * 128:
+            out = torch.empty((1, max(H, 1), 128), dtype=torch.uint8, device=a.device)
+        stride = row_bytes if plane else 2 * row_bytes
+        c = plan.dev["tail"]
+        _abi.call("rsr_fp4_gather_columns", _abi.ptr(a), stride, H, row_bytes, _abi.ptr(c),
+                  c.numel(), _abi.ptr(out), 128, 128, st)
+        bu = upper_set.device_fp4_tail(n_states, plan.tail_cols[1], plan.tail_tn, plan.n_pad)
+        if events:
+            events[1].record()
+        _abi.call("rsr_classify_fp4_tail", _abi.ptr(out), H * 128, H, _abi.ptr(bu), plan.n_pad,
+                  128, plan.tail_tn, _abi.ptr(flags), accumulate, st)
+        return
+    a2, pl2, rb2, (bl, nl, al), (bu, nu, au) = fp4_compact_operands(
+        plan, a, plane, H, row_bytes, n_states, lower_set, upper_set, out=out)
+    if events:
+        events[1].record()
+    _abi.call("rsr_classify_fp4_planar", _abi.ptr(a2), pl2, H, None, _abi.ptr(bl), nl, al,
+              _abi.ptr(bu), nu, au, rb2, _abi.ptr(flags), _abi.ptr(first_lower),
+              _abi.ptr(first_upper), accumulate, st)
 
 
 def fp4_compact_operands(plan: Fp4Compaction, a: torch.Tensor, plane: int, n_samples: int,
@@ -403,10 +475,15 @@ def classify_flags(batch: SampleBatch, lower_set: ReferenceSet | None,
         a = batch.fp4(m_eff)
         plane = batch.fp4_plane_stride(m_eff)
         rb = _abi.fp4_row_bytes(batch.n_components, m_eff)
-        cplan = fp4_compaction(H, batch.n_components, m_eff, lower_set, upper_set)
+        cplan = fp4_compaction(H, batch.n_components, m_eff, lower_set, upper_set,
+                               want_first=want_first)
         if cplan is not None:
-            a, plane, rb, (bl, nl, al), (bu, nu, au) = fp4_compact_operands(
-                cplan, a, plane, H, rb, m_eff, lower_set, upper_set)
+            if want_first:
+                fl = torch.empty(H, dtype=torch.int64, device=dev)
+                fu = torch.empty(H, dtype=torch.int64, device=dev)
+            fp4_classify_compacted(cplan, a, plane, H, rb, m_eff, lower_set, upper_set, flags,
+                                   fl, fu)
+            return flags, fl, fu
         else:
             bl, nl, al = lower_set.device_fp4_rows(m_eff) if lower_set is not None else (None, 0, 0)
             bu, nu, au = upper_set.device_fp4_rows(m_eff) if upper_set is not None else (None, 0, 0)
@@ -629,11 +706,8 @@ def _classify_host_stream(host, N, n_states, lower_set, upper_set, chunk_rows, l
             _abi.call("rsr_encode_samples", _abi.ptr(bufs[slot]), hi - lo, N, m_eff,
                       _abi.ptr(opnd[slot]), width, st)
         if cbuf is not None:
-            a2, pl2, rb2, (bl2, nl2, al2), (bu2, nu2, au2) = fp4_compact_operands(
-                cplan, opnd[slot], plane, hi - lo, width, m_eff, lower_set, upper_set, out=cbuf)
-            _abi.call("rsr_classify_fp4_planar", _abi.ptr(a2), pl2, hi - lo, None, _abi.ptr(bl2),
-                      nl2, al2, _abi.ptr(bu2), nu2, au2, rb2, _abi.ptr(flags[lo:hi]), None, None,
-                      0, st)
+            fp4_classify_compacted(cplan, opnd[slot], plane, hi - lo, width, m_eff, lower_set,
+                                   upper_set, flags[lo:hi], out=cbuf)
         elif fp4 and plane:
             _abi.call("rsr_classify_fp4_planar", _abi.ptr(opnd[slot]), plane, hi - lo, None,
                       _abi.ptr(bl), nl, al, _abi.ptr(bu), nu, au, width, _abi.ptr(flags[lo:hi]),

@@ -61,6 +61,14 @@ constexpr uint32_t kSfbHiCol = 464, kSfbHiByte = 0x79;
 // tests tile b by min16 < 256 and tile a by min16 of the low bytes moved up (one PRMT per
 // register): two 16x2 min chains instead of one, after the buffer is released.
 constexpr uint32_t kSfbHi8Byte = 0x71;
+// PAIR = 3 ("shared tail"): rows of 4 K-steps whose columns are [192 main | 32 tail | the
+// same 32 tail] on the sample side.  The even tile a of each pair (2p, 2p+1) carries in its
+// last K-step [its own tail | tile b's tail] (the host builds that layout), so one MMA
+// covers both tiles' tail columns: A scale 2^-127 on K-block 0 and 2^-111 (x 2^16) on
+// K-block 1 (TMEM column kSfaTailCol, word p.sfa_tail_word).  Tile a issues 4 MMAs,
+// tile b 3: 7 instead of 8 per pair.  Needs kBufs * TN <= kSfaTailCol and pair-aligned
+// tile sequences (even rotation, even tile counts: the host pads with never-hit tiles).
+constexpr uint32_t kSfaTailCol = 448;
 
 // Reference tiles are 240 rows (120 per CTA).  TMEM holds two accumulator
 // buffers of 240 columns (0..479; 480..511 hold the scale factors), so the
@@ -162,6 +170,7 @@ struct Fp4Params {
   const int64_t* S_dev;  // optional device sample count (<= S): rows [S_dev, S) are skipped
   int flag_or;      // flags merged with 32-bit atomic ORs (no FIRST; flags 4-byte aligned,
                     // zeroed before the first launch unless accumulating)
+  uint32_t sfa_tail_word;  // PAIR = 3: the A scale-factor word of the shared tail K-step
 };
 
 // SW32 K-major descriptor: 8-row core groups 256 B apart, version 1, layout 6.
@@ -431,6 +440,7 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
   constexpr int kBufs = Tile<TN>::kBufs;
   constexpr uint32_t kAstep = kChunkA >> 4, kBstep = Tile<TN>::kChunkB >> 4;
   const uint32_t sfa = m.tm0 + kSfaCol, sfb = m.tm0 + kSfbCol, sfb_hi = m.tm0 + kSfbHiCol;
+  const uint32_t sfa_tail = m.tm0 + kSfaTailCol;
   // launch constants in registers (the asm statements' memory clobbers would
   // otherwise reload them from the parameter bank on every tile)
   const int cq = CQ > 0 ? CQ : p.cq;
@@ -498,7 +508,15 @@ __device__ __forceinline__ void mma_role(const MmaRole& m, const Fp4Params& p PR
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sb = second ? sfb_hi : sfb;
-          if constexpr (CQ > 0) {
+          if constexpr (PAIR == 3 && CQ == 4) {
+            // main K-steps of either tile; the shared tail K-step with tile a only
+#pragma unroll
+            for (int ks = 0; ks < 3; ++ks)
+              umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sb,
+                             second || ks != 0);
+            if (!second)
+              umma_mxf4_pair(d, al + 3 * kAstep, bl + 3 * kBstep, idesc, sfa_tail, sfb, true);
+          } else if constexpr (CQ > 0) {
 #pragma unroll
             for (int ks = 0; ks < CQ; ++ks)
               umma_mxf4_pair(d, al + ks * kAstep, bl + ks * kBstep, idesc, sfa, sb,
@@ -549,6 +567,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   constexpr int kHalfRows = Tile<TN>::kHalfRows;
   constexpr int kChunkB = Tile<TN>::kChunkB;
   static_assert(!PAIR || (!FIRST && kBufs * TN <= (int)kSfbHiCol), "paired accumulators");
+  static_assert(PAIR != 3 || kBufs * TN <= (int)kSfaTailCol, "shared-tail pairs");
   extern __shared__ uint8_t smem_raw[];
 #ifdef RSR_FP4_PROF
   const long long k_entry = clock64();
@@ -635,6 +654,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
           "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
           "%1,%1,%1};" ::"r"(addr + kSfbHiCol),
           "r"((PAIR == 2 ? kSfbHi8Byte : kSfbHiByte) * 0x01010101u));
+    if (PAIR == 3)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+          "%1,%1,%1};" ::"r"(addr + kSfaTailCol),
+          "r"(p.sfa_tail_word));
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
@@ -647,8 +671,9 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
   // upper tiles run (and A_up while the next lower tiles run): single-buffered
   // wide rows (M = 3: 80 KB per buffer) still overlap their sample loads.
   const int nt_l = p.nt_lower, nt_u = p.nt_total - p.nt_lower;
-  const int rot_l = (int)(((int64_t)cluster * nt_l) / n_clusters);
-  const int rot_u = (int)(((int64_t)cluster * nt_u) / n_clusters);
+  // PAIR = 3: even rotations keep the (2p, 2p+1) pairs of the host's tail layout together
+  const int rot_l = (int)(((int64_t)cluster * nt_l) / n_clusters) & (PAIR == 3 ? ~1 : ~0);
+  const int rot_u = (int)(((int64_t)cluster * nt_u) / n_clusters) & (PAIR == 3 ? ~1 : ~0);
   auto tile_of = [&](int jj) -> int {
     if (jj < nt_l) {
       const int j = rot_l + jj;
@@ -1009,6 +1034,8 @@ struct Fp4Call {
   int sm_count;
   int64_t chunk_tiles;  // reference tiles per launch (0: the L2-sized default)
   int pair;             // paired accumulators (kSfbHiCol): 0 off, 1 2^16 halves, 2 packed 2^8
+  int tail;             // shared-tail layout (PAIR = 3; needs a paired plan at 4 K-steps)
+  uint32_t sfa_tail_word;
 };
 
 constexpr size_t kMinSmem = 120 * 1024;  // > half of the SM's 228 KB
@@ -1140,6 +1167,9 @@ int launch_fp4(const Fp4Call& c) {
     if (c.pair == 1) kern = classify_fp4_pair_kernel<TN, false, 1>;
     if (c.pair == 2) kern = classify_fp4_pair_kernel<TN, false, 2>;
   }
+  if constexpr (Tile<TN>::kBufs * TN <= (int)kSfaTailCol)
+    if (c.tail) kern = classify_fp4_pair_kernel<TN, false, 3>;
+  p.sfa_tail_word = c.sfa_tail_word;
   int clusters = c.sm_count / 2;
   if (p.n_groups < clusters) clusters = p.n_groups;
   p.flag_or = (!want_first && kEpiSets > 1 && (reinterpret_cast<uintptr_t>(c.flags) & 3) == 0 &&
@@ -1362,7 +1392,8 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
                       int64_t avail_lower, const uint8_t* B_upper, int64_t n_upper,
                       int64_t avail_upper, int row_bytes, uint8_t* flags, int64_t* first_lower,
                       int64_t* first_upper, int accumulate, void* stream,
-                      const int64_t* S_dev = nullptr, int64_t a_plane_stride = 0) {
+                      const int64_t* S_dev = nullptr, int64_t a_plane_stride = 0,
+                      int tail_tn = 0) {
   RSR_REQUIRE(S >= 0 && n_lower >= 0 && n_upper >= 0, "rsr_classify_fp4: negative size");
   RSR_REQUIRE(avail_lower >= n_lower && avail_upper >= n_upper,
               "rsr_classify_fp4: readable rows below the reference count");
@@ -1420,6 +1451,19 @@ int classify_fp4_impl(const uint8_t* A, int64_t S, const uint8_t* B_lower, int64
   }
   c.chunk_tiles = plan.chunk_tiles;
   c.pair = plan.pair;
+  c.tail = 0;
+  c.sfa_tail_word = 0;
+  if (tail_tn) {
+    // the host built the shared-tail layout for pairs of tail_tn-row tiles
+    if (plan.pair != 1 || plan.tn != tail_tn || plan.chunk_tiles != 0) {
+      rsr::set_error("rsr_classify_fp4_tail: the plan for this call is not a streamed paired "
+                     "plan of %d-row tiles (tile_n %d, paired %d)", tail_tn, plan.tn, plan.pair);
+      return RSR_EUNSUPPORTED;
+    }
+    c.tail = 1;
+    const char* w = getenv("RSR_FP4_TAIL_SFA");
+    c.sfa_tail_word = w ? (uint32_t)strtoul(w, nullptr, 0) : 0x00001000u;
+  }
   switch (plan.tn) {
     case 224: return launch_fp4<224>(c);
     case 208: return launch_fp4<208>(c);
@@ -1719,6 +1763,37 @@ extern "C" int rsr_classify_fp4_planar(const uint8_t* A, int64_t a_plane_stride,
   return classify_fp4_impl(A, S, B_lower, n_lower, avail_lower, B_upper, n_upper, avail_upper,
                            row_bytes, flags, first_lower, first_upper, accumulate, stream, S_dev,
                            a_plane_stride);
+}
+
+extern "C" int rsr_classify_fp4_tail(const uint8_t* A, int64_t a_plane_stride, int64_t S,
+                                     const uint8_t* B_upper, int64_t n_upper, int row_bytes,
+                                     int tile_n, uint8_t* flags, int accumulate, void* stream) {
+  RSR_REQUIRE(row_bytes == 4 * kChunk, "rsr_classify_fp4_tail: rows must be 4 K-steps (128 B)");
+  RSR_REQUIRE(tile_n == 224 || tile_n == 208 || tile_n == 192 || tile_n == 176,
+              "rsr_classify_fp4_tail: tile_n must be 176..224");
+  RSR_REQUIRE(n_upper % (2 * tile_n) == 0,
+              "rsr_classify_fp4_tail: n_upper must be whole tile pairs (pad with never-hit rows)");
+  RSR_REQUIRE(a_plane_stride > 0, "rsr_classify_fp4_tail: planar sample operand required");
+  return classify_fp4_impl(A, S, nullptr, 0, 0, B_upper, n_upper, n_upper, row_bytes, flags,
+                           nullptr, nullptr, accumulate, stream, nullptr, a_plane_stride, tile_n);
+}
+
+extern "C" int rsr_classify_fp4_plan_ex(int64_t S, int64_t n_lower, int64_t n_upper,
+                                        int row_bytes, int want_first, int* tile_n,
+                                        int64_t* launches, int* paired) {
+  int rc = rsr_classify_fp4_plan(S, n_lower, n_upper, row_bytes, want_first, tile_n, launches);
+  if (rc || !paired) return rc;
+  int sm_count = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      sm_count = v;
+  }
+  cudaGetLastError();
+  const TilePlan plan = pick_tile_n(S, sm_count, n_lower, n_upper, row_bytes / kChunk,
+                                    want_first != 0);
+  *paired = plan.pair == 1 && plan.chunk_tiles == 0 ? 1 : 0;
+  return RSR_OK;
 }
 
 extern "C" int rsr_classify_fp4_dev(const uint8_t* A, int64_t S_cap, const int64_t* S_dev,

@@ -181,3 +181,34 @@ def test_cost_model_picks_compaction_for_config4_only(paths):
     ncols = up_big.device_fp4_support(2).size + 1  # + bias column
     assert plan is not None and plan.row_bytes == (ncols + 63) // 64 * 32 < 160
     assert C.fp4_compaction(1 << 22, 295, 2, None, up_big, force=False) is None
+
+
+@pytest.mark.parametrize("k,p1", [(60_001, 0.85), (100_000, 0.9)])
+def test_shared_tail_layout_equals_plain_bits_and_oracle(k, p1, monkeypatch):
+    """Shared-tail pairs (csrc/classify_fp4.cu PAIR = 3): 193..224 compacted columns, the
+    last K-step of each tile pair shared by both tiles (per-K-block A scales), odd tile
+    counts padded with a never-hit tile.  Labels equal the plain compacted kernel, the
+    uncompacted one, the bit-packed kernel and the oracle."""
+    paths = W.random_st_paths(W.cfg3(0), k, seed=0)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, paths, trusted=True)
+    lo = P.ReferenceSet(P.Side.LOWER, 0)
+    H = 1 << 16
+    b = P.sample_batch(P.ComponentDistribution.iid(295, [1 - p1, p1]), H, seed=k)
+    monkeypatch.setenv("RSR_FP4_COMPACT", "force")
+    monkeypatch.setenv("RSR_FP4_TAIL", "1")
+    plan = C.fp4_compaction(H, 295, 2, lo, up)
+    assert plan is not None and plan.tail_tn > 0 and plan.n_pad % (2 * plan.tail_tn) == 0
+    tail = P.classify(b, lo, up, n_states=2)
+    monkeypatch.setenv("RSR_FP4_TAIL", "0")
+    plain = P.classify(b, lo, up, n_states=2)
+    monkeypatch.setenv("RSR_FP4_COMPACT", "0")
+    full = P.classify(b, lo, up, n_states=2)
+    bits = P.classify(b, lo, up, n_states=2, method="bits")
+    t = tail.labels_device.cpu().numpy()
+    assert np.array_equal(t, plain.labels_device.cpu().numpy())
+    assert np.array_equal(t, full.labels_device.cpu().numpy())
+    assert np.array_equal(t, bits.labels_device.cpu().numpy())
+    assert tail.counts == full.counts and min(tail.counts[1], tail.counts[2]) > 0
+    xs = b.device_states()[-2000:].cpu().numpy()
+    want = oracle.classify_labels(xs, np.zeros((0, 295), np.int64), paths, 2)
+    assert np.array_equal(t[-2000:], want["labels"])
