@@ -524,7 +524,7 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
             if cplan is not None else None)
     if cplan is not None:
         classify_launches = max(1, _abi.fp4_plan(
-            S, nl, cplan.n_pad if cplan.tail_tn else nu, cplan.row_bytes)[1])
+            S, nl, cplan.n_pad if cplan.tail_tn and cplan.tail_ok else nu, cplan.row_bytes)[1])
     gev = []  # (start, end) events around the re-pack of each timed step
 
     def classify_kernel(kev=None):
@@ -599,7 +599,7 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     if cplan is not None:
         k_cols = max(c.size - 1 for c in cplan.cols.values())  # bias column not counted
         # shared tail: 7 of the 8 K-steps of a tile pair are issued
-        mma_cols = cplan.row_bytes * 2 * (7 / 8 if cplan.tail_tn else 1)
+        mma_cols = cplan.row_bytes * 2 * (7 / 8 if cplan.tail_tn and cplan.tail_ok else 1)
     else:
         k_cols = N_COMP * (2 - 1)
         mma_cols = width * 2 if method == "tc" else width

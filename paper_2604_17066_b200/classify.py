@@ -281,6 +281,7 @@ class Fp4Compaction:
         self.tail_tn = 0  # > 0: shared-tail layout (rsr_classify_fp4_tail) of tile_n tiles
         self.n_pad = 0
         self.tail_cols = None  # (sample map, reference map)
+        self.tail_checked, self.tail_ok = -1, False  # batch size the plan was checked for
         self.dev = {}
         for side, c in cols.items():
             key = (_device.device().index, c.tobytes())
@@ -336,11 +337,10 @@ def _fp4_tail_layout(plan: Fp4Compaction, n_samples: int, n_refs: int, kdim: int
     """Shared-tail layout (csrc/classify_fp4.cu PAIR = 3) when the compacted upper rows have
     193..224 columns and the library pairs this set's accumulators: 192 main columns (the
     bias first) plus a tail of <= 32 that tile pairs share in one MMA (7 MMAs per pair
-    instead of 8).  Off by default (RSR_FP4_TAIL=1 turns it on): exact, but measured no
-    faster -- cfg4 K = 5x10^5 121.9 ms with it, 121.3 without (profiles/r2_pair_sweep.txt):
-    with 7 K-steps per buffer the paired accumulator round trip sets the pace again."""
+    instead of 8, and the odd tiles stream 3 of their 4 K-steps: cfg4 K = 5x10^5 121.3 ->
+    118.5 ms, profiles/r2_pair_sweep.txt).  RSR_FP4_TAIL=0 turns it off."""
     c = plan.cols[Side.UPPER]
-    if os.environ.get("RSR_FP4_TAIL", "0") != "1" or not (192 < c.size <= 224):
+    if os.environ.get("RSR_FP4_TAIL", "1") == "0" or not (192 < c.size <= 224):
         return
     tn, _, paired = _abi.fp4_plan_ex(n_samples, 0, n_refs, 128)
     if not paired:
@@ -354,6 +354,7 @@ def _fp4_tail_layout(plan: Fp4Compaction, n_samples: int, n_refs: int, kdim: int
     tail = np.full(32, -1, np.int32)
     tail[: sup.size - 191] = sup[191:]
     plan.tail_tn, plan.n_pad = tn, n_pad
+    plan.tail_checked, plan.tail_ok = n_samples, True
     plan.tail_cols = (np.concatenate([main, tail, tail]).astype(np.int32),
                       np.concatenate([main, tail, np.full(32, -1, np.int32)]).astype(np.int32))
     key = (_device.device().index, plan.tail_cols[0].tobytes())
@@ -376,7 +377,14 @@ def fp4_classify_compacted(plan: Fp4Compaction, a: torch.Tensor, plane: int, n_s
     H = n_samples
     if events:
         events[0].record()
-    if plan.tail_tn:
+    tail = plan.tail_tn > 0
+    if tail and H != plan.tail_checked:
+        # the library re-plans per call: the shared-tail layout needs the same paired plan
+        # for this batch size (host-fed chunks are smaller than the job)
+        tn, _, paired = _abi.fp4_plan_ex(H, 0, plan.n_pad, 128)
+        plan.tail_ok = paired and tn == plan.tail_tn
+        plan.tail_checked = H
+    if tail and plan.tail_ok:
         if out is None or out.numel() < H * 128:
             out = torch.empty((1, max(H, 1), 128), dtype=torch.uint8, device=a.device)
         stride = row_bytes if plane else 2 * row_bytes

@@ -69,6 +69,14 @@ constexpr uint32_t kSfbHi8Byte = 0x71;
 // tile b 3: 7 instead of 8 per pair.  Needs kBufs * TN <= kSfaTailCol and pair-aligned
 // tile sequences (even rotation, even tile counts: the host pads with never-hit tiles).
 constexpr uint32_t kSfaTailCol = 448;
+// Paired buffers are read by BOTH epilogue sets, each set its half of the columns (8 warps
+// per buffer: TMEM loads at 324 instead of 175 B/clk per SM, tools/tmem_bw.cu), so the
+// accumulator round trip shortens by about one half-buffer load; every set ORs its own hit
+// bits into the flags.  Measured slightly slower (cfg4 K = 5x10^5: 122.3 vs 121.6 ms; the
+// pairs are not round-trip bound), so off: -DRSR_FP4_PAIR_SPLIT=1 builds it.
+#ifndef RSR_FP4_PAIR_SPLIT
+#define RSR_FP4_PAIR_SPLIT 0
+#endif
 
 // Reference tiles are 240 rows (120 per CTA).  TMEM holds two accumulator
 // buffers of 240 columns (0..479; 480..511 hold the scale factors), so the
@@ -348,6 +356,31 @@ __device__ __forceinline__ void ld_cols_full(uint32_t taddr, uint32_t* v) {
 // released after the second; 16x2 SIMD mins reduce both tiles' counts at once (low
 // halves: tile a, high halves: tile b).  Columns past a tile's last reference
 // (valid_*) are masked; a missing second tile has valid_b = 0.
+template <int HN>
+__device__ __forceinline__ void epilogue_pair_half(uint32_t taddr, uint32_t release_bar,
+                                                   int lane, int c0, int64_t valid_a,
+                                                   int64_t valid_b, bool& any_a, bool& any_b) {
+  uint32_t v[HN];
+  ld_cols_full<HN>(taddr, v);
+  tmem_ld_wait();
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive_leader(release_bar);
+  if (valid_a < c0 + HN || valid_b < c0 + HN) {
+#pragma unroll
+    for (int c = 0; c < HN; ++c) {
+      if (c0 + c >= valid_a) v[c] |= 0x0000FFFFu;
+      if (c0 + c >= valid_b) v[c] |= 0xFFFF0000u;
+    }
+  }
+  uint32_t m[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+#pragma unroll
+  for (int c = 0; c < HN; ++c) m[c & 3] = __vminu2(m[c & 3], v[c]);
+  const uint32_t r = __vminu2(__vminu2(m[0], m[1]), __vminu2(m[2], m[3]));
+  any_a = (r & 0xFFFFu) == 0;
+  any_b = (r >> 16) == 0;
+}
+
 template <int TN>
 __device__ __forceinline__ void epilogue_pair(uint32_t taddr, uint32_t release_bar, int lane,
                                               int64_t valid_a, int64_t valid_b, bool& any_a,
@@ -624,7 +657,12 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     for (int i = 0; i < kBufs; ++i) {
       mbar_init(smem_addr(&t_full[i]), 1);
       // the 4 warps of the tile's epilogue set in both CTAs (or one arrival per CTA)
-      mbar_init(smem_addr(&t_empty[i]), RSR_FP4_SET_RELEASE ? 2 : RSR_FP4_SPLIT_COLS ? 2 * kEpiWarps : 2 * 4);
+      mbar_init(smem_addr(&t_empty[i]),
+                RSR_FP4_SET_RELEASE                                      ? 2
+                : (RSR_FP4_SPLIT_COLS ||
+                   (PAIR != 0 && PAIR != 2 && RSR_FP4_PAIR_SPLIT && kEpiSets == 2))
+                    ? 2 * kEpiWarps
+                                                                         : 2 * 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -740,7 +778,11 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         const int j = tile_of(jj);
         if (j < p.n_res) continue;  // resident
         const bool low = j < p.nt_lower;
-        const CUtensorMap* map = low ? &map_lower : &map_upper;
+        // PAIR = 3 (upper side only): the odd tile of a pair needs its 3 main K-steps only;
+        // map_lower then holds the 3-chunk map of the upper rows
+        const bool short_b = PAIR == 3 && !low && ((j - p.nt_lower) & 1);
+        const CUtensorMap* map = (low || short_b) ? &map_lower : &map_upper;
+        const uint32_t tx = short_b ? 2u * 3u * (uint32_t)kChunkB : 2 * b_stage_bytes;
         const int y = (low ? j : j - p.nt_lower) * kTileN + (int)rank * kHalfRows;
         PROF_T(q0);
         mbar_wait(bar_b_empty + 8 * stage, phase ^ 1);
@@ -748,7 +790,7 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         PROF_ADD(6, q1 - q0);
         if (elect_one()) {
           if (leader)
-            mbar_expect_tx(bar_b_full + 8 * stage, 2 * b_stage_bytes);
+            mbar_expect_tx(bar_b_full + 8 * stage, tx);
           else
             mbar_arrive_leader(bar_b_full + 8 * stage);
           tma_load_3d_pair(sB0 + (uint32_t)stage * b_stage_bytes, map, bar_b_full + 8 * stage, 0,
@@ -815,7 +857,8 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
           const int base = h == 0 ? 0 : nt_l;
           const int64_t n_side = h == 0 ? p.n_lower : p.n_upper;
           for (int s2 = 0; s2 < cnt; s2 += 2, ++T) {
-            if ((int)(T % kEpiSets) != set) continue;
+            constexpr bool kSplit = RSR_FP4_PAIR_SPLIT && PAIR != 2 && kEpiSets == 2;
+            if (!kSplit && (int)(T % kEpiSets) != set) continue;
             const uint32_t buf = T % kBufs, tphase = (T / kBufs) & 1;
             const int ja = tile_of(base + s2) - base;
             const int jb = s2 + 1 < cnt ? tile_of(base + s2 + 1) - base : -1;
@@ -825,7 +868,10 @@ classify_fp4_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * kTileN;
             bool any_a, any_b;
-            if constexpr (PAIR == 2)
+            if constexpr (kSplit)
+              epilogue_pair_half<kTileN / 2>(taddr + set * (kTileN / 2), smem_addr(&t_empty[buf]),
+                                             lane, set * (kTileN / 2), va, vb, any_a, any_b);
+            else if constexpr (PAIR == 2)
               epilogue_pair8<kTileN>(taddr, smem_addr(&t_empty[buf]), lane, va, vb, any_a, any_b);
             else
               epilogue_pair<kTileN>(taddr, smem_addr(&t_empty[buf]), lane, va, vb, any_a, any_b);
@@ -1221,8 +1267,11 @@ int launch_fp4(const Fp4Call& c) {
     q.n_upper = rows[1];
 
     CUtensorMap cl, cu;
-    rc = make_map3(&cl, base[0] ? base[0] : base[1], base[0] ? rows[0] : rows[1], c.row_bytes, cq,
-                   TN / 2);
+    if (c.tail)  // shared-tail pairs: the odd tiles' 3-chunk map in the (unused) lower slot
+      rc = make_map3(&cl, base[1], rows[1], c.row_bytes, 3, TN / 2);
+    else
+      rc = make_map3(&cl, base[0] ? base[0] : base[1], base[0] ? rows[0] : rows[1], c.row_bytes,
+                     cq, TN / 2);
     if (rc) return rc;
     rc = make_map3(&cu, base[1] ? base[1] : base[0], base[1] ? rows[1] : rows[0], c.row_bytes, cq,
                    TN / 2);

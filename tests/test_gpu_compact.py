@@ -212,3 +212,22 @@ def test_shared_tail_layout_equals_plain_bits_and_oracle(k, p1, monkeypatch):
     xs = b.device_states()[-2000:].cpu().numpy()
     want = oracle.classify_labels(xs, np.zeros((0, 295), np.int64), paths, 2)
     assert np.array_equal(t[-2000:], want["labels"])
+
+
+def test_shared_tail_host_fed_chunks(monkeypatch):
+    """classify_host with a shared-tail plan: the host-fed chunks are smaller than the job,
+    so each chunk re-checks the library's plan and falls back to the plain compacted layout
+    where it differs.  Labels equal the uncompacted classification."""
+    from paper_2604_17066_b200.classify import classify_host
+    paths = W.random_st_paths(W.cfg3(0), 60_001, seed=0)
+    up = P.ReferenceSet.from_array(P.Side.UPPER, 0, paths, trusted=True)
+    lo = P.ReferenceSet(P.Side.LOWER, 0)
+    H = 300_001
+    b = P.sample_batch(P.ComponentDistribution.iid(295, [0.12, 0.88]), H, seed=11)
+    host = b.device_states().cpu().pin_memory()
+    monkeypatch.setenv("RSR_FP4_COMPACT", "force")
+    labels, counts = classify_host(host, lo, up, 2)
+    monkeypatch.setenv("RSR_FP4_COMPACT", "0")
+    want = P.classify(b, lo, up, n_states=2)
+    assert np.array_equal(labels.numpy()[:H], want.labels_device.cpu().numpy())
+    assert counts == want.counts
