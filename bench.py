@@ -616,7 +616,8 @@ def measure_classify(comm, config, k, samples, method, steps, warmup, *, weak=Fa
     peak = 9000.0 if method == "tc" else int8_peak
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
                 "frac": achieved / peak, "traffic": ncu_traffic(kname, config, K,
-                                       f"_rb{cplan.row_bytes}" if cplan is not None else ""), "kernel": kname,
+                                       "" if cplan is None else f"_rb{cplan.row_bytes}" +
+                                       ("_tail" if cplan.tail_tn and cplan.tail_ok else "")), "kernel": kname,
                 "kernel_ms": kern_avg, "kernel_launches_per_step": classify_launches,
                 "ops_per_pair": ops_per_pair, "pairs_per_rank_step": S * K,
                 "peak_source": ("B200 dense FP4 spec = measured tcgen05 kind::mxf4 rate "
