@@ -1348,10 +1348,12 @@ TilePlan pick_tile_n(int64_t S, int sm_count, int64_t n_lower, int64_t n_upper, 
   static const int kCost[] = {1000, 957, 971, 920, 843, 778};  // relative time per tile
   // resident tiles (cfg4 K = 10^3 per-tile times, profiles/r1_tile_n_small_k.txt)
   static const int kCostResident[] = {1000, 956, 935, 869, 862, 779};
-  // paired accumulators: the round trip no longer sets a tile's time, which follows TN
-  // (cfg4 K = 10^5 / 5x10^5 at 4 K-steps: a 208 tile takes 0.924 of a 224 tile;
-  // tools/compact_tile_sweep.sh)
-  static const int kCostPair[] = {0, 1000, 924, 870, 810, 0};
+  // paired accumulators: the round trip no longer sets a tile's time.  Plain pairs: a 208
+  // tile takes 0.924 of a 224 tile (cfg4 K = 5x10^5: 121.2 vs 121.9 ms); shared-tail pairs
+  // (the host's default layout for 193..224 compacted columns): 224 tiles 111.9 ms, 208
+  // 118.4, 192 128.0, 176 137.1 (tools/compact_tile_sweep.sh) -- so 224 unless narrower
+  // tiles save padding
+  static const int kCostPair[] = {0, 1000, 965, 920, 880, 0};
   (void)kCostPair;
   // Streaming the tiles through the ring costs per sample group, over keeping them
   // resident, about 2.5 tiles for short sets (cfg4 K = 2000: 9 resident tiles of 224 take
