@@ -90,6 +90,36 @@ def _fp4_pair_selfcheck(rng) -> None:
         warnings.warn("FP4 paired-accumulator self-check failed: pairing disabled",
                       RuntimeWarning)
         os.environ["RSR_FP4_PAIR"] = "0"
+        return
+    # shared tail (rsr_classify_fp4_tail): references using 210 of the 250 components, so
+    # the compacted rows have 211 columns = 192 main + a 19-column tail shared per tile pair
+    # (per-K-block A scales); on mismatch the shared tail is switched off
+    n2 = 295  # 160-byte rows, so the compaction to 128 bytes applies
+    tup = np.zeros((k, n2), dtype=np.uint8)
+    tup[:, :n] = up
+    tup[:, 210:] = 0
+    tup[:8, :210] = 1  # every support column used
+    x2 = np.ones((h, n2), dtype=np.uint8)
+    x2[:, :n] = x
+    batch = SampleBatch(_device.to_device(x2), 0, 0, state_bound=2)
+    tset = ReferenceSet.from_array(Side.UPPER, 0, tup, trusted=True)
+    saved = {k: os.environ.get(k) for k in ("RSR_FP4_PAIR", "RSR_FP4_COMPACT", "RSR_FP4_TAIL")}
+    os.environ.update(RSR_FP4_PAIR="force", RSR_FP4_COMPACT="force", RSR_FP4_TAIL="1")
+    try:
+        plan = fp4_compaction(h, n2, 2, None, tset)
+        used = plan is not None and plan.tail_tn > 0
+        ft, _, _ = classify_flags(batch, None, tset, 2, "fp4")
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    fbt, _, _ = classify_flags(batch, None, tset, 2, "bits")
+    if not used or not np.array_equal(ft.cpu().numpy(), fbt.cpu().numpy()):
+        import warnings
+        warnings.warn("FP4 shared-tail self-check failed: shared tail disabled", RuntimeWarning)
+        os.environ["RSR_FP4_TAIL"] = "0"
 
 
 def fp4_exact() -> bool:

@@ -134,5 +134,7 @@ def test_paired_selfcheck_passes(monkeypatch):
     import os
     C = importlib.import_module("paper_2604_17066_b200.classify")
     monkeypatch.delenv("RSR_FP4_PAIR", raising=False)
+    monkeypatch.delenv("RSR_FP4_TAIL", raising=False)
     C._fp4_pair_selfcheck(np.random.default_rng(20260419))
-    assert os.environ.get("RSR_FP4_PAIR") is None
+    assert os.environ.get("RSR_FP4_PAIR") is None  # pairing stays on
+    assert os.environ.get("RSR_FP4_TAIL") is None  # and the shared tail
